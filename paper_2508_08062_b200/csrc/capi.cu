@@ -1,0 +1,242 @@
+// capi.cu — extern "C" entry points of include/aapdhg_cuda.h.
+// Exceptions never cross the boundary: they map onto aapdhg_status codes
+// (InputError / DimensionError / UnsupportedError / SingularError /
+// CUDA runtime errors) with the message copied into the caller's buffer.
+#include <cstring>
+#include <new>
+
+#include "aapdhg_cuda.h"
+#include "engine.h"
+
+using aapdhg_b200::CudaError;
+using aapdhg_b200::Problem;
+using aapdhg_b200::StatusError;
+
+struct aapdhg_handle {
+  Problem* prob;
+};
+
+namespace {
+
+void put_err(char* err, size_t errlen, const char* msg) {
+  if (!err || errlen == 0) return;
+  std::strncpy(err, msg, errlen - 1);
+  err[errlen - 1] = '\0';
+}
+
+template <class F>
+int guard(char* err, size_t errlen, F&& f) {
+  try {
+    return f();
+  } catch (const StatusError& e) {
+    put_err(err, errlen, e.what());
+    return e.code;
+  } catch (const CudaError& e) {
+    put_err(err, errlen, e.what());
+    return AAPDHG_ERR_CUDA;
+  } catch (const std::bad_alloc&) {
+    put_err(err, errlen, "host allocation failed");
+    return AAPDHG_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return AAPDHG_ERR_INTERNAL;
+  }
+}
+
+int need(const void* p, const char* what, char* err, size_t errlen) {
+  if (p) return AAPDHG_OK;
+  put_err(err, errlen, what);
+  return AAPDHG_ERR_INPUT;
+}
+
+}  // namespace
+
+extern "C" {
+
+int aapdhg_cuda_abi_version(void) { return AAPDHG_ABI_VERSION; }
+
+int aapdhg_cuda_device_info(char* out, size_t outlen) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return AAPDHG_ERR_CUDA;
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return AAPDHG_ERR_CUDA;
+  char buf[256];
+  std::snprintf(buf, sizeof buf, "%s, sm_%d%d, %d SMs", p.name, p.major, p.minor,
+                p.multiProcessorCount);
+  put_err(out, outlen, buf);
+  return AAPDHG_OK;
+}
+
+int aapdhg_cuda_problem_create(const aapdhg_problem_view* prob, int device,
+                               aapdhg_handle** out, char* err, size_t errlen) {
+  if (int rc = need(out, "problem_create: null out", err, errlen)) return rc;
+  *out = nullptr;
+  return guard(err, errlen, [&] {
+    auto* h = new aapdhg_handle{new Problem(prob, device)};
+    *out = h;
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_problem_destroy(aapdhg_handle* h) {
+  if (!h) return AAPDHG_OK;
+  delete h->prob;
+  delete h;
+  return AAPDHG_OK;
+}
+
+int aapdhg_cuda_problem_dims(const aapdhg_handle* h, int32_t* n, int32_t* m1, int32_t* m2,
+                             int64_t* nnz) {
+  if (!h) return AAPDHG_ERR_INPUT;
+  if (n) *n = h->prob->n();
+  if (m1) *m1 = h->prob->m1();
+  if (m2) *m2 = h->prob->m() - h->prob->m1();
+  if (nnz) *nnz = h->prob->nnz();
+  return AAPDHG_OK;
+}
+
+int aapdhg_cuda_solve(aapdhg_handle* h, const aapdhg_solve_params* prm, const double* x0,
+                      const double* y0, aapdhg_solve_result* res, double* x_out,
+                      double* y_out, double* lambda_out, aapdhg_record_sink sink, void* ctx,
+                      char* err, size_t errlen) {
+  if (int rc = need(h, "solve: null handle", err, errlen)) return rc;
+  if (int rc = need(prm, "solve: null params", err, errlen)) return rc;
+  if (int rc = need(res, "solve: null result", err, errlen)) return rc;
+  return guard(err, errlen, [&] {
+    h->prob->solve(prm, x0, y0, res, x_out, y_out, lambda_out, sink, ctx);
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_select_step_sizes(aapdhg_handle* h, const aapdhg_solve_params* prm,
+                                  double* tau, double* sigma, char* err, size_t errlen) {
+  if (int rc = need(h && prm && tau && sigma ? h : nullptr, "select_step_sizes: null argument",
+                    err, errlen))
+    return rc;
+  return guard(err, errlen, [&] {
+    h->prob->select_step_sizes(prm, tau, sigma);
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_power_norm(aapdhg_handle* h, int32_t max_iters, double rel_tol, uint64_t seed,
+                           int32_t reduction, double* out, int32_t* rounds, char* err,
+                           size_t errlen) {
+  if (int rc = need(h && out ? h : nullptr, "power_norm: null argument", err, errlen)) return rc;
+  return guard(err, errlen, [&] {
+    int r = 0;
+    const bool serial = reduction == AAPDHG_REDUCE_SERIAL ||
+                        (reduction == AAPDHG_REDUCE_AUTO &&
+                         int64_t(h->prob->n()) + h->prob->m() <= 65536);
+    *out = h->prob->power_norm(max_iters, rel_tol, seed, serial, &r);
+    if (rounds) *rounds = r;
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_matvec(aapdhg_handle* h, const double* x, double* out, char* err,
+                       size_t errlen) {
+  if (int rc = need(h && out && (x || h->prob->n() == 0) ? h : nullptr, "matvec: null argument",
+                    err, errlen))
+    return rc;
+  return guard(err, errlen, [&] {
+    h->prob->matvec(x, out);
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_matvec_transpose(aapdhg_handle* h, const double* y, double* out, char* err,
+                                 size_t errlen) {
+  if (int rc = need(h && out ? h : nullptr, "matvec_transpose: null argument", err, errlen))
+    return rc;
+  return guard(err, errlen, [&] {
+    h->prob->matvec_transpose(y, out);
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_pdhg_step(aapdhg_handle* h, double tau, double sigma, const double* x,
+                          const double* y, double* xn, double* yn, char* err, size_t errlen) {
+  if (int rc = need(h && xn && yn ? h : nullptr, "pdhg_step: null argument", err, errlen))
+    return rc;
+  return guard(err, errlen, [&] {
+    h->prob->pdhg_step(tau, sigma, x, y, xn, yn);
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_kkt_metrics(aapdhg_handle* h, int32_t reduction, const double* x,
+                            const double* y, double* kkt, double* lambda, char* err,
+                            size_t errlen) {
+  if (int rc = need(h && kkt ? h : nullptr, "kkt_metrics: null argument", err, errlen)) return rc;
+  return guard(err, errlen, [&] {
+    h->prob->kkt_metrics(reduction, x, y, kkt, lambda);
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_aa_apply(aapdhg_handle* h, int32_t reduction, int32_t p, const double* du_cols,
+                         const double* dg_cols, double beta, const double* d_hat, double eta,
+                         const double* u, const double* g, double* out, char* err,
+                         size_t errlen) {
+  if (int rc = need(h && u && g && out ? h : nullptr, "aa_apply: null argument", err, errlen))
+    return rc;
+  return guard(err, errlen, [&] {
+    const int rc = h->prob->aa_apply(reduction, false, p, du_cols, dg_cols, beta, d_hat, eta,
+                                     0.2, 1e9, u, g, out, nullptr);
+    if (rc == AAPDHG_ERR_SINGULAR) put_err(err, errlen, "aa: normal equations not positive definite");
+    return rc;
+  });
+}
+
+int aapdhg_cuda_filtered_aa_apply(aapdhg_handle* h, int32_t reduction, int32_t p,
+                                  const double* e_cols, const double* f_cols, double c_s,
+                                  double kappa_bar, double beta, const double* d_hat,
+                                  const double* u, const double* g, double* out,
+                                  int32_t* kept, char* err, size_t errlen) {
+  if (int rc = need(h && u && g && out ? h : nullptr, "filtered_aa_apply: null argument", err,
+                    errlen))
+    return rc;
+  return guard(err, errlen, [&] {
+    const int rc = h->prob->aa_apply(reduction, true, p, e_cols, f_cols, beta, d_hat, 0.0, c_s,
+                                     kappa_bar, u, g, out, kept);
+    if (rc == AAPDHG_ERR_SINGULAR) put_err(err, errlen, "filtered memory: singular");
+    return rc;
+  });
+}
+
+int aapdhg_cuda_set_profiling(aapdhg_handle* h, int32_t enable) {
+  if (!h) return AAPDHG_ERR_INPUT;
+  h->prob->set_profiling(enable != 0);
+  return AAPDHG_OK;
+}
+
+int aapdhg_cuda_kernel_times(aapdhg_handle* h, char* names, size_t names_len, double* ms,
+                             uint64_t* launches, int32_t cap, int32_t* count) {
+  if (!h) return AAPDHG_ERR_INPUT;
+  const auto& st = h->prob->kernel_stats();
+  std::string all;
+  int k = 0;
+  for (const auto& kv : st) {
+    if (k < cap) {
+      if (ms) ms[k] = kv.second.ms;
+      if (launches) launches[k] = kv.second.launches;
+      all += kv.first;
+      all += '\n';
+    }
+    ++k;
+  }
+  if (names && names_len) put_err(names, names_len, all.c_str());
+  if (count) *count = k;
+  return AAPDHG_OK;
+}
+
+int aapdhg_cuda_last_launch_count(aapdhg_handle* h, uint64_t* launches,
+                                  uint64_t* loop_iterations) {
+  if (!h) return AAPDHG_ERR_INPUT;
+  if (launches) *launches = h->prob->last_launches();
+  if (loop_iterations) *loop_iterations = h->prob->last_loop_iters();
+  return AAPDHG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+// common.cuh — shared device/host definitions of the sm_100a AA-PDHG path.
+//
+// Layout of the iteration state in HBM:
+//   upool[4][N]   stacked iterates u = (x[n]; y[m]); roles CUR/PREV/HAT/CAND
+//                 are indices held in DevState and rotated on the device.
+//   kxpool[3][m]  cached K*x for CUR / HAT (= K*xhat) / CAND.
+//   gpool[2][N]   fixed-point residual g = T(u) - u for CUR / PREV.
+//   du[cap][N], dg[cap][N]   difference memory ring (slot-major columns).
+//   T[n]          K'y of the current iterate (serial reduction mode only).
+// All arithmetic is IEEE fp64 compiled with -fmad=false: every product and
+// sum is rounded exactly where the reference rounds it.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "aapdhg_cuda.h"
+
+namespace aapdhg_b200 {
+
+constexpr int kThreads = 256;        // CTA size of the tile kernels
+constexpr int kTile = 2048;          // nnz staged per CTA (8 per thread)
+constexpr int kMaxRowsPerBlock = kThreads;
+constexpr int kMaxMemory = 64;       // largest AA memory capacity supported
+constexpr int kDotChunk = 512;       // elements per CTA in the tree multi-dot
+constexpr int kCtrlThreads = 256;
+
+// iterate roles
+enum { U_CUR = 0, U_PREV = 1, U_HAT = 2, U_CAND = 3 };
+enum { KX_CUR = 0, KX_HAT = 1, KX_CAND = 2 };
+enum { G_CUR = 0, G_PREV = 1 };
+
+// partial-sum quantities
+enum { P1_GX2 = 0, P1_BOUND = 1, P1_DUALSQ = 2, P1_CX = 3, P1_COUNT = 4 };
+enum { P2_GY2 = 0, P2_QY = 1, P2_INFEAS = 2, P2_COUNT = 3 };
+// serial chain results (index into DevState::sres)
+enum { S_G2 = 0, S_BOUND = 1, S_QY = 2, S_CX = 3, S_INFEAS = 4, S_DUALSQ = 5, S_COUNT = 6 };
+
+struct CsrDev {
+  int32_t nrows = 0, ncols = 0;
+  int64_t nnz = 0;
+  const int32_t* rp = nullptr;
+  const int32_t* ci = nullptr;
+  const double* v = nullptr;
+  int32_t nblocks = 0;
+  const int32_t* blk = nullptr;  // nblocks + 1 row boundaries
+};
+
+// Constant per solve (written before the loop starts).
+struct DevParams {
+  int32_t method, serial, m1, kkt_terminate;
+  int32_t n, mrows, cap;
+  int64_t N;
+  double safeguard_d, safeguard_eps, beta, eta, c_s, kappa_bar, toll, kkt_eps;
+  double tau, sigma;
+  uint64_t max_iters;
+  double max_wall_s;
+  double wall_offset_s;   // host time already spent before the loop started
+  double nrm_q, nrm_c;
+  const double* d_hat;    // nullptr = identity
+  const double* pow_tab;  // (i+1)^-(1+eps), host std::pow
+  uint64_t pow_len;
+  aapdhg_record* rec;     // ring of rec_cap records
+  uint64_t rec_cap;
+  int32_t nblk1, nblk2, ndot_blk, pad;
+};
+
+// Mutable solver state, device resident; the host reads it at polls.
+struct DevState {
+  int32_t done, status, final_role, aa_attempt;
+  int32_t aa_ok, mem_size, push_slot, mix_p;
+  uint64_t k, i, j, aa_failures;
+  uint64_t rec_complete;
+  double g0n, gkn, g_final;
+  double kkt[4];  // r_gap, r_primal, r_dual, objective of CUR
+  int32_t u_idx[4];
+  int32_t kx_idx[3];
+  int32_t g_idx[2];
+  int32_t mem_slots[kMaxMemory];   // memory order, oldest first
+  int32_t mix_slots[kMaxMemory];   // columns entering the mix (kept set)
+  double w[kMaxMemory];
+  double sres[8];                  // serial chain results
+  uint64_t t0_ns;
+  uint64_t loop_iters;             // iterations that did work (launch accounting)
+};
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StatusError : std::runtime_error {
+  int code;
+  StatusError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define AAPDHG_CUDA(call)                                                        \
+  do {                                                                           \
+    cudaError_t e_ = (call);                                                     \
+    if (e_ != cudaSuccess)                                                       \
+      throw ::aapdhg_b200::CudaError(std::string(#call) + ": " +                 \
+                                     cudaGetErrorString(e_));                   \
+  } while (0)
+
+// libstdc++ std::max / std::min semantics (signed zeros, NaN order).
+__host__ __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+__host__ __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+
+// build_lambda_set + project_lambda (lp_model.cpp:293-306, pdhg_core.cpp:27-39)
+__device__ __forceinline__ double project_lambda1(double v, double l, double u) {
+  const bool lo = isfinite(l), hi = isfinite(u);
+  if (!lo && !hi) return 0.0;
+  if (!lo) return smin(v, 0.0);
+  if (!hi) return smax(v, 0.0);
+  return v;
+}
+
+// damp, anderson.cpp:10-20
+__device__ __forceinline__ double damp1(double beta, const double* d_hat, int64_t i, double v) {
+  return d_hat ? beta * d_hat[i] * v : beta * v;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace aapdhg_b200

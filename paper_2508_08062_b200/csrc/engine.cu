@@ -1,0 +1,872 @@
+// engine.cu — host orchestration of the sm_100a AA-PDHG / FAA-PDHG solver.
+//
+// The reference solve() (proj/src/solver.cpp:125-253) runs entirely on the
+// device: one iteration = the kernel sequence in launch_iteration(), whose
+// branches (termination, safeguard, AA success / SingularError fallback)
+// are predicates in device memory, so iterations are replayed from a CUDA
+// graph without any host round trip. The host only polls the small
+// DevState mirror (pinned) between graph batches to stream trajectory
+// records out and to stop.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <random>
+
+#include "engine.h"
+#include "kernels.cuh"
+
+namespace aapdhg_b200 {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double secs(Clock::time_point t0) {
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+constexpr int kGraphIters = 8;        // iterations per captured graph
+constexpr int kMaxBatchGraphs = 64;   // graph launches between polls (max)
+constexpr uint64_t kRecCap = 1 << 16;  // device record ring
+constexpr uint64_t kPowTabMax = 1 << 22;
+constexpr int kPowerBatch = 8;
+
+// Row blocks: consecutive rows with <= kTile nonzeros and <= kMaxRowsPerBlock
+// rows; a row longer than kTile forms a block of its own.
+std::vector<int32_t> build_blocks(const int32_t* rp, int nrows) {
+  std::vector<int32_t> blk{0};
+  int r = 0;
+  while (r < nrows) {
+    const int start = r;
+    if (rp[r + 1] - rp[r] > kTile) {
+      ++r;
+    } else {
+      int64_t nz = 0;
+      while (r < nrows && r - start < kMaxRowsPerBlock && nz + (rp[r + 1] - rp[r]) <= kTile) {
+        nz += rp[r + 1] - rp[r];
+        ++r;
+      }
+    }
+    blk.push_back(r);
+  }
+  return blk;
+}
+
+int num_items_host(int p, int method) {
+  return p * (p + 1) / 2 + p + (method == AAPDHG_METHOD_FAA ? p : 0);
+}
+
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes) AAPDHG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+}
+void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes) AAPDHG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+}
+
+int grid_for(int64_t n, int per_block = kThreads, int cap = 148 * 8) {
+  int64_t g = (n + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+}  // namespace
+
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+
+void DevBuf::reserve(size_t b) {
+  if (b == 0) b = 16;
+  if (p && b <= bytes) return;
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+  AAPDHG_CUDA(cudaMalloc(&p, b));
+  bytes = b;
+}
+
+struct SolveSetup {
+  IterBufs B;
+  DotBufs D;
+  SolveScratch W;
+  const DevParams* P;
+  DevState* S;
+  bool serial, push;
+  int method, cap, nblk1, nblk2, ndot_blk, items_max;
+};
+
+// ---------------------------------------------------------------------------
+Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
+  if (!v) throw StatusError(AAPDHG_ERR_INPUT, "problem_create: null problem");
+  const aapdhg_csr_view& k = v->k;
+  if (k.nrows < 0 || k.ncols < 0 || k.nnz < 0)
+    throw StatusError(AAPDHG_ERR_DIMENSION, "problem_create: negative dimension");
+  if (v->m1 < 0 || v->m1 > k.nrows)
+    throw StatusError(AAPDHG_ERR_DIMENSION, "problem_create: bad m1");
+  if (!k.row_ptr || (k.nnz > 0 && (!k.col_idx || !k.vals)))
+    throw StatusError(AAPDHG_ERR_INPUT, "problem_create: null CSR array");
+  if (k.row_ptr[0] != 0 || int64_t(k.row_ptr[k.nrows]) != k.nnz)
+    throw StatusError(AAPDHG_ERR_DIMENSION, "problem_create: row_ptr does not span nnz");
+  if (k.ncols > 0 && (!v->c || !v->l || !v->u))
+    throw StatusError(AAPDHG_ERR_INPUT, "problem_create: null c/l/u");
+  if (k.nrows > 0 && !v->q) throw StatusError(AAPDHG_ERR_INPUT, "problem_create: null q");
+  for (int r = 0; r < k.nrows; ++r)
+    if (k.row_ptr[r + 1] < k.row_ptr[r])
+      throw StatusError(AAPDHG_ERR_DIMENSION, "problem_create: row_ptr not monotone");
+  for (int64_t e = 0; e < k.nnz; ++e)
+    if (k.col_idx[e] < 0 || k.col_idx[e] >= k.ncols)
+      throw StatusError(AAPDHG_ERR_DIMENSION, "problem_create: column index out of range");
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw CudaError("no CUDA device available (the sm_100a path has no CPU fallback)");
+  if (device < 0 || device >= ndev) throw CudaError("device ordinal out of range");
+  AAPDHG_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  AAPDHG_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    throw CudaError(std::string("device ") + prop.name + " is not sm_100 class");
+  AAPDHG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+
+  n_ = k.ncols;
+  m_ = k.nrows;
+  m1_ = v->m1;
+  nnz_ = k.nnz;
+  N_ = int64_t(n_) + m_;
+  for (int64_t e = 0; e < nnz_ && all_zero_; ++e) all_zero_ = k.vals[e] == 0.0;
+
+  // K and its row blocks
+  const std::vector<int32_t> kb = build_blocks(k.row_ptr, m_);
+  k_rp_.reserve(sizeof(int32_t) * (m_ + 1));
+  k_ci_.reserve(sizeof(int32_t) * nnz_);
+  k_v_.reserve(sizeof(double) * nnz_);
+  k_blk_.reserve(sizeof(int32_t) * kb.size());
+  h2d(k_rp_.p, k.row_ptr, sizeof(int32_t) * (m_ + 1), stream_);
+  h2d(k_ci_.p, k.col_idx, sizeof(int32_t) * nnz_, stream_);
+  h2d(k_v_.p, k.vals, sizeof(double) * nnz_, stream_);
+  h2d(k_blk_.p, kb.data(), sizeof(int32_t) * kb.size(), stream_);
+  K_ = CsrDev{m_, n_, nnz_, k_rp_.as<int32_t>(), k_ci_.as<int32_t>(), k_v_.as<double>(),
+              int32_t(kb.size() - 1), k_blk_.as<int32_t>()};
+
+  // K' as CSR, entries of each row in ascending original row (counting sort)
+  std::vector<int32_t> trp(static_cast<size_t>(n_) + 1, 0), tci(static_cast<size_t>(nnz_));
+  std::vector<double> tv(static_cast<size_t>(nnz_));
+  for (int64_t e = 0; e < nnz_; ++e) trp[size_t(k.col_idx[e]) + 1]++;
+  for (int j = 0; j < n_; ++j) trp[j + 1] += trp[j];
+  {
+    std::vector<int32_t> next(trp.begin(), trp.end() - 1);
+    for (int r = 0; r < m_; ++r)
+      for (int32_t e = k.row_ptr[r]; e < k.row_ptr[r + 1]; ++e) {
+        const int32_t pos = next[size_t(k.col_idx[e])]++;
+        tci[size_t(pos)] = r;
+        tv[size_t(pos)] = k.vals[e];
+      }
+  }
+  const std::vector<int32_t> tb = build_blocks(trp.data(), n_);
+  t_rp_.reserve(sizeof(int32_t) * (n_ + 1));
+  t_ci_.reserve(sizeof(int32_t) * nnz_);
+  t_v_.reserve(sizeof(double) * nnz_);
+  t_blk_.reserve(sizeof(int32_t) * tb.size());
+  h2d(t_rp_.p, trp.data(), sizeof(int32_t) * (n_ + 1), stream_);
+  h2d(t_ci_.p, tci.data(), sizeof(int32_t) * nnz_, stream_);
+  h2d(t_v_.p, tv.data(), sizeof(double) * nnz_, stream_);
+  h2d(t_blk_.p, tb.data(), sizeof(int32_t) * tb.size(), stream_);
+  KT_ = CsrDev{n_, m_, nnz_, t_rp_.as<int32_t>(), t_ci_.as<int32_t>(), t_v_.as<double>(),
+               int32_t(tb.size() - 1), t_blk_.as<int32_t>()};
+
+  c_.reserve(sizeof(double) * n_);
+  q_.reserve(sizeof(double) * m_);
+  l_.reserve(sizeof(double) * n_);
+  u_.reserve(sizeof(double) * n_);
+  h2d(c_.p, v->c, sizeof(double) * n_, stream_);
+  h2d(q_.p, v->q, sizeof(double) * m_, stream_);
+  h2d(l_.p, v->l, sizeof(double) * n_, stream_);
+  h2d(u_.p, v->u, sizeof(double) * n_, stream_);
+  bounds_ok_ = true;
+  for (int j = 0; j < n_; ++j)
+    if (v->l[j] > v->u[j]) bounds_ok_ = false;
+
+  // scratch for power iteration / per-op / KKT evaluation
+  pw_x_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
+  pw_mx_.reserve(sizeof(double) * std::max<int64_t>(m_, 1));
+  pw_mtmx_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
+  pw_state_.reserve(sizeof(PowerState));
+  lam_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
+  scal_.reserve(sizeof(double) * 64);
+  const int64_t nbig = std::max<int64_t>(std::max<int64_t>(n_, m_), 1);
+  part_small_.reserve(sizeof(double) * 5 * (nbig / kThreads + 2));
+  AAPDHG_CUDA(cudaMallocHost(&h_state_, sizeof(DevState)));
+
+  // ||q|| and ||c|| under both reduction orders (constants of kkt_metrics)
+  for (int serial = 0; serial < 2; ++serial) {
+    nrm_q_[serial ? 0 : 1] = std::sqrt(device_dot(q_.as<double>(), nullptr, m_, serial != 0));
+    nrm_c_[serial ? 0 : 1] = std::sqrt(device_dot(c_.as<double>(), nullptr, n_, serial != 0));
+  }
+}
+
+Problem::~Problem() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  for (auto& e : event_pool_) cudaEventDestroy(e);
+  for (auto& p : pending_) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  if (h_state_) cudaFreeHost(h_state_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Problem::sync() { AAPDHG_CUDA(cudaStreamSynchronize(stream_)); }
+
+bool Problem::resolve_serial(int reduction) const {
+  if (reduction == AAPDHG_REDUCE_SERIAL) return true;
+  if (reduction == AAPDHG_REDUCE_TREE) return false;
+  return N_ <= 65536;
+}
+
+// a.b (b == nullptr: a.a) on the device in the requested order; synchronous.
+double Problem::device_dot(const double* a, const double* b, int64_t n, bool serial) {
+  double* part = part_small_.as<double>();
+  const int nb = grid_for(n);
+  if (!serial && n > 0) k_sumsq_partials<<<nb, kThreads, 0, stream_>>>(a, b, n, part, nullptr);
+  k_dot_final<<<1, kCtrlThreads, 0, stream_>>>(a, b, n, part, n > 0 ? nb : 0, serial ? 1 : 0,
+                                                scal_.as<double>() + 40);
+  AAPDHG_CUDA(cudaGetLastError());
+  double out = 0.0;
+  d2h(&out, scal_.as<double>() + 40, sizeof(double), stream_);
+  sync();
+  return out;
+}
+
+void Problem::ensure_iter_buffers(int method, int cap) {
+  const int nblk1 = KT_.nblocks, nblk2 = K_.nblocks;
+  upool_.reserve(sizeof(double) * 4 * std::max<int64_t>(N_, 1));
+  kxpool_.reserve(sizeof(double) * 3 * std::max<int64_t>(m_, 1));
+  T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
+  part1_.reserve(sizeof(double) * P1_COUNT * std::max(nblk1, 1));
+  part2_.reserve(sizeof(double) * P2_COUNT * std::max(nblk2, 1));
+  gram_.reserve(sizeof(double) * kMaxMemory * kMaxMemory);
+  work_.reserve(sizeof(double) * kMaxMemory * kMaxMemory);
+  vec_.reserve(sizeof(double) * 8 * kMaxMemory);
+  rec_.reserve(sizeof(aapdhg_record) * kRecCap);
+  rec_cap_ = kRecCap;
+  dparams_.reserve(sizeof(DevParams));
+  dstate_.reserve(sizeof(DevState));
+  ndot_blk_ = int((N_ + kDotChunk - 1) / kDotChunk);
+  if (method != AAPDHG_METHOD_PDHG) {
+    gpool_.reserve(sizeof(double) * 2 * std::max<int64_t>(N_, 1));
+    du_.reserve(sizeof(double) * size_t(cap) * std::max<int64_t>(N_, 1));
+    dg_.reserve(sizeof(double) * size_t(cap) * std::max<int64_t>(N_, 1));
+    const int items = num_items_host(cap, AAPDHG_METHOD_FAA);
+    partdot_.reserve(sizeof(double) * size_t(items) * std::max(ndot_blk_, 1));
+  }
+}
+
+void Problem::upload_iterate(int slot, const double* x, const double* y) {
+  double* base = upool_.as<double>() + int64_t(slot) * N_;
+  if (x) h2d(base, x, sizeof(double) * n_, stream_);
+  else if (n_) AAPDHG_CUDA(cudaMemsetAsync(base, 0, sizeof(double) * n_, stream_));
+  if (y) h2d(base + n_, y, sizeof(double) * m_, stream_);
+  else if (m_) AAPDHG_CUDA(cudaMemsetAsync(base + n_, 0, sizeof(double) * m_, stream_));
+}
+
+// kkt_metrics (solver.cpp:64-110) of the iterate stored in upool slot `slot`.
+void Problem::kkt_eval(int slot, bool serial, double* out_dev, double* lam_dev) {
+  const double* x = upool_.as<double>() + int64_t(slot) * N_;
+  const double* y = x + n_;
+  double* T = T_.as<double>();
+  double* KX = pw_mx_.as<double>();
+  SpmvArgs a{};
+  if (n_ && KT_.nblocks) {
+    a.x = y;
+    a.out = T;
+    if (serial) k_spmv<true><<<KT_.nblocks, kThreads, 0, stream_>>>(KT_, a, nullptr);
+    else k_spmv<false><<<KT_.nblocks, kThreads, 0, stream_>>>(KT_, a, nullptr);
+  }
+  if (m_ && K_.nblocks) {
+    a.x = x;
+    a.out = KX;
+    if (serial) k_spmv<true><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
+    else k_spmv<false><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
+  }
+  const int64_t nbig = std::max<int64_t>(std::max<int64_t>(n_, m_), 1);
+  const int nb = int((nbig + kThreads - 1) / kThreads);
+  k_kkt_terms<<<nb, kThreads, 0, stream_>>>(x, y, T, KX, c_.as<double>(), q_.as<double>(),
+                                            l_.as<double>(), u_.as<double>(), n_, m_, m1_,
+                                            lam_dev, part_small_.as<double>(), nb);
+  k_kkt_final<<<1, kCtrlThreads, 0, stream_>>>(
+      x, y, T, KX, c_.as<double>(), q_.as<double>(), l_.as<double>(), u_.as<double>(), n_, m_,
+      m1_, part_small_.as<double>(), nb, serial ? 1 : 0, nrm_q_[serial ? 0 : 1],
+      nrm_c_[serial ? 0 : 1], out_dev);
+  AAPDHG_CUDA(cudaGetLastError());
+}
+
+// ---- profiling ------------------------------------------------------------
+void Problem::prof_begin(cudaStream_t s, const char* name) {
+  if (!profiling_) return;
+  cudaEvent_t a;
+  if (event_pool_.empty()) {
+    AAPDHG_CUDA(cudaEventCreate(&a));
+  } else {
+    a = event_pool_.back();
+    event_pool_.pop_back();
+  }
+  AAPDHG_CUDA(cudaEventRecord(a, s));
+  cur_name_ = name;
+  cur_a_ = a;
+}
+
+void Problem::prof_end(cudaStream_t s) {
+  if (!profiling_) return;
+  cudaEvent_t b;
+  if (event_pool_.empty()) {
+    AAPDHG_CUDA(cudaEventCreate(&b));
+  } else {
+    b = event_pool_.back();
+    event_pool_.pop_back();
+  }
+  AAPDHG_CUDA(cudaEventRecord(b, s));
+  pending_.push_back({cur_name_, cur_a_, b});
+}
+
+void Problem::prof_collect() {
+  for (auto& p : pending_) {
+    float ms = 0.f;
+    AAPDHG_CUDA(cudaEventSynchronize(p.b));
+    AAPDHG_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    KernelStat& st = stats_[p.name];
+    st.ms += ms;
+    st.launches += 1;
+    event_pool_.push_back(p.a);
+    event_pool_.push_back(p.b);
+  }
+  pending_.clear();
+}
+
+#define LAUNCH(name, ...)      \
+  do {                         \
+    prof_begin(s, name);       \
+    __VA_ARGS__;               \
+    prof_end(s);               \
+    ++nodes;                   \
+  } while (0)
+
+// One solver iteration (solver.cpp:188-252) as a predicated kernel sequence.
+void Problem::launch_iteration(cudaStream_t s, const SolveSetup& su) {
+  int nodes = 0;
+  const bool ser = su.serial, push = su.push;
+  if (su.nblk1 > 0) {
+    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<su.nblk1, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<su.nblk1, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<su.nblk1, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else LAUNCH("k_dual_side", k_dual_side<false, false><<<su.nblk1, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+  }
+  if (su.nblk2 > 0) {
+    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<su.nblk2, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<su.nblk2, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<su.nblk2, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else LAUNCH("k_primal_side", k_primal_side<false, false><<<su.nblk2, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+  }
+  if (ser) LAUNCH("k_serial_reduce", k_serial_reduce<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S, 1));
+  LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(su.B, su.P, su.S));
+  if (su.method != AAPDHG_METHOD_PDHG) {
+    if (ser) {
+      const int blocks = (su.items_max * 32 + kThreads - 1) / kThreads;
+      LAUNCH("k_serial_dots", k_serial_dots<<<blocks, kThreads, 0, s>>>(su.D, su.P, su.S));
+    } else {
+      LAUNCH("k_tree_dots", k_tree_dots<<<su.ndot_blk, kThreads, 0, s>>>(su.D, su.P, su.S));
+    }
+    LAUNCH("k_aa_solve", k_aa_solve<<<1, 1024, 0, s>>>(su.D, su.W, su.P, su.S, 0));
+    LAUNCH("k_mix", k_mix<<<grid_for(N_), kThreads, 0, s>>>(su.B, su.B.dg, su.P, su.S, 1));
+    if (K_.nblocks > 0) {
+      SpmvArgs a{};
+      a.x_pool = su.B.upool;
+      a.x_role = U_CAND;
+      a.x_stride = N_;
+      a.out_pool = su.B.kxpool;
+      a.out_role = KX_CAND;
+      a.out_stride = m_;
+      a.pred_aa_ok = 1;
+      if (ser) LAUNCH("k_spmv_recache", k_spmv<true><<<K_.nblocks, kThreads, 0, s>>>(K_, a, su.S));
+      else LAUNCH("k_spmv_recache", k_spmv<false><<<K_.nblocks, kThreads, 0, s>>>(K_, a, su.S));
+    }
+  }
+  LAUNCH("k_commit", k_commit<<<1, 1, 0, s>>>(su.P, su.S));
+  nodes_per_iter_ = nodes;
+  AAPDHG_CUDA(cudaGetLastError());
+}
+#undef LAUNCH
+
+// ---- step sizes -------------------------------------------------------------
+static void validate_config(const aapdhg_solve_params* c) {
+  // validate, solver.cpp:25-38 (same messages)
+  const char* msg = nullptr;
+  if (c->m < 1) msg = "solver: m must be >= 1";
+  else if (c->safeguard_d <= 0.0) msg = "solver: D must be > 0";
+  else if (c->safeguard_eps <= 0.0) msg = "solver: eps must be > 0";
+  else if (c->toll <= 0.0) msg = "solver: toll must be > 0";
+  else if (c->kkt_eps <= 0.0) msg = "solver: kkt_eps must be > 0";
+  else if (c->beta <= 0.0 || c->beta > 1.0) msg = "solver: beta must be in (0, 1]";
+  else if (c->eta < 0.0) msg = "solver: eta must be >= 0";
+  else if (c->c_s <= 0.0 || c->c_s > 1.0) msg = "solver: c_s must be in (0, 1]";
+  else if (c->kappa_bar <= 0.0) msg = "solver: kappa_bar must be > 0";
+  if (msg) throw StatusError(AAPDHG_ERR_INPUT, msg);
+  if (c->method < AAPDHG_METHOD_PDHG || c->method > AAPDHG_METHOD_FAA)
+    throw StatusError(AAPDHG_ERR_INPUT, "solver: unknown method");
+  if (c->reduction < AAPDHG_REDUCE_AUTO || c->reduction > AAPDHG_REDUCE_TREE)
+    throw StatusError(AAPDHG_ERR_INPUT, "solver: unknown reduction mode");
+}
+
+void Problem::run_power(const double* x0, int max_iters, double rel_tol, bool serial,
+                        double* out, int* rounds) {
+  double* x = pw_x_.as<double>();
+  double* mx = pw_mx_.as<double>();
+  double* mtmx = pw_mtmx_.as<double>();
+  double* scal = scal_.as<double>();
+  double* part = part_small_.as<double>();
+  PowerState* ps = pw_state_.as<PowerState>();
+  h2d(x, x0, sizeof(double) * n_, stream_);
+  const int nb = grid_for(n_);
+  if (!serial) k_sumsq_partials<<<nb, kThreads, 0, stream_>>>(x, nullptr, n_, part, nullptr);
+  k_dot_final<<<1, kCtrlThreads, 0, stream_>>>(x, nullptr, n_, part, nb, serial, scal);
+  k_power_init_norm<<<1, 1, 0, stream_>>>(x, scal);
+  k_scale<<<grid_for(n_), kThreads, 0, stream_>>>(x, x, n_, nullptr, scal + 1);
+  PowerState h{};
+  h.max_iters = max_iters;
+  h.rel_tol = rel_tol;
+  h2d(ps, &h, sizeof h, stream_);
+  SpmvArgs a1{}, a2{};
+  a1.x = x;
+  a1.out = mx;
+  a1.stop = &ps->done;
+  a2.x = mx;
+  a2.out = mtmx;
+  a2.stop = &ps->done;
+  PowerState hs{};
+  for (;;) {
+    for (int r = 0; r < kPowerBatch; ++r) {
+      if (K_.nblocks) {
+        if (serial) k_spmv<true><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a1, nullptr);
+        else k_spmv<false><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a1, nullptr);
+      }
+      if (KT_.nblocks) {
+        if (serial) k_spmv<true><<<KT_.nblocks, kThreads, 0, stream_>>>(KT_, a2, nullptr);
+        else k_spmv<false><<<KT_.nblocks, kThreads, 0, stream_>>>(KT_, a2, nullptr);
+      }
+      if (!serial) k_sumsq_partials<<<nb, kThreads, 0, stream_>>>(mtmx, nullptr, n_, part, &ps->done);
+      k_power_ctrl<<<1, kCtrlThreads, 0, stream_>>>(mtmx, n_, part, nb, serial, ps);
+      k_scale<<<grid_for(n_), kThreads, 0, stream_>>>(x, mtmx, n_, ps, nullptr);
+    }
+    AAPDHG_CUDA(cudaGetLastError());
+    d2h(&hs, ps, sizeof hs, stream_);
+    sync();
+    if (hs.done) break;
+  }
+  *out = hs.result;
+  if (rounds) *rounds = hs.rounds;
+}
+
+// power_iteration_norm, sparse_linalg.cpp:95-123 (start vector drawn on the
+// host with the same std::mt19937_64 + uniform_real_distribution(-1, 1)).
+double Problem::power_norm(int max_iters, double rel_tol, uint64_t seed, bool serial,
+                           int* rounds) {
+  AAPDHG_CUDA(cudaSetDevice(device_));
+  if (rounds) *rounds = 0;
+  if (all_zero_ || n_ == 0) return 0.0;
+  if (max_iters <= 0) return 0.0;
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unif(-1.0, 1.0);
+  std::vector<double> x0(static_cast<size_t>(n_));
+  for (double& v : x0) v = unif(rng);
+  double out = 0.0;
+  run_power(x0.data(), max_iters, rel_tol, serial, &out, rounds);
+  return out;
+}
+
+// select_step_sizes, solver.cpp:112-123
+void Problem::select_step_sizes(const aapdhg_solve_params* prm, double* tau, double* sigma) {
+  if (prm->tau > 0.0 || prm->sigma > 0.0) {
+    if (!(prm->tau > 0.0 && prm->sigma > 0.0))
+      throw StatusError(AAPDHG_ERR_INPUT, "step sizes: override requires both tau and sigma");
+    *tau = prm->tau;
+    *sigma = prm->sigma;
+    return;
+  }
+  const double k_norm = power_norm(5000, 1e-4, 12345u, resolve_serial(prm->reduction), nullptr);
+  if (k_norm == 0.0) {
+    *tau = *sigma = 1.0;
+    return;
+  }
+  const double s = 0.9 / k_norm;
+  *tau = *sigma = s;
+}
+
+// ---- solve ------------------------------------------------------------------
+void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const double* y0,
+                    aapdhg_solve_result* res, double* x_out, double* y_out, double* lam_out,
+                    aapdhg_record_sink sink, void* ctx) {
+  const auto t_start = Clock::now();
+  AAPDHG_CUDA(cudaSetDevice(device_));
+  validate_config(prm);
+  if (!bounds_ok_) throw StatusError(AAPDHG_ERR_INPUT, "build_lambda_set: l > u");
+  const int method = prm->method;
+  if (method != AAPDHG_METHOD_PDHG && prm->m > uint64_t(kMaxMemory))
+    throw StatusError(AAPDHG_ERR_UNSUPPORTED,
+                      "solver: memory capacity m > " + std::to_string(kMaxMemory) +
+                          " is not supported by the sm_100a path");
+  if (prm->d_hat)
+    for (int64_t i = 0; i < N_; ++i)
+      if (prm->d_hat[i] <= 0.0) throw StatusError(AAPDHG_ERR_INPUT, "aa: d_hat entries must be > 0");
+  double tau, sigma;
+  select_step_sizes(prm, &tau, &sigma);
+
+  const bool serial = resolve_serial(prm->reduction);
+  const int cap = method == AAPDHG_METHOD_PDHG ? 0 : int(prm->m);
+  ensure_iter_buffers(method, std::max(cap, 1));
+  if (prm->d_hat) {
+    dhat_.reserve(sizeof(double) * N_);
+    h2d(dhat_.p, prm->d_hat, sizeof(double) * N_, stream_);
+  }
+  std::vector<double> ptab;
+  if (method != AAPDHG_METHOD_PDHG) {
+    const uint64_t len = std::min<uint64_t>(prm->max_iters + 1, kPowTabMax);
+    ptab.resize(len);
+    for (uint64_t i = 0; i < len; ++i) ptab[i] = std::pow(double(i) + 1.0, -(1.0 + prm->safeguard_eps));
+    pow_tab_.reserve(sizeof(double) * len);
+    h2d(pow_tab_.p, ptab.data(), sizeof(double) * len, stream_);
+  }
+
+  DevParams P{};
+  P.method = method;
+  P.serial = serial ? 1 : 0;
+  P.m1 = m1_;
+  P.kkt_terminate = prm->kkt_terminate ? 1 : 0;
+  P.n = n_;
+  P.mrows = m_;
+  P.cap = cap;
+  P.N = N_;
+  P.safeguard_d = prm->safeguard_d;
+  P.safeguard_eps = prm->safeguard_eps;
+  P.beta = prm->beta;
+  P.eta = prm->eta;
+  P.c_s = prm->c_s;
+  P.kappa_bar = prm->kappa_bar;
+  P.toll = prm->toll;
+  P.kkt_eps = prm->kkt_eps;
+  P.tau = tau;
+  P.sigma = sigma;
+  P.max_iters = prm->max_iters;
+  P.max_wall_s = prm->max_wall_seconds;
+  P.nrm_q = nrm_q_[serial ? 0 : 1];
+  P.nrm_c = nrm_c_[serial ? 0 : 1];
+  P.d_hat = prm->d_hat ? dhat_.as<double>() : nullptr;
+  P.pow_tab = ptab.empty() ? nullptr : pow_tab_.as<double>();
+  P.pow_len = ptab.size();
+  P.rec = rec_.as<aapdhg_record>();
+  P.rec_cap = rec_cap_;
+  P.nblk1 = KT_.nblocks;
+  P.nblk2 = K_.nblocks;
+  P.ndot_blk = ndot_blk_;
+
+  DevState S0{};
+  for (int r = 0; r < 4; ++r) S0.u_idx[r] = r;
+  for (int r = 0; r < 3; ++r) S0.kx_idx[r] = r;
+  S0.g_idx[0] = 0;
+  S0.g_idx[1] = 1;
+  DevState* S = dstate_.as<DevState>();
+
+  // start iterate P(u0) in slot 0, its K x cached in kx slot 0; fresh pools
+  AAPDHG_CUDA(cudaMemsetAsync(upool_.p, 0, sizeof(double) * 4 * N_, stream_));
+  if (method != AAPDHG_METHOD_PDHG) {
+    AAPDHG_CUDA(cudaMemsetAsync(gpool_.p, 0, sizeof(double) * 2 * N_, stream_));
+  }
+  upload_iterate(0, x0, y0);
+  P.wall_offset_s = secs(t_start);
+  h2d(dparams_.p, &P, sizeof P, stream_);
+  h2d(S, &S0, sizeof S0, stream_);
+  k_project_start<<<grid_for(N_, kThreads, 1 << 30), kThreads, 0, stream_>>>(
+      upool_.as<double>(), l_.as<double>(), u_.as<double>(), n_, N_, m1_, S);
+  if (m_ && K_.nblocks) {
+    SpmvArgs a{};
+    a.x = upool_.as<double>();
+    a.out = kxpool_.as<double>();
+    if (serial) k_spmv<true><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
+    else k_spmv<false><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
+  }
+  AAPDHG_CUDA(cudaGetLastError());
+
+  SolveSetup su;
+  su.B = IterBufs{upool_.as<double>(), kxpool_.as<double>(), gpool_.as<double>(),
+                  du_.as<double>(), dg_.as<double>(), T_.as<double>(), part1_.as<double>(),
+                  part2_.as<double>(), c_.as<double>(), q_.as<double>(), l_.as<double>(),
+                  u_.as<double>()};
+  su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
+                 partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
+  su.W = SolveScratch{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
+  su.P = dparams_.as<DevParams>();
+  su.S = S;
+  su.serial = serial;
+  su.push = method != AAPDHG_METHOD_PDHG;
+  su.method = method;
+  su.cap = cap;
+  su.nblk1 = KT_.nblocks;
+  su.nblk2 = K_.nblocks;
+  su.ndot_blk = ndot_blk_;
+  su.items_max = num_items_host(std::max(cap, 1), method);
+
+  // graph of kGraphIters iterations, cached per launch layout
+  const bool use_graph = !profiling_;
+  if (use_graph) {
+    char key[256];
+    std::snprintf(key, sizeof key, "%d/%d/%d/%p/%p/%p/%p/%p", method, int(serial), cap,
+                  upool_.p, du_.p, partdot_.p, dparams_.p, rec_.p);
+    if (graph_key_ != key || !graph_exec_) {
+      if (graph_exec_) {
+        cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+      }
+      cudaGraph_t g;
+      AAPDHG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+      for (int it = 0; it < kGraphIters; ++it) launch_iteration(stream_, su);
+      AAPDHG_CUDA(cudaStreamEndCapture(stream_, &g));
+      AAPDHG_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
+      cudaGraphDestroy(g);
+      graph_key_ = key;
+    }
+  }
+
+  uint64_t flushed = 0, iters_launched = 0;
+  int batch = 1;
+  std::vector<aapdhg_record> host_recs;
+  const aapdhg_record* drec = rec_.as<aapdhg_record>();
+  for (;;) {
+    for (int b = 0; b < batch; ++b) {
+      if (use_graph) {
+        AAPDHG_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+      } else {
+        for (int it = 0; it < kGraphIters; ++it) launch_iteration(stream_, su);
+      }
+      iters_launched += kGraphIters;
+    }
+    d2h(h_state_, S, sizeof(DevState), stream_);
+    sync();
+    if (profiling_) prof_collect();
+    // stream completed records out of the device ring
+    const uint64_t done_recs = h_state_->rec_complete;
+    if (done_recs > flushed) {
+      const uint64_t cnt = done_recs - flushed;
+      host_recs.resize(cnt);
+      uint64_t got = 0;
+      while (got < cnt) {
+        const uint64_t pos = (flushed + got) % rec_cap_;
+        const uint64_t chunk = std::min<uint64_t>(cnt - got, rec_cap_ - pos);
+        d2h(host_recs.data() + got, drec + pos, chunk * sizeof(aapdhg_record), stream_);
+        got += chunk;
+      }
+      sync();
+      if (sink) sink(host_recs.data(), cnt, ctx);
+      flushed = done_recs;
+    }
+    if (h_state_->done) break;
+    // ring safety: never run further ahead than the ring can hold
+    batch = std::min(batch * 2, kMaxBatchGraphs);
+    while (uint64_t(batch) * kGraphIters * 2 > rec_cap_) batch /= 2;
+  }
+  const DevState st = *h_state_;
+
+  // finish, solver.cpp:153-166
+  const int slot = st.u_idx[st.final_role];
+  double* kkt_dev = scal_.as<double>() + 8;
+  kkt_eval(slot, serial, kkt_dev, lam_.as<double>());
+  double kkt[4];
+  d2h(kkt, kkt_dev, sizeof kkt, stream_);
+  const double* ufin = upool_.as<double>() + int64_t(slot) * N_;
+  if (x_out) d2h(x_out, ufin, sizeof(double) * n_, stream_);
+  if (y_out) d2h(y_out, ufin + n_, sizeof(double) * m_, stream_);
+  if (lam_out) d2h(lam_out, lam_.as<double>(), sizeof(double) * n_, stream_);
+  sync();
+  std::memset(res, 0, sizeof *res);
+  res->status = st.status;
+  res->iterations = st.i + st.j;
+  res->i = st.i;
+  res->j = st.j;
+  res->aa_failures = st.aa_failures;
+  res->g_norm = st.g_final;
+  res->r_gap = kkt[0];
+  res->r_primal = kkt[1];
+  res->r_dual = kkt[2];
+  res->objective = kkt[3];
+  res->tau = tau;
+  res->sigma = sigma;
+  res->wall_seconds = secs(t_start);
+  last_loop_iters_ = st.loop_iters;
+  last_launches_ = iters_launched * uint64_t(nodes_per_iter_);
+}
+
+// ---- single-op entry points ----------------------------------------------
+void Problem::matvec(const double* x, double* out) {
+  AAPDHG_CUDA(cudaSetDevice(device_));
+  h2d(pw_x_.p, x, sizeof(double) * n_, stream_);
+  SpmvArgs a{};
+  a.x = pw_x_.as<double>();
+  a.out = pw_mx_.as<double>();
+  if (K_.nblocks) k_spmv<true><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
+  AAPDHG_CUDA(cudaGetLastError());
+  d2h(out, pw_mx_.p, sizeof(double) * m_, stream_);
+  sync();
+}
+
+void Problem::matvec_transpose(const double* y, double* out) {
+  AAPDHG_CUDA(cudaSetDevice(device_));
+  h2d(pw_mx_.p, y, sizeof(double) * m_, stream_);
+  SpmvArgs a{};
+  a.x = pw_mx_.as<double>();
+  a.out = pw_mtmx_.as<double>();
+  if (KT_.nblocks) k_spmv<true><<<KT_.nblocks, kThreads, 0, stream_>>>(KT_, a, nullptr);
+  AAPDHG_CUDA(cudaGetLastError());
+  d2h(out, pw_mtmx_.p, sizeof(double) * n_, stream_);
+  sync();
+}
+
+static DevState identity_state() {
+  DevState S{};
+  for (int r = 0; r < 4; ++r) S.u_idx[r] = r;
+  for (int r = 0; r < 3; ++r) S.kx_idx[r] = r;
+  S.g_idx[0] = 0;
+  S.g_idx[1] = 1;
+  return S;
+}
+
+// pdhg_step, pdhg_core.cpp:45-63, through the fused K1/K2 kernels
+void Problem::pdhg_step(double tau, double sigma, const double* x, const double* y,
+                        double* xn, double* yn) {
+  AAPDHG_CUDA(cudaSetDevice(device_));
+  ensure_iter_buffers(AAPDHG_METHOD_PDHG, 1);
+  upload_iterate(0, x, y);
+  if (K_.nblocks) {
+    SpmvArgs a{};
+    a.x = upool_.as<double>();
+    a.out = kxpool_.as<double>();
+    k_spmv<true><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
+  }
+  DevParams P{};
+  P.method = AAPDHG_METHOD_PDHG;
+  P.serial = 1;
+  P.m1 = m1_;
+  P.n = n_;
+  P.mrows = m_;
+  P.N = N_;
+  P.tau = tau;
+  P.sigma = sigma;
+  P.nblk1 = KT_.nblocks;
+  P.nblk2 = K_.nblocks;
+  const DevState S = identity_state();
+  h2d(dparams_.p, &P, sizeof P, stream_);
+  h2d(dstate_.p, &S, sizeof S, stream_);
+  IterBufs B{upool_.as<double>(), kxpool_.as<double>(), nullptr, nullptr, nullptr,
+             T_.as<double>(), part1_.as<double>(), part2_.as<double>(), c_.as<double>(),
+             q_.as<double>(), l_.as<double>(), u_.as<double>()};
+  if (KT_.nblocks)
+    k_dual_side<true, false><<<KT_.nblocks, kThreads, 0, stream_>>>(
+        KT_, B, dparams_.as<DevParams>(), dstate_.as<DevState>());
+  if (K_.nblocks)
+    k_primal_side<true, false><<<K_.nblocks, kThreads, 0, stream_>>>(
+        K_, B, dparams_.as<DevParams>(), dstate_.as<DevState>());
+  AAPDHG_CUDA(cudaGetLastError());
+  const double* hat = upool_.as<double>() + 2 * N_;
+  d2h(xn, hat, sizeof(double) * n_, stream_);
+  d2h(yn, hat + n_, sizeof(double) * m_, stream_);
+  sync();
+}
+
+void Problem::kkt_metrics(int reduction, const double* x, const double* y, double* kkt,
+                          double* lam) {
+  AAPDHG_CUDA(cudaSetDevice(device_));
+  ensure_iter_buffers(AAPDHG_METHOD_PDHG, 1);
+  upload_iterate(0, x, y);
+  double* kd = scal_.as<double>() + 16;
+  kkt_eval(0, resolve_serial(reduction), kd, lam_.as<double>());
+  d2h(kkt, kd, 4 * sizeof(double), stream_);
+  if (lam) d2h(lam, lam_.p, sizeof(double) * n_, stream_);
+  sync();
+}
+
+// aa_apply (anderson.cpp:106-135) or build_filtered_memory + filtered_aa_apply
+// (filtering.cpp:140-181) through the solver's own kernels. Returns an
+// aapdhg_status (AAPDHG_ERR_SINGULAR for the reference's SingularError).
+int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols,
+                      const double* dg_cols, double beta, const double* d_hat, double eta,
+                      double c_s, double kappa_bar, const double* u, const double* g,
+                      double* out, int32_t* kept) {
+  AAPDHG_CUDA(cudaSetDevice(device_));
+  if (p < 0) throw StatusError(AAPDHG_ERR_DIMENSION, "aa_apply: negative memory size");
+  if (p > kMaxMemory)
+    throw StatusError(AAPDHG_ERR_UNSUPPORTED, "aa_apply: memory larger than supported");
+  if (d_hat)
+    for (int64_t i = 0; i < N_; ++i)
+      if (d_hat[i] <= 0.0) throw StatusError(AAPDHG_ERR_INPUT, "aa: d_hat entries must be > 0");
+  const int method = filtered ? AAPDHG_METHOD_FAA : AAPDHG_METHOD_AA;
+  const bool serial = resolve_serial(reduction);
+  ensure_iter_buffers(method, std::max(p, 1));
+  h2d(du_.p, du_cols, sizeof(double) * size_t(p) * N_, stream_);
+  h2d(dg_.p, dg_cols, sizeof(double) * size_t(p) * N_, stream_);
+  h2d(gpool_.p, g, sizeof(double) * N_, stream_);
+  h2d(upool_.p, u, sizeof(double) * N_, stream_);
+  if (d_hat) {
+    dhat_.reserve(sizeof(double) * N_);
+    h2d(dhat_.p, d_hat, sizeof(double) * N_, stream_);
+  }
+  DevParams P{};
+  P.method = method;
+  P.serial = serial ? 1 : 0;
+  P.m1 = m1_;
+  P.n = n_;
+  P.mrows = m_;
+  P.cap = std::max(p, 1);
+  P.N = N_;
+  P.beta = beta;
+  P.eta = eta;
+  P.c_s = c_s;
+  P.kappa_bar = kappa_bar;
+  P.d_hat = d_hat ? dhat_.as<double>() : nullptr;
+  P.rec = rec_.as<aapdhg_record>();
+  P.rec_cap = rec_cap_;
+  P.ndot_blk = ndot_blk_;
+  DevState S = identity_state();
+  S.aa_attempt = 1;
+  S.mem_size = p;
+  for (int t = 0; t < p; ++t) S.mem_slots[t] = t;
+  h2d(dparams_.p, &P, sizeof P, stream_);
+  h2d(dstate_.p, &S, sizeof S, stream_);
+  DotBufs D{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(), partdot_.as<double>(),
+            num_items_host(std::max(p, 1), method)};
+  SolveScratch W{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
+  IterBufs B{upool_.as<double>(), kxpool_.as<double>(), gpool_.as<double>(), du_.as<double>(),
+             dg_.as<double>(), T_.as<double>(), part1_.as<double>(), part2_.as<double>(),
+             c_.as<double>(), q_.as<double>(), l_.as<double>(), u_.as<double>()};
+  const DevParams* Pd = dparams_.as<DevParams>();
+  DevState* Sd = dstate_.as<DevState>();
+  const int items = num_items_host(p, method);
+  if (items > 0) {
+    if (serial) {
+      k_serial_dots<<<(items * 32 + kThreads - 1) / kThreads, kThreads, 0, stream_>>>(D, Pd, Sd);
+    } else {
+      k_tree_dots<<<ndot_blk_, kThreads, 0, stream_>>>(D, Pd, Sd);
+    }
+  }
+  k_aa_solve<<<1, 1024, 0, stream_>>>(D, W, Pd, Sd, 1);
+  k_mix<<<grid_for(N_), kThreads, 0, stream_>>>(B, dg_.as<double>(), Pd, Sd, 0);
+  AAPDHG_CUDA(cudaGetLastError());
+  d2h(h_state_, Sd, sizeof(DevState), stream_);
+  sync();
+  if (!h_state_->aa_ok) return AAPDHG_ERR_SINGULAR;
+  d2h(out, upool_.as<double>() + 3 * N_, sizeof(double) * N_, stream_);
+  sync();
+  if (kept) {
+    for (int t = 0; t < p; ++t) kept[t] = 0;
+    for (int t = 0; t < h_state_->mix_p; ++t) kept[h_state_->mix_slots[t]] = 1;
+  }
+  return AAPDHG_OK;
+}
+
+}  // namespace aapdhg_b200

@@ -1,0 +1,118 @@
+// engine.h — host side of the sm_100a solver: one Problem per handle.
+#pragma once
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace aapdhg_b200 {
+
+// Device allocation that frees itself.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf();
+  void reserve(size_t b);  // grows, never shrinks (contents lost on growth)
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct KernelStat {
+  double ms = 0.0;
+  uint64_t launches = 0;
+};
+
+struct SolveSetup;
+
+class Problem {
+ public:
+  Problem(const aapdhg_problem_view* v, int device);
+  ~Problem();
+
+  int n() const { return n_; }
+  int m() const { return m_; }
+  int m1() const { return m1_; }
+  int64_t nnz() const { return nnz_; }
+
+  void solve(const aapdhg_solve_params* prm, const double* x0, const double* y0,
+             aapdhg_solve_result* res, double* x_out, double* y_out, double* lam_out,
+             aapdhg_record_sink sink, void* ctx);
+  void select_step_sizes(const aapdhg_solve_params* prm, double* tau, double* sigma);
+  double power_norm(int max_iters, double rel_tol, uint64_t seed, bool serial, int* rounds);
+
+  void matvec(const double* x, double* out);
+  void matvec_transpose(const double* y, double* out);
+  void pdhg_step(double tau, double sigma, const double* x, const double* y, double* xn,
+                 double* yn);
+  void kkt_metrics(int reduction, const double* x, const double* y, double* kkt, double* lam);
+  int aa_apply(int reduction, bool filtered, int p, const double* du_cols,
+               const double* dg_cols, double beta, const double* d_hat, double eta,
+               double c_s, double kappa_bar, const double* u, const double* g, double* out,
+               int32_t* kept);
+
+  void set_profiling(bool on) { profiling_ = on; }
+  const std::map<std::string, KernelStat>& kernel_stats() const { return stats_; }
+  uint64_t last_launches() const { return last_launches_; }
+  uint64_t last_loop_iters() const { return last_loop_iters_; }
+
+ private:
+  bool resolve_serial(int reduction) const;
+  double device_dot(const double* a, const double* b, int64_t n, bool serial);
+  void ensure_iter_buffers(int method, int cap);
+  void upload_iterate(int slot, const double* x, const double* y);
+  void kkt_eval(int slot, bool serial, double* kkt_dev_out, double* lam_dev);
+  void launch_iteration(cudaStream_t s, const SolveSetup& su);
+  void run_power(const double* x0_host, int max_iters, double rel_tol, bool serial, double* out,
+                 int* rounds);
+  void sync();
+
+  // profiling-aware launch bookkeeping
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  void prof_begin(cudaStream_t s, const char* name);
+  void prof_end(cudaStream_t s);
+  void prof_collect();
+  std::vector<Pending> pending_;
+  std::vector<cudaEvent_t> event_pool_;
+  std::string cur_name_;
+  cudaEvent_t cur_a_ = nullptr;
+
+  int device_;
+  cudaStream_t stream_ = nullptr;
+  int n_ = 0, m_ = 0, m1_ = 0;
+  int64_t nnz_ = 0, N_ = 0;
+  bool all_zero_ = true;
+  bool bounds_ok_ = true;
+  CsrDev K_, KT_;
+  DevBuf k_rp_, k_ci_, k_v_, k_blk_, t_rp_, t_ci_, t_v_, t_blk_;
+  DevBuf c_, q_, l_, u_;
+  double nrm_q_[2] = {0, 0}, nrm_c_[2] = {0, 0};  // [serial, tree]
+
+  // iteration buffers
+  int buf_method_ = -1, buf_cap_ = 0;
+  DevBuf upool_, kxpool_, gpool_, du_, dg_, T_, part1_, part2_, partdot_, gram_, work_, vec_;
+  DevBuf rec_, pow_tab_, dparams_, dstate_, dhat_, scal_, part_small_, lam_, pw_x_, pw_mx_,
+      pw_mtmx_, pw_state_;
+  int ndot_blk_ = 0;
+  uint64_t rec_cap_ = 0;
+  DevState* h_state_ = nullptr;  // pinned mirror
+
+  // CUDA graph of G iterations, cached per launch layout
+  cudaGraphExec_t graph_exec_ = nullptr;
+  std::string graph_key_;
+  int graph_iters_ = 0;
+  int nodes_per_iter_ = 0;
+
+  bool profiling_ = false;
+  std::map<std::string, KernelStat> stats_;
+  uint64_t last_launches_ = 0, last_loop_iters_ = 0;
+};
+
+}  // namespace aapdhg_b200

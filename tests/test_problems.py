@@ -1,0 +1,87 @@
+"""Synthetic stand-ins for BASELINE.json's configs and the
+host-side model types. CPU only."""
+import numpy as np
+import pytest
+
+from paper_2508_08062_b200 import problems
+from paper_2508_08062_b200.api import (DimensionError, InputError, Method, ProblemData,
+                                       SolverConfig, SparseMatrix, vstack)
+
+
+def _rows(k):
+    return np.repeat(np.arange(k.nrows), np.diff(k.row_ptr))
+
+
+def _check_csr(k):
+    assert k.row_ptr[0] == 0 and k.row_ptr[-1] == k.nnz
+    assert np.all(np.diff(k.row_ptr) >= 0)
+    r = _rows(k)
+    key = r.astype(np.int64) * k.ncols + k.col_idx
+    assert np.all(np.diff(key) > 0), "columns strictly increasing within rows"
+
+
+def test_config0_shape_and_planted_optimum():
+    p = problems.make_config(0)
+    assert (p.k.nrows, p.k.ncols, p.k.nnz, p.m1) == (1000, 2000, 20000, 0)
+    _check_csr(p.k)
+    assert np.all(p.l == 0) and np.all(np.isinf(p.u))
+    # b = A x*, c = A'y* + s*, s* complementary to x*  =>  c'x* = b'y*
+    assert abs(p.c @ p.planted_x - p.q @ p.planted_y) < 1e-9 * abs(p.c @ p.planted_x)
+    assert np.all(p.planted_x[p.c - p.k.transpose().dense() @ p.planted_y > 1e-12] == 0)
+
+
+def test_config1_distinct_rows_per_column():
+    p = problems.make_config(1, scale=0.02)
+    _check_csr(p.k)
+    assert np.all(np.bincount(p.k.col_idx, minlength=p.n()) == 20)
+
+
+def test_transport_structure():
+    p = problems.make_config(2, scale=0.01)  # 20 x 20
+    S = T = 20
+    _check_csr(p.k)
+    assert p.k.nrows == S + T and p.n() == S * T and p.k.nnz == 2 * S * T
+    assert np.all(np.bincount(p.k.col_idx) == 2)
+    assert abs(p.q[:S].sum() - p.q[S:].sum()) < 1e-9
+    assert np.all(np.diff(p.k.row_ptr) == np.r_[np.full(S, T), np.full(T, S)])
+
+
+def test_zipf_row_lengths():
+    p = problems.make_config(3, scale=0.002)
+    _check_csr(p.k)
+    lens = np.diff(p.k.row_ptr)
+    assert lens.min() >= 1 and (lens == 1).mean() > 0.3
+
+
+def test_from_triplets_sums_duplicates_in_order():
+    k = SparseMatrix.from_triplets(2, 3, [1, 0, 1, 1], [2, 1, 2, 0], [0.1, 5.0, 0.2, 7.0])
+    assert k.row_ptr.tolist() == [0, 1, 3]
+    assert k.col_idx.tolist() == [1, 0, 2]
+    assert k.vals.tolist() == [5.0, 7.0, 0.1 + 0.2]
+    with pytest.raises(DimensionError):
+        SparseMatrix.from_triplets(1, 1, [1], [0], [1.0])
+
+
+def test_transpose_keeps_row_order():
+    p = problems.make_config(0, scale=0.1)
+    kt = p.k.transpose()
+    _check_csr(kt)
+    np.testing.assert_array_equal(kt.dense(), p.k.dense().T)
+
+
+def test_vstack_and_problem_validation():
+    a = SparseMatrix.from_triplets(1, 2, [0], [1], [2.0])
+    b = SparseMatrix.from_triplets(2, 2, [0, 1], [0, 0], [1.0, 3.0])
+    k = vstack(a, b)
+    assert k.dense().tolist() == [[0, 2], [1, 0], [3, 0]]
+    with pytest.raises(DimensionError):
+        ProblemData(k, 1, np.zeros(3), np.zeros(3), np.zeros(2), np.ones(2))
+
+
+def test_config_params_validation():
+    cfg = SolverConfig(method=Method.AA_PDHG, reduction="bogus")
+    with pytest.raises(InputError):
+        cfg.to_params(4)
+    cfg = SolverConfig(aa=type(SolverConfig().aa)(d_hat=np.ones(3)))
+    with pytest.raises(DimensionError):
+        cfg.to_params(4)
