@@ -1,0 +1,336 @@
+"""Benchmark: AA-PDHG fp64 iterations/sec on BASELINE.json configs[1].
+
+Workload (BASELINE.json configs[1]): planted-optimum LP,
+100,000 rows x 200,000 cols, exactly 20 distinct uniform rows per column
+(4.0M nnz), N(0,1) values, AA-PDHG with memory m = 10, D = 1, eps = 1,
+beta = 1, eta = 1e-10, toll = 1e-6. Synthetic seeded data (the reference
+publishes no instance files). One "step" = one solver iteration (PDHG map +
+history push + safeguard, the AA candidate on accepted steps, KKT records).
+
+Arms
+  ours (default)      the sm_100a C-ABI (paper_2508_08062_b200/lib/libaapdhg_cuda.so)
+  --impl reference    the reference's own CPU solve() (oracle/_ref, compiled from
+                      /root/reference sources; the oracle/ C port if absent)
+
+JSON keys beyond the base contract: roofline (dominant kernel, live CUDA
+events), cpu_baseline (the reference on this host's cores), e2e (C-ABI call
+from host buffers), time_to_tol (full solve to 1e-6), clocks, gpu_launches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIG_ID = 1
+MEMORY = 10
+TOLL = 1e-6
+METRIC = "AA-PDHG fp64 iterations/sec (BASELINE configs[1]: 100k x 200k, 4M nnz, m=10)"
+
+
+def workload_config(p):
+    return {"workload": "configs[1] planted LP 100000x200000, 20 nnz/col (4.0M nnz), "
+                        "AA-PDHG m=10, D=1, eps=1, toll=1e-6",
+            "rows": p.k.nrows, "cols": p.n(), "nnz": p.k.nnz, "memory": MEMORY,
+            "l2": "working set > 126 MB L2 (K + K' + history >= 150 MB), no flush"}
+
+
+def solver_config(tau=0.0, max_iters=100000, reduction="tree", max_wall=3600.0):
+    from paper_2508_08062_b200 import Method, SolverConfig
+    return SolverConfig(method=Method.AA_PDHG, m=MEMORY, safeguard_d=1.0, safeguard_eps=1.0,
+                        toll=TOLL, max_iters=max_iters, tau=tau, sigma=tau, reduction=reduction,
+                        max_wall_seconds=max_wall)
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) >= 7:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peak():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def kernel_bytes(p, name):
+    """Algorithmic bytes per launch: CSR streams + compulsory
+    gathers (each gathered element counted once) + vector reads/writes."""
+    n, m, nnz = p.n(), p.k.nrows, p.k.nnz
+    if name == "k_dual_side":   # K'y + xhat + KKT dual terms + history push (x half)
+        return 12 * nnz + 4 * (n + 1) + 8 * m + 8 * n * (4 + 1) + 8 * n * (2 + 3)
+    if name == "k_primal_side":  # K xhat + yhat + KKT primal terms + push (y half)
+        return 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m * (3 + 2) + 8 * m * (2 + 3)
+    if name == "k_spmv_recache":
+        return 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
+    return None
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_sample(p, tau, iters):
+    """The reference CPU solve() on a bounded sample of the workload (explicit
+    tau, `iters` iterations). Returns (iterations/s, kind, seconds)."""
+    from oracle.pyoracle import Oracle, ref_available
+    kind = "reference" if ref_available() else "port"
+    orc = Oracle("ref" if kind == "reference" else "port")
+    cfg = solver_config(tau=tau, max_iters=iters)
+    t0 = time.perf_counter()
+    out = orc.solve(p, cfg)
+    dt = time.perf_counter() - t0
+    return out.result.iterations / dt, kind, dt
+
+
+def run_reference_arm(args, rank, world):
+    from paper_2508_08062_b200 import problems
+    if rank != 0:
+        return
+    p = problems.make_config(CONFIG_ID)
+    from oracle.pyoracle import Oracle, ref_available
+    kind = "reference" if ref_available() else "port"
+    orc = Oracle("ref" if kind == "reference" else "port")
+    # step sizes once (the reference's seeded power iteration), then time
+    # `steps` iterations per sample after `warmup` untimed iterations
+    tau = orc.select_step_sizes(p, solver_config()).tau
+    iters_per_step = 1
+    orc.solve(p, solver_config(tau=tau, max_iters=max(args.warmup, 1)))
+    t0 = time.perf_counter()
+    out = orc.solve(p, solver_config(tau=tau, max_iters=args.steps * iters_per_step))
+    dt = time.perf_counter() - t0
+    val = out.result.iterations / dt
+    line = {"metric": METRIC, "value": val, "unit": "iterations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(out.result.iterations, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded planted-optimum generator, SURVEY.md 8(d))",
+            "config": workload_config(p), "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": 1, "kind": kind,
+                             "sample": f"{out.result.iterations} iterations of configs[1] "
+                                       f"(explicit tau, single-threaded solve())"},
+            "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+
+    import torch
+
+    from paper_2508_08062_b200 import Solver, _abi, problems
+    from paper_2508_08062_b200.api import check, errbuf
+
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    p = problems.make_config(CONFIG_ID)
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+
+    stream = torch.cuda.Stream(device=dev)
+    s = Solver(p, device=dev)
+    lib = s.lib
+    check(lib.aapdhg_cuda_set_stream(s.h, C.c_void_p(stream.cuda_stream)), errbuf())
+    tau = s.select_step_sizes(solver_config()).tau
+
+    # warm-up: graph instantiation, caches
+    s.solve(solver_config(tau=tau, max_iters=max(args.warmup, 3)))
+
+    # ---- timed: exactly K iterations, inputs resident in HBM ---------------
+    cfg = solver_config(tau=tau, max_iters=args.steps)
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            out = s.solve(cfg)
+            ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1)
+    iters = out.result.iterations
+    launches, loop_iters = C.c_uint64(), C.c_uint64()
+    lib.aapdhg_cuda_last_launch_count(s.h, C.byref(launches), C.byref(loop_iters))
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+        tot = torch.tensor([float(iters)], device=f"cuda:{dev}")
+        tdist.all_reduce(tot, op=tdist.ReduceOp.SUM)
+        total_iters = float(tot.item())
+    else:
+        total_iters = float(iters)
+    value = total_iters / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel: per-launch CUDA events -----------
+    lib.aapdhg_cuda_set_profiling(s.h, 1)
+    s.solve(solver_config(tau=tau, max_iters=min(args.steps, 400)))
+    names = C.create_string_buffer(4096)
+    msa = (C.c_double * 64)()
+    la = (C.c_uint64 * 64)()
+    cnt = C.c_int32()
+    lib.aapdhg_cuda_kernel_times(s.h, names, 4096, msa, la, 64, C.byref(cnt))
+    lib.aapdhg_cuda_set_profiling(s.h, 0)
+    kn = names.value.decode().split("\n")[: cnt.value]
+    kstats = {kn[i]: (msa[i], la[i]) for i in range(cnt.value)}
+    tot_ms = sum(v[0] for v in kstats.values())
+    dom = max((k for k in kstats if kernel_bytes(p, k)), key=lambda k: kstats[k][0])
+    avg_ms = kstats[dom][0] / kstats[dom][1]
+    peak, peak_kind = measured_peak()
+    achieved = kernel_bytes(p, dom) / (avg_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": args.traffic, "bytes_per_launch": kernel_bytes(p, dom),
+                "avg_launch_us": avg_ms * 1e3,
+                "share_of_step": kstats[dom][0] / tot_ms if tot_ms else None,
+                "per_kernel_us": {k: 1e3 * v[0] / max(v[1], 1) for k, v in kstats.items()}}
+
+    # ---- time to tolerance (full solve to toll 1e-6, step sizes included) --
+    ttt = None
+    if not args.no_ttt:
+        t0 = time.perf_counter()
+        full = s.solve(solver_config(max_wall=args.ttt_cap))
+        ttt = {"seconds": time.perf_counter() - t0, "iterations": full.result.iterations,
+               "aa_steps": full.result.i, "status": full.result.status.name,
+               "objective": full.result.objective,
+               "planted_objective": getattr(p, "planted_objective", None),
+               "max_kkt": full.result.kkt.max()}
+        kk = full.trajectory
+        if kk.size:
+            mk = np.maximum(np.maximum(kk["r_gap"], kk["r_primal"]), kk["r_dual"])
+            hit = np.flatnonzero(mk <= 1e-6)
+            if hit.size:
+                ttt["first_kkt_le_1e-6"] = {"k": int(kk["k"][hit[0]]),
+                                            "elapsed_s": float(kk["elapsed_s"][hit[0]])}
+    s.close()
+
+    # ---- e2e: C-ABI call from host buffers (upload + solve + download) -----
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    with Solver(p, device=dev) as s2:
+        out2 = s2.solve(solver_config(tau=tau, max_iters=args.steps))
+    e2e_s = time.perf_counter() - t0
+    h2d = (p.k.row_ptr.nbytes + p.k.col_idx.nbytes + p.k.vals.nbytes + p.c.nbytes + p.q.nbytes
+           + p.l.nbytes + p.u.nbytes)
+    d2h = (p.n() * 16 + p.k.nrows * 8) + out2.trajectory.nbytes
+    e2e = {"value": out2.result.iterations / e2e_s, "unit": "iterations/s",
+           "h2d_bytes_per_step": h2d / max(out2.result.iterations, 1),
+           "d2h_bytes_per_step": d2h / max(out2.result.iterations, 1),
+           "seconds": e2e_s, "path": "aapdhg_cuda_problem_create + aapdhg_cuda_solve "
+                                     "(explicit tau) + result download, host numpy buffers"}
+
+    # ---- CPU baseline on this host (rank 0, N=1 only) ----------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, kind, dt = cpu_reference_sample(p, tau, args.cpu_iters)
+        cpu = {"value": v, "unit": "iterations/s", "cores": 1, "kind": kind,
+               "sample": f"{args.cpu_iters} iterations of configs[1] (explicit tau), "
+                         f"{dt:.1f} s, single-threaded reference solve()"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / max(iters, 1),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded planted-optimum generator, SURVEY.md 8(d))",
+                "config": dict(workload_config(p), parallelism=f"replicas{world}" if world > 1
+                               else "single"),
+                "iterations_timed": iters, "aa_steps_timed": out.result.i,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt,
+                "clocks": clk.summary(), "gpu_launches": int(launches.value),
+                "gpu_loop_iterations": int(loop_iters.value)}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-iters", type=int, default=20)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ttt", action="store_true")
+    ap.add_argument("--ttt-cap", type=float, default=60.0)
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch of the dominant kernel, if captured")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        args.warmup = max(args.warmup, 0)
+        args.steps = min(args.steps, 20)  # bounded CPU sample (~2 s of work)
+        args.warmup = min(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl")
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, rank, world)
+        else:
+            run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1 and args.impl == "ours":
+            import torch.distributed as tdist
+            tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

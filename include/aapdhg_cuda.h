@@ -243,7 +243,13 @@ int aapdhg_cuda_filtered_aa_apply(aapdhg_handle* h, int32_t reduction,
                                   const double* g, double* out, int32_t* kept,
                                   char* err, size_t errlen);
 
-/* ---- instrumentation (bench / profiling) -------------------------------- */
+/* ---- streams & instrumentation (bench / profiling) ---------------------- */
+
+/* Makes the handle enqueue all its work on `stream` (a cudaStream_t owned by
+ * the caller, must not be the legacy default stream; NULL restores the
+ * handle's own stream). Lets a caller bracket a solve with its own CUDA
+ * events or order it after its own kernels. */
+int aapdhg_cuda_set_stream(aapdhg_handle* h, void* stream);
 
 /* Per-kernel device time accounting, measured with CUDA events recorded on
  * the handle's own stream around each launch. Enabling it switches the

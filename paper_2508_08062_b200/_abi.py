@@ -143,6 +143,7 @@ def _declare_cuda(lib):
         "aapdhg_cuda_filtered_aa_apply": ([H, C.c_int32, C.c_int32, _dp, _dp, C.c_double,
                                            C.c_double, C.c_double, _dp, _dp, _dp, _dp, _ip]
                                           + E, C.c_int),
+        "aapdhg_cuda_set_stream": ([H, C.c_void_p], C.c_int),
         "aapdhg_cuda_set_profiling": ([H, C.c_int32], C.c_int),
         "aapdhg_cuda_kernel_times": ([H, C.c_char_p, C.c_size_t, _dp,
                                       C.POINTER(C.c_uint64), C.c_int32, _ip], C.c_int),
@@ -162,7 +163,8 @@ CUDA_SYMBOLS = (
     "aapdhg_cuda_problem_destroy", "aapdhg_cuda_problem_dims", "aapdhg_cuda_solve",
     "aapdhg_cuda_select_step_sizes", "aapdhg_cuda_power_norm", "aapdhg_cuda_matvec",
     "aapdhg_cuda_matvec_transpose", "aapdhg_cuda_pdhg_step", "aapdhg_cuda_kkt_metrics",
-    "aapdhg_cuda_aa_apply", "aapdhg_cuda_filtered_aa_apply", "aapdhg_cuda_set_profiling",
+    "aapdhg_cuda_aa_apply", "aapdhg_cuda_filtered_aa_apply", "aapdhg_cuda_set_stream",
+    "aapdhg_cuda_set_profiling",
     "aapdhg_cuda_kernel_times", "aapdhg_cuda_last_launch_count",
 )
 

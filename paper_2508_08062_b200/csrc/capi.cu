@@ -205,6 +205,14 @@ int aapdhg_cuda_filtered_aa_apply(aapdhg_handle* h, int32_t reduction, int32_t p
   });
 }
 
+int aapdhg_cuda_set_stream(aapdhg_handle* h, void* stream) {
+  if (!h) return AAPDHG_ERR_INPUT;
+  return guard(nullptr, 0, [&] {
+    h->prob->set_stream(static_cast<cudaStream_t>(stream));
+    return AAPDHG_OK;
+  });
+}
+
 int aapdhg_cuda_set_profiling(aapdhg_handle* h, int32_t enable) {
   if (!h) return AAPDHG_ERR_INPUT;
   h->prob->set_profiling(enable != 0);

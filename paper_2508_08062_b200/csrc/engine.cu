@@ -127,7 +127,8 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   AAPDHG_CUDA(cudaGetDeviceProperties(&prop, device));
   if (prop.major < 10)
     throw CudaError(std::string("device ") + prop.name + " is not sm_100 class");
-  AAPDHG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  AAPDHG_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+  stream_ = own_stream_;
 
   n_ = k.ncols;
   m_ = k.nrows;
@@ -213,7 +214,15 @@ Problem::~Problem() {
     cudaEventDestroy(p.b);
   }
   if (h_state_) cudaFreeHost(h_state_);
-  if (stream_) cudaStreamDestroy(stream_);
+  if (own_stream_) cudaStreamDestroy(own_stream_);
+}
+
+void Problem::set_stream(cudaStream_t s) {
+  AAPDHG_CUDA(cudaSetDevice(device_));
+  AAPDHG_CUDA(cudaStreamSynchronize(stream_));
+  stream_ = s ? s : own_stream_;
+  if (graph_exec_) {  // a graph is replayed on whatever stream; keep it
+  }
 }
 
 void Problem::sync() { AAPDHG_CUDA(cudaStreamSynchronize(stream_)); }

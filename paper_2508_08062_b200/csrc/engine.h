@@ -56,6 +56,7 @@ class Problem {
                int32_t* kept);
 
   void set_profiling(bool on) { profiling_ = on; }
+  void set_stream(cudaStream_t s);
   const std::map<std::string, KernelStat>& kernel_stats() const { return stats_; }
   uint64_t last_launches() const { return last_launches_; }
   uint64_t last_loop_iters() const { return last_loop_iters_; }
@@ -86,6 +87,7 @@ class Problem {
 
   int device_;
   cudaStream_t stream_ = nullptr;
+  cudaStream_t own_stream_ = nullptr;
   int n_ = 0, m_ = 0, m1_ = 0;
   int64_t nnz_ = 0, N_ = 0;
   bool all_zero_ = true;

