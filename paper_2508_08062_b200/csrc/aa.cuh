@@ -1,515 +1,13 @@
-// kernels.cuh — sm_100a kernels of the AA-PDHG / FAA-PDHG iteration.
-//
-// One solver iteration (evaluated at the current iterate u_k = (x, y)):
-//   k_dual_side    K'y row-block SpMV fused with the primal step
-//                  xhat = P_X(x - tau (c - K'y)) and the dual-side KKT terms
-//                  of u_k (lambda, bound terms, ||c - K'y - lambda||^2, c'x)
-//                  plus the x-half of the history push (du, dg, g)
-//                  — pdhg_core.cpp:49-53 + solver.cpp:67-88,102-107 + solver.cpp:204-209
-//   k_primal_side  K xhat row-block SpMV fused with the dual step
-//                  yhat = P_Y(y + sigma (q - (2 K xhat - K x))) and the
-//                  primal-side KKT terms of u_k, plus the y-half of the push
-//                  — pdhg_core.cpp:55-60 + solver.cpp:90-100
-//   k_serial_reduce (SERIAL mode) all norms / dots as index-ordered chains
-//   k_control      termination, records, memory push commit, safeguard
-//                  — solver.cpp:188-215,241-247
-//   k_*_dots, k_aa_solve, k_mix, k_spmv(cand) — the AA / FAA step
-//                  (anderson.cpp:106-135, filtering.cpp:140-181)
-//   k_commit       role rotation u_prev <- u, u <- u_next (solver.cpp:249-251)
-//
-// SpMV: CSR rows are grouped into row blocks of <= kTile nonzeros (host
-// schedule). A CTA streams its block's (col, val) pairs coalesced, gathers
-// x[col], stages the products v*x in shared memory, then each thread sums
-// one row's products sequentially in CSR order — bit-identical to the
-// reference's row-serial matvec (sparse_linalg.cpp:60-69) and, on the
-// transposed CSR (entries in ascending original row), to its row-ordered
-// scatter matvec_transpose (sparse_linalg.cpp:77-87). Rows longer than
-// kTile get a CTA of their own that walks them in kTile chunks.
+// aa.cuh — AA / FAA step kernels, role rotation, setup and power-iteration
+// helpers of the sm_100a solver (see pipeline.cuh for the iteration core).
 #pragma once
 
-#include "common.cuh"
+#include "pipeline.cuh"
 
 namespace aapdhg_b200 {
 
 // ---------------------------------------------------------------------------
-// reductions
-// ---------------------------------------------------------------------------
-
-// Fixed-shape block sum (warp xor tree, then warps in order); result valid in
-// thread 0. Deterministic: the association never depends on timing.
-template <int NV>
-__device__ __forceinline__ void block_sum(double (&v)[NV], double* red) {
-#pragma unroll
-  for (int q = 0; q < NV; ++q)
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int W = kThreads / 32;
-  if (lane == 0)
-#pragma unroll
-    for (int q = 0; q < NV; ++q) red[q * W + warp] = v[q];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      double s = red[q * W];
-#pragma unroll
-      for (int w = 1; w < W; ++w) s += red[q * W + w];
-      v[q] = s;
-    }
-  }
-  __syncthreads();
-}
-
-// Block-wide sum of a strided sequence (fixed order); any blockDim multiple
-// of 32 up to 1024. Result returned to all threads.
-__device__ __forceinline__ double block_sum_dyn(double v, double* red32) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  __syncthreads();
-  if (lane == 0) red32[warp] = v;
-  __syncthreads();
-  double s = red32[0];
-  for (int w = 1; w < nw; ++w) s += red32[w];
-  return s;
-}
-
-// Index-ordered serial sums: the reference's vec.hpp:16-29 loops.
-__device__ __forceinline__ double serial_dot(const double* __restrict__ a,
-                                             const double* __restrict__ b, int64_t n) {
-  double s = 0.0;
-  int64_t i = 0;
-  for (; i + 8 <= n; i += 8) {
-    double p[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) p[u] = __dmul_rn(a[i + u], b[i + u]);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, p[u]);
-  }
-  for (; i < n; ++i) s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
-  return s;
-}
-
-// ---------------------------------------------------------------------------
-// row-block SpMV core
-// ---------------------------------------------------------------------------
-
-// prod[t] = vals[e0+t] * x[col[e0+t]], t < cnt. Matrix streams are read with
-// the evict-first (.cs) hint so the gathered vectors stay L2-resident.
-__device__ __forceinline__ void stage_products(const CsrDev& A, const double* __restrict__ x,
-                                               int64_t e0, int cnt, double* prod) {
-  int t = threadIdx.x;
-  for (; t + 7 * kThreads < cnt; t += 8 * kThreads) {
-    int c[8];
-    double a[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      c[u] = __ldcs(A.ci + e0 + t + u * kThreads);
-      a[u] = __ldcs(A.v + e0 + t + u * kThreads);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) prod[t + u * kThreads] = __dmul_rn(a[u], __ldg(x + c[u]));
-  }
-  for (; t < cnt; t += kThreads)
-    prod[t] = __dmul_rn(__ldcs(A.v + e0 + t), __ldg(x + __ldcs(A.ci + e0 + t)));
-}
-
-// Sum of one CSR row of any length handled by a whole CTA (kTile chunks).
-// SERIAL: thread 0 adds the products in CSR order (bitwise = reference);
-// else per-chunk fixed block tree, chunks added in order. Valid in thread 0.
-template <bool SERIAL>
-__device__ double long_row_sum(const CsrDev& A, const double* __restrict__ x, int64_t e0,
-                               int64_t e1, double* prod, double* red) {
-  double s = 0.0;
-  for (int64_t c0 = e0; c0 < e1; c0 += kTile) {
-    const int cnt = (int)((e1 - c0) < kTile ? (e1 - c0) : kTile);
-    stage_products(A, x, c0, cnt, prod);
-    __syncthreads();
-    if (SERIAL) {
-      if (threadIdx.x == 0)
-        for (int t = 0; t < cnt; ++t) s = __dadd_rn(s, prod[t]);
-    } else {
-      double v[1] = {0.0};
-      for (int t = threadIdx.x; t < cnt; t += kThreads) v[0] = __dadd_rn(v[0], prod[t]);
-      block_sum<1>(v, red);
-      if (threadIdx.x == 0) s = __dadd_rn(s, v[0]);
-    }
-    __syncthreads();
-  }
-  return s;
-}
-
-// Computes the row sum owned by this thread for row block `b`.
-// Returns the row index (or -1 when the thread owns no row).
-template <bool SERIAL>
-__device__ __forceinline__ int block_rows(const CsrDev& A, const double* __restrict__ x, int b,
-                                          double* prod, double* red, double& out) {
-  const int r0 = A.blk[b], r1 = A.blk[b + 1];
-  const int64_t e0 = A.rp[r0], e1 = A.rp[r1];
-  if (r1 - r0 == 1 && e1 - e0 > kTile) {
-    out = long_row_sum<SERIAL>(A, x, e0, e1, prod, red);
-    return threadIdx.x == 0 ? r0 : -1;
-  }
-  stage_products(A, x, e0, (int)(e1 - e0), prod);
-  __syncthreads();
-  int row = -1;
-  out = 0.0;
-  if ((int)threadIdx.x < r1 - r0) {
-    row = r0 + threadIdx.x;
-    const int a = (int)(A.rp[row] - e0), z = (int)(A.rp[row + 1] - e0);
-    double s = 0.0;
-    for (int e = a; e < z; ++e) s = __dadd_rn(s, prod[e]);
-    out = s;
-  }
-  return row;
-}
-
-// out[r] = (A x)_r. Plain SpMV (power iteration, K x recache, per-op matvec).
-// `x_role`/`out_*` resolve device-side roles when `S` is given.
-struct SpmvArgs {
-  const double* x;       // used when x_pool == nullptr
-  double* out;           // used when out_pool == nullptr
-  const double* x_pool;  // upool base: x = x_pool + u_idx[x_role]*N
-  double* out_pool;      // kxpool base: out = out_pool + kx_idx[out_role]*m
-  int32_t x_role, out_role;
-  int64_t x_stride, out_stride;
-  int32_t pred_aa_ok;    // run only when S->aa_ok
-  const int32_t* stop;   // optional: skip when *stop != 0 (power iteration)
-};
-
-template <bool SERIAL>
-__global__ void __launch_bounds__(kThreads) k_spmv(CsrDev A, SpmvArgs g, const DevState* S) {
-  if (S) {
-    if (S->done) return;
-    if (g.pred_aa_ok && !S->aa_ok) return;
-  }
-  if (g.stop && *g.stop) return;
-  __shared__ double prod[kTile];
-  __shared__ double red[kThreads / 32];
-  const double* x = g.x_pool ? g.x_pool + (int64_t)S->u_idx[g.x_role] * g.x_stride : g.x;
-  double* out = g.out_pool ? g.out_pool + (int64_t)S->kx_idx[g.out_role] * g.out_stride : g.out;
-  double s;
-  const int row = block_rows<SERIAL>(A, x, blockIdx.x, prod, red, s);
-  if (row >= 0) out[row] = s;
-}
-
-// ---------------------------------------------------------------------------
-// the fused PDHG halves
-// ---------------------------------------------------------------------------
-
-struct IterBufs {
-  double* upool;   // 4 x N
-  double* kxpool;  // 3 x m
-  double* gpool;   // 2 x N
-  double* du;      // cap x N
-  double* dg;      // cap x N
-  double* T;       // n
-  double* part1;   // P1_COUNT x nblk1
-  double* part2;   // P2_COUNT x nblk2
-  const double* c;
-  const double* q;
-  const double* l;
-  const double* u;
-};
-
-// K1: t = (K'y)_j for the row block of K' (= columns j of K), then
-//   xhat_j = min(max(x_j - tau (c_j - t), l_j), u_j)      pdhg_core.cpp:49-53
-//   lambda_j = P_Lambda(c_j - t)                           solver.cpp:67-71
-//   partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
-//   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
-template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kThreads)
-    k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, const DevState* S) {
-  if (S->done) return;
-  __shared__ double prod[kTile];
-  __shared__ double red[P1_COUNT * (kThreads / 32)];
-  const int64_t N = P->N;
-  const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-  const double* y = x + P->n;
-  double t;
-  const int j = block_rows<SERIAL>(KT, y, blockIdx.x, prod, red, t);
-  double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
-  if (j >= 0) {
-    double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-    const double xj = x[j], cj = B.c[j], lj = B.l[j], uj = B.u[j];
-    double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));
-    xn = smin(smax(xn, lj), uj);
-    xh[j] = xn;
-    const double d = __dsub_rn(xn, xj);
-    const double red_c = __dsub_rn(cj, t);
-    const double lam = project_lambda1(red_c, lj, uj);
-    double bt = 0.0;
-    if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
-    if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
-    const double dv = __dsub_rn(red_c, lam);
-    acc[P1_GX2] = __dmul_rn(d, d);
-    acc[P1_BOUND] = bt;
-    acc[P1_DUALSQ] = __dmul_rn(dv, dv);
-    acc[P1_CX] = __dmul_rn(cj, xj);
-    if (PUSH) {
-      const int64_t slot = S->push_slot;
-      const double xp = B.upool[(int64_t)S->u_idx[U_PREV] * N + j];
-      const double gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + j];
-      B.du[slot * N + j] = __dsub_rn(xj, xp);
-      B.dg[slot * N + j] = __dsub_rn(d, gp);
-      B.gpool[(int64_t)S->g_idx[G_CUR] * N + j] = d;
-    }
-    if (SERIAL) B.T[j] = t;
-  }
-  if (!SERIAL) {
-    block_sum<P1_COUNT>(acc, red);
-    if (threadIdx.x == 0)
-#pragma unroll
-      for (int q = 0; q < P1_COUNT; ++q) B.part1[q * P->nblk1 + blockIdx.x] = acc[q];
-  }
-}
-
-// K2: s = (K xhat)_i, then
-//   yhat_i = y_i + sigma (q_i - (2 s - (K x)_i)), clamped >= 0 for i < m1
-//                                                         pdhg_core.cpp:55-60
-//   K xhat cached as the next K x (solver.cpp:90 / pdhg_core.cpp:56)
-//   partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
-template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kThreads)
-    k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, const DevState* S) {
-  if (S->done) return;
-  __shared__ double prod[kTile];
-  __shared__ double red[P2_COUNT * (kThreads / 32)];
-  const int64_t N = P->N;
-  const int n = P->n, mr = P->mrows;
-  const double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-  double s;
-  const int i = block_rows<SERIAL>(K, xh, blockIdx.x, prod, red, s);
-  double acc[P2_COUNT] = {0.0, 0.0, 0.0};
-  if (i >= 0) {
-    const double* u = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-    double* uh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-    const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
-    double* kxh = B.kxpool + (int64_t)S->kx_idx[KX_HAT] * mr;
-    const double yi = u[n + i], qi = B.q[i], kxi = kx[i];
-    double yn = __dadd_rn(yi, __dmul_rn(P->sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
-    if (i < P->m1) yn = smax(yn, 0.0);
-    uh[n + i] = yn;
-    kxh[i] = s;
-    const double d = __dsub_rn(yn, yi);
-    double v = __dsub_rn(qi, kxi);
-    if (i < P->m1) v = smax(v, 0.0);
-    acc[P2_GY2] = __dmul_rn(d, d);
-    acc[P2_QY] = __dmul_rn(qi, yi);
-    acc[P2_INFEAS] = __dmul_rn(v, v);
-    if (PUSH) {
-      const int64_t slot = S->push_slot;
-      const double yp = B.upool[(int64_t)S->u_idx[U_PREV] * N + n + i];
-      const double gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + n + i];
-      B.du[slot * N + n + i] = __dsub_rn(yi, yp);
-      B.dg[slot * N + n + i] = __dsub_rn(d, gp);
-      B.gpool[(int64_t)S->g_idx[G_CUR] * N + n + i] = d;
-    }
-  }
-  if (!SERIAL) {
-    block_sum<P2_COUNT>(acc, red);
-    if (threadIdx.x == 0)
-#pragma unroll
-      for (int q = 0; q < P2_COUNT; ++q) B.part2[q * P->nblk2 + blockIdx.x] = acc[q];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// SERIAL mode: every scalar reduction as one index-ordered chain
-// (fixed_point_residual pdhg_core.cpp:65-74; kkt_metrics solver.cpp:64-110)
-// One warp per chain, lane 0 sums; chain w -> S->sres[w].
-// ---------------------------------------------------------------------------
-__global__ void k_serial_reduce(IterBufs B, const DevParams* __restrict__ P, DevState* S,
-                                int with_g2) {
-  if (S->done) return;
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) != 0 || w >= S_COUNT) return;
-  if (w == S_G2 && !with_g2) return;
-  const int64_t N = P->N;
-  const int n = P->n, mr = P->mrows, m1 = P->m1;
-  const double* u = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-  const double* uh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-  const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
-  const double* T = B.T;
-  double s = 0.0;
-  switch (w) {
-    case S_G2: {
-      int64_t i = 0;
-      for (; i + 8 <= N; i += 8) {
-        double p[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const double d = __dsub_rn(uh[i + k], u[i + k]);
-          p[k] = __dmul_rn(d, d);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) s = __dadd_rn(s, p[k]);
-      }
-      for (; i < N; ++i) {
-        const double d = __dsub_rn(uh[i], u[i]);
-        s = __dadd_rn(s, __dmul_rn(d, d));
-      }
-      break;
-    }
-    case S_BOUND:
-      for (int j = 0; j < n; ++j) {
-        const double lj = B.l[j], uj = B.u[j];
-        const double lam = project_lambda1(__dsub_rn(B.c[j], T[j]), lj, uj);
-        if (isfinite(lj) && lam > 0.0) s = __dadd_rn(s, __dmul_rn(lj, lam));
-        if (isfinite(uj) && lam < 0.0) s = __dadd_rn(s, __dmul_rn(uj, lam));
-      }
-      break;
-    case S_QY: s = serial_dot(B.q, u + n, mr); break;
-    case S_CX: s = serial_dot(B.c, u, n); break;
-    case S_INFEAS: {
-      for (int i = 0; i < mr; ++i) {
-        double v = __dsub_rn(B.q[i], kx[i]);
-        if (i < m1) v = smax(v, 0.0);
-        s = __dadd_rn(s, __dmul_rn(v, v));
-      }
-      break;
-    }
-    case S_DUALSQ:
-      for (int j = 0; j < n; ++j) {
-        const double rc = __dsub_rn(B.c[j], T[j]);
-        const double v = __dsub_rn(rc, project_lambda1(rc, B.l[j], B.u[j]));
-        s = __dadd_rn(s, __dmul_rn(v, v));
-      }
-      break;
-  }
-  S->sres[w] = s;
-}
-
-// KKT scalars of the CUR iterate from the reduced sums (solver.cpp:83-107).
-__device__ __forceinline__ void kkt_from_sums(const DevParams* P, double bound, double qy,
-                                              double cx, double infeas, double dual_sq,
-                                              double* kkt) {
-  const double dual_core = __dadd_rn(qy, bound);
-  const double primal_obj = cx;
-  kkt[0] = fabs(__dsub_rn(dual_core, primal_obj)) /
-           __dadd_rn(__dadd_rn(1.0, fabs(dual_core)), fabs(primal_obj));
-  kkt[1] = sqrt(infeas) / __dadd_rn(1.0, P->nrm_q);
-  kkt[2] = sqrt(dual_sq) / __dadd_rn(1.0, P->nrm_c);
-  kkt[3] = primal_obj;
-}
-
-// Thread-strided sum of part[0..nb) then fixed block tree (kCtrlThreads).
-__device__ __forceinline__ double reduce_partials(const double* part, int nb, double* red32) {
-  double s = 0.0;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) s = __dadd_rn(s, part[b]);
-  return block_sum_dyn(s, red32);
-}
-
-__device__ __forceinline__ void finish_solve(DevState* S, int status, int role, double g) {
-  S->status = status;
-  S->final_role = role;
-  S->g_final = g;
-  S->done = 1;
-}
-
-// ---------------------------------------------------------------------------
-// control: solver.cpp:188-215 + record bookkeeping (solver.cpp:138-151,241-247)
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kCtrlThreads)
-    k_control(IterBufs B, const DevParams* __restrict__ P, DevState* S) {
-  if (S->done) return;
-  __shared__ double red32[32];
-  double sums[7];
-  if (!P->serial) {
-    sums[0] = reduce_partials(B.part1 + P1_GX2 * P->nblk1, P->nblk1, red32);
-    sums[1] = reduce_partials(B.part2 + P2_GY2 * P->nblk2, P->nblk2, red32);
-    sums[2] = reduce_partials(B.part1 + P1_BOUND * P->nblk1, P->nblk1, red32);
-    sums[3] = reduce_partials(B.part2 + P2_QY * P->nblk2, P->nblk2, red32);
-    sums[4] = reduce_partials(B.part1 + P1_CX * P->nblk1, P->nblk1, red32);
-    sums[5] = reduce_partials(B.part2 + P2_INFEAS * P->nblk2, P->nblk2, red32);
-    sums[6] = reduce_partials(B.part1 + P1_DUALSQ * P->nblk1, P->nblk1, red32);
-  }
-  if (threadIdx.x != 0) return;
-  double g2, bound, qy, cx, infeas, dual_sq;
-  if (P->serial) {
-    g2 = S->sres[S_G2];
-    bound = S->sres[S_BOUND];
-    qy = S->sres[S_QY];
-    cx = S->sres[S_CX];
-    infeas = S->sres[S_INFEAS];
-    dual_sq = S->sres[S_DUALSQ];
-  } else {
-    g2 = __dadd_rn(sums[0], sums[1]);
-    bound = sums[2];
-    qy = sums[3];
-    cx = sums[4];
-    infeas = sums[5];
-    dual_sq = sums[6];
-  }
-  double kkt[4];
-  kkt_from_sums(P, bound, qy, cx, infeas, dual_sq, kkt);
-  for (int q = 0; q < 4; ++q) S->kkt[q] = kkt[q];
-  const double gkn = sqrt(g2);
-  S->gkn = gkn;
-  S->aa_attempt = 0;
-  S->aa_ok = 0;
-  const uint64_t k = S->k;
-  const double elapsed = (double)(globaltimer_ns() - S->t0_ns) * 1e-9 + P->wall_offset_s;
-  if (k == 0) {  // priming step, solver.cpp:168-172
-    S->g0n = gkn;
-    aapdhg_record* r = P->rec;
-    r->k = 0;
-    r->g_norm = gkn;
-    r->aa_step = 0;
-    r->i = 0;
-    r->j = 0;
-    return;
-  }
-  // the record of iterate k-1 takes the KKT of the produced iterate u_k
-  {
-    aapdhg_record* r = P->rec + (k - 1) % P->rec_cap;
-    r->r_gap = kkt[0];
-    r->r_primal = kkt[1];
-    r->r_dual = kkt[2];
-    r->objective = kkt[3];
-    r->elapsed_s = elapsed;
-    S->rec_complete = k;
-  }
-  const double kmax = smax(smax(kkt[0], kkt[1]), kkt[2]);
-  if (k == 1 && S->g0n == 0.0) { finish_solve(S, AAPDHG_SOLVE_FIXED_POINT_START, U_PREV, 0.0); return; }
-  if (P->kkt_terminate && kmax <= P->kkt_eps) { finish_solve(S, AAPDHG_SOLVE_KKT_TOL, U_CUR, gkn); return; }
-  if (gkn < P->toll) { finish_solve(S, AAPDHG_SOLVE_RESIDUAL_TOL, U_CUR, gkn); return; }
-  if (S->i + S->j >= P->max_iters) { finish_solve(S, AAPDHG_SOLVE_MAX_ITERS, U_CUR, gkn); return; }
-  if (elapsed >= P->max_wall_s) { finish_solve(S, AAPDHG_SOLVE_TIMEOUT, U_CUR, gkn); return; }
-
-  if (P->method != AAPDHG_METHOD_PDHG) {  // memory_push / FaaState::push
-    if (S->mem_size == P->cap) {
-      for (int t = 1; t < S->mem_size; ++t) S->mem_slots[t - 1] = S->mem_slots[t];
-      S->mem_slots[S->mem_size - 1] = S->push_slot;
-    } else {
-      S->mem_slots[S->mem_size++] = S->push_slot;
-    }
-  }
-  aapdhg_record* r = P->rec + k % P->rec_cap;
-  r->k = k;
-  r->g_norm = gkn;
-  r->aa_step = 0;
-  r->i = S->i;
-  r->j = S->j;
-  bool pass = false;
-  if (P->method != AAPDHG_METHOD_PDHG) {
-    // safeguard_pass, solver.cpp:59-62, with the host-computed pow table
-    const double pw = S->i < P->pow_len ? P->pow_tab[S->i]
-                                        : pow((double)S->i + 1.0, -(1.0 + P->safeguard_eps));
-    pass = gkn <= __dmul_rn(__dmul_rn(P->safeguard_d, S->g0n), pw);
-  }
-  if (pass) {
-    S->aa_attempt = 1;
-  } else {
-    S->j += 1;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // AA / FAA: dots over the memory columns
-// item list: [pairs (a<=b) of f/dg columns][rhs f_a . g][FAA: |e_a|^2]
-// ---------------------------------------------------------------------------
 __device__ __forceinline__ int num_items(int p, int method) {
   return p * (p + 1) / 2 + p + (method == AAPDHG_METHOD_FAA ? p : 0);
 }
@@ -851,7 +349,10 @@ __global__ void __launch_bounds__(kThreads)
 
 // role rotation at the end of an iteration (solver.cpp:249-251) + next push slot
 __global__ void k_commit(const DevParams* __restrict__ P, DevState* S) {
-  if (S->done) return;
+  if (S->done) {
+    if (P->use_cond) cudaGraphSetConditional(P->cond_loop, 0u);
+    return;
+  }
   int* U = S->u_idx;
   int* KX = S->kx_idx;
   const int old_prev = U[U_PREV];
@@ -890,6 +391,11 @@ __global__ void k_commit(const DevParams* __restrict__ P, DevState* S) {
   S->aa_ok = 0;
   S->k += 1;
   S->loop_iters += 1;
+  // WHILE node of the graph batch: keep going while work is left
+  if (P->use_cond) {
+    const int left = --S->batch_left;
+    cudaGraphSetConditional(P->cond_loop, left > 0 ? 1u : 0u);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -969,10 +475,7 @@ __global__ void __launch_bounds__(kCtrlThreads)
     s[3] = serial_dot(q, y, mr);
     s[4] = infeas;
   }
-  DevParams P;
-  P.nrm_q = nrm_q;
-  P.nrm_c = nrm_c;
-  kkt_from_sums(&P, s[0], s[3], s[2], s[4], s[1], out);
+  kkt_from_sums(nrm_q, nrm_c, s[0], s[3], s[2], s[4], s[1], out);
 }
 
 // sum of squares: tree partials per CTA (grid-stride, fixed)

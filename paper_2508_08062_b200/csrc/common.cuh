@@ -23,8 +23,8 @@
 namespace aapdhg_b200 {
 
 constexpr int kThreads = 256;        // CTA size of the tile kernels
-constexpr int kTile = 2048;          // nnz staged per CTA (8 per thread)
-constexpr int kMaxRowsPerBlock = kThreads;
+constexpr int kWarps = kThreads / 32;
+constexpr int kWarpTile = 256;       // nnz staged per warp tile (8 per lane)
 constexpr int kMaxMemory = 64;       // largest AA memory capacity supported
 constexpr int kDotChunk = 512;       // elements per CTA in the tree multi-dot
 constexpr int kCtrlThreads = 256;
@@ -46,8 +46,9 @@ struct CsrDev {
   const int32_t* rp = nullptr;
   const int32_t* ci = nullptr;
   const double* v = nullptr;
-  int32_t nblocks = 0;
-  const int32_t* blk = nullptr;  // nblocks + 1 row boundaries
+  int32_t ntiles = 0;
+  const int32_t* tile = nullptr;  // ntiles + 1 row boundaries (warp tiles)
+  int32_t grid() const { return (ntiles + kWarps - 1) / kWarps; }
 };
 
 // Constant per solve (written before the loop starts).
@@ -66,7 +67,9 @@ struct DevParams {
   uint64_t pow_len;
   aapdhg_record* rec;     // ring of rec_cap records
   uint64_t rec_cap;
-  int32_t nblk1, nblk2, ndot_blk, pad;
+  int32_t nblk1, nblk2, ndot_blk, use_cond;
+  cudaGraphConditionalHandle cond_aa;    // IF node of the AA branch
+  cudaGraphConditionalHandle cond_loop;  // WHILE node of the iteration batch
 };
 
 // Mutable solver state, device resident; the host reads it at polls.
@@ -86,6 +89,8 @@ struct DevState {
   double sres[8];                  // serial chain results
   uint64_t t0_ns;
   uint64_t loop_iters;             // iterations that did work (launch accounting)
+  uint32_t ticket;                 // last-CTA election in k_primal_side
+  int32_t batch_left;              // iterations left in this graph launch
 };
 
 struct CudaError : std::runtime_error {

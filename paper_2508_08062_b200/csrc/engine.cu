@@ -14,7 +14,8 @@
 #include <random>
 
 #include "engine.h"
-#include "kernels.cuh"
+#include "aa.cuh"
+#include "pipeline.cuh"
 
 namespace aapdhg_b200 {
 
@@ -25,31 +26,30 @@ double secs(Clock::time_point t0) {
   return std::chrono::duration<double>(Clock::now() - t0).count();
 }
 
-constexpr int kGraphIters = 8;        // iterations per captured graph
-constexpr int kMaxBatchGraphs = 64;   // graph launches between polls (max)
+constexpr uint64_t kMaxBatch = 4096;  // iterations per graph launch (max)
 constexpr uint64_t kRecCap = 1 << 16;  // device record ring
 constexpr uint64_t kPowTabMax = 1 << 22;
 constexpr int kPowerBatch = 8;
 
-// Row blocks: consecutive rows with <= kTile nonzeros and <= kMaxRowsPerBlock
-// rows; a row longer than kTile forms a block of its own.
-std::vector<int32_t> build_blocks(const int32_t* rp, int nrows) {
-  std::vector<int32_t> blk{0};
+// Warp tiles: consecutive rows, at most 32 rows and kWarpTile nonzeros;
+// a row longer than kWarpTile forms a tile of its own.
+std::vector<int32_t> build_tiles(const int32_t* rp, int nrows) {
+  std::vector<int32_t> t{0};
   int r = 0;
   while (r < nrows) {
     const int start = r;
-    if (rp[r + 1] - rp[r] > kTile) {
+    if (rp[r + 1] - rp[r] > kWarpTile) {
       ++r;
     } else {
       int64_t nz = 0;
-      while (r < nrows && r - start < kMaxRowsPerBlock && nz + (rp[r + 1] - rp[r]) <= kTile) {
+      while (r < nrows && r - start < 32 && nz + (rp[r + 1] - rp[r]) <= kWarpTile) {
         nz += rp[r + 1] - rp[r];
         ++r;
       }
     }
-    blk.push_back(r);
+    t.push_back(r);
   }
-  return blk;
+  return t;
 }
 
 int num_items_host(int p, int method) {
@@ -138,17 +138,17 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   for (int64_t e = 0; e < nnz_ && all_zero_; ++e) all_zero_ = k.vals[e] == 0.0;
 
   // K and its row blocks
-  const std::vector<int32_t> kb = build_blocks(k.row_ptr, m_);
+  const std::vector<int32_t> kb = build_tiles(k.row_ptr, m_);
   k_rp_.reserve(sizeof(int32_t) * (m_ + 1));
   k_ci_.reserve(sizeof(int32_t) * nnz_);
   k_v_.reserve(sizeof(double) * nnz_);
-  k_blk_.reserve(sizeof(int32_t) * kb.size());
+  k_tile_.reserve(sizeof(int32_t) * kb.size());
   h2d(k_rp_.p, k.row_ptr, sizeof(int32_t) * (m_ + 1), stream_);
   h2d(k_ci_.p, k.col_idx, sizeof(int32_t) * nnz_, stream_);
   h2d(k_v_.p, k.vals, sizeof(double) * nnz_, stream_);
-  h2d(k_blk_.p, kb.data(), sizeof(int32_t) * kb.size(), stream_);
+  h2d(k_tile_.p, kb.data(), sizeof(int32_t) * kb.size(), stream_);
   K_ = CsrDev{m_, n_, nnz_, k_rp_.as<int32_t>(), k_ci_.as<int32_t>(), k_v_.as<double>(),
-              int32_t(kb.size() - 1), k_blk_.as<int32_t>()};
+              int32_t(kb.size() - 1), k_tile_.as<int32_t>()};
 
   // K' as CSR, entries of each row in ascending original row (counting sort)
   std::vector<int32_t> trp(static_cast<size_t>(n_) + 1, 0), tci(static_cast<size_t>(nnz_));
@@ -164,17 +164,17 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
         tv[size_t(pos)] = k.vals[e];
       }
   }
-  const std::vector<int32_t> tb = build_blocks(trp.data(), n_);
+  const std::vector<int32_t> tb = build_tiles(trp.data(), n_);
   t_rp_.reserve(sizeof(int32_t) * (n_ + 1));
   t_ci_.reserve(sizeof(int32_t) * nnz_);
   t_v_.reserve(sizeof(double) * nnz_);
-  t_blk_.reserve(sizeof(int32_t) * tb.size());
+  t_tile_.reserve(sizeof(int32_t) * tb.size());
   h2d(t_rp_.p, trp.data(), sizeof(int32_t) * (n_ + 1), stream_);
   h2d(t_ci_.p, tci.data(), sizeof(int32_t) * nnz_, stream_);
   h2d(t_v_.p, tv.data(), sizeof(double) * nnz_, stream_);
-  h2d(t_blk_.p, tb.data(), sizeof(int32_t) * tb.size(), stream_);
+  h2d(t_tile_.p, tb.data(), sizeof(int32_t) * tb.size(), stream_);
   KT_ = CsrDev{n_, m_, nnz_, t_rp_.as<int32_t>(), t_ci_.as<int32_t>(), t_v_.as<double>(),
-               int32_t(tb.size() - 1), t_blk_.as<int32_t>()};
+               int32_t(tb.size() - 1), t_tile_.as<int32_t>()};
 
   c_.reserve(sizeof(double) * n_);
   q_.reserve(sizeof(double) * m_);
@@ -198,6 +198,7 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   const int64_t nbig = std::max<int64_t>(std::max<int64_t>(n_, m_), 1);
   part_small_.reserve(sizeof(double) * 5 * (nbig / kThreads + 2));
   AAPDHG_CUDA(cudaMallocHost(&h_state_, sizeof(DevState)));
+  AAPDHG_CUDA(cudaMallocHost(&h_batch_, sizeof(int32_t)));
 
   // ||q|| and ||c|| under both reduction orders (constants of kkt_metrics)
   for (int serial = 0; serial < 2; ++serial) {
@@ -214,6 +215,7 @@ Problem::~Problem() {
     cudaEventDestroy(p.b);
   }
   if (h_state_) cudaFreeHost(h_state_);
+  if (h_batch_) cudaFreeHost(h_batch_);
   if (own_stream_) cudaStreamDestroy(own_stream_);
 }
 
@@ -229,6 +231,7 @@ void Problem::sync() { AAPDHG_CUDA(cudaStreamSynchronize(stream_)); }
 
 bool Problem::resolve_serial(int reduction) const {
   if (reduction == AAPDHG_REDUCE_SERIAL) return true;
+  if (m_ == 0 || n_ == 0) return true;  // TREE control rides on the K xhat kernel
   if (reduction == AAPDHG_REDUCE_TREE) return false;
   return N_ <= 65536;
 }
@@ -248,7 +251,7 @@ double Problem::device_dot(const double* a, const double* b, int64_t n, bool ser
 }
 
 void Problem::ensure_iter_buffers(int method, int cap) {
-  const int nblk1 = KT_.nblocks, nblk2 = K_.nblocks;
+  const int nblk1 = KT_.grid(), nblk2 = K_.grid();
   upool_.reserve(sizeof(double) * 4 * std::max<int64_t>(N_, 1));
   kxpool_.reserve(sizeof(double) * 3 * std::max<int64_t>(m_, 1));
   T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
@@ -261,13 +264,13 @@ void Problem::ensure_iter_buffers(int method, int cap) {
   rec_cap_ = kRecCap;
   dparams_.reserve(sizeof(DevParams));
   dstate_.reserve(sizeof(DevState));
-  ndot_blk_ = int((N_ + kDotChunk - 1) / kDotChunk);
+  ndot_tile_ = int((N_ + kDotChunk - 1) / kDotChunk);
   if (method != AAPDHG_METHOD_PDHG) {
     gpool_.reserve(sizeof(double) * 2 * std::max<int64_t>(N_, 1));
     du_.reserve(sizeof(double) * size_t(cap) * std::max<int64_t>(N_, 1));
     dg_.reserve(sizeof(double) * size_t(cap) * std::max<int64_t>(N_, 1));
     const int items = num_items_host(cap, AAPDHG_METHOD_FAA);
-    partdot_.reserve(sizeof(double) * size_t(items) * std::max(ndot_blk_, 1));
+    partdot_.reserve(sizeof(double) * size_t(items) * std::max(ndot_tile_, 1));
   }
 }
 
@@ -286,17 +289,17 @@ void Problem::kkt_eval(int slot, bool serial, double* out_dev, double* lam_dev) 
   double* T = T_.as<double>();
   double* KX = pw_mx_.as<double>();
   SpmvArgs a{};
-  if (n_ && KT_.nblocks) {
+  if (n_ && KT_.ntiles) {
     a.x = y;
     a.out = T;
-    if (serial) k_spmv<true><<<KT_.nblocks, kThreads, 0, stream_>>>(KT_, a, nullptr);
-    else k_spmv<false><<<KT_.nblocks, kThreads, 0, stream_>>>(KT_, a, nullptr);
+    if (serial) k_spmv<true><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, a, nullptr);
+    else k_spmv<false><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, a, nullptr);
   }
-  if (m_ && K_.nblocks) {
+  if (m_ && K_.ntiles) {
     a.x = x;
     a.out = KX;
-    if (serial) k_spmv<true><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
-    else k_spmv<false><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
+    if (serial) k_spmv<true><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
+    else k_spmv<false><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
   }
   const int64_t nbig = std::max<int64_t>(std::max<int64_t>(n_, m_), 1);
   const int nb = int((nbig + kThreads - 1) / kThreads);
@@ -360,8 +363,13 @@ void Problem::prof_collect() {
     ++nodes;                   \
   } while (0)
 
-// One solver iteration (solver.cpp:188-252) as a predicated kernel sequence.
-void Problem::launch_iteration(cudaStream_t s, const SolveSetup& su) {
+// One solver iteration (solver.cpp:188-252) as three kernel segments:
+//   core   K1, K2 (+ last-CTA control) or K1, K2, serial control
+//   aa     the AA / FAA candidate: dots, small solve, mix, K x recache
+//   commit role rotation and loop bookkeeping
+// Eagerly the aa kernels are predicated on device flags; under graph replay
+// they sit in an IF node the control sets, inside a WHILE node commit drives.
+int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   int nodes = 0;
   const bool ser = su.serial, push = su.push;
   if (su.nblk1 > 0) {
@@ -376,33 +384,98 @@ void Problem::launch_iteration(cudaStream_t s, const SolveSetup& su) {
     else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<su.nblk2, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
     else LAUNCH("k_primal_side", k_primal_side<false, false><<<su.nblk2, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
   }
-  if (ser) LAUNCH("k_serial_reduce", k_serial_reduce<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S, 1));
-  LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(su.B, su.P, su.S));
-  if (su.method != AAPDHG_METHOD_PDHG) {
-    if (ser) {
-      const int blocks = (su.items_max * 32 + kThreads - 1) / kThreads;
-      LAUNCH("k_serial_dots", k_serial_dots<<<blocks, kThreads, 0, s>>>(su.D, su.P, su.S));
-    } else {
-      LAUNCH("k_tree_dots", k_tree_dots<<<su.ndot_blk, kThreads, 0, s>>>(su.D, su.P, su.S));
-    }
-    LAUNCH("k_aa_solve", k_aa_solve<<<1, 1024, 0, s>>>(su.D, su.W, su.P, su.S, 0));
-    LAUNCH("k_mix", k_mix<<<grid_for(N_), kThreads, 0, s>>>(su.B, su.B.dg, su.P, su.S, 1));
-    if (K_.nblocks > 0) {
-      SpmvArgs a{};
-      a.x_pool = su.B.upool;
-      a.x_role = U_CAND;
-      a.x_stride = N_;
-      a.out_pool = su.B.kxpool;
-      a.out_role = KX_CAND;
-      a.out_stride = m_;
-      a.pred_aa_ok = 1;
-      if (ser) LAUNCH("k_spmv_recache", k_spmv<true><<<K_.nblocks, kThreads, 0, s>>>(K_, a, su.S));
-      else LAUNCH("k_spmv_recache", k_spmv<false><<<K_.nblocks, kThreads, 0, s>>>(K_, a, su.S));
-    }
-  }
-  LAUNCH("k_commit", k_commit<<<1, 1, 0, s>>>(su.P, su.S));
-  nodes_per_iter_ = nodes;
+  if (ser) LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
   AAPDHG_CUDA(cudaGetLastError());
+  return nodes;
+}
+
+int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
+  int nodes = 0;
+  if (su.method == AAPDHG_METHOD_PDHG) return 0;
+  if (su.serial) {
+    const int blocks = (su.items_max * 32 + kThreads - 1) / kThreads;
+    LAUNCH("k_serial_dots", k_serial_dots<<<blocks, kThreads, 0, s>>>(su.D, su.P, su.S));
+  } else {
+    LAUNCH("k_tree_dots", k_tree_dots<<<su.ndot_blk, kThreads, 0, s>>>(su.D, su.P, su.S));
+  }
+  LAUNCH("k_aa_solve", k_aa_solve<<<1, 1024, 0, s>>>(su.D, su.W, su.P, su.S, 0));
+  LAUNCH("k_mix", k_mix<<<grid_for(N_), kThreads, 0, s>>>(su.B, su.B.dg, su.P, su.S, 1));
+  if (K_.ntiles > 0) {
+    SpmvArgs a{};
+    a.x_pool = su.B.upool;
+    a.x_role = U_CAND;
+    a.x_stride = N_;
+    a.out_pool = su.B.kxpool;
+    a.out_role = KX_CAND;
+    a.out_stride = m_;
+    a.pred_aa_ok = 1;
+    if (su.serial) LAUNCH("k_spmv_recache", k_spmv<true><<<K_.grid(), kThreads, 0, s>>>(K_, a, su.S));
+    else LAUNCH("k_spmv_recache", k_spmv<false><<<K_.grid(), kThreads, 0, s>>>(K_, a, su.S));
+  }
+  AAPDHG_CUDA(cudaGetLastError());
+  return nodes;
+}
+
+int Problem::launch_commit(cudaStream_t s, const SolveSetup& su) {
+  int nodes = 0;
+  LAUNCH("k_commit", k_commit<<<1, 1, 0, s>>>(su.P, su.S));
+  AAPDHG_CUDA(cudaGetLastError());
+  return nodes;
+}
+
+void Problem::launch_iteration(cudaStream_t s, const SolveSetup& su) {
+  launch_core(s, su);
+  launch_aa(s, su);
+  launch_commit(s, su);
+}
+
+// WHILE(batch) { core; IF(aa_attempt) { aa }; commit } as one executable graph.
+void Problem::build_graph(const SolveSetup& su) {
+  const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
+  cudaStream_t s = stream_;
+  cudaGraph_t g;
+  AAPDHG_CUDA(cudaGraphCreate(&g, 0));
+  AAPDHG_CUDA(cudaGraphConditionalHandleCreate(&cond_loop_, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams wp{};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = cond_loop_;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  AAPDHG_CUDA(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+
+  AAPDHG_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, mode));
+  core_nodes_ = launch_core(s, su);
+  cudaStreamCaptureStatus cst;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  AAPDHG_CUDA(cudaStreamGetCaptureInfo(s, &cst, nullptr, nullptr, &deps, &ndeps));
+  std::vector<cudaGraphNode_t> tail(deps, deps + ndeps);
+  cudaGraph_t captured;
+  AAPDHG_CUDA(cudaStreamEndCapture(s, &captured));
+
+  cudaGraphNode_t after = nullptr;
+  aa_nodes_ = 0;
+  if (su.method != AAPDHG_METHOD_PDHG) {
+    AAPDHG_CUDA(cudaGraphConditionalHandleCreate(&cond_aa_, body, 0, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams ip{};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = cond_aa_;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    AAPDHG_CUDA(cudaGraphAddNode(&after, body, tail.data(), tail.size(), &ip));
+    cudaGraph_t ifbody = ip.conditional.phGraph_out[0];
+    AAPDHG_CUDA(cudaStreamBeginCaptureToGraph(s, ifbody, nullptr, nullptr, 0, mode));
+    aa_nodes_ = launch_aa(s, su);
+    AAPDHG_CUDA(cudaStreamEndCapture(s, &captured));
+    tail.assign(1, after);
+  }
+  AAPDHG_CUDA(cudaStreamBeginCaptureToGraph(s, body, tail.data(), nullptr, tail.size(), mode));
+  commit_nodes_ = launch_commit(s, su);
+  AAPDHG_CUDA(cudaStreamEndCapture(s, &captured));
+  AAPDHG_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
+  cudaGraphDestroy(g);
 }
 #undef LAUNCH
 
@@ -454,13 +527,13 @@ void Problem::run_power(const double* x0, int max_iters, double rel_tol, bool se
   PowerState hs{};
   for (;;) {
     for (int r = 0; r < kPowerBatch; ++r) {
-      if (K_.nblocks) {
-        if (serial) k_spmv<true><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a1, nullptr);
-        else k_spmv<false><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a1, nullptr);
+      if (K_.ntiles) {
+        if (serial) k_spmv<true><<<K_.grid(), kThreads, 0, stream_>>>(K_, a1, nullptr);
+        else k_spmv<false><<<K_.grid(), kThreads, 0, stream_>>>(K_, a1, nullptr);
       }
-      if (KT_.nblocks) {
-        if (serial) k_spmv<true><<<KT_.nblocks, kThreads, 0, stream_>>>(KT_, a2, nullptr);
-        else k_spmv<false><<<KT_.nblocks, kThreads, 0, stream_>>>(KT_, a2, nullptr);
+      if (KT_.ntiles) {
+        if (serial) k_spmv<true><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, a2, nullptr);
+        else k_spmv<false><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, a2, nullptr);
       }
       if (!serial) k_sumsq_partials<<<nb, kThreads, 0, stream_>>>(mtmx, nullptr, n_, part, &ps->done);
       k_power_ctrl<<<1, kCtrlThreads, 0, stream_>>>(mtmx, n_, part, nb, serial, ps);
@@ -573,9 +646,9 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.pow_len = ptab.size();
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
-  P.nblk1 = KT_.nblocks;
-  P.nblk2 = K_.nblocks;
-  P.ndot_blk = ndot_blk_;
+  P.nblk1 = KT_.grid();
+  P.nblk2 = K_.grid();
+  P.ndot_blk = ndot_tile_;
 
   DevState S0{};
   for (int r = 0; r < 4; ++r) S0.u_idx[r] = r;
@@ -583,26 +656,6 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   S0.g_idx[0] = 0;
   S0.g_idx[1] = 1;
   DevState* S = dstate_.as<DevState>();
-
-  // start iterate P(u0) in slot 0, its K x cached in kx slot 0; fresh pools
-  AAPDHG_CUDA(cudaMemsetAsync(upool_.p, 0, sizeof(double) * 4 * N_, stream_));
-  if (method != AAPDHG_METHOD_PDHG) {
-    AAPDHG_CUDA(cudaMemsetAsync(gpool_.p, 0, sizeof(double) * 2 * N_, stream_));
-  }
-  upload_iterate(0, x0, y0);
-  P.wall_offset_s = secs(t_start);
-  h2d(dparams_.p, &P, sizeof P, stream_);
-  h2d(S, &S0, sizeof S0, stream_);
-  k_project_start<<<grid_for(N_, kThreads, 1 << 30), kThreads, 0, stream_>>>(
-      upool_.as<double>(), l_.as<double>(), u_.as<double>(), n_, N_, m1_, S);
-  if (m_ && K_.nblocks) {
-    SpmvArgs a{};
-    a.x = upool_.as<double>();
-    a.out = kxpool_.as<double>();
-    if (serial) k_spmv<true><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
-    else k_spmv<false><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
-  }
-  AAPDHG_CUDA(cudaGetLastError());
 
   SolveSetup su;
   su.B = IterBufs{upool_.as<double>(), kxpool_.as<double>(), gpool_.as<double>(),
@@ -618,44 +671,61 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.push = method != AAPDHG_METHOD_PDHG;
   su.method = method;
   su.cap = cap;
-  su.nblk1 = KT_.nblocks;
-  su.nblk2 = K_.nblocks;
-  su.ndot_blk = ndot_blk_;
+  su.nblk1 = KT_.grid();
+  su.nblk2 = K_.grid();
+  su.ndot_blk = ndot_tile_;
   su.items_max = num_items_host(std::max(cap, 1), method);
 
-  // graph of kGraphIters iterations, cached per launch layout
+  // executable graph, cached per launch layout
   const bool use_graph = !profiling_;
   if (use_graph) {
     char key[256];
-    std::snprintf(key, sizeof key, "%d/%d/%d/%p/%p/%p/%p/%p", method, int(serial), cap,
-                  upool_.p, du_.p, partdot_.p, dparams_.p, rec_.p);
+    std::snprintf(key, sizeof key, "%d/%d/%d/%p/%p/%p/%p/%p/%p", method, int(serial), cap,
+                  upool_.p, du_.p, partdot_.p, dparams_.p, rec_.p, stream_);
     if (graph_key_ != key || !graph_exec_) {
       if (graph_exec_) {
         cudaGraphExecDestroy(graph_exec_);
         graph_exec_ = nullptr;
       }
-      cudaGraph_t g;
-      AAPDHG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-      for (int it = 0; it < kGraphIters; ++it) launch_iteration(stream_, su);
-      AAPDHG_CUDA(cudaStreamEndCapture(stream_, &g));
-      AAPDHG_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
-      cudaGraphDestroy(g);
+      build_graph(su);
       graph_key_ = key;
     }
   }
+  P.use_cond = use_graph ? 1 : 0;
+  P.cond_aa = cond_aa_;
+  P.cond_loop = cond_loop_;
 
-  uint64_t flushed = 0, iters_launched = 0;
-  int batch = 1;
+  // start iterate P(u0) in slot 0, its K x cached in kx slot 0; fresh pools
+  AAPDHG_CUDA(cudaMemsetAsync(upool_.p, 0, sizeof(double) * 4 * N_, stream_));
+  if (method != AAPDHG_METHOD_PDHG) {
+    AAPDHG_CUDA(cudaMemsetAsync(gpool_.p, 0, sizeof(double) * 2 * N_, stream_));
+  }
+  upload_iterate(0, x0, y0);
+  P.wall_offset_s = secs(t_start);
+  h2d(dparams_.p, &P, sizeof P, stream_);
+  h2d(S, &S0, sizeof S0, stream_);
+  k_project_start<<<grid_for(N_, kThreads, 1 << 30), kThreads, 0, stream_>>>(
+      upool_.as<double>(), l_.as<double>(), u_.as<double>(), n_, N_, m1_, S);
+  if (m_ && K_.ntiles) {
+    SpmvArgs a{};
+    a.x = upool_.as<double>();
+    a.out = kxpool_.as<double>();
+    if (serial) k_spmv<true><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
+    else k_spmv<false><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
+  }
+  AAPDHG_CUDA(cudaGetLastError());
+
+  uint64_t flushed = 0;
+  int batch = 8;  // iterations per launch, grows geometrically
   std::vector<aapdhg_record> host_recs;
   const aapdhg_record* drec = rec_.as<aapdhg_record>();
   for (;;) {
-    for (int b = 0; b < batch; ++b) {
-      if (use_graph) {
-        AAPDHG_CUDA(cudaGraphLaunch(graph_exec_, stream_));
-      } else {
-        for (int it = 0; it < kGraphIters; ++it) launch_iteration(stream_, su);
-      }
-      iters_launched += kGraphIters;
+    if (use_graph) {
+      *h_batch_ = batch;
+      h2d(&S->batch_left, h_batch_, sizeof(int32_t), stream_);
+      AAPDHG_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+    } else {
+      for (int it = 0; it < batch; ++it) launch_iteration(stream_, su);
     }
     d2h(h_state_, S, sizeof(DevState), stream_);
     sync();
@@ -677,9 +747,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
       flushed = done_recs;
     }
     if (h_state_->done) break;
-    // ring safety: never run further ahead than the ring can hold
-    batch = std::min(batch * 2, kMaxBatchGraphs);
-    while (uint64_t(batch) * kGraphIters * 2 > rec_cap_) batch /= 2;
+    // ring safety: a launch never runs further ahead than half the ring
+    batch = int(std::min<uint64_t>(uint64_t(batch) * 2, std::min<uint64_t>(kMaxBatch, rec_cap_ / 2)));
   }
   const DevState st = *h_state_;
 
@@ -709,7 +778,11 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   res->sigma = sigma;
   res->wall_seconds = secs(t_start);
   last_loop_iters_ = st.loop_iters;
-  last_launches_ = iters_launched * uint64_t(nodes_per_iter_);
+  if (use_graph)
+    last_launches_ = st.loop_iters * uint64_t(core_nodes_ + commit_nodes_) +
+                     (st.i + st.aa_failures) * uint64_t(aa_nodes_);
+  else
+    last_launches_ = st.loop_iters * uint64_t(core_nodes_ + commit_nodes_ + aa_nodes_);
 }
 
 // ---- single-op entry points ----------------------------------------------
@@ -719,7 +792,7 @@ void Problem::matvec(const double* x, double* out) {
   SpmvArgs a{};
   a.x = pw_x_.as<double>();
   a.out = pw_mx_.as<double>();
-  if (K_.nblocks) k_spmv<true><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
+  if (K_.ntiles) k_spmv<true><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
   AAPDHG_CUDA(cudaGetLastError());
   d2h(out, pw_mx_.p, sizeof(double) * m_, stream_);
   sync();
@@ -731,7 +804,7 @@ void Problem::matvec_transpose(const double* y, double* out) {
   SpmvArgs a{};
   a.x = pw_mx_.as<double>();
   a.out = pw_mtmx_.as<double>();
-  if (KT_.nblocks) k_spmv<true><<<KT_.nblocks, kThreads, 0, stream_>>>(KT_, a, nullptr);
+  if (KT_.ntiles) k_spmv<true><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, a, nullptr);
   AAPDHG_CUDA(cudaGetLastError());
   d2h(out, pw_mtmx_.p, sizeof(double) * n_, stream_);
   sync();
@@ -752,11 +825,11 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   AAPDHG_CUDA(cudaSetDevice(device_));
   ensure_iter_buffers(AAPDHG_METHOD_PDHG, 1);
   upload_iterate(0, x, y);
-  if (K_.nblocks) {
+  if (K_.ntiles) {
     SpmvArgs a{};
     a.x = upool_.as<double>();
     a.out = kxpool_.as<double>();
-    k_spmv<true><<<K_.nblocks, kThreads, 0, stream_>>>(K_, a, nullptr);
+    k_spmv<true><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
   }
   DevParams P{};
   P.method = AAPDHG_METHOD_PDHG;
@@ -767,19 +840,19 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   P.N = N_;
   P.tau = tau;
   P.sigma = sigma;
-  P.nblk1 = KT_.nblocks;
-  P.nblk2 = K_.nblocks;
+  P.nblk1 = KT_.grid();
+  P.nblk2 = K_.grid();
   const DevState S = identity_state();
   h2d(dparams_.p, &P, sizeof P, stream_);
   h2d(dstate_.p, &S, sizeof S, stream_);
   IterBufs B{upool_.as<double>(), kxpool_.as<double>(), nullptr, nullptr, nullptr,
              T_.as<double>(), part1_.as<double>(), part2_.as<double>(), c_.as<double>(),
              q_.as<double>(), l_.as<double>(), u_.as<double>()};
-  if (KT_.nblocks)
-    k_dual_side<true, false><<<KT_.nblocks, kThreads, 0, stream_>>>(
+  if (KT_.ntiles)
+    k_dual_side<true, false><<<KT_.grid(), kThreads, 0, stream_>>>(
         KT_, B, dparams_.as<DevParams>(), dstate_.as<DevState>());
-  if (K_.nblocks)
-    k_primal_side<true, false><<<K_.nblocks, kThreads, 0, stream_>>>(
+  if (K_.ntiles)
+    k_primal_side<true, false><<<K_.grid(), kThreads, 0, stream_>>>(
         K_, B, dparams_.as<DevParams>(), dstate_.as<DevState>());
   AAPDHG_CUDA(cudaGetLastError());
   const double* hat = upool_.as<double>() + 2 * N_;
@@ -840,7 +913,7 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
   P.d_hat = d_hat ? dhat_.as<double>() : nullptr;
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
-  P.ndot_blk = ndot_blk_;
+  P.ndot_blk = ndot_tile_;
   DevState S = identity_state();
   S.aa_attempt = 1;
   S.mem_size = p;
@@ -860,7 +933,7 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
     if (serial) {
       k_serial_dots<<<(items * 32 + kThreads - 1) / kThreads, kThreads, 0, stream_>>>(D, Pd, Sd);
     } else {
-      k_tree_dots<<<ndot_blk_, kThreads, 0, stream_>>>(D, Pd, Sd);
+      k_tree_dots<<<ndot_tile_, kThreads, 0, stream_>>>(D, Pd, Sd);
     }
   }
   k_aa_solve<<<1, 1024, 0, stream_>>>(D, W, Pd, Sd, 1);

@@ -67,7 +67,11 @@ class Problem {
   void ensure_iter_buffers(int method, int cap);
   void upload_iterate(int slot, const double* x, const double* y);
   void kkt_eval(int slot, bool serial, double* kkt_dev_out, double* lam_dev);
+  int launch_core(cudaStream_t s, const SolveSetup& su);
+  int launch_aa(cudaStream_t s, const SolveSetup& su);
+  int launch_commit(cudaStream_t s, const SolveSetup& su);
   void launch_iteration(cudaStream_t s, const SolveSetup& su);
+  void build_graph(const SolveSetup& su);
   void run_power(const double* x0_host, int max_iters, double rel_tol, bool serial, double* out,
                  int* rounds);
   void sync();
@@ -93,7 +97,7 @@ class Problem {
   bool all_zero_ = true;
   bool bounds_ok_ = true;
   CsrDev K_, KT_;
-  DevBuf k_rp_, k_ci_, k_v_, k_blk_, t_rp_, t_ci_, t_v_, t_blk_;
+  DevBuf k_rp_, k_ci_, k_v_, k_tile_, t_rp_, t_ci_, t_v_, t_tile_;
   DevBuf c_, q_, l_, u_;
   double nrm_q_[2] = {0, 0}, nrm_c_[2] = {0, 0};  // [serial, tree]
 
@@ -102,15 +106,16 @@ class Problem {
   DevBuf upool_, kxpool_, gpool_, du_, dg_, T_, part1_, part2_, partdot_, gram_, work_, vec_;
   DevBuf rec_, pow_tab_, dparams_, dstate_, dhat_, scal_, part_small_, lam_, pw_x_, pw_mx_,
       pw_mtmx_, pw_state_;
-  int ndot_blk_ = 0;
+  int ndot_tile_ = 0;
   uint64_t rec_cap_ = 0;
   DevState* h_state_ = nullptr;  // pinned mirror
 
-  // CUDA graph of G iterations, cached per launch layout
+  // CUDA graph WHILE(batch){core; IF(aa){aa}; commit}, cached per layout
   cudaGraphExec_t graph_exec_ = nullptr;
   std::string graph_key_;
-  int graph_iters_ = 0;
-  int nodes_per_iter_ = 0;
+  cudaGraphConditionalHandle cond_loop_ = 0, cond_aa_ = 0;
+  int core_nodes_ = 0, aa_nodes_ = 0, commit_nodes_ = 0;
+  int32_t* h_batch_ = nullptr;  // pinned
 
   bool profiling_ = false;
   std::map<std::string, KernelStat> stats_;

@@ -1,0 +1,583 @@
+// pipeline.cuh — the per-iteration core of the sm_100a AA-PDHG solver.
+//
+// One iteration, evaluated at the current iterate u_k = (x, y):
+//   k_dual_side     K'y warp-tile SpMV fused with the primal step
+//                   xhat = P_X(x - tau (c - K'y)) and the dual-side KKT terms
+//                   of u_k (lambda, bound terms, ||c - K'y - lambda||^2, c'x),
+//                   plus the x-half of the history push (du, dg, g)
+//                   — pdhg_core.cpp:49-53, solver.cpp:67-88,102-107,204-209
+//   k_primal_side   K xhat warp-tile SpMV fused with the dual step
+//                   yhat = P_Y(y + sigma (q - (2 K xhat - K x))) and the
+//                   primal-side KKT terms of u_k, plus the y-half of the push
+//                   — pdhg_core.cpp:55-60, solver.cpp:90-100
+//                   TREE mode: its last CTA reduces every partial sum and runs
+//                   the control logic (no extra launch).
+//   k_serial_control SERIAL mode: all reductions as index-ordered chains, then
+//                   the control logic.
+// Control (solver.cpp:188-215,241-247): termination tests, trajectory
+// records, memory push commit, safeguard — and, under graph replay, sets the
+// IF condition of the AA branch.
+//
+// SpMV: CSR rows are grouped on the host into warp tiles of <= 32 rows and
+// <= kWarpTile nonzeros (a longer row is a tile of its own). A warp streams
+// its tile's (col, val) pairs coalesced, gathers x[col] through the read-only
+// path, stages the products in its own shared-memory slice, and lane r sums
+// row r sequentially in CSR order — bit-identical to the reference's
+// row-serial matvec (sparse_linalg.cpp:60-69) and, on the transposed CSR
+// (entries in ascending original row), to its row-ordered scatter
+// matvec_transpose (sparse_linalg.cpp:77-87). No CTA barrier sits between a
+// warp's loads and its sums, so warps stream independently; the epilogue
+// operands of a lane's row are prefetched before the tile's loads.
+#pragma once
+
+#include "common.cuh"
+
+namespace aapdhg_b200 {
+
+// ---------------------------------------------------------------------------
+// reductions
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;  // identical in every lane (commutative butterfly)
+}
+
+// Fixed-shape block sum (warp xor tree, then warps in order); result valid in
+// thread 0. Deterministic: the association never depends on timing.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* red) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) red[q * kWarps + warp] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = red[q * kWarps];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) s += red[q * kWarps + w];
+      v[q] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Block-wide sum for any blockDim multiple of 32; result to all threads.
+__device__ __forceinline__ double block_sum_dyn(double v, double* red32) {
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red32[warp] = v;
+  __syncthreads();
+  double s = red32[0];
+  for (int w = 1; w < nw; ++w) s += red32[w];
+  return s;
+}
+
+// Thread-strided sum of part[0..nb) with 8 independent loads in flight,
+// then the fixed block tree. L1-bypassing loads: the partials were written
+// by other CTAs of the same kernel.
+__device__ __forceinline__ double reduce_partials(const double* part, int nb, double* red32) {
+  double s = 0.0;
+  int b = threadIdx.x;
+  const int st = blockDim.x;
+  for (; b + 7 * st < nb; b += 8 * st) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + b + u * st);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+  }
+  for (; b < nb; b += st) s = __dadd_rn(s, __ldcg(part + b));
+  return block_sum_dyn(s, red32);
+}
+
+// Index-ordered serial sums: the reference's vec.hpp:16-29 loops.
+__device__ __forceinline__ double serial_dot(const double* __restrict__ a,
+                                             const double* __restrict__ b, int64_t n) {
+  double s = 0.0;
+  int64_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    double p[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) p[u] = __dmul_rn(a[i + u], b[i + u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, p[u]);
+  }
+  for (; i < n; ++i) s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// warp-tile SpMV core
+// ---------------------------------------------------------------------------
+
+// wprod[t] = vals[e0+t] * x[col[e0+t]], t < cnt <= kWarpTile, one warp.
+// Two rounds of 4 coalesced (col, val) loads per lane, then the 4 gathers;
+// matrix streams use the evict-first (.cs) hint so the gathered vectors and
+// iterates stay L2-resident.
+__device__ __forceinline__ void warp_stage(const CsrDev& A, const double* __restrict__ x,
+                                           int64_t e0, int cnt, double* wprod, int lane) {
+  constexpr int U = 4;
+#pragma unroll 1
+  for (int base = 0; base < cnt; base += 32 * U) {
+    int c[U];
+    double a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = base + lane + 32 * u;
+      if (t < cnt) {
+        c[u] = __ldcs(A.ci + e0 + t);
+        a[u] = __ldcs(A.v + e0 + t);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = base + lane + 32 * u;
+      if (t < cnt) wprod[t] = __dmul_rn(a[u], __ldg(x + c[u]));
+    }
+  }
+}
+
+// Row owned by this lane for warp tile `tile` (or -1) — known before any
+// load so the caller can prefetch its epilogue operands.
+__device__ __forceinline__ int tile_row(const CsrDev& A, int tile, int lane, bool& is_long) {
+  const int r0 = A.tile[tile], r1 = A.tile[tile + 1];
+  is_long = (r1 - r0 == 1) && (A.rp[r1] - A.rp[r0] > kWarpTile);
+  if (is_long) return lane == 0 ? r0 : -1;
+  return lane < r1 - r0 ? r0 + lane : -1;
+}
+
+// Sum of one long row (> kWarpTile nonzeros) by one warp, kWarpTile chunks;
+// SERIAL adds every product in CSR order in lane 0 (bitwise = reference),
+// TREE adds per-chunk warp trees in order. Out of line: rare, register-heavy.
+template <bool SERIAL>
+__device__ __forceinline__ double long_row_sum(const CsrDev& A, const double* __restrict__ x,
+                                            int64_t e0, int64_t e1, double* wprod, int lane) {
+  double s = 0.0;
+  for (int64_t c0 = e0; c0 < e1; c0 += kWarpTile) {
+    const int cnt = (int)((e1 - c0) < kWarpTile ? (e1 - c0) : kWarpTile);
+    warp_stage(A, x, c0, cnt, wprod, lane);
+    __syncwarp();
+    if (SERIAL) {
+      if (lane == 0)
+        for (int t = 0; t < cnt; ++t) s = __dadd_rn(s, wprod[t]);
+    } else {
+      double v = 0.0;
+      for (int t = lane; t < cnt; t += 32) v = __dadd_rn(v, wprod[t]);
+      s = __dadd_rn(s, warp_sum(v));
+    }
+    __syncwarp();
+  }
+  return s;
+}
+
+// Row sum(s) of one warp tile; the value is valid in the lane that owns the
+// row (lane r <- row r0 + r; lane 0 for a long row).
+template <bool SERIAL>
+__device__ __forceinline__ double tile_sums(const CsrDev& A, const double* __restrict__ x,
+                                            int tile, double* wprod, int lane, bool is_long) {
+  const int r0 = A.tile[tile], r1 = A.tile[tile + 1];
+  const int64_t e0 = A.rp[r0], e1 = A.rp[r1];
+  if (is_long) return long_row_sum<SERIAL>(A, x, e0, e1, wprod, lane);
+  warp_stage(A, x, e0, (int)(e1 - e0), wprod, lane);
+  __syncwarp();
+  double s = 0.0;
+  if (lane < r1 - r0) {
+    const int a = (int)(A.rp[r0 + lane] - e0), z = (int)(A.rp[r0 + lane + 1] - e0);
+    for (int e = a; e < z; ++e) s = __dadd_rn(s, wprod[e]);
+  }
+  __syncwarp();
+  return s;
+}
+
+// CTAs per SM the tile kernels are register-budgeted for (6 x 8 warps = 48
+// warps: enough loads in flight for HBM; ptxas caps registers at 40).
+constexpr int kMinBlocks = 4;
+
+// out[r] = (A x)_r — power iteration, K x recache, per-op matvec.
+struct SpmvArgs {
+  const double* x;       // used when x_pool == nullptr
+  double* out;           // used when out_pool == nullptr
+  const double* x_pool;  // upool base: x = x_pool + u_idx[x_role]*x_stride
+  double* out_pool;      // kxpool base: out = out_pool + kx_idx[out_role]*out_stride
+  int32_t x_role, out_role;
+  int64_t x_stride, out_stride;
+  int32_t pred_aa_ok;    // run only when S->aa_ok
+  const int32_t* stop;   // optional: skip when *stop != 0 (power iteration)
+};
+
+template <bool SERIAL>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_spmv(CsrDev A, SpmvArgs g, const DevState* S) {
+  if (S) {
+    if (S->done) return;
+    if (g.pred_aa_ok && !S->aa_ok) return;
+  }
+  if (g.stop && *g.stop) return;
+  __shared__ double prod[kWarps][kWarpTile];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kWarps + warp;
+  if (tile >= A.ntiles) return;
+  const double* x = g.x_pool ? g.x_pool + (int64_t)S->u_idx[g.x_role] * g.x_stride : g.x;
+  double* out = g.out_pool ? g.out_pool + (int64_t)S->kx_idx[g.out_role] * g.out_stride : g.out;
+  bool is_long;
+  const int row = tile_row(A, tile, lane, is_long);
+  const double s = tile_sums<SERIAL>(A, x, tile, prod[warp], lane, is_long);
+  if (row >= 0) out[row] = s;
+}
+
+// ---------------------------------------------------------------------------
+// the fused PDHG halves
+// ---------------------------------------------------------------------------
+
+struct IterBufs {
+  double* upool;   // 4 x N
+  double* kxpool;  // 3 x m
+  double* gpool;   // 2 x N
+  double* du;      // cap x N
+  double* dg;      // cap x N
+  double* T;       // n
+  double* part1;   // P1_COUNT x nblk1
+  double* part2;   // P2_COUNT x nblk2
+  const double* c;
+  const double* q;
+  const double* l;
+  const double* u;
+};
+
+// Writes the warp's sums of acc[] into wred[warp][.], then thread 0 adds the
+// warps in order into part[q * nb + blockIdx.x].
+template <int NV>
+__device__ __forceinline__ void block_partials(double (&acc)[NV], double (*wred)[NV],
+                                               double* part, int nb) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = warp_sum(acc[q]);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) wred[warp][q] = acc[q];
+  __syncthreads();
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = wred[0][q];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, wred[w][q]);
+      part[q * nb + blockIdx.x] = s;
+    }
+}
+
+// K1: t = (K'y)_j (row j of K' = column j of K), then
+//   xhat_j = min(max(x_j - tau (c_j - t), l_j), u_j)      pdhg_core.cpp:49-53
+//   lambda_j = P_Lambda(c_j - t)                           solver.cpp:67-71
+//   partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
+//   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
+template <bool SERIAL, bool PUSH>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+  if (S->done) return;
+  __shared__ double prod[kWarps][kWarpTile];
+  __shared__ double wred[kWarps][P1_COUNT];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kWarps + warp;
+  double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
+  if (tile < KT.ntiles) {
+    const int64_t N = P->N;
+    const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
+    const double* y = x + P->n;
+    bool is_long;
+    const int j = tile_row(KT, tile, lane, is_long);
+    // epilogue operands first: independent of the SpMV, in flight with it
+    double xj = 0.0, cj = 0.0, lj = 0.0, uj = 0.0, xp = 0.0, gp = 0.0;
+    if (j >= 0) {
+      xj = x[j];
+      cj = __ldg(B.c + j);
+      lj = __ldg(B.l + j);
+      uj = __ldg(B.u + j);
+      if (PUSH) {
+        xp = B.upool[(int64_t)S->u_idx[U_PREV] * N + j];
+        gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + j];
+      }
+    }
+    const double t = tile_sums<SERIAL>(KT, y, tile, prod[warp], lane, is_long);
+    if (j >= 0) {
+      double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+      double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));
+      xn = smin(smax(xn, lj), uj);
+      xh[j] = xn;
+      const double d = __dsub_rn(xn, xj);
+      const double red_c = __dsub_rn(cj, t);
+      const double lam = project_lambda1(red_c, lj, uj);
+      double bt = 0.0;
+      if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
+      if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
+      const double dv = __dsub_rn(red_c, lam);
+      acc[P1_GX2] = __dmul_rn(d, d);
+      acc[P1_BOUND] = bt;
+      acc[P1_DUALSQ] = __dmul_rn(dv, dv);
+      acc[P1_CX] = __dmul_rn(cj, xj);
+      if (PUSH) {
+        const int64_t slot = S->push_slot;
+        B.du[slot * N + j] = __dsub_rn(xj, xp);
+        B.dg[slot * N + j] = __dsub_rn(d, gp);
+        B.gpool[(int64_t)S->g_idx[G_CUR] * N + j] = d;
+      }
+      if (SERIAL) B.T[j] = t;
+    }
+  }
+  if (!SERIAL) block_partials<P1_COUNT>(acc, wred, B.part1, P->nblk1);
+}
+
+__device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2, double bound, double qy,
+                              double cx, double infeas, double dual_sq);
+
+// TREE mode: reduce all partials of K1/K2 and run the control (one CTA).
+__device__ __forceinline__ void control_from_partials(const IterBufs& B, const DevParams* P,
+                                                      DevState* S) {
+  __shared__ double red32[32];
+  const double gx2 = reduce_partials(B.part1 + P1_GX2 * P->nblk1, P->nblk1, red32);
+  const double gy2 = reduce_partials(B.part2 + P2_GY2 * P->nblk2, P->nblk2, red32);
+  const double bound = reduce_partials(B.part1 + P1_BOUND * P->nblk1, P->nblk1, red32);
+  const double qy = reduce_partials(B.part2 + P2_QY * P->nblk2, P->nblk2, red32);
+  const double cx = reduce_partials(B.part1 + P1_CX * P->nblk1, P->nblk1, red32);
+  const double inf = reduce_partials(B.part2 + P2_INFEAS * P->nblk2, P->nblk2, red32);
+  const double dsq = reduce_partials(B.part1 + P1_DUALSQ * P->nblk1, P->nblk1, red32);
+  if (threadIdx.x == 0) control_logic(P, S, __dadd_rn(gx2, gy2), bound, qy, cx, inf, dsq);
+}
+
+// K2: s = (K xhat)_i, then
+//   yhat_i = y_i + sigma (q_i - (2 s - (K x)_i)), clamped >= 0 for i < m1
+//                                                         pdhg_core.cpp:55-60
+//   K xhat cached as the next K x (solver.cpp:90 / pdhg_core.cpp:56)
+//   partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
+template <bool SERIAL, bool PUSH>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+  if (S->done) return;
+  __shared__ double prod[kWarps][kWarpTile];
+  __shared__ double wred[kWarps][P2_COUNT];
+  __shared__ int is_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kWarps + warp;
+  double acc[P2_COUNT] = {0.0, 0.0, 0.0};
+  if (tile < K.ntiles) {
+    const int64_t N = P->N;
+    const int n = P->n, mr = P->mrows;
+    const double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+    bool is_long;
+    const int i = tile_row(K, tile, lane, is_long);
+    const double* u = B.upool + (int64_t)S->u_idx[U_CUR] * N;
+    double yi = 0.0, qi = 0.0, kxi = 0.0, yp = 0.0, gp = 0.0;
+    if (i >= 0) {
+      yi = u[n + i];
+      qi = __ldg(B.q + i);
+      kxi = B.kxpool[(int64_t)S->kx_idx[KX_CUR] * mr + i];
+      if (PUSH) {
+        yp = B.upool[(int64_t)S->u_idx[U_PREV] * N + n + i];
+        gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + n + i];
+      }
+    }
+    const double s = tile_sums<SERIAL>(K, xh, tile, prod[warp], lane, is_long);
+    if (i >= 0) {
+      double* uh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+      double* kxh = B.kxpool + (int64_t)S->kx_idx[KX_HAT] * mr;
+      double yn =
+          __dadd_rn(yi, __dmul_rn(P->sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
+      if (i < P->m1) yn = smax(yn, 0.0);
+      uh[n + i] = yn;
+      kxh[i] = s;
+      const double d = __dsub_rn(yn, yi);
+      double v = __dsub_rn(qi, kxi);
+      if (i < P->m1) v = smax(v, 0.0);
+      acc[P2_GY2] = __dmul_rn(d, d);
+      acc[P2_QY] = __dmul_rn(qi, yi);
+      acc[P2_INFEAS] = __dmul_rn(v, v);
+      if (PUSH) {
+        const int64_t slot = S->push_slot;
+        B.du[slot * N + n + i] = __dsub_rn(yi, yp);
+        B.dg[slot * N + n + i] = __dsub_rn(d, gp);
+        B.gpool[(int64_t)S->g_idx[G_CUR] * N + n + i] = d;
+      }
+    }
+  }
+  if (SERIAL) return;
+  block_partials<P2_COUNT>(acc, wred, B.part2, P->nblk2);
+  // last CTA to finish reduces all partials and runs the control logic
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(&S->ticket, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  control_from_partials(B, P, S);
+  if (threadIdx.x == 0) S->ticket = 0;
+}
+
+// ---------------------------------------------------------------------------
+// SERIAL mode: every scalar reduction as one index-ordered chain
+// (fixed_point_residual pdhg_core.cpp:65-74; kkt_metrics solver.cpp:64-110),
+// one warp per chain (lane 0 sums), then the control logic.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(32 * S_COUNT)
+    k_serial_control(IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+  if (S->done) {
+    if (threadIdx.x == 0 && P->use_cond) cudaGraphSetConditional(P->cond_aa, 0);
+    return;
+  }
+  __shared__ double res[S_COUNT];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    const int64_t N = P->N;
+    const int n = P->n, mr = P->mrows, m1 = P->m1;
+    const double* u = B.upool + (int64_t)S->u_idx[U_CUR] * N;
+    const double* uh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+    const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
+    const double* T = B.T;
+    double s = 0.0;
+    switch (w) {
+      case S_G2: {
+        int64_t i = 0;
+        for (; i + 8 <= N; i += 8) {
+          double p[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const double d = __dsub_rn(uh[i + k], u[i + k]);
+            p[k] = __dmul_rn(d, d);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s = __dadd_rn(s, p[k]);
+        }
+        for (; i < N; ++i) {
+          const double d = __dsub_rn(uh[i], u[i]);
+          s = __dadd_rn(s, __dmul_rn(d, d));
+        }
+        break;
+      }
+      case S_BOUND:
+        for (int j = 0; j < n; ++j) {
+          const double lj = B.l[j], uj = B.u[j];
+          const double lam = project_lambda1(__dsub_rn(B.c[j], T[j]), lj, uj);
+          if (isfinite(lj) && lam > 0.0) s = __dadd_rn(s, __dmul_rn(lj, lam));
+          if (isfinite(uj) && lam < 0.0) s = __dadd_rn(s, __dmul_rn(uj, lam));
+        }
+        break;
+      case S_QY: s = serial_dot(B.q, u + n, mr); break;
+      case S_CX: s = serial_dot(B.c, u, n); break;
+      case S_INFEAS:
+        for (int i = 0; i < mr; ++i) {
+          double v = __dsub_rn(B.q[i], kx[i]);
+          if (i < m1) v = smax(v, 0.0);
+          s = __dadd_rn(s, __dmul_rn(v, v));
+        }
+        break;
+      case S_DUALSQ:
+        for (int j = 0; j < n; ++j) {
+          const double rc = __dsub_rn(B.c[j], T[j]);
+          const double v = __dsub_rn(rc, project_lambda1(rc, B.l[j], B.u[j]));
+          s = __dadd_rn(s, __dmul_rn(v, v));
+        }
+        break;
+    }
+    res[w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    control_logic(P, S, res[S_G2], res[S_BOUND], res[S_QY], res[S_CX], res[S_INFEAS],
+                  res[S_DUALSQ]);
+}
+
+// KKT scalars of the CUR iterate from the reduced sums (solver.cpp:83-107).
+__device__ __forceinline__ void kkt_from_sums(double nrm_q, double nrm_c, double bound,
+                                              double qy, double cx, double infeas,
+                                              double dual_sq, double* kkt) {
+  const double dual_core = __dadd_rn(qy, bound);
+  const double primal_obj = cx;
+  kkt[0] = fabs(__dsub_rn(dual_core, primal_obj)) /
+           __dadd_rn(__dadd_rn(1.0, fabs(dual_core)), fabs(primal_obj));
+  kkt[1] = sqrt(infeas) / __dadd_rn(1.0, nrm_q);
+  kkt[2] = sqrt(dual_sq) / __dadd_rn(1.0, nrm_c);
+  kkt[3] = primal_obj;
+}
+
+__device__ __forceinline__ void finish_solve(DevState* S, int status, int role, double g) {
+  S->status = status;
+  S->final_role = role;
+  S->g_final = g;
+  S->done = 1;
+}
+
+// The scalar part of one iteration of solve() (solver.cpp:188-215,241-247),
+// run by a single thread after every sum of the iteration is known.
+__device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2, double bound, double qy,
+                              double cx, double infeas, double dual_sq) {
+  double kkt[4];
+  kkt_from_sums(P->nrm_q, P->nrm_c, bound, qy, cx, infeas, dual_sq, kkt);
+  for (int q = 0; q < 4; ++q) S->kkt[q] = kkt[q];
+  const double gkn = sqrt(g2);
+  S->gkn = gkn;
+  S->aa_attempt = 0;
+  S->aa_ok = 0;
+  const uint64_t k = S->k;
+  const double elapsed = (double)(globaltimer_ns() - S->t0_ns) * 1e-9 + P->wall_offset_s;
+  bool attempt = false;
+  do {
+    if (k == 0) {  // priming step, solver.cpp:168-172
+      S->g0n = gkn;
+      aapdhg_record* r = P->rec;
+      r->k = 0;
+      r->g_norm = gkn;
+      r->aa_step = 0;
+      r->i = 0;
+      r->j = 0;
+      break;
+    }
+    {  // the record of iterate k-1 takes the KKT of the produced iterate u_k
+      aapdhg_record* r = P->rec + (k - 1) % P->rec_cap;
+      r->r_gap = kkt[0];
+      r->r_primal = kkt[1];
+      r->r_dual = kkt[2];
+      r->objective = kkt[3];
+      r->elapsed_s = elapsed;
+      S->rec_complete = k;
+    }
+    const double kmax = smax(smax(kkt[0], kkt[1]), kkt[2]);
+    if (k == 1 && S->g0n == 0.0) { finish_solve(S, AAPDHG_SOLVE_FIXED_POINT_START, U_PREV, 0.0); break; }
+    if (P->kkt_terminate && kmax <= P->kkt_eps) { finish_solve(S, AAPDHG_SOLVE_KKT_TOL, U_CUR, gkn); break; }
+    if (gkn < P->toll) { finish_solve(S, AAPDHG_SOLVE_RESIDUAL_TOL, U_CUR, gkn); break; }
+    if (S->i + S->j >= P->max_iters) { finish_solve(S, AAPDHG_SOLVE_MAX_ITERS, U_CUR, gkn); break; }
+    if (elapsed >= P->max_wall_s) { finish_solve(S, AAPDHG_SOLVE_TIMEOUT, U_CUR, gkn); break; }
+
+    if (P->method != AAPDHG_METHOD_PDHG) {  // memory_push / FaaState::push
+      if (S->mem_size == P->cap) {
+        for (int t = 1; t < S->mem_size; ++t) S->mem_slots[t - 1] = S->mem_slots[t];
+        S->mem_slots[S->mem_size - 1] = S->push_slot;
+      } else {
+        S->mem_slots[S->mem_size++] = S->push_slot;
+      }
+    }
+    aapdhg_record* r = P->rec + k % P->rec_cap;
+    r->k = k;
+    r->g_norm = gkn;
+    r->aa_step = 0;
+    r->i = S->i;
+    r->j = S->j;
+    if (P->method != AAPDHG_METHOD_PDHG) {
+      // safeguard_pass, solver.cpp:59-62, with the host std::pow table
+      const double pw = S->i < P->pow_len ? P->pow_tab[S->i]
+                                          : pow((double)S->i + 1.0, -(1.0 + P->safeguard_eps));
+      attempt = gkn <= __dmul_rn(__dmul_rn(P->safeguard_d, S->g0n), pw);
+    }
+    if (attempt) S->aa_attempt = 1;
+    else S->j += 1;
+  } while (false);
+  if (P->use_cond) cudaGraphSetConditional(P->cond_aa, attempt ? 1u : 0u);
+}
+
+}  // namespace aapdhg_b200
