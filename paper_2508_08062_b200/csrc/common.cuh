@@ -47,8 +47,9 @@ struct CsrDev {
   const int32_t* ci = nullptr;
   const double* v = nullptr;
   int32_t ntiles = 0;
-  const int32_t* tile = nullptr;  // ntiles + 1 row boundaries (warp tiles)
-  int32_t grid() const { return (ntiles + kWarps - 1) / kWarps; }
+  const int4* meta = nullptr;     // per warp tile {r0, r1, e0, e1}
+  int32_t grid_blocks = 0;        // persistent grid of the tile kernels
+  int32_t grid() const { return grid_blocks; }
 };
 
 // Constant per solve (written before the loop starts).

@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <random>
 
 #include "engine.h"
@@ -96,6 +97,34 @@ struct SolveSetup {
   int method, cap, nblk1, nblk2, ndot_blk, items_max;
 };
 
+// Uploads one CSR (arrays padded by kPad elements) with its warp-tile
+// metadata {r0, r1, e0, e1} and persistent grid size.
+void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows,
+                         int ncols, DevBuf& d_rp, DevBuf& d_ci, DevBuf& d_v, DevBuf& d_meta,
+                         CsrDev& out) {
+  constexpr int kPad = 16;
+  const int64_t nnz = rp[nrows];
+  const std::vector<int32_t> tb = build_tiles(rp, nrows);
+  const int ntiles = int(tb.size() - 1);
+  std::vector<int4> meta(size_t(std::max(ntiles, 1)));
+  for (int t = 0; t < ntiles; ++t) meta[size_t(t)] = make_int4(tb[t], tb[t + 1], rp[tb[t]], rp[tb[t + 1]]);
+  d_rp.reserve(sizeof(int32_t) * (nrows + 1 + kPad));
+  d_ci.reserve(sizeof(int32_t) * (nnz + kPad));
+  d_v.reserve(sizeof(double) * (nnz + kPad));
+  d_meta.reserve(sizeof(int4) * meta.size());
+  AAPDHG_CUDA(cudaMemsetAsync(d_ci.p, 0, d_ci.bytes, stream_));
+  AAPDHG_CUDA(cudaMemsetAsync(d_v.p, 0, d_v.bytes, stream_));
+  h2d(d_rp.p, rp, sizeof(int32_t) * (nrows + 1), stream_);
+  h2d(d_ci.p, ci, sizeof(int32_t) * nnz, stream_);
+  h2d(d_v.p, v, sizeof(double) * nnz, stream_);
+  h2d(d_meta.p, meta.data(), sizeof(int4) * ntiles, stream_);
+  sync();  // host vectors go out of scope
+  const int64_t want = (int64_t(ntiles) + kPipeWarps - 1) / kPipeWarps;
+  const int64_t cap = int64_t(num_sms_) * kPipeBlocksPerSM;
+  out = CsrDev{nrows, ncols, nnz, d_rp.as<int32_t>(), d_ci.as<int32_t>(), d_v.as<double>(),
+               ntiles, d_meta.as<int4>(), int32_t(std::max<int64_t>(1, std::min(want, cap)))};
+}
+
 // ---------------------------------------------------------------------------
 Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   if (!v) throw StatusError(AAPDHG_ERR_INPUT, "problem_create: null problem");
@@ -137,19 +166,9 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   N_ = int64_t(n_) + m_;
   for (int64_t e = 0; e < nnz_ && all_zero_; ++e) all_zero_ = k.vals[e] == 0.0;
 
-  // K and its row blocks
-  const std::vector<int32_t> kb = build_tiles(k.row_ptr, m_);
-  k_rp_.reserve(sizeof(int32_t) * (m_ + 1));
-  k_ci_.reserve(sizeof(int32_t) * nnz_);
-  k_v_.reserve(sizeof(double) * nnz_);
-  k_tile_.reserve(sizeof(int32_t) * kb.size());
-  h2d(k_rp_.p, k.row_ptr, sizeof(int32_t) * (m_ + 1), stream_);
-  h2d(k_ci_.p, k.col_idx, sizeof(int32_t) * nnz_, stream_);
-  h2d(k_v_.p, k.vals, sizeof(double) * nnz_, stream_);
-  h2d(k_tile_.p, kb.data(), sizeof(int32_t) * kb.size(), stream_);
-  K_ = CsrDev{m_, n_, nnz_, k_rp_.as<int32_t>(), k_ci_.as<int32_t>(), k_v_.as<double>(),
-              int32_t(kb.size() - 1), k_tile_.as<int32_t>()};
-
+  // K, padded so 16-byte cp.async of a tile's aligned superset stays in bounds
+  AAPDHG_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device));
+  upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_rp_, k_ci_, k_v_, k_tile_, K_);
   // K' as CSR, entries of each row in ascending original row (counting sort)
   std::vector<int32_t> trp(static_cast<size_t>(n_) + 1, 0), tci(static_cast<size_t>(nnz_));
   std::vector<double> tv(static_cast<size_t>(nnz_));
@@ -164,17 +183,7 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
         tv[size_t(pos)] = k.vals[e];
       }
   }
-  const std::vector<int32_t> tb = build_tiles(trp.data(), n_);
-  t_rp_.reserve(sizeof(int32_t) * (n_ + 1));
-  t_ci_.reserve(sizeof(int32_t) * nnz_);
-  t_v_.reserve(sizeof(double) * nnz_);
-  t_tile_.reserve(sizeof(int32_t) * tb.size());
-  h2d(t_rp_.p, trp.data(), sizeof(int32_t) * (n_ + 1), stream_);
-  h2d(t_ci_.p, tci.data(), sizeof(int32_t) * nnz_, stream_);
-  h2d(t_v_.p, tv.data(), sizeof(double) * nnz_, stream_);
-  h2d(t_tile_.p, tb.data(), sizeof(int32_t) * tb.size(), stream_);
-  KT_ = CsrDev{n_, m_, nnz_, t_rp_.as<int32_t>(), t_ci_.as<int32_t>(), t_v_.as<double>(),
-               int32_t(tb.size() - 1), t_tile_.as<int32_t>()};
+  upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_rp_, t_ci_, t_v_, t_tile_, KT_);
 
   c_.reserve(sizeof(double) * n_);
   q_.reserve(sizeof(double) * m_);
@@ -292,14 +301,14 @@ void Problem::kkt_eval(int slot, bool serial, double* out_dev, double* lam_dev) 
   if (n_ && KT_.ntiles) {
     a.x = y;
     a.out = T;
-    if (serial) k_spmv<true><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, a, nullptr);
-    else k_spmv<false><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, a, nullptr);
+    if (serial) k_spmv<true><<<KT_.grid(), kPipeThreads, 0, stream_>>>(KT_, a, nullptr);
+    else k_spmv<false><<<KT_.grid(), kPipeThreads, 0, stream_>>>(KT_, a, nullptr);
   }
   if (m_ && K_.ntiles) {
     a.x = x;
     a.out = KX;
-    if (serial) k_spmv<true><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
-    else k_spmv<false><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
+    if (serial) k_spmv<true><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
+    else k_spmv<false><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
   }
   const int64_t nbig = std::max<int64_t>(std::max<int64_t>(n_, m_), 1);
   const int nb = int((nbig + kThreads - 1) / kThreads);
@@ -373,16 +382,16 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   int nodes = 0;
   const bool ser = su.serial, push = su.push;
   if (su.nblk1 > 0) {
-    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<su.nblk1, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<su.nblk1, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<su.nblk1, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else LAUNCH("k_dual_side", k_dual_side<false, false><<<su.nblk1, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<su.nblk1, kPipeThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<su.nblk1, kPipeThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<su.nblk1, kPipeThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else LAUNCH("k_dual_side", k_dual_side<false, false><<<su.nblk1, kPipeThreads, 0, s>>>(KT_, su.B, su.P, su.S));
   }
   if (su.nblk2 > 0) {
-    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<su.nblk2, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<su.nblk2, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<su.nblk2, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else LAUNCH("k_primal_side", k_primal_side<false, false><<<su.nblk2, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<su.nblk2, kPipeThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<su.nblk2, kPipeThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<su.nblk2, kPipeThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else LAUNCH("k_primal_side", k_primal_side<false, false><<<su.nblk2, kPipeThreads, 0, s>>>(K_, su.B, su.P, su.S));
   }
   if (ser) LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
   AAPDHG_CUDA(cudaGetLastError());
@@ -409,8 +418,8 @@ int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
     a.out_role = KX_CAND;
     a.out_stride = m_;
     a.pred_aa_ok = 1;
-    if (su.serial) LAUNCH("k_spmv_recache", k_spmv<true><<<K_.grid(), kThreads, 0, s>>>(K_, a, su.S));
-    else LAUNCH("k_spmv_recache", k_spmv<false><<<K_.grid(), kThreads, 0, s>>>(K_, a, su.S));
+    if (su.serial) LAUNCH("k_spmv_recache", k_spmv<true><<<K_.grid(), kPipeThreads, 0, s>>>(K_, a, su.S));
+    else LAUNCH("k_spmv_recache", k_spmv<false><<<K_.grid(), kPipeThreads, 0, s>>>(K_, a, su.S));
   }
   AAPDHG_CUDA(cudaGetLastError());
   return nodes;
@@ -528,12 +537,12 @@ void Problem::run_power(const double* x0, int max_iters, double rel_tol, bool se
   for (;;) {
     for (int r = 0; r < kPowerBatch; ++r) {
       if (K_.ntiles) {
-        if (serial) k_spmv<true><<<K_.grid(), kThreads, 0, stream_>>>(K_, a1, nullptr);
-        else k_spmv<false><<<K_.grid(), kThreads, 0, stream_>>>(K_, a1, nullptr);
+        if (serial) k_spmv<true><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a1, nullptr);
+        else k_spmv<false><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a1, nullptr);
       }
       if (KT_.ntiles) {
-        if (serial) k_spmv<true><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, a2, nullptr);
-        else k_spmv<false><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, a2, nullptr);
+        if (serial) k_spmv<true><<<KT_.grid(), kPipeThreads, 0, stream_>>>(KT_, a2, nullptr);
+        else k_spmv<false><<<KT_.grid(), kPipeThreads, 0, stream_>>>(KT_, a2, nullptr);
       }
       if (!serial) k_sumsq_partials<<<nb, kThreads, 0, stream_>>>(mtmx, nullptr, n_, part, &ps->done);
       k_power_ctrl<<<1, kCtrlThreads, 0, stream_>>>(mtmx, n_, part, nb, serial, ps);
@@ -677,7 +686,13 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.items_max = num_items_host(std::max(cap, 1), method);
 
   // executable graph, cached per launch layout
-  const bool use_graph = !profiling_;
+  // AAPDHG_EAGER=1 forces stream launches (ncu cannot profile kernels inside
+  // graphs that hold conditional nodes)
+  static const bool force_eager = [] {
+    const char* e = std::getenv("AAPDHG_EAGER");
+    return e && e[0] == '1';
+  }();
+  const bool use_graph = !profiling_ && !force_eager;
   if (use_graph) {
     char key[256];
     std::snprintf(key, sizeof key, "%d/%d/%d/%p/%p/%p/%p/%p/%p", method, int(serial), cap,
@@ -710,8 +725,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
     SpmvArgs a{};
     a.x = upool_.as<double>();
     a.out = kxpool_.as<double>();
-    if (serial) k_spmv<true><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
-    else k_spmv<false><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
+    if (serial) k_spmv<true><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
+    else k_spmv<false><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
   }
   AAPDHG_CUDA(cudaGetLastError());
 
@@ -792,7 +807,7 @@ void Problem::matvec(const double* x, double* out) {
   SpmvArgs a{};
   a.x = pw_x_.as<double>();
   a.out = pw_mx_.as<double>();
-  if (K_.ntiles) k_spmv<true><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
+  if (K_.ntiles) k_spmv<true><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
   AAPDHG_CUDA(cudaGetLastError());
   d2h(out, pw_mx_.p, sizeof(double) * m_, stream_);
   sync();
@@ -804,7 +819,7 @@ void Problem::matvec_transpose(const double* y, double* out) {
   SpmvArgs a{};
   a.x = pw_mx_.as<double>();
   a.out = pw_mtmx_.as<double>();
-  if (KT_.ntiles) k_spmv<true><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, a, nullptr);
+  if (KT_.ntiles) k_spmv<true><<<KT_.grid(), kPipeThreads, 0, stream_>>>(KT_, a, nullptr);
   AAPDHG_CUDA(cudaGetLastError());
   d2h(out, pw_mtmx_.p, sizeof(double) * n_, stream_);
   sync();
@@ -829,7 +844,7 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
     SpmvArgs a{};
     a.x = upool_.as<double>();
     a.out = kxpool_.as<double>();
-    k_spmv<true><<<K_.grid(), kThreads, 0, stream_>>>(K_, a, nullptr);
+    k_spmv<true><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
   }
   DevParams P{};
   P.method = AAPDHG_METHOD_PDHG;
@@ -849,10 +864,10 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
              T_.as<double>(), part1_.as<double>(), part2_.as<double>(), c_.as<double>(),
              q_.as<double>(), l_.as<double>(), u_.as<double>()};
   if (KT_.ntiles)
-    k_dual_side<true, false><<<KT_.grid(), kThreads, 0, stream_>>>(
+    k_dual_side<true, false><<<KT_.grid(), kPipeThreads, 0, stream_>>>(
         KT_, B, dparams_.as<DevParams>(), dstate_.as<DevState>());
   if (K_.ntiles)
-    k_primal_side<true, false><<<K_.grid(), kThreads, 0, stream_>>>(
+    k_primal_side<true, false><<<K_.grid(), kPipeThreads, 0, stream_>>>(
         K_, B, dparams_.as<DevParams>(), dstate_.as<DevState>());
   AAPDHG_CUDA(cudaGetLastError());
   const double* hat = upool_.as<double>() + 2 * N_;

@@ -64,6 +64,8 @@ class Problem {
  private:
   bool resolve_serial(int reduction) const;
   double device_dot(const double* a, const double* b, int64_t n, bool serial);
+  void upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
+                  DevBuf& d_rp, DevBuf& d_ci, DevBuf& d_v, DevBuf& d_meta, CsrDev& out);
   void ensure_iter_buffers(int method, int cap);
   void upload_iterate(int slot, const double* x, const double* y);
   void kkt_eval(int slot, bool serial, double* kkt_dev_out, double* lam_dev);
@@ -90,6 +92,7 @@ class Problem {
   cudaEvent_t cur_a_ = nullptr;
 
   int device_;
+  int num_sms_ = 148;
   cudaStream_t stream_ = nullptr;
   cudaStream_t own_stream_ = nullptr;
   int n_ = 0, m_ = 0, m1_ = 0;

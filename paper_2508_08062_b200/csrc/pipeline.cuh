@@ -114,13 +114,76 @@ __device__ __forceinline__ double serial_dot(const double* __restrict__ a,
 }
 
 // ---------------------------------------------------------------------------
-// warp-tile SpMV core
+// pipelined warp-tile SpMV core
 // ---------------------------------------------------------------------------
+//
+// Rows are grouped on the host into warp tiles (<= 32 rows, <= kWarpTile
+// nonzeros; a longer row is a tile of its own) described by int4 metadata
+// {r0, r1, e0, e1}. The tile kernels are persistent: warp w of the grid
+// handles tiles w, w + W, w + 2W, ... and keeps two tiles in flight — while
+// it gathers and sums tile t out of shared memory, cp.async is already
+// streaming tile t+W's (val, col) slice, its row offsets and the epilogue
+// operands of its rows (x, c, l, u, ...) into the other stage. In-flight
+// data costs no registers, so ~2 tiles x 20 warps per SM keep HBM busy.
 
-// wprod[t] = vals[e0+t] * x[col[e0+t]], t < cnt <= kWarpTile, one warp.
-// Two rounds of 4 coalesced (col, val) loads per lane, then the 4 gathers;
-// matrix streams use the evict-first (.cs) hint so the gathered vectors and
-// iterates stay L2-resident.
+constexpr int kPipeWarps = 4;  // warps per CTA of the tile kernels
+constexpr int kPipeThreads = 32 * kPipeWarps;
+constexpr int kPipeBlocksPerSM = 5;  // 5 x 38 KB of stages per SM
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// One stage of a warp's pipeline. v/ci hold the 16-byte aligned superset of
+// the tile's [e0, e1) slice (offsets e0 & 1 and e0 & 3); products overwrite v.
+template <int NE>
+struct __align__(16) WarpStage {
+  double v[kWarpTile + 2];
+  int32_t ci[kWarpTile + 8];
+  int32_t rp[36];
+  double epi[NE > 0 ? NE : 1][32];
+};
+
+__device__ __forceinline__ bool tile_is_long(const int4& m) {
+  return (m.y - m.x == 1) && (m.w - m.z > kWarpTile);
+}
+
+// Starts the async copies of tile m into stage st (one commit group, empty
+// for a long row, which is streamed synchronously when processed).
+template <int NE>
+__device__ __forceinline__ void issue_tile(const CsrDev& A, const int4& m, WarpStage<NE>& st,
+                                           const double* const* src, int lane) {
+  if (!tile_is_long(m)) {
+    const int r0 = m.x, r1 = m.y, e0 = m.z, e1 = m.w;
+    const int a0 = e0 & ~1, nv = (e1 - a0 + 1) >> 1;
+    for (int k = lane; k < nv; k += 32) cp_async16(&st.v[2 * k], A.v + a0 + 2 * k);
+    const int c0 = e0 & ~3, nc = (e1 - c0 + 3) >> 2;
+    for (int k = lane; k < nc; k += 32) cp_async16(&st.ci[4 * k], A.ci + c0 + 4 * k);
+    const int nr = r1 - r0;
+    for (int i = lane; i <= nr; i += 32) cp_async4(&st.rp[i], A.rp + r0 + i);
+    if (lane < nr)
+#pragma unroll
+      for (int q = 0; q < NE; ++q) cp_async8(&st.epi[q][lane], src[q] + r0 + lane);
+  }
+  cp_async_commit();
+}
+
+// wprod[t] = vals[e0+t] * x[col[e0+t]], t < cnt <= kWarpTile (register path,
+// used for the chunks of long rows).
 __device__ __forceinline__ void warp_stage(const CsrDev& A, const double* __restrict__ x,
                                            int64_t e0, int cnt, double* wprod, int lane) {
   constexpr int U = 4;
@@ -144,21 +207,12 @@ __device__ __forceinline__ void warp_stage(const CsrDev& A, const double* __rest
   }
 }
 
-// Row owned by this lane for warp tile `tile` (or -1) — known before any
-// load so the caller can prefetch its epilogue operands.
-__device__ __forceinline__ int tile_row(const CsrDev& A, int tile, int lane, bool& is_long) {
-  const int r0 = A.tile[tile], r1 = A.tile[tile + 1];
-  is_long = (r1 - r0 == 1) && (A.rp[r1] - A.rp[r0] > kWarpTile);
-  if (is_long) return lane == 0 ? r0 : -1;
-  return lane < r1 - r0 ? r0 + lane : -1;
-}
-
 // Sum of one long row (> kWarpTile nonzeros) by one warp, kWarpTile chunks;
 // SERIAL adds every product in CSR order in lane 0 (bitwise = reference),
-// TREE adds per-chunk warp trees in order. Out of line: rare, register-heavy.
+// TREE adds per-chunk warp trees in order. Valid in lane 0.
 template <bool SERIAL>
-__device__ __forceinline__ double long_row_sum(const CsrDev& A, const double* __restrict__ x,
-                                            int64_t e0, int64_t e1, double* wprod, int lane) {
+__device__ double long_row_sum(const CsrDev& A, const double* __restrict__ x, int64_t e0,
+                               int64_t e1, double* wprod, int lane) {
   double s = 0.0;
   for (int64_t c0 = e0; c0 < e1; c0 += kWarpTile) {
     const int cnt = (int)((e1 - c0) < kWarpTile ? (e1 - c0) : kWarpTile);
@@ -177,28 +231,45 @@ __device__ __forceinline__ double long_row_sum(const CsrDev& A, const double* __
   return s;
 }
 
-// Row sum(s) of one warp tile; the value is valid in the lane that owns the
-// row (lane r <- row r0 + r; lane 0 for a long row).
-template <bool SERIAL>
-__device__ __forceinline__ double tile_sums(const CsrDev& A, const double* __restrict__ x,
-                                            int tile, double* wprod, int lane, bool is_long) {
-  const int r0 = A.tile[tile], r1 = A.tile[tile + 1];
-  const int64_t e0 = A.rp[r0], e1 = A.rp[r1];
-  if (is_long) return long_row_sum<SERIAL>(A, x, e0, e1, wprod, lane);
-  warp_stage(A, x, e0, (int)(e1 - e0), wprod, lane);
-  __syncwarp();
-  double s = 0.0;
-  if (lane < r1 - r0) {
-    const int a = (int)(A.rp[r0 + lane] - e0), z = (int)(A.rp[r0 + lane + 1] - e0);
-    for (int e = a; e < z; ++e) s = __dadd_rn(s, wprod[e]);
+// Row sums of a staged tile: gathers x[col] (8 per lane in flight), products
+// in place, then lane r adds row r0 + r in CSR order. Returns the lane's
+// row (-1 if none); `s` valid there.
+template <bool SERIAL, int NE>
+__device__ __forceinline__ int tile_sums(const CsrDev& A, const int4& m, WarpStage<NE>& st,
+                                         const double* __restrict__ x, int lane, double& s) {
+  const int r0 = m.x, r1 = m.y, e0 = m.z, e1 = m.w;
+  s = 0.0;
+  if (tile_is_long(m)) {
+    s = long_row_sum<SERIAL>(A, x, e0, e1, st.v, lane);
+    return lane == 0 ? r0 : -1;
+  }
+  const int cnt = e1 - e0, vo = e0 & 1, co = e0 & 3;
+  double g[kWarpTile / 32];
+#pragma unroll
+  for (int u = 0; u < kWarpTile / 32; ++u) {
+    const int t = lane + 32 * u;
+    if (t < cnt) g[u] = __ldg(x + st.ci[co + t]);
+  }
+#pragma unroll
+  for (int u = 0; u < kWarpTile / 32; ++u) {
+    const int t = lane + 32 * u;
+    if (t < cnt) st.v[vo + t] = __dmul_rn(st.v[vo + t], g[u]);
   }
   __syncwarp();
-  return s;
+  if (lane >= r1 - r0) return -1;
+  const int a = st.rp[lane] - e0, z = st.rp[lane + 1] - e0;
+  double acc = 0.0;
+  for (int e = a; e < z; ++e) acc = __dadd_rn(acc, st.v[vo + e]);
+  s = acc;
+  return r0 + lane;
 }
 
-// CTAs per SM the tile kernels are register-budgeted for (6 x 8 warps = 48
-// warps: enough loads in flight for HBM; ptxas caps registers at 40).
-constexpr int kMinBlocks = 4;
+// Epilogue operand q of the lane's row: staged, or read directly for a long row.
+template <int NE>
+__device__ __forceinline__ double operand(const WarpStage<NE>& st, bool is_long,
+                                          const double* const* src, int q, int row, int lane) {
+  return is_long ? src[q][row] : st.epi[q][lane];
+}
 
 // out[r] = (A x)_r — power iteration, K x recache, per-op matvec.
 struct SpmvArgs {
@@ -213,22 +284,42 @@ struct SpmvArgs {
 };
 
 template <bool SERIAL>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_spmv(CsrDev A, SpmvArgs g, const DevState* S) {
+__global__ void __launch_bounds__(kPipeThreads, kPipeBlocksPerSM)
+    k_spmv(CsrDev A, SpmvArgs g, const DevState* S) {
   if (S) {
     if (S->done) return;
     if (g.pred_aa_ok && !S->aa_ok) return;
   }
   if (g.stop && *g.stop) return;
-  __shared__ double prod[kWarps][kWarpTile];
+  __shared__ WarpStage<0> stage[kPipeWarps][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kWarps + warp;
-  if (tile >= A.ntiles) return;
+  const int W = gridDim.x * kPipeWarps;
   const double* x = g.x_pool ? g.x_pool + (int64_t)S->u_idx[g.x_role] * g.x_stride : g.x;
   double* out = g.out_pool ? g.out_pool + (int64_t)S->kx_idx[g.out_role] * g.out_stride : g.out;
-  bool is_long;
-  const int row = tile_row(A, tile, lane, is_long);
-  const double s = tile_sums<SERIAL>(A, x, tile, prod[warp], lane, is_long);
-  if (row >= 0) out[row] = s;
+  const double* const src[1] = {nullptr};
+  int tile = blockIdx.x * kPipeWarps + warp;
+  if (tile >= A.ntiles) return;
+  int4 m = A.meta[tile];
+  issue_tile<0>(A, m, stage[warp][0], src, lane);
+  for (int buf = 0; tile < A.ntiles; buf ^= 1) {
+    const int next = tile + W;
+    int4 mn = m;
+    if (next < A.ntiles) {
+      mn = A.meta[next];
+      issue_tile<0>(A, mn, stage[warp][buf ^ 1], src, lane);
+    } else {
+      cp_async_commit();
+    }
+    cp_async_wait<1>();
+    __syncwarp();
+    double s;
+    const int row = tile_sums<SERIAL, 0>(A, m, stage[warp][buf], x, lane, s);
+    if (row >= 0) out[row] = s;
+    __syncwarp();
+    tile = next;
+    m = mn;
+  }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -250,8 +341,7 @@ struct IterBufs {
   const double* u;
 };
 
-// Writes the warp's sums of acc[] into wred[warp][.], then thread 0 adds the
-// warps in order into part[q * nb + blockIdx.x].
+// Adds the warps' acc[] in order into part[q * nb + blockIdx.x].
 template <int NV>
 __device__ __forceinline__ void block_partials(double (&acc)[NV], double (*wred)[NV],
                                                double* part, int nb) {
@@ -267,7 +357,7 @@ __device__ __forceinline__ void block_partials(double (&acc)[NV], double (*wred)
     for (int q = 0; q < NV; ++q) {
       double s = wred[0][q];
 #pragma unroll
-      for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, wred[w][q]);
+      for (int w = 1; w < kPipeWarps; ++w) s = __dadd_rn(s, wred[w][q]);
       part[q * nb + blockIdx.x] = s;
     }
 }
@@ -277,37 +367,62 @@ __device__ __forceinline__ void block_partials(double (&acc)[NV], double (*wred)
 //   lambda_j = P_Lambda(c_j - t)                           solver.cpp:67-71
 //   partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
 //   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
+// Per-lane partial sums run over the warp's tiles in a fixed order, so the
+// CTA partials are deterministic.
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+__global__ void __launch_bounds__(kPipeThreads, kPipeBlocksPerSM)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
-  __shared__ double prod[kWarps][kWarpTile];
-  __shared__ double wred[kWarps][P1_COUNT];
+  constexpr int NE = PUSH ? 6 : 4;
+  __shared__ WarpStage<NE> stage[kPipeWarps][2];
+  __shared__ double wred[kPipeWarps][P1_COUNT];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kWarps + warp;
+  const int W = gridDim.x * kPipeWarps;
+  const int64_t N = P->N;
+  const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
+  const double* y = x + P->n;
+  double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+  const double* xp = B.upool + (int64_t)S->u_idx[U_PREV] * N;
+  const double* gp = PUSH ? B.gpool + (int64_t)S->g_idx[G_PREV] * N : nullptr;
+  double* gc = PUSH ? B.gpool + (int64_t)S->g_idx[G_CUR] * N : nullptr;
+  const int64_t slot = S->push_slot;
+  double* du = PUSH ? B.du + slot * N : nullptr;
+  double* dg = PUSH ? B.dg + slot * N : nullptr;
+  const double tau = P->tau;
+  const double* src[NE];
+  src[0] = x;
+  src[1] = B.c;
+  src[2] = B.l;
+  src[3] = B.u;
+  if constexpr (PUSH) {
+    src[4] = xp;
+    src[5] = gp;
+  }
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
-  if (tile < KT.ntiles) {
-    const int64_t N = P->N;
-    const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-    const double* y = x + P->n;
-    bool is_long;
-    const int j = tile_row(KT, tile, lane, is_long);
-    // epilogue operands first: independent of the SpMV, in flight with it
-    double xj = 0.0, cj = 0.0, lj = 0.0, uj = 0.0, xp = 0.0, gp = 0.0;
-    if (j >= 0) {
-      xj = x[j];
-      cj = __ldg(B.c + j);
-      lj = __ldg(B.l + j);
-      uj = __ldg(B.u + j);
-      if (PUSH) {
-        xp = B.upool[(int64_t)S->u_idx[U_PREV] * N + j];
-        gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + j];
-      }
+  int tile = blockIdx.x * kPipeWarps + warp;
+  int4 m = tile < KT.ntiles ? KT.meta[tile] : make_int4(0, 0, 0, 0);
+  if (tile < KT.ntiles) issue_tile<NE>(KT, m, stage[warp][0], src, lane);
+  for (int buf = 0; tile < KT.ntiles; buf ^= 1) {
+    const int next = tile + W;
+    int4 mn = m;
+    if (next < KT.ntiles) {
+      mn = KT.meta[next];
+      issue_tile<NE>(KT, mn, stage[warp][buf ^ 1], src, lane);
+    } else {
+      cp_async_commit();
     }
-    const double t = tile_sums<SERIAL>(KT, y, tile, prod[warp], lane, is_long);
+    cp_async_wait<1>();
+    __syncwarp();
+    WarpStage<NE>& st = stage[warp][buf];
+    const bool lg = tile_is_long(m);
+    double t;
+    const int j = tile_sums<SERIAL, NE>(KT, m, st, y, lane, t);
     if (j >= 0) {
-      double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-      double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));
+      const double xj = operand<NE>(st, lg, src, 0, j, lane);
+      const double cj = operand<NE>(st, lg, src, 1, j, lane);
+      const double lj = operand<NE>(st, lg, src, 2, j, lane);
+      const double uj = operand<NE>(st, lg, src, 3, j, lane);
+      double xn = __dsub_rn(xj, __dmul_rn(tau, __dsub_rn(cj, t)));
       xn = smin(smax(xn, lj), uj);
       xh[j] = xn;
       const double d = __dsub_rn(xn, xj);
@@ -317,24 +432,28 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
       if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
       const double dv = __dsub_rn(red_c, lam);
-      acc[P1_GX2] = __dmul_rn(d, d);
-      acc[P1_BOUND] = bt;
-      acc[P1_DUALSQ] = __dmul_rn(dv, dv);
-      acc[P1_CX] = __dmul_rn(cj, xj);
-      if (PUSH) {
-        const int64_t slot = S->push_slot;
-        B.du[slot * N + j] = __dsub_rn(xj, xp);
-        B.dg[slot * N + j] = __dsub_rn(d, gp);
-        B.gpool[(int64_t)S->g_idx[G_CUR] * N + j] = d;
+      acc[P1_GX2] = __dadd_rn(acc[P1_GX2], __dmul_rn(d, d));
+      acc[P1_BOUND] = __dadd_rn(acc[P1_BOUND], bt);
+      acc[P1_DUALSQ] = __dadd_rn(acc[P1_DUALSQ], __dmul_rn(dv, dv));
+      acc[P1_CX] = __dadd_rn(acc[P1_CX], __dmul_rn(cj, xj));
+      if constexpr (PUSH) {
+        du[j] = __dsub_rn(xj, operand<NE>(st, lg, src, 4, j, lane));
+        dg[j] = __dsub_rn(d, operand<NE>(st, lg, src, 5, j, lane));
+        gc[j] = d;
       }
       if (SERIAL) B.T[j] = t;
     }
+    __syncwarp();
+    tile = next;
+    m = mn;
   }
+  cp_async_wait<0>();
   if (!SERIAL) block_partials<P1_COUNT>(acc, wred, B.part1, P->nblk1);
 }
 
-__device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2, double bound, double qy,
-                              double cx, double infeas, double dual_sq);
+__device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2,
+                                           double bound, double qy, double cx, double infeas,
+                                           double dual_sq);
 
 // TREE mode: reduce all partials of K1/K2 and run the control (one CTA).
 __device__ __forceinline__ void control_from_partials(const IterBufs& B, const DevParams* P,
@@ -355,63 +474,89 @@ __device__ __forceinline__ void control_from_partials(const IterBufs& B, const D
 //                                                         pdhg_core.cpp:55-60
 //   K xhat cached as the next K x (solver.cpp:90 / pdhg_core.cpp:56)
 //   partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
+// TREE: the last CTA to finish reduces every partial and runs the control.
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+__global__ void __launch_bounds__(kPipeThreads, kPipeBlocksPerSM)
     k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
-  __shared__ double prod[kWarps][kWarpTile];
-  __shared__ double wred[kWarps][P2_COUNT];
+  constexpr int NE = PUSH ? 5 : 3;
+  __shared__ WarpStage<NE> stage[kPipeWarps][2];
+  __shared__ double wred[kPipeWarps][P2_COUNT];
   __shared__ int is_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kWarps + warp;
+  const int W = gridDim.x * kPipeWarps;
+  const int64_t N = P->N;
+  const int n = P->n, mr = P->mrows, m1 = P->m1;
+  const double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+  const double* y = B.upool + (int64_t)S->u_idx[U_CUR] * N + n;
+  double* yh = B.upool + (int64_t)S->u_idx[U_HAT] * N + n;
+  const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
+  double* kxh = B.kxpool + (int64_t)S->kx_idx[KX_HAT] * mr;
+  const int64_t slot = S->push_slot;
+  double* du = PUSH ? B.du + slot * N + n : nullptr;
+  double* dg = PUSH ? B.dg + slot * N + n : nullptr;
+  double* gc = PUSH ? B.gpool + (int64_t)S->g_idx[G_CUR] * N + n : nullptr;
+  const double sigma = P->sigma;
+  const double* src[NE];
+  src[0] = y;
+  src[1] = B.q;
+  src[2] = kx;
+  if constexpr (PUSH) {
+    src[3] = B.upool + (int64_t)S->u_idx[U_PREV] * N + n;
+    src[4] = B.gpool + (int64_t)S->g_idx[G_PREV] * N + n;
+  }
   double acc[P2_COUNT] = {0.0, 0.0, 0.0};
-  if (tile < K.ntiles) {
-    const int64_t N = P->N;
-    const int n = P->n, mr = P->mrows;
-    const double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-    bool is_long;
-    const int i = tile_row(K, tile, lane, is_long);
-    const double* u = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-    double yi = 0.0, qi = 0.0, kxi = 0.0, yp = 0.0, gp = 0.0;
-    if (i >= 0) {
-      yi = u[n + i];
-      qi = __ldg(B.q + i);
-      kxi = B.kxpool[(int64_t)S->kx_idx[KX_CUR] * mr + i];
-      if (PUSH) {
-        yp = B.upool[(int64_t)S->u_idx[U_PREV] * N + n + i];
-        gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + n + i];
-      }
+  int tile = blockIdx.x * kPipeWarps + warp;
+  int4 m = tile < K.ntiles ? K.meta[tile] : make_int4(0, 0, 0, 0);
+  if (tile < K.ntiles) issue_tile<NE>(K, m, stage[warp][0], src, lane);
+  for (int buf = 0; tile < K.ntiles; buf ^= 1) {
+    const int next = tile + W;
+    int4 mn = m;
+    if (next < K.ntiles) {
+      mn = K.meta[next];
+      issue_tile<NE>(K, mn, stage[warp][buf ^ 1], src, lane);
+    } else {
+      cp_async_commit();
     }
-    const double s = tile_sums<SERIAL>(K, xh, tile, prod[warp], lane, is_long);
+    cp_async_wait<1>();
+    __syncwarp();
+    WarpStage<NE>& st = stage[warp][buf];
+    const bool lg = tile_is_long(m);
+    double s;
+    const int i = tile_sums<SERIAL, NE>(K, m, st, xh, lane, s);
     if (i >= 0) {
-      double* uh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-      double* kxh = B.kxpool + (int64_t)S->kx_idx[KX_HAT] * mr;
+      const double yi = operand<NE>(st, lg, src, 0, i, lane);
+      const double qi = operand<NE>(st, lg, src, 1, i, lane);
+      const double kxi = operand<NE>(st, lg, src, 2, i, lane);
       double yn =
-          __dadd_rn(yi, __dmul_rn(P->sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
-      if (i < P->m1) yn = smax(yn, 0.0);
-      uh[n + i] = yn;
+          __dadd_rn(yi, __dmul_rn(sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
+      if (i < m1) yn = smax(yn, 0.0);
+      yh[i] = yn;
       kxh[i] = s;
       const double d = __dsub_rn(yn, yi);
       double v = __dsub_rn(qi, kxi);
-      if (i < P->m1) v = smax(v, 0.0);
-      acc[P2_GY2] = __dmul_rn(d, d);
-      acc[P2_QY] = __dmul_rn(qi, yi);
-      acc[P2_INFEAS] = __dmul_rn(v, v);
-      if (PUSH) {
-        const int64_t slot = S->push_slot;
-        B.du[slot * N + n + i] = __dsub_rn(yi, yp);
-        B.dg[slot * N + n + i] = __dsub_rn(d, gp);
-        B.gpool[(int64_t)S->g_idx[G_CUR] * N + n + i] = d;
+      if (i < m1) v = smax(v, 0.0);
+      acc[P2_GY2] = __dadd_rn(acc[P2_GY2], __dmul_rn(d, d));
+      acc[P2_QY] = __dadd_rn(acc[P2_QY], __dmul_rn(qi, yi));
+      acc[P2_INFEAS] = __dadd_rn(acc[P2_INFEAS], __dmul_rn(v, v));
+      if constexpr (PUSH) {
+        du[i] = __dsub_rn(yi, operand<NE>(st, lg, src, 3, i, lane));
+        dg[i] = __dsub_rn(d, operand<NE>(st, lg, src, 4, i, lane));
+        gc[i] = d;
       }
     }
+    __syncwarp();
+    tile = next;
+    m = mn;
   }
+  cp_async_wait<0>();
   if (SERIAL) return;
   block_partials<P2_COUNT>(acc, wred, B.part2, P->nblk2);
   // last CTA to finish reduces all partials and runs the control logic
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned t = atomicAdd(&S->ticket, 1u);
-    is_last = (t == gridDim.x - 1);
+    const unsigned tk = atomicAdd(&S->ticket, 1u);
+    is_last = (tk == gridDim.x - 1);
   }
   __syncthreads();
   if (!is_last) return;

@@ -1,8 +1,11 @@
 """Short, deterministic workload for ncu captures: BASELINE configs[1]
 (100k x 200k, 4M nnz), AA-PDHG m=10, explicit step size (no power
 iteration), 40 iterations through the C-ABI. Not a benchmark."""
+import os
 import sys
 from pathlib import Path
+
+os.environ.setdefault("AAPDHG_EAGER", "1")  # ncu cannot see kernels of conditional graphs
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2508_08062_b200 import Method, Solver, SolverConfig, problems  # noqa: E402
