@@ -24,7 +24,6 @@ namespace aapdhg_b200 {
 
 constexpr int kThreads = 256;        // CTA size of the tile kernels
 constexpr int kWarps = kThreads / 32;
-constexpr int kWarpTile = 256;       // nnz staged per warp tile (8 per lane)
 constexpr int kMaxMemory = 64;       // largest AA memory capacity supported
 constexpr int kDotChunk = 512;       // elements per CTA in the tree multi-dot
 constexpr int kCtrlThreads = 256;
@@ -47,9 +46,7 @@ struct CsrDev {
   const int32_t* ci = nullptr;
   const double* v = nullptr;
   int32_t ntiles = 0;
-  const int4* meta = nullptr;     // per warp tile {r0, r1, e0, e1}
-  int32_t grid_blocks = 0;        // persistent grid of the tile kernels
-  int32_t grid() const { return grid_blocks; }
+  const int4* meta = nullptr;     // per row block {r0, r1, e0, e1}
 };
 
 // Constant per solve (written before the loop starts).
@@ -92,6 +89,37 @@ struct DevState {
   uint64_t loop_iters;             // iterations that did work (launch accounting)
   uint32_t ticket;                 // last-CTA election in k_primal_side
   int32_t batch_left;              // iterations left in this graph launch
+};
+
+// Gathered vector: a plain pointer, or a role of the iterate pool resolved
+// on the device (graph replay rotates roles).
+struct VecRef {
+  const double* p;      // used when pool == nullptr
+  const double* pool;   // upool base
+  int32_t role;
+  int64_t stride;       // N
+  int64_t offset;       // 0 for x, n for y
+  __device__ __forceinline__ const double* get(const DevState* S) const {
+    return pool ? pool + (int64_t)S->u_idx[role] * stride + offset : p;
+  }
+};
+
+struct GatherArgs {
+  VecRef x;
+  double* prod;
+  int32_t pred_aa_ok;   // run only when S->aa_ok
+  const int32_t* stop;  // optional: skip when *stop != 0 (power iteration)
+};
+
+// out[r] = sum of row r's products (power iteration, K x recache, matvec).
+struct RowsumArgs {
+  const double* prod;
+  double* out;           // used when out_pool == nullptr
+  double* out_pool;      // kxpool base: out = out_pool + kx_idx[out_role]*out_stride
+  int32_t out_role;
+  int64_t out_stride;
+  int32_t pred_aa_ok;
+  const int32_t* stop;
 };
 
 struct CudaError : std::runtime_error {

@@ -32,18 +32,18 @@ constexpr uint64_t kRecCap = 1 << 16;  // device record ring
 constexpr uint64_t kPowTabMax = 1 << 22;
 constexpr int kPowerBatch = 8;
 
-// Warp tiles: consecutive rows, at most 32 rows and kWarpTile nonzeros;
-// a row longer than kWarpTile forms a tile of its own.
+// Row blocks: consecutive rows, at most kRowsPerBlock rows and kTile
+// nonzeros; a row longer than kTile forms a block of its own.
 std::vector<int32_t> build_tiles(const int32_t* rp, int nrows) {
   std::vector<int32_t> t{0};
   int r = 0;
   while (r < nrows) {
     const int start = r;
-    if (rp[r + 1] - rp[r] > kWarpTile) {
+    if (rp[r + 1] - rp[r] > kTile) {
       ++r;
     } else {
       int64_t nz = 0;
-      while (r < nrows && r - start < 32 && nz + (rp[r + 1] - rp[r]) <= kWarpTile) {
+      while (r < nrows && r - start < kRowsPerBlock && nz + (rp[r + 1] - rp[r]) <= kTile) {
         nz += rp[r + 1] - rp[r];
         ++r;
       }
@@ -119,10 +119,46 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
   h2d(d_v.p, v, sizeof(double) * nnz, stream_);
   h2d(d_meta.p, meta.data(), sizeof(int4) * ntiles, stream_);
   sync();  // host vectors go out of scope
-  const int64_t want = (int64_t(ntiles) + kPipeWarps - 1) / kPipeWarps;
-  const int64_t cap = int64_t(num_sms_) * kPipeBlocksPerSM;
   out = CsrDev{nrows, ncols, nnz, d_rp.as<int32_t>(), d_ci.as<int32_t>(), d_v.as<double>(),
-               ntiles, d_meta.as<int4>(), int32_t(std::max<int64_t>(1, std::min(want, cap)))};
+               ntiles, d_meta.as<int4>()};
+}
+
+// out = A x: k_gather (products) + k_rowsum (CSR-ordered row sums).
+int Problem::spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const RowsumArgs& o,
+                  bool serial, const DevState* S, int pred, const int32_t* stop) {
+  int nodes = 0;
+  if (A.nnz > 0) {
+    GatherArgs g{x, prod_.as<double>(), pred, stop};
+    prof_begin(s, "k_gather");
+    k_gather<<<gather_grid(A), kThreads, 0, s>>>(A, g, S);
+    prof_end(s);
+    ++nodes;
+  }
+  if (A.ntiles > 0) {
+    RowsumArgs r = o;
+    r.prod = prod_.as<double>();
+    r.pred_aa_ok = pred;
+    r.stop = stop;
+    prof_begin(s, "k_rowsum");
+    if (serial) k_rowsum<true><<<A.ntiles, kThreads, 0, s>>>(A, r, S);
+    else k_rowsum<false><<<A.ntiles, kThreads, 0, s>>>(A, r, S);
+    prof_end(s);
+    ++nodes;
+  }
+  AAPDHG_CUDA(cudaGetLastError());
+  return nodes;
+}
+
+int Problem::gather_grid(const CsrDev& A) const {
+  return int(std::max<int64_t>(1, std::min<int64_t>((A.nnz + kThreads - 1) / kThreads,
+                                                   int64_t(num_sms_) * kGatherBlocksPerSM)));
+}
+
+static VecRef vref(const double* p) { return VecRef{p, nullptr, 0, 0, 0}; }
+static RowsumArgs rout(double* out) {
+  RowsumArgs r{};
+  r.out = out;
+  return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -185,6 +221,7 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   }
   upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_rp_, t_ci_, t_v_, t_tile_, KT_);
 
+  prod_.reserve(sizeof(double) * (std::max<int64_t>(nnz_, 1) + 16));
   c_.reserve(sizeof(double) * n_);
   q_.reserve(sizeof(double) * m_);
   l_.reserve(sizeof(double) * n_);
@@ -260,7 +297,7 @@ double Problem::device_dot(const double* a, const double* b, int64_t n, bool ser
 }
 
 void Problem::ensure_iter_buffers(int method, int cap) {
-  const int nblk1 = KT_.grid(), nblk2 = K_.grid();
+  const int nblk1 = KT_.ntiles, nblk2 = K_.ntiles;
   upool_.reserve(sizeof(double) * 4 * std::max<int64_t>(N_, 1));
   kxpool_.reserve(sizeof(double) * 3 * std::max<int64_t>(m_, 1));
   T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
@@ -297,19 +334,8 @@ void Problem::kkt_eval(int slot, bool serial, double* out_dev, double* lam_dev) 
   const double* y = x + n_;
   double* T = T_.as<double>();
   double* KX = pw_mx_.as<double>();
-  SpmvArgs a{};
-  if (n_ && KT_.ntiles) {
-    a.x = y;
-    a.out = T;
-    if (serial) k_spmv<true><<<KT_.grid(), kPipeThreads, 0, stream_>>>(KT_, a, nullptr);
-    else k_spmv<false><<<KT_.grid(), kPipeThreads, 0, stream_>>>(KT_, a, nullptr);
-  }
-  if (m_ && K_.ntiles) {
-    a.x = x;
-    a.out = KX;
-    if (serial) k_spmv<true><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
-    else k_spmv<false><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
-  }
+  if (n_) spmv(stream_, KT_, vref(y), rout(T), serial, nullptr, 0, nullptr);
+  if (m_) spmv(stream_, K_, vref(x), rout(KX), serial, nullptr, 0, nullptr);
   const int64_t nbig = std::max<int64_t>(std::max<int64_t>(n_, m_), 1);
   const int nb = int((nbig + kThreads - 1) / kThreads);
   k_kkt_terms<<<nb, kThreads, 0, stream_>>>(x, y, T, KX, c_.as<double>(), q_.as<double>(),
@@ -381,17 +407,27 @@ void Problem::prof_collect() {
 int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   int nodes = 0;
   const bool ser = su.serial, push = su.push;
-  if (su.nblk1 > 0) {
-    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<su.nblk1, kPipeThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<su.nblk1, kPipeThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<su.nblk1, kPipeThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else LAUNCH("k_dual_side", k_dual_side<false, false><<<su.nblk1, kPipeThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+  // K'y: products of K' with y = u_cur[n:], then the fused dual-side rows
+  if (n_ > 0) {
+    if (KT_.nnz > 0) {
+      GatherArgs g{VecRef{nullptr, su.B.upool, U_CUR, N_, n_}, su.B.prod, 0, nullptr};
+      LAUNCH("k_gather", k_gather<<<gather_grid(KT_), kThreads, 0, s>>>(KT_, g, su.S));
+    }
+    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KT_.ntiles, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KT_.ntiles, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KT_.ntiles, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KT_.ntiles, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
   }
-  if (su.nblk2 > 0) {
-    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<su.nblk2, kPipeThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<su.nblk2, kPipeThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<su.nblk2, kPipeThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else LAUNCH("k_primal_side", k_primal_side<false, false><<<su.nblk2, kPipeThreads, 0, s>>>(K_, su.B, su.P, su.S));
+  // K xhat: products of K with xhat = u_hat[:n], then the fused dual step
+  if (m_ > 0) {
+    if (K_.nnz > 0) {
+      GatherArgs g{VecRef{nullptr, su.B.upool, U_HAT, N_, 0}, su.B.prod, 0, nullptr};
+      LAUNCH("k_gather", k_gather<<<gather_grid(K_), kThreads, 0, s>>>(K_, g, su.S));
+    }
+    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<K_.ntiles, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<K_.ntiles, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<K_.ntiles, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else LAUNCH("k_primal_side", k_primal_side<false, false><<<K_.ntiles, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
   }
   if (ser) LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
   AAPDHG_CUDA(cudaGetLastError());
@@ -409,17 +445,13 @@ int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
   }
   LAUNCH("k_aa_solve", k_aa_solve<<<1, 1024, 0, s>>>(su.D, su.W, su.P, su.S, 0));
   LAUNCH("k_mix", k_mix<<<grid_for(N_), kThreads, 0, s>>>(su.B, su.B.dg, su.P, su.S, 1));
-  if (K_.ntiles > 0) {
-    SpmvArgs a{};
-    a.x_pool = su.B.upool;
-    a.x_role = U_CAND;
-    a.x_stride = N_;
-    a.out_pool = su.B.kxpool;
-    a.out_role = KX_CAND;
-    a.out_stride = m_;
-    a.pred_aa_ok = 1;
-    if (su.serial) LAUNCH("k_spmv_recache", k_spmv<true><<<K_.grid(), kPipeThreads, 0, s>>>(K_, a, su.S));
-    else LAUNCH("k_spmv_recache", k_spmv<false><<<K_.grid(), kPipeThreads, 0, s>>>(K_, a, su.S));
+  if (m_ > 0) {  // K x recache of the accepted candidate
+    RowsumArgs r{};
+    r.out_pool = su.B.kxpool;
+    r.out_role = KX_CAND;
+    r.out_stride = m_;
+    nodes += spmv(s, K_, VecRef{nullptr, su.B.upool, U_CAND, N_, 0}, r, su.serial, su.S, 1,
+                  nullptr);
   }
   AAPDHG_CUDA(cudaGetLastError());
   return nodes;
@@ -526,24 +558,11 @@ void Problem::run_power(const double* x0, int max_iters, double rel_tol, bool se
   h.max_iters = max_iters;
   h.rel_tol = rel_tol;
   h2d(ps, &h, sizeof h, stream_);
-  SpmvArgs a1{}, a2{};
-  a1.x = x;
-  a1.out = mx;
-  a1.stop = &ps->done;
-  a2.x = mx;
-  a2.out = mtmx;
-  a2.stop = &ps->done;
   PowerState hs{};
   for (;;) {
     for (int r = 0; r < kPowerBatch; ++r) {
-      if (K_.ntiles) {
-        if (serial) k_spmv<true><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a1, nullptr);
-        else k_spmv<false><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a1, nullptr);
-      }
-      if (KT_.ntiles) {
-        if (serial) k_spmv<true><<<KT_.grid(), kPipeThreads, 0, stream_>>>(KT_, a2, nullptr);
-        else k_spmv<false><<<KT_.grid(), kPipeThreads, 0, stream_>>>(KT_, a2, nullptr);
-      }
+      spmv(stream_, K_, vref(x), rout(mx), serial, nullptr, 0, &ps->done);
+      spmv(stream_, KT_, vref(mx), rout(mtmx), serial, nullptr, 0, &ps->done);
       if (!serial) k_sumsq_partials<<<nb, kThreads, 0, stream_>>>(mtmx, nullptr, n_, part, &ps->done);
       k_power_ctrl<<<1, kCtrlThreads, 0, stream_>>>(mtmx, n_, part, nb, serial, ps);
       k_scale<<<grid_for(n_), kThreads, 0, stream_>>>(x, mtmx, n_, ps, nullptr);
@@ -655,8 +674,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.pow_len = ptab.size();
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
-  P.nblk1 = KT_.grid();
-  P.nblk2 = K_.grid();
+  P.nblk1 = KT_.ntiles;
+  P.nblk2 = K_.ntiles;
   P.ndot_blk = ndot_tile_;
 
   DevState S0{};
@@ -669,8 +688,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   SolveSetup su;
   su.B = IterBufs{upool_.as<double>(), kxpool_.as<double>(), gpool_.as<double>(),
                   du_.as<double>(), dg_.as<double>(), T_.as<double>(), part1_.as<double>(),
-                  part2_.as<double>(), c_.as<double>(), q_.as<double>(), l_.as<double>(),
-                  u_.as<double>()};
+                  part2_.as<double>(), prod_.as<double>(), c_.as<double>(), q_.as<double>(),
+                  l_.as<double>(), u_.as<double>()};
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
                  partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
   su.W = SolveScratch{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
@@ -680,8 +699,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.push = method != AAPDHG_METHOD_PDHG;
   su.method = method;
   su.cap = cap;
-  su.nblk1 = KT_.grid();
-  su.nblk2 = K_.grid();
+  su.nblk1 = KT_.ntiles;
+  su.nblk2 = K_.ntiles;
   su.ndot_blk = ndot_tile_;
   su.items_max = num_items_host(std::max(cap, 1), method);
 
@@ -721,13 +740,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   h2d(S, &S0, sizeof S0, stream_);
   k_project_start<<<grid_for(N_, kThreads, 1 << 30), kThreads, 0, stream_>>>(
       upool_.as<double>(), l_.as<double>(), u_.as<double>(), n_, N_, m1_, S);
-  if (m_ && K_.ntiles) {
-    SpmvArgs a{};
-    a.x = upool_.as<double>();
-    a.out = kxpool_.as<double>();
-    if (serial) k_spmv<true><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
-    else k_spmv<false><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
-  }
+  if (m_) spmv(stream_, K_, vref(upool_.as<double>()), rout(kxpool_.as<double>()), serial, nullptr, 0,
+               nullptr);
   AAPDHG_CUDA(cudaGetLastError());
 
   uint64_t flushed = 0;
@@ -804,11 +818,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
 void Problem::matvec(const double* x, double* out) {
   AAPDHG_CUDA(cudaSetDevice(device_));
   h2d(pw_x_.p, x, sizeof(double) * n_, stream_);
-  SpmvArgs a{};
-  a.x = pw_x_.as<double>();
-  a.out = pw_mx_.as<double>();
-  if (K_.ntiles) k_spmv<true><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
-  AAPDHG_CUDA(cudaGetLastError());
+  spmv(stream_, K_, vref(pw_x_.as<double>()), rout(pw_mx_.as<double>()), true, nullptr, 0,
+       nullptr);
   d2h(out, pw_mx_.p, sizeof(double) * m_, stream_);
   sync();
 }
@@ -816,11 +827,8 @@ void Problem::matvec(const double* x, double* out) {
 void Problem::matvec_transpose(const double* y, double* out) {
   AAPDHG_CUDA(cudaSetDevice(device_));
   h2d(pw_mx_.p, y, sizeof(double) * m_, stream_);
-  SpmvArgs a{};
-  a.x = pw_mx_.as<double>();
-  a.out = pw_mtmx_.as<double>();
-  if (KT_.ntiles) k_spmv<true><<<KT_.grid(), kPipeThreads, 0, stream_>>>(KT_, a, nullptr);
-  AAPDHG_CUDA(cudaGetLastError());
+  spmv(stream_, KT_, vref(pw_mx_.as<double>()), rout(pw_mtmx_.as<double>()), true, nullptr, 0,
+       nullptr);
   d2h(out, pw_mtmx_.p, sizeof(double) * n_, stream_);
   sync();
 }
@@ -840,12 +848,8 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   AAPDHG_CUDA(cudaSetDevice(device_));
   ensure_iter_buffers(AAPDHG_METHOD_PDHG, 1);
   upload_iterate(0, x, y);
-  if (K_.ntiles) {
-    SpmvArgs a{};
-    a.x = upool_.as<double>();
-    a.out = kxpool_.as<double>();
-    k_spmv<true><<<K_.grid(), kPipeThreads, 0, stream_>>>(K_, a, nullptr);
-  }
+  spmv(stream_, K_, vref(upool_.as<double>()), rout(kxpool_.as<double>()), true, nullptr, 0,
+       nullptr);
   DevParams P{};
   P.method = AAPDHG_METHOD_PDHG;
   P.serial = 1;
@@ -855,20 +859,30 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   P.N = N_;
   P.tau = tau;
   P.sigma = sigma;
-  P.nblk1 = KT_.grid();
-  P.nblk2 = K_.grid();
+  P.nblk1 = KT_.ntiles;
+  P.nblk2 = K_.ntiles;
   const DevState S = identity_state();
   h2d(dparams_.p, &P, sizeof P, stream_);
   h2d(dstate_.p, &S, sizeof S, stream_);
   IterBufs B{upool_.as<double>(), kxpool_.as<double>(), nullptr, nullptr, nullptr,
-             T_.as<double>(), part1_.as<double>(), part2_.as<double>(), c_.as<double>(),
-             q_.as<double>(), l_.as<double>(), u_.as<double>()};
-  if (KT_.ntiles)
-    k_dual_side<true, false><<<KT_.grid(), kPipeThreads, 0, stream_>>>(
-        KT_, B, dparams_.as<DevParams>(), dstate_.as<DevState>());
-  if (K_.ntiles)
-    k_primal_side<true, false><<<K_.grid(), kPipeThreads, 0, stream_>>>(
-        K_, B, dparams_.as<DevParams>(), dstate_.as<DevState>());
+             T_.as<double>(), part1_.as<double>(), part2_.as<double>(), prod_.as<double>(),
+             c_.as<double>(), q_.as<double>(), l_.as<double>(), u_.as<double>()};
+  const DevParams* Pd = dparams_.as<DevParams>();
+  DevState* Sd = dstate_.as<DevState>();
+  if (n_) {
+    if (KT_.nnz) {
+      GatherArgs g{vref(upool_.as<double>() + n_), prod_.as<double>(), 0, nullptr};
+      k_gather<<<gather_grid(KT_), kThreads, 0, stream_>>>(KT_, g, Sd);
+    }
+    k_dual_side<true, false><<<KT_.ntiles, kThreads, 0, stream_>>>(KT_, B, Pd, Sd);
+  }
+  if (m_) {
+    if (K_.nnz) {
+      GatherArgs g{vref(upool_.as<double>() + 2 * N_), prod_.as<double>(), 0, nullptr};
+      k_gather<<<gather_grid(K_), kThreads, 0, stream_>>>(K_, g, Sd);
+    }
+    k_primal_side<true, false><<<K_.ntiles, kThreads, 0, stream_>>>(K_, B, Pd, Sd);
+  }
   AAPDHG_CUDA(cudaGetLastError());
   const double* hat = upool_.as<double>() + 2 * N_;
   d2h(xn, hat, sizeof(double) * n_, stream_);
@@ -940,7 +954,8 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
   SolveScratch W{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
   IterBufs B{upool_.as<double>(), kxpool_.as<double>(), gpool_.as<double>(), du_.as<double>(),
              dg_.as<double>(), T_.as<double>(), part1_.as<double>(), part2_.as<double>(),
-             c_.as<double>(), q_.as<double>(), l_.as<double>(), u_.as<double>()};
+             prod_.as<double>(), c_.as<double>(), q_.as<double>(), l_.as<double>(),
+             u_.as<double>()};
   const DevParams* Pd = dparams_.as<DevParams>();
   DevState* Sd = dstate_.as<DevState>();
   const int items = num_items_host(p, method);

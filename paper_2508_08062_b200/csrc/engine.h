@@ -64,6 +64,9 @@ class Problem {
  private:
   bool resolve_serial(int reduction) const;
   double device_dot(const double* a, const double* b, int64_t n, bool serial);
+  int spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const RowsumArgs& o, bool serial,
+           const DevState* S, int pred, const int32_t* stop);
+  int gather_grid(const CsrDev& A) const;
   void upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
                   DevBuf& d_rp, DevBuf& d_ci, DevBuf& d_v, DevBuf& d_meta, CsrDev& out);
   void ensure_iter_buffers(int method, int cap);
@@ -101,7 +104,7 @@ class Problem {
   bool bounds_ok_ = true;
   CsrDev K_, KT_;
   DevBuf k_rp_, k_ci_, k_v_, k_tile_, t_rp_, t_ci_, t_v_, t_tile_;
-  DevBuf c_, q_, l_, u_;
+  DevBuf c_, q_, l_, u_, prod_;
   double nrm_q_[2] = {0, 0}, nrm_c_[2] = {0, 0};  // [serial, tree]
 
   // iteration buffers

@@ -114,21 +114,28 @@ __device__ __forceinline__ double serial_dot(const double* __restrict__ a,
 }
 
 // ---------------------------------------------------------------------------
-// pipelined warp-tile SpMV core
+// SpMV = gather-multiply pass + row-block reduce pass
 // ---------------------------------------------------------------------------
 //
-// Rows are grouped on the host into warp tiles (<= 32 rows, <= kWarpTile
-// nonzeros; a longer row is a tile of its own) described by int4 metadata
-// {r0, r1, e0, e1}. The tile kernels are persistent: warp w of the grid
-// handles tiles w, w + W, w + 2W, ... and keeps two tiles in flight — while
-// it gathers and sums tile t out of shared memory, cp.async is already
-// streaming tile t+W's (val, col) slice, its row offsets and the epilogue
-// operands of its rows (x, c, l, u, ...) into the other stage. In-flight
-// data costs no registers, so ~2 tiles x 20 warps per SM keep HBM busy.
+// Random-column SpMVs on B200 are bound by the L1TEX gather rate (~0.85
+// cycles per random 8-byte gather per SM, measured: profiles/microbench),
+// which needs ~512 gathers in flight per SM. So each SpMV is two kernels:
+//   k_gather   prod[e] = vals[e] * x[col[e]] over all nonzeros — lean
+//              (<= 32 registers, 2048 threads/SM, 8 gathers in flight per
+//              thread), nnz-parallel, hence perfectly load balanced for any
+//              row-length distribution (Zipf, transport rows);
+//   row kernels  CSR row blocks (<= kTile nonzeros, <= kRowsPerBlock rows;
+//              a longer row is a block of its own) staged by cp.async from
+//              the L2-resident products: thread r adds row r0 + r in CSR
+//              order — bit-identical to the reference's row-serial matvec
+//              (sparse_linalg.cpp:60-69) and, on the transposed CSR (entries
+//              in ascending original row), to its row-ordered scatter
+//              matvec_transpose (sparse_linalg.cpp:77-87) — then runs the
+//              fused PDHG epilogue of that row.
 
-constexpr int kPipeWarps = 4;  // warps per CTA of the tile kernels
-constexpr int kPipeThreads = 32 * kPipeWarps;
-constexpr int kPipeBlocksPerSM = 5;  // 5 x 38 KB of stages per SM
+constexpr int kTile = 2048;          // nonzeros per row block
+constexpr int kRowsPerBlock = kThreads;
+constexpr int kGatherBlocksPerSM = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -148,182 +155,139 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// One stage of a warp's pipeline. v/ci hold the 16-byte aligned superset of
-// the tile's [e0, e1) slice (offsets e0 & 1 and e0 & 3); products overwrite v.
+__device__ __forceinline__ bool skip_launch(const DevState* S, int pred_aa_ok,
+                                            const int32_t* stop) {
+  if (S) {
+    if (S->done) return true;
+    if (pred_aa_ok && !S->aa_ok) return true;
+  }
+  return stop && *stop;
+}
+
+// prod[e] = vals[e] * x[col[e]]: 8 coalesced (col, val) loads, then 8
+// independent gathers per thread in flight; matrix streams evict-first.
+__global__ void __launch_bounds__(kThreads, kGatherBlocksPerSM)
+    k_gather(CsrDev A, GatherArgs g, const DevState* S) {
+  if (skip_launch(S, g.pred_aa_ok, g.stop)) return;
+  const double* __restrict__ x = g.x.get(S);
+  double* __restrict__ prod = g.prod;
+  const int64_t nnz = A.nnz;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 7 * stride < nnz; i += 8 * stride) {
+    int c[8];
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      c[u] = __ldcs(A.ci + i + u * stride);
+      v[u] = __ldcs(A.v + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __dmul_rn(v[u], __ldg(x + c[u]));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) prod[i + u * stride] = v[u];
+  }
+  for (; i < nnz; i += stride) prod[i] = __dmul_rn(__ldcs(A.v + i), __ldg(x + __ldcs(A.ci + i)));
+}
+
+__device__ __forceinline__ bool block_is_long(const int4& m) {
+  return (m.y - m.x == 1) && (m.w - m.z > kTile);
+}
+
+// Shared-memory stage of a row block: the 16-byte aligned superset of
+// prod[e0, e1) (offset e0 & 1), the row offsets and NE epilogue operands.
 template <int NE>
-struct __align__(16) WarpStage {
-  double v[kWarpTile + 2];
-  int32_t ci[kWarpTile + 8];
-  int32_t rp[36];
-  double epi[NE > 0 ? NE : 1][32];
+struct __align__(16) RowStage {
+  double prod[kTile + 2];
+  int32_t rp[kRowsPerBlock + 4];
+  double epi[NE > 0 ? NE : 1][kRowsPerBlock];
 };
 
-__device__ __forceinline__ bool tile_is_long(const int4& m) {
-  return (m.y - m.x == 1) && (m.w - m.z > kWarpTile);
-}
-
-// Starts the async copies of tile m into stage st (one commit group, empty
-// for a long row, which is streamed synchronously when processed).
+// Copies row block m into st (cp.async, all threads), waits, syncs.
 template <int NE>
-__device__ __forceinline__ void issue_tile(const CsrDev& A, const int4& m, WarpStage<NE>& st,
-                                           const double* const* src, int lane) {
-  if (!tile_is_long(m)) {
-    const int r0 = m.x, r1 = m.y, e0 = m.z, e1 = m.w;
-    const int a0 = e0 & ~1, nv = (e1 - a0 + 1) >> 1;
-    for (int k = lane; k < nv; k += 32) cp_async16(&st.v[2 * k], A.v + a0 + 2 * k);
-    const int c0 = e0 & ~3, nc = (e1 - c0 + 3) >> 2;
-    for (int k = lane; k < nc; k += 32) cp_async16(&st.ci[4 * k], A.ci + c0 + 4 * k);
-    const int nr = r1 - r0;
-    for (int i = lane; i <= nr; i += 32) cp_async4(&st.rp[i], A.rp + r0 + i);
-    if (lane < nr)
+__device__ __forceinline__ void stage_rows(const int4& m, const int32_t* __restrict__ rp,
+                                           const double* __restrict__ prod, RowStage<NE>& st,
+                                           const double* const* src) {
+  const int r0 = m.x, r1 = m.y, e0 = m.z, e1 = m.w, nr = r1 - r0;
+  const int a0 = e0 & ~1, nv = (e1 - a0 + 1) >> 1;
+  for (int k = threadIdx.x; k < nv; k += blockDim.x) cp_async16(&st.prod[2 * k], prod + a0 + 2 * k);
+  for (int i = threadIdx.x; i <= nr; i += blockDim.x) cp_async4(&st.rp[i], rp + r0 + i);
 #pragma unroll
-      for (int q = 0; q < NE; ++q) cp_async8(&st.epi[q][lane], src[q] + r0 + lane);
-  }
+  for (int q = 0; q < NE; ++q)
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) cp_async8(&st.epi[q][i], src[q] + r0 + i);
   cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
 }
 
-// wprod[t] = vals[e0+t] * x[col[e0+t]], t < cnt <= kWarpTile (register path,
-// used for the chunks of long rows).
-__device__ __forceinline__ void warp_stage(const CsrDev& A, const double* __restrict__ x,
-                                           int64_t e0, int cnt, double* wprod, int lane) {
-  constexpr int U = 4;
-#pragma unroll 1
-  for (int base = 0; base < cnt; base += 32 * U) {
-    int c[U];
-    double a[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int t = base + lane + 32 * u;
-      if (t < cnt) {
-        c[u] = __ldcs(A.ci + e0 + t);
-        a[u] = __ldcs(A.v + e0 + t);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int t = base + lane + 32 * u;
-      if (t < cnt) wprod[t] = __dmul_rn(a[u], __ldg(x + c[u]));
-    }
-  }
-}
-
-// Sum of one long row (> kWarpTile nonzeros) by one warp, kWarpTile chunks;
-// SERIAL adds every product in CSR order in lane 0 (bitwise = reference),
-// TREE adds per-chunk warp trees in order. Valid in lane 0.
-template <bool SERIAL>
-__device__ double long_row_sum(const CsrDev& A, const double* __restrict__ x, int64_t e0,
-                               int64_t e1, double* wprod, int lane) {
+// Sum of one long row (> kTile nonzeros) by the whole CTA, kTile chunks:
+// SERIAL adds every product in CSR order in thread 0 (bitwise = reference),
+// TREE adds fixed per-chunk block trees in order. Valid in thread 0.
+template <bool SERIAL, int NE>
+__device__ double long_row_sum(const int4& m, const double* __restrict__ prod,
+                               RowStage<NE>& st, double* red) {
   double s = 0.0;
-  for (int64_t c0 = e0; c0 < e1; c0 += kWarpTile) {
-    const int cnt = (int)((e1 - c0) < kWarpTile ? (e1 - c0) : kWarpTile);
-    warp_stage(A, x, c0, cnt, wprod, lane);
-    __syncwarp();
+  for (int c0 = m.z; c0 < m.w; c0 += kTile) {
+    const int c1 = min(m.w, c0 + kTile);
+    const int a0 = c0 & ~1, nv = (c1 - a0 + 1) >> 1, vo = c0 & 1;
+    for (int k = threadIdx.x; k < nv; k += blockDim.x) cp_async16(&st.prod[2 * k], prod + a0 + 2 * k);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
     if (SERIAL) {
-      if (lane == 0)
-        for (int t = 0; t < cnt; ++t) s = __dadd_rn(s, wprod[t]);
+      if (threadIdx.x == 0)
+        for (int t = 0; t < c1 - c0; ++t) s = __dadd_rn(s, st.prod[vo + t]);
     } else {
-      double v = 0.0;
-      for (int t = lane; t < cnt; t += 32) v = __dadd_rn(v, wprod[t]);
-      s = __dadd_rn(s, warp_sum(v));
+      double v[1] = {0.0};
+      for (int t = threadIdx.x; t < c1 - c0; t += blockDim.x) v[0] = __dadd_rn(v[0], st.prod[vo + t]);
+      block_sum<1>(v, red);
+      if (threadIdx.x == 0) s = __dadd_rn(s, v[0]);
     }
-    __syncwarp();
+    __syncthreads();
   }
   return s;
 }
 
-// Row sums of a staged tile: gathers x[col] (8 per lane in flight), products
-// in place, then lane r adds row r0 + r in CSR order. Returns the lane's
-// row (-1 if none); `s` valid there.
+// Row sums of row block b. Returns this thread's row (-1 if none) with its
+// sum in s and `from_stage` telling whether the epilogue operands are staged.
 template <bool SERIAL, int NE>
-__device__ __forceinline__ int tile_sums(const CsrDev& A, const int4& m, WarpStage<NE>& st,
-                                         const double* __restrict__ x, int lane, double& s) {
-  const int r0 = m.x, r1 = m.y, e0 = m.z, e1 = m.w;
+__device__ __forceinline__ int block_rows(const CsrDev& A, const double* __restrict__ prod,
+                                          RowStage<NE>& st, const double* const* src,
+                                          double* red, double& s, bool& from_stage) {
+  const int4 m = A.meta[blockIdx.x];
   s = 0.0;
-  if (tile_is_long(m)) {
-    s = long_row_sum<SERIAL>(A, x, e0, e1, st.v, lane);
-    return lane == 0 ? r0 : -1;
+  if (block_is_long(m)) {
+    from_stage = false;
+    s = long_row_sum<SERIAL, NE>(m, prod, st, red);
+    return threadIdx.x == 0 ? m.x : -1;
   }
-  const int cnt = e1 - e0, vo = e0 & 1, co = e0 & 3;
-  double g[kWarpTile / 32];
-#pragma unroll
-  for (int u = 0; u < kWarpTile / 32; ++u) {
-    const int t = lane + 32 * u;
-    if (t < cnt) g[u] = __ldg(x + st.ci[co + t]);
-  }
-#pragma unroll
-  for (int u = 0; u < kWarpTile / 32; ++u) {
-    const int t = lane + 32 * u;
-    if (t < cnt) st.v[vo + t] = __dmul_rn(st.v[vo + t], g[u]);
-  }
-  __syncwarp();
-  if (lane >= r1 - r0) return -1;
-  const int a = st.rp[lane] - e0, z = st.rp[lane + 1] - e0;
+  from_stage = true;
+  stage_rows<NE>(m, A.rp, prod, st, src);
+  const int r = threadIdx.x;
+  if (r >= m.y - m.x) return -1;
+  const int vo = m.z & 1;
+  const int a = st.rp[r] - m.z, z = st.rp[r + 1] - m.z;
   double acc = 0.0;
-  for (int e = a; e < z; ++e) acc = __dadd_rn(acc, st.v[vo + e]);
+  for (int e = a; e < z; ++e) acc = __dadd_rn(acc, st.prod[vo + e]);
   s = acc;
-  return r0 + lane;
+  return m.x + r;
 }
-
-// Epilogue operand q of the lane's row: staged, or read directly for a long row.
-template <int NE>
-__device__ __forceinline__ double operand(const WarpStage<NE>& st, bool is_long,
-                                          const double* const* src, int q, int row, int lane) {
-  return is_long ? src[q][row] : st.epi[q][lane];
-}
-
-// out[r] = (A x)_r — power iteration, K x recache, per-op matvec.
-struct SpmvArgs {
-  const double* x;       // used when x_pool == nullptr
-  double* out;           // used when out_pool == nullptr
-  const double* x_pool;  // upool base: x = x_pool + u_idx[x_role]*x_stride
-  double* out_pool;      // kxpool base: out = out_pool + kx_idx[out_role]*out_stride
-  int32_t x_role, out_role;
-  int64_t x_stride, out_stride;
-  int32_t pred_aa_ok;    // run only when S->aa_ok
-  const int32_t* stop;   // optional: skip when *stop != 0 (power iteration)
-};
 
 template <bool SERIAL>
-__global__ void __launch_bounds__(kPipeThreads, kPipeBlocksPerSM)
-    k_spmv(CsrDev A, SpmvArgs g, const DevState* S) {
-  if (S) {
-    if (S->done) return;
-    if (g.pred_aa_ok && !S->aa_ok) return;
-  }
-  if (g.stop && *g.stop) return;
-  __shared__ WarpStage<0> stage[kPipeWarps][2];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int W = gridDim.x * kPipeWarps;
-  const double* x = g.x_pool ? g.x_pool + (int64_t)S->u_idx[g.x_role] * g.x_stride : g.x;
+__global__ void __launch_bounds__(kThreads) k_rowsum(CsrDev A, RowsumArgs g, const DevState* S) {
+  if (skip_launch(S, g.pred_aa_ok, g.stop)) return;
+  __shared__ RowStage<0> st;
+  __shared__ double red[kWarps];
   double* out = g.out_pool ? g.out_pool + (int64_t)S->kx_idx[g.out_role] * g.out_stride : g.out;
   const double* const src[1] = {nullptr};
-  int tile = blockIdx.x * kPipeWarps + warp;
-  if (tile >= A.ntiles) return;
-  int4 m = A.meta[tile];
-  issue_tile<0>(A, m, stage[warp][0], src, lane);
-  for (int buf = 0; tile < A.ntiles; buf ^= 1) {
-    const int next = tile + W;
-    int4 mn = m;
-    if (next < A.ntiles) {
-      mn = A.meta[next];
-      issue_tile<0>(A, mn, stage[warp][buf ^ 1], src, lane);
-    } else {
-      cp_async_commit();
-    }
-    cp_async_wait<1>();
-    __syncwarp();
-    double s;
-    const int row = tile_sums<SERIAL, 0>(A, m, stage[warp][buf], x, lane, s);
-    if (row >= 0) out[row] = s;
-    __syncwarp();
-    tile = next;
-    m = mn;
-  }
-  cp_async_wait<0>();
+  double s;
+  bool fs;
+  const int row = block_rows<SERIAL, 0>(A, g.prod, st, src, red, s, fs);
+  if (row >= 0) out[row] = s;
 }
 
 // ---------------------------------------------------------------------------
-// the fused PDHG halves
+// the fused PDHG halves (row kernels)
 // ---------------------------------------------------------------------------
 
 struct IterBufs {
@@ -335,120 +299,77 @@ struct IterBufs {
   double* T;       // n
   double* part1;   // P1_COUNT x nblk1
   double* part2;   // P2_COUNT x nblk2
+  double* prod;    // max(nnz) products of the current SpMV
   const double* c;
   const double* q;
   const double* l;
   const double* u;
 };
 
-// Adds the warps' acc[] in order into part[q * nb + blockIdx.x].
-template <int NV>
-__device__ __forceinline__ void block_partials(double (&acc)[NV], double (*wred)[NV],
-                                               double* part, int nb) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int q = 0; q < NV; ++q) acc[q] = warp_sum(acc[q]);
-  if (lane == 0)
-#pragma unroll
-    for (int q = 0; q < NV; ++q) wred[warp][q] = acc[q];
-  __syncthreads();
-  if (threadIdx.x == 0)
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      double s = wred[0][q];
-#pragma unroll
-      for (int w = 1; w < kPipeWarps; ++w) s = __dadd_rn(s, wred[w][q]);
-      part[q * nb + blockIdx.x] = s;
-    }
-}
-
-// K1: t = (K'y)_j (row j of K' = column j of K), then
+// K1 row kernel on K' (row j of K' = column j of K), t = (K'y)_j:
 //   xhat_j = min(max(x_j - tau (c_j - t), l_j), u_j)      pdhg_core.cpp:49-53
 //   lambda_j = P_Lambda(c_j - t)                           solver.cpp:67-71
 //   partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
 //   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
-// Per-lane partial sums run over the warp's tiles in a fixed order, so the
-// CTA partials are deterministic.
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kPipeThreads, kPipeBlocksPerSM)
+__global__ void __launch_bounds__(kThreads)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
   constexpr int NE = PUSH ? 6 : 4;
-  __shared__ WarpStage<NE> stage[kPipeWarps][2];
-  __shared__ double wred[kPipeWarps][P1_COUNT];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int W = gridDim.x * kPipeWarps;
+  __shared__ RowStage<NE> st;
+  __shared__ double red[P1_COUNT * kWarps];
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-  const double* y = x + P->n;
-  double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-  const double* xp = B.upool + (int64_t)S->u_idx[U_PREV] * N;
-  const double* gp = PUSH ? B.gpool + (int64_t)S->g_idx[G_PREV] * N : nullptr;
-  double* gc = PUSH ? B.gpool + (int64_t)S->g_idx[G_CUR] * N : nullptr;
-  const int64_t slot = S->push_slot;
-  double* du = PUSH ? B.du + slot * N : nullptr;
-  double* dg = PUSH ? B.dg + slot * N : nullptr;
-  const double tau = P->tau;
   const double* src[NE];
   src[0] = x;
   src[1] = B.c;
   src[2] = B.l;
   src[3] = B.u;
   if constexpr (PUSH) {
-    src[4] = xp;
-    src[5] = gp;
+    src[4] = B.upool + (int64_t)S->u_idx[U_PREV] * N;
+    src[5] = B.gpool + (int64_t)S->g_idx[G_PREV] * N;
   }
+  double t;
+  bool fs;
+  const int j = block_rows<SERIAL, NE>(KT, B.prod, st, src, red, t, fs);
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
-  int tile = blockIdx.x * kPipeWarps + warp;
-  int4 m = tile < KT.ntiles ? KT.meta[tile] : make_int4(0, 0, 0, 0);
-  if (tile < KT.ntiles) issue_tile<NE>(KT, m, stage[warp][0], src, lane);
-  for (int buf = 0; tile < KT.ntiles; buf ^= 1) {
-    const int next = tile + W;
-    int4 mn = m;
-    if (next < KT.ntiles) {
-      mn = KT.meta[next];
-      issue_tile<NE>(KT, mn, stage[warp][buf ^ 1], src, lane);
-    } else {
-      cp_async_commit();
+  if (j >= 0) {
+    const int r = fs ? (int)threadIdx.x : 0;
+    const double xj = fs ? st.epi[0][r] : src[0][j];
+    const double cj = fs ? st.epi[1][r] : src[1][j];
+    const double lj = fs ? st.epi[2][r] : src[2][j];
+    const double uj = fs ? st.epi[3][r] : src[3][j];
+    double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+    double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));
+    xn = smin(smax(xn, lj), uj);
+    xh[j] = xn;
+    const double d = __dsub_rn(xn, xj);
+    const double red_c = __dsub_rn(cj, t);
+    const double lam = project_lambda1(red_c, lj, uj);
+    double bt = 0.0;
+    if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
+    if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
+    const double dv = __dsub_rn(red_c, lam);
+    acc[P1_GX2] = __dmul_rn(d, d);
+    acc[P1_BOUND] = bt;
+    acc[P1_DUALSQ] = __dmul_rn(dv, dv);
+    acc[P1_CX] = __dmul_rn(cj, xj);
+    if constexpr (PUSH) {
+      const int64_t slot = S->push_slot;
+      const double xp = fs ? st.epi[4][r] : src[4][j];
+      const double gp = fs ? st.epi[5][r] : src[5][j];
+      B.du[slot * N + j] = __dsub_rn(xj, xp);
+      B.dg[slot * N + j] = __dsub_rn(d, gp);
+      B.gpool[(int64_t)S->g_idx[G_CUR] * N + j] = d;
     }
-    cp_async_wait<1>();
-    __syncwarp();
-    WarpStage<NE>& st = stage[warp][buf];
-    const bool lg = tile_is_long(m);
-    double t;
-    const int j = tile_sums<SERIAL, NE>(KT, m, st, y, lane, t);
-    if (j >= 0) {
-      const double xj = operand<NE>(st, lg, src, 0, j, lane);
-      const double cj = operand<NE>(st, lg, src, 1, j, lane);
-      const double lj = operand<NE>(st, lg, src, 2, j, lane);
-      const double uj = operand<NE>(st, lg, src, 3, j, lane);
-      double xn = __dsub_rn(xj, __dmul_rn(tau, __dsub_rn(cj, t)));
-      xn = smin(smax(xn, lj), uj);
-      xh[j] = xn;
-      const double d = __dsub_rn(xn, xj);
-      const double red_c = __dsub_rn(cj, t);
-      const double lam = project_lambda1(red_c, lj, uj);
-      double bt = 0.0;
-      if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
-      if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
-      const double dv = __dsub_rn(red_c, lam);
-      acc[P1_GX2] = __dadd_rn(acc[P1_GX2], __dmul_rn(d, d));
-      acc[P1_BOUND] = __dadd_rn(acc[P1_BOUND], bt);
-      acc[P1_DUALSQ] = __dadd_rn(acc[P1_DUALSQ], __dmul_rn(dv, dv));
-      acc[P1_CX] = __dadd_rn(acc[P1_CX], __dmul_rn(cj, xj));
-      if constexpr (PUSH) {
-        du[j] = __dsub_rn(xj, operand<NE>(st, lg, src, 4, j, lane));
-        dg[j] = __dsub_rn(d, operand<NE>(st, lg, src, 5, j, lane));
-        gc[j] = d;
-      }
-      if (SERIAL) B.T[j] = t;
-    }
-    __syncwarp();
-    tile = next;
-    m = mn;
+    if (SERIAL) B.T[j] = t;
   }
-  cp_async_wait<0>();
-  if (!SERIAL) block_partials<P1_COUNT>(acc, wred, B.part1, P->nblk1);
+  if (!SERIAL) {
+    block_sum<P1_COUNT>(acc, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int q = 0; q < P1_COUNT; ++q) B.part1[q * P->nblk1 + blockIdx.x] = acc[q];
+  }
 }
 
 __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2,
@@ -469,91 +390,65 @@ __device__ __forceinline__ void control_from_partials(const IterBufs& B, const D
   if (threadIdx.x == 0) control_logic(P, S, __dadd_rn(gx2, gy2), bound, qy, cx, inf, dsq);
 }
 
-// K2: s = (K xhat)_i, then
+// K2 row kernel on K, s = (K xhat)_i:
 //   yhat_i = y_i + sigma (q_i - (2 s - (K x)_i)), clamped >= 0 for i < m1
 //                                                         pdhg_core.cpp:55-60
 //   K xhat cached as the next K x (solver.cpp:90 / pdhg_core.cpp:56)
 //   partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
 // TREE: the last CTA to finish reduces every partial and runs the control.
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kPipeThreads, kPipeBlocksPerSM)
+__global__ void __launch_bounds__(kThreads)
     k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
   constexpr int NE = PUSH ? 5 : 3;
-  __shared__ WarpStage<NE> stage[kPipeWarps][2];
-  __shared__ double wred[kPipeWarps][P2_COUNT];
+  __shared__ RowStage<NE> st;
+  __shared__ double red[P2_COUNT * kWarps];
   __shared__ int is_last;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int W = gridDim.x * kPipeWarps;
   const int64_t N = P->N;
-  const int n = P->n, mr = P->mrows, m1 = P->m1;
-  const double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-  const double* y = B.upool + (int64_t)S->u_idx[U_CUR] * N + n;
-  double* yh = B.upool + (int64_t)S->u_idx[U_HAT] * N + n;
-  const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
-  double* kxh = B.kxpool + (int64_t)S->kx_idx[KX_HAT] * mr;
-  const int64_t slot = S->push_slot;
-  double* du = PUSH ? B.du + slot * N + n : nullptr;
-  double* dg = PUSH ? B.dg + slot * N + n : nullptr;
-  double* gc = PUSH ? B.gpool + (int64_t)S->g_idx[G_CUR] * N + n : nullptr;
-  const double sigma = P->sigma;
+  const int n = P->n, mr = P->mrows;
   const double* src[NE];
-  src[0] = y;
+  src[0] = B.upool + (int64_t)S->u_idx[U_CUR] * N + n;
   src[1] = B.q;
-  src[2] = kx;
+  src[2] = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
   if constexpr (PUSH) {
     src[3] = B.upool + (int64_t)S->u_idx[U_PREV] * N + n;
     src[4] = B.gpool + (int64_t)S->g_idx[G_PREV] * N + n;
   }
+  double s;
+  bool fs;
+  const int i = block_rows<SERIAL, NE>(K, B.prod, st, src, red, s, fs);
   double acc[P2_COUNT] = {0.0, 0.0, 0.0};
-  int tile = blockIdx.x * kPipeWarps + warp;
-  int4 m = tile < K.ntiles ? K.meta[tile] : make_int4(0, 0, 0, 0);
-  if (tile < K.ntiles) issue_tile<NE>(K, m, stage[warp][0], src, lane);
-  for (int buf = 0; tile < K.ntiles; buf ^= 1) {
-    const int next = tile + W;
-    int4 mn = m;
-    if (next < K.ntiles) {
-      mn = K.meta[next];
-      issue_tile<NE>(K, mn, stage[warp][buf ^ 1], src, lane);
-    } else {
-      cp_async_commit();
+  if (i >= 0) {
+    const int r = fs ? (int)threadIdx.x : 0;
+    const double yi = fs ? st.epi[0][r] : src[0][i];
+    const double qi = fs ? st.epi[1][r] : src[1][i];
+    const double kxi = fs ? st.epi[2][r] : src[2][i];
+    double yn =
+        __dadd_rn(yi, __dmul_rn(P->sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
+    if (i < P->m1) yn = smax(yn, 0.0);
+    B.upool[(int64_t)S->u_idx[U_HAT] * N + n + i] = yn;
+    B.kxpool[(int64_t)S->kx_idx[KX_HAT] * mr + i] = s;
+    const double d = __dsub_rn(yn, yi);
+    double v = __dsub_rn(qi, kxi);
+    if (i < P->m1) v = smax(v, 0.0);
+    acc[P2_GY2] = __dmul_rn(d, d);
+    acc[P2_QY] = __dmul_rn(qi, yi);
+    acc[P2_INFEAS] = __dmul_rn(v, v);
+    if constexpr (PUSH) {
+      const int64_t slot = S->push_slot;
+      const double yp = fs ? st.epi[3][r] : src[3][i];
+      const double gp = fs ? st.epi[4][r] : src[4][i];
+      B.du[slot * N + n + i] = __dsub_rn(yi, yp);
+      B.dg[slot * N + n + i] = __dsub_rn(d, gp);
+      B.gpool[(int64_t)S->g_idx[G_CUR] * N + n + i] = d;
     }
-    cp_async_wait<1>();
-    __syncwarp();
-    WarpStage<NE>& st = stage[warp][buf];
-    const bool lg = tile_is_long(m);
-    double s;
-    const int i = tile_sums<SERIAL, NE>(K, m, st, xh, lane, s);
-    if (i >= 0) {
-      const double yi = operand<NE>(st, lg, src, 0, i, lane);
-      const double qi = operand<NE>(st, lg, src, 1, i, lane);
-      const double kxi = operand<NE>(st, lg, src, 2, i, lane);
-      double yn =
-          __dadd_rn(yi, __dmul_rn(sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
-      if (i < m1) yn = smax(yn, 0.0);
-      yh[i] = yn;
-      kxh[i] = s;
-      const double d = __dsub_rn(yn, yi);
-      double v = __dsub_rn(qi, kxi);
-      if (i < m1) v = smax(v, 0.0);
-      acc[P2_GY2] = __dadd_rn(acc[P2_GY2], __dmul_rn(d, d));
-      acc[P2_QY] = __dadd_rn(acc[P2_QY], __dmul_rn(qi, yi));
-      acc[P2_INFEAS] = __dadd_rn(acc[P2_INFEAS], __dmul_rn(v, v));
-      if constexpr (PUSH) {
-        du[i] = __dsub_rn(yi, operand<NE>(st, lg, src, 3, i, lane));
-        dg[i] = __dsub_rn(d, operand<NE>(st, lg, src, 4, i, lane));
-        gc[i] = d;
-      }
-    }
-    __syncwarp();
-    tile = next;
-    m = mn;
   }
-  cp_async_wait<0>();
   if (SERIAL) return;
-  block_partials<P2_COUNT>(acc, wred, B.part2, P->nblk2);
-  // last CTA to finish reduces all partials and runs the control logic
+  block_sum<P2_COUNT>(acc, red);
   if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < P2_COUNT; ++q) B.part2[q * P->nblk2 + blockIdx.x] = acc[q];
+    // the last CTA to finish reduces all partials and runs the control
     __threadfence();
     const unsigned tk = atomicAdd(&S->ticket, 1u);
     is_last = (tk == gridDim.x - 1);
