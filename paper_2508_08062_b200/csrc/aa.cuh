@@ -147,9 +147,15 @@ struct SolveScratch {
 // Success: S->aa_ok, weights and mix columns set, i += 1.
 // SingularError: plain step, j += 1, aa_failures += 1 (solver.cpp:229-235).
 __global__ void __launch_bounds__(1024)
-    k_aa_solve(DotBufs D, SolveScratch W, const DevParams* __restrict__ P, DevState* S,
-               int per_op) {
-  if (S->done || !S->aa_attempt) return;
+    k_aa_solve(DotBufs D, const DevParams* __restrict__ P, DevState* Sg, int per_op) {
+  if (Sg->done || !Sg->aa_attempt) return;
+  __shared__ DevState smS;
+  state_load(&smS, Sg);
+  DevState* S = &smS;
+  // p x p Gram and factor in dynamic shared memory (2 * cap^2 doubles)
+  extern __shared__ double dyn_smem[];
+  __shared__ double vecs[8 * kMaxMemory];
+  const SolveScratch W{dyn_smem, dyn_smem + P->cap * P->cap, vecs};
   const int p = S->mem_size;
   const int nit = num_items(p, P->method);
   __shared__ double vals[kMaxMemory * (kMaxMemory + 1) / 2 + 2 * kMaxMemory];
@@ -168,7 +174,7 @@ __global__ void __launch_bounds__(1024)
     }
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x == 0) {
   const int npair = p * (p + 1) / 2;
   double* G = W.gram;  // p x p column-major, full symmetric
   {
@@ -314,6 +320,8 @@ __global__ void __launch_bounds__(1024)
     S->j += 1;
     S->aa_failures += 1;
   }
+  }  // thread 0
+  state_store(Sg, &smS);
 }
 
 // cand = P_feasible(u + damp(g) - sum_j w_j (du_j + damp(dg_j)))
@@ -330,12 +338,19 @@ __global__ void __launch_bounds__(kThreads)
   const int pm = S->mix_p;
   const double beta = P->beta;
   const double* dh = P->d_hat;
+  __shared__ double nw[kMaxMemory];
+  __shared__ int64_t sls[kMaxMemory];
+  for (int jj = threadIdx.x; jj < pm; jj += blockDim.x) {
+    nw[jj] = -S->w[jj];
+    sls[jj] = S->mix_slots[jj];
+  }
+  __syncthreads();
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N;
        t += (int64_t)gridDim.x * blockDim.x) {
     double o = __dadd_rn(u[t], damp1(beta, dh, t, g[t]));
     for (int jj = 0; jj < pm; ++jj) {
-      const int64_t sl = S->mix_slots[jj];
-      const double a = -S->w[jj];
+      const int64_t sl = sls[jj];
+      const double a = nw[jj];
       o = __dadd_rn(o, __dmul_rn(a, B.du[sl * N + t]));
       o = __dadd_rn(o, __dmul_rn(a, damp1(beta, dh, t, dg[sl * N + t])));
     }
@@ -347,55 +362,14 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// role rotation at the end of an iteration (solver.cpp:249-251) + next push slot
-__global__ void k_commit(const DevParams* __restrict__ P, DevState* S) {
-  if (S->done) {
-    if (P->use_cond) cudaGraphSetConditional(P->cond_loop, 0u);
-    return;
-  }
-  int* U = S->u_idx;
-  int* KX = S->kx_idx;
-  const int old_prev = U[U_PREV];
-  if (S->aa_ok) {
-    U[U_PREV] = U[U_CUR];
-    U[U_CUR] = U[U_CAND];
-    U[U_CAND] = old_prev;
-    const int okx = KX[KX_CUR];
-    KX[KX_CUR] = KX[KX_CAND];
-    KX[KX_CAND] = okx;
-  } else {
-    U[U_PREV] = U[U_CUR];
-    U[U_CUR] = U[U_HAT];
-    U[U_HAT] = old_prev;
-    const int okx = KX[KX_CUR];
-    KX[KX_CUR] = KX[KX_HAT];
-    KX[KX_HAT] = okx;
-  }
-  if (P->method != AAPDHG_METHOD_PDHG) {
-    const int t = S->g_idx[G_CUR];
-    S->g_idx[G_CUR] = S->g_idx[G_PREV];
-    S->g_idx[G_PREV] = t;
-    if (S->mem_size < P->cap) {  // first slot not in the memory
-      int slot = 0;
-      for (; slot < P->cap; ++slot) {
-        bool used = false;
-        for (int q = 0; q < S->mem_size; ++q) used |= S->mem_slots[q] == slot;
-        if (!used) break;
-      }
-      S->push_slot = slot;
-    } else {
-      S->push_slot = S->mem_slots[0];
-    }
-  }
-  S->aa_attempt = 0;
-  S->aa_ok = 0;
-  S->k += 1;
-  S->loop_iters += 1;
-  // WHILE node of the graph batch: keep going while work is left
-  if (P->use_cond) {
-    const int left = --S->batch_left;
-    cudaGraphSetConditional(P->cond_loop, left > 0 ? 1u : 0u);
-  }
+// End of an iteration that attempted an AA step (the IF body of the graph):
+// rotate to the candidate (or to T(u) after a SingularError fallback).
+__global__ void k_aa_commit(const DevParams* __restrict__ P, DevState* S) {
+  if (S->done || !S->aa_attempt) return;
+  __shared__ DevState sm;
+  state_load(&sm, S);
+  if (threadIdx.x == 0) advance(P, &sm);
+  state_store(S, &sm);
 }
 
 // ---------------------------------------------------------------------------

@@ -149,6 +149,8 @@ int Problem::spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const Rowsum
   return nodes;
 }
 
+size_t Problem::aa_smem(int cap) { return sizeof(double) * 2 * size_t(cap) * size_t(cap); }
+
 int Problem::gather_grid(const CsrDev& A) const {
   return int(std::max<int64_t>(1, std::min<int64_t>((A.nnz + kThreads - 1) / kThreads,
                                                    int64_t(num_sms_) * kGatherBlocksPerSM)));
@@ -245,6 +247,8 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   part_small_.reserve(sizeof(double) * 5 * (nbig / kThreads + 2));
   AAPDHG_CUDA(cudaMallocHost(&h_state_, sizeof(DevState)));
   AAPDHG_CUDA(cudaMallocHost(&h_batch_, sizeof(int32_t)));
+  AAPDHG_CUDA(cudaFuncSetAttribute(k_aa_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(aa_smem(kMaxMemory))));
 
   // ||q|| and ||c|| under both reduction orders (constants of kkt_metrics)
   for (int serial = 0; serial < 2; ++serial) {
@@ -443,7 +447,7 @@ int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
   } else {
     LAUNCH("k_tree_dots", k_tree_dots<<<su.ndot_blk, kThreads, 0, s>>>(su.D, su.P, su.S));
   }
-  LAUNCH("k_aa_solve", k_aa_solve<<<1, 1024, 0, s>>>(su.D, su.W, su.P, su.S, 0));
+  LAUNCH("k_aa_solve", k_aa_solve<<<1, 1024, aa_smem(su.cap), s>>>(su.D, su.P, su.S, 0));
   LAUNCH("k_mix", k_mix<<<grid_for(N_), kThreads, 0, s>>>(su.B, su.B.dg, su.P, su.S, 1));
   if (m_ > 0) {  // K x recache of the accepted candidate
     RowsumArgs r{};
@@ -453,13 +457,7 @@ int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
     nodes += spmv(s, K_, VecRef{nullptr, su.B.upool, U_CAND, N_, 0}, r, su.serial, su.S, 1,
                   nullptr);
   }
-  AAPDHG_CUDA(cudaGetLastError());
-  return nodes;
-}
-
-int Problem::launch_commit(cudaStream_t s, const SolveSetup& su) {
-  int nodes = 0;
-  LAUNCH("k_commit", k_commit<<<1, 1, 0, s>>>(su.P, su.S));
+  LAUNCH("k_aa_commit", k_aa_commit<<<1, 128, 0, s>>>(su.P, su.S));
   AAPDHG_CUDA(cudaGetLastError());
   return nodes;
 }
@@ -467,10 +465,10 @@ int Problem::launch_commit(cudaStream_t s, const SolveSetup& su) {
 void Problem::launch_iteration(cudaStream_t s, const SolveSetup& su) {
   launch_core(s, su);
   launch_aa(s, su);
-  launch_commit(s, su);
 }
 
-// WHILE(batch) { core; IF(aa_attempt) { aa }; commit } as one executable graph.
+// WHILE(batch) { core (+control); IF(aa_attempt) { aa (+commit) } } as one
+// executable graph: the control kernel sets both conditions.
 void Problem::build_graph(const SolveSetup& su) {
   const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
   cudaStream_t s = stream_;
@@ -510,11 +508,8 @@ void Problem::build_graph(const SolveSetup& su) {
     AAPDHG_CUDA(cudaStreamBeginCaptureToGraph(s, ifbody, nullptr, nullptr, 0, mode));
     aa_nodes_ = launch_aa(s, su);
     AAPDHG_CUDA(cudaStreamEndCapture(s, &captured));
-    tail.assign(1, after);
   }
-  AAPDHG_CUDA(cudaStreamBeginCaptureToGraph(s, body, tail.data(), nullptr, tail.size(), mode));
-  commit_nodes_ = launch_commit(s, su);
-  AAPDHG_CUDA(cudaStreamEndCapture(s, &captured));
+  (void)after;
   AAPDHG_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
   cudaGraphDestroy(g);
 }
@@ -808,10 +803,10 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   res->wall_seconds = secs(t_start);
   last_loop_iters_ = st.loop_iters;
   if (use_graph)
-    last_launches_ = st.loop_iters * uint64_t(core_nodes_ + commit_nodes_) +
+    last_launches_ = st.loop_iters * uint64_t(core_nodes_) +
                      (st.i + st.aa_failures) * uint64_t(aa_nodes_);
   else
-    last_launches_ = st.loop_iters * uint64_t(core_nodes_ + commit_nodes_ + aa_nodes_);
+    last_launches_ = st.loop_iters * uint64_t(core_nodes_ + aa_nodes_);
 }
 
 // ---- single-op entry points ----------------------------------------------
@@ -966,7 +961,7 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
       k_tree_dots<<<ndot_tile_, kThreads, 0, stream_>>>(D, Pd, Sd);
     }
   }
-  k_aa_solve<<<1, 1024, 0, stream_>>>(D, W, Pd, Sd, 1);
+  k_aa_solve<<<1, 1024, aa_smem(std::max(p, 1)), stream_>>>(D, Pd, Sd, 1);
   k_mix<<<grid_for(N_), kThreads, 0, stream_>>>(B, dg_.as<double>(), Pd, Sd, 0);
   AAPDHG_CUDA(cudaGetLastError());
   d2h(h_state_, Sd, sizeof(DevState), stream_);

@@ -67,6 +67,7 @@ class Problem {
   int spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const RowsumArgs& o, bool serial,
            const DevState* S, int pred, const int32_t* stop);
   int gather_grid(const CsrDev& A) const;
+  static size_t aa_smem(int cap);
   void upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
                   DevBuf& d_rp, DevBuf& d_ci, DevBuf& d_v, DevBuf& d_meta, CsrDev& out);
   void ensure_iter_buffers(int method, int cap);
@@ -74,7 +75,6 @@ class Problem {
   void kkt_eval(int slot, bool serial, double* kkt_dev_out, double* lam_dev);
   int launch_core(cudaStream_t s, const SolveSetup& su);
   int launch_aa(cudaStream_t s, const SolveSetup& su);
-  int launch_commit(cudaStream_t s, const SolveSetup& su);
   void launch_iteration(cudaStream_t s, const SolveSetup& su);
   void build_graph(const SolveSetup& su);
   void run_power(const double* x0_host, int max_iters, double rel_tol, bool serial, double* out,
@@ -120,7 +120,7 @@ class Problem {
   cudaGraphExec_t graph_exec_ = nullptr;
   std::string graph_key_;
   cudaGraphConditionalHandle cond_loop_ = 0, cond_aa_ = 0;
-  int core_nodes_ = 0, aa_nodes_ = 0, commit_nodes_ = 0;
+  int core_nodes_ = 0, aa_nodes_ = 0;
   int32_t* h_batch_ = nullptr;  // pinned
 
   bool profiling_ = false;

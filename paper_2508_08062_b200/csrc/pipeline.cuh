@@ -372,6 +372,65 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// The iteration state is tiny (~1.3 KB) but a single thread walking it in
+// global memory pays one L2 round trip per field; the scalar kernels stage it
+// in shared memory with one coalesced block-wide copy each way.
+__device__ __forceinline__ void state_load(DevState* sm, const DevState* g) {
+  constexpr int W = sizeof(DevState) / 4;
+  const int* s = reinterpret_cast<const int*>(g);
+  int* d = reinterpret_cast<int*>(sm);
+  for (int i = threadIdx.x; i < W; i += blockDim.x) d[i] = __ldcg(s + i);
+  __syncthreads();
+}
+__device__ __forceinline__ void state_store(DevState* g, const DevState* sm) {
+  constexpr int W = sizeof(DevState) / 4;
+  __syncthreads();
+  const int* s = reinterpret_cast<const int*>(sm);
+  int* d = reinterpret_cast<int*>(g);
+  for (int i = threadIdx.x; i < W; i += blockDim.x) d[i] = s[i];
+}
+
+// Role rotation at the end of an iteration (solver.cpp:249-251) and the
+// next push slot: u_prev <- u, u <- u_next (the AA candidate or T(u)).
+__device__ __forceinline__ void advance(const DevParams* P, DevState* S) {
+  int* U = S->u_idx;
+  int* KX = S->kx_idx;
+  const int old_prev = U[U_PREV];
+  U[U_PREV] = U[U_CUR];
+  const int okx = KX[KX_CUR];
+  if (S->aa_ok) {
+    U[U_CUR] = U[U_CAND];
+    U[U_CAND] = old_prev;
+    KX[KX_CUR] = KX[KX_CAND];
+    KX[KX_CAND] = okx;
+  } else {
+    U[U_CUR] = U[U_HAT];
+    U[U_HAT] = old_prev;
+    KX[KX_CUR] = KX[KX_HAT];
+    KX[KX_HAT] = okx;
+  }
+  if (P->method != AAPDHG_METHOD_PDHG) {
+    const int t = S->g_idx[G_CUR];
+    S->g_idx[G_CUR] = S->g_idx[G_PREV];
+    S->g_idx[G_PREV] = t;
+    if (S->mem_size < P->cap) {  // first slot not in the memory
+      int slot = 0;
+      for (; slot < P->cap; ++slot) {
+        bool used = false;
+        for (int q = 0; q < S->mem_size; ++q) used |= S->mem_slots[q] == slot;
+        if (!used) break;
+      }
+      S->push_slot = slot;
+    } else {
+      S->push_slot = S->mem_slots[0];
+    }
+  }
+  S->aa_attempt = 0;
+  S->aa_ok = 0;
+  S->k += 1;
+  S->loop_iters += 1;
+}
+
 __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2,
                                            double bound, double qy, double cx, double infeas,
                                            double dual_sq);
@@ -387,7 +446,13 @@ __device__ __forceinline__ void control_from_partials(const IterBufs& B, const D
   const double cx = reduce_partials(B.part1 + P1_CX * P->nblk1, P->nblk1, red32);
   const double inf = reduce_partials(B.part2 + P2_INFEAS * P->nblk2, P->nblk2, red32);
   const double dsq = reduce_partials(B.part1 + P1_DUALSQ * P->nblk1, P->nblk1, red32);
-  if (threadIdx.x == 0) control_logic(P, S, __dadd_rn(gx2, gy2), bound, qy, cx, inf, dsq);
+  __shared__ DevState sm;
+  state_load(&sm, S);
+  if (threadIdx.x == 0) {
+    control_logic(P, &sm, __dadd_rn(gx2, gy2), bound, qy, cx, inf, dsq);
+    sm.ticket = 0;
+  }
+  state_store(S, &sm);
 }
 
 // K2 row kernel on K, s = (K xhat)_i:
@@ -457,7 +522,6 @@ __global__ void __launch_bounds__(kThreads)
   if (!is_last) return;
   __threadfence();
   control_from_partials(B, P, S);
-  if (threadIdx.x == 0) S->ticket = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -468,7 +532,10 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(32 * S_COUNT)
     k_serial_control(IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) {
-    if (threadIdx.x == 0 && P->use_cond) cudaGraphSetConditional(P->cond_aa, 0);
+    if (threadIdx.x == 0 && P->use_cond) {
+      cudaGraphSetConditional(P->cond_aa, 0);
+      cudaGraphSetConditional(P->cond_loop, 0);
+    }
     return;
   }
   __shared__ double res[S_COUNT];
@@ -527,10 +594,12 @@ __global__ void __launch_bounds__(32 * S_COUNT)
     }
     res[w] = s;
   }
-  __syncthreads();
+  __shared__ DevState sm;
+  state_load(&sm, S);  // (syncs: res[] complete)
   if (threadIdx.x == 0)
-    control_logic(P, S, res[S_G2], res[S_BOUND], res[S_QY], res[S_CX], res[S_INFEAS],
+    control_logic(P, &sm, res[S_G2], res[S_BOUND], res[S_QY], res[S_CX], res[S_INFEAS],
                   res[S_DUALSQ]);
+  state_store(S, &sm);
 }
 
 // KKT scalars of the CUR iterate from the reduced sums (solver.cpp:83-107).
@@ -617,7 +686,13 @@ __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, doub
     if (attempt) S->aa_attempt = 1;
     else S->j += 1;
   } while (false);
-  if (P->use_cond) cudaGraphSetConditional(P->cond_aa, attempt ? 1u : 0u);
+  // no AA attempt: the iteration ends here (the AA branch commits otherwise)
+  if (!S->done && !attempt) advance(P, S);
+  const int left = S->done ? 0 : --S->batch_left;
+  if (P->use_cond) {
+    cudaGraphSetConditional(P->cond_aa, attempt ? 1u : 0u);
+    cudaGraphSetConditional(P->cond_loop, left > 0 ? 1u : 0u);
+  }
 }
 
 }  // namespace aapdhg_b200
