@@ -382,6 +382,13 @@ __device__ __forceinline__ void state_load(DevState* sm, const DevState* g) {
   for (int i = threadIdx.x; i < W; i += blockDim.x) d[i] = __ldcg(s + i);
   __syncthreads();
 }
+__device__ __forceinline__ void params_load(DevParams* sm, const DevParams* g) {
+  constexpr int W = sizeof(DevParams) / 4;
+  const int* s = reinterpret_cast<const int*>(g);
+  int* d = reinterpret_cast<int*>(sm);
+  for (int i = threadIdx.x; i < W; i += blockDim.x) d[i] = __ldg(s + i);
+  // (the caller's state_load provides the barrier)
+}
 __device__ __forceinline__ void state_store(DevState* g, const DevState* sm) {
   constexpr int W = sizeof(DevState) / 4;
   __syncthreads();
@@ -436,20 +443,33 @@ __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, doub
                                            double dual_sq);
 
 // TREE mode: reduce all partials of K1/K2 and run the control (one CTA).
+// One pass: each thread keeps the 7 strided sums, then one fixed block tree.
 __device__ __forceinline__ void control_from_partials(const IterBufs& B, const DevParams* P,
                                                       DevState* S) {
-  __shared__ double red32[32];
-  const double gx2 = reduce_partials(B.part1 + P1_GX2 * P->nblk1, P->nblk1, red32);
-  const double gy2 = reduce_partials(B.part2 + P2_GY2 * P->nblk2, P->nblk2, red32);
-  const double bound = reduce_partials(B.part1 + P1_BOUND * P->nblk1, P->nblk1, red32);
-  const double qy = reduce_partials(B.part2 + P2_QY * P->nblk2, P->nblk2, red32);
-  const double cx = reduce_partials(B.part1 + P1_CX * P->nblk1, P->nblk1, red32);
-  const double inf = reduce_partials(B.part2 + P2_INFEAS * P->nblk2, P->nblk2, red32);
-  const double dsq = reduce_partials(B.part1 + P1_DUALSQ * P->nblk1, P->nblk1, red32);
+  __shared__ double red7[7 * kWarps];
+  const int nb1 = P->nblk1, nb2 = P->nblk2;
+  double v[7] = {0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+  for (int b = threadIdx.x; b < nb1; b += blockDim.x) {
+    v[0] = __dadd_rn(v[0], __ldcg(B.part1 + P1_GX2 * nb1 + b));
+    v[1] = __dadd_rn(v[1], __ldcg(B.part1 + P1_BOUND * nb1 + b));
+    v[2] = __dadd_rn(v[2], __ldcg(B.part1 + P1_CX * nb1 + b));
+    v[3] = __dadd_rn(v[3], __ldcg(B.part1 + P1_DUALSQ * nb1 + b));
+  }
+#pragma unroll 4
+  for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
+    v[4] = __dadd_rn(v[4], __ldcg(B.part2 + P2_GY2 * nb2 + b));
+    v[5] = __dadd_rn(v[5], __ldcg(B.part2 + P2_QY * nb2 + b));
+    v[6] = __dadd_rn(v[6], __ldcg(B.part2 + P2_INFEAS * nb2 + b));
+  }
+  block_sum<7>(v, red7);
+  const double gx2 = v[0], bound = v[1], cx = v[2], dsq = v[3], gy2 = v[4], qy = v[5], inf = v[6];
   __shared__ DevState sm;
+  __shared__ DevParams sp;
+  params_load(&sp, P);
   state_load(&sm, S);
   if (threadIdx.x == 0) {
-    control_logic(P, &sm, __dadd_rn(gx2, gy2), bound, qy, cx, inf, dsq);
+    control_logic(&sp, &sm, __dadd_rn(gx2, gy2), bound, qy, cx, inf, dsq);
     sm.ticket = 0;
   }
   state_store(S, &sm);
@@ -595,9 +615,11 @@ __global__ void __launch_bounds__(32 * S_COUNT)
     res[w] = s;
   }
   __shared__ DevState sm;
+  __shared__ DevParams sp;
+  params_load(&sp, P);
   state_load(&sm, S);  // (syncs: res[] complete)
   if (threadIdx.x == 0)
-    control_logic(P, &sm, res[S_G2], res[S_BOUND], res[S_QY], res[S_CX], res[S_INFEAS],
+    control_logic(&sp, &sm, res[S_G2], res[S_BOUND], res[S_QY], res[S_CX], res[S_INFEAS],
                   res[S_DUALSQ]);
   state_store(S, &sm);
 }
