@@ -39,15 +39,33 @@ enum { P2_GY2 = 0, P2_QY = 1, P2_INFEAS = 2, P2_COUNT = 3 };
 // serial chain results (index into DevState::sres)
 enum { S_G2 = 0, S_BOUND = 1, S_QY = 2, S_CX = 3, S_INFEAS = 4, S_DUALSQ = 5, S_COUNT = 6 };
 
+// A CSR matrix on the device in the layout the SpMV kernels stream:
+//   rp/ci/v        the CSR itself (row lengths; long rows read from here)
+//   SELL-32        short rows (<= kLongRow nonzeros) grouped 32 per slice in
+//                  row order; element k of the slice's lane-r row sits at
+//                  sl_ptr[s] + 32 k + r of sci/sv; sl_row[32 s + r] = row
+//                  (-1 = empty lane), sl_len[s] = longest row of the slice
+//   long rows      row ids, one warp each
+// Launch grid = nblk_short CTAs of slices + nblk_long CTAs of long rows.
 struct CsrDev {
   int32_t nrows = 0, ncols = 0;
   int64_t nnz = 0;
   const int32_t* rp = nullptr;
   const int32_t* ci = nullptr;
   const double* v = nullptr;
-  int32_t ntiles = 0;
-  const int4* meta = nullptr;     // per row block {r0, r1, e0, e1}
+  int32_t nslices = 0, nlong = 0;
+  const int64_t* sl_ptr = nullptr;
+  const int32_t* sl_len = nullptr;
+  const int32_t* sl_row = nullptr;
+  const int32_t* sci = nullptr;
+  const double* sv = nullptr;
+  const int32_t* long_rows = nullptr;
+  int32_t nblk_short = 0, nblk_long = 0;
+  int32_t grid() const { return nblk_short + nblk_long; }
 };
+
+constexpr int kLongRow = 256;        // rows longer than this get a warp each
+constexpr int kSpmvBlocksPerSM = 6;  // register budget of the SpMV kernels
 
 // Constant per solve (written before the loop starts).
 struct DevParams {
@@ -104,16 +122,8 @@ struct VecRef {
   }
 };
 
-struct GatherArgs {
-  VecRef x;
-  double* prod;
-  int32_t pred_aa_ok;   // run only when S->aa_ok
-  const int32_t* stop;  // optional: skip when *stop != 0 (power iteration)
-};
-
 // out[r] = sum of row r's products (power iteration, K x recache, matvec).
 struct RowsumArgs {
-  const double* prod;
   double* out;           // used when out_pool == nullptr
   double* out_pool;      // kxpool base: out = out_pool + kx_idx[out_role]*out_stride
   int32_t out_role;

@@ -32,27 +32,6 @@ constexpr uint64_t kRecCap = 1 << 16;  // device record ring
 constexpr uint64_t kPowTabMax = 1 << 22;
 constexpr int kPowerBatch = 8;
 
-// Row blocks: consecutive rows, at most kRowsPerBlock rows and kTile
-// nonzeros; a row longer than kTile forms a block of its own.
-std::vector<int32_t> build_tiles(const int32_t* rp, int nrows) {
-  std::vector<int32_t> t{0};
-  int r = 0;
-  while (r < nrows) {
-    const int start = r;
-    if (rp[r + 1] - rp[r] > kTile) {
-      ++r;
-    } else {
-      int64_t nz = 0;
-      while (r < nrows && r - start < kRowsPerBlock && nz + (rp[r + 1] - rp[r]) <= kTile) {
-        nz += rp[r + 1] - rp[r];
-        ++r;
-      }
-    }
-    t.push_back(r);
-  }
-  return t;
-}
-
 int num_items_host(int p, int method) {
   return p * (p + 1) / 2 + p + (method == AAPDHG_METHOD_FAA ? p : 0);
 }
@@ -97,63 +76,92 @@ struct SolveSetup {
   int method, cap, nblk1, nblk2, ndot_blk, items_max;
 };
 
-// Uploads one CSR (arrays padded by kPad elements) with its warp-tile
-// metadata {r0, r1, e0, e1} and persistent grid size.
+// Uploads one CSR and its SELL-32 slices of the short rows (see CsrDev).
 void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows,
-                         int ncols, DevBuf& d_rp, DevBuf& d_ci, DevBuf& d_v, DevBuf& d_meta,
-                         CsrDev& out) {
-  constexpr int kPad = 16;
+                         int ncols, CsrStore& st, CsrDev& out) {
   const int64_t nnz = rp[nrows];
-  const std::vector<int32_t> tb = build_tiles(rp, nrows);
-  const int ntiles = int(tb.size() - 1);
-  std::vector<int4> meta(size_t(std::max(ntiles, 1)));
-  for (int t = 0; t < ntiles; ++t) meta[size_t(t)] = make_int4(tb[t], tb[t + 1], rp[tb[t]], rp[tb[t + 1]]);
-  d_rp.reserve(sizeof(int32_t) * (nrows + 1 + kPad));
-  d_ci.reserve(sizeof(int32_t) * (nnz + kPad));
-  d_v.reserve(sizeof(double) * (nnz + kPad));
-  d_meta.reserve(sizeof(int4) * meta.size());
-  AAPDHG_CUDA(cudaMemsetAsync(d_ci.p, 0, d_ci.bytes, stream_));
-  AAPDHG_CUDA(cudaMemsetAsync(d_v.p, 0, d_v.bytes, stream_));
-  h2d(d_rp.p, rp, sizeof(int32_t) * (nrows + 1), stream_);
-  h2d(d_ci.p, ci, sizeof(int32_t) * nnz, stream_);
-  h2d(d_v.p, v, sizeof(double) * nnz, stream_);
-  h2d(d_meta.p, meta.data(), sizeof(int4) * ntiles, stream_);
-  sync();  // host vectors go out of scope
-  out = CsrDev{nrows, ncols, nnz, d_rp.as<int32_t>(), d_ci.as<int32_t>(), d_v.as<double>(),
-               ntiles, d_meta.as<int4>()};
+  std::vector<int32_t> shorts, longs;
+  shorts.reserve(size_t(nrows));
+  for (int r = 0; r < nrows; ++r) (rp[r + 1] - rp[r] > kLongRow ? longs : shorts).push_back(r);
+  const int nslices = int((shorts.size() + 31) / 32);
+  std::vector<int64_t> sl_ptr(size_t(std::max(nslices, 1)));
+  std::vector<int32_t> sl_len(size_t(std::max(nslices, 1))), sl_row(size_t(std::max(nslices, 1)) * 32, -1);
+  int64_t total = 0;
+  for (int s = 0; s < nslices; ++s) {
+    int L = 0;
+    for (int r = 0; r < 32 && size_t(s) * 32 + r < shorts.size(); ++r) {
+      const int row = shorts[size_t(s) * 32 + r];
+      sl_row[size_t(s) * 32 + r] = row;
+      L = std::max(L, rp[row + 1] - rp[row]);
+    }
+    sl_ptr[size_t(s)] = total;
+    sl_len[size_t(s)] = L;
+    total += int64_t(32) * L;
+  }
+  std::vector<int32_t> sci(size_t(std::max<int64_t>(total, 1)), 0);
+  std::vector<double> sv(size_t(std::max<int64_t>(total, 1)), 0.0);
+  for (int s = 0; s < nslices; ++s)
+    for (int r = 0; r < 32; ++r) {
+      const int row = sl_row[size_t(s) * 32 + r];
+      if (row < 0) continue;
+      for (int k = 0; k < rp[row + 1] - rp[row]; ++k) {
+        const size_t dst = size_t(sl_ptr[size_t(s)] + 32 * int64_t(k) + r);
+        sci[dst] = ci[rp[row] + k];
+        sv[dst] = v[rp[row] + k];
+      }
+    }
+  st.rp.reserve(sizeof(int32_t) * (nrows + 1));
+  st.ci.reserve(sizeof(int32_t) * nnz);
+  st.v.reserve(sizeof(double) * nnz);
+  st.sl_ptr.reserve(sizeof(int64_t) * sl_ptr.size());
+  st.sl_len.reserve(sizeof(int32_t) * sl_len.size());
+  st.sl_row.reserve(sizeof(int32_t) * sl_row.size());
+  st.sci.reserve(sizeof(int32_t) * sci.size());
+  st.sv.reserve(sizeof(double) * sv.size());
+  st.longs.reserve(sizeof(int32_t) * std::max<size_t>(longs.size(), 1));
+  h2d(st.rp.p, rp, sizeof(int32_t) * (nrows + 1), stream_);
+  h2d(st.ci.p, ci, sizeof(int32_t) * nnz, stream_);
+  h2d(st.v.p, v, sizeof(double) * nnz, stream_);
+  h2d(st.sl_ptr.p, sl_ptr.data(), sizeof(int64_t) * sl_ptr.size(), stream_);
+  h2d(st.sl_len.p, sl_len.data(), sizeof(int32_t) * sl_len.size(), stream_);
+  h2d(st.sl_row.p, sl_row.data(), sizeof(int32_t) * sl_row.size(), stream_);
+  h2d(st.sci.p, sci.data(), sizeof(int32_t) * sci.size(), stream_);
+  h2d(st.sv.p, sv.data(), sizeof(double) * sv.size(), stream_);
+  h2d(st.longs.p, longs.data(), sizeof(int32_t) * longs.size(), stream_);
+  sync();  // host staging vectors go out of scope
+  sell_bytes_ += (sizeof(int32_t) + sizeof(double)) * size_t(total);
+  out = CsrDev{};
+  out.nrows = nrows;
+  out.ncols = ncols;
+  out.nnz = nnz;
+  out.rp = st.rp.as<int32_t>();
+  out.ci = st.ci.as<int32_t>();
+  out.v = st.v.as<double>();
+  out.nslices = nslices;
+  out.nlong = int32_t(longs.size());
+  out.sl_ptr = st.sl_ptr.as<int64_t>();
+  out.sl_len = st.sl_len.as<int32_t>();
+  out.sl_row = st.sl_row.as<int32_t>();
+  out.sci = st.sci.as<int32_t>();
+  out.sv = st.sv.as<double>();
+  out.long_rows = st.longs.as<int32_t>();
+  out.nblk_short = (nslices + kWarps - 1) / kWarps;
+  out.nblk_long = (out.nlong + kWarps - 1) / kWarps;
 }
 
-// out = A x: k_gather (products) + k_rowsum (CSR-ordered row sums).
+// out = A x (CSR-ordered row sums).
 int Problem::spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const RowsumArgs& o,
                   bool serial, const DevState* S, int pred, const int32_t* stop) {
-  int nodes = 0;
-  if (A.nnz > 0) {
-    GatherArgs g{x, prod_.as<double>(), pred, stop};
-    prof_begin(s, "k_gather");
-    k_gather<<<gather_grid(A), kThreads, 0, s>>>(A, g, S);
-    prof_end(s);
-    ++nodes;
-  }
-  if (A.ntiles > 0) {
-    RowsumArgs r = o;
-    r.prod = prod_.as<double>();
-    r.pred_aa_ok = pred;
-    r.stop = stop;
-    prof_begin(s, "k_rowsum");
-    if (serial) k_rowsum<true><<<A.ntiles, kThreads, 0, s>>>(A, r, S);
-    else k_rowsum<false><<<A.ntiles, kThreads, 0, s>>>(A, r, S);
-    prof_end(s);
-    ++nodes;
-  }
+  if (A.grid() == 0) return 0;
+  RowsumArgs r = o;
+  r.pred_aa_ok = pred;
+  r.stop = stop;
+  prof_begin(s, "k_spmv");
+  if (serial) k_spmv<true><<<A.grid(), kThreads, 0, s>>>(A, x, r, S);
+  else k_spmv<false><<<A.grid(), kThreads, 0, s>>>(A, x, r, S);
+  prof_end(s);
   AAPDHG_CUDA(cudaGetLastError());
-  return nodes;
-}
-
-size_t Problem::aa_smem(int cap) { return sizeof(double) * 2 * size_t(cap) * size_t(cap); }
-
-int Problem::gather_grid(const CsrDev& A) const {
-  return int(std::max<int64_t>(1, std::min<int64_t>((A.nnz + kThreads - 1) / kThreads,
-                                                   int64_t(num_sms_) * kGatherBlocksPerSM)));
+  return 1;
 }
 
 static VecRef vref(const double* p) { return VecRef{p, nullptr, 0, 0, 0}; }
@@ -162,6 +170,9 @@ static RowsumArgs rout(double* out) {
   r.out = out;
   return r;
 }
+
+size_t Problem::aa_smem(int cap) { return sizeof(double) * 2 * size_t(cap) * size_t(cap); }
+
 
 // ---------------------------------------------------------------------------
 Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
@@ -206,7 +217,7 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
 
   // K, padded so 16-byte cp.async of a tile's aligned superset stays in bounds
   AAPDHG_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device));
-  upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_rp_, k_ci_, k_v_, k_tile_, K_);
+  upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, K_);
   // K' as CSR, entries of each row in ascending original row (counting sort)
   std::vector<int32_t> trp(static_cast<size_t>(n_) + 1, 0), tci(static_cast<size_t>(nnz_));
   std::vector<double> tv(static_cast<size_t>(nnz_));
@@ -221,9 +232,8 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
         tv[size_t(pos)] = k.vals[e];
       }
   }
-  upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_rp_, t_ci_, t_v_, t_tile_, KT_);
+  upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_store_, KT_);
 
-  prod_.reserve(sizeof(double) * (std::max<int64_t>(nnz_, 1) + 16));
   c_.reserve(sizeof(double) * n_);
   q_.reserve(sizeof(double) * m_);
   l_.reserve(sizeof(double) * n_);
@@ -301,7 +311,7 @@ double Problem::device_dot(const double* a, const double* b, int64_t n, bool ser
 }
 
 void Problem::ensure_iter_buffers(int method, int cap) {
-  const int nblk1 = KT_.ntiles, nblk2 = K_.ntiles;
+  const int nblk1 = KT_.grid(), nblk2 = K_.grid();
   upool_.reserve(sizeof(double) * 4 * std::max<int64_t>(N_, 1));
   kxpool_.reserve(sizeof(double) * 3 * std::max<int64_t>(m_, 1));
   T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
@@ -413,25 +423,17 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   const bool ser = su.serial, push = su.push;
   // K'y: products of K' with y = u_cur[n:], then the fused dual-side rows
   if (n_ > 0) {
-    if (KT_.nnz > 0) {
-      GatherArgs g{VecRef{nullptr, su.B.upool, U_CUR, N_, n_}, su.B.prod, 0, nullptr};
-      LAUNCH("k_gather", k_gather<<<gather_grid(KT_), kThreads, 0, s>>>(KT_, g, su.S));
-    }
-    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KT_.ntiles, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KT_.ntiles, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KT_.ntiles, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KT_.ntiles, kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KT_.grid(), kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KT_.grid(), kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KT_.grid(), kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KT_.grid(), kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
   }
   // K xhat: products of K with xhat = u_hat[:n], then the fused dual step
   if (m_ > 0) {
-    if (K_.nnz > 0) {
-      GatherArgs g{VecRef{nullptr, su.B.upool, U_HAT, N_, 0}, su.B.prod, 0, nullptr};
-      LAUNCH("k_gather", k_gather<<<gather_grid(K_), kThreads, 0, s>>>(K_, g, su.S));
-    }
-    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<K_.ntiles, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<K_.ntiles, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<K_.ntiles, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else LAUNCH("k_primal_side", k_primal_side<false, false><<<K_.ntiles, kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<K_.grid(), kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<K_.grid(), kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<K_.grid(), kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    else LAUNCH("k_primal_side", k_primal_side<false, false><<<K_.grid(), kThreads, 0, s>>>(K_, su.B, su.P, su.S));
   }
   if (ser) LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
   AAPDHG_CUDA(cudaGetLastError());
@@ -669,8 +671,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.pow_len = ptab.size();
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
-  P.nblk1 = KT_.ntiles;
-  P.nblk2 = K_.ntiles;
+  P.nblk1 = KT_.grid();
+  P.nblk2 = K_.grid();
   P.ndot_blk = ndot_tile_;
 
   DevState S0{};
@@ -683,7 +685,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   SolveSetup su;
   su.B = IterBufs{upool_.as<double>(), kxpool_.as<double>(), gpool_.as<double>(),
                   du_.as<double>(), dg_.as<double>(), T_.as<double>(), part1_.as<double>(),
-                  part2_.as<double>(), prod_.as<double>(), c_.as<double>(), q_.as<double>(),
+                  part2_.as<double>(), c_.as<double>(), q_.as<double>(),
                   l_.as<double>(), u_.as<double>()};
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
                  partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
@@ -694,8 +696,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.push = method != AAPDHG_METHOD_PDHG;
   su.method = method;
   su.cap = cap;
-  su.nblk1 = KT_.ntiles;
-  su.nblk2 = K_.ntiles;
+  su.nblk1 = KT_.grid();
+  su.nblk2 = K_.grid();
   su.ndot_blk = ndot_tile_;
   su.items_max = num_items_host(std::max(cap, 1), method);
 
@@ -854,29 +856,21 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   P.N = N_;
   P.tau = tau;
   P.sigma = sigma;
-  P.nblk1 = KT_.ntiles;
-  P.nblk2 = K_.ntiles;
+  P.nblk1 = KT_.grid();
+  P.nblk2 = K_.grid();
   const DevState S = identity_state();
   h2d(dparams_.p, &P, sizeof P, stream_);
   h2d(dstate_.p, &S, sizeof S, stream_);
   IterBufs B{upool_.as<double>(), kxpool_.as<double>(), nullptr, nullptr, nullptr,
-             T_.as<double>(), part1_.as<double>(), part2_.as<double>(), prod_.as<double>(),
+             T_.as<double>(), part1_.as<double>(), part2_.as<double>(),
              c_.as<double>(), q_.as<double>(), l_.as<double>(), u_.as<double>()};
   const DevParams* Pd = dparams_.as<DevParams>();
   DevState* Sd = dstate_.as<DevState>();
   if (n_) {
-    if (KT_.nnz) {
-      GatherArgs g{vref(upool_.as<double>() + n_), prod_.as<double>(), 0, nullptr};
-      k_gather<<<gather_grid(KT_), kThreads, 0, stream_>>>(KT_, g, Sd);
-    }
-    k_dual_side<true, false><<<KT_.ntiles, kThreads, 0, stream_>>>(KT_, B, Pd, Sd);
+    k_dual_side<true, false><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, B, Pd, Sd);
   }
   if (m_) {
-    if (K_.nnz) {
-      GatherArgs g{vref(upool_.as<double>() + 2 * N_), prod_.as<double>(), 0, nullptr};
-      k_gather<<<gather_grid(K_), kThreads, 0, stream_>>>(K_, g, Sd);
-    }
-    k_primal_side<true, false><<<K_.ntiles, kThreads, 0, stream_>>>(K_, B, Pd, Sd);
+    k_primal_side<true, false><<<K_.grid(), kThreads, 0, stream_>>>(K_, B, Pd, Sd);
   }
   AAPDHG_CUDA(cudaGetLastError());
   const double* hat = upool_.as<double>() + 2 * N_;
@@ -949,7 +943,7 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
   SolveScratch W{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
   IterBufs B{upool_.as<double>(), kxpool_.as<double>(), gpool_.as<double>(), du_.as<double>(),
              dg_.as<double>(), T_.as<double>(), part1_.as<double>(), part2_.as<double>(),
-             prod_.as<double>(), c_.as<double>(), q_.as<double>(), l_.as<double>(),
+             c_.as<double>(), q_.as<double>(), l_.as<double>(),
              u_.as<double>()};
   const DevParams* Pd = dparams_.as<DevParams>();
   DevState* Sd = dstate_.as<DevState>();

@@ -66,10 +66,12 @@ class Problem {
   double device_dot(const double* a, const double* b, int64_t n, bool serial);
   int spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const RowsumArgs& o, bool serial,
            const DevState* S, int pred, const int32_t* stop);
-  int gather_grid(const CsrDev& A) const;
   static size_t aa_smem(int cap);
+  struct CsrStore {
+    DevBuf rp, ci, v, sl_ptr, sl_len, sl_row, sci, sv, longs;
+  };
   void upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
-                  DevBuf& d_rp, DevBuf& d_ci, DevBuf& d_v, DevBuf& d_meta, CsrDev& out);
+                  CsrStore& st, CsrDev& out);
   void ensure_iter_buffers(int method, int cap);
   void upload_iterate(int slot, const double* x, const double* y);
   void kkt_eval(int slot, bool serial, double* kkt_dev_out, double* lam_dev);
@@ -103,8 +105,9 @@ class Problem {
   bool all_zero_ = true;
   bool bounds_ok_ = true;
   CsrDev K_, KT_;
-  DevBuf k_rp_, k_ci_, k_v_, k_tile_, t_rp_, t_ci_, t_v_, t_tile_;
-  DevBuf c_, q_, l_, u_, prod_;
+  CsrStore k_store_, t_store_;
+  size_t sell_bytes_ = 0;
+  DevBuf c_, q_, l_, u_;
   double nrm_q_[2] = {0, 0}, nrm_c_[2] = {0, 0};  // [serial, tree]
 
   // iteration buffers

@@ -114,47 +114,24 @@ __device__ __forceinline__ double serial_dot(const double* __restrict__ a,
 }
 
 // ---------------------------------------------------------------------------
-// SpMV = gather-multiply pass + row-block reduce pass
+// SpMV core: SELL-32 slices of the short rows + warp-per-row long rows
 // ---------------------------------------------------------------------------
 //
 // Random-column SpMVs on B200 are bound by the L1TEX gather rate (~0.85
-// cycles per random 8-byte gather per SM, measured: profiles/microbench),
-// which needs ~512 gathers in flight per SM. So each SpMV is two kernels:
-//   k_gather   prod[e] = vals[e] * x[col[e]] over all nonzeros — lean
-//              (<= 32 registers, 2048 threads/SM, 8 gathers in flight per
-//              thread), nnz-parallel, hence perfectly load balanced for any
-//              row-length distribution (Zipf, transport rows);
-//   row kernels  CSR row blocks (<= kTile nonzeros, <= kRowsPerBlock rows;
-//              a longer row is a block of its own) staged by cp.async from
-//              the L2-resident products: thread r adds row r0 + r in CSR
-//              order — bit-identical to the reference's row-serial matvec
-//              (sparse_linalg.cpp:60-69) and, on the transposed CSR (entries
-//              in ascending original row), to its row-ordered scatter
-//              matvec_transpose (sparse_linalg.cpp:77-87) — then runs the
-//              fused PDHG epilogue of that row.
+// cycles per random 8-byte gather per SM when ~400+ gathers are in flight
+// per SM; measured, profiles/microbench/gather_bench.cu). The matrix is
+// therefore stored (once, on upload) in a sliced layout: consecutive short
+// rows are grouped 32 to a slice and element k of the slice's lane-r row
+// sits at sl_ptr[s] + 32 k + r. A warp owns a slice: its (col, val) loads
+// are coalesced, each lane keeps 8 gathers x[col] in flight and adds its
+// row's products sequentially in CSR order — bit-identical to the
+// reference's row-serial matvec (sparse_linalg.cpp:60-69) and, on the
+// transposed CSR (entries in ascending original row), to its row-ordered
+// scatter matvec_transpose (sparse_linalg.cpp:77-87). No shared memory, no
+// barrier, no product buffer. Rows longer than kLongRow are handled one per
+// warp by extra CTAs of the same launch (grid = short blocks + long blocks).
 
-constexpr int kTile = 2048;          // nonzeros per row block
-constexpr int kRowsPerBlock = kThreads;
-constexpr int kGatherBlocksPerSM = 8;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g));
-}
-__device__ __forceinline__ void cp_async8(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(s)), "l"(g));
-}
-__device__ __forceinline__ void cp_async4(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
+// Plain SpMV output / input references (power iteration, recache, matvec).
 __device__ __forceinline__ bool skip_launch(const DevState* S, int pred_aa_ok,
                                             const int32_t* stop) {
   if (S) {
@@ -164,130 +141,80 @@ __device__ __forceinline__ bool skip_launch(const DevState* S, int pred_aa_ok,
   return stop && *stop;
 }
 
-// prod[e] = vals[e] * x[col[e]]: 8 coalesced (col, val) loads, then 8
-// independent gathers per thread in flight; matrix streams evict-first.
-__global__ void __launch_bounds__(kThreads, kGatherBlocksPerSM)
-    k_gather(CsrDev A, GatherArgs g, const DevState* S) {
-  if (skip_launch(S, g.pred_aa_ok, g.stop)) return;
-  const double* __restrict__ x = g.x.get(S);
-  double* __restrict__ prod = g.prod;
-  const int64_t nnz = A.nnz;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + 7 * stride < nnz; i += 8 * stride) {
-    int c[8];
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      c[u] = __ldcs(A.ci + i + u * stride);
-      v[u] = __ldcs(A.v + i + u * stride);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __dmul_rn(v[u], __ldg(x + c[u]));
-#pragma unroll
-    for (int u = 0; u < 8; ++u) prod[i + u * stride] = v[u];
-  }
-  for (; i < nnz; i += stride) prod[i] = __dmul_rn(__ldcs(A.v + i), __ldg(x + __ldcs(A.ci + i)));
-}
+constexpr int kUnroll = 4;  // gathers in flight per lane (x 48 warps per SM)
 
-__device__ __forceinline__ bool block_is_long(const int4& m) {
-  return (m.y - m.x == 1) && (m.w - m.z > kTile);
-}
-
-// Shared-memory stage of a row block: the 16-byte aligned superset of
-// prod[e0, e1) (offset e0 & 1), the row offsets and NE epilogue operands.
-template <int NE>
-struct __align__(16) RowStage {
-  double prod[kTile + 2];
-  int32_t rp[kRowsPerBlock + 4];
-  double epi[NE > 0 ? NE : 1][kRowsPerBlock];
-};
-
-// Copies row block m into st (cp.async, all threads), waits, syncs.
-template <int NE>
-__device__ __forceinline__ void stage_rows(const int4& m, const int32_t* __restrict__ rp,
-                                           const double* __restrict__ prod, RowStage<NE>& st,
-                                           const double* const* src) {
-  const int r0 = m.x, r1 = m.y, e0 = m.z, e1 = m.w, nr = r1 - r0;
-  const int a0 = e0 & ~1, nv = (e1 - a0 + 1) >> 1;
-  for (int k = threadIdx.x; k < nv; k += blockDim.x) cp_async16(&st.prod[2 * k], prod + a0 + 2 * k);
-  for (int i = threadIdx.x; i <= nr; i += blockDim.x) cp_async4(&st.rp[i], rp + r0 + i);
-#pragma unroll
-  for (int q = 0; q < NE; ++q)
-    for (int i = threadIdx.x; i < nr; i += blockDim.x) cp_async8(&st.epi[q][i], src[q] + r0 + i);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-}
-
-// Sum of one long row (> kTile nonzeros) by the whole CTA, kTile chunks:
-// SERIAL adds every product in CSR order in thread 0 (bitwise = reference),
-// TREE adds fixed per-chunk block trees in order. Valid in thread 0.
-template <bool SERIAL, int NE>
-__device__ double long_row_sum(const int4& m, const double* __restrict__ prod,
-                               RowStage<NE>& st, double* red) {
-  double s = 0.0;
-  for (int c0 = m.z; c0 < m.w; c0 += kTile) {
-    const int c1 = min(m.w, c0 + kTile);
-    const int a0 = c0 & ~1, nv = (c1 - a0 + 1) >> 1, vo = c0 & 1;
-    for (int k = threadIdx.x; k < nv; k += blockDim.x) cp_async16(&st.prod[2 * k], prod + a0 + 2 * k);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    if (SERIAL) {
-      if (threadIdx.x == 0)
-        for (int t = 0; t < c1 - c0; ++t) s = __dadd_rn(s, st.prod[vo + t]);
-    } else {
-      double v[1] = {0.0};
-      for (int t = threadIdx.x; t < c1 - c0; t += blockDim.x) v[0] = __dadd_rn(v[0], st.prod[vo + t]);
-      block_sum<1>(v, red);
-      if (threadIdx.x == 0) s = __dadd_rn(s, v[0]);
-    }
-    __syncthreads();
-  }
-  return s;
-}
-
-// Row sums of row block b. Returns this thread's row (-1 if none) with its
-// sum in s and `from_stage` telling whether the epilogue operands are staged.
-template <bool SERIAL, int NE>
-__device__ __forceinline__ int block_rows(const CsrDev& A, const double* __restrict__ prod,
-                                          RowStage<NE>& st, const double* const* src,
-                                          double* red, double& s, bool& from_stage) {
-  const int4 m = A.meta[blockIdx.x];
+// Row sum of the row owned by (warp, lane) of this CTA; returns the row or
+// -1. SERIAL only matters for long rows: lane 0 adds in CSR order (bitwise)
+// instead of the fixed warp tree.
+template <bool SERIAL>
+__device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, int warp,
+                                       int lane, double& s) {
   s = 0.0;
-  if (block_is_long(m)) {
-    from_stage = false;
-    s = long_row_sum<SERIAL, NE>(m, prod, st, red);
-    return threadIdx.x == 0 ? m.x : -1;
+  if ((int)blockIdx.x < A.nblk_short) {
+    const int sl = blockIdx.x * kWarps + warp;
+    if (sl >= A.nslices) return -1;
+    const int row = __ldg(A.sl_row + sl * 32 + lane);
+    const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
+    const int L = __ldg(A.sl_len + sl);
+    const int64_t base = __ldg(A.sl_ptr + sl) + lane;
+    double acc = 0.0;
+    for (int k0 = 0; k0 < L; k0 += kUnroll) {
+      int c[kUnroll];
+      double v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (k0 + u < len) {
+          c[u] = __ldcs(A.sci + base + 32 * (k0 + u));
+          v[u] = __ldcs(A.sv + base + 32 * (k0 + u));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (k0 + u < len) v[u] = __dmul_rn(v[u], __ldg(x + c[u]));
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (k0 + u < len) acc = __dadd_rn(acc, v[u]);
+    }
+    s = acc;
+    return row;
   }
-  from_stage = true;
-  stage_rows<NE>(m, A.rp, prod, st, src);
-  const int r = threadIdx.x;
-  if (r >= m.y - m.x) return -1;
-  const int vo = m.z & 1;
-  const int a = st.rp[r] - m.z, z = st.rp[r + 1] - m.z;
+  const int lr = (blockIdx.x - A.nblk_short) * kWarps + warp;
+  if (lr >= A.nlong) return -1;
+  const int row = __ldg(A.long_rows + lr);
+  const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
   double acc = 0.0;
-  for (int e = a; e < z; ++e) acc = __dadd_rn(acc, st.prod[vo + e]);
+  for (int64_t e = e0 + lane; e - lane < e1; e += 32) {
+    const double p = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
+    if (SERIAL) {  // CSR order through lane 0
+      const int64_t rem = e1 - (e - lane);
+      const int cnt = rem < 32 ? (int)rem : 32;
+      for (int j = 0; j < cnt; ++j) {
+        const double t = __shfl_sync(0xffffffffu, p, j);
+        if (lane == 0) acc = __dadd_rn(acc, t);
+      }
+    } else {
+      if (e < e1) acc = __dadd_rn(acc, p);
+    }
+  }
+  if (!SERIAL) acc = warp_sum(acc);
   s = acc;
-  return m.x + r;
+  return lane == 0 ? row : -1;
 }
 
 template <bool SERIAL>
-__global__ void __launch_bounds__(kThreads) k_rowsum(CsrDev A, RowsumArgs g, const DevState* S) {
-  if (skip_launch(S, g.pred_aa_ok, g.stop)) return;
-  __shared__ RowStage<0> st;
-  __shared__ double red[kWarps];
-  double* out = g.out_pool ? g.out_pool + (int64_t)S->kx_idx[g.out_role] * g.out_stride : g.out;
-  const double* const src[1] = {nullptr};
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+    k_spmv(CsrDev A, VecRef xr, RowsumArgs o, const DevState* S) {
+  if (skip_launch(S, o.pred_aa_ok, o.stop)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* x = xr.get(S);
+  double* out = o.out_pool ? o.out_pool + (int64_t)S->kx_idx[o.out_role] * o.out_stride : o.out;
   double s;
-  bool fs;
-  const int row = block_rows<SERIAL, 0>(A, g.prod, st, src, red, s, fs);
+  const int row = row_sum<SERIAL>(A, x, warp, lane, s);
   if (row >= 0) out[row] = s;
 }
 
 // ---------------------------------------------------------------------------
-// the fused PDHG halves (row kernels)
+// the fused PDHG halves
 // ---------------------------------------------------------------------------
 
 struct IterBufs {
@@ -299,50 +226,33 @@ struct IterBufs {
   double* T;       // n
   double* part1;   // P1_COUNT x nblk1
   double* part2;   // P2_COUNT x nblk2
-  double* prod;    // max(nnz) products of the current SpMV
   const double* c;
   const double* q;
   const double* l;
   const double* u;
 };
 
-// K1 row kernel on K' (row j of K' = column j of K), t = (K'y)_j:
+// K1 on K' (row j of K' = column j of K), t = (K'y)_j:
 //   xhat_j = min(max(x_j - tau (c_j - t), l_j), u_j)      pdhg_core.cpp:49-53
 //   lambda_j = P_Lambda(c_j - t)                           solver.cpp:67-71
 //   partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
 //   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
-  constexpr int NE = PUSH ? 6 : 4;
-  __shared__ RowStage<NE> st;
   __shared__ double red[P1_COUNT * kWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-  const double* src[NE];
-  src[0] = x;
-  src[1] = B.c;
-  src[2] = B.l;
-  src[3] = B.u;
-  if constexpr (PUSH) {
-    src[4] = B.upool + (int64_t)S->u_idx[U_PREV] * N;
-    src[5] = B.gpool + (int64_t)S->g_idx[G_PREV] * N;
-  }
   double t;
-  bool fs;
-  const int j = block_rows<SERIAL, NE>(KT, B.prod, st, src, red, t, fs);
+  const int j = row_sum<SERIAL>(KT, x + P->n, warp, lane, t);
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
   if (j >= 0) {
-    const int r = fs ? (int)threadIdx.x : 0;
-    const double xj = fs ? st.epi[0][r] : src[0][j];
-    const double cj = fs ? st.epi[1][r] : src[1][j];
-    const double lj = fs ? st.epi[2][r] : src[2][j];
-    const double uj = fs ? st.epi[3][r] : src[3][j];
-    double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+    const double xj = x[j], cj = __ldg(B.c + j), lj = __ldg(B.l + j), uj = __ldg(B.u + j);
     double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));
     xn = smin(smax(xn, lj), uj);
-    xh[j] = xn;
+    B.upool[(int64_t)S->u_idx[U_HAT] * N + j] = xn;
     const double d = __dsub_rn(xn, xj);
     const double red_c = __dsub_rn(cj, t);
     const double lam = project_lambda1(red_c, lj, uj);
@@ -356,8 +266,8 @@ __global__ void __launch_bounds__(kThreads)
     acc[P1_CX] = __dmul_rn(cj, xj);
     if constexpr (PUSH) {
       const int64_t slot = S->push_slot;
-      const double xp = fs ? st.epi[4][r] : src[4][j];
-      const double gp = fs ? st.epi[5][r] : src[5][j];
+      const double xp = B.upool[(int64_t)S->u_idx[U_PREV] * N + j];
+      const double gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + j];
       B.du[slot * N + j] = __dsub_rn(xj, xp);
       B.dg[slot * N + j] = __dsub_rn(d, gp);
       B.gpool[(int64_t)S->g_idx[G_CUR] * N + j] = d;
@@ -475,39 +385,28 @@ __device__ __forceinline__ void control_from_partials(const IterBufs& B, const D
   state_store(S, &sm);
 }
 
-// K2 row kernel on K, s = (K xhat)_i:
+// K2 on K, s = (K xhat)_i:
 //   yhat_i = y_i + sigma (q_i - (2 s - (K x)_i)), clamped >= 0 for i < m1
 //                                                         pdhg_core.cpp:55-60
 //   K xhat cached as the next K x (solver.cpp:90 / pdhg_core.cpp:56)
 //   partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
 // TREE: the last CTA to finish reduces every partial and runs the control.
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
-  constexpr int NE = PUSH ? 5 : 3;
-  __shared__ RowStage<NE> st;
   __shared__ double red[P2_COUNT * kWarps];
   __shared__ int is_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t N = P->N;
   const int n = P->n, mr = P->mrows;
-  const double* src[NE];
-  src[0] = B.upool + (int64_t)S->u_idx[U_CUR] * N + n;
-  src[1] = B.q;
-  src[2] = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
-  if constexpr (PUSH) {
-    src[3] = B.upool + (int64_t)S->u_idx[U_PREV] * N + n;
-    src[4] = B.gpool + (int64_t)S->g_idx[G_PREV] * N + n;
-  }
   double s;
-  bool fs;
-  const int i = block_rows<SERIAL, NE>(K, B.prod, st, src, red, s, fs);
+  const int i = row_sum<SERIAL>(K, B.upool + (int64_t)S->u_idx[U_HAT] * N, warp, lane, s);
   double acc[P2_COUNT] = {0.0, 0.0, 0.0};
   if (i >= 0) {
-    const int r = fs ? (int)threadIdx.x : 0;
-    const double yi = fs ? st.epi[0][r] : src[0][i];
-    const double qi = fs ? st.epi[1][r] : src[1][i];
-    const double kxi = fs ? st.epi[2][r] : src[2][i];
+    const double yi = B.upool[(int64_t)S->u_idx[U_CUR] * N + n + i];
+    const double qi = __ldg(B.q + i);
+    const double kxi = B.kxpool[(int64_t)S->kx_idx[KX_CUR] * mr + i];
     double yn =
         __dadd_rn(yi, __dmul_rn(P->sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
     if (i < P->m1) yn = smax(yn, 0.0);
@@ -521,8 +420,8 @@ __global__ void __launch_bounds__(kThreads)
     acc[P2_INFEAS] = __dmul_rn(v, v);
     if constexpr (PUSH) {
       const int64_t slot = S->push_slot;
-      const double yp = fs ? st.epi[3][r] : src[3][i];
-      const double gp = fs ? st.epi[4][r] : src[4][i];
+      const double yp = B.upool[(int64_t)S->u_idx[U_PREV] * N + n + i];
+      const double gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + n + i];
       B.du[slot * N + n + i] = __dsub_rn(yi, yp);
       B.dg[slot * N + n + i] = __dsub_rn(d, gp);
       B.gpool[(int64_t)S->g_idx[G_CUR] * N + n + i] = d;
