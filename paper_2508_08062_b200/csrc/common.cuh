@@ -61,11 +61,12 @@ struct CsrDev {
   const double* sv = nullptr;
   const int32_t* long_rows = nullptr;
   int32_t nblk_short = 0, nblk_long = 0;
+  int32_t sf = 1;  // lanes per row in the slices (1 = CSR-ordered row sums)
   int32_t grid() const { return nblk_short + nblk_long; }
 };
 
 constexpr int kLongRow = 256;        // rows longer than this get a warp each
-constexpr int kSpmvBlocksPerSM = 6;  // register budget of the SpMV kernels
+constexpr int kSpmvBlocksPerSM = 5;  // register budget of the SpMV kernels (51 regs)
 
 // Constant per solve (written before the loop starts).
 struct DevParams {

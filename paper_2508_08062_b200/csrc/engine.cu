@@ -76,23 +76,24 @@ struct SolveSetup {
   int method, cap, nblk1, nblk2, ndot_blk, items_max;
 };
 
-// Uploads one CSR and its SELL-32 slices of the short rows (see CsrDev).
-void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows,
-                         int ncols, CsrStore& st, CsrDev& out) {
-  const int64_t nnz = rp[nrows];
-  std::vector<int32_t> shorts, longs;
-  shorts.reserve(size_t(nrows));
-  for (int r = 0; r < nrows; ++r) (rp[r + 1] - rp[r] > kLongRow ? longs : shorts).push_back(r);
-  const int nslices = int((shorts.size() + 31) / 32);
+// SELL-32 slices of the short rows with split factor sf (see CsrDev):
+// slice = 32 / sf rows; element k of the slice's row rho sits at
+// sl_ptr + 32 (k / sf) + rho sf + (k % sf).
+void Problem::build_sell(const int32_t* rp, const int32_t* ci, const double* v,
+                         const std::vector<int32_t>& shorts, int sf, SellStore& st,
+                         CsrDev& out) {
+  const int R = 32 / sf;
+  const int nslices = int((shorts.size() + R - 1) / R);
   std::vector<int64_t> sl_ptr(size_t(std::max(nslices, 1)));
-  std::vector<int32_t> sl_len(size_t(std::max(nslices, 1))), sl_row(size_t(std::max(nslices, 1)) * 32, -1);
+  std::vector<int32_t> sl_len(size_t(std::max(nslices, 1))),
+      sl_row(size_t(std::max(nslices, 1)) * 32, -1);
   int64_t total = 0;
   for (int s = 0; s < nslices; ++s) {
     int L = 0;
-    for (int r = 0; r < 32 && size_t(s) * 32 + r < shorts.size(); ++r) {
-      const int row = shorts[size_t(s) * 32 + r];
-      sl_row[size_t(s) * 32 + r] = row;
-      L = std::max(L, rp[row + 1] - rp[row]);
+    for (int r = 0; r < R && size_t(s) * R + r < shorts.size(); ++r) {
+      const int row = shorts[size_t(s) * R + r];
+      for (int j = 0; j < sf; ++j) sl_row[size_t(s) * 32 + r * sf + j] = row;
+      L = std::max(L, (rp[row + 1] - rp[row] + sf - 1) / sf);
     }
     sl_ptr[size_t(s)] = total;
     sl_len[size_t(s)] = L;
@@ -101,52 +102,88 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
   std::vector<int32_t> sci(size_t(std::max<int64_t>(total, 1)), 0);
   std::vector<double> sv(size_t(std::max<int64_t>(total, 1)), 0.0);
   for (int s = 0; s < nslices; ++s)
-    for (int r = 0; r < 32; ++r) {
-      const int row = sl_row[size_t(s) * 32 + r];
-      if (row < 0) continue;
+    for (int r = 0; r < R && size_t(s) * R + r < shorts.size(); ++r) {
+      const int row = shorts[size_t(s) * R + r];
       for (int k = 0; k < rp[row + 1] - rp[row]; ++k) {
-        const size_t dst = size_t(sl_ptr[size_t(s)] + 32 * int64_t(k) + r);
+        const size_t dst = size_t(sl_ptr[size_t(s)] + 32 * int64_t(k / sf) + r * sf + k % sf);
         sci[dst] = ci[rp[row] + k];
         sv[dst] = v[rp[row] + k];
       }
     }
-  st.rp.reserve(sizeof(int32_t) * (nrows + 1));
-  st.ci.reserve(sizeof(int32_t) * nnz);
-  st.v.reserve(sizeof(double) * nnz);
   st.sl_ptr.reserve(sizeof(int64_t) * sl_ptr.size());
   st.sl_len.reserve(sizeof(int32_t) * sl_len.size());
   st.sl_row.reserve(sizeof(int32_t) * sl_row.size());
   st.sci.reserve(sizeof(int32_t) * sci.size());
   st.sv.reserve(sizeof(double) * sv.size());
-  st.longs.reserve(sizeof(int32_t) * std::max<size_t>(longs.size(), 1));
-  h2d(st.rp.p, rp, sizeof(int32_t) * (nrows + 1), stream_);
-  h2d(st.ci.p, ci, sizeof(int32_t) * nnz, stream_);
-  h2d(st.v.p, v, sizeof(double) * nnz, stream_);
   h2d(st.sl_ptr.p, sl_ptr.data(), sizeof(int64_t) * sl_ptr.size(), stream_);
   h2d(st.sl_len.p, sl_len.data(), sizeof(int32_t) * sl_len.size(), stream_);
   h2d(st.sl_row.p, sl_row.data(), sizeof(int32_t) * sl_row.size(), stream_);
   h2d(st.sci.p, sci.data(), sizeof(int32_t) * sci.size(), stream_);
   h2d(st.sv.p, sv.data(), sizeof(double) * sv.size(), stream_);
-  h2d(st.longs.p, longs.data(), sizeof(int32_t) * longs.size(), stream_);
   sync();  // host staging vectors go out of scope
   sell_bytes_ += (sizeof(int32_t) + sizeof(double)) * size_t(total);
-  out = CsrDev{};
-  out.nrows = nrows;
-  out.ncols = ncols;
-  out.nnz = nnz;
-  out.rp = st.rp.as<int32_t>();
-  out.ci = st.ci.as<int32_t>();
-  out.v = st.v.as<double>();
   out.nslices = nslices;
-  out.nlong = int32_t(longs.size());
   out.sl_ptr = st.sl_ptr.as<int64_t>();
   out.sl_len = st.sl_len.as<int32_t>();
   out.sl_row = st.sl_row.as<int32_t>();
   out.sci = st.sci.as<int32_t>();
   out.sv = st.sv.as<double>();
-  out.long_rows = st.longs.as<int32_t>();
-  out.nblk_short = (nslices + kWarps - 1) / kWarps;
-  out.nblk_long = (out.nlong + kWarps - 1) / kWarps;
+  out.sf = sf;
+  const int64_t want = (int64_t(nslices) + kWarps - 1) / kWarps;
+  out.nblk_short = int32_t(std::min<int64_t>(want, int64_t(num_sms_) * kSpmvBlocksPerSM));
+}
+
+// Uploads one CSR with its two sliced layouts: `ser` (sf = 1, CSR-ordered
+// row sums for the SERIAL mode) and `tree` (sf chosen so the slices fill
+// ~48 warps on every SM; aliases `ser` when sf = 1).
+void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows,
+                         int ncols, CsrStore& st, CsrDev& ser, CsrDev& tree) {
+  const int64_t nnz = rp[nrows];
+  std::vector<int32_t> shorts, longs;
+  shorts.reserve(size_t(nrows));
+  int64_t short_nnz = 0;
+  for (int r = 0; r < nrows; ++r) {
+    const int len = rp[r + 1] - rp[r];
+    if (len > kLongRow) {
+      longs.push_back(r);
+    } else {
+      shorts.push_back(r);
+      short_nnz += len;
+    }
+  }
+  st.rp.reserve(sizeof(int32_t) * (nrows + 1));
+  st.ci.reserve(sizeof(int32_t) * nnz);
+  st.v.reserve(sizeof(double) * nnz);
+  st.longs.reserve(sizeof(int32_t) * std::max<size_t>(longs.size(), 1));
+  h2d(st.rp.p, rp, sizeof(int32_t) * (nrows + 1), stream_);
+  h2d(st.ci.p, ci, sizeof(int32_t) * nnz, stream_);
+  h2d(st.v.p, v, sizeof(double) * nnz, stream_);
+  h2d(st.longs.p, longs.data(), sizeof(int32_t) * longs.size(), stream_);
+  CsrDev base{};
+  base.nrows = nrows;
+  base.ncols = ncols;
+  base.nnz = nnz;
+  base.rp = st.rp.as<int32_t>();
+  base.ci = st.ci.as<int32_t>();
+  base.v = st.v.as<double>();
+  base.nlong = int32_t(longs.size());
+  base.long_rows = st.longs.as<int32_t>();
+  base.nblk_long = (base.nlong + kWarps - 1) / kWarps;
+  // split factor: enough slices for ~48 warps per SM, no more lanes than
+  // a quarter of the mean row length
+  const double mean = shorts.empty() ? 0.0 : double(short_nnz) / double(shorts.size());
+  int sf = 1;
+  while (sf < 8 && double(shorts.size()) * sf / 32.0 < double(num_sms_) * 48.0 &&
+         mean >= 4.0 * (2 * sf))
+    sf *= 2;
+  ser = base;
+  build_sell(rp, ci, v, shorts, 1, st.sell[0], ser);
+  tree = base;
+  if (sf == 1) {
+    tree = ser;
+  } else {
+    build_sell(rp, ci, v, shorts, sf, st.sell[1], tree);
+  }
 }
 
 // out = A x (CSR-ordered row sums).
@@ -217,7 +254,7 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
 
   // K, padded so 16-byte cp.async of a tile's aligned superset stays in bounds
   AAPDHG_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device));
-  upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, K_);
+  upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
   // K' as CSR, entries of each row in ascending original row (counting sort)
   std::vector<int32_t> trp(static_cast<size_t>(n_) + 1, 0), tci(static_cast<size_t>(nnz_));
   std::vector<double> tv(static_cast<size_t>(nnz_));
@@ -232,7 +269,7 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
         tv[size_t(pos)] = k.vals[e];
       }
   }
-  upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_store_, KT_);
+  upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_store_, KTs_, KTt_);
 
   c_.reserve(sizeof(double) * n_);
   q_.reserve(sizeof(double) * m_);
@@ -311,7 +348,7 @@ double Problem::device_dot(const double* a, const double* b, int64_t n, bool ser
 }
 
 void Problem::ensure_iter_buffers(int method, int cap) {
-  const int nblk1 = KT_.grid(), nblk2 = K_.grid();
+  const int nblk1 = std::max(KTs_.grid(), KTt_.grid()), nblk2 = std::max(Ks_.grid(), Kt_.grid());
   upool_.reserve(sizeof(double) * 4 * std::max<int64_t>(N_, 1));
   kxpool_.reserve(sizeof(double) * 3 * std::max<int64_t>(m_, 1));
   T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
@@ -348,8 +385,8 @@ void Problem::kkt_eval(int slot, bool serial, double* out_dev, double* lam_dev) 
   const double* y = x + n_;
   double* T = T_.as<double>();
   double* KX = pw_mx_.as<double>();
-  if (n_) spmv(stream_, KT_, vref(y), rout(T), serial, nullptr, 0, nullptr);
-  if (m_) spmv(stream_, K_, vref(x), rout(KX), serial, nullptr, 0, nullptr);
+  if (n_) spmv(stream_, KTm(serial), vref(y), rout(T), serial, nullptr, 0, nullptr);
+  if (m_) spmv(stream_, Km(serial), vref(x), rout(KX), serial, nullptr, 0, nullptr);
   const int64_t nbig = std::max<int64_t>(std::max<int64_t>(n_, m_), 1);
   const int nb = int((nbig + kThreads - 1) / kThreads);
   k_kkt_terms<<<nb, kThreads, 0, stream_>>>(x, y, T, KX, c_.as<double>(), q_.as<double>(),
@@ -423,17 +460,17 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   const bool ser = su.serial, push = su.push;
   // K'y: products of K' with y = u_cur[n:], then the fused dual-side rows
   if (n_ > 0) {
-    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KT_.grid(), kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KT_.grid(), kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KT_.grid(), kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
-    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KT_.grid(), kThreads, 0, s>>>(KT_, su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
   }
   // K xhat: products of K with xhat = u_hat[:n], then the fused dual step
   if (m_ > 0) {
-    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<K_.grid(), kThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<K_.grid(), kThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<K_.grid(), kThreads, 0, s>>>(K_, su.B, su.P, su.S));
-    else LAUNCH("k_primal_side", k_primal_side<false, false><<<K_.grid(), kThreads, 0, s>>>(K_, su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else LAUNCH("k_primal_side", k_primal_side<false, false><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
   }
   if (ser) LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
   AAPDHG_CUDA(cudaGetLastError());
@@ -456,7 +493,7 @@ int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
     r.out_pool = su.B.kxpool;
     r.out_role = KX_CAND;
     r.out_stride = m_;
-    nodes += spmv(s, K_, VecRef{nullptr, su.B.upool, U_CAND, N_, 0}, r, su.serial, su.S, 1,
+    nodes += spmv(s, Km(su.serial), VecRef{nullptr, su.B.upool, U_CAND, N_, 0}, r, su.serial, su.S, 1,
                   nullptr);
   }
   LAUNCH("k_aa_commit", k_aa_commit<<<1, 128, 0, s>>>(su.P, su.S));
@@ -558,8 +595,8 @@ void Problem::run_power(const double* x0, int max_iters, double rel_tol, bool se
   PowerState hs{};
   for (;;) {
     for (int r = 0; r < kPowerBatch; ++r) {
-      spmv(stream_, K_, vref(x), rout(mx), serial, nullptr, 0, &ps->done);
-      spmv(stream_, KT_, vref(mx), rout(mtmx), serial, nullptr, 0, &ps->done);
+      spmv(stream_, Km(serial), vref(x), rout(mx), serial, nullptr, 0, &ps->done);
+      spmv(stream_, KTm(serial), vref(mx), rout(mtmx), serial, nullptr, 0, &ps->done);
       if (!serial) k_sumsq_partials<<<nb, kThreads, 0, stream_>>>(mtmx, nullptr, n_, part, &ps->done);
       k_power_ctrl<<<1, kCtrlThreads, 0, stream_>>>(mtmx, n_, part, nb, serial, ps);
       k_scale<<<grid_for(n_), kThreads, 0, stream_>>>(x, mtmx, n_, ps, nullptr);
@@ -671,8 +708,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.pow_len = ptab.size();
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
-  P.nblk1 = KT_.grid();
-  P.nblk2 = K_.grid();
+  P.nblk1 = KTm(serial).grid();
+  P.nblk2 = Km(serial).grid();
   P.ndot_blk = ndot_tile_;
 
   DevState S0{};
@@ -696,8 +733,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.push = method != AAPDHG_METHOD_PDHG;
   su.method = method;
   su.cap = cap;
-  su.nblk1 = KT_.grid();
-  su.nblk2 = K_.grid();
+  su.nblk1 = KTm(serial).grid();
+  su.nblk2 = Km(serial).grid();
   su.ndot_blk = ndot_tile_;
   su.items_max = num_items_host(std::max(cap, 1), method);
 
@@ -737,7 +774,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   h2d(S, &S0, sizeof S0, stream_);
   k_project_start<<<grid_for(N_, kThreads, 1 << 30), kThreads, 0, stream_>>>(
       upool_.as<double>(), l_.as<double>(), u_.as<double>(), n_, N_, m1_, S);
-  if (m_) spmv(stream_, K_, vref(upool_.as<double>()), rout(kxpool_.as<double>()), serial, nullptr, 0,
+  if (m_) spmv(stream_, Km(serial), vref(upool_.as<double>()), rout(kxpool_.as<double>()), serial, nullptr, 0,
                nullptr);
   AAPDHG_CUDA(cudaGetLastError());
 
@@ -815,7 +852,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
 void Problem::matvec(const double* x, double* out) {
   AAPDHG_CUDA(cudaSetDevice(device_));
   h2d(pw_x_.p, x, sizeof(double) * n_, stream_);
-  spmv(stream_, K_, vref(pw_x_.as<double>()), rout(pw_mx_.as<double>()), true, nullptr, 0,
+  spmv(stream_, Ks_, vref(pw_x_.as<double>()), rout(pw_mx_.as<double>()), true, nullptr, 0,
        nullptr);
   d2h(out, pw_mx_.p, sizeof(double) * m_, stream_);
   sync();
@@ -824,7 +861,7 @@ void Problem::matvec(const double* x, double* out) {
 void Problem::matvec_transpose(const double* y, double* out) {
   AAPDHG_CUDA(cudaSetDevice(device_));
   h2d(pw_mx_.p, y, sizeof(double) * m_, stream_);
-  spmv(stream_, KT_, vref(pw_mx_.as<double>()), rout(pw_mtmx_.as<double>()), true, nullptr, 0,
+  spmv(stream_, KTs_, vref(pw_mx_.as<double>()), rout(pw_mtmx_.as<double>()), true, nullptr, 0,
        nullptr);
   d2h(out, pw_mtmx_.p, sizeof(double) * n_, stream_);
   sync();
@@ -845,7 +882,7 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   AAPDHG_CUDA(cudaSetDevice(device_));
   ensure_iter_buffers(AAPDHG_METHOD_PDHG, 1);
   upload_iterate(0, x, y);
-  spmv(stream_, K_, vref(upool_.as<double>()), rout(kxpool_.as<double>()), true, nullptr, 0,
+  spmv(stream_, Ks_, vref(upool_.as<double>()), rout(kxpool_.as<double>()), true, nullptr, 0,
        nullptr);
   DevParams P{};
   P.method = AAPDHG_METHOD_PDHG;
@@ -856,8 +893,8 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   P.N = N_;
   P.tau = tau;
   P.sigma = sigma;
-  P.nblk1 = KT_.grid();
-  P.nblk2 = K_.grid();
+  P.nblk1 = KTs_.grid();
+  P.nblk2 = Ks_.grid();
   const DevState S = identity_state();
   h2d(dparams_.p, &P, sizeof P, stream_);
   h2d(dstate_.p, &S, sizeof S, stream_);
@@ -867,10 +904,10 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   const DevParams* Pd = dparams_.as<DevParams>();
   DevState* Sd = dstate_.as<DevState>();
   if (n_) {
-    k_dual_side<true, false><<<KT_.grid(), kThreads, 0, stream_>>>(KT_, B, Pd, Sd);
+    k_dual_side<true, false><<<KTs_.grid(), kThreads, 0, stream_>>>(KTs_, B, Pd, Sd);
   }
   if (m_) {
-    k_primal_side<true, false><<<K_.grid(), kThreads, 0, stream_>>>(K_, B, Pd, Sd);
+    k_primal_side<true, false><<<Ks_.grid(), kThreads, 0, stream_>>>(Ks_, B, Pd, Sd);
   }
   AAPDHG_CUDA(cudaGetLastError());
   const double* hat = upool_.as<double>() + 2 * N_;

@@ -67,11 +67,19 @@ class Problem {
   int spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const RowsumArgs& o, bool serial,
            const DevState* S, int pred, const int32_t* stop);
   static size_t aa_smem(int cap);
-  struct CsrStore {
-    DevBuf rp, ci, v, sl_ptr, sl_len, sl_row, sci, sv, longs;
+  struct SellStore {
+    DevBuf sl_ptr, sl_len, sl_row, sci, sv;
   };
+  struct CsrStore {
+    DevBuf rp, ci, v, longs;
+    SellStore sell[2];
+  };
+  void build_sell(const int32_t* rp, const int32_t* ci, const double* v,
+                  const std::vector<int32_t>& shorts, int sf, SellStore& st, CsrDev& out);
   void upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
-                  CsrStore& st, CsrDev& out);
+                  CsrStore& st, CsrDev& ser, CsrDev& tree);
+  const CsrDev& Km(bool serial) const { return serial ? Ks_ : Kt_; }
+  const CsrDev& KTm(bool serial) const { return serial ? KTs_ : KTt_; }
   void ensure_iter_buffers(int method, int cap);
   void upload_iterate(int slot, const double* x, const double* y);
   void kkt_eval(int slot, bool serial, double* kkt_dev_out, double* lam_dev);
@@ -104,7 +112,7 @@ class Problem {
   int64_t nnz_ = 0, N_ = 0;
   bool all_zero_ = true;
   bool bounds_ok_ = true;
-  CsrDev K_, KT_;
+  CsrDev Ks_, Kt_, KTs_, KTt_;  // SERIAL (sf = 1) and TREE layouts
   CsrStore k_store_, t_store_;
   size_t sell_bytes_ = 0;
   DevBuf c_, q_, l_, u_;

@@ -143,74 +143,88 @@ __device__ __forceinline__ bool skip_launch(const DevState* S, int pred_aa_ok,
 
 constexpr int kUnroll = 4;  // gathers in flight per lane (x 48 warps per SM)
 
-// Row sum of the row owned by (warp, lane) of this CTA; returns the row or
-// -1. SERIAL only matters for long rows: lane 0 adds in CSR order (bitwise)
-// instead of the fixed warp tree.
-template <bool SERIAL>
-__device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, int warp,
-                                       int lane, double& s) {
-  s = 0.0;
+// Visits every row this warp owns: f(row, sum) is called by the lane that
+// owns the row once its sum is complete.
+//  * CTAs [0, nblk_short): persistent over SELL slices (warp w takes slices
+//    w, w + W, ...; static, so per-lane partial sums stay deterministic).
+//    With split factor sf a row's elements go round-robin to sf lanes, which
+//    add their share in CSR order and meet in a fixed xor tree; sf = 1 (the
+//    SERIAL layout) keeps each row in one lane = reference order.
+//  * CTAs [nblk_short, grid): one long row per warp; SERIAL adds in CSR
+//    order through lane 0, TREE uses per-lane strided sums + xor tree.
+template <bool SERIAL, class F>
+__device__ __forceinline__ void for_rows(const CsrDev& A, const double* __restrict__ x, F&& f) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if ((int)blockIdx.x < A.nblk_short) {
-    const int sl = blockIdx.x * kWarps + warp;
-    if (sl >= A.nslices) return -1;
-    const int row = __ldg(A.sl_row + sl * 32 + lane);
-    const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
-    const int L = __ldg(A.sl_len + sl);
-    const int64_t base = __ldg(A.sl_ptr + sl) + lane;
-    double acc = 0.0;
-    for (int k0 = 0; k0 < L; k0 += kUnroll) {
-      int c[kUnroll];
-      double v[kUnroll];
+    const int sf = A.sf, j = lane & (sf - 1);
+    const int W = A.nblk_short * kWarps;
+    for (int sl = blockIdx.x * kWarps + warp; sl < A.nslices; sl += W) {
+      const int row = __ldg(A.sl_row + sl * 32 + lane);
+      const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
+      const int L = __ldg(A.sl_len + sl);
+      const int64_t base = __ldg(A.sl_ptr + sl) + lane;
+      double acc = 0.0;
+      for (int t0 = 0; t0 < L; t0 += kUnroll) {
+        int c[kUnroll];
+        double v[kUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        if (k0 + u < len) {
-          c[u] = __ldcs(A.sci + base + 32 * (k0 + u));
-          v[u] = __ldcs(A.sv + base + 32 * (k0 + u));
+        for (int u = 0; u < kUnroll; ++u) {
+          if ((t0 + u) * sf + j < len) {
+            c[u] = __ldcs(A.sci + base + 32 * (t0 + u));
+            v[u] = __ldcs(A.sv + base + 32 * (t0 + u));
+          }
         }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if ((t0 + u) * sf + j < len) v[u] = __dmul_rn(v[u], __ldg(x + c[u]));
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if ((t0 + u) * sf + j < len) acc = __dadd_rn(acc, v[u]);
       }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (k0 + u < len) v[u] = __dmul_rn(v[u], __ldg(x + c[u]));
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (k0 + u < len) acc = __dadd_rn(acc, v[u]);
+      for (int off = sf >> 1; off > 0; off >>= 1)
+        acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+      if (row >= 0 && j == 0) f(row, acc);
     }
-    s = acc;
-    return row;
+    return;
   }
   const int lr = (blockIdx.x - A.nblk_short) * kWarps + warp;
-  if (lr >= A.nlong) return -1;
+  if (lr >= A.nlong) return;
   const int row = __ldg(A.long_rows + lr);
   const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
   double acc = 0.0;
-  for (int64_t e = e0 + lane; e - lane < e1; e += 32) {
-    const double p = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
-    if (SERIAL) {  // CSR order through lane 0
-      const int64_t rem = e1 - (e - lane);
-      const int cnt = rem < 32 ? (int)rem : 32;
-      for (int j = 0; j < cnt; ++j) {
-        const double t = __shfl_sync(0xffffffffu, p, j);
+  if (SERIAL) {  // CSR order through lane 0
+    for (int64_t c0 = e0; c0 < e1; c0 += 32) {
+      const int64_t e = c0 + lane;
+      const double pr = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
+      const int cnt = (e1 - c0) < 32 ? (int)(e1 - c0) : 32;
+      for (int q = 0; q < cnt; ++q) {
+        const double t = __shfl_sync(0xffffffffu, pr, q);
         if (lane == 0) acc = __dadd_rn(acc, t);
       }
-    } else {
-      if (e < e1) acc = __dadd_rn(acc, p);
     }
+  } else {
+    for (int64_t c0 = e0 + lane; c0 < e1; c0 += 32 * kUnroll) {
+      double pr[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t e = c0 + 32 * u;
+        pr[u] = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) acc = __dadd_rn(acc, pr[u]);
+    }
+    acc = warp_sum(acc);
   }
-  if (!SERIAL) acc = warp_sum(acc);
-  s = acc;
-  return lane == 0 ? row : -1;
+  if (lane == 0) f(row, acc);
 }
 
 template <bool SERIAL>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_spmv(CsrDev A, VecRef xr, RowsumArgs o, const DevState* S) {
   if (skip_launch(S, o.pred_aa_ok, o.stop)) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* x = xr.get(S);
   double* out = o.out_pool ? o.out_pool + (int64_t)S->kx_idx[o.out_role] * o.out_stride : o.out;
-  double s;
-  const int row = row_sum<SERIAL>(A, x, warp, lane, s);
-  if (row >= 0) out[row] = s;
+  for_rows<SERIAL>(A, x, [&](int row, double s) { out[row] = s; });
 }
 
 // ---------------------------------------------------------------------------
@@ -242,17 +256,22 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
   __shared__ double red[P1_COUNT * kWarps];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-  double t;
-  const int j = row_sum<SERIAL>(KT, x + P->n, warp, lane, t);
+  double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+  const double* xp = B.upool + (int64_t)S->u_idx[U_PREV] * N;
+  const double* gp = PUSH ? B.gpool + (int64_t)S->g_idx[G_PREV] * N : nullptr;
+  double* gc = PUSH ? B.gpool + (int64_t)S->g_idx[G_CUR] * N : nullptr;
+  const int64_t slot = PUSH ? S->push_slot : 0;
+  double* du = PUSH ? B.du + slot * N : nullptr;
+  double* dg = PUSH ? B.dg + slot * N : nullptr;
+  const double tau = P->tau;
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
-  if (j >= 0) {
+  for_rows<SERIAL>(KT, x + P->n, [&](int j, double t) {
     const double xj = x[j], cj = __ldg(B.c + j), lj = __ldg(B.l + j), uj = __ldg(B.u + j);
-    double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));
+    double xn = __dsub_rn(xj, __dmul_rn(tau, __dsub_rn(cj, t)));
     xn = smin(smax(xn, lj), uj);
-    B.upool[(int64_t)S->u_idx[U_HAT] * N + j] = xn;
+    xh[j] = xn;
     const double d = __dsub_rn(xn, xj);
     const double red_c = __dsub_rn(cj, t);
     const double lam = project_lambda1(red_c, lj, uj);
@@ -260,20 +279,17 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
     if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
     const double dv = __dsub_rn(red_c, lam);
-    acc[P1_GX2] = __dmul_rn(d, d);
-    acc[P1_BOUND] = bt;
-    acc[P1_DUALSQ] = __dmul_rn(dv, dv);
-    acc[P1_CX] = __dmul_rn(cj, xj);
+    acc[P1_GX2] = __dadd_rn(acc[P1_GX2], __dmul_rn(d, d));
+    acc[P1_BOUND] = __dadd_rn(acc[P1_BOUND], bt);
+    acc[P1_DUALSQ] = __dadd_rn(acc[P1_DUALSQ], __dmul_rn(dv, dv));
+    acc[P1_CX] = __dadd_rn(acc[P1_CX], __dmul_rn(cj, xj));
     if constexpr (PUSH) {
-      const int64_t slot = S->push_slot;
-      const double xp = B.upool[(int64_t)S->u_idx[U_PREV] * N + j];
-      const double gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + j];
-      B.du[slot * N + j] = __dsub_rn(xj, xp);
-      B.dg[slot * N + j] = __dsub_rn(d, gp);
-      B.gpool[(int64_t)S->g_idx[G_CUR] * N + j] = d;
+      du[j] = __dsub_rn(xj, xp[j]);
+      dg[j] = __dsub_rn(d, gp[j]);
+      gc[j] = d;
     }
     if (SERIAL) B.T[j] = t;
-  }
+  });
   if (!SERIAL) {
     block_sum<P1_COUNT>(acc, red);
     if (threadIdx.x == 0)
@@ -397,36 +413,39 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   if (S->done) return;
   __shared__ double red[P2_COUNT * kWarps];
   __shared__ int is_last;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t N = P->N;
-  const int n = P->n, mr = P->mrows;
-  double s;
-  const int i = row_sum<SERIAL>(K, B.upool + (int64_t)S->u_idx[U_HAT] * N, warp, lane, s);
+  const int n = P->n, mr = P->mrows, m1 = P->m1;
+  const double* y = B.upool + (int64_t)S->u_idx[U_CUR] * N + n;
+  double* yh = B.upool + (int64_t)S->u_idx[U_HAT] * N + n;
+  const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
+  double* kxh = B.kxpool + (int64_t)S->kx_idx[KX_HAT] * mr;
+  const double* yp = B.upool + (int64_t)S->u_idx[U_PREV] * N + n;
+  const double* gp = PUSH ? B.gpool + (int64_t)S->g_idx[G_PREV] * N + n : nullptr;
+  double* gc = PUSH ? B.gpool + (int64_t)S->g_idx[G_CUR] * N + n : nullptr;
+  const int64_t slot = PUSH ? S->push_slot : 0;
+  double* du = PUSH ? B.du + slot * N + n : nullptr;
+  double* dg = PUSH ? B.dg + slot * N + n : nullptr;
+  const double sigma = P->sigma;
   double acc[P2_COUNT] = {0.0, 0.0, 0.0};
-  if (i >= 0) {
-    const double yi = B.upool[(int64_t)S->u_idx[U_CUR] * N + n + i];
-    const double qi = __ldg(B.q + i);
-    const double kxi = B.kxpool[(int64_t)S->kx_idx[KX_CUR] * mr + i];
+  for_rows<SERIAL>(K, B.upool + (int64_t)S->u_idx[U_HAT] * N, [&](int i, double s) {
+    const double yi = y[i], qi = __ldg(B.q + i), kxi = kx[i];
     double yn =
-        __dadd_rn(yi, __dmul_rn(P->sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
-    if (i < P->m1) yn = smax(yn, 0.0);
-    B.upool[(int64_t)S->u_idx[U_HAT] * N + n + i] = yn;
-    B.kxpool[(int64_t)S->kx_idx[KX_HAT] * mr + i] = s;
+        __dadd_rn(yi, __dmul_rn(sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
+    if (i < m1) yn = smax(yn, 0.0);
+    yh[i] = yn;
+    kxh[i] = s;
     const double d = __dsub_rn(yn, yi);
     double v = __dsub_rn(qi, kxi);
-    if (i < P->m1) v = smax(v, 0.0);
-    acc[P2_GY2] = __dmul_rn(d, d);
-    acc[P2_QY] = __dmul_rn(qi, yi);
-    acc[P2_INFEAS] = __dmul_rn(v, v);
+    if (i < m1) v = smax(v, 0.0);
+    acc[P2_GY2] = __dadd_rn(acc[P2_GY2], __dmul_rn(d, d));
+    acc[P2_QY] = __dadd_rn(acc[P2_QY], __dmul_rn(qi, yi));
+    acc[P2_INFEAS] = __dadd_rn(acc[P2_INFEAS], __dmul_rn(v, v));
     if constexpr (PUSH) {
-      const int64_t slot = S->push_slot;
-      const double yp = B.upool[(int64_t)S->u_idx[U_PREV] * N + n + i];
-      const double gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + n + i];
-      B.du[slot * N + n + i] = __dsub_rn(yi, yp);
-      B.dg[slot * N + n + i] = __dsub_rn(d, gp);
-      B.gpool[(int64_t)S->g_idx[G_CUR] * N + n + i] = d;
+      du[i] = __dsub_rn(yi, yp[i]);
+      dg[i] = __dsub_rn(d, gp[i]);
+      gc[i] = d;
     }
-  }
+  });
   if (SERIAL) return;
   block_sum<P2_COUNT>(acc, red);
   if (threadIdx.x == 0) {
