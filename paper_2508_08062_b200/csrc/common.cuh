@@ -66,7 +66,10 @@ struct CsrDev {
 };
 
 constexpr int kLongRow = 256;        // rows longer than this get a warp each
-constexpr int kSpmvBlocksPerSM = 5;  // register budget of the SpMV kernels (51 regs)
+constexpr int kSpmvWarps = 2;        // small CTAs: slices balance across SMs
+constexpr int kSpmvThreads = 32 * kSpmvWarps;
+constexpr int kSpmvBlocksPerSM = 20; // register budget (51 regs, 40 warps/SM)
+constexpr int kGroup = 64;           // CTAs per first-level partial group
 
 // Constant per solve (written before the loop starts).
 struct DevParams {
@@ -131,6 +134,25 @@ struct RowsumArgs {
   int64_t out_stride;
   int32_t pred_aa_ok;
   const int32_t* stop;
+};
+
+struct IterBufs {
+  double* upool;   // 4 x N
+  double* kxpool;  // 3 x m
+  double* gpool;   // 2 x N
+  double* du;      // cap x N
+  double* dg;      // cap x N
+  double* T;       // n
+  double* part1;   // P1_COUNT x nblk1 (per CTA)
+  double* part2;   // P2_COUNT x nblk2
+  double* gpart1;  // P1_COUNT x ceil(nblk1 / kGroup) (per group of CTAs)
+  double* gpart2;  // P2_COUNT x ceil(nblk2 / kGroup)
+  unsigned* tk1;   // group tickets (+1 top-level), self-resetting
+  unsigned* tk2;
+  const double* c;
+  const double* q;
+  const double* l;
+  const double* u;
 };
 
 struct CudaError : std::runtime_error {

@@ -129,8 +129,7 @@ void Problem::build_sell(const int32_t* rp, const int32_t* ci, const double* v,
   out.sci = st.sci.as<int32_t>();
   out.sv = st.sv.as<double>();
   out.sf = sf;
-  const int64_t want = (int64_t(nslices) + kWarps - 1) / kWarps;
-  out.nblk_short = int32_t(std::min<int64_t>(want, int64_t(num_sms_) * kSpmvBlocksPerSM));
+  out.nblk_short = (nslices + kSpmvWarps - 1) / kSpmvWarps;
 }
 
 // Uploads one CSR with its two sliced layouts: `ser` (sf = 1, CSR-ordered
@@ -168,7 +167,7 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
   base.v = st.v.as<double>();
   base.nlong = int32_t(longs.size());
   base.long_rows = st.longs.as<int32_t>();
-  base.nblk_long = (base.nlong + kWarps - 1) / kWarps;
+  base.nblk_long = (base.nlong + kSpmvWarps - 1) / kSpmvWarps;
   // split factor: enough slices for ~48 warps per SM, no more lanes than
   // a quarter of the mean row length
   const double mean = shorts.empty() ? 0.0 : double(short_nnz) / double(shorts.size());
@@ -194,8 +193,8 @@ int Problem::spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const Rowsum
   r.pred_aa_ok = pred;
   r.stop = stop;
   prof_begin(s, "k_spmv");
-  if (serial) k_spmv<true><<<A.grid(), kThreads, 0, s>>>(A, x, r, S);
-  else k_spmv<false><<<A.grid(), kThreads, 0, s>>>(A, x, r, S);
+  if (serial) k_spmv<true><<<A.grid(), kSpmvThreads, 0, s>>>(A, x, r, S);
+  else k_spmv<false><<<A.grid(), kSpmvThreads, 0, s>>>(A, x, r, S);
   prof_end(s);
   AAPDHG_CUDA(cudaGetLastError());
   return 1;
@@ -354,6 +353,10 @@ void Problem::ensure_iter_buffers(int method, int cap) {
   T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
   part1_.reserve(sizeof(double) * P1_COUNT * std::max(nblk1, 1));
   part2_.reserve(sizeof(double) * P2_COUNT * std::max(nblk2, 1));
+  const int ng1 = (nblk1 + kGroup - 1) / kGroup + 1, ng2 = (nblk2 + kGroup - 1) / kGroup + 1;
+  gpart1_.reserve(sizeof(double) * P1_COUNT * ng1);
+  gpart2_.reserve(sizeof(double) * P2_COUNT * ng2);
+  tk_.reserve(sizeof(unsigned) * (ng1 + ng2 + 2));
   gram_.reserve(sizeof(double) * kMaxMemory * kMaxMemory);
   work_.reserve(sizeof(double) * kMaxMemory * kMaxMemory);
   vec_.reserve(sizeof(double) * 8 * kMaxMemory);
@@ -369,6 +372,28 @@ void Problem::ensure_iter_buffers(int method, int cap) {
     const int items = num_items_host(cap, AAPDHG_METHOD_FAA);
     partdot_.reserve(sizeof(double) * size_t(items) * std::max(ndot_tile_, 1));
   }
+}
+
+IterBufs Problem::iter_bufs() {
+  IterBufs B{};
+  B.upool = upool_.as<double>();
+  B.kxpool = kxpool_.as<double>();
+  B.gpool = gpool_.as<double>();
+  B.du = du_.as<double>();
+  B.dg = dg_.as<double>();
+  B.T = T_.as<double>();
+  B.part1 = part1_.as<double>();
+  B.part2 = part2_.as<double>();
+  B.gpart1 = gpart1_.as<double>();
+  B.gpart2 = gpart2_.as<double>();
+  const int ng1 = (std::max(KTs_.grid(), KTt_.grid()) + kGroup - 1) / kGroup + 1;
+  B.tk1 = tk_.as<unsigned>();
+  B.tk2 = tk_.as<unsigned>() + ng1 + 1;
+  B.c = c_.as<double>();
+  B.q = q_.as<double>();
+  B.l = l_.as<double>();
+  B.u = u_.as<double>();
+  return B;
 }
 
 void Problem::upload_iterate(int slot, const double* x, const double* y) {
@@ -460,17 +485,17 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   const bool ser = su.serial, push = su.push;
   // K'y: products of K' with y = u_cur[n:], then the fused dual-side rows
   if (n_ > 0) {
-    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KTm(ser).grid(), kSpmvThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KTm(ser).grid(), kSpmvThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KTm(ser).grid(), kSpmvThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KTm(ser).grid(), kSpmvThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
   }
   // K xhat: products of K with xhat = u_hat[:n], then the fused dual step
   if (m_ > 0) {
-    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
-    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
-    else LAUNCH("k_primal_side", k_primal_side<false, false><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<Km(ser).grid(), kSpmvThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<Km(ser).grid(), kSpmvThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<Km(ser).grid(), kSpmvThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else LAUNCH("k_primal_side", k_primal_side<false, false><<<Km(ser).grid(), kSpmvThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
   }
   if (ser) LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
   AAPDHG_CUDA(cudaGetLastError());
@@ -720,10 +745,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   DevState* S = dstate_.as<DevState>();
 
   SolveSetup su;
-  su.B = IterBufs{upool_.as<double>(), kxpool_.as<double>(), gpool_.as<double>(),
-                  du_.as<double>(), dg_.as<double>(), T_.as<double>(), part1_.as<double>(),
-                  part2_.as<double>(), c_.as<double>(), q_.as<double>(),
-                  l_.as<double>(), u_.as<double>()};
+  su.B = iter_bufs();
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
                  partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
   su.W = SolveScratch{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
@@ -764,6 +786,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.cond_loop = cond_loop_;
 
   // start iterate P(u0) in slot 0, its K x cached in kx slot 0; fresh pools
+  AAPDHG_CUDA(cudaMemsetAsync(tk_.p, 0, tk_.bytes, stream_));
   AAPDHG_CUDA(cudaMemsetAsync(upool_.p, 0, sizeof(double) * 4 * N_, stream_));
   if (method != AAPDHG_METHOD_PDHG) {
     AAPDHG_CUDA(cudaMemsetAsync(gpool_.p, 0, sizeof(double) * 2 * N_, stream_));
@@ -898,16 +921,14 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   const DevState S = identity_state();
   h2d(dparams_.p, &P, sizeof P, stream_);
   h2d(dstate_.p, &S, sizeof S, stream_);
-  IterBufs B{upool_.as<double>(), kxpool_.as<double>(), nullptr, nullptr, nullptr,
-             T_.as<double>(), part1_.as<double>(), part2_.as<double>(),
-             c_.as<double>(), q_.as<double>(), l_.as<double>(), u_.as<double>()};
+  IterBufs B = iter_bufs();
   const DevParams* Pd = dparams_.as<DevParams>();
   DevState* Sd = dstate_.as<DevState>();
   if (n_) {
-    k_dual_side<true, false><<<KTs_.grid(), kThreads, 0, stream_>>>(KTs_, B, Pd, Sd);
+    k_dual_side<true, false><<<KTs_.grid(), kSpmvThreads, 0, stream_>>>(KTs_, B, Pd, Sd);
   }
   if (m_) {
-    k_primal_side<true, false><<<Ks_.grid(), kThreads, 0, stream_>>>(Ks_, B, Pd, Sd);
+    k_primal_side<true, false><<<Ks_.grid(), kSpmvThreads, 0, stream_>>>(Ks_, B, Pd, Sd);
   }
   AAPDHG_CUDA(cudaGetLastError());
   const double* hat = upool_.as<double>() + 2 * N_;
@@ -978,10 +999,7 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
   DotBufs D{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(), partdot_.as<double>(),
             num_items_host(std::max(p, 1), method)};
   SolveScratch W{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
-  IterBufs B{upool_.as<double>(), kxpool_.as<double>(), gpool_.as<double>(), du_.as<double>(),
-             dg_.as<double>(), T_.as<double>(), part1_.as<double>(), part2_.as<double>(),
-             c_.as<double>(), q_.as<double>(), l_.as<double>(),
-             u_.as<double>()};
+  IterBufs B = iter_bufs();
   const DevParams* Pd = dparams_.as<DevParams>();
   DevState* Sd = dstate_.as<DevState>();
   const int items = num_items_host(p, method);

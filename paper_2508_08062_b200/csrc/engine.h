@@ -82,6 +82,7 @@ class Problem {
   const CsrDev& KTm(bool serial) const { return serial ? KTs_ : KTt_; }
   void ensure_iter_buffers(int method, int cap);
   void upload_iterate(int slot, const double* x, const double* y);
+  IterBufs iter_bufs();
   void kkt_eval(int slot, bool serial, double* kkt_dev_out, double* lam_dev);
   int launch_core(cudaStream_t s, const SolveSetup& su);
   int launch_aa(cudaStream_t s, const SolveSetup& su);
@@ -120,7 +121,8 @@ class Problem {
 
   // iteration buffers
   int buf_method_ = -1, buf_cap_ = 0;
-  DevBuf upool_, kxpool_, gpool_, du_, dg_, T_, part1_, part2_, partdot_, gram_, work_, vec_;
+  DevBuf upool_, kxpool_, gpool_, du_, dg_, T_, part1_, part2_, gpart1_, gpart2_, tk_, partdot_,
+      gram_, work_, vec_;
   DevBuf rec_, pow_tab_, dparams_, dstate_, dhat_, scal_, part_small_, lam_, pw_x_, pw_mx_,
       pw_mtmx_, pw_state_;
   int ndot_tile_ = 0;

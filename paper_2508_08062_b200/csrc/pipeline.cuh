@@ -46,21 +46,21 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // Fixed-shape block sum (warp xor tree, then warps in order); result valid in
 // thread 0. Deterministic: the association never depends on timing.
-template <int NV>
+template <int NV, int WARPS = kWarps>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* red) {
 #pragma unroll
   for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0)
 #pragma unroll
-    for (int q = 0; q < NV; ++q) red[q * kWarps + warp] = v[q];
+    for (int q = 0; q < NV; ++q) red[q * WARPS + warp] = v[q];
   __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
-      double s = red[q * kWarps];
+      double s = red[q * WARPS];
 #pragma unroll
-      for (int w = 1; w < kWarps; ++w) s += red[q * kWarps + w];
+      for (int w = 1; w < WARPS; ++w) s += red[q * WARPS + w];
       v[q] = s;
     }
   }
@@ -145,9 +145,8 @@ constexpr int kUnroll = 4;  // gathers in flight per lane (x 48 warps per SM)
 
 // Visits every row this warp owns: f(row, sum) is called by the lane that
 // owns the row once its sum is complete.
-//  * CTAs [0, nblk_short): persistent over SELL slices (warp w takes slices
-//    w, w + W, ...; static, so per-lane partial sums stay deterministic).
-//    With split factor sf a row's elements go round-robin to sf lanes, which
+//  * CTAs [0, nblk_short): one SELL slice per warp (small CTAs: the block
+//    scheduler balances the load). With split factor sf a row's elements go round-robin to sf lanes, which
 //    add their share in CSR order and meet in a fixed xor tree; sf = 1 (the
 //    SERIAL layout) keeps each row in one lane = reference order.
 //  * CTAs [nblk_short, grid): one long row per warp; SERIAL adds in CSR
@@ -157,8 +156,9 @@ __device__ __forceinline__ void for_rows(const CsrDev& A, const double* __restri
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if ((int)blockIdx.x < A.nblk_short) {
     const int sf = A.sf, j = lane & (sf - 1);
-    const int W = A.nblk_short * kWarps;
-    for (int sl = blockIdx.x * kWarps + warp; sl < A.nslices; sl += W) {
+    {
+      const int sl = blockIdx.x * kSpmvWarps + warp;
+      if (sl >= A.nslices) return;
       const int row = __ldg(A.sl_row + sl * 32 + lane);
       const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
       const int L = __ldg(A.sl_len + sl);
@@ -187,7 +187,7 @@ __device__ __forceinline__ void for_rows(const CsrDev& A, const double* __restri
     }
     return;
   }
-  const int lr = (blockIdx.x - A.nblk_short) * kWarps + warp;
+  const int lr = (blockIdx.x - A.nblk_short) * kSpmvWarps + warp;
   if (lr >= A.nlong) return;
   const int row = __ldg(A.long_rows + lr);
   const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
@@ -219,7 +219,7 @@ __device__ __forceinline__ void for_rows(const CsrDev& A, const double* __restri
 }
 
 template <bool SERIAL>
-__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSM)
     k_spmv(CsrDev A, VecRef xr, RowsumArgs o, const DevState* S) {
   if (skip_launch(S, o.pred_aa_ok, o.stop)) return;
   const double* x = xr.get(S);
@@ -231,20 +231,48 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 // the fused PDHG halves
 // ---------------------------------------------------------------------------
 
-struct IterBufs {
-  double* upool;   // 4 x N
-  double* kxpool;  // 3 x m
-  double* gpool;   // 2 x N
-  double* du;      // cap x N
-  double* dg;      // cap x N
-  double* T;       // n
-  double* part1;   // P1_COUNT x nblk1
-  double* part2;   // P2_COUNT x nblk2
-  const double* c;
-  const double* q;
-  const double* l;
-  const double* u;
-};
+
+// Deterministic two-level reduction of per-CTA partials without a second
+// launch: thread 0 holds the CTA's NV values; they go to part[q * nb + b];
+// the last CTA to finish in each group of kGroup consecutive CTAs adds its
+// group in a fixed tree into gpart[q * ng + g]; returns true in the CTA that
+// completes the last group (then all of gpart is valid). Tickets reset
+// themselves, so the kernel can be replayed.
+template <int NV>
+__device__ __forceinline__ bool group_reduce(const double (&v)[NV], double* part, double* gpart,
+                                             unsigned* tk, int nb, double* red) {
+  __shared__ int flag;
+  const int b = blockIdx.x, g = b / kGroup, ng = (nb + kGroup - 1) / kGroup;
+  const int gsz = min(kGroup, nb - g * kGroup);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) part[q * nb + b] = v[q];
+    __threadfence();
+    flag = atomicAdd(&tk[g], 1u) == unsigned(gsz - 1);
+  }
+  __syncthreads();
+  if (!flag) return false;
+  __threadfence();
+  double w[NV];
+  for (int q = 0; q < NV; ++q) {
+    double s = 0.0;
+    for (int t = threadIdx.x; t < gsz; t += blockDim.x) s = __dadd_rn(s, __ldcg(part + q * nb + g * kGroup + t));
+    w[q] = s;
+  }
+  block_sum<NV, kSpmvWarps>(w, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) gpart[q * ng + g] = w[q];
+    tk[g] = 0;
+    __threadfence();
+    flag = atomicAdd(&tk[ng], 1u) == unsigned(ng - 1);
+  }
+  __syncthreads();
+  if (!flag) return false;
+  __threadfence();
+  if (threadIdx.x == 0) tk[ng] = 0;
+  return true;
+}
 
 // K1 on K' (row j of K' = column j of K), t = (K'y)_j:
 //   xhat_j = min(max(x_j - tau (c_j - t), l_j), u_j)      pdhg_core.cpp:49-53
@@ -252,10 +280,10 @@ struct IterBufs {
 //   partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
 //   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSM)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
-  __shared__ double red[P1_COUNT * kWarps];
+  __shared__ double red[P1_COUNT * kSpmvWarps];
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
   double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
@@ -291,10 +319,8 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     if (SERIAL) B.T[j] = t;
   });
   if (!SERIAL) {
-    block_sum<P1_COUNT>(acc, red);
-    if (threadIdx.x == 0)
-#pragma unroll
-      for (int q = 0; q < P1_COUNT; ++q) B.part1[q * P->nblk1 + blockIdx.x] = acc[q];
+    block_sum<P1_COUNT, kSpmvWarps>(acc, red);
+    group_reduce<P1_COUNT>(acc, B.part1, B.gpart1, B.tk1, P->nblk1, red);
   }
 }
 
@@ -368,27 +394,24 @@ __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, doub
                                            double bound, double qy, double cx, double infeas,
                                            double dual_sq);
 
-// TREE mode: reduce all partials of K1/K2 and run the control (one CTA).
-// One pass: each thread keeps the 7 strided sums, then one fixed block tree.
+// TREE mode: add the group sums of K1/K2 (fixed order) and run the control.
 __device__ __forceinline__ void control_from_partials(const IterBufs& B, const DevParams* P,
                                                       DevState* S) {
-  __shared__ double red7[7 * kWarps];
-  const int nb1 = P->nblk1, nb2 = P->nblk2;
+  __shared__ double red7[7 * kSpmvWarps];
+  const int ng1 = (P->nblk1 + kGroup - 1) / kGroup, ng2 = (P->nblk2 + kGroup - 1) / kGroup;
   double v[7] = {0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 4
-  for (int b = threadIdx.x; b < nb1; b += blockDim.x) {
-    v[0] = __dadd_rn(v[0], __ldcg(B.part1 + P1_GX2 * nb1 + b));
-    v[1] = __dadd_rn(v[1], __ldcg(B.part1 + P1_BOUND * nb1 + b));
-    v[2] = __dadd_rn(v[2], __ldcg(B.part1 + P1_CX * nb1 + b));
-    v[3] = __dadd_rn(v[3], __ldcg(B.part1 + P1_DUALSQ * nb1 + b));
+  for (int b = threadIdx.x; b < ng1; b += blockDim.x) {
+    v[0] = __dadd_rn(v[0], __ldcg(B.gpart1 + P1_GX2 * ng1 + b));
+    v[1] = __dadd_rn(v[1], __ldcg(B.gpart1 + P1_BOUND * ng1 + b));
+    v[2] = __dadd_rn(v[2], __ldcg(B.gpart1 + P1_CX * ng1 + b));
+    v[3] = __dadd_rn(v[3], __ldcg(B.gpart1 + P1_DUALSQ * ng1 + b));
   }
-#pragma unroll 4
-  for (int b = threadIdx.x; b < nb2; b += blockDim.x) {
-    v[4] = __dadd_rn(v[4], __ldcg(B.part2 + P2_GY2 * nb2 + b));
-    v[5] = __dadd_rn(v[5], __ldcg(B.part2 + P2_QY * nb2 + b));
-    v[6] = __dadd_rn(v[6], __ldcg(B.part2 + P2_INFEAS * nb2 + b));
+  for (int b = threadIdx.x; b < ng2; b += blockDim.x) {
+    v[4] = __dadd_rn(v[4], __ldcg(B.gpart2 + P2_GY2 * ng2 + b));
+    v[5] = __dadd_rn(v[5], __ldcg(B.gpart2 + P2_QY * ng2 + b));
+    v[6] = __dadd_rn(v[6], __ldcg(B.gpart2 + P2_INFEAS * ng2 + b));
   }
-  block_sum<7>(v, red7);
+  block_sum<7, kSpmvWarps>(v, red7);
   const double gx2 = v[0], bound = v[1], cx = v[2], dsq = v[3], gy2 = v[4], qy = v[5], inf = v[6];
   __shared__ DevState sm;
   __shared__ DevParams sp;
@@ -396,7 +419,6 @@ __device__ __forceinline__ void control_from_partials(const IterBufs& B, const D
   state_load(&sm, S);
   if (threadIdx.x == 0) {
     control_logic(&sp, &sm, __dadd_rn(gx2, gy2), bound, qy, cx, inf, dsq);
-    sm.ticket = 0;
   }
   state_store(S, &sm);
 }
@@ -408,11 +430,10 @@ __device__ __forceinline__ void control_from_partials(const IterBufs& B, const D
 //   partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
 // TREE: the last CTA to finish reduces every partial and runs the control.
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSM)
     k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
-  __shared__ double red[P2_COUNT * kWarps];
-  __shared__ int is_last;
+  __shared__ double red[P2_COUNT * kSpmvWarps];
   const int64_t N = P->N;
   const int n = P->n, mr = P->mrows, m1 = P->m1;
   const double* y = B.upool + (int64_t)S->u_idx[U_CUR] * N + n;
@@ -447,18 +468,9 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     }
   });
   if (SERIAL) return;
-  block_sum<P2_COUNT>(acc, red);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q < P2_COUNT; ++q) B.part2[q * P->nblk2 + blockIdx.x] = acc[q];
-    // the last CTA to finish reduces all partials and runs the control
-    __threadfence();
-    const unsigned tk = atomicAdd(&S->ticket, 1u);
-    is_last = (tk == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
+  block_sum<P2_COUNT, kSpmvWarps>(acc, red);
+  // the CTA completing the last group adds the group sums and runs the control
+  if (!group_reduce<P2_COUNT>(acc, B.part2, B.gpart2, B.tk2, P->nblk2, red)) return;
   control_from_partials(B, P, S);
 }
 
