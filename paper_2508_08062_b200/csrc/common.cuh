@@ -62,13 +62,13 @@ struct CsrDev {
   const int32_t* long_rows = nullptr;
   int32_t nblk_short = 0, nblk_long = 0;
   int32_t sf = 1;  // lanes per row in the slices (1 = CSR-ordered row sums)
+  int32_t warps = 8;  // warps per CTA of the kernels streaming this layout
   int32_t grid() const { return nblk_short + nblk_long; }
+  int32_t threads() const { return 32 * warps; }
 };
 
 constexpr int kLongRow = 256;        // rows longer than this get a warp each
-constexpr int kSpmvWarps = 2;        // small CTAs: slices balance across SMs
-constexpr int kSpmvThreads = 32 * kSpmvWarps;
-constexpr int kSpmvBlocksPerSM = 20; // register budget (51 regs, 40 warps/SM)
+
 constexpr int kGroup = 64;           // CTAs per first-level partial group
 
 // Constant per solve (written before the loop starts).

@@ -32,6 +32,12 @@ constexpr uint64_t kRecCap = 1 << 16;  // device record ring
 constexpr uint64_t kPowTabMax = 1 << 22;
 constexpr int kPowerBatch = 8;
 
+// tuning overrides (experiments): AAPDHG_SF, AAPDHG_SPMV_WARPS
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
 int num_items_host(int p, int method) {
   return p * (p + 1) / 2 + p + (method == AAPDHG_METHOD_FAA ? p : 0);
 }
@@ -129,7 +135,7 @@ void Problem::build_sell(const int32_t* rp, const int32_t* ci, const double* v,
   out.sci = st.sci.as<int32_t>();
   out.sv = st.sv.as<double>();
   out.sf = sf;
-  out.nblk_short = (nslices + kSpmvWarps - 1) / kSpmvWarps;
+  out.nblk_short = (nslices + out.warps - 1) / out.warps;
 }
 
 // Uploads one CSR with its two sliced layouts: `ser` (sf = 1, CSR-ordered
@@ -167,7 +173,8 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
   base.v = st.v.as<double>();
   base.nlong = int32_t(longs.size());
   base.long_rows = st.longs.as<int32_t>();
-  base.nblk_long = (base.nlong + kSpmvWarps - 1) / kSpmvWarps;
+  base.warps = env_int("AAPDHG_SPMV_WARPS", 8);
+  base.nblk_long = (base.nlong + base.warps - 1) / base.warps;
   // split factor: enough slices for ~48 warps per SM, no more lanes than
   // a quarter of the mean row length
   const double mean = shorts.empty() ? 0.0 : double(short_nnz) / double(shorts.size());
@@ -175,6 +182,7 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
   while (sf < 8 && double(shorts.size()) * sf / 32.0 < double(num_sms_) * 48.0 &&
          mean >= 4.0 * (2 * sf))
     sf *= 2;
+  sf = env_int("AAPDHG_SF", sf);
   ser = base;
   build_sell(rp, ci, v, shorts, 1, st.sell[0], ser);
   tree = base;
@@ -193,8 +201,8 @@ int Problem::spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const Rowsum
   r.pred_aa_ok = pred;
   r.stop = stop;
   prof_begin(s, "k_spmv");
-  if (serial) k_spmv<true><<<A.grid(), kSpmvThreads, 0, s>>>(A, x, r, S);
-  else k_spmv<false><<<A.grid(), kSpmvThreads, 0, s>>>(A, x, r, S);
+  if (serial) k_spmv<true><<<A.grid(), A.threads(), 0, s>>>(A, x, r, S);
+  else k_spmv<false><<<A.grid(), A.threads(), 0, s>>>(A, x, r, S);
   prof_end(s);
   AAPDHG_CUDA(cudaGetLastError());
   return 1;
@@ -485,17 +493,17 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   const bool ser = su.serial, push = su.push;
   // K'y: products of K' with y = u_cur[n:], then the fused dual-side rows
   if (n_ > 0) {
-    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KTm(ser).grid(), kSpmvThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KTm(ser).grid(), kSpmvThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KTm(ser).grid(), kSpmvThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KTm(ser).grid(), kSpmvThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KTm(ser).grid(), KTm(ser).threads(), 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KTm(ser).grid(), KTm(ser).threads(), 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KTm(ser).grid(), KTm(ser).threads(), 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KTm(ser).grid(), KTm(ser).threads(), 0, s>>>(KTm(ser), su.B, su.P, su.S));
   }
   // K xhat: products of K with xhat = u_hat[:n], then the fused dual step
   if (m_ > 0) {
-    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<Km(ser).grid(), kSpmvThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<Km(ser).grid(), kSpmvThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
-    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<Km(ser).grid(), kSpmvThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
-    else LAUNCH("k_primal_side", k_primal_side<false, false><<<Km(ser).grid(), kSpmvThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<Km(ser).grid(), Km(ser).threads(), 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<Km(ser).grid(), Km(ser).threads(), 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<Km(ser).grid(), Km(ser).threads(), 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else LAUNCH("k_primal_side", k_primal_side<false, false><<<Km(ser).grid(), Km(ser).threads(), 0, s>>>(Km(ser), su.B, su.P, su.S));
   }
   if (ser) LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
   AAPDHG_CUDA(cudaGetLastError());
@@ -925,10 +933,10 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   const DevParams* Pd = dparams_.as<DevParams>();
   DevState* Sd = dstate_.as<DevState>();
   if (n_) {
-    k_dual_side<true, false><<<KTs_.grid(), kSpmvThreads, 0, stream_>>>(KTs_, B, Pd, Sd);
+    k_dual_side<true, false><<<KTs_.grid(), KTs_.threads(), 0, stream_>>>(KTs_, B, Pd, Sd);
   }
   if (m_) {
-    k_primal_side<true, false><<<Ks_.grid(), kSpmvThreads, 0, stream_>>>(Ks_, B, Pd, Sd);
+    k_primal_side<true, false><<<Ks_.grid(), Ks_.threads(), 0, stream_>>>(Ks_, B, Pd, Sd);
   }
   AAPDHG_CUDA(cudaGetLastError());
   const double* hat = upool_.as<double>() + 2 * N_;

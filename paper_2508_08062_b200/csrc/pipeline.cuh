@@ -46,21 +46,21 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // Fixed-shape block sum (warp xor tree, then warps in order); result valid in
 // thread 0. Deterministic: the association never depends on timing.
-template <int NV, int WARPS = kWarps>
+// red must hold NV * kWarps doubles; any blockDim multiple of 32 <= 256.
+template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* red) {
 #pragma unroll
   for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   if (lane == 0)
 #pragma unroll
-    for (int q = 0; q < NV; ++q) red[q * WARPS + warp] = v[q];
+    for (int q = 0; q < NV; ++q) red[q * kWarps + warp] = v[q];
   __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
-      double s = red[q * WARPS];
-#pragma unroll
-      for (int w = 1; w < WARPS; ++w) s += red[q * WARPS + w];
+      double s = red[q * kWarps];
+      for (int w = 1; w < nw; ++w) s += red[q * kWarps + w];
       v[q] = s;
     }
   }
@@ -157,7 +157,7 @@ __device__ __forceinline__ void for_rows(const CsrDev& A, const double* __restri
   if ((int)blockIdx.x < A.nblk_short) {
     const int sf = A.sf, j = lane & (sf - 1);
     {
-      const int sl = blockIdx.x * kSpmvWarps + warp;
+      const int sl = blockIdx.x * (blockDim.x >> 5) + warp;
       if (sl >= A.nslices) return;
       const int row = __ldg(A.sl_row + sl * 32 + lane);
       const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
@@ -187,7 +187,7 @@ __device__ __forceinline__ void for_rows(const CsrDev& A, const double* __restri
     }
     return;
   }
-  const int lr = (blockIdx.x - A.nblk_short) * kSpmvWarps + warp;
+  const int lr = (blockIdx.x - A.nblk_short) * (blockDim.x >> 5) + warp;
   if (lr >= A.nlong) return;
   const int row = __ldg(A.long_rows + lr);
   const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
@@ -219,7 +219,7 @@ __device__ __forceinline__ void for_rows(const CsrDev& A, const double* __restri
 }
 
 template <bool SERIAL>
-__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSM)
+__global__ void __launch_bounds__(kThreads, 5)
     k_spmv(CsrDev A, VecRef xr, RowsumArgs o, const DevState* S) {
   if (skip_launch(S, o.pred_aa_ok, o.stop)) return;
   const double* x = xr.get(S);
@@ -259,7 +259,7 @@ __device__ __forceinline__ bool group_reduce(const double (&v)[NV], double* part
     for (int t = threadIdx.x; t < gsz; t += blockDim.x) s = __dadd_rn(s, __ldcg(part + q * nb + g * kGroup + t));
     w[q] = s;
   }
-  block_sum<NV, kSpmvWarps>(w, red);
+  block_sum<NV>(w, red);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int q = 0; q < NV; ++q) gpart[q * ng + g] = w[q];
@@ -280,10 +280,10 @@ __device__ __forceinline__ bool group_reduce(const double (&v)[NV], double* part
 //   partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
 //   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSM)
+__global__ void __launch_bounds__(kThreads, 5)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
-  __shared__ double red[P1_COUNT * kSpmvWarps];
+  __shared__ double red[P1_COUNT * kWarps];
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
   double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSM)
     if (SERIAL) B.T[j] = t;
   });
   if (!SERIAL) {
-    block_sum<P1_COUNT, kSpmvWarps>(acc, red);
+    block_sum<P1_COUNT>(acc, red);
     group_reduce<P1_COUNT>(acc, B.part1, B.gpart1, B.tk1, P->nblk1, red);
   }
 }
@@ -397,7 +397,7 @@ __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, doub
 // TREE mode: add the group sums of K1/K2 (fixed order) and run the control.
 __device__ __forceinline__ void control_from_partials(const IterBufs& B, const DevParams* P,
                                                       DevState* S) {
-  __shared__ double red7[7 * kSpmvWarps];
+  __shared__ double red7[7 * kWarps];
   const int ng1 = (P->nblk1 + kGroup - 1) / kGroup, ng2 = (P->nblk2 + kGroup - 1) / kGroup;
   double v[7] = {0, 0, 0, 0, 0, 0, 0};
   for (int b = threadIdx.x; b < ng1; b += blockDim.x) {
@@ -411,7 +411,7 @@ __device__ __forceinline__ void control_from_partials(const IterBufs& B, const D
     v[5] = __dadd_rn(v[5], __ldcg(B.gpart2 + P2_QY * ng2 + b));
     v[6] = __dadd_rn(v[6], __ldcg(B.gpart2 + P2_INFEAS * ng2 + b));
   }
-  block_sum<7, kSpmvWarps>(v, red7);
+  block_sum<7>(v, red7);
   const double gx2 = v[0], bound = v[1], cx = v[2], dsq = v[3], gy2 = v[4], qy = v[5], inf = v[6];
   __shared__ DevState sm;
   __shared__ DevParams sp;
@@ -430,10 +430,10 @@ __device__ __forceinline__ void control_from_partials(const IterBufs& B, const D
 //   partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
 // TREE: the last CTA to finish reduces every partial and runs the control.
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSM)
+__global__ void __launch_bounds__(kThreads, 5)
     k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
-  __shared__ double red[P2_COUNT * kSpmvWarps];
+  __shared__ double red[P2_COUNT * kWarps];
   const int64_t N = P->N;
   const int n = P->n, mr = P->mrows, m1 = P->m1;
   const double* y = B.upool + (int64_t)S->u_idx[U_CUR] * N + n;
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSM)
     }
   });
   if (SERIAL) return;
-  block_sum<P2_COUNT, kSpmvWarps>(acc, red);
+  block_sum<P2_COUNT>(acc, red);
   // the CTA completing the last group adds the group sums and runs the control
   if (!group_reduce<P2_COUNT>(acc, B.part2, B.gpart2, B.tk2, P->nblk2, red)) return;
   control_from_partials(B, P, S);
