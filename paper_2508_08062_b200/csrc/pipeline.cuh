@@ -161,25 +161,28 @@ __device__ __forceinline__ void for_rows(const CsrDev& A, const double* __restri
       if (sl >= A.nslices) return;
       const int row = __ldg(A.sl_row + sl * 32 + lane);
       const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
+      const int cnt = (len - j + sf - 1) / sf;  // this lane's elements
       const int L = __ldg(A.sl_len + sl);
       const int64_t base = __ldg(A.sl_ptr + sl) + lane;
+      const int32_t* __restrict__ cp = A.sci + base;
+      const double* __restrict__ vp = A.sv + base;
       double acc = 0.0;
       for (int t0 = 0; t0 < L; t0 += kUnroll) {
+        // all loads of the group first: kUnroll gathers in flight per lane
         int c[kUnroll];
         double v[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-          if ((t0 + u) * sf + j < len) {
-            c[u] = __ldcs(A.sci + base + 32 * (t0 + u));
-            v[u] = __ldcs(A.sv + base + 32 * (t0 + u));
-          }
+          const bool on = t0 + u < cnt;
+          c[u] = on ? __ldcs(cp + 32 * (t0 + u)) : 0;
+          v[u] = on ? __ldcs(vp + 32 * (t0 + u)) : 0.0;
         }
+        double g[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) g[u] = t0 + u < cnt ? __ldg(x + c[u]) : 0.0;
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
-          if ((t0 + u) * sf + j < len) v[u] = __dmul_rn(v[u], __ldg(x + c[u]));
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-          if ((t0 + u) * sf + j < len) acc = __dadd_rn(acc, v[u]);
+          if (t0 + u < cnt) acc = __dadd_rn(acc, __dmul_rn(v[u], g[u]));
       }
       for (int off = sf >> 1; off > 0; off >>= 1)
         acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
