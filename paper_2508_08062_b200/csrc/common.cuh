@@ -46,7 +46,7 @@ enum { S_G2 = 0, S_BOUND = 1, S_QY = 2, S_CX = 3, S_INFEAS = 4, S_DUALSQ = 5, S_
 //                  sl_ptr[s] + 32 k + r of sci/sv; sl_row[32 s + r] = row
 //                  (-1 = empty lane), sl_len[s] = longest row of the slice
 //   long rows      row ids, one warp each
-// Launch grid = nblk_short CTAs of slices + nblk_long CTAs of long rows.
+// Work units = slices then long rows, pulled by persistent warps.
 struct CsrDev {
   int32_t nrows = 0, ncols = 0;
   int64_t nnz = 0;
@@ -60,14 +60,15 @@ struct CsrDev {
   const int32_t* sci = nullptr;
   const double* sv = nullptr;
   const int32_t* long_rows = nullptr;
-  int32_t nblk_short = 0, nblk_long = 0;
-  int32_t sf = 1;  // lanes per row in the slices (1 = CSR-ordered row sums)
-  int32_t warps = 8;  // warps per CTA of the kernels streaming this layout
-  int32_t grid() const { return nblk_short + nblk_long; }
-  int32_t threads() const { return 32 * warps; }
+  int32_t nblocks = 0;  // persistent grid of the kernels streaming this matrix
+  int32_t grid() const { return nblocks; }
+  int32_t units() const { return nslices + nlong; }
 };
 
 constexpr int kLongRow = 256;        // rows longer than this get a warp each
+constexpr int kUnitWarps = 4;        // warps per CTA of the SpMV kernels
+constexpr int kUnitThreads = 32 * kUnitWarps;
+constexpr int kUnitBlocksPerSM = 10; // 40 warps/SM: 51 registers, ~200 KB of rings
 
 constexpr int kGroup = 64;           // CTAs per first-level partial group
 
@@ -145,14 +146,19 @@ struct IterBufs {
   double* T;       // n
   double* part1;   // P1_COUNT x nblk1 (per CTA)
   double* part2;   // P2_COUNT x nblk2
-  double* gpart1;  // P1_COUNT x ceil(nblk1 / kGroup) (per group of CTAs)
-  double* gpart2;  // P2_COUNT x ceil(nblk2 / kGroup)
-  unsigned* tk1;   // group tickets (+1 top-level), self-resetting
-  unsigned* tk2;
   const double* c;
   const double* q;
   const double* l;
   const double* u;
+};
+
+// Unit-level scheduling state of one launch site (self-resetting).
+struct Sched {
+  unsigned* next;   // unit counter
+  unsigned* done;   // warps that found no more work
+  unsigned* tk;     // group tickets [ngroups] + top-level ticket
+  double* part;     // NV x nunits per-unit partials
+  double* gpart;    // NV x ngroups group sums
 };
 
 struct CudaError : std::runtime_error {

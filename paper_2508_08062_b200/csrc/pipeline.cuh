@@ -113,220 +113,6 @@ __device__ __forceinline__ double serial_dot(const double* __restrict__ a,
   return s;
 }
 
-// ---------------------------------------------------------------------------
-// SpMV core: SELL-32 slices of the short rows + warp-per-row long rows
-// ---------------------------------------------------------------------------
-//
-// Random-column SpMVs on B200 are bound by the L1TEX gather rate (~0.85
-// cycles per random 8-byte gather per SM when ~400+ gathers are in flight
-// per SM; measured, profiles/microbench/gather_bench.cu). The matrix is
-// therefore stored (once, on upload) in a sliced layout: consecutive short
-// rows are grouped 32 to a slice and element k of the slice's lane-r row
-// sits at sl_ptr[s] + 32 k + r. A warp owns a slice: its (col, val) loads
-// are coalesced, each lane keeps 8 gathers x[col] in flight and adds its
-// row's products sequentially in CSR order — bit-identical to the
-// reference's row-serial matvec (sparse_linalg.cpp:60-69) and, on the
-// transposed CSR (entries in ascending original row), to its row-ordered
-// scatter matvec_transpose (sparse_linalg.cpp:77-87). No shared memory, no
-// barrier, no product buffer. Rows longer than kLongRow are handled one per
-// warp by extra CTAs of the same launch (grid = short blocks + long blocks).
-
-// Plain SpMV output / input references (power iteration, recache, matvec).
-__device__ __forceinline__ bool skip_launch(const DevState* S, int pred_aa_ok,
-                                            const int32_t* stop) {
-  if (S) {
-    if (S->done) return true;
-    if (pred_aa_ok && !S->aa_ok) return true;
-  }
-  return stop && *stop;
-}
-
-constexpr int kUnroll = 4;  // gathers in flight per lane (x 48 warps per SM)
-
-// Visits every row this warp owns: f(row, sum) is called by the lane that
-// owns the row once its sum is complete.
-//  * CTAs [0, nblk_short): one SELL slice per warp (small CTAs: the block
-//    scheduler balances the load). With split factor sf a row's elements go round-robin to sf lanes, which
-//    add their share in CSR order and meet in a fixed xor tree; sf = 1 (the
-//    SERIAL layout) keeps each row in one lane = reference order.
-//  * CTAs [nblk_short, grid): one long row per warp; SERIAL adds in CSR
-//    order through lane 0, TREE uses per-lane strided sums + xor tree.
-template <bool SERIAL, class F>
-__device__ __forceinline__ void for_rows(const CsrDev& A, const double* __restrict__ x, F&& f) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if ((int)blockIdx.x < A.nblk_short) {
-    const int sf = A.sf, j = lane & (sf - 1);
-    {
-      const int sl = blockIdx.x * (blockDim.x >> 5) + warp;
-      if (sl >= A.nslices) return;
-      const int row = __ldg(A.sl_row + sl * 32 + lane);
-      const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
-      const int cnt = (len - j + sf - 1) / sf;  // this lane's elements
-      const int L = __ldg(A.sl_len + sl);
-      const int64_t base = __ldg(A.sl_ptr + sl) + lane;
-      const int32_t* __restrict__ cp = A.sci + base;
-      const double* __restrict__ vp = A.sv + base;
-      double acc = 0.0;
-      for (int t0 = 0; t0 < L; t0 += kUnroll) {
-        // all loads of the group first: kUnroll gathers in flight per lane
-        int c[kUnroll];
-        double v[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const bool on = t0 + u < cnt;
-          c[u] = on ? __ldcs(cp + 32 * (t0 + u)) : 0;
-          v[u] = on ? __ldcs(vp + 32 * (t0 + u)) : 0.0;
-        }
-        double g[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) g[u] = t0 + u < cnt ? __ldg(x + c[u]) : 0.0;
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-          if (t0 + u < cnt) acc = __dadd_rn(acc, __dmul_rn(v[u], g[u]));
-      }
-      for (int off = sf >> 1; off > 0; off >>= 1)
-        acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
-      if (row >= 0 && j == 0) f(row, acc);
-    }
-    return;
-  }
-  const int lr = (blockIdx.x - A.nblk_short) * (blockDim.x >> 5) + warp;
-  if (lr >= A.nlong) return;
-  const int row = __ldg(A.long_rows + lr);
-  const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
-  double acc = 0.0;
-  if (SERIAL) {  // CSR order through lane 0
-    for (int64_t c0 = e0; c0 < e1; c0 += 32) {
-      const int64_t e = c0 + lane;
-      const double pr = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
-      const int cnt = (e1 - c0) < 32 ? (int)(e1 - c0) : 32;
-      for (int q = 0; q < cnt; ++q) {
-        const double t = __shfl_sync(0xffffffffu, pr, q);
-        if (lane == 0) acc = __dadd_rn(acc, t);
-      }
-    }
-  } else {
-    for (int64_t c0 = e0 + lane; c0 < e1; c0 += 32 * kUnroll) {
-      double pr[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t e = c0 + 32 * u;
-        pr[u] = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) acc = __dadd_rn(acc, pr[u]);
-    }
-    acc = warp_sum(acc);
-  }
-  if (lane == 0) f(row, acc);
-}
-
-template <bool SERIAL>
-__global__ void __launch_bounds__(kThreads, 5)
-    k_spmv(CsrDev A, VecRef xr, RowsumArgs o, const DevState* S) {
-  if (skip_launch(S, o.pred_aa_ok, o.stop)) return;
-  const double* x = xr.get(S);
-  double* out = o.out_pool ? o.out_pool + (int64_t)S->kx_idx[o.out_role] * o.out_stride : o.out;
-  for_rows<SERIAL>(A, x, [&](int row, double s) { out[row] = s; });
-}
-
-// ---------------------------------------------------------------------------
-// the fused PDHG halves
-// ---------------------------------------------------------------------------
-
-
-// Deterministic two-level reduction of per-CTA partials without a second
-// launch: thread 0 holds the CTA's NV values; they go to part[q * nb + b];
-// the last CTA to finish in each group of kGroup consecutive CTAs adds its
-// group in a fixed tree into gpart[q * ng + g]; returns true in the CTA that
-// completes the last group (then all of gpart is valid). Tickets reset
-// themselves, so the kernel can be replayed.
-template <int NV>
-__device__ __forceinline__ bool group_reduce(const double (&v)[NV], double* part, double* gpart,
-                                             unsigned* tk, int nb, double* red) {
-  __shared__ int flag;
-  const int b = blockIdx.x, g = b / kGroup, ng = (nb + kGroup - 1) / kGroup;
-  const int gsz = min(kGroup, nb - g * kGroup);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q < NV; ++q) part[q * nb + b] = v[q];
-    __threadfence();
-    flag = atomicAdd(&tk[g], 1u) == unsigned(gsz - 1);
-  }
-  __syncthreads();
-  if (!flag) return false;
-  __threadfence();
-  double w[NV];
-  for (int q = 0; q < NV; ++q) {
-    double s = 0.0;
-    for (int t = threadIdx.x; t < gsz; t += blockDim.x) s = __dadd_rn(s, __ldcg(part + q * nb + g * kGroup + t));
-    w[q] = s;
-  }
-  block_sum<NV>(w, red);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q < NV; ++q) gpart[q * ng + g] = w[q];
-    tk[g] = 0;
-    __threadfence();
-    flag = atomicAdd(&tk[ng], 1u) == unsigned(ng - 1);
-  }
-  __syncthreads();
-  if (!flag) return false;
-  __threadfence();
-  if (threadIdx.x == 0) tk[ng] = 0;
-  return true;
-}
-
-// K1 on K' (row j of K' = column j of K), t = (K'y)_j:
-//   xhat_j = min(max(x_j - tau (c_j - t), l_j), u_j)      pdhg_core.cpp:49-53
-//   lambda_j = P_Lambda(c_j - t)                           solver.cpp:67-71
-//   partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
-//   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
-template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kThreads, 5)
-    k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
-  if (S->done) return;
-  __shared__ double red[P1_COUNT * kWarps];
-  const int64_t N = P->N;
-  const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-  double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-  const double* xp = B.upool + (int64_t)S->u_idx[U_PREV] * N;
-  const double* gp = PUSH ? B.gpool + (int64_t)S->g_idx[G_PREV] * N : nullptr;
-  double* gc = PUSH ? B.gpool + (int64_t)S->g_idx[G_CUR] * N : nullptr;
-  const int64_t slot = PUSH ? S->push_slot : 0;
-  double* du = PUSH ? B.du + slot * N : nullptr;
-  double* dg = PUSH ? B.dg + slot * N : nullptr;
-  const double tau = P->tau;
-  double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
-  for_rows<SERIAL>(KT, x + P->n, [&](int j, double t) {
-    const double xj = x[j], cj = __ldg(B.c + j), lj = __ldg(B.l + j), uj = __ldg(B.u + j);
-    double xn = __dsub_rn(xj, __dmul_rn(tau, __dsub_rn(cj, t)));
-    xn = smin(smax(xn, lj), uj);
-    xh[j] = xn;
-    const double d = __dsub_rn(xn, xj);
-    const double red_c = __dsub_rn(cj, t);
-    const double lam = project_lambda1(red_c, lj, uj);
-    double bt = 0.0;
-    if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
-    if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
-    const double dv = __dsub_rn(red_c, lam);
-    acc[P1_GX2] = __dadd_rn(acc[P1_GX2], __dmul_rn(d, d));
-    acc[P1_BOUND] = __dadd_rn(acc[P1_BOUND], bt);
-    acc[P1_DUALSQ] = __dadd_rn(acc[P1_DUALSQ], __dmul_rn(dv, dv));
-    acc[P1_CX] = __dadd_rn(acc[P1_CX], __dmul_rn(cj, xj));
-    if constexpr (PUSH) {
-      du[j] = __dsub_rn(xj, xp[j]);
-      dg[j] = __dsub_rn(d, gp[j]);
-      gc[j] = d;
-    }
-    if (SERIAL) B.T[j] = t;
-  });
-  if (!SERIAL) {
-    block_sum<P1_COUNT>(acc, red);
-    group_reduce<P1_COUNT>(acc, B.part1, B.gpart1, B.tk1, P->nblk1, red);
-  }
-}
-
 // The iteration state is tiny (~1.3 KB) but a single thread walking it in
 // global memory pays one L2 round trip per field; the scalar kernels stage it
 // in shared memory with one coalesced block-wide copy each way.
@@ -393,50 +179,353 @@ __device__ __forceinline__ void advance(const DevParams* P, DevState* S) {
   S->loop_iters += 1;
 }
 
+
+// ---------------------------------------------------------------------------
+// SpMV core: SELL-32 slices streamed through a cp.async ring
+// ---------------------------------------------------------------------------
+//
+// Random-column SpMVs on B200 are bound by the L1TEX gather rate (~0.85
+// cycles per random 8-byte gather per SM with thousands of gathers in flight;
+// measured, profiles/microbench/gather_bench.cu) and by the per-warp chain of
+// dependent loads. The matrix is stored once, on upload, in 32-row slices
+// (SELL-32): element k of the slice's lane-r row sits at sl_ptr[s] + 32 k + r,
+// so 4 consecutive steps of a slice are one contiguous, 16-byte aligned span.
+// A warp streams a slice through a 3-stage cp.async ring in shared memory (no
+// registers held by in-flight data), gathers x[col] 4 per lane at a time and
+// adds its row's products in CSR order — bit-identical to the reference's
+// row-serial matvec (sparse_linalg.cpp:60-69) and, on the transposed CSR
+// (entries in ascending original row), to its row-ordered scatter
+// matvec_transpose (sparse_linalg.cpp:77-87).
+//
+// Work units = slices, then long rows (> kLongRow nonzeros, one warp each).
+// Warps are persistent and pull units from an atomic counter, so no wave
+// quantization or slow-slice tail; per-unit partial sums are then reduced in
+// unit order (two levels of self-resetting tickets), which keeps every sum
+// deterministic whatever warp ran which unit.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+constexpr int kStep = 4;    // slice steps per ring stage (= gathers in flight per lane)
+constexpr int kRing = 3;    // ring depth
+struct __align__(16) SliceStage {
+  int32_t c[kStep * 32];
+  double v[kStep * 32];
+};
+struct WarpRing {
+  SliceStage st[kRing];
+};
+
+__device__ __forceinline__ bool skip_launch(const DevState* S, int pred_aa_ok,
+                                            const int32_t* stop) {
+  if (S) {
+    if (S->done) return true;
+    if (pred_aa_ok && !S->aa_ok) return true;
+  }
+  return stop && *stop;
+}
+
+// Copies stage g (steps 4g .. 4g+3) of the slice at `base` into st.
+__device__ __forceinline__ void issue_stage(const CsrDev& A, int64_t base, int g,
+                                            SliceStage& st, int lane) {
+  const int64_t off = base + int64_t(g) * (kStep * 32);
+  cp_async16(&st.c[4 * lane], A.sci + off + 4 * lane);
+  cp_async16(&st.v[2 * lane], A.sv + off + 2 * lane);
+  cp_async16(&st.v[64 + 2 * lane], A.sv + off + 64 + 2 * lane);
+  cp_async_commit();
+}
+
+// Row sum of this lane's row in slice sl (CSR order). Returns the row (-1
+// for an empty lane).
+__device__ __forceinline__ int slice_sum(const CsrDev& A, int sl, const double* __restrict__ x,
+                                         WarpRing& R, int lane, double& s) {
+  const int row = __ldg(A.sl_row + sl * 32 + lane);
+  const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
+  const int L = __ldg(A.sl_len + sl);
+  const int64_t base = __ldg(A.sl_ptr + sl);
+  const int G = (L + kStep - 1) / kStep;
+  __syncwarp();  // ring free (previous unit fully consumed)
+  if (G > 0) issue_stage(A, base, 0, R.st[0], lane);
+  if (G > 1) issue_stage(A, base, 1, R.st[1], lane);
+  double acc = 0.0;
+  for (int g = 0; g < G; ++g) {
+    if (g + 2 < G) issue_stage(A, base, g + 2, R.st[(g + 2) % kRing], lane);
+    else cp_async_commit();  // keep the group count uniform
+    cp_async_wait<2>();
+    __syncwarp();
+    const SliceStage& st = R.st[g % kRing];
+    double gx[kStep];
+#pragma unroll
+    for (int u = 0; u < kStep; ++u)
+      gx[u] = (g * kStep + u < len) ? __ldg(x + st.c[u * 32 + lane]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kStep; ++u)
+      if (g * kStep + u < len) acc = __dadd_rn(acc, __dmul_rn(st.v[u * 32 + lane], gx[u]));
+    __syncwarp();  // stage consumed before it is refilled
+  }
+  cp_async_wait<0>();
+  s = acc;
+  return row;
+}
+
+// Long row: one warp; SERIAL adds in CSR order through lane 0, TREE adds
+// per-lane strided sums then the fixed xor tree. Valid in lane 0.
+template <bool SERIAL>
+__device__ __forceinline__ double long_row_sum(const CsrDev& A, int row,
+                                               const double* __restrict__ x, int lane) {
+  const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
+  double acc = 0.0;
+  if (SERIAL) {
+    for (int64_t c0 = e0; c0 < e1; c0 += 32) {
+      const int64_t e = c0 + lane;
+      const double pr = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
+      const int cnt = (e1 - c0) < 32 ? (int)(e1 - c0) : 32;
+      for (int q = 0; q < cnt; ++q) {
+        const double t = __shfl_sync(0xffffffffu, pr, q);
+        if (lane == 0) acc = __dadd_rn(acc, t);
+      }
+    }
+    return acc;
+  }
+  for (int64_t c0 = e0 + lane; c0 < e1; c0 += 32 * 4) {
+    double pr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t e = c0 + 32 * u;
+      pr[u] = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, pr[u]);
+  }
+  return warp_sum(acc);
+}
+
+
+__device__ __forceinline__ int grab_unit(const Sched& sc, int lane) {
+  unsigned u = 0;
+  if (lane == 0) u = atomicAdd(sc.next, 1u);
+  return (int)__shfl_sync(0xffffffffu, u, 0);
+}
+
+// The last warp to run out of work resets the unit counter for the next
+// launch (no warp of this launch touches it afterwards).
+__device__ __forceinline__ void retire_warp(const Sched& sc, int lane) {
+  if (lane == 0) {
+    const unsigned total = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(sc.done, 1u) == total - 1) {
+      *sc.next = 0u;
+      *sc.done = 0u;
+    }
+  }
+}
+
+// Per-unit partials v[] (lane 0 valid) -> part; the warp completing a group
+// of kGroup units adds the group in unit order -> gpart; returns true (all
+// lanes) in the warp that completes the last group. Deterministic.
+template <int NV>
+__device__ __forceinline__ bool unit_reduce(const Sched& sc, const double (&v)[NV], int unit,
+                                            int nunits, int lane) {
+  const int g = unit / kGroup, ng = (nunits + kGroup - 1) / kGroup;
+  const int gsz = min(kGroup, nunits - g * kGroup);
+  int flag = 0;
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sc.part[q * nunits + unit] = v[q];
+    __threadfence();
+    flag = atomicAdd(&sc.tk[g], 1u) == unsigned(gsz - 1);
+  }
+  if (!__shfl_sync(0xffffffffu, flag, 0)) return false;
+  __threadfence();
+  double w[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double s = 0.0;
+    for (int t = lane; t < gsz; t += 32) s = __dadd_rn(s, __ldcg(sc.part + q * nunits + g * kGroup + t));
+    w[q] = warp_sum(s);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sc.gpart[q * ng + g] = w[q];
+    sc.tk[g] = 0u;
+    __threadfence();
+    flag = atomicAdd(&sc.tk[ng], 1u) == unsigned(ng - 1);
+    if (flag) sc.tk[ng] = 0u;
+  }
+  flag = __shfl_sync(0xffffffffu, flag, 0);
+  if (flag) __threadfence();
+  return flag != 0;
+}
+
+// Runs f(row, sum) (lane-level, rows of the unit) for every unit this warp
+// pulls; after each unit calls done(unit) on all lanes. Returns when no units
+// are left.
+template <bool SERIAL, class F, class D>
+__device__ __forceinline__ void for_units(const CsrDev& A, const Sched& sc,
+                                          const double* __restrict__ x, WarpRing& R, F&& f,
+                                          D&& done) {
+  const int lane = threadIdx.x & 31;
+  const int nunits = A.nslices + A.nlong;
+  for (int u = grab_unit(sc, lane); u < nunits; u = grab_unit(sc, lane)) {
+    if (u < A.nslices) {
+      double s;
+      const int row = slice_sum(A, u, x, R, lane, s);
+      if (row >= 0) f(row, s);
+    } else {
+      const int row = __ldg(A.long_rows + (u - A.nslices));
+      const double s = long_row_sum<SERIAL>(A, row, x, lane);
+      if (lane == 0) f(row, s);
+    }
+    done(u);
+  }
+  retire_warp(sc, lane);
+}
+
+template <bool SERIAL>
+__global__ void __launch_bounds__(kUnitThreads, kUnitBlocksPerSM)
+    k_spmv(CsrDev A, VecRef xr, RowsumArgs o, Sched sc, const DevState* S) {
+  if (skip_launch(S, o.pred_aa_ok, o.stop)) return;
+  __shared__ WarpRing ring[kUnitWarps];
+  const double* x = xr.get(S);
+  double* out = o.out_pool ? o.out_pool + (int64_t)S->kx_idx[o.out_role] * o.out_stride : o.out;
+  for_units<SERIAL>(A, sc, x, ring[threadIdx.x >> 5], [&](int row, double s) { out[row] = s; },
+                    [](int) {});
+}
+
+// ---------------------------------------------------------------------------
+// the fused PDHG halves
+// ---------------------------------------------------------------------------
+
+// K1 on K' (row j of K' = column j of K), t = (K'y)_j:
+//   xhat_j = min(max(x_j - tau (c_j - t), l_j), u_j)      pdhg_core.cpp:49-53
+//   lambda_j = P_Lambda(c_j - t)                           solver.cpp:67-71
+//   per-unit partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
+//   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
+template <bool SERIAL, bool PUSH>
+__global__ void __launch_bounds__(kUnitThreads, kUnitBlocksPerSM)
+    k_dual_side(CsrDev KT, IterBufs B, Sched sc, const DevParams* __restrict__ P,
+                DevState* S) {
+  if (S->done) return;
+  __shared__ WarpRing ring[kUnitWarps];
+  const int lane = threadIdx.x & 31;
+  const int64_t N = P->N;
+  const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
+  double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+  const double* xp = B.upool + (int64_t)S->u_idx[U_PREV] * N;
+  const double* gp = PUSH ? B.gpool + (int64_t)S->g_idx[G_PREV] * N : nullptr;
+  double* gc = PUSH ? B.gpool + (int64_t)S->g_idx[G_CUR] * N : nullptr;
+  const int64_t slot = PUSH ? S->push_slot : 0;
+  double* du = PUSH ? B.du + slot * N : nullptr;
+  double* dg = PUSH ? B.dg + slot * N : nullptr;
+  const double tau = P->tau;
+  const int nunits = KT.nslices + KT.nlong;
+  double acc[P1_COUNT];
+  auto reset = [&] {
+#pragma unroll
+    for (int q = 0; q < P1_COUNT; ++q) acc[q] = 0.0;
+  };
+  reset();
+  for_units<SERIAL>(
+      KT, sc, x + P->n, ring[threadIdx.x >> 5],
+      [&](int j, double t) {
+        const double xj = x[j], cj = __ldg(B.c + j), lj = __ldg(B.l + j), uj = __ldg(B.u + j);
+        double xn = __dsub_rn(xj, __dmul_rn(tau, __dsub_rn(cj, t)));
+        xn = smin(smax(xn, lj), uj);
+        xh[j] = xn;
+        const double d = __dsub_rn(xn, xj);
+        const double red_c = __dsub_rn(cj, t);
+        const double lam = project_lambda1(red_c, lj, uj);
+        double bt = 0.0;
+        if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
+        if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
+        const double dv = __dsub_rn(red_c, lam);
+        acc[P1_GX2] = __dmul_rn(d, d);
+        acc[P1_BOUND] = bt;
+        acc[P1_DUALSQ] = __dmul_rn(dv, dv);
+        acc[P1_CX] = __dmul_rn(cj, xj);
+        if constexpr (PUSH) {
+          du[j] = __dsub_rn(xj, xp[j]);
+          dg[j] = __dsub_rn(d, gp[j]);
+          gc[j] = d;
+        }
+        if (SERIAL) B.T[j] = t;
+      },
+      [&](int u) {
+        if (!SERIAL) {
+#pragma unroll
+          for (int q = 0; q < P1_COUNT; ++q) acc[q] = warp_sum(acc[q]);
+          unit_reduce<P1_COUNT>(sc, acc, u, nunits, lane);
+        }
+        reset();
+      });
+}
+
 __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2,
                                            double bound, double qy, double cx, double infeas,
                                            double dual_sq);
 
-// TREE mode: add the group sums of K1/K2 (fixed order) and run the control.
-__device__ __forceinline__ void control_from_partials(const IterBufs& B, const DevParams* P,
-                                                      DevState* S) {
-  __shared__ double red7[7 * kWarps];
-  const int ng1 = (P->nblk1 + kGroup - 1) / kGroup, ng2 = (P->nblk2 + kGroup - 1) / kGroup;
+// TREE mode, run by the one warp that completed K2's last group: add the
+// group sums of K1 and K2 in group order, then the control logic on a
+// shared-memory copy of the state.
+__device__ __forceinline__ void control_from_groups(const Sched& s1, int ng1, const Sched& s2,
+                                                    int ng2, const DevParams* P, DevState* S,
+                                                    DevState* sm, DevParams* sp, int lane) {
   double v[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (int b = threadIdx.x; b < ng1; b += blockDim.x) {
-    v[0] = __dadd_rn(v[0], __ldcg(B.gpart1 + P1_GX2 * ng1 + b));
-    v[1] = __dadd_rn(v[1], __ldcg(B.gpart1 + P1_BOUND * ng1 + b));
-    v[2] = __dadd_rn(v[2], __ldcg(B.gpart1 + P1_CX * ng1 + b));
-    v[3] = __dadd_rn(v[3], __ldcg(B.gpart1 + P1_DUALSQ * ng1 + b));
+  for (int b = lane; b < ng1; b += 32) {
+    v[0] = __dadd_rn(v[0], __ldcg(s1.gpart + P1_GX2 * ng1 + b));
+    v[1] = __dadd_rn(v[1], __ldcg(s1.gpart + P1_BOUND * ng1 + b));
+    v[2] = __dadd_rn(v[2], __ldcg(s1.gpart + P1_CX * ng1 + b));
+    v[3] = __dadd_rn(v[3], __ldcg(s1.gpart + P1_DUALSQ * ng1 + b));
   }
-  for (int b = threadIdx.x; b < ng2; b += blockDim.x) {
-    v[4] = __dadd_rn(v[4], __ldcg(B.gpart2 + P2_GY2 * ng2 + b));
-    v[5] = __dadd_rn(v[5], __ldcg(B.gpart2 + P2_QY * ng2 + b));
-    v[6] = __dadd_rn(v[6], __ldcg(B.gpart2 + P2_INFEAS * ng2 + b));
+  for (int b = lane; b < ng2; b += 32) {
+    v[4] = __dadd_rn(v[4], __ldcg(s2.gpart + P2_GY2 * ng2 + b));
+    v[5] = __dadd_rn(v[5], __ldcg(s2.gpart + P2_QY * ng2 + b));
+    v[6] = __dadd_rn(v[6], __ldcg(s2.gpart + P2_INFEAS * ng2 + b));
   }
-  block_sum<7>(v, red7);
-  const double gx2 = v[0], bound = v[1], cx = v[2], dsq = v[3], gy2 = v[4], qy = v[5], inf = v[6];
-  __shared__ DevState sm;
-  __shared__ DevParams sp;
-  params_load(&sp, P);
-  state_load(&sm, S);
-  if (threadIdx.x == 0) {
-    control_logic(&sp, &sm, __dadd_rn(gx2, gy2), bound, qy, cx, inf, dsq);
+#pragma unroll
+  for (int q = 0; q < 7; ++q) v[q] = warp_sum(v[q]);
+  // stage params + state (one coalesced copy each way)
+  {
+    const int* ps = reinterpret_cast<const int*>(P);
+    int* pd = reinterpret_cast<int*>(sp);
+    for (int i = lane; i < int(sizeof(DevParams) / 4); i += 32) pd[i] = __ldg(ps + i);
+    const int* ss = reinterpret_cast<const int*>(S);
+    int* sd = reinterpret_cast<int*>(sm);
+    for (int i = lane; i < int(sizeof(DevState) / 4); i += 32) sd[i] = __ldcg(ss + i);
   }
-  state_store(S, &sm);
+  __syncwarp();
+  if (lane == 0) control_logic(sp, sm, __dadd_rn(v[0], v[4]), v[1], v[5], v[2], v[6], v[3]);
+  __syncwarp();
+  {
+    const int* ss = reinterpret_cast<const int*>(sm);
+    int* sd = reinterpret_cast<int*>(S);
+    for (int i = lane; i < int(sizeof(DevState) / 4); i += 32) sd[i] = ss[i];
+  }
 }
 
 // K2 on K, s = (K xhat)_i:
 //   yhat_i = y_i + sigma (q_i - (2 s - (K x)_i)), clamped >= 0 for i < m1
 //                                                         pdhg_core.cpp:55-60
 //   K xhat cached as the next K x (solver.cpp:90 / pdhg_core.cpp:56)
-//   partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
-// TREE: the last CTA to finish reduces every partial and runs the control.
+//   per-unit partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
+// TREE: the warp completing the last group runs the control.
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kThreads, 5)
-    k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+__global__ void __launch_bounds__(kUnitThreads, kUnitBlocksPerSM)
+    k_primal_side(CsrDev K, IterBufs B, Sched s1, int ng1, Sched sc,
+                  const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
-  __shared__ double red[P2_COUNT * kWarps];
+  __shared__ WarpRing ring[kUnitWarps];
+  __shared__ DevState sm;
+  __shared__ DevParams sp;
+  const int lane = threadIdx.x & 31;
   const int64_t N = P->N;
   const int n = P->n, mr = P->mrows, m1 = P->m1;
   const double* y = B.upool + (int64_t)S->u_idx[U_CUR] * N + n;
@@ -450,31 +539,44 @@ __global__ void __launch_bounds__(kThreads, 5)
   double* du = PUSH ? B.du + slot * N + n : nullptr;
   double* dg = PUSH ? B.dg + slot * N + n : nullptr;
   const double sigma = P->sigma;
-  double acc[P2_COUNT] = {0.0, 0.0, 0.0};
-  for_rows<SERIAL>(K, B.upool + (int64_t)S->u_idx[U_HAT] * N, [&](int i, double s) {
-    const double yi = y[i], qi = __ldg(B.q + i), kxi = kx[i];
-    double yn =
-        __dadd_rn(yi, __dmul_rn(sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
-    if (i < m1) yn = smax(yn, 0.0);
-    yh[i] = yn;
-    kxh[i] = s;
-    const double d = __dsub_rn(yn, yi);
-    double v = __dsub_rn(qi, kxi);
-    if (i < m1) v = smax(v, 0.0);
-    acc[P2_GY2] = __dadd_rn(acc[P2_GY2], __dmul_rn(d, d));
-    acc[P2_QY] = __dadd_rn(acc[P2_QY], __dmul_rn(qi, yi));
-    acc[P2_INFEAS] = __dadd_rn(acc[P2_INFEAS], __dmul_rn(v, v));
-    if constexpr (PUSH) {
-      du[i] = __dsub_rn(yi, yp[i]);
-      dg[i] = __dsub_rn(d, gp[i]);
-      gc[i] = d;
-    }
-  });
-  if (SERIAL) return;
-  block_sum<P2_COUNT>(acc, red);
-  // the CTA completing the last group adds the group sums and runs the control
-  if (!group_reduce<P2_COUNT>(acc, B.part2, B.gpart2, B.tk2, P->nblk2, red)) return;
-  control_from_partials(B, P, S);
+  const int nunits = K.nslices + K.nlong;
+  const int ng2 = (nunits + kGroup - 1) / kGroup;
+  double acc[P2_COUNT];
+  auto reset = [&] {
+#pragma unroll
+    for (int q = 0; q < P2_COUNT; ++q) acc[q] = 0.0;
+  };
+  reset();
+  for_units<SERIAL>(
+      K, sc, B.upool + (int64_t)S->u_idx[U_HAT] * N, ring[threadIdx.x >> 5],
+      [&](int i, double s) {
+        const double yi = y[i], qi = __ldg(B.q + i), kxi = kx[i];
+        double yn =
+            __dadd_rn(yi, __dmul_rn(sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
+        if (i < m1) yn = smax(yn, 0.0);
+        yh[i] = yn;
+        kxh[i] = s;
+        const double d = __dsub_rn(yn, yi);
+        double v = __dsub_rn(qi, kxi);
+        if (i < m1) v = smax(v, 0.0);
+        acc[P2_GY2] = __dmul_rn(d, d);
+        acc[P2_QY] = __dmul_rn(qi, yi);
+        acc[P2_INFEAS] = __dmul_rn(v, v);
+        if constexpr (PUSH) {
+          du[i] = __dsub_rn(yi, yp[i]);
+          dg[i] = __dsub_rn(d, gp[i]);
+          gc[i] = d;
+        }
+      },
+      [&](int u) {
+        if (!SERIAL) {
+#pragma unroll
+          for (int q = 0; q < P2_COUNT; ++q) acc[q] = warp_sum(acc[q]);
+          if (unit_reduce<P2_COUNT>(sc, acc, u, nunits, lane))
+            control_from_groups(s1, ng1, sc, ng2, P, S, &sm, &sp, lane);
+        }
+        reset();
+      });
 }
 
 // ---------------------------------------------------------------------------
