@@ -26,7 +26,7 @@ constexpr int kThreads = 256;        // CTA size of the tile kernels
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxMemory = 64;       // largest AA memory capacity supported
 constexpr int kDotChunk = 512;       // elements per CTA in the tree multi-dot
-constexpr int kCtrlThreads = 256;
+constexpr int kCtrlThreads = 1024;
 
 // iterate roles
 enum { U_CUR = 0, U_PREV = 1, U_HAT = 2, U_CAND = 3 };

@@ -514,12 +514,18 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   }
   // K xhat: products of K with xhat = u_hat[:n], then the fused dual step
   if (m_ > 0) {
-    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(1), ngroups(KTm(ser)), sched(2), su.P, su.S));
-    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(1), ngroups(KTm(ser)), sched(2), su.P, su.S));
-    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(1), ngroups(KTm(ser)), sched(2), su.P, su.S));
-    else LAUNCH("k_primal_side", k_primal_side<false, false><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(1), ngroups(KTm(ser)), sched(2), su.P, su.S));
+    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(2), su.P, su.S));
+    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(2), su.P, su.S));
+    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(2), su.P, su.S));
+    else LAUNCH("k_primal_side", k_primal_side<false, false><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(2), su.P, su.S));
   }
-  if (ser) LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
+  if (ser) {
+    LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
+  } else {
+    LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), KTm(ser).units(),
+                                                            part2_.as<double>(), Km(ser).units(),
+                                                            su.P, su.S));
+  }
   AAPDHG_CUDA(cudaGetLastError());
   return nodes;
 }
@@ -949,7 +955,7 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
     k_dual_side<true, false><<<KTs_.grid(), kUnitThreads, 0, stream_>>>(KTs_, B, sched(1), Pd, Sd);
   }
   if (m_) {
-    k_primal_side<true, false><<<Ks_.grid(), kUnitThreads, 0, stream_>>>(Ks_, B, sched(1), ngroups(KTs_), sched(2), Pd, Sd);
+    k_primal_side<true, false><<<Ks_.grid(), kUnitThreads, 0, stream_>>>(Ks_, B, sched(2), Pd, Sd);
   }
   AAPDHG_CUDA(cudaGetLastError());
   const double* hat = upool_.as<double>() + 2 * N_;

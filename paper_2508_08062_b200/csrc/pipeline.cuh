@@ -254,8 +254,12 @@ __device__ __forceinline__ int slice_sum(const CsrDev& A, int sl, const double* 
   const int64_t base = __ldg(A.sl_ptr + sl);
   const int G = (L + kStep - 1) / kStep;
   __syncwarp();  // ring free (previous unit fully consumed)
+  // always two groups in flight before the loop (empty when G < 2), so
+  // wait_group<2> below always retires exactly stage g
   if (G > 0) issue_stage(A, base, 0, R.st[0], lane);
+  else cp_async_commit();
   if (G > 1) issue_stage(A, base, 1, R.st[1], lane);
+  else cp_async_commit();
   double acc = 0.0;
   for (int g = 0; g < G; ++g) {
     if (g + 2 < G) issue_stage(A, base, g + 2, R.st[(g + 2) % kRing], lane);
@@ -328,53 +332,19 @@ __device__ __forceinline__ void retire_warp(const Sched& sc, int lane) {
   }
 }
 
-// Per-unit partials v[] (lane 0 valid) -> part; the warp completing a group
-// of kGroup units adds the group in unit order -> gpart; returns true (all
-// lanes) in the warp that completes the last group. Deterministic.
-template <int NV>
-__device__ __forceinline__ bool unit_reduce(const Sched& sc, const double (&v)[NV], int unit,
-                                            int nunits, int lane) {
-  const int g = unit / kGroup, ng = (nunits + kGroup - 1) / kGroup;
-  const int gsz = min(kGroup, nunits - g * kGroup);
-  int flag = 0;
-  if (lane == 0) {
-#pragma unroll
-    for (int q = 0; q < NV; ++q) sc.part[q * nunits + unit] = v[q];
-    __threadfence();
-    flag = atomicAdd(&sc.tk[g], 1u) == unsigned(gsz - 1);
-  }
-  if (!__shfl_sync(0xffffffffu, flag, 0)) return false;
-  __threadfence();
-  double w[NV];
-#pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    double s = 0.0;
-    for (int t = lane; t < gsz; t += 32) s = __dadd_rn(s, __ldcg(sc.part + q * nunits + g * kGroup + t));
-    w[q] = warp_sum(s);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int q = 0; q < NV; ++q) sc.gpart[q * ng + g] = w[q];
-    sc.tk[g] = 0u;
-    __threadfence();
-    flag = atomicAdd(&sc.tk[ng], 1u) == unsigned(ng - 1);
-    if (flag) sc.tk[ng] = 0u;
-  }
-  flag = __shfl_sync(0xffffffffu, flag, 0);
-  if (flag) __threadfence();
-  return flag != 0;
-}
-
-// Runs f(row, sum) (lane-level, rows of the unit) for every unit this warp
-// pulls; after each unit calls done(unit) on all lanes. Returns when no units
-// are left.
+// Runs f(row, sum) (by the lane owning the row) for every unit this warp
+// pulls, then done(unit) on all lanes. The next unit index is fetched while
+// the current one is processed (the atomic's latency stays off the path).
 template <bool SERIAL, class F, class D>
 __device__ __forceinline__ void for_units(const CsrDev& A, const Sched& sc,
                                           const double* __restrict__ x, WarpRing& R, F&& f,
                                           D&& done) {
   const int lane = threadIdx.x & 31;
   const int nunits = A.nslices + A.nlong;
-  for (int u = grab_unit(sc, lane); u < nunits; u = grab_unit(sc, lane)) {
+  int u = grab_unit(sc, lane);
+  while (u < nunits) {
+    unsigned nx = 0;
+    if (lane == 0) nx = atomicAdd(sc.next, 1u);  // consumed after this unit
     if (u < A.nslices) {
       double s;
       const int row = slice_sum(A, u, x, R, lane, s);
@@ -385,8 +355,18 @@ __device__ __forceinline__ void for_units(const CsrDev& A, const Sched& sc,
       if (lane == 0) f(row, s);
     }
     done(u);
+    u = (int)__shfl_sync(0xffffffffu, nx, 0);
   }
   retire_warp(sc, lane);
+}
+
+// Per-unit partial sums (warp totals, lane 0 valid) -> part[q * nunits + u].
+template <int NV>
+__device__ __forceinline__ void store_unit(double* part, const double (&v)[NV], int u,
+                                           int nunits, int lane) {
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) part[q * nunits + u] = v[q];
 }
 
 template <bool SERIAL>
@@ -462,7 +442,7 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitBlocksPerSM)
         if (!SERIAL) {
 #pragma unroll
           for (int q = 0; q < P1_COUNT; ++q) acc[q] = warp_sum(acc[q]);
-          unit_reduce<P1_COUNT>(sc, acc, u, nunits, lane);
+          store_unit<P1_COUNT>(sc.part, acc, u, nunits, lane);
         }
         reset();
       });
@@ -472,59 +452,17 @@ __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, doub
                                            double bound, double qy, double cx, double infeas,
                                            double dual_sq);
 
-// TREE mode, run by the one warp that completed K2's last group: add the
-// group sums of K1 and K2 in group order, then the control logic on a
-// shared-memory copy of the state.
-__device__ __forceinline__ void control_from_groups(const Sched& s1, int ng1, const Sched& s2,
-                                                    int ng2, const DevParams* P, DevState* S,
-                                                    DevState* sm, DevParams* sp, int lane) {
-  double v[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (int b = lane; b < ng1; b += 32) {
-    v[0] = __dadd_rn(v[0], __ldcg(s1.gpart + P1_GX2 * ng1 + b));
-    v[1] = __dadd_rn(v[1], __ldcg(s1.gpart + P1_BOUND * ng1 + b));
-    v[2] = __dadd_rn(v[2], __ldcg(s1.gpart + P1_CX * ng1 + b));
-    v[3] = __dadd_rn(v[3], __ldcg(s1.gpart + P1_DUALSQ * ng1 + b));
-  }
-  for (int b = lane; b < ng2; b += 32) {
-    v[4] = __dadd_rn(v[4], __ldcg(s2.gpart + P2_GY2 * ng2 + b));
-    v[5] = __dadd_rn(v[5], __ldcg(s2.gpart + P2_QY * ng2 + b));
-    v[6] = __dadd_rn(v[6], __ldcg(s2.gpart + P2_INFEAS * ng2 + b));
-  }
-#pragma unroll
-  for (int q = 0; q < 7; ++q) v[q] = warp_sum(v[q]);
-  // stage params + state (one coalesced copy each way)
-  {
-    const int* ps = reinterpret_cast<const int*>(P);
-    int* pd = reinterpret_cast<int*>(sp);
-    for (int i = lane; i < int(sizeof(DevParams) / 4); i += 32) pd[i] = __ldg(ps + i);
-    const int* ss = reinterpret_cast<const int*>(S);
-    int* sd = reinterpret_cast<int*>(sm);
-    for (int i = lane; i < int(sizeof(DevState) / 4); i += 32) sd[i] = __ldcg(ss + i);
-  }
-  __syncwarp();
-  if (lane == 0) control_logic(sp, sm, __dadd_rn(v[0], v[4]), v[1], v[5], v[2], v[6], v[3]);
-  __syncwarp();
-  {
-    const int* ss = reinterpret_cast<const int*>(sm);
-    int* sd = reinterpret_cast<int*>(S);
-    for (int i = lane; i < int(sizeof(DevState) / 4); i += 32) sd[i] = ss[i];
-  }
-}
-
 // K2 on K, s = (K xhat)_i:
 //   yhat_i = y_i + sigma (q_i - (2 s - (K x)_i)), clamped >= 0 for i < m1
 //                                                         pdhg_core.cpp:55-60
 //   K xhat cached as the next K x (solver.cpp:90 / pdhg_core.cpp:56)
 //   per-unit partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
-// TREE: the warp completing the last group runs the control.
 template <bool SERIAL, bool PUSH>
 __global__ void __launch_bounds__(kUnitThreads, kUnitBlocksPerSM)
-    k_primal_side(CsrDev K, IterBufs B, Sched s1, int ng1, Sched sc,
-                  const DevParams* __restrict__ P, DevState* S) {
+    k_primal_side(CsrDev K, IterBufs B, Sched sc, const DevParams* __restrict__ P,
+                  DevState* S) {
   if (S->done) return;
   __shared__ WarpRing ring[kUnitWarps];
-  __shared__ DevState sm;
-  __shared__ DevParams sp;
   const int lane = threadIdx.x & 31;
   const int64_t N = P->N;
   const int n = P->n, mr = P->mrows, m1 = P->m1;
@@ -540,7 +478,6 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitBlocksPerSM)
   double* dg = PUSH ? B.dg + slot * N + n : nullptr;
   const double sigma = P->sigma;
   const int nunits = K.nslices + K.nlong;
-  const int ng2 = (nunits + kGroup - 1) / kGroup;
   double acc[P2_COUNT];
   auto reset = [&] {
 #pragma unroll
@@ -572,11 +509,60 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitBlocksPerSM)
         if (!SERIAL) {
 #pragma unroll
           for (int q = 0; q < P2_COUNT; ++q) acc[q] = warp_sum(acc[q]);
-          if (unit_reduce<P2_COUNT>(sc, acc, u, nunits, lane))
-            control_from_groups(s1, ng1, sc, ng2, P, S, &sm, &sp, lane);
+          store_unit<P2_COUNT>(sc.part, acc, u, nunits, lane);
         }
         reset();
       });
+}
+
+// TREE mode control: add the per-unit partials of K1 (nu1 units) and K2 (nu2)
+// in unit order (thread-strided + fixed block tree), then run the control
+// logic on a shared-memory copy of the state.
+__global__ void __launch_bounds__(kCtrlThreads)
+    k_control(const double* __restrict__ part1, int nu1, const double* __restrict__ part2,
+              int nu2, const DevParams* __restrict__ P, DevState* S) {
+  if (S->done) {
+    if (threadIdx.x == 0 && P->use_cond) {
+      cudaGraphSetConditional(P->cond_aa, 0);
+      cudaGraphSetConditional(P->cond_loop, 0);
+    }
+    return;
+  }
+  __shared__ double red[7 * 32];
+  double v[7] = {0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+  for (int b = threadIdx.x; b < nu1; b += blockDim.x) {
+    v[0] = __dadd_rn(v[0], __ldcg(part1 + P1_GX2 * nu1 + b));
+    v[1] = __dadd_rn(v[1], __ldcg(part1 + P1_BOUND * nu1 + b));
+    v[2] = __dadd_rn(v[2], __ldcg(part1 + P1_CX * nu1 + b));
+    v[3] = __dadd_rn(v[3], __ldcg(part1 + P1_DUALSQ * nu1 + b));
+  }
+#pragma unroll 4
+  for (int b = threadIdx.x; b < nu2; b += blockDim.x) {
+    v[4] = __dadd_rn(v[4], __ldcg(part2 + P2_GY2 * nu2 + b));
+    v[5] = __dadd_rn(v[5], __ldcg(part2 + P2_QY * nu2 + b));
+    v[6] = __dadd_rn(v[6], __ldcg(part2 + P2_INFEAS * nu2 + b));
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 7; ++q) v[q] = warp_sum(v[q]);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 7; ++q) red[q * 32 + warp] = v[q];
+  __shared__ DevState sm;
+  __shared__ DevParams sp;
+  params_load(&sp, P);
+  state_load(&sm, S);  // (syncs: red[] complete)
+  if (threadIdx.x == 0) {
+    double t[7];
+    for (int q = 0; q < 7; ++q) {
+      double s = red[q * 32];
+      for (int w = 1; w < nw; ++w) s = __dadd_rn(s, red[q * 32 + w]);
+      t[q] = s;
+    }
+    control_logic(&sp, &sm, __dadd_rn(t[0], t[4]), t[1], t[5], t[2], t[6], t[3]);
+  }
+  state_store(S, &sm);
 }
 
 // ---------------------------------------------------------------------------
