@@ -60,15 +60,13 @@ struct CsrDev {
   const int32_t* sci = nullptr;
   const double* sv = nullptr;
   const int32_t* long_rows = nullptr;
-  int32_t nblocks = 0;  // persistent grid of the kernels streaming this matrix
-  int32_t grid() const { return nblocks; }
-  int32_t units() const { return nslices + nlong; }
+  int32_t nblk_short = 0, nblk_long = 0;
+  int32_t sf = 1;  // lanes per row in the slices (1 = CSR-ordered row sums)
+  int32_t grid() const { return nblk_short + nblk_long; }
 };
 
 constexpr int kLongRow = 256;        // rows longer than this get a warp each
-constexpr int kUnitWarps = 4;        // warps per CTA of the SpMV kernels
-constexpr int kUnitThreads = 32 * kUnitWarps;
-constexpr int kUnitBlocksPerSM = 10; // 40 warps/SM: 51 registers, ~200 KB of rings
+constexpr int kSpmvBlocksPerSM = 6;  // 48 warps/SM at <= 40 registers
 
 constexpr int kGroup = 64;           // CTAs per first-level partial group
 
@@ -152,14 +150,6 @@ struct IterBufs {
   const double* u;
 };
 
-// Unit-level scheduling state of one launch site (self-resetting).
-struct Sched {
-  unsigned* next;   // unit counter
-  unsigned* done;   // warps that found no more work
-  unsigned* tk;     // group tickets [ngroups] + top-level ticket
-  double* part;     // NV x nunits per-unit partials
-  double* gpart;    // NV x ngroups group sums
-};
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;

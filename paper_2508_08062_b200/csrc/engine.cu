@@ -105,9 +105,8 @@ void Problem::build_sell(const int32_t* rp, const int32_t* ci, const double* v,
     sl_len[size_t(s)] = L;
     total += int64_t(32) * L;
   }
-  // padded: the ring copies whole 4-step stages (up to 3 steps past a slice)
-  std::vector<int32_t> sci(size_t(total + kStep * 32), 0);
-  std::vector<double> sv(size_t(total + kStep * 32), 0.0);
+  std::vector<int32_t> sci(size_t(std::max<int64_t>(total, 1)), 0);
+  std::vector<double> sv(size_t(std::max<int64_t>(total, 1)), 0.0);
   for (int s = 0; s < nslices; ++s)
     for (int r = 0; r < R && size_t(s) * R + r < shorts.size(); ++r) {
       const int row = shorts[size_t(s) * R + r];
@@ -135,7 +134,8 @@ void Problem::build_sell(const int32_t* rp, const int32_t* ci, const double* v,
   out.sl_row = st.sl_row.as<int32_t>();
   out.sci = st.sci.as<int32_t>();
   out.sv = st.sv.as<double>();
-  (void)sf;
+  out.sf = sf;
+  out.nblk_short = (nslices + kWarps - 1) / kWarps;
 }
 
 // Uploads one CSR with its two sliced layouts: `ser` (sf = 1, CSR-ordered
@@ -173,13 +173,19 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
   base.v = st.v.as<double>();
   base.nlong = int32_t(longs.size());
   base.long_rows = st.longs.as<int32_t>();
+  base.nblk_long = (base.nlong + kWarps - 1) / kWarps;
   ser = base;
   build_sell(rp, ci, v, shorts, 1, st.sell[0], ser);
-  const int64_t want = (int64_t(ser.units()) + kUnitWarps - 1) / kUnitWarps;
-  ser.nblocks = int32_t(std::max<int64_t>(
-      1, std::min<int64_t>(want, int64_t(num_sms_) * kUnitBlocksPerSM)));
-  tree = ser;
-  (void)short_nnz;
+  // TREE layout: split rows over sf lanes only while the slices still fit in
+  // one wave of resident warps (a matrix with few rows, e.g. K of config 1)
+  const double mean = shorts.empty() ? 0.0 : double(short_nnz) / double(shorts.size());
+  const int64_t slots = int64_t(num_sms_) * kSpmvBlocksPerSM * kWarps;
+  int sf = 1;
+  while (sf < 8 && int64_t(ser.nslices) * 2 * sf <= slots && mean >= 8.0 * sf) sf *= 2;
+  sf = env_int("AAPDHG_SF", sf);
+  tree = base;
+  if (sf == 1) tree = ser;
+  else build_sell(rp, ci, v, shorts, sf, st.sell[1], tree);
 }
 
 // out = A x (CSR-ordered row sums).
@@ -190,44 +196,11 @@ int Problem::spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const Rowsum
   r.pred_aa_ok = pred;
   r.stop = stop;
   prof_begin(s, "k_spmv");
-  const Sched sc = sched(0);
-  if (serial) k_spmv<true><<<A.grid(), kUnitThreads, 0, s>>>(A, x, r, sc, S);
-  else k_spmv<false><<<A.grid(), kUnitThreads, 0, s>>>(A, x, r, sc, S);
+  if (serial) k_spmv<true><<<A.grid(), kThreads, 0, s>>>(A, x, r, S);
+  else k_spmv<false><<<A.grid(), kThreads, 0, s>>>(A, x, r, S);
   prof_end(s);
   AAPDHG_CUDA(cudaGetLastError());
   return 1;
-}
-
-int Problem::ngroups(const CsrDev& A) { return (A.units() + kGroup - 1) / kGroup; }
-
-// Scheduling buffers of the unit kernels: site 0 = plain SpMV (no partials),
-// 1 = K'y side (P1 partials), 2 = K xhat side (P2 partials). Counters and
-// tickets are shared (launches are stream ordered and self-resetting).
-Sched Problem::sched(int site) {
-  Sched s{};
-  unsigned* base = sched_.as<unsigned>();
-  s.next = base;
-  s.done = base + 1;
-  s.tk = base + 2;
-  if (site == 1) {
-    s.part = part1_.as<double>();
-    s.gpart = gpart1_.as<double>();
-  } else if (site == 2) {
-    s.part = part2_.as<double>();
-    s.gpart = gpart2_.as<double>();
-  }
-  return s;
-}
-
-void Problem::alloc_sched() {
-  const int u1 = KTs_.units(), u2 = Ks_.units();
-  const int gmax = std::max(ngroups(KTs_), ngroups(Ks_));
-  sched_.reserve(sizeof(unsigned) * (2 + gmax + 1));
-  AAPDHG_CUDA(cudaMemsetAsync(sched_.p, 0, sched_.bytes, stream_));
-  part1_.reserve(sizeof(double) * P1_COUNT * std::max(u1, 1));
-  part2_.reserve(sizeof(double) * P2_COUNT * std::max(u2, 1));
-  gpart1_.reserve(sizeof(double) * P1_COUNT * std::max(ngroups(KTs_), 1));
-  gpart2_.reserve(sizeof(double) * P2_COUNT * std::max(ngroups(Ks_), 1));
 }
 
 static VecRef vref(const double* p) { return VecRef{p, nullptr, 0, 0, 0}; }
@@ -299,7 +272,6 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
       }
   }
   upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_store_, KTs_, KTt_);
-  alloc_sched();
 
   c_.reserve(sizeof(double) * n_);
   q_.reserve(sizeof(double) * m_);
@@ -382,8 +354,8 @@ void Problem::ensure_iter_buffers(int method, int cap) {
   upool_.reserve(sizeof(double) * 4 * std::max<int64_t>(N_, 1));
   kxpool_.reserve(sizeof(double) * 3 * std::max<int64_t>(m_, 1));
   T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
-  (void)nblk1;
-  (void)nblk2;
+  part1_.reserve(sizeof(double) * P1_COUNT * std::max(nblk1, 1));
+  part2_.reserve(sizeof(double) * P2_COUNT * std::max(nblk2, 1));
   gram_.reserve(sizeof(double) * kMaxMemory * kMaxMemory);
   work_.reserve(sizeof(double) * kMaxMemory * kMaxMemory);
   vec_.reserve(sizeof(double) * 8 * kMaxMemory);
@@ -507,23 +479,23 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   const bool ser = su.serial, push = su.push;
   // K'y: products of K' with y = u_cur[n:], then the fused dual-side rows
   if (n_ > 0) {
-    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KTm(ser).grid(), kUnitThreads, 0, s>>>(KTm(ser), su.B, sched(1), su.P, su.S));
-    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KTm(ser).grid(), kUnitThreads, 0, s>>>(KTm(ser), su.B, sched(1), su.P, su.S));
-    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KTm(ser).grid(), kUnitThreads, 0, s>>>(KTm(ser), su.B, sched(1), su.P, su.S));
-    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KTm(ser).grid(), kUnitThreads, 0, s>>>(KTm(ser), su.B, sched(1), su.P, su.S));
+    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
   }
   // K xhat: products of K with xhat = u_hat[:n], then the fused dual step
   if (m_ > 0) {
-    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(2), su.P, su.S));
-    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(2), su.P, su.S));
-    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(2), su.P, su.S));
-    else LAUNCH("k_primal_side", k_primal_side<false, false><<<Km(ser).grid(), kUnitThreads, 0, s>>>(Km(ser), su.B, sched(2), su.P, su.S));
+    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    else LAUNCH("k_primal_side", k_primal_side<false, false><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
   }
   if (ser) {
     LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
   } else {
-    LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), KTm(ser).units(),
-                                                            part2_.as<double>(), Km(ser).units(),
+    LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), KTm(ser).grid(),
+                                                            part2_.as<double>(), Km(ser).grid(),
                                                             su.P, su.S));
   }
   AAPDHG_CUDA(cudaGetLastError());
@@ -952,10 +924,10 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   const DevParams* Pd = dparams_.as<DevParams>();
   DevState* Sd = dstate_.as<DevState>();
   if (n_) {
-    k_dual_side<true, false><<<KTs_.grid(), kUnitThreads, 0, stream_>>>(KTs_, B, sched(1), Pd, Sd);
+    k_dual_side<true, false><<<KTs_.grid(), kThreads, 0, stream_>>>(KTs_, B, Pd, Sd);
   }
   if (m_) {
-    k_primal_side<true, false><<<Ks_.grid(), kUnitThreads, 0, stream_>>>(Ks_, B, sched(2), Pd, Sd);
+    k_primal_side<true, false><<<Ks_.grid(), kThreads, 0, stream_>>>(Ks_, B, Pd, Sd);
   }
   AAPDHG_CUDA(cudaGetLastError());
   const double* hat = upool_.as<double>() + 2 * N_;

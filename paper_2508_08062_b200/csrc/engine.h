@@ -83,9 +83,7 @@ class Problem {
   void ensure_iter_buffers(int method, int cap);
   void upload_iterate(int slot, const double* x, const double* y);
   IterBufs iter_bufs();
-  static int ngroups(const CsrDev& A);
-  Sched sched(int site);
-  void alloc_sched();
+
   void kkt_eval(int slot, bool serial, double* kkt_dev_out, double* lam_dev);
   int launch_core(cudaStream_t s, const SolveSetup& su);
   int launch_aa(cudaStream_t s, const SolveSetup& su);
@@ -124,7 +122,7 @@ class Problem {
 
   // iteration buffers
   int buf_method_ = -1, buf_cap_ = 0;
-  DevBuf upool_, kxpool_, gpool_, du_, dg_, T_, part1_, part2_, gpart1_, gpart2_, sched_, partdot_,
+  DevBuf upool_, kxpool_, gpool_, du_, dg_, T_, part1_, part2_, partdot_,
       gram_, work_, vec_;
   DevBuf rec_, pow_tab_, dparams_, dstate_, dhat_, scal_, part_small_, lam_, pw_x_, pw_mx_,
       pw_mtmx_, pw_state_;

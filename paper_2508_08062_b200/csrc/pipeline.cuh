@@ -181,49 +181,26 @@ __device__ __forceinline__ void advance(const DevParams* P, DevState* S) {
 
 
 // ---------------------------------------------------------------------------
-// SpMV core: SELL-32 slices streamed through a cp.async ring
+// SpMV core: SELL-32 slices, one per warp
 // ---------------------------------------------------------------------------
 //
 // Random-column SpMVs on B200 are bound by the L1TEX gather rate (~0.85
 // cycles per random 8-byte gather per SM with thousands of gathers in flight;
-// measured, profiles/microbench/gather_bench.cu) and by the per-warp chain of
-// dependent loads. The matrix is stored once, on upload, in 32-row slices
-// (SELL-32): element k of the slice's lane-r row sits at sl_ptr[s] + 32 k + r,
-// so 4 consecutive steps of a slice are one contiguous, 16-byte aligned span.
-// A warp streams a slice through a 3-stage cp.async ring in shared memory (no
-// registers held by in-flight data), gathers x[col] 4 per lane at a time and
-// adds its row's products in CSR order — bit-identical to the reference's
-// row-serial matvec (sparse_linalg.cpp:60-69) and, on the transposed CSR
-// (entries in ascending original row), to its row-ordered scatter
-// matvec_transpose (sparse_linalg.cpp:77-87).
-//
-// Work units = slices, then long rows (> kLongRow nonzeros, one warp each).
-// Warps are persistent and pull units from an atomic counter, so no wave
-// quantization or slow-slice tail; per-unit partial sums are then reduced in
-// unit order (two levels of self-resetting tickets), which keeps every sum
-// deterministic whatever warp ran which unit.
+// measured, profiles/microbench/gather_bench.cu). The matrix is stored once,
+// on upload, in 32-lane slices (SELL-32): with split factor sf a slice holds
+// 32 / sf consecutive short rows, and element k of the slice's row rho sits at
+// sl_ptr[s] + 32 (k / sf) + rho sf + (k % sf). A warp owns a slice: its
+// (col, val) loads are coalesced, each lane issues all loads of a group of
+// kUnroll steps before using them (kUnroll gathers x[col] in flight per lane)
+// and adds its share of the row in CSR order; the sf lanes of a row meet in a
+// fixed xor tree. sf = 1 (the SERIAL layout) keeps each row in one lane —
+// bit-identical to the reference's row-serial matvec (sparse_linalg.cpp:60-69)
+// and, on the transposed CSR (entries in ascending original row), to its
+// row-ordered scatter matvec_transpose (sparse_linalg.cpp:77-87). The TREE
+// layout uses sf > 1 only for matrices with too few rows to fill the GPU.
+// Rows longer than kLongRow get a warp each (CTAs after the slice CTAs).
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-constexpr int kStep = 4;    // slice steps per ring stage (= gathers in flight per lane)
-constexpr int kRing = 3;    // ring depth
-struct __align__(16) SliceStage {
-  int32_t c[kStep * 32];
-  double v[kStep * 32];
-};
-struct WarpRing {
-  SliceStage st[kRing];
-};
+constexpr int kUnroll = 4;
 
 __device__ __forceinline__ bool skip_launch(const DevState* S, int pred_aa_ok,
                                             const int32_t* stop) {
@@ -234,150 +211,86 @@ __device__ __forceinline__ bool skip_launch(const DevState* S, int pred_aa_ok,
   return stop && *stop;
 }
 
-// Copies stage g (steps 4g .. 4g+3) of the slice at `base` into st.
-__device__ __forceinline__ void issue_stage(const CsrDev& A, int64_t base, int g,
-                                            SliceStage& st, int lane) {
-  const int64_t off = base + int64_t(g) * (kStep * 32);
-  cp_async16(&st.c[4 * lane], A.sci + off + 4 * lane);
-  cp_async16(&st.v[2 * lane], A.sv + off + 2 * lane);
-  cp_async16(&st.v[64 + 2 * lane], A.sv + off + 64 + 2 * lane);
-  cp_async_commit();
-}
-
-// Row sum of this lane's row in slice sl (CSR order). Returns the row (-1
-// for an empty lane).
-__device__ __forceinline__ int slice_sum(const CsrDev& A, int sl, const double* __restrict__ x,
-                                         WarpRing& R, int lane, double& s) {
-  const int row = __ldg(A.sl_row + sl * 32 + lane);
-  const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
-  const int L = __ldg(A.sl_len + sl);
-  const int64_t base = __ldg(A.sl_ptr + sl);
-  const int G = (L + kStep - 1) / kStep;
-  __syncwarp();  // ring free (previous unit fully consumed)
-  // always two groups in flight before the loop (empty when G < 2), so
-  // wait_group<2> below always retires exactly stage g
-  if (G > 0) issue_stage(A, base, 0, R.st[0], lane);
-  else cp_async_commit();
-  if (G > 1) issue_stage(A, base, 1, R.st[1], lane);
-  else cp_async_commit();
-  double acc = 0.0;
-  for (int g = 0; g < G; ++g) {
-    if (g + 2 < G) issue_stage(A, base, g + 2, R.st[(g + 2) % kRing], lane);
-    else cp_async_commit();  // keep the group count uniform
-    cp_async_wait<2>();
-    __syncwarp();
-    const SliceStage& st = R.st[g % kRing];
-    double gx[kStep];
-#pragma unroll
-    for (int u = 0; u < kStep; ++u)
-      gx[u] = (g * kStep + u < len) ? __ldg(x + st.c[u * 32 + lane]) : 0.0;
-#pragma unroll
-    for (int u = 0; u < kStep; ++u)
-      if (g * kStep + u < len) acc = __dadd_rn(acc, __dmul_rn(st.v[u * 32 + lane], gx[u]));
-    __syncwarp();  // stage consumed before it is refilled
-  }
-  cp_async_wait<0>();
-  s = acc;
-  return row;
-}
-
-// Long row: one warp; SERIAL adds in CSR order through lane 0, TREE adds
-// per-lane strided sums then the fixed xor tree. Valid in lane 0.
+// Sum of the row this lane owns in this CTA's work; returns the row (-1 if
+// none): the sum is valid in the owning lane only.
 template <bool SERIAL>
-__device__ __forceinline__ double long_row_sum(const CsrDev& A, int row,
-                                               const double* __restrict__ x, int lane) {
+__device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, double& s) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  s = 0.0;
+  if ((int)blockIdx.x < A.nblk_short) {
+    const int sl = blockIdx.x * kWarps + warp;
+    if (sl >= A.nslices) return -1;
+    const int sf = A.sf, j = lane & (sf - 1);
+    const int row = __ldg(A.sl_row + sl * 32 + lane);
+    const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
+    const int cnt = (len - j + sf - 1) / sf;  // this lane's elements
+    const int L = __ldg(A.sl_len + sl);
+    const int64_t base = __ldg(A.sl_ptr + sl) + lane;
+    const int32_t* __restrict__ cp = A.sci + base;
+    const double* __restrict__ vp = A.sv + base;
+    double acc = 0.0;
+    for (int t0 = 0; t0 < L; t0 += kUnroll) {
+      int c[kUnroll];
+      double v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const bool on = t0 + u < cnt;
+        c[u] = on ? __ldcs(cp + 32 * (t0 + u)) : 0;
+        v[u] = on ? __ldcs(vp + 32 * (t0 + u)) : 0.0;
+      }
+      double g[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) g[u] = t0 + u < cnt ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (t0 + u < cnt) acc = __dadd_rn(acc, __dmul_rn(v[u], g[u]));
+    }
+    for (int off = sf >> 1; off > 0; off >>= 1)
+      acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+    s = acc;
+    return (row >= 0 && j == 0) ? row : -1;
+  }
+  const int lr = (blockIdx.x - A.nblk_short) * kWarps + warp;
+  if (lr >= A.nlong) return -1;
+  const int row = __ldg(A.long_rows + lr);
   const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
   double acc = 0.0;
-  if (SERIAL) {
+  if (SERIAL) {  // CSR order through lane 0
     for (int64_t c0 = e0; c0 < e1; c0 += 32) {
       const int64_t e = c0 + lane;
       const double pr = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
-      const int cnt = (e1 - c0) < 32 ? (int)(e1 - c0) : 32;
-      for (int q = 0; q < cnt; ++q) {
+      const int n = (e1 - c0) < 32 ? (int)(e1 - c0) : 32;
+      for (int q = 0; q < n; ++q) {
         const double t = __shfl_sync(0xffffffffu, pr, q);
         if (lane == 0) acc = __dadd_rn(acc, t);
       }
     }
-    return acc;
-  }
-  for (int64_t c0 = e0 + lane; c0 < e1; c0 += 32 * 4) {
-    double pr[4];
+  } else {
+    for (int64_t c0 = e0 + lane; c0 < e1; c0 += 32 * kUnroll) {
+      double pr[kUnroll];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t e = c0 + 32 * u;
-      pr[u] = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
-    }
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t e = c0 + 32 * u;
+        pr[u] = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
+      }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, pr[u]);
-  }
-  return warp_sum(acc);
-}
-
-
-__device__ __forceinline__ int grab_unit(const Sched& sc, int lane) {
-  unsigned u = 0;
-  if (lane == 0) u = atomicAdd(sc.next, 1u);
-  return (int)__shfl_sync(0xffffffffu, u, 0);
-}
-
-// The last warp to run out of work resets the unit counter for the next
-// launch (no warp of this launch touches it afterwards).
-__device__ __forceinline__ void retire_warp(const Sched& sc, int lane) {
-  if (lane == 0) {
-    const unsigned total = gridDim.x * (blockDim.x >> 5);
-    if (atomicAdd(sc.done, 1u) == total - 1) {
-      *sc.next = 0u;
-      *sc.done = 0u;
+      for (int u = 0; u < kUnroll; ++u) acc = __dadd_rn(acc, pr[u]);
     }
+    acc = warp_sum(acc);
   }
-}
-
-// Runs f(row, sum) (by the lane owning the row) for every unit this warp
-// pulls, then done(unit) on all lanes. The next unit index is fetched while
-// the current one is processed (the atomic's latency stays off the path).
-template <bool SERIAL, class F, class D>
-__device__ __forceinline__ void for_units(const CsrDev& A, const Sched& sc,
-                                          const double* __restrict__ x, WarpRing& R, F&& f,
-                                          D&& done) {
-  const int lane = threadIdx.x & 31;
-  const int nunits = A.nslices + A.nlong;
-  int u = grab_unit(sc, lane);
-  while (u < nunits) {
-    unsigned nx = 0;
-    if (lane == 0) nx = atomicAdd(sc.next, 1u);  // consumed after this unit
-    if (u < A.nslices) {
-      double s;
-      const int row = slice_sum(A, u, x, R, lane, s);
-      if (row >= 0) f(row, s);
-    } else {
-      const int row = __ldg(A.long_rows + (u - A.nslices));
-      const double s = long_row_sum<SERIAL>(A, row, x, lane);
-      if (lane == 0) f(row, s);
-    }
-    done(u);
-    u = (int)__shfl_sync(0xffffffffu, nx, 0);
-  }
-  retire_warp(sc, lane);
-}
-
-// Per-unit partial sums (warp totals, lane 0 valid) -> part[q * nunits + u].
-template <int NV>
-__device__ __forceinline__ void store_unit(double* part, const double (&v)[NV], int u,
-                                           int nunits, int lane) {
-  if (lane == 0)
-#pragma unroll
-    for (int q = 0; q < NV; ++q) part[q * nunits + u] = v[q];
+  s = acc;
+  return lane == 0 ? row : -1;
 }
 
 template <bool SERIAL>
-__global__ void __launch_bounds__(kUnitThreads, kUnitBlocksPerSM)
-    k_spmv(CsrDev A, VecRef xr, RowsumArgs o, Sched sc, const DevState* S) {
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+    k_spmv(CsrDev A, VecRef xr, RowsumArgs o, const DevState* S) {
   if (skip_launch(S, o.pred_aa_ok, o.stop)) return;
-  __shared__ WarpRing ring[kUnitWarps];
   const double* x = xr.get(S);
   double* out = o.out_pool ? o.out_pool + (int64_t)S->kx_idx[o.out_role] * o.out_stride : o.out;
-  for_units<SERIAL>(A, sc, x, ring[threadIdx.x >> 5], [&](int row, double s) { out[row] = s; },
-                    [](int) {});
+  double s;
+  const int row = row_sum<SERIAL>(A, x, s);
+  if (row >= 0) out[row] = s;
 }
 
 // ---------------------------------------------------------------------------
@@ -387,136 +300,105 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitBlocksPerSM)
 // K1 on K' (row j of K' = column j of K), t = (K'y)_j:
 //   xhat_j = min(max(x_j - tau (c_j - t), l_j), u_j)      pdhg_core.cpp:49-53
 //   lambda_j = P_Lambda(c_j - t)                           solver.cpp:67-71
-//   per-unit partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
+//   per-CTA partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
 //   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
 template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kUnitThreads, kUnitBlocksPerSM)
-    k_dual_side(CsrDev KT, IterBufs B, Sched sc, const DevParams* __restrict__ P,
-                DevState* S) {
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+    k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
-  __shared__ WarpRing ring[kUnitWarps];
-  const int lane = threadIdx.x & 31;
+  __shared__ double red[P1_COUNT * kWarps];
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-  double* xh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-  const double* xp = B.upool + (int64_t)S->u_idx[U_PREV] * N;
-  const double* gp = PUSH ? B.gpool + (int64_t)S->g_idx[G_PREV] * N : nullptr;
-  double* gc = PUSH ? B.gpool + (int64_t)S->g_idx[G_CUR] * N : nullptr;
-  const int64_t slot = PUSH ? S->push_slot : 0;
-  double* du = PUSH ? B.du + slot * N : nullptr;
-  double* dg = PUSH ? B.dg + slot * N : nullptr;
-  const double tau = P->tau;
-  const int nunits = KT.nslices + KT.nlong;
-  double acc[P1_COUNT];
-  auto reset = [&] {
+  double t;
+  const int j = row_sum<SERIAL>(KT, x + P->n, t);
+  double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
+  if (j >= 0) {
+    const double xj = x[j], cj = __ldg(B.c + j), lj = __ldg(B.l + j), uj = __ldg(B.u + j);
+    double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));
+    xn = smin(smax(xn, lj), uj);
+    B.upool[(int64_t)S->u_idx[U_HAT] * N + j] = xn;
+    const double d = __dsub_rn(xn, xj);
+    const double red_c = __dsub_rn(cj, t);
+    const double lam = project_lambda1(red_c, lj, uj);
+    double bt = 0.0;
+    if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
+    if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
+    const double dv = __dsub_rn(red_c, lam);
+    acc[P1_GX2] = __dmul_rn(d, d);
+    acc[P1_BOUND] = bt;
+    acc[P1_DUALSQ] = __dmul_rn(dv, dv);
+    acc[P1_CX] = __dmul_rn(cj, xj);
+    if constexpr (PUSH) {
+      const int64_t slot = S->push_slot;
+      const double xp = B.upool[(int64_t)S->u_idx[U_PREV] * N + j];
+      const double gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + j];
+      B.du[slot * N + j] = __dsub_rn(xj, xp);
+      B.dg[slot * N + j] = __dsub_rn(d, gp);
+      B.gpool[(int64_t)S->g_idx[G_CUR] * N + j] = d;
+    }
+    if (SERIAL) B.T[j] = t;
+  }
+  if (!SERIAL) {
+    block_sum<P1_COUNT>(acc, red);
+    if (threadIdx.x == 0)
 #pragma unroll
-    for (int q = 0; q < P1_COUNT; ++q) acc[q] = 0.0;
-  };
-  reset();
-  for_units<SERIAL>(
-      KT, sc, x + P->n, ring[threadIdx.x >> 5],
-      [&](int j, double t) {
-        const double xj = x[j], cj = __ldg(B.c + j), lj = __ldg(B.l + j), uj = __ldg(B.u + j);
-        double xn = __dsub_rn(xj, __dmul_rn(tau, __dsub_rn(cj, t)));
-        xn = smin(smax(xn, lj), uj);
-        xh[j] = xn;
-        const double d = __dsub_rn(xn, xj);
-        const double red_c = __dsub_rn(cj, t);
-        const double lam = project_lambda1(red_c, lj, uj);
-        double bt = 0.0;
-        if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
-        if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
-        const double dv = __dsub_rn(red_c, lam);
-        acc[P1_GX2] = __dmul_rn(d, d);
-        acc[P1_BOUND] = bt;
-        acc[P1_DUALSQ] = __dmul_rn(dv, dv);
-        acc[P1_CX] = __dmul_rn(cj, xj);
-        if constexpr (PUSH) {
-          du[j] = __dsub_rn(xj, xp[j]);
-          dg[j] = __dsub_rn(d, gp[j]);
-          gc[j] = d;
-        }
-        if (SERIAL) B.T[j] = t;
-      },
-      [&](int u) {
-        if (!SERIAL) {
+      for (int q = 0; q < P1_COUNT; ++q) B.part1[q * gridDim.x + blockIdx.x] = acc[q];
+  }
+}
+
+// K2 on K, s = (K xhat)_i:
+//   yhat_i = y_i + sigma (q_i - (2 s - (K x)_i)), clamped >= 0 for i < m1
+//                                                         pdhg_core.cpp:55-60
+//   K xhat cached as the next K x (solver.cpp:90 / pdhg_core.cpp:56)
+//   per-CTA partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
+template <bool SERIAL, bool PUSH>
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+    k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+  if (S->done) return;
+  __shared__ double red[P2_COUNT * kWarps];
+  const int64_t N = P->N;
+  const int n = P->n, mr = P->mrows;
+  double s;
+  const int i = row_sum<SERIAL>(K, B.upool + (int64_t)S->u_idx[U_HAT] * N, s);
+  double acc[P2_COUNT] = {0.0, 0.0, 0.0};
+  if (i >= 0) {
+    const double yi = B.upool[(int64_t)S->u_idx[U_CUR] * N + n + i];
+    const double qi = __ldg(B.q + i);
+    const double kxi = B.kxpool[(int64_t)S->kx_idx[KX_CUR] * mr + i];
+    double yn =
+        __dadd_rn(yi, __dmul_rn(P->sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
+    if (i < P->m1) yn = smax(yn, 0.0);
+    B.upool[(int64_t)S->u_idx[U_HAT] * N + n + i] = yn;
+    B.kxpool[(int64_t)S->kx_idx[KX_HAT] * mr + i] = s;
+    const double d = __dsub_rn(yn, yi);
+    double v = __dsub_rn(qi, kxi);
+    if (i < P->m1) v = smax(v, 0.0);
+    acc[P2_GY2] = __dmul_rn(d, d);
+    acc[P2_QY] = __dmul_rn(qi, yi);
+    acc[P2_INFEAS] = __dmul_rn(v, v);
+    if constexpr (PUSH) {
+      const int64_t slot = S->push_slot;
+      const double yp = B.upool[(int64_t)S->u_idx[U_PREV] * N + n + i];
+      const double gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + n + i];
+      B.du[slot * N + n + i] = __dsub_rn(yi, yp);
+      B.dg[slot * N + n + i] = __dsub_rn(d, gp);
+      B.gpool[(int64_t)S->g_idx[G_CUR] * N + n + i] = d;
+    }
+  }
+  if (!SERIAL) {
+    block_sum<P2_COUNT>(acc, red);
+    if (threadIdx.x == 0)
 #pragma unroll
-          for (int q = 0; q < P1_COUNT; ++q) acc[q] = warp_sum(acc[q]);
-          store_unit<P1_COUNT>(sc.part, acc, u, nunits, lane);
-        }
-        reset();
-      });
+      for (int q = 0; q < P2_COUNT; ++q) B.part2[q * gridDim.x + blockIdx.x] = acc[q];
+  }
 }
 
 __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2,
                                            double bound, double qy, double cx, double infeas,
                                            double dual_sq);
 
-// K2 on K, s = (K xhat)_i:
-//   yhat_i = y_i + sigma (q_i - (2 s - (K x)_i)), clamped >= 0 for i < m1
-//                                                         pdhg_core.cpp:55-60
-//   K xhat cached as the next K x (solver.cpp:90 / pdhg_core.cpp:56)
-//   per-unit partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
-template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kUnitThreads, kUnitBlocksPerSM)
-    k_primal_side(CsrDev K, IterBufs B, Sched sc, const DevParams* __restrict__ P,
-                  DevState* S) {
-  if (S->done) return;
-  __shared__ WarpRing ring[kUnitWarps];
-  const int lane = threadIdx.x & 31;
-  const int64_t N = P->N;
-  const int n = P->n, mr = P->mrows, m1 = P->m1;
-  const double* y = B.upool + (int64_t)S->u_idx[U_CUR] * N + n;
-  double* yh = B.upool + (int64_t)S->u_idx[U_HAT] * N + n;
-  const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
-  double* kxh = B.kxpool + (int64_t)S->kx_idx[KX_HAT] * mr;
-  const double* yp = B.upool + (int64_t)S->u_idx[U_PREV] * N + n;
-  const double* gp = PUSH ? B.gpool + (int64_t)S->g_idx[G_PREV] * N + n : nullptr;
-  double* gc = PUSH ? B.gpool + (int64_t)S->g_idx[G_CUR] * N + n : nullptr;
-  const int64_t slot = PUSH ? S->push_slot : 0;
-  double* du = PUSH ? B.du + slot * N + n : nullptr;
-  double* dg = PUSH ? B.dg + slot * N + n : nullptr;
-  const double sigma = P->sigma;
-  const int nunits = K.nslices + K.nlong;
-  double acc[P2_COUNT];
-  auto reset = [&] {
-#pragma unroll
-    for (int q = 0; q < P2_COUNT; ++q) acc[q] = 0.0;
-  };
-  reset();
-  for_units<SERIAL>(
-      K, sc, B.upool + (int64_t)S->u_idx[U_HAT] * N, ring[threadIdx.x >> 5],
-      [&](int i, double s) {
-        const double yi = y[i], qi = __ldg(B.q + i), kxi = kx[i];
-        double yn =
-            __dadd_rn(yi, __dmul_rn(sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
-        if (i < m1) yn = smax(yn, 0.0);
-        yh[i] = yn;
-        kxh[i] = s;
-        const double d = __dsub_rn(yn, yi);
-        double v = __dsub_rn(qi, kxi);
-        if (i < m1) v = smax(v, 0.0);
-        acc[P2_GY2] = __dmul_rn(d, d);
-        acc[P2_QY] = __dmul_rn(qi, yi);
-        acc[P2_INFEAS] = __dmul_rn(v, v);
-        if constexpr (PUSH) {
-          du[i] = __dsub_rn(yi, yp[i]);
-          dg[i] = __dsub_rn(d, gp[i]);
-          gc[i] = d;
-        }
-      },
-      [&](int u) {
-        if (!SERIAL) {
-#pragma unroll
-          for (int q = 0; q < P2_COUNT; ++q) acc[q] = warp_sum(acc[q]);
-          store_unit<P2_COUNT>(sc.part, acc, u, nunits, lane);
-        }
-        reset();
-      });
-}
-
-// TREE mode control: add the per-unit partials of K1 (nu1 units) and K2 (nu2)
-// in unit order (thread-strided + fixed block tree), then run the control
+// TREE mode control: add the per-CTA partials of K1 (nu1 CTAs) and K2 (nu2)
+// in CTA order (thread-strided + fixed block tree), then run the control
 // logic on a shared-memory copy of the state.
 __global__ void __launch_bounds__(kCtrlThreads)
     k_control(const double* __restrict__ part1, int nu1, const double* __restrict__ part2,
