@@ -279,3 +279,45 @@ def test_config1_first_50_iterates(port):
     ref_tau = port.select_step_sizes(p, SolverConfig()).tau
     assert abs(tau - ref_tau) <= 1e-10 * ref_tau
     del base
+
+
+@pytest.mark.parametrize("reduction", ["serial", "tree"])
+def test_config2_transport_faa_long_rows(port, reduction):
+    """BASELINE config 2 shape (transport, FAA m=10, cos>0.99, length 1e4),
+    scaled to 300 x 300: K rows of 300 nonzeros exercise the long-row path."""
+    p = problems.make_config(2, scale=0.15)
+    assert np.diff(p.k.row_ptr).max() > 256
+    spec = problems.CONFIGS[2]
+    with Solver(p) as s:
+        tau = s.select_step_sizes(SolverConfig(reduction="serial")).tau
+        cfg = SolverConfig(method=Method.FAA_PDHG, m=10, toll=1e-9, max_iters=60, tau=tau,
+                           sigma=tau, reduction=reduction,
+                           filter=type(SolverConfig().filter)(c_s=spec["c_s"],
+                                                              kappa_bar=spec["kappa_bar"]))
+        got = s.solve(cfg)
+    ref = port.solve(p, cfg)
+    k = 50
+    np.testing.assert_allclose(got.trajectory["g_norm"][:k], ref.trajectory["g_norm"][:k],
+                               rtol=1e-8)
+    assert np.array_equal(got.trajectory["aa_step"][:k], ref.trajectory["aa_step"][:k])
+
+
+@pytest.mark.parametrize("reduction", ["serial", "tree"])
+def test_config3_zipf_rows(port, reduction):
+    """BASELINE config 3 shape (Zipf(1.5) row lengths, AA m=20), scaled: long
+    and length-1 rows side by side. SERIAL is bit-exact; TREE 1e-10."""
+    p = problems.make_config(3, scale=0.002)
+    lens = np.diff(p.k.row_ptr)
+    assert lens.max() > 256 and (lens == 1).any()
+    with Solver(p) as s:
+        tau = s.select_step_sizes(SolverConfig(reduction="serial")).tau
+        cfg = SolverConfig(method=Method.AA_PDHG, m=20, toll=1e-9, max_iters=50, tau=tau,
+                           sigma=tau, reduction=reduction)
+        got = s.solve(cfg)
+    ref = port.solve(p, cfg)
+    if reduction == "serial":
+        assert np.array_equal(got.trajectory["g_norm"], ref.trajectory["g_norm"])
+        assert np.array_equal(got.result.u.x, ref.result.u.x)
+    else:
+        np.testing.assert_allclose(got.trajectory["g_norm"], ref.trajectory["g_norm"],
+                                   rtol=1e-10)
