@@ -106,6 +106,7 @@ struct DevState {
   int32_t mix_slots[kMaxMemory];   // columns entering the mix (kept set)
   double w[kMaxMemory];
   double sres[8];                  // serial chain results
+  double tot1[4];                  // K1 partial totals (TREE, fused control)
   uint64_t t0_ns;
   uint64_t loop_iters;             // iterations that did work (launch accounting)
   uint32_t ticket;                 // last-CTA election in k_primal_side
@@ -144,6 +145,8 @@ struct IterBufs {
   double* T;       // n
   double* part1;   // P1_COUNT x nblk1 (per CTA)
   double* part2;   // P2_COUNT x nblk2
+  int32_t nu1;        // K1 CTAs (rows of part1)
+  int32_t fused_ctrl; // TREE solve: k_primal_side's last CTA runs the control
   const double* c;
   const double* q;
   const double* l;

@@ -135,7 +135,12 @@ void Problem::build_sell(const int32_t* rp, const int32_t* ci, const double* v,
   out.sci = st.sci.as<int32_t>();
   out.sv = st.sv.as<double>();
   out.sf = sf;
-  out.nblk_short = (nslices + kWarps - 1) / kWarps;
+  // One wave: exactly kSpmvBlocksPerSM CTAs on every SM with the slices
+  // spread evenly over them (a ceil(nslices / 8) grid would leave some SMs
+  // one CTA more than others: ~20% idle tail). Several waves: 8 per CTA.
+  const int wave = num_sms_ * kSpmvBlocksPerSM;
+  out.nblk_short = int64_t(nslices) <= int64_t(wave) * kWarps ? std::min(nslices, wave)
+                                                              : (nslices + kWarps - 1) / kWarps;
 }
 
 // Uploads one CSR with its two sliced layouts: `ser` (sf = 1, CSR-ordered
@@ -256,6 +261,7 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
 
   // K, padded so 16-byte cp.async of a tile's aligned superset stays in bounds
   AAPDHG_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device));
+  pdl_ = env_int("AAPDHG_PDL", 1) != 0;
   upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
   // K' as CSR, entries of each row in ascending original row (counting sort)
   std::vector<int32_t> trp(static_cast<size_t>(n_) + 1, 0), tci(static_cast<size_t>(nnz_));
@@ -460,6 +466,24 @@ void Problem::prof_collect() {
   pending_.clear();
 }
 
+// cudaLaunchKernelEx, optionally with programmatic stream serialization
+// (captured into the graph as a programmatic dependency edge).
+template <typename... KArgs, typename... Args>
+static void launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t s, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  AAPDHG_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 #define LAUNCH(name, ...)      \
   do {                         \
     prof_begin(s, name);       \
@@ -484,16 +508,19 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
     else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
     else LAUNCH("k_dual_side", k_dual_side<false, false><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
   }
-  // K xhat: products of K with xhat = u_hat[:n], then the fused dual step
+  // K xhat: products of K with xhat = u_hat[:n], then the fused dual step;
+  // launched as a programmatic dependent of K1 (its CTAs load their slice
+  // metadata while K1 drains, then wait for K1's xhat)
   if (m_ > 0) {
-    if (ser && push) LAUNCH("k_primal_side", k_primal_side<true, true><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_primal_side", k_primal_side<true, false><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
-    else if (push) LAUNCH("k_primal_side", k_primal_side<false, true><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
-    else LAUNCH("k_primal_side", k_primal_side<false, false><<<Km(ser).grid(), kThreads, 0, s>>>(Km(ser), su.B, su.P, su.S));
+    const bool pdl = pdl_ && n_ > 0;
+    const dim3 g(Km(ser).grid());
+    auto kern = ser ? (push ? k_primal_side<true, true> : k_primal_side<true, false>)
+                    : (push ? k_primal_side<false, true> : k_primal_side<false, false>);
+    LAUNCH("k_primal_side", launch_ex(kern, g, dim3(kThreads), 0, s, pdl, Km(ser), su.B, su.P, su.S));
   }
   if (ser) {
     LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
-  } else {
+  } else if (!su.B.fused_ctrl) {  // (otherwise k_primal_side's last CTA)
     LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), KTm(ser).grid(),
                                                             part2_.as<double>(), Km(ser).grid(),
                                                             su.P, su.S));
@@ -746,6 +773,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
 
   SolveSetup su;
   su.B = iter_bufs();
+  su.B.nu1 = n_ > 0 ? KTm(serial).grid() : 0;
+  su.B.fused_ctrl = (!serial && m_ > 0) ? 1 : 0;
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
                  partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
   su.W = SolveScratch{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};

@@ -108,6 +108,7 @@ class Problem {
 
   int device_;
   int num_sms_ = 148;
+  bool pdl_ = true;  // AAPDHG_PDL=0 disables programmatic dependent launch
   cudaStream_t stream_ = nullptr;
   cudaStream_t own_stream_ = nullptr;
   int n_ = 0, m_ = 0, m1_ = 0;

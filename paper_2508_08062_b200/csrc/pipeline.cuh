@@ -202,6 +202,17 @@ __device__ __forceinline__ void advance(const DevParams* P, DevState* S) {
 
 constexpr int kUnroll = 4;
 
+// Programmatic dependent launch (no-ops when the kernel was launched without
+// the attribute): a dependent kernel's CTAs may become resident while the
+// primary drains; they load their slice metadata, then wait here until the
+// primary grid has completed and its writes are visible.
+__device__ __forceinline__ void grid_dependency_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
 __device__ __forceinline__ bool skip_launch(const DevState* S, int pred_aa_ok,
                                             const int32_t* stop) {
   if (S) {
@@ -218,8 +229,9 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   s = 0.0;
   if ((int)blockIdx.x < A.nblk_short) {
-    const int sl = blockIdx.x * kWarps + warp;
-    if (sl >= A.nslices) return -1;
+    // CTA b owns slices [b * ns / nblk, (b + 1) * ns / nblk): <= kWarps each
+    const int sl = int(int64_t(blockIdx.x) * A.nslices / A.nblk_short) + warp;
+    if (sl >= int(int64_t(blockIdx.x + 1) * A.nslices / A.nblk_short)) return -1;
     const int sf = A.sf, j = lane & (sf - 1);
     const int row = __ldg(A.sl_row + sl * 32 + lane);
     const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
@@ -228,6 +240,7 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     const int64_t base = __ldg(A.sl_ptr + sl) + lane;
     const int32_t* __restrict__ cp = A.sci + base;
     const double* __restrict__ vp = A.sv + base;
+    grid_dependency_wait();  // x may be the previous kernel's output (PDL)
     double acc = 0.0;
     for (int t0 = 0; t0 < L; t0 += kUnroll) {
       int c[kUnroll];
@@ -254,6 +267,7 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
   if (lr >= A.nlong) return -1;
   const int row = __ldg(A.long_rows + lr);
   const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
+  grid_dependency_wait();
   double acc = 0.0;
   if (SERIAL) {  // CSR order through lane 0
     for (int64_t c0 = e0; c0 < e1; c0 += 32) {
@@ -294,6 +308,83 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 }
 
 // ---------------------------------------------------------------------------
+// TREE-mode control without a launch of its own
+// ---------------------------------------------------------------------------
+
+__device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2,
+                                           double bound, double qy, double cx, double infeas,
+                                           double dual_sq);
+
+// Sums NQ rows of per-CTA partials (row q at part[q * nu]) in a fixed shape:
+// thread-strided in CTA order, warp xor tree, warps in order. Result in
+// thread 0 of the calling CTA. red holds NQ * 32 doubles.
+template <int NQ>
+__device__ __forceinline__ void reduce_partial_rows(const double* part, int nu, double (&t)[NQ],
+                                                    double* red) {
+  double v[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) v[q] = 0.0;
+#pragma unroll 4
+  for (int b = threadIdx.x; b < nu; b += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v[q] = __dadd_rn(v[q], __ldcg(part + q * nu + b));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) v[q] = warp_sum(v[q]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) red[q * 32 + warp] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double s = red[q * 32];
+      for (int w = 1; w < nw; ++w) s = __dadd_rn(s, red[q * 32 + w]);
+      t[q] = s;
+    }
+}
+
+// Runs at the end of every k_primal_side CTA in TREE mode. CTA 0 first folds
+// K1's per-CTA partials (complete: K1 finished before K2 started) into
+// S->tot1 while the other CTAs still stream; the last CTA to finish (ticket
+// election, threadFenceReduction pattern) folds K2's partials and runs the
+// control logic on a shared-memory copy of the state. The sums are in CTA
+// order whichever CTA is last, so the result is deterministic.
+__device__ __forceinline__ void fused_control_tail(const IterBufs& B, const DevParams* P,
+                                                   DevState* S) {
+  __shared__ double red[P1_COUNT * 32];
+  __shared__ int last;
+  if (blockIdx.x == 0) {
+    double t1[P1_COUNT];
+    reduce_partial_rows<P1_COUNT>(B.part1, B.nu1, t1, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int q = 0; q < P1_COUNT; ++q) S->tot1[q] = B.nu1 > 0 ? t1[q] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&S->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t2[P2_COUNT];
+  reduce_partial_rows<P2_COUNT>(B.part2, gridDim.x, t2, red);
+  __shared__ DevState sm;
+  __shared__ DevParams sp;
+  params_load(&sp, P);
+  state_load(&sm, S);
+  if (threadIdx.x == 0) {
+    sm.ticket = 0;
+    const double* t1 = sm.tot1;
+    control_logic(&sp, &sm, __dadd_rn(t1[P1_GX2], t2[P2_GY2]), t1[P1_BOUND], t2[P2_QY],
+                  t1[P1_CX], t2[P2_INFEAS], t1[P1_DUALSQ]);
+  }
+  state_store(S, &sm);
+}
+
+// ---------------------------------------------------------------------------
 // the fused PDHG halves
 // ---------------------------------------------------------------------------
 
@@ -305,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 template <bool SERIAL, bool PUSH>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+  launch_dependents();  // k_primal_side may start its prologue (PDL)
   if (S->done) return;
   __shared__ double red[P1_COUNT * kWarps];
   const int64_t N = P->N;
@@ -390,12 +482,9 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     if (threadIdx.x == 0)
 #pragma unroll
       for (int q = 0; q < P2_COUNT; ++q) B.part2[q * gridDim.x + blockIdx.x] = acc[q];
+    if (B.fused_ctrl) fused_control_tail(B, P, S);
   }
 }
-
-__device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2,
-                                           double bound, double qy, double cx, double infeas,
-                                           double dual_sq);
 
 // TREE mode control: add the per-CTA partials of K1 (nu1 CTAs) and K2 (nu2)
 // in CTA order (thread-strided + fixed block tree), then run the control
@@ -410,39 +499,19 @@ __global__ void __launch_bounds__(kCtrlThreads)
     }
     return;
   }
-  __shared__ double red[7 * 32];
-  double v[7] = {0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 4
-  for (int b = threadIdx.x; b < nu1; b += blockDim.x) {
-    v[0] = __dadd_rn(v[0], __ldcg(part1 + P1_GX2 * nu1 + b));
-    v[1] = __dadd_rn(v[1], __ldcg(part1 + P1_BOUND * nu1 + b));
-    v[2] = __dadd_rn(v[2], __ldcg(part1 + P1_CX * nu1 + b));
-    v[3] = __dadd_rn(v[3], __ldcg(part1 + P1_DUALSQ * nu1 + b));
-  }
-#pragma unroll 4
-  for (int b = threadIdx.x; b < nu2; b += blockDim.x) {
-    v[4] = __dadd_rn(v[4], __ldcg(part2 + P2_GY2 * nu2 + b));
-    v[5] = __dadd_rn(v[5], __ldcg(part2 + P2_QY * nu2 + b));
-    v[6] = __dadd_rn(v[6], __ldcg(part2 + P2_INFEAS * nu2 + b));
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int q = 0; q < 7; ++q) v[q] = warp_sum(v[q]);
-  if (lane == 0)
-#pragma unroll
-    for (int q = 0; q < 7; ++q) red[q * 32 + warp] = v[q];
+  __shared__ double red[P1_COUNT * 32];
+  double t1[P1_COUNT], t2[P2_COUNT];
+  reduce_partial_rows<P1_COUNT>(part1, nu1, t1, red);
+  reduce_partial_rows<P2_COUNT>(part2, nu2, t2, red);
   __shared__ DevState sm;
   __shared__ DevParams sp;
   params_load(&sp, P);
-  state_load(&sm, S);  // (syncs: red[] complete)
+  state_load(&sm, S);
   if (threadIdx.x == 0) {
-    double t[7];
-    for (int q = 0; q < 7; ++q) {
-      double s = red[q * 32];
-      for (int w = 1; w < nw; ++w) s = __dadd_rn(s, red[q * 32 + w]);
-      t[q] = s;
-    }
-    control_logic(&sp, &sm, __dadd_rn(t[0], t[4]), t[1], t[5], t[2], t[6], t[3]);
+    if (nu1 == 0) t1[P1_GX2] = t1[P1_BOUND] = t1[P1_CX] = t1[P1_DUALSQ] = 0.0;
+    if (nu2 == 0) t2[P2_GY2] = t2[P2_QY] = t2[P2_INFEAS] = 0.0;
+    control_logic(&sp, &sm, __dadd_rn(t1[P1_GX2], t2[P2_GY2]), t1[P1_BOUND], t2[P2_QY],
+                  t1[P1_CX], t2[P2_INFEAS], t1[P1_DUALSQ]);
   }
   state_store(S, &sm);
 }

@@ -23,12 +23,15 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
         t0 = time.perf_counter()
         out = s.solve(cfg)
         dt = time.perf_counter() - t0
-    print(f"{os.environ.get('AAPDHG_EAGER','0')=} {meth.name:9s} scale={sys.argv[3] if len(sys.argv)>3 else 1} "
+    print(f"eager={os.environ.get('AAPDHG_EAGER','0')} pdl={os.environ.get('AAPDHG_PDL','1')} {meth.name:9s} scale={sys.argv[3] if len(sys.argv)>3 else 1} "
           f"{out.result.iterations/dt:10.1f} it/s  {1e6*dt/out.result.iterations:8.1f} us/it  aa={out.result.i}")
     sys.exit(0)
 
-for eager in ("0", "1"):
+# usage: exp_timing.py [eager,pdl ...]   e.g. 0,1 0,0 1,1
+combos = sys.argv[1:] or ["0,1", "0,0", "1,1"]
+for combo in combos:
+    eager, pdl = combo.split(",")
     for meth in ("PDHG", "AA_PDHG"):
         for scale in ("1", "0.01"):
-            env = dict(os.environ, AAPDHG_EAGER=eager)
+            env = dict(os.environ, AAPDHG_EAGER=eager, AAPDHG_PDL=pdl)
             subprocess.run([sys.executable, __file__, "child", meth, scale], env=env)
