@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define AAPDHG_ABI_VERSION 1
+#define AAPDHG_ABI_VERSION 2
 
 /* Error codes (errors.hpp:8-30). */
 typedef enum aapdhg_status {
@@ -148,6 +148,27 @@ typedef void (*aapdhg_record_sink)(const aapdhg_record* recs, uint64_t count,
 
 typedef struct aapdhg_handle aapdhg_handle;
 
+/* Sharded (multi-GPU) solve, SURVEY.md §8(e) / DESIGN.md §8: the LP's rows
+ * and columns are split into `world` contiguous nnz-balanced blocks; shard r
+ * owns row block R_r (y, q, K x) and column block C_r (x, c, l, u).
+ *   NCCL:     one shard per process (rank, world), one GPU each; all shards
+ *             pass the same whole LP and the same 128-byte NCCL id (made by
+ *             aapdhg_cuda_nccl_id on rank 0 and broadcast by the caller).
+ *   LOOPBACK: all `world` shards in this process on `device`, exchanging by
+ *             device copies (tests the partitioned path on one GPU).
+ * No reference counterpart: the reference solve() is single-threaded
+ * (proj/src/solver.cpp:125-253); results match it within the TREE-mode
+ * tolerance (scalar sums meet in rank order). */
+enum { AAPDHG_DIST_NCCL = 0, AAPDHG_DIST_LOOPBACK = 1 };
+#define AAPDHG_NCCL_ID_BYTES 128
+typedef struct aapdhg_dist_view {
+  int32_t rank;       /* this process's shard (NCCL); ignored by LOOPBACK */
+  int32_t world;      /* number of shards, 1 <= world <= min(n, m) */
+  int32_t transport;  /* AAPDHG_DIST_* */
+  int32_t pad0;
+  const uint8_t* nccl_id; /* AAPDHG_NCCL_ID_BYTES bytes (NCCL only) */
+} aapdhg_dist_view;
+
 /* ---- library ------------------------------------------------------------ */
 
 int aapdhg_cuda_abi_version(void);
@@ -264,6 +285,24 @@ int aapdhg_cuda_kernel_times(aapdhg_handle* h, char* names, size_t names_len,
  * nodes counted individually) and the iterations it ran. */
 int aapdhg_cuda_last_launch_count(aapdhg_handle* h, uint64_t* launches,
                                   uint64_t* loop_iterations);
+
+/* ---- sharded solve ------------------------------------------------------ */
+
+/* Fills out[0..AAPDHG_NCCL_ID_BYTES) with a fresh NCCL unique id.
+ * AAPDHG_ERR_UNSUPPORTED when libnccl.so.2 cannot be loaded. */
+int aapdhg_cuda_nccl_id(uint8_t* out, size_t len, char* err, size_t errlen);
+/* The row / column blocks a world-way sharded solve uses (host only, no GPU
+ * needed): row_bounds[world + 1], col_bounds[world + 1]. */
+int aapdhg_cuda_partition(const aapdhg_csr_view* k, int32_t world, int32_t* row_bounds,
+                          int32_t* col_bounds);
+/* Like aapdhg_cuda_problem_create, for one process's part of a sharded
+ * solve. aapdhg_cuda_solve / aapdhg_cuda_select_step_sizes on the handle are
+ * collective (every rank calls them with the same arguments) and return the
+ * whole x, y, lambda and the same records on every rank. The single-op
+ * entry points return AAPDHG_ERR_UNSUPPORTED on such a handle. */
+int aapdhg_cuda_problem_create_dist(const aapdhg_problem_view* prob, int device,
+                                    const aapdhg_dist_view* dist, aapdhg_handle** out,
+                                    char* err, size_t errlen);
 
 #ifdef __cplusplus
 }

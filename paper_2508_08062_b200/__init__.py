@@ -4,15 +4,15 @@ Drop-in for the reference C++ solver API (proj/include/aapdhg/solver.hpp);
 the compute path is ``lib/libaapdhg_cuda.so`` (hand-written CUDA, C-ABI in
 ``include/aapdhg_cuda.h``). See DESIGN.md.
 """
-from .api import (AAParams, CudaError, DimensionError, Error, FilterParams, InputError,
-                  Iterate, KktMetrics, Method, ProblemData, SingularError, SolveOutput,
-                  SolveResult, SolveStatus, Solver, SolverConfig, SparseMatrix, StepSizes,
-                  UnsupportedError, kkt_metrics, safeguard_pass, select_step_sizes, solve,
-                  vstack)
+from .api import (AAParams, CudaError, DimensionError, DistConfig, Error, FilterParams,
+                  InputError, Iterate, KktMetrics, Method, ProblemData, SingularError,
+                  SolveOutput, SolveResult, SolveStatus, Solver, SolverConfig, SparseMatrix,
+                  StepSizes, UnsupportedError, kkt_metrics, nccl_unique_id, partition,
+                  safeguard_pass, select_step_sizes, solve, vstack)
 
 __all__ = [
-    "AAParams", "CudaError", "DimensionError", "Error", "FilterParams", "InputError", "Iterate",
+    "AAParams", "CudaError", "DimensionError", "DistConfig", "Error", "FilterParams", "InputError", "Iterate",
     "KktMetrics", "Method", "ProblemData", "SingularError", "SolveOutput", "SolveResult",
     "SolveStatus", "Solver", "SolverConfig", "SparseMatrix", "StepSizes", "UnsupportedError",
-    "kkt_metrics", "safeguard_pass", "select_step_sizes", "solve", "vstack",
+    "kkt_metrics", "nccl_unique_id", "partition", "safeguard_pass", "select_step_sizes", "solve", "vstack",
 ]

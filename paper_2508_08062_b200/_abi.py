@@ -18,7 +18,7 @@ LIB_DIR = PKG_DIR / "lib"
 CUDA_LIB = LIB_DIR / "libaapdhg_cuda.so"
 HOST_LIB = LIB_DIR / "libaapdhg.so"
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # aapdhg_status
 OK, ERR_INPUT, ERR_DIMENSION, ERR_UNSUPPORTED, ERR_SINGULAR, ERR_CUDA, ERR_INTERNAL = range(7)
@@ -27,6 +27,9 @@ METHOD_PDHG, METHOD_AA, METHOD_FAA = 0, 1, 2
 (SOLVE_RESIDUAL_TOL, SOLVE_KKT_TOL, SOLVE_MAX_ITERS, SOLVE_TIMEOUT,
  SOLVE_FIXED_POINT_START) = range(5)
 REDUCE_AUTO, REDUCE_SERIAL, REDUCE_TREE = 0, 1, 2
+# sharded-solve transports
+DIST_NCCL, DIST_LOOPBACK = 0, 1
+NCCL_ID_BYTES = 128
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -40,6 +43,11 @@ class CsrView(C.Structure):
 class ProblemView(C.Structure):
     _fields_ = [("k", CsrView), ("m1", C.c_int32), ("c", _dp), ("q", _dp),
                 ("l", _dp), ("u", _dp)]
+
+
+class DistView(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("transport", C.c_int32),
+                ("pad0", C.c_int32), ("nccl_id", C.POINTER(C.c_uint8))]
 
 
 class SolveParams(C.Structure):
@@ -109,6 +117,12 @@ class RecordCollector:
         return np.concatenate(self.chunks)
 
 
+def csr_view(k):
+    """CsrView over a SparseMatrix-like object (arrays kept alive by k)."""
+    return CsrView(int(k.nrows), int(k.ncols), int(k.nnz), iptr(k.row_ptr), iptr(k.col_idx),
+                   dptr(k.vals))
+
+
 def problem_view(prob):
     """ProblemView over a ProblemData-like object (arrays kept alive by prob)."""
     k = prob.k
@@ -147,6 +161,10 @@ def _declare_cuda(lib):
         "aapdhg_cuda_set_profiling": ([H, C.c_int32], C.c_int),
         "aapdhg_cuda_kernel_times": ([H, C.c_char_p, C.c_size_t, _dp,
                                       C.POINTER(C.c_uint64), C.c_int32, _ip], C.c_int),
+        "aapdhg_cuda_nccl_id": ([C.POINTER(C.c_uint8), C.c_size_t] + E, C.c_int),
+        "aapdhg_cuda_partition": ([C.POINTER(CsrView), C.c_int32, _ip, _ip], C.c_int),
+        "aapdhg_cuda_problem_create_dist": ([C.POINTER(ProblemView), C.c_int, C.POINTER(DistView),
+                                             C.POINTER(H)] + E, C.c_int),
         "aapdhg_cuda_last_launch_count": ([H, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
                                           C.c_int),
     }
@@ -166,6 +184,7 @@ CUDA_SYMBOLS = (
     "aapdhg_cuda_aa_apply", "aapdhg_cuda_filtered_aa_apply", "aapdhg_cuda_set_stream",
     "aapdhg_cuda_set_profiling",
     "aapdhg_cuda_kernel_times", "aapdhg_cuda_last_launch_count",
+    "aapdhg_cuda_nccl_id", "aapdhg_cuda_partition", "aapdhg_cuda_problem_create_dist",
 )
 
 _cuda_lib = None

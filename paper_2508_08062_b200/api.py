@@ -320,18 +320,72 @@ def safeguard_pass(g_norm: float, g0_norm: float, i: int, d: float, eps: float) 
     return g_norm <= d * g0_norm * math.pow(float(i) + 1.0, -(1.0 + eps))
 
 
+@dataclass
+class DistConfig:
+    """A sharded solve (include/aapdhg_cuda.h aapdhg_dist_view): `world`
+    row/column blocks of the LP. transport "nccl": this process is shard
+    `rank` on its own GPU, all ranks pass the same `nccl_id` (nccl_unique_id()
+    on rank 0, broadcast by the caller). "loopback": all shards in this
+    process on one device (exercises the partitioned path on one GPU)."""
+    world: int
+    rank: int = 0
+    transport: str = "nccl"
+    nccl_id: Optional[bytes] = None
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 of a sharded solve)."""
+    lib = _abi.cuda_lib()
+    buf = (C.c_uint8 * _abi.NCCL_ID_BYTES)()
+    err = errbuf()
+    check(lib.aapdhg_cuda_nccl_id(buf, len(buf), err, len(err)), err)
+    return bytes(buf)
+
+
+def partition(k: SparseMatrix, world: int):
+    """Row / column block bounds of a `world`-way sharded solve (host only)."""
+    lib = _abi.cuda_lib()
+    view = _abi.csr_view(k)
+    rows = np.zeros(world + 1, dtype=np.int32)
+    cols = np.zeros(world + 1, dtype=np.int32)
+    rc = lib.aapdhg_cuda_partition(C.byref(view), int(world), _abi.iptr(rows), _abi.iptr(cols))
+    if rc == _abi.ERR_UNSUPPORTED:
+        raise UnsupportedError("partition: every shard needs at least one row and one column")
+    if rc:
+        raise InputError("partition: bad arguments")
+    return rows, cols
+
+
 class Solver:
     """A problem resident in HBM (one device handle); reusable across solves
-    (the reference's sweep mode re-solves one ProblemData many times)."""
+    (the reference's sweep mode re-solves one ProblemData many times).
+    With `dist`, this process's part of a sharded multi-GPU solve: solve()
+    and select_step_sizes() are then collective over the ranks."""
 
-    def __init__(self, p: ProblemData, device: int = 0):
+    def __init__(self, p: ProblemData, device: int = 0, dist: Optional[DistConfig] = None):
         self.p = p
         self.lib = _abi.cuda_lib()
         self._view = _abi.problem_view(p)
         h = C.c_void_p()
         err = errbuf()
-        check(self.lib.aapdhg_cuda_problem_create(C.byref(self._view), int(device), C.byref(h),
-                                                   err, len(err)), err)
+        if dist is None:
+            check(self.lib.aapdhg_cuda_problem_create(C.byref(self._view), int(device),
+                                                       C.byref(h), err, len(err)), err)
+        else:
+            dv = _abi.DistView()
+            dv.rank = int(dist.rank)
+            dv.world = int(dist.world)
+            if dist.transport not in ("nccl", "loopback"):
+                raise InputError("dist: transport must be 'nccl' or 'loopback'")
+            dv.transport = _abi.DIST_NCCL if dist.transport == "nccl" else _abi.DIST_LOOPBACK
+            self._id = None
+            if dist.nccl_id is not None:
+                self._id = (C.c_uint8 * _abi.NCCL_ID_BYTES).from_buffer_copy(
+                    bytes(dist.nccl_id).ljust(_abi.NCCL_ID_BYTES, b"\0"))
+                dv.nccl_id = C.cast(self._id, C.POINTER(C.c_uint8))
+            check(self.lib.aapdhg_cuda_problem_create_dist(C.byref(self._view), int(device),
+                                                            C.byref(dv), C.byref(h), err,
+                                                            len(err)), err)
         self.h = h
 
     def close(self):

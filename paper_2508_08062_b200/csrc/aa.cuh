@@ -147,7 +147,9 @@ struct SolveScratch {
 // Success: S->aa_ok, weights and mix columns set, i += 1.
 // SingularError: plain step, j += 1, aa_failures += 1 (solver.cpp:229-235).
 __global__ void __launch_bounds__(1024)
-    k_aa_solve(DotBufs D, const DevParams* __restrict__ P, DevState* Sg, int per_op) {
+    k_aa_solve(DotBufs D, const DevParams* __restrict__ P, DevState* Sg, int per_op,
+               const double* __restrict__ rank_tot = nullptr, int nranks = 0,
+               int rank_stride = 0) {
   if (Sg->done || !Sg->aa_attempt) return;
   __shared__ DevState smS;
   state_load(&smS, Sg);
@@ -159,7 +161,13 @@ __global__ void __launch_bounds__(1024)
   const int p = S->mem_size;
   const int nit = num_items(p, P->method);
   __shared__ double vals[kMaxMemory * (kMaxMemory + 1) / 2 + 2 * kMaxMemory];
-  if (P->serial) {
+  if (rank_tot) {  // sharded: per-shard totals summed in rank order
+    for (int it = threadIdx.x; it < nit; it += blockDim.x) {
+      double s = rank_tot[it];
+      for (int r = 1; r < nranks; ++r) s = __dadd_rn(s, rank_tot[(int64_t)r * rank_stride + it]);
+      vals[it] = s;
+    }
+  } else if (P->serial) {
     for (int it = threadIdx.x; it < nit; it += blockDim.x) vals[it] = D.part[it];
   } else {
     // warp per item, lanes stride over the CTAs' partials, fixed tree
@@ -223,7 +231,7 @@ __global__ void __launch_bounds__(1024)
         R[j * p + i] = rjj > 0.0 ? s / rjj : 0.0;
       }
       const double fn = sqrt(G[gj * p + gj]);
-      const double sine = ((int64_t)j < P->N && fn > 0.0) ? rjj / fn : 0.0;
+      const double sine = ((int64_t)j < P->Nglob && fn > 0.0) ? rjj / fn : 0.0;
       keep[j] = 1;
       if (j == 0) {
         if (fn == 0.0) ok = false;  // zero leading column -> SingularError

@@ -7,13 +7,16 @@
 
 #include "aapdhg_cuda.h"
 #include "engine.h"
+#include "shard.h"
 
 using aapdhg_b200::CudaError;
 using aapdhg_b200::Problem;
+using aapdhg_b200::ShardGroup;
 using aapdhg_b200::StatusError;
 
 struct aapdhg_handle {
-  Problem* prob;
+  Problem* prob;      // whole-LP handle
+  ShardGroup* group;  // sharded handle (prob == nullptr)
 };
 
 namespace {
@@ -49,6 +52,13 @@ int need(const void* p, const char* what, char* err, size_t errlen) {
   return AAPDHG_ERR_INPUT;
 }
 
+// single-op entry points work on whole-LP handles only
+int whole(const aapdhg_handle* h, const char* what, char* err, size_t errlen) {
+  if (!h || !h->group) return AAPDHG_OK;
+  put_err(err, errlen, (std::string(what) + ": not available on a sharded handle").c_str());
+  return AAPDHG_ERR_UNSUPPORTED;
+}
+
 }  // namespace
 
 extern "C" {
@@ -72,8 +82,42 @@ int aapdhg_cuda_problem_create(const aapdhg_problem_view* prob, int device,
   if (int rc = need(out, "problem_create: null out", err, errlen)) return rc;
   *out = nullptr;
   return guard(err, errlen, [&] {
-    auto* h = new aapdhg_handle{new Problem(prob, device)};
+    auto* h = new aapdhg_handle{new Problem(prob, device), nullptr};
     *out = h;
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_problem_create_dist(const aapdhg_problem_view* prob, int device,
+                                    const aapdhg_dist_view* dist, aapdhg_handle** out,
+                                    char* err, size_t errlen) {
+  if (int rc = need(out, "problem_create_dist: null out", err, errlen)) return rc;
+  *out = nullptr;
+  return guard(err, errlen, [&] {
+    auto* h = new aapdhg_handle{nullptr, new ShardGroup(prob, device, dist)};
+    *out = h;
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_nccl_id(uint8_t* out, size_t len, char* err, size_t errlen) {
+  if (int rc = need(out, "nccl_id: null out", err, errlen)) return rc;
+  return guard(err, errlen, [&] {
+    aapdhg_b200::nccl_unique_id(out, len);
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_partition(const aapdhg_csr_view* k, int32_t world, int32_t* row_bounds,
+                          int32_t* col_bounds) {
+  if (!k || !row_bounds || !col_bounds || world < 1) return AAPDHG_ERR_INPUT;
+  if (world > k->nrows || world > k->ncols) return AAPDHG_ERR_UNSUPPORTED;
+  return guard(nullptr, 0, [&] {
+    const aapdhg_b200::Partition p = aapdhg_b200::plan_partition(*k, world);
+    for (int r = 0; r <= world; ++r) {
+      row_bounds[r] = p.rows[r];
+      col_bounds[r] = p.cols[r];
+    }
     return AAPDHG_OK;
   });
 }
@@ -81,6 +125,7 @@ int aapdhg_cuda_problem_create(const aapdhg_problem_view* prob, int device,
 int aapdhg_cuda_problem_destroy(aapdhg_handle* h) {
   if (!h) return AAPDHG_OK;
   delete h->prob;
+  delete h->group;
   delete h;
   return AAPDHG_OK;
 }
@@ -88,6 +133,13 @@ int aapdhg_cuda_problem_destroy(aapdhg_handle* h) {
 int aapdhg_cuda_problem_dims(const aapdhg_handle* h, int32_t* n, int32_t* m1, int32_t* m2,
                              int64_t* nnz) {
   if (!h) return AAPDHG_ERR_INPUT;
+  if (h->group) {
+    if (n) *n = h->group->n();
+    if (m1) *m1 = h->group->m1();
+    if (m2) *m2 = h->group->m() - h->group->m1();
+    if (nnz) *nnz = h->group->nnz();
+    return AAPDHG_OK;
+  }
   if (n) *n = h->prob->n();
   if (m1) *m1 = h->prob->m1();
   if (m2) *m2 = h->prob->m() - h->prob->m1();
@@ -103,7 +155,8 @@ int aapdhg_cuda_solve(aapdhg_handle* h, const aapdhg_solve_params* prm, const do
   if (int rc = need(prm, "solve: null params", err, errlen)) return rc;
   if (int rc = need(res, "solve: null result", err, errlen)) return rc;
   return guard(err, errlen, [&] {
-    h->prob->solve(prm, x0, y0, res, x_out, y_out, lambda_out, sink, ctx);
+    if (h->group) h->group->solve(prm, x0, y0, res, x_out, y_out, lambda_out, sink, ctx);
+    else h->prob->solve(prm, x0, y0, res, x_out, y_out, lambda_out, sink, ctx);
     return AAPDHG_OK;
   });
 }
@@ -114,7 +167,8 @@ int aapdhg_cuda_select_step_sizes(aapdhg_handle* h, const aapdhg_solve_params* p
                     err, errlen))
     return rc;
   return guard(err, errlen, [&] {
-    h->prob->select_step_sizes(prm, tau, sigma);
+    if (h->group) h->group->select_step_sizes(prm, tau, sigma);
+    else h->prob->select_step_sizes(prm, tau, sigma);
     return AAPDHG_OK;
   });
 }
@@ -122,6 +176,7 @@ int aapdhg_cuda_select_step_sizes(aapdhg_handle* h, const aapdhg_solve_params* p
 int aapdhg_cuda_power_norm(aapdhg_handle* h, int32_t max_iters, double rel_tol, uint64_t seed,
                            int32_t reduction, double* out, int32_t* rounds, char* err,
                            size_t errlen) {
+  if (int rc = whole(h, "power_norm", err, errlen)) return rc;
   if (int rc = need(h && out ? h : nullptr, "power_norm: null argument", err, errlen)) return rc;
   return guard(err, errlen, [&] {
     int r = 0;
@@ -136,6 +191,7 @@ int aapdhg_cuda_power_norm(aapdhg_handle* h, int32_t max_iters, double rel_tol, 
 
 int aapdhg_cuda_matvec(aapdhg_handle* h, const double* x, double* out, char* err,
                        size_t errlen) {
+  if (int rc = whole(h, "matvec", err, errlen)) return rc;
   if (int rc = need(h && out && (x || h->prob->n() == 0) ? h : nullptr, "matvec: null argument",
                     err, errlen))
     return rc;
@@ -147,6 +203,7 @@ int aapdhg_cuda_matvec(aapdhg_handle* h, const double* x, double* out, char* err
 
 int aapdhg_cuda_matvec_transpose(aapdhg_handle* h, const double* y, double* out, char* err,
                                  size_t errlen) {
+  if (int rc = whole(h, "matvec_transpose", err, errlen)) return rc;
   if (int rc = need(h && out ? h : nullptr, "matvec_transpose: null argument", err, errlen))
     return rc;
   return guard(err, errlen, [&] {
@@ -157,6 +214,7 @@ int aapdhg_cuda_matvec_transpose(aapdhg_handle* h, const double* y, double* out,
 
 int aapdhg_cuda_pdhg_step(aapdhg_handle* h, double tau, double sigma, const double* x,
                           const double* y, double* xn, double* yn, char* err, size_t errlen) {
+  if (int rc = whole(h, "pdhg_step", err, errlen)) return rc;
   if (int rc = need(h && xn && yn ? h : nullptr, "pdhg_step: null argument", err, errlen))
     return rc;
   return guard(err, errlen, [&] {
@@ -168,6 +226,7 @@ int aapdhg_cuda_pdhg_step(aapdhg_handle* h, double tau, double sigma, const doub
 int aapdhg_cuda_kkt_metrics(aapdhg_handle* h, int32_t reduction, const double* x,
                             const double* y, double* kkt, double* lambda, char* err,
                             size_t errlen) {
+  if (int rc = whole(h, "kkt_metrics", err, errlen)) return rc;
   if (int rc = need(h && kkt ? h : nullptr, "kkt_metrics: null argument", err, errlen)) return rc;
   return guard(err, errlen, [&] {
     h->prob->kkt_metrics(reduction, x, y, kkt, lambda);
@@ -179,6 +238,7 @@ int aapdhg_cuda_aa_apply(aapdhg_handle* h, int32_t reduction, int32_t p, const d
                          const double* dg_cols, double beta, const double* d_hat, double eta,
                          const double* u, const double* g, double* out, char* err,
                          size_t errlen) {
+  if (int rc = whole(h, "aa_apply", err, errlen)) return rc;
   if (int rc = need(h && u && g && out ? h : nullptr, "aa_apply: null argument", err, errlen))
     return rc;
   return guard(err, errlen, [&] {
@@ -194,6 +254,7 @@ int aapdhg_cuda_filtered_aa_apply(aapdhg_handle* h, int32_t reduction, int32_t p
                                   double kappa_bar, double beta, const double* d_hat,
                                   const double* u, const double* g, double* out,
                                   int32_t* kept, char* err, size_t errlen) {
+  if (int rc = whole(h, "filtered_aa_apply", err, errlen)) return rc;
   if (int rc = need(h && u && g && out ? h : nullptr, "filtered_aa_apply: null argument", err,
                     errlen))
     return rc;
@@ -208,13 +269,15 @@ int aapdhg_cuda_filtered_aa_apply(aapdhg_handle* h, int32_t reduction, int32_t p
 int aapdhg_cuda_set_stream(aapdhg_handle* h, void* stream) {
   if (!h) return AAPDHG_ERR_INPUT;
   return guard(nullptr, 0, [&] {
-    h->prob->set_stream(static_cast<cudaStream_t>(stream));
+    if (h->group) h->group->set_stream(static_cast<cudaStream_t>(stream));
+    else h->prob->set_stream(static_cast<cudaStream_t>(stream));
     return AAPDHG_OK;
   });
 }
 
 int aapdhg_cuda_set_profiling(aapdhg_handle* h, int32_t enable) {
   if (!h) return AAPDHG_ERR_INPUT;
+  if (h->group) return enable ? AAPDHG_ERR_UNSUPPORTED : AAPDHG_OK;
   h->prob->set_profiling(enable != 0);
   return AAPDHG_OK;
 }
@@ -222,6 +285,11 @@ int aapdhg_cuda_set_profiling(aapdhg_handle* h, int32_t enable) {
 int aapdhg_cuda_kernel_times(aapdhg_handle* h, char* names, size_t names_len, double* ms,
                              uint64_t* launches, int32_t cap, int32_t* count) {
   if (!h) return AAPDHG_ERR_INPUT;
+  if (h->group) {
+    if (count) *count = 0;
+    if (names && names_len) names[0] = '\0';
+    return AAPDHG_OK;
+  }
   const auto& st = h->prob->kernel_stats();
   std::string all;
   int k = 0;
@@ -242,8 +310,9 @@ int aapdhg_cuda_kernel_times(aapdhg_handle* h, char* names, size_t names_len, do
 int aapdhg_cuda_last_launch_count(aapdhg_handle* h, uint64_t* launches,
                                   uint64_t* loop_iterations) {
   if (!h) return AAPDHG_ERR_INPUT;
-  if (launches) *launches = h->prob->last_launches();
-  if (loop_iterations) *loop_iterations = h->prob->last_loop_iters();
+  if (launches) *launches = h->group ? h->group->last_launches() : h->prob->last_launches();
+  if (loop_iterations)
+    *loop_iterations = h->group ? h->group->last_loop_iters() : h->prob->last_loop_iters();
   return AAPDHG_OK;
 }
 

@@ -89,6 +89,14 @@ struct DevParams {
   int32_t nblk1, nblk2, ndot_blk, use_cond;
   cudaGraphConditionalHandle cond_aa;    // IF node of the AA branch
   cudaGraphConditionalHandle cond_loop;  // WHILE node of the iteration batch
+  // sharded solve (nullptr / 0 on a single GPU): K1 gathers y from the
+  // all-gathered ygather, K2 gathers xhat from xgather; K1 also writes xhat
+  // into this shard's chunk of xgather (xg_own) and keeps K'y in T.
+  const double* xgather;
+  const double* ygather;
+  double* xg_own;
+  int32_t store_T, pad_sh;
+  int64_t Nglob;  // n + m of the whole LP (FAA's QR row-count test)
 };
 
 // Mutable solver state, device resident; the host reads it at polls.

@@ -17,6 +17,7 @@
 #include "engine.h"
 #include "aa.cuh"
 #include "pipeline.cuh"
+#include "shard.cuh"
 
 namespace aapdhg_b200 {
 
@@ -219,7 +220,7 @@ size_t Problem::aa_smem(int cap) { return sizeof(double) * 2 * size_t(cap) * siz
 
 
 // ---------------------------------------------------------------------------
-Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
+void validate_problem_view(const aapdhg_problem_view* v) {
   if (!v) throw StatusError(AAPDHG_ERR_INPUT, "problem_create: null problem");
   const aapdhg_csr_view& k = v->k;
   if (k.nrows < 0 || k.ncols < 0 || k.nnz < 0)
@@ -239,7 +240,29 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   for (int64_t e = 0; e < k.nnz; ++e)
     if (k.col_idx[e] < 0 || k.col_idx[e] >= k.ncols)
       throw StatusError(AAPDHG_ERR_DIMENSION, "problem_create: column index out of range");
+}
 
+// K' as CSR with the entries of each row in ascending original row of K
+// (stable counting sort), the order matvec_transpose accumulates in
+// (sparse_linalg.cpp:77-87).
+void transpose_csr(const aapdhg_csr_view& k, std::vector<int32_t>& trp, std::vector<int32_t>& tci,
+                   std::vector<double>& tv) {
+  const int n = k.ncols, m = k.nrows;
+  trp.assign(static_cast<size_t>(n) + 1, 0);
+  tci.resize(static_cast<size_t>(k.nnz));
+  tv.resize(static_cast<size_t>(k.nnz));
+  for (int64_t e = 0; e < k.nnz; ++e) trp[size_t(k.col_idx[e]) + 1]++;
+  for (int j = 0; j < n; ++j) trp[j + 1] += trp[j];
+  std::vector<int32_t> next(trp.begin(), trp.end() - 1);
+  for (int r = 0; r < m; ++r)
+    for (int32_t e = k.row_ptr[r]; e < k.row_ptr[r + 1]; ++e) {
+      const int32_t pos = next[size_t(k.col_idx[e])]++;
+      tci[size_t(pos)] = r;
+      tv[size_t(pos)] = k.vals[e];
+    }
+}
+
+void Problem::init_device(int device) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw CudaError("no CUDA device available (the sm_100a path has no CPU fallback)");
@@ -251,47 +274,21 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
     throw CudaError(std::string("device ") + prop.name + " is not sm_100 class");
   AAPDHG_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
   stream_ = own_stream_;
-
-  n_ = k.ncols;
-  m_ = k.nrows;
-  m1_ = v->m1;
-  nnz_ = k.nnz;
-  N_ = int64_t(n_) + m_;
-  for (int64_t e = 0; e < nnz_ && all_zero_; ++e) all_zero_ = k.vals[e] == 0.0;
-
-  // K, padded so 16-byte cp.async of a tile's aligned superset stays in bounds
   AAPDHG_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device));
   pdl_ = env_int("AAPDHG_PDL", 1) != 0;
-  upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
-  // K' as CSR, entries of each row in ascending original row (counting sort)
-  std::vector<int32_t> trp(static_cast<size_t>(n_) + 1, 0), tci(static_cast<size_t>(nnz_));
-  std::vector<double> tv(static_cast<size_t>(nnz_));
-  for (int64_t e = 0; e < nnz_; ++e) trp[size_t(k.col_idx[e]) + 1]++;
-  for (int j = 0; j < n_; ++j) trp[j + 1] += trp[j];
-  {
-    std::vector<int32_t> next(trp.begin(), trp.end() - 1);
-    for (int r = 0; r < m_; ++r)
-      for (int32_t e = k.row_ptr[r]; e < k.row_ptr[r + 1]; ++e) {
-        const int32_t pos = next[size_t(k.col_idx[e])]++;
-        tci[size_t(pos)] = r;
-        tv[size_t(pos)] = k.vals[e];
-      }
-  }
-  upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_store_, KTs_, KTt_);
+}
 
+// c, q, l, u on the device plus the scratch of power iteration / per-op /
+// KKT evaluation.
+void Problem::init_vectors(const double* c, const double* q, const double* l, const double* u) {
   c_.reserve(sizeof(double) * n_);
   q_.reserve(sizeof(double) * m_);
   l_.reserve(sizeof(double) * n_);
   u_.reserve(sizeof(double) * n_);
-  h2d(c_.p, v->c, sizeof(double) * n_, stream_);
-  h2d(q_.p, v->q, sizeof(double) * m_, stream_);
-  h2d(l_.p, v->l, sizeof(double) * n_, stream_);
-  h2d(u_.p, v->u, sizeof(double) * n_, stream_);
-  bounds_ok_ = true;
-  for (int j = 0; j < n_; ++j)
-    if (v->l[j] > v->u[j]) bounds_ok_ = false;
-
-  // scratch for power iteration / per-op / KKT evaluation
+  h2d(c_.p, c, sizeof(double) * n_, stream_);
+  h2d(q_.p, q, sizeof(double) * m_, stream_);
+  h2d(l_.p, l, sizeof(double) * n_, stream_);
+  h2d(u_.p, u, sizeof(double) * n_, stream_);
   pw_x_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
   pw_mx_.reserve(sizeof(double) * std::max<int64_t>(m_, 1));
   pw_mtmx_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
@@ -304,6 +301,30 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   AAPDHG_CUDA(cudaMallocHost(&h_batch_, sizeof(int32_t)));
   AAPDHG_CUDA(cudaFuncSetAttribute(k_aa_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(aa_smem(kMaxMemory))));
+}
+
+Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
+  validate_problem_view(v);
+  const aapdhg_csr_view& k = v->k;
+  init_device(device);
+  n_ = k.ncols;
+  m_ = k.nrows;
+  m1_ = v->m1;
+  nnz_ = k.nnz;
+  N_ = int64_t(n_) + m_;
+  nglob_ = N_;
+  for (int64_t e = 0; e < nnz_ && all_zero_; ++e) all_zero_ = k.vals[e] == 0.0;
+
+  upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
+  std::vector<int32_t> trp, tci;
+  std::vector<double> tv;
+  transpose_csr(k, trp, tci, tv);
+  upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_store_, KTs_, KTt_);
+
+  bounds_ok_ = true;
+  for (int j = 0; j < n_; ++j)
+    if (v->l[j] > v->u[j]) bounds_ok_ = false;
+  init_vectors(v->c, v->q, v->l, v->u);
 
   // ||q|| and ||c|| under both reduction orders (constants of kkt_metrics)
   for (int serial = 0; serial < 2; ++serial) {
@@ -321,6 +342,7 @@ Problem::~Problem() {
   }
   if (h_state_) cudaFreeHost(h_state_);
   if (h_batch_) cudaFreeHost(h_batch_);
+  delete sh_su_;
   if (own_stream_) cudaStreamDestroy(own_stream_);
 }
 
@@ -607,7 +629,7 @@ void Problem::build_graph(const SolveSetup& su) {
 #undef LAUNCH
 
 // ---- step sizes -------------------------------------------------------------
-static void validate_config(const aapdhg_solve_params* c) {
+void validate_config(const aapdhg_solve_params* c) {
   // validate, solver.cpp:25-38 (same messages)
   const char* msg = nullptr;
   if (c->m < 1) msg = "solver: m must be >= 1";
@@ -741,6 +763,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.mrows = m_;
   P.cap = cap;
   P.N = N_;
+  P.Nglob = nglob_;
   P.safeguard_d = prm->safeguard_d;
   P.safeguard_eps = prm->safeguard_eps;
   P.beta = prm->beta;
@@ -942,6 +965,7 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   P.n = n_;
   P.mrows = m_;
   P.N = N_;
+  P.Nglob = nglob_;
   P.tau = tau;
   P.sigma = sigma;
   P.nblk1 = KTs_.grid();
@@ -1010,6 +1034,7 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
   P.mrows = m_;
   P.cap = std::max(p, 1);
   P.N = N_;
+  P.Nglob = nglob_;
   P.beta = beta;
   P.eta = eta;
   P.c_s = c_s;
@@ -1051,6 +1076,310 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
     for (int t = 0; t < h_state_->mix_p; ++t) kept[h_state_->mix_slots[t]] = 1;
   }
   return AAPDHG_OK;
+}
+
+// ===========================================================================
+// Sharded solve: one Problem per shard, phases driven in lockstep by
+// ShardGroup (shard.cu) with all-gathers in between (shard.cuh)
+// ===========================================================================
+
+Problem::Problem(const ShardSpec& sp, int device) : device_(device) {
+  init_device(device);
+  shard_rank_ = sp.rank;
+  n_ = sp.n_loc;
+  m_ = sp.m_loc;
+  m1_ = sp.m1_loc;
+  nnz_ = sp.k_rp.empty() ? 0 : sp.k_rp.back();
+  N_ = int64_t(n_) + m_;
+  nglob_ = sp.n_glob + sp.m_glob;
+  maxc_ = sp.maxc;
+  maxr_ = sp.maxr;
+  all_zero_ = sp.all_zero;
+  bounds_ok_ = sp.bounds_ok;
+  upload_csr(sp.k_rp.data(), sp.k_ci.data(), sp.k_v.data(), m_, int(sp.world * sp.maxc),
+             k_store_, Ks_, Kt_);
+  upload_csr(sp.t_rp.data(), sp.t_ci.data(), sp.t_v.data(), n_, int(sp.world * sp.maxr),
+             t_store_, KTs_, KTt_);
+  init_vectors(sp.c.data(), sp.q.data(), sp.l.data(), sp.u.data());
+  nrm_q_[0] = nrm_q_[1] = sp.nrm_q;
+  nrm_c_[0] = nrm_c_[1] = sp.nrm_c;
+  const int64_t W = sp.world;
+  xg_.reserve(sizeof(double) * W * maxc_);
+  yg_.reserve(sizeof(double) * W * maxr_);
+  lg_.reserve(sizeof(double) * W * maxc_);
+  scal_all_.reserve(sizeof(double) * W * 8);
+  AAPDHG_CUDA(cudaMemsetAsync(xg_.p, 0, xg_.bytes, stream_));
+  AAPDHG_CUDA(cudaMemsetAsync(yg_.p, 0, yg_.bytes, stream_));
+  AAPDHG_CUDA(cudaMemsetAsync(lg_.p, 0, lg_.bytes, stream_));
+  AAPDHG_CUDA(cudaMemsetAsync(scal_all_.p, 0, scal_all_.bytes, stream_));
+  shard_world_ = sp.world;
+  sync();
+}
+
+ShardBufs Problem::shard_bufs() const {
+  return ShardBufs{xg_.as<double>(), yg_.as<double>(), lg_.as<double>(), scal_all_.as<double>(),
+                   dots_all_.as<double>(), maxc_, maxr_, dot_stride_};
+}
+
+void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
+                       const double* x0, const double* y0, const double* d_hat,
+                       double wall_offset) {
+  AAPDHG_CUDA(cudaSetDevice(device_));
+  const int method = prm->method;
+  const int cap = method == AAPDHG_METHOD_PDHG ? 0 : int(prm->m);
+  ensure_iter_buffers(method, std::max(cap, 1));
+  dot_stride_ = num_items_host(std::max(cap, 1), AAPDHG_METHOD_FAA);
+  dots_all_.reserve(sizeof(double) * size_t(shard_world_) * size_t(dot_stride_));
+  if (d_hat) {
+    dhat_.reserve(sizeof(double) * std::max<int64_t>(N_, 1));
+    h2d(dhat_.p, d_hat, sizeof(double) * N_, stream_);
+  }
+  std::vector<double> ptab;
+  if (method != AAPDHG_METHOD_PDHG) {
+    const uint64_t len = std::min<uint64_t>(prm->max_iters + 1, kPowTabMax);
+    ptab.resize(len);
+    for (uint64_t i = 0; i < len; ++i) ptab[i] = std::pow(double(i) + 1.0, -(1.0 + prm->safeguard_eps));
+    pow_tab_.reserve(sizeof(double) * len);
+    h2d(pow_tab_.p, ptab.data(), sizeof(double) * len, stream_);
+  }
+  DevParams P{};
+  P.method = method;
+  P.serial = 0;
+  P.m1 = m1_;
+  P.kkt_terminate = prm->kkt_terminate ? 1 : 0;
+  P.n = n_;
+  P.mrows = m_;
+  P.cap = cap;
+  P.N = N_;
+  P.Nglob = nglob_;
+  P.safeguard_d = prm->safeguard_d;
+  P.safeguard_eps = prm->safeguard_eps;
+  P.beta = prm->beta;
+  P.eta = prm->eta;
+  P.c_s = prm->c_s;
+  P.kappa_bar = prm->kappa_bar;
+  P.toll = prm->toll;
+  P.kkt_eps = prm->kkt_eps;
+  P.tau = tau;
+  P.sigma = sigma;
+  P.max_iters = prm->max_iters;
+  P.max_wall_s = prm->max_wall_seconds;
+  P.wall_offset_s = wall_offset;
+  P.nrm_q = nrm_q_[1];
+  P.nrm_c = nrm_c_[1];
+  P.d_hat = d_hat ? dhat_.as<double>() : nullptr;
+  P.pow_tab = ptab.empty() ? nullptr : pow_tab_.as<double>();
+  P.pow_len = ptab.size();
+  P.rec = rec_.as<aapdhg_record>();
+  P.rec_cap = rec_cap_;
+  P.nblk1 = KTt_.grid();
+  P.nblk2 = Kt_.grid();
+  P.ndot_blk = ndot_tile_;
+  P.use_cond = 0;
+  P.xgather = xg_.as<double>();
+  P.ygather = yg_.as<double>();
+  P.xg_own = xg_.as<double>() + int64_t(shard_rank_) * maxc_;
+  P.store_T = 1;
+
+  DevState S0 = DevState{};
+  for (int r = 0; r < 4; ++r) S0.u_idx[r] = r;
+  for (int r = 0; r < 3; ++r) S0.kx_idx[r] = r;
+  S0.g_idx[0] = 0;
+  S0.g_idx[1] = 1;
+  DevState* S = dstate_.as<DevState>();
+
+  if (!sh_su_) sh_su_ = new SolveSetup{};
+  SolveSetup& su = *sh_su_;
+  su.B = iter_bufs();
+  su.B.nu1 = KTt_.grid();
+  su.B.fused_ctrl = 0;
+  su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
+                 partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
+  su.W = SolveScratch{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
+  su.P = dparams_.as<DevParams>();
+  su.S = S;
+  su.serial = false;
+  su.push = method != AAPDHG_METHOD_PDHG;
+  su.method = method;
+  su.cap = cap;
+  su.nblk1 = KTt_.grid();
+  su.nblk2 = Kt_.grid();
+  su.ndot_blk = ndot_tile_;
+  su.items_max = num_items_host(std::max(cap, 1), method);
+
+  AAPDHG_CUDA(cudaMemsetAsync(upool_.p, 0, sizeof(double) * 4 * N_, stream_));
+  if (method != AAPDHG_METHOD_PDHG)
+    AAPDHG_CUDA(cudaMemsetAsync(gpool_.p, 0, sizeof(double) * 2 * N_, stream_));
+  upload_iterate(0, x0, y0);
+  h2d(dparams_.p, &P, sizeof P, stream_);
+  h2d(S, &S0, sizeof S0, stream_);
+  k_project_start<<<grid_for(N_, kThreads, 1 << 30), kThreads, 0, stream_>>>(
+      upool_.as<double>(), l_.as<double>(), u_.as<double>(), n_, N_, m1_, S);
+  AAPDHG_CUDA(cudaGetLastError());
+  sh_launches_ = 1;
+}
+
+void Problem::sh_stage_x(int role, int mode) {
+  k_stage<<<grid_for(n_), kThreads, 0, stream_>>>(upool_.as<double>(), role, N_, 0, n_,
+                                                   xg_.as<double>() + shard_rank_ * maxc_,
+                                                   sh_su_->S, mode);
+  AAPDHG_CUDA(cudaGetLastError());
+  ++sh_launches_;
+}
+
+void Problem::sh_stage_y(int role, int mode) {
+  k_stage<<<grid_for(m_), kThreads, 0, stream_>>>(upool_.as<double>(), role, N_, n_, m_,
+                                                   yg_.as<double>() + shard_rank_ * maxr_,
+                                                   sh_su_->S, mode);
+  AAPDHG_CUDA(cudaGetLastError());
+  ++sh_launches_;
+}
+
+void Problem::sh_init_kx() {
+  sh_launches_ += spmv(stream_, Kt_, vref(xg_.as<double>()), rout(kxpool_.as<double>()), false,
+                       nullptr, 0, nullptr);
+}
+
+void Problem::sh_k1() {
+  const SolveSetup& su = *sh_su_;
+  if (su.push)
+    k_dual_side<false, true><<<KTt_.grid(), kThreads, 0, stream_>>>(KTt_, su.B, su.P, su.S);
+  else
+    k_dual_side<false, false><<<KTt_.grid(), kThreads, 0, stream_>>>(KTt_, su.B, su.P, su.S);
+  AAPDHG_CUDA(cudaGetLastError());
+  ++sh_launches_;
+}
+
+void Problem::sh_k2_totals() {
+  const SolveSetup& su = *sh_su_;
+  if (su.push)
+    k_primal_side<false, true><<<Kt_.grid(), kThreads, 0, stream_>>>(Kt_, su.B, su.P, su.S);
+  else
+    k_primal_side<false, false><<<Kt_.grid(), kThreads, 0, stream_>>>(Kt_, su.B, su.P, su.S);
+  k_local_totals<<<1, kThreads, 0, stream_>>>(part1_.as<double>(), KTt_.grid(),
+                                               part2_.as<double>(), Kt_.grid(), su.P, su.S,
+                                               scal_all_.as<double>() + shard_rank_ * 8);
+  AAPDHG_CUDA(cudaGetLastError());
+  sh_launches_ += 2;
+}
+
+void Problem::sh_control(int world) {
+  k_control_dist<<<1, 128, 0, stream_>>>(scal_all_.as<double>(), world, sh_su_->P, sh_su_->S);
+  AAPDHG_CUDA(cudaGetLastError());
+  ++sh_launches_;
+}
+
+void Problem::sh_read_state(DevState* out) {
+  d2h(h_state_, sh_su_->S, sizeof(DevState), stream_);
+  sync();
+  *out = *h_state_;
+}
+
+void Problem::sh_aa_dots() {
+  const SolveSetup& su = *sh_su_;
+  k_tree_dots<<<su.ndot_blk, kThreads, 0, stream_>>>(su.D, su.P, su.S);
+  k_dot_totals<<<1, 1024, 0, stream_>>>(su.D, su.P, su.S,
+                                         dots_all_.as<double>() + shard_rank_ * dot_stride_);
+  AAPDHG_CUDA(cudaGetLastError());
+  sh_launches_ += 2;
+}
+
+void Problem::sh_aa_solve_mix(int world) {
+  const SolveSetup& su = *sh_su_;
+  k_aa_solve<<<1, 1024, aa_smem(su.cap), stream_>>>(su.D, su.P, su.S, 0, dots_all_.as<double>(),
+                                                     world, int(dot_stride_));
+  k_mix<<<grid_for(N_), kThreads, 0, stream_>>>(su.B, su.B.dg, su.P, su.S, 1);
+  AAPDHG_CUDA(cudaGetLastError());
+  sh_launches_ += 2;
+  sh_stage_x(U_CAND, 2);
+}
+
+void Problem::sh_aa_recache_commit() {
+  const SolveSetup& su = *sh_su_;
+  RowsumArgs r{};
+  r.out_pool = su.B.kxpool;
+  r.out_role = KX_CAND;
+  r.out_stride = m_;
+  sh_launches_ += spmv(stream_, Kt_, vref(xg_.as<double>()), r, false, su.S, 1, nullptr);
+  k_aa_commit<<<1, 128, 0, stream_>>>(su.P, su.S);
+  AAPDHG_CUDA(cudaGetLastError());
+  ++sh_launches_;
+}
+
+void Problem::sh_lambda() {
+  k_lambda_from_T<<<grid_for(n_), kThreads, 0, stream_>>>(
+      T_.as<double>(), c_.as<double>(), l_.as<double>(), u_.as<double>(), n_,
+      lg_.as<double>() + shard_rank_ * maxc_);
+  AAPDHG_CUDA(cudaGetLastError());
+}
+
+void Problem::sh_records(uint64_t from, uint64_t cnt, aapdhg_record* out) {
+  const aapdhg_record* drec = rec_.as<aapdhg_record>();
+  uint64_t got = 0;
+  while (got < cnt) {
+    const uint64_t pos = (from + got) % rec_cap_;
+    const uint64_t chunk = std::min<uint64_t>(cnt - got, rec_cap_ - pos);
+    d2h(out + got, drec + pos, chunk * sizeof(aapdhg_record), stream_);
+    got += chunk;
+  }
+  sync();
+}
+
+// power_iteration_norm (sparse_linalg.cpp:95-123) phases of one shard
+void Problem::sh_pw_init(const double* x0_loc) {
+  AAPDHG_CUDA(cudaSetDevice(device_));
+  double* x = pw_x_.as<double>();
+  h2d(x, x0_loc, sizeof(double) * n_, stream_);
+  const int nb = grid_for(n_);
+  double* part = part_small_.as<double>();
+  k_sumsq_partials<<<nb, kThreads, 0, stream_>>>(x, nullptr, n_, part, nullptr);
+  k_dot_final<<<1, kCtrlThreads, 0, stream_>>>(x, nullptr, n_, part, nb, 0,
+                                                scal_all_.as<double>() + shard_rank_ * 8);
+  AAPDHG_CUDA(cudaGetLastError());
+}
+
+void Problem::sh_pw_div(double by) {
+  h2d(scal_.as<double>(), &by, sizeof(double), stream_);
+  k_scale<<<grid_for(n_), kThreads, 0, stream_>>>(pw_x_.as<double>(), pw_x_.as<double>(), n_,
+                                                   nullptr, scal_.as<double>());
+  AAPDHG_CUDA(cudaGetLastError());
+}
+
+void Problem::sh_pw_stage_x() {
+  AAPDHG_CUDA(cudaMemcpyAsync(xg_.as<double>() + shard_rank_ * maxc_, pw_x_.p,
+                              sizeof(double) * n_, cudaMemcpyDeviceToDevice, stream_));
+}
+
+void Problem::sh_pw_kx() {
+  spmv(stream_, Kt_, vref(xg_.as<double>()), rout(yg_.as<double>() + shard_rank_ * maxr_), false,
+       nullptr, 0, nullptr);
+}
+
+void Problem::sh_pw_ktkx() {
+  double* v = pw_mtmx_.as<double>();
+  spmv(stream_, KTt_, vref(yg_.as<double>()), rout(v), false, nullptr, 0, nullptr);
+  const int nb = grid_for(n_);
+  double* part = part_small_.as<double>();
+  k_sumsq_partials<<<nb, kThreads, 0, stream_>>>(v, nullptr, n_, part, nullptr);
+  k_dot_final<<<1, kCtrlThreads, 0, stream_>>>(v, nullptr, n_, part, nb, 0,
+                                                scal_all_.as<double>() + shard_rank_ * 8);
+  AAPDHG_CUDA(cudaGetLastError());
+}
+
+void Problem::sh_pw_update(double lam) {
+  h2d(scal_.as<double>() + 1, &lam, sizeof(double), stream_);
+  k_scale<<<grid_for(n_), kThreads, 0, stream_>>>(pw_x_.as<double>(), pw_mtmx_.as<double>(), n_,
+                                                   nullptr, scal_.as<double>() + 1);
+  AAPDHG_CUDA(cudaGetLastError());
+}
+
+double Problem::sh_read_scal(int world, int q) {
+  std::vector<double> v(size_t(world) * 8);
+  d2h(v.data(), scal_all_.p, sizeof(double) * v.size(), stream_);
+  sync();
+  double s = v[size_t(q)];
+  for (int r = 1; r < world; ++r) s += v[size_t(r) * 8 + q];
+  return s;
 }
 
 }  // namespace aapdhg_b200

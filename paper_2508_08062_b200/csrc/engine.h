@@ -29,10 +29,71 @@ struct KernelStat {
 
 struct SolveSetup;
 
+void validate_problem_view(const aapdhg_problem_view* v);
+void validate_config(const aapdhg_solve_params* c);
+void transpose_csr(const aapdhg_csr_view& k, std::vector<int32_t>& trp, std::vector<int32_t>& tci,
+                   std::vector<double>& tv);
+
+// One shard of a row/column-partitioned LP (shard.cuh): K's
+// rows R_r with column indices relabelled into the padded x all-gather
+// buffer, K's columns C_r (rows of K') with row indices relabelled into the
+// padded y buffer, and the local slices of c, l, u (C_r) and q (R_r).
+struct ShardSpec {
+  int rank = 0, world = 1;
+  int n_loc = 0, m_loc = 0, m1_loc = 0;
+  int64_t maxc = 0, maxr = 0;  // chunk lengths of the x / y all-gather buffers
+  int64_t n_glob = 0, m_glob = 0;
+  std::vector<int32_t> k_rp, k_ci, t_rp, t_ci;
+  std::vector<double> k_v, t_v;
+  std::vector<double> c, l, u, q;
+  double nrm_q = 0.0, nrm_c = 0.0;
+  bool all_zero = false, bounds_ok = true;
+};
+
+// Device buffers a shard exchanges with its peers: chunk r of each belongs
+// to shard r (all-gathered in place).
+struct ShardBufs {
+  double* xg;    // world x maxc: x-space vectors (xhat, candidates, power x)
+  double* yg;    // world x maxr: y-space vectors
+  double* lg;    // world x maxc: lambda of the final iterate
+  double* scal;  // world x 8: per-shard iteration totals / power-iteration norms
+  double* dots;  // world x dot_stride: per-shard AA dot totals
+  int64_t maxc, maxr, dot_stride;
+};
+
 class Problem {
  public:
   Problem(const aapdhg_problem_view* v, int device);
+  Problem(const ShardSpec& sp, int device);  // one shard of a sharded solve
   ~Problem();
+
+  // ---- sharded solve phases (driven by ShardGroup, in lockstep) -------------
+  ShardBufs shard_bufs() const;
+  cudaStream_t stream() const { return stream_; }
+  int device() const { return device_; }
+  int shard_rank() const { return shard_rank_; }
+  void sh_begin(const aapdhg_solve_params* prm, double tau, double sigma, const double* x0,
+                const double* y0, const double* d_hat, double wall_offset);
+  void sh_stage_x(int role, int mode);  // x-part of an iterate -> own chunk of xg
+  void sh_stage_y(int role, int mode);  // y-part -> own chunk of yg
+  void sh_init_kx();                    // K x of the start iterate (after AG of xg)
+  void sh_k1();                         // K'y + xhat (+ own chunk of xg)
+  void sh_k2_totals();                  // K xhat + yhat, then own iteration totals
+  void sh_control(int world);           // after AG of scal
+  void sh_read_state(DevState* out);    // synchronous
+  void sh_aa_dots();                    // own dot totals (AA attempt)
+  void sh_aa_solve_mix(int world);      // after AG of dots; candidate x -> xg
+  void sh_aa_recache_commit();          // after AG of xg
+  void sh_lambda();                     // lambda of the final iterate -> lg
+  void sh_records(uint64_t from, uint64_t cnt, aapdhg_record* out);
+  void sh_pw_init(const double* x0_loc);  // power x; own ||x||^2 -> scal
+  void sh_pw_div(double by);              // x /= by
+  void sh_pw_stage_x();                   // x -> own chunk of xg
+  void sh_pw_kx();                        // K xg -> own chunk of yg
+  void sh_pw_ktkx();                      // K' yg -> mtmx; own ||mtmx||^2 -> scal
+  void sh_pw_update(double lam);          // x = mtmx / lam
+  double sh_read_scal(int world, int q);  // rank-ordered sum of scal[r][q] (sync)
+  uint64_t sh_launches() const { return sh_launches_; }
 
   int n() const { return n_; }
   int m() const { return m_; }
@@ -84,6 +145,8 @@ class Problem {
   void upload_iterate(int slot, const double* x, const double* y);
   IterBufs iter_bufs();
 
+  void init_device(int device);
+  void init_vectors(const double* c, const double* q, const double* l, const double* u);
   void kkt_eval(int slot, bool serial, double* kkt_dev_out, double* lam_dev);
   int launch_core(cudaStream_t s, const SolveSetup& su);
   int launch_aa(cudaStream_t s, const SolveSetup& su);
@@ -112,7 +175,14 @@ class Problem {
   cudaStream_t stream_ = nullptr;
   cudaStream_t own_stream_ = nullptr;
   int n_ = 0, m_ = 0, m1_ = 0;
-  int64_t nnz_ = 0, N_ = 0;
+  int64_t nnz_ = 0, N_ = 0, nglob_ = 0;
+  // sharded solve
+  int shard_rank_ = -1;  // -1: a whole-LP handle
+  int shard_world_ = 1;
+  int64_t maxc_ = 0, maxr_ = 0, dot_stride_ = 0;
+  DevBuf xg_, yg_, lg_, scal_all_, dots_all_;
+  SolveSetup* sh_su_ = nullptr;
+  uint64_t sh_launches_ = 0;
   bool all_zero_ = true;
   bool bounds_ok_ = true;
   CsrDev Ks_, Kt_, KTs_, KTt_;  // SERIAL (sf = 1) and TREE layouts

@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 
 __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2,
                                            double bound, double qy, double cx, double infeas,
-                                           double dual_sq);
+                                           double dual_sq, double elapsed_in = -1.0);
 
 // Sums NQ rows of per-CTA partials (row q at part[q * nu]) in a fixed shape:
 // thread-strided in CTA order, warp xor tree, warps in order. Result in
@@ -402,13 +402,14 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
   double t;
-  const int j = row_sum<SERIAL>(KT, x + P->n, t);
+  const int j = row_sum<SERIAL>(KT, P->ygather ? P->ygather : x + P->n, t);
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
   if (j >= 0) {
     const double xj = x[j], cj = __ldg(B.c + j), lj = __ldg(B.l + j), uj = __ldg(B.u + j);
     double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));
     xn = smin(smax(xn, lj), uj);
     B.upool[(int64_t)S->u_idx[U_HAT] * N + j] = xn;
+    if (P->xg_own) P->xg_own[j] = xn;
     const double d = __dsub_rn(xn, xj);
     const double red_c = __dsub_rn(cj, t);
     const double lam = project_lambda1(red_c, lj, uj);
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
       B.dg[slot * N + j] = __dsub_rn(d, gp);
       B.gpool[(int64_t)S->g_idx[G_CUR] * N + j] = d;
     }
-    if (SERIAL) B.T[j] = t;
+    if (SERIAL || P->store_T) B.T[j] = t;
   }
   if (!SERIAL) {
     block_sum<P1_COUNT>(acc, red);
@@ -451,7 +452,8 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   const int64_t N = P->N;
   const int n = P->n, mr = P->mrows;
   double s;
-  const int i = row_sum<SERIAL>(K, B.upool + (int64_t)S->u_idx[U_HAT] * N, s);
+  const int i = row_sum<SERIAL>(
+      K, P->xgather ? P->xgather : B.upool + (int64_t)S->u_idx[U_HAT] * N, s);
   double acc[P2_COUNT] = {0.0, 0.0, 0.0};
   if (i >= 0) {
     const double yi = B.upool[(int64_t)S->u_idx[U_CUR] * N + n + i];
@@ -618,8 +620,9 @@ __device__ __forceinline__ void finish_solve(DevState* S, int status, int role, 
 
 // The scalar part of one iteration of solve() (solver.cpp:188-215,241-247),
 // run by a single thread after every sum of the iteration is known.
+// elapsed_in >= 0: the wall clock agreed by all shards (sharded solve)
 __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2, double bound, double qy,
-                              double cx, double infeas, double dual_sq) {
+                              double cx, double infeas, double dual_sq, double elapsed_in) {
   double kkt[4];
   kkt_from_sums(P->nrm_q, P->nrm_c, bound, qy, cx, infeas, dual_sq, kkt);
   for (int q = 0; q < 4; ++q) S->kkt[q] = kkt[q];
@@ -628,7 +631,9 @@ __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, doub
   S->aa_attempt = 0;
   S->aa_ok = 0;
   const uint64_t k = S->k;
-  const double elapsed = (double)(globaltimer_ns() - S->t0_ns) * 1e-9 + P->wall_offset_s;
+  const double elapsed = elapsed_in >= 0.0
+                             ? elapsed_in
+                             : (double)(globaltimer_ns() - S->t0_ns) * 1e-9 + P->wall_offset_s;
   bool attempt = false;
   do {
     if (k == 0) {  // priming step, solver.cpp:168-172

@@ -1,0 +1,106 @@
+// shard.cuh — kernels of the sharded (multi-GPU) solve.
+//
+// Layout: shard r owns a contiguous block R_r of K's rows
+// (its y, q, K x slices) and a block C_r of K's columns (its x, c, l, u
+// slices). It stores K[R_r, :] for K xhat and K[:, C_r]' (rows of K') for
+// (K'y)[C_r], with column indices relabelled into the padded all-gather
+// buffers (chunk r of xgather holds x[C_r], chunk r of ygather y[R_r]).
+// Every row sum is still the full CSR-ordered row of K or K', so the SpMVs
+// match the single-GPU ones bit for bit; only the scalar sums meet across
+// shards, in rank order. The control logic runs replicated on every shard
+// from identical all-gathered scalars, so all shards take the same branch.
+#pragma once
+
+#include "aa.cuh"
+
+namespace aapdhg_b200 {
+
+// dst[t] = (vector of role `role`, or of slot `-role - 1` when role < 0)
+// [off + t], t < len — into this shard's chunk of an all-gather buffer.
+// mode 0: always; 1: while the solve runs; 2: only after an accepted AA step.
+__global__ void k_stage(const double* __restrict__ upool, int role, int64_t N, int64_t off,
+                        int64_t len, double* __restrict__ dst, const DevState* S, int mode) {
+  if (mode >= 1 && S->done) return;
+  if (mode == 2 && !S->aa_ok) return;
+  const int r = role >= 0 ? S->u_idx[role] : -role - 1;
+  const double* src = upool + (int64_t)r * N + off;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < len;
+       t += (int64_t)gridDim.x * blockDim.x)
+    dst[t] = src[t];
+}
+
+// This shard's 7 partial sums of the iteration (K1 and K2 per-CTA partials
+// in CTA order) and its elapsed wall time, into own[0..8).
+__global__ void __launch_bounds__(kThreads)
+    k_local_totals(const double* __restrict__ part1, int nu1, const double* __restrict__ part2,
+                   int nu2, const DevParams* __restrict__ P, const DevState* S, double* own) {
+  if (S->done) return;
+  __shared__ double red[P1_COUNT * 32];
+  double t1[P1_COUNT], t2[P2_COUNT];
+  reduce_partial_rows<P1_COUNT>(part1, nu1, t1, red);
+  reduce_partial_rows<P2_COUNT>(part2, nu2, t2, red);
+  if (threadIdx.x == 0) {
+    if (nu1 == 0) t1[P1_GX2] = t1[P1_BOUND] = t1[P1_CX] = t1[P1_DUALSQ] = 0.0;
+    if (nu2 == 0) t2[P2_GY2] = t2[P2_QY] = t2[P2_INFEAS] = 0.0;
+    own[0] = t1[P1_GX2];
+    own[1] = t1[P1_BOUND];
+    own[2] = t1[P1_CX];
+    own[3] = t1[P1_DUALSQ];
+    own[4] = t2[P2_GY2];
+    own[5] = t2[P2_QY];
+    own[6] = t2[P2_INFEAS];
+    own[7] = (double)(globaltimer_ns() - S->t0_ns) * 1e-9 + P->wall_offset_s;
+  }
+}
+
+// Sums the all-gathered shard totals in rank order (elapsed: the maximum, so
+// a TIMEOUT is taken by every shard at the same iteration) and runs the
+// control logic.
+__global__ void __launch_bounds__(128)
+    k_control_dist(const double* __restrict__ all, int nranks, const DevParams* __restrict__ P,
+                   DevState* S) {
+  if (S->done) return;
+  __shared__ DevState sm;
+  __shared__ DevParams sp;
+  params_load(&sp, P);
+  state_load(&sm, S);
+  if (threadIdx.x == 0) {
+    double t[7];
+    double el = all[7];
+    for (int q = 0; q < 7; ++q) t[q] = all[q];
+    for (int r = 1; r < nranks; ++r) {
+      for (int q = 0; q < 7; ++q) t[q] = __dadd_rn(t[q], all[r * 8 + q]);
+      el = smax(el, all[r * 8 + 7]);
+    }
+    control_logic(&sp, &sm, __dadd_rn(t[0], t[4]), t[1], t[5], t[2], t[6], t[3], el);
+  }
+  state_store(S, &sm);
+}
+
+// This shard's Gram / rhs / column-norm partial dots (k_tree_dots per-CTA
+// partials, summed in CTA order like k_aa_solve does) into own[items].
+__global__ void __launch_bounds__(1024)
+    k_dot_totals(DotBufs D, const DevParams* __restrict__ P, const DevState* S, double* own) {
+  if (S->done || !S->aa_attempt) return;
+  const int nit = num_items(S->mem_size, P->method);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int it = warp; it < nit; it += nw) {
+    const double* pp = D.part + (int64_t)it * P->ndot_blk;
+    double s = 0.0;
+    for (int b = lane; b < P->ndot_blk; b += 32) s = __dadd_rn(s, pp[b]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) own[it] = s;
+  }
+}
+
+// lambda = P_Lambda(c - K'y) of the final iterate from the K'y kept by K1
+// (project_lambda, pdhg_core.cpp:27-39), into this shard's chunk.
+__global__ void k_lambda_from_T(const double* __restrict__ T, const double* __restrict__ c,
+                                const double* __restrict__ l, const double* __restrict__ u,
+                                int n, double* __restrict__ lam) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+    lam[t] = project_lambda1(__dsub_rn(c[t], T[t]), l[t], u[t]);
+}
+
+}  // namespace aapdhg_b200
