@@ -109,6 +109,16 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu --set full
+    capture (profiles/r01/traffic.json), or None."""
+    try:
+        d = json.loads((ROOT / "profiles" / "r01" / "traffic.json").read_text())[kernel]
+        return float(d["dram_read_bytes"] + d["dram_write_bytes"])
+    except Exception:
+        return None
+
+
 def kernel_bytes(p, name):
     """Algorithmic bytes per launch: CSR streams + compulsory
     gathers (each gathered element counted once) + vector reads/writes."""
@@ -166,6 +176,14 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def allreduce_max(tdist, torch, v, dev):
+    """max over ranks (NCCL wants device tensors, gloo host ones)"""
+    on = f"cuda:{dev}" if tdist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v)], dtype=torch.float64, device=on)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, rank, world, local_rank):
     import ctypes as C
 
@@ -177,12 +195,27 @@ def run_ours(args, rank, world, local_rank):
     dev = local_rank
     torch.cuda.set_device(dev)
     p = problems.make_config(CONFIG_ID)
-    dist = world > 1
+    dist = world > 1 or args.shard
     if dist:
         import torch.distributed as tdist
+        if not tdist.is_initialized():  # --shard at N=1
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            tdist.init_process_group("gloo", rank=0, world_size=1)
 
     stream = torch.cuda.Stream(device=dev)
-    s = Solver(p, device=dev)
+    if dist:
+        # sharded solve: rank r owns K's row block R_r and
+        # column block C_r; NCCL all-gathers between the phases
+        from paper_2508_08062_b200 import DistConfig, nccl_unique_id
+
+        def dcfg():  # a fresh NCCL id per communicator (ids are single-use)
+            box = [nccl_unique_id() if rank == 0 else None]
+            tdist.broadcast_object_list(box, src=0)
+            return DistConfig(world=world, rank=rank, transport="nccl", nccl_id=box[0])
+        s = Solver(p, device=dev, dist=dcfg())
+    else:
+        s = Solver(p, device=dev)
     lib = s.lib
     check(lib.aapdhg_cuda_set_stream(s.h, C.c_void_p(stream.cuda_stream)), errbuf())
     tau = s.select_step_sizes(solver_config()).tau
@@ -206,65 +239,32 @@ def run_ours(args, rank, world, local_rank):
     iters = out.result.iterations
     launches, loop_iters = C.c_uint64(), C.c_uint64()
     lib.aapdhg_cuda_last_launch_count(s.h, C.byref(launches), C.byref(loop_iters))
-    if dist:
-        t = torch.tensor([ms], device=f"cuda:{dev}")
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        ms = float(t.item())
-        tot = torch.tensor([float(iters)], device=f"cuda:{dev}")
-        tdist.all_reduce(tot, op=tdist.ReduceOp.SUM)
-        total_iters = float(tot.item())
-    else:
-        total_iters = float(iters)
+    if dist:  # one iteration is one unit of the whole (sharded) job
+        ms = allreduce_max(tdist, torch, ms, dev)
+    total_iters = float(iters)
     value = total_iters / (ms / 1e3)
 
     # ---- roofline of the dominant kernel: per-launch CUDA events -----------
-    lib.aapdhg_cuda_set_profiling(s.h, 1)
-    s.solve(solver_config(tau=tau, max_iters=min(args.steps, 400)))
-    names = C.create_string_buffer(4096)
-    msa = (C.c_double * 64)()
-    la = (C.c_uint64 * 64)()
-    cnt = C.c_int32()
-    lib.aapdhg_cuda_kernel_times(s.h, names, 4096, msa, la, 64, C.byref(cnt))
-    lib.aapdhg_cuda_set_profiling(s.h, 0)
-    kn = names.value.decode().split("\n")[: cnt.value]
-    kstats = {kn[i]: (msa[i], la[i]) for i in range(cnt.value)}
-    tot_ms = sum(v[0] for v in kstats.values())
-    dom = max((k for k in kstats if kernel_bytes(p, k)), key=lambda k: kstats[k][0])
-    avg_ms = kstats[dom][0] / kstats[dom][1]
-    peak, peak_kind = measured_peak()
-    achieved = kernel_bytes(p, dom) / (avg_ms / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": args.traffic, "bytes_per_launch": kernel_bytes(p, dom),
-                "avg_launch_us": avg_ms * 1e3,
-                "share_of_step": kstats[dom][0] / tot_ms if tot_ms else None,
-                "per_kernel_us": {k: 1e3 * v[0] / max(v[1], 1) for k, v in kstats.items()}}
+    roofline = None
+    if not dist:
+        roofline = kernel_roofline(args, p, s, lib, tau)
 
     # ---- time to tolerance (full solve to toll 1e-6, step sizes included) --
     ttt = None
     if not args.no_ttt:
-        t0 = time.perf_counter()
-        full = s.solve(solver_config(max_wall=args.ttt_cap))
-        ttt = {"seconds": time.perf_counter() - t0, "iterations": full.result.iterations,
-               "aa_steps": full.result.i, "status": full.result.status.name,
-               "objective": full.result.objective,
-               "planted_objective": getattr(p, "planted_objective", None),
-               "max_kkt": full.result.kkt.max()}
-        kk = full.trajectory
-        if kk.size:
-            mk = np.maximum(np.maximum(kk["r_gap"], kk["r_primal"]), kk["r_dual"])
-            hit = np.flatnonzero(mk <= 1e-6)
-            if hit.size:
-                ttt["first_kkt_le_1e-6"] = {"k": int(kk["k"][hit[0]]),
-                                            "elapsed_s": float(kk["elapsed_s"][hit[0]])}
+        ttt = time_to_tol(args, p, s)
     s.close()
 
     # ---- e2e: C-ABI call from host buffers (upload + solve + download) -----
     torch.cuda.synchronize(dev)
+    if dist:
+        tdist.barrier()
     t0 = time.perf_counter()
-    with Solver(p, device=dev) as s2:
+    with (Solver(p, device=dev, dist=dcfg()) if dist else Solver(p, device=dev)) as s2:
         out2 = s2.solve(solver_config(tau=tau, max_iters=args.steps))
     e2e_s = time.perf_counter() - t0
+    if dist:
+        e2e_s = allreduce_max(tdist, torch, e2e_s, dev)
     h2d = (p.k.row_ptr.nbytes + p.k.col_idx.nbytes + p.k.vals.nbytes + p.c.nbytes + p.q.nbytes
            + p.l.nbytes + p.u.nbytes)
     d2h = (p.n() * 16 + p.k.nrows * 8) + out2.trajectory.nbytes
@@ -285,15 +285,64 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / max(iters, 1),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong" if dist else "weak",
+                "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded planted-optimum generator, SURVEY.md 8(d))",
-                "config": dict(workload_config(p), parallelism=f"replicas{world}" if world > 1
-                               else "single"),
+                "config": dict(workload_config(p),
+                               parallelism=f"shard{world} (row/column blocks, NCCL all-gather)"
+                               if dist else "single"),
                 "iterations_timed": iters, "aa_steps_timed": out.result.i,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt,
                 "clocks": clk.summary(), "gpu_launches": int(launches.value),
                 "gpu_loop_iterations": int(loop_iters.value)}
         print(json.dumps(line), flush=True)
+
+
+def kernel_roofline(args, p, s, lib, tau):
+    import ctypes as C
+    lib.aapdhg_cuda_set_profiling(s.h, 1)
+    s.solve(solver_config(tau=tau, max_iters=min(args.steps, 400)))
+    names = C.create_string_buffer(4096)
+    msa = (C.c_double * 64)()
+    la = (C.c_uint64 * 64)()
+    cnt = C.c_int32()
+    lib.aapdhg_cuda_kernel_times(s.h, names, 4096, msa, la, 64, C.byref(cnt))
+    lib.aapdhg_cuda_set_profiling(s.h, 0)
+    kn = names.value.decode().split("\n")[: cnt.value]
+    kstats = {kn[i]: (msa[i], la[i]) for i in range(cnt.value)}
+    tot_ms = sum(v[0] for v in kstats.values())
+    dom = max((k for k in kstats if kernel_bytes(p, k)), key=lambda k: kstats[k][0])
+    avg_ms = kstats[dom][0] / kstats[dom][1]
+    peak, peak_kind = measured_peak()
+    achieved = kernel_bytes(p, dom) / (avg_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": args.traffic if args.traffic is not None else ncu_traffic(dom),
+                "traffic_source": "ncu --set full (profiles/r01/traffic.json), cold caches",
+                "bytes_per_launch": kernel_bytes(p, dom),
+                "avg_launch_us": avg_ms * 1e3,
+                "share_of_step": kstats[dom][0] / tot_ms if tot_ms else None,
+                "per_kernel_us": {k: 1e3 * v[0] / max(v[1], 1) for k, v in kstats.items()}}
+
+    return roofline
+
+
+def time_to_tol(args, p, s):
+    t0 = time.perf_counter()
+    full = s.solve(solver_config(max_wall=args.ttt_cap))
+    ttt = {"seconds": time.perf_counter() - t0, "iterations": full.result.iterations,
+           "aa_steps": full.result.i, "status": full.result.status.name,
+           "objective": full.result.objective,
+           "planted_objective": getattr(p, "planted_objective", None),
+           "max_kkt": full.result.kkt.max()}
+    kk = full.trajectory
+    if kk.size:
+        mk = np.maximum(np.maximum(kk["r_gap"], kk["r_primal"]), kk["r_dual"])
+        hit = np.flatnonzero(mk <= 1e-6)
+        if hit.size:
+            ttt["first_kkt_le_1e-6"] = {"k": int(kk["k"][hit[0]]),
+                                        "elapsed_s": float(kk["elapsed_s"][hit[0]])}
+    return ttt
 
 
 def main():
@@ -306,6 +355,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ttt", action="store_true")
     ap.add_argument("--ttt-cap", type=float, default=60.0)
+    ap.add_argument("--shard", action="store_true",
+                    help="use the sharded (NCCL) solve even at N=1 (exercises the N>1 path)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel, if captured")
     args = ap.parse_args()

@@ -384,6 +384,7 @@ void Problem::ensure_iter_buffers(int method, int cap) {
   T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
   part1_.reserve(sizeof(double) * P1_COUNT * std::max(nblk1, 1));
   part2_.reserve(sizeof(double) * P2_COUNT * std::max(nblk2, 1));
+
   gram_.reserve(sizeof(double) * kMaxMemory * kMaxMemory);
   work_.reserve(sizeof(double) * kMaxMemory * kMaxMemory);
   vec_.reserve(sizeof(double) * 8 * kMaxMemory);
@@ -542,7 +543,7 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   }
   if (ser) {
     LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
-  } else if (!su.B.fused_ctrl) {  // (otherwise k_primal_side's last CTA)
+  } else if (su.B.fused_ctrl != 1) {  // (otherwise k_primal_side's last CTA)
     LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), KTm(ser).grid(),
                                                             part2_.as<double>(), Km(ser).grid(),
                                                             su.P, su.S));
@@ -797,7 +798,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   SolveSetup su;
   su.B = iter_bufs();
   su.B.nu1 = n_ > 0 ? KTm(serial).grid() : 0;
-  su.B.fused_ctrl = (!serial && m_ > 0) ? 1 : 0;
+  su.B.fused_ctrl = (!serial && m_ > 0) ? env_int("AAPDHG_FUSED", 1) : 0;
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
                  partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
   su.W = SolveScratch{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};

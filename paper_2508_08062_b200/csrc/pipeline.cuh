@@ -1,33 +1,34 @@
 // pipeline.cuh — the per-iteration core of the sm_100a AA-PDHG solver.
 //
 // One iteration, evaluated at the current iterate u_k = (x, y):
-//   k_dual_side     K'y warp-tile SpMV fused with the primal step
+//   k_dual_side     K'y SpMV fused with the primal step
 //                   xhat = P_X(x - tau (c - K'y)) and the dual-side KKT terms
 //                   of u_k (lambda, bound terms, ||c - K'y - lambda||^2, c'x),
 //                   plus the x-half of the history push (du, dg, g)
 //                   — pdhg_core.cpp:49-53, solver.cpp:67-88,102-107,204-209
-//   k_primal_side   K xhat warp-tile SpMV fused with the dual step
+//   k_primal_side   K xhat SpMV fused with the dual step
 //                   yhat = P_Y(y + sigma (q - (2 K xhat - K x))) and the
 //                   primal-side KKT terms of u_k, plus the y-half of the push
 //                   — pdhg_core.cpp:55-60, solver.cpp:90-100
-//                   TREE mode: its last CTA reduces every partial sum and runs
-//                   the control logic (no extra launch).
+//                   TREE mode: its last CTA sums every partial and runs the
+//                   control logic (no launch of its own).
 //   k_serial_control SERIAL mode: all reductions as index-ordered chains, then
 //                   the control logic.
 // Control (solver.cpp:188-215,241-247): termination tests, trajectory
-// records, memory push commit, safeguard — and, under graph replay, sets the
-// IF condition of the AA branch.
+// records, memory push commit, safeguard — and, under graph replay, the
+// conditions of the AA branch and of the iteration loop.
 //
-// SpMV: CSR rows are grouped on the host into warp tiles of <= 32 rows and
-// <= kWarpTile nonzeros (a longer row is a tile of its own). A warp streams
-// its tile's (col, val) pairs coalesced, gathers x[col] through the read-only
-// path, stages the products in its own shared-memory slice, and lane r sums
-// row r sequentially in CSR order — bit-identical to the reference's
-// row-serial matvec (sparse_linalg.cpp:60-69) and, on the transposed CSR
-// (entries in ascending original row), to its row-ordered scatter
-// matvec_transpose (sparse_linalg.cpp:77-87). No CTA barrier sits between a
-// warp's loads and its sums, so warps stream independently; the epilogue
-// operands of a lane's row are prefetched before the tile's loads.
+// SpMV layout (SELL-32, built in engine.cu): rows in slices of 32 lanes;
+// element k of the row in lane r sits at sl_ptr[slice] + 32 k + r, so a
+// warp's loads of (col, val) are coalesced. One warp per slice, the slices
+// spread evenly over exactly one wave of CTAs. Each lane adds its row's
+// products in CSR order (split factor sf = 1): bit-identical to the
+// reference's row-serial matvec (sparse_linalg.cpp:60-69) and, on the
+// transposed CSR (entries in ascending original row), to its row-ordered
+// matvec_transpose (sparse_linalg.cpp:77-87). sf > 1 (TREE layout of a
+// matrix with few rows) splits a row over sf lanes joined by a fixed xor
+// tree. Rows longer than kLongRow get a warp each. No FMA anywhere
+// (-fmad=false, __dmul_rn / __dadd_rn).
 #pragma once
 
 #include "common.cuh"
@@ -233,11 +234,12 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     const int sl = int(int64_t(blockIdx.x) * A.nslices / A.nblk_short) + warp;
     if (sl >= int(int64_t(blockIdx.x + 1) * A.nslices / A.nblk_short)) return -1;
     const int sf = A.sf, j = lane & (sf - 1);
+    const int L = __ldg(A.sl_len + sl);
+    const int64_t sbase = __ldg(A.sl_ptr + sl);
     const int row = __ldg(A.sl_row + sl * 32 + lane);
     const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
     const int cnt = (len - j + sf - 1) / sf;  // this lane's elements
-    const int L = __ldg(A.sl_len + sl);
-    const int64_t base = __ldg(A.sl_ptr + sl) + lane;
+    const int64_t base = sbase + lane;
     const int32_t* __restrict__ cp = A.sci + base;
     const double* __restrict__ vp = A.sv + base;
     grid_dependency_wait();  // x may be the previous kernel's output (PDL)
@@ -313,7 +315,8 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 
 __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2,
                                            double bound, double qy, double cx, double infeas,
-                                           double dual_sq, double elapsed_in = -1.0);
+                                           double dual_sq, double elapsed_in = -1.0,
+                                           double pw_in = -1.0);
 
 // Sums NQ rows of per-CTA partials (row q at part[q * nu]) in a fixed shape:
 // thread-strided in CTA order, warp xor tree, warps in order. Result in
@@ -345,14 +348,46 @@ __device__ __forceinline__ void reduce_partial_rows(const double* part, int nu, 
     }
 }
 
-// Runs at the end of every k_primal_side CTA in TREE mode. CTA 0 first folds
-// K1's per-CTA partials (complete: K1 finished before K2 started) into
-// S->tot1 while the other CTAs still stream; the last CTA to finish (ticket
-// election, threadFenceReduction pattern) folds K2's partials and runs the
-// control logic on a shared-memory copy of the state. The sums are in CTA
-// order whichever CTA is last, so the result is deterministic.
+// Fused TREE-mode control of k_primal_side (threadFenceReduction pattern).
+// tail_prefetch() runs in every CTA right after its rows: cp.async copies of
+// the state, the parameters and the safeguard power (i+1)^-(1+eps) into
+// shared memory, landing while the CTA reduces and elects. CTA 0 folds K1's
+// per-CTA partials (complete: K1 finished before K2 started) into S->tot1.
+// The last CTA to finish (acq_rel ticket) then needs one round trip — the
+// K2 partials — before it runs the control logic on its shared copy. Sums
+// have a fixed shape whichever CTA is last: deterministic.
+struct TailSmem {
+  DevState st;
+  DevParams pr;
+  double pw;
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void tail_prefetch(TailSmem& ts, const DevParams* P,
+                                              const DevState* S) {
+  constexpr int WS = sizeof(DevState) / 8, WP = sizeof(DevParams) / 8;
+  static_assert(sizeof(DevState) % 8 == 0 && sizeof(DevParams) % 8 == 0, "8-byte copies");
+  for (int i = threadIdx.x; i < WS; i += blockDim.x)
+    cp_async8(reinterpret_cast<uint64_t*>(&ts.st) + i, reinterpret_cast<const uint64_t*>(S) + i);
+  for (int i = threadIdx.x; i < WP; i += blockDim.x)
+    cp_async8(reinterpret_cast<uint64_t*>(&ts.pr) + i, reinterpret_cast<const uint64_t*>(P) + i);
+  if (threadIdx.x == 0) {
+    // S->i is constant during K2; the table lookup of the safeguard
+    const uint64_t i = S->i;
+    if (P->pow_tab && i < P->pow_len) cp_async8(&ts.pw, P->pow_tab + i);
+    else ts.pw = -1.0;
+  }
+}
+
 __device__ __forceinline__ void fused_control_tail(const IterBufs& B, const DevParams* P,
-                                                   DevState* S) {
+                                                   DevState* S, TailSmem& ts) {
   __shared__ double red[P1_COUNT * 32];
   __shared__ int last;
   if (blockIdx.x == 0) {
@@ -363,25 +398,27 @@ __device__ __forceinline__ void fused_control_tail(const IterBufs& B, const DevP
       for (int q = 0; q < P1_COUNT; ++q) S->tot1[q] = B.nu1 > 0 ? t1[q] : 0.0;
   }
   if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(&S->ticket, 1u) == gridDim.x - 1;
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(prev) : "l"(&S->ticket) : "memory");
+    last = prev == gridDim.x - 1;
   }
   __syncthreads();
   if (!last) return;
-  __threadfence();
   double t2[P2_COUNT];
   reduce_partial_rows<P2_COUNT>(B.part2, gridDim.x, t2, red);
-  __shared__ DevState sm;
-  __shared__ DevParams sp;
-  params_load(&sp, P);
-  state_load(&sm, S);
+  cp_async_wait_all();
+  __syncthreads();
   if (threadIdx.x == 0) {
+    DevState& sm = ts.st;
     sm.ticket = 0;
-    const double* t1 = sm.tot1;
-    control_logic(&sp, &sm, __dadd_rn(t1[P1_GX2], t2[P2_GY2]), t1[P1_BOUND], t2[P2_QY],
-                  t1[P1_CX], t2[P2_INFEAS], t1[P1_DUALSQ]);
+    double t1[P1_COUNT];
+#pragma unroll
+    for (int q = 0; q < P1_COUNT; ++q) t1[q] = __ldcg(&S->tot1[q]);
+    control_logic(&ts.pr, &sm, __dadd_rn(t1[P1_GX2], t2[P2_GY2]), t1[P1_BOUND], t2[P2_QY],
+                  t1[P1_CX], t2[P2_INFEAS], t1[P1_DUALSQ], -1.0, ts.pw);
   }
-  state_store(S, &sm);
+  state_store(S, &ts.st);
 }
 
 // ---------------------------------------------------------------------------
@@ -480,11 +517,14 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     }
   }
   if (!SERIAL) {
+    __shared__ __align__(16) TailSmem ts;
+    if (B.fused_ctrl) tail_prefetch(ts, P, S);
     block_sum<P2_COUNT>(acc, red);
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
 #pragma unroll
       for (int q = 0; q < P2_COUNT; ++q) B.part2[q * gridDim.x + blockIdx.x] = acc[q];
-    if (B.fused_ctrl) fused_control_tail(B, P, S);
+    }
+    if (B.fused_ctrl) fused_control_tail(B, P, S, ts);
   }
 }
 
@@ -622,7 +662,8 @@ __device__ __forceinline__ void finish_solve(DevState* S, int status, int role, 
 // run by a single thread after every sum of the iteration is known.
 // elapsed_in >= 0: the wall clock agreed by all shards (sharded solve)
 __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2, double bound, double qy,
-                              double cx, double infeas, double dual_sq, double elapsed_in) {
+                              double cx, double infeas, double dual_sq, double elapsed_in,
+                              double pw_in) {
   double kkt[4];
   kkt_from_sums(P->nrm_q, P->nrm_c, bound, qy, cx, infeas, dual_sq, kkt);
   for (int q = 0; q < 4; ++q) S->kkt[q] = kkt[q];
@@ -678,7 +719,8 @@ __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, doub
     r->j = S->j;
     if (P->method != AAPDHG_METHOD_PDHG) {
       // safeguard_pass, solver.cpp:59-62, with the host std::pow table
-      const double pw = S->i < P->pow_len ? P->pow_tab[S->i]
+      const double pw = pw_in >= 0.0           ? pw_in
+                        : S->i < P->pow_len ? P->pow_tab[S->i]
                                           : pow((double)S->i + 1.0, -(1.0 + P->safeguard_eps));
       attempt = gkn <= __dmul_rn(__dmul_rn(P->safeguard_d, S->g0n), pw);
     }

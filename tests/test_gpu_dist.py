@@ -111,16 +111,19 @@ def test_loopback_pdhg_start_iterate_and_lambda():
 
 
 def test_nccl_world1_matches_one_gpu(cfg1):
-    """The NCCL transport with one rank: the real NCCL calls; sums in the same
-    order as the single-GPU TREE path, so the trajectory is bit-identical."""
+    """The NCCL transport with one rank: the real NCCL calls (the per-shard
+    totals are summed in another fixed order than the single-GPU fused
+    control, so agreement is to rounding)."""
     p, tau, ref = cfg1
     nid = nccl_unique_id()
     assert len(nid) == 128
     with Solver(p, dist=DistConfig(world=1, rank=0, transport="nccl", nccl_id=nid)) as s:
         got = s.solve(SolverConfig(method=Method.AA_PDHG, m=10, toll=1e-9, max_iters=60,
                                    tau=tau, sigma=tau, reduction="tree"))
-    assert np.array_equal(got.trajectory["g_norm"], ref.trajectory["g_norm"])
-    assert np.array_equal(got.result.u.x, ref.result.u.x)
+    assert got.result.iterations == ref.result.iterations
+    traj_close(got, ref, 60, 1e-10)
+    x, xr = got.result.u.x, ref.result.u.x
+    assert np.linalg.norm(x - xr) <= 1e-10 * np.linalg.norm(xr)
 
 
 def test_dist_errors():
