@@ -36,6 +36,7 @@ sys.path.insert(0, str(ROOT))
 CONFIG_ID = 1
 MEMORY = 10
 TOLL = 1e-6
+GATHER_CEILING = 240.3e9  # measured random-gather rate (profiles/r01/gather.txt)
 METRIC = "AA-PDHG fp64 iterations/sec (BASELINE configs[1]: 100k x 200k, 4M nnz, m=10)"
 
 
@@ -324,6 +325,20 @@ def kernel_roofline(args, p, s, lib, tau):
                 "share_of_step": kstats[dom][0] / tot_ms if tot_ms else None,
                 "per_kernel_us": {k: 1e3 * v[0] / max(v[1], 1) for k, v in kstats.items()}}
 
+    # the bound that actually binds: random 8-byte gathers of
+    # x[col], one per nonzero, against the measured B200 ceiling
+    gr = {}
+    for k in ("k_dual_side", "k_primal_side"):
+        if k in kstats:
+            us = 1e3 * kstats[k][0] / max(kstats[k][1], 1)
+            gr[k] = {"gathers_per_launch": int(p.k.nnz), "avg_launch_us": us,
+                     "achieved_gather_per_s": p.k.nnz / (us * 1e-6),
+                     "frac": p.k.nnz / (us * 1e-6) / GATHER_CEILING}
+    roofline["gather_roofline"] = {
+        "bound": "random 8-byte gathers (L1TEX sectors)", "ceiling_gather_per_s": GATHER_CEILING,
+        "ceiling_source": "profiles/r01/gather.txt: 4M random gathers from an L2-resident "
+                          "vector, 16.6 us on this pool's B200 (1.21 cycles/gather/SM)",
+        "kernels": gr}
     return roofline
 
 

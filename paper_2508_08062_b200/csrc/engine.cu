@@ -528,6 +528,10 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   if (n_ > 0) {
     if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
     else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (push && env_int("AAPDHG_K1VAR", 0) == 1) LAUNCH("k_dual_side", k_dual_side<false, true, 1><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (push && env_int("AAPDHG_K1VAR", 0) == 3) LAUNCH("k_dual_side", k_dual_side<false, true, 3><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (push && env_int("AAPDHG_K1VAR", 0) == 4) LAUNCH("k_dual_side", k_dual_side<false, true, 4><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    else if (push && env_int("AAPDHG_K1VAR", 0) == 2) LAUNCH("k_dual_side", k_dual_side<false, true, 2><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
     else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
     else LAUNCH("k_dual_side", k_dual_side<false, false><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
   }

@@ -203,6 +203,15 @@ __device__ __forceinline__ void advance(const DevParams* P, DevState* S) {
 
 constexpr int kUnroll = 4;
 
+// cp.async (LDGSTS): global -> shared without a register round trip
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 // Programmatic dependent launch (no-ops when the kernel was launched without
 // the attribute): a dependent kernel's CTAs may become resident while the
 // primary drains; they load their slice metadata, then wait here until the
@@ -225,7 +234,7 @@ __device__ __forceinline__ bool skip_launch(const DevState* S, int pred_aa_ok,
 
 // Sum of the row this lane owns in this CTA's work; returns the row (-1 if
 // none): the sum is valid in the owning lane only.
-template <bool SERIAL>
+template <bool SERIAL, int UNROLL = kUnroll, bool STAGE_V = false>
 __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, double& s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   s = 0.0;
@@ -244,20 +253,43 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     const double* __restrict__ vp = A.sv + base;
     grid_dependency_wait();  // x may be the previous kernel's output (PDL)
     double acc = 0.0;
-    for (int t0 = 0; t0 < L; t0 += kUnroll) {
-      int c[kUnroll];
-      double v[kUnroll];
+    if constexpr (STAGE_V) {
+      // values go global -> shared by cp.async (no registers held while the
+      // gathers are in flight): UNROLL gathers per lane in flight at the
+      // register cost of the column indices and the gathered values only
+      __shared__ double vst[kWarps * UNROLL * 32];
+      double* my = vst + warp * UNROLL * 32 + lane;
+      for (int t0 = 0; t0 < L; t0 += UNROLL) {
+        int c[UNROLL];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+        for (int u = 0; u < UNROLL; ++u) {
+          const bool on = t0 + u < cnt;
+          if (on) cp_async8(my + 32 * u, vp + 32 * (t0 + u));
+          c[u] = on ? __ldcs(cp + 32 * (t0 + u)) : 0;
+        }
+        double g[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) g[u] = t0 + u < cnt ? __ldg(x + c[u]) : 0.0;
+        cp_async_wait_all();
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+          if (t0 + u < cnt) acc = __dadd_rn(acc, __dmul_rn(my[32 * u], g[u]));
+      }
+    } else
+    for (int t0 = 0; t0 < L; t0 += UNROLL) {
+      int c[UNROLL];
+      double v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
         const bool on = t0 + u < cnt;
         c[u] = on ? __ldcs(cp + 32 * (t0 + u)) : 0;
         v[u] = on ? __ldcs(vp + 32 * (t0 + u)) : 0.0;
       }
-      double g[kUnroll];
+      double g[UNROLL];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) g[u] = t0 + u < cnt ? __ldg(x + c[u]) : 0.0;
+      for (int u = 0; u < UNROLL; ++u) g[u] = t0 + u < cnt ? __ldg(x + c[u]) : 0.0;
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
+      for (int u = 0; u < UNROLL; ++u)
         if (t0 + u < cnt) acc = __dadd_rn(acc, __dmul_rn(v[u], g[u]));
     }
     for (int off = sf >> 1; off > 0; off >>= 1)
@@ -362,13 +394,6 @@ struct TailSmem {
   double pw;
 };
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
 
 __device__ __forceinline__ void tail_prefetch(TailSmem& ts, const DevParams* P,
                                               const DevState* S) {
@@ -430,7 +455,7 @@ __device__ __forceinline__ void fused_control_tail(const IterBufs& B, const DevP
 //   lambda_j = P_Lambda(c_j - t)                           solver.cpp:67-71
 //   per-CTA partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
 //   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
-template <bool SERIAL, bool PUSH>
+template <bool SERIAL, bool PUSH, int VAR = 0>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   launch_dependents();  // k_primal_side may start its prologue (PDL)
@@ -439,8 +464,13 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
   double t;
-  const int j = row_sum<SERIAL>(KT, P->ygather ? P->ygather : x + P->n, t);
+  const int j = row_sum<SERIAL, (VAR == 1 || VAR == 3) ? 8 : (VAR == 4 ? 16 : kUnroll),
+                        (VAR >= 3)>(KT, P->ygather ? P->ygather : x + P->n, t);
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
+  if (VAR == 2) {  // experiment: SpMV only
+    if (j >= 0) B.T[j] = t;
+    return;
+  }
   if (j >= 0) {
     const double xj = x[j], cj = __ldg(B.c + j), lj = __ldg(B.l + j), uj = __ldg(B.u + j);
     double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));

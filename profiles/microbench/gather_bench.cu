@@ -54,6 +54,7 @@ __global__ void gather8(const double* __restrict__ x, const int* __restrict__ id
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc += v[u];
   }
+  for (; i < n; i += stride) acc += ld<MODE>(x + __ldcs(idx + i));  // remainder
   if (acc == 12345.0) out[0] = acc;
 }
 
