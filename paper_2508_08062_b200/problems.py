@@ -30,8 +30,11 @@ CONFIGS = {
 
 def _csr_from_coo(m, n, rows, cols, vals) -> SparseMatrix:
     """CSR with columns ascending in each row (entries distinct)."""
-    order = np.lexsort((cols, rows))
-    rows, cols, vals = rows[order], cols[order], vals[order]
+    key = rows.astype(np.int64) * np.int64(n) + cols.astype(np.int64)
+    if key.size > 1 and not bool(np.all(key[1:] > key[:-1])):
+        order = np.argsort(key, kind="stable")  # = lexsort((cols, rows)): keys distinct
+        rows, cols, vals = rows[order], cols[order], vals[order]
+    del key
     rp = np.zeros(m + 1, dtype=np.int64)
     np.cumsum(np.bincount(rows, minlength=m), out=rp[1:])
     return SparseMatrix(m, n, rp.astype(np.int32), cols.astype(np.int32), vals)
@@ -43,6 +46,19 @@ def _distinct_per_group(rng, groups: int, k, universe: int):
     total = int(k.sum())
     grp = np.repeat(np.arange(groups, dtype=np.int64), k)
     val = rng.integers(0, universe, size=total, dtype=np.int64)
+    if total and int(k.min()) == int(k.max()):
+        # equal group sizes: the same draws and redraws as the general loop
+        # below, sorting each group in place (groups are already contiguous)
+        w = int(k[0])
+        v = val.reshape(groups, w)
+        while True:
+            v.sort(axis=1)
+            dup = np.zeros_like(v, dtype=bool)
+            dup[:, 1:] = v[:, 1:] == v[:, :-1]
+            nd = int(dup.sum())
+            if nd == 0:
+                return grp, v.reshape(-1)
+            v[dup] = rng.integers(0, universe, size=nd, dtype=np.int64)
     while True:
         order = np.lexsort((val, grp))
         g2, v2 = grp[order], val[order]
