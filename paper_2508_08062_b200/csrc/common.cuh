@@ -38,6 +38,9 @@ enum { P1_GX2 = 0, P1_BOUND = 1, P1_DUALSQ = 2, P1_CX = 3, P1_COUNT = 4 };
 enum { P2_GY2 = 0, P2_QY = 1, P2_INFEAS = 2, P2_COUNT = 3 };
 // serial chain results (index into DevState::sres)
 enum { S_G2 = 0, S_BOUND = 1, S_QY = 2, S_CX = 3, S_INFEAS = 4, S_DUALSQ = 5, S_COUNT = 6 };
+constexpr int kSerThreads = 256;  // k_serial_control
+constexpr int kSerChunk = 1024;   // elements staged per pass
+constexpr size_t kSerSmem = sizeof(double) * S_COUNT * kSerChunk + kSerChunk;
 
 // A CSR matrix on the device in the layout the SpMV kernels stream:
 //   rp/ci/v        the CSR itself (row lengths; long rows read from here)

@@ -87,9 +87,23 @@ struct SolveSetup {
 // slice = 32 / sf rows; element k of the slice's row rho sits at
 // sl_ptr + 32 (k / sf) + rho sf + (k % sf).
 void Problem::build_sell(const int32_t* rp, const int32_t* ci, const double* v,
-                         const std::vector<int32_t>& shorts, int sf, SellStore& st,
+                         const std::vector<int32_t>& shorts_in, int sf, SellStore& st,
                          CsrDev& out) {
   const int R = 32 / sf;
+  // SELL-C-sigma: inside windows of one CTA's rows (sigma = 8 slices) the
+  // rows go by decreasing length, so a slice's lanes loop nearly equally
+  // often (ragged rows: Zipf lengths). Only the lane -> row map changes;
+  // every row is still summed in CSR order (bitwise unchanged).
+  std::vector<int32_t> shorts(shorts_in);
+  const int sigma = env_int("AAPDHG_SIGMA", kWarps * R);
+  if (sigma > 1)
+    for (size_t w0 = 0; w0 < shorts.size(); w0 += size_t(sigma)) {
+      const auto b = shorts.begin() + int64_t(w0);
+      const auto e = shorts.begin() + int64_t(std::min(shorts.size(), w0 + size_t(sigma)));
+      std::stable_sort(b, e, [&](int32_t a, int32_t c) {
+        return rp[a + 1] - rp[a] > rp[c + 1] - rp[c];
+      });
+    }
   const int nslices = int((shorts.size() + R - 1) / R);
   std::vector<int64_t> sl_ptr(size_t(std::max(nslices, 1)));
   std::vector<int32_t> sl_len(size_t(std::max(nslices, 1))),
@@ -162,6 +176,11 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
       short_nnz += len;
     }
   }
+  // longest rows first: their CTAs start first (longest-processing-time
+  // order) and each CTA's warps get rows of similar length
+  std::stable_sort(longs.begin(), longs.end(), [&](int32_t a, int32_t b) {
+    return rp[a + 1] - rp[a] > rp[b + 1] - rp[b];
+  });
   st.rp.reserve(sizeof(int32_t) * (nrows + 1));
   st.ci.reserve(sizeof(int32_t) * nnz);
   st.v.reserve(sizeof(double) * nnz);
@@ -301,6 +320,8 @@ void Problem::init_vectors(const double* c, const double* q, const double* l, co
   AAPDHG_CUDA(cudaMallocHost(&h_batch_, sizeof(int32_t)));
   AAPDHG_CUDA(cudaFuncSetAttribute(k_aa_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(aa_smem(kMaxMemory))));
+  AAPDHG_CUDA(cudaFuncSetAttribute(k_serial_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kSerSmem)));
 }
 
 Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
@@ -546,7 +567,7 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
     LAUNCH("k_primal_side", launch_ex(kern, g, dim3(kThreads), 0, s, pdl, Km(ser), su.B, su.P, su.S));
   }
   if (ser) {
-    LAUNCH("k_serial_control", k_serial_control<<<1, 32 * S_COUNT, 0, s>>>(su.B, su.P, su.S));
+    LAUNCH("k_serial_control", k_serial_control<<<1, kSerThreads, kSerSmem, s>>>(su.B, su.P, su.S));
   } else if (su.B.fused_ctrl != 1) {  // (otherwise k_primal_side's last CTA)
     LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), KTm(ser).grid(),
                                                             part2_.as<double>(), Km(ser).grid(),

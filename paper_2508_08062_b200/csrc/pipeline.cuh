@@ -238,10 +238,11 @@ template <bool SERIAL, int UNROLL = kUnroll, bool STAGE_V = false>
 __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, double& s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   s = 0.0;
-  if ((int)blockIdx.x < A.nblk_short) {
+  if ((int)blockIdx.x >= A.nblk_long) {
     // CTA b owns slices [b * ns / nblk, (b + 1) * ns / nblk): <= kWarps each
-    const int sl = int(int64_t(blockIdx.x) * A.nslices / A.nblk_short) + warp;
-    if (sl >= int(int64_t(blockIdx.x + 1) * A.nslices / A.nblk_short)) return -1;
+    const int b = int(blockIdx.x) - A.nblk_long;
+    const int sl = int(int64_t(b) * A.nslices / A.nblk_short) + warp;
+    if (sl >= int(int64_t(b + 1) * A.nslices / A.nblk_short)) return -1;
     const int sf = A.sf, j = lane & (sf - 1);
     const int L = __ldg(A.sl_len + sl);
     const int64_t sbase = __ldg(A.sl_ptr + sl);
@@ -297,7 +298,7 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     s = acc;
     return (row >= 0 && j == 0) ? row : -1;
   }
-  const int lr = (blockIdx.x - A.nblk_short) * kWarps + warp;
+  const int lr = blockIdx.x * kWarps + warp;  // long rows: the first CTAs
   if (lr >= A.nlong) return -1;
   const int row = __ldg(A.long_rows + lr);
   const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
@@ -593,7 +594,7 @@ __global__ void __launch_bounds__(kCtrlThreads)
 // (fixed_point_residual pdhg_core.cpp:65-74; kkt_metrics solver.cpp:64-110),
 // one warp per chain (lane 0 sums), then the control logic.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(32 * S_COUNT)
+__global__ void __launch_bounds__(kSerThreads)
     k_serial_control(IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) {
     if (threadIdx.x == 0 && P->use_cond) {
@@ -602,62 +603,72 @@ __global__ void __launch_bounds__(32 * S_COUNT)
     }
     return;
   }
+  // The elementwise terms of a chunk are formed by all threads into shared
+  // memory; one lane per quantity then adds them in index order, so the chain
+  // is only the dependent adds (the reference's loops, bit for bit).
+  extern __shared__ double terms[];                 // S_COUNT x kSerChunk
+  unsigned char* take = reinterpret_cast<unsigned char*>(terms + S_COUNT * kSerChunk);
   __shared__ double res[S_COUNT];
+  const int64_t N = P->N;
+  const int n = P->n, mr = P->mrows, m1 = P->m1;
+  const double* u = B.upool + (int64_t)S->u_idx[U_CUR] * N;
+  const double* uh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+  const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
+  const double* T = B.T;
   const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    const int64_t N = P->N;
-    const int n = P->n, mr = P->mrows, m1 = P->m1;
-    const double* u = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-    const double* uh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-    const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
-    const double* T = B.T;
-    double s = 0.0;
-    switch (w) {
-      case S_G2: {
-        int64_t i = 0;
-        for (; i + 8 <= N; i += 8) {
+  const bool chain = (threadIdx.x & 31) == 0 && w < S_COUNT;
+  const int64_t len = w == S_G2 ? N : (w == S_QY || w == S_INFEAS) ? mr : n;
+  double s = 0.0;
+  for (int64_t c0 = 0; c0 < N; c0 += kSerChunk) {
+    for (int t = threadIdx.x; t < kSerChunk; t += blockDim.x) {
+      const int64_t i = c0 + t;
+      if (i < N) {
+        const double d = __dsub_rn(uh[i], u[i]);
+        terms[S_G2 * kSerChunk + t] = __dmul_rn(d, d);
+      }
+      if (i < n) {  // pdhg_core.cpp:27-39 / solver.cpp:67-88,102-107
+        const double lj = B.l[i], uj = B.u[i], cj = B.c[i];
+        const double rc = __dsub_rn(cj, T[i]);
+        const double lam = project_lambda1(rc, lj, uj);
+        double bt = 0.0;
+        unsigned char tk = 0;
+        if (isfinite(lj) && lam > 0.0) { bt = __dmul_rn(lj, lam); tk = 1; }
+        if (isfinite(uj) && lam < 0.0) { bt = __dmul_rn(uj, lam); tk = 1; }
+        terms[S_BOUND * kSerChunk + t] = bt;
+        take[t] = tk;
+        terms[S_CX * kSerChunk + t] = __dmul_rn(cj, u[i]);
+        const double v = __dsub_rn(rc, lam);
+        terms[S_DUALSQ * kSerChunk + t] = __dmul_rn(v, v);
+      }
+      if (i < mr) {  // solver.cpp:90-100
+        terms[S_QY * kSerChunk + t] = __dmul_rn(B.q[i], u[n + i]);
+        double v = __dsub_rn(B.q[i], kx[i]);
+        if (i < m1) v = smax(v, 0.0);
+        terms[S_INFEAS * kSerChunk + t] = __dmul_rn(v, v);
+      }
+    }
+    __syncthreads();
+    if (chain && c0 < len) {
+      const int cnt = int(len - c0 < kSerChunk ? len - c0 : kSerChunk);
+      const double* tm = terms + w * kSerChunk;
+      if (w == S_BOUND) {
+        for (int k = 0; k < cnt; ++k)
+          if (take[k]) s = __dadd_rn(s, tm[k]);
+      } else {
+        int k = 0;
+        for (; k + 8 <= cnt; k += 8) {
           double p[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const double d = __dsub_rn(uh[i + k], u[i + k]);
-            p[k] = __dmul_rn(d, d);
-          }
+          for (int q = 0; q < 8; ++q) p[q] = tm[k + q];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) s = __dadd_rn(s, p[k]);
+          for (int q = 0; q < 8; ++q) s = __dadd_rn(s, p[q]);
         }
-        for (; i < N; ++i) {
-          const double d = __dsub_rn(uh[i], u[i]);
-          s = __dadd_rn(s, __dmul_rn(d, d));
-        }
-        break;
+        for (; k < cnt; ++k) s = __dadd_rn(s, tm[k]);
       }
-      case S_BOUND:
-        for (int j = 0; j < n; ++j) {
-          const double lj = B.l[j], uj = B.u[j];
-          const double lam = project_lambda1(__dsub_rn(B.c[j], T[j]), lj, uj);
-          if (isfinite(lj) && lam > 0.0) s = __dadd_rn(s, __dmul_rn(lj, lam));
-          if (isfinite(uj) && lam < 0.0) s = __dadd_rn(s, __dmul_rn(uj, lam));
-        }
-        break;
-      case S_QY: s = serial_dot(B.q, u + n, mr); break;
-      case S_CX: s = serial_dot(B.c, u, n); break;
-      case S_INFEAS:
-        for (int i = 0; i < mr; ++i) {
-          double v = __dsub_rn(B.q[i], kx[i]);
-          if (i < m1) v = smax(v, 0.0);
-          s = __dadd_rn(s, __dmul_rn(v, v));
-        }
-        break;
-      case S_DUALSQ:
-        for (int j = 0; j < n; ++j) {
-          const double rc = __dsub_rn(B.c[j], T[j]);
-          const double v = __dsub_rn(rc, project_lambda1(rc, B.l[j], B.u[j]));
-          s = __dadd_rn(s, __dmul_rn(v, v));
-        }
-        break;
     }
-    res[w] = s;
+    __syncthreads();
   }
+  if (chain) res[w] = s;
   __shared__ DevState sm;
   __shared__ DevParams sp;
   params_load(&sp, P);
