@@ -156,6 +156,8 @@ struct IterBufs {
   double* T;       // n
   double* part1;   // P1_COUNT x nblk1 (per CTA)
   double* part2;   // P2_COUNT x nblk2
+  const double* rinit1;  // L2-blocked K': partial K'y of the earlier column passes
+  const double* rinit2;  // L2-blocked K: partial K xhat of the earlier passes
   int32_t nu1;        // K1 CTAs (rows of part1)
   int32_t fused_ctrl; // TREE solve: k_primal_side's last CTA runs the control
   const double* c;

@@ -213,6 +213,65 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
   else build_sell(rp, ci, v, shorts, sf, st.sell[1], tree);
 }
 
+// L2 column blocking (TREE mode only). A matrix whose gathered vector is
+// larger than the L2 budget (AAPDHG_L2_BLOCK_KB, default 64 MB per block;
+// blocking starts above AAPDHG_L2_BLOCK_MIN_KB, default 64 MB) is split into column blocks; each block's
+// rows are the same rows restricted to its columns (CSR order kept), so a
+// pass gathers only from an L2-resident slice of the vector instead of one
+// DRAM sector per nonzero. Row sums become (((b0 + b1) + b2) + ...) — fixed
+// order, deterministic, not the CPU's association.
+void Problem::build_blocks(const int32_t* rp, const int32_t* ci, const double* v, int nrows,
+                           int ncols, Blocked& out) {
+  const int64_t kb = env_int("AAPDHG_L2_BLOCK_KB", 64 << 10);      // per block
+  const int64_t min_kb = env_int("AAPDHG_L2_BLOCK_MIN_KB", 64 << 10);  // start above
+  const int64_t vec_bytes = int64_t(ncols) * 8;
+  if (kb <= 0 || nrows == 0 || vec_bytes <= (min_kb << 10)) return;
+  const int64_t per = std::max<int64_t>((kb << 10) / 8, 1);
+  const int nb = int((int64_t(ncols) + per - 1) / per);
+  if (nb < 2) return;
+  const int64_t W = (int64_t(ncols) + nb - 1) / nb;
+  std::vector<int32_t> cur(rp, rp + nrows);  // per-row cursor (rows sorted by column)
+  std::vector<int32_t> brp(static_cast<size_t>(nrows) + 1);
+  std::vector<int32_t> bci;
+  std::vector<double> bv;
+  for (int b = 0; b < nb; ++b) {
+    const int64_t hi = std::min<int64_t>(int64_t(ncols), (b + 1) * W);
+    bci.clear();
+    bv.clear();
+    brp[0] = 0;
+    for (int r = 0; r < nrows; ++r) {
+      int32_t e = cur[r];
+      const int32_t end = rp[r + 1];
+      while (e < end && ci[e] < hi) {
+        bci.push_back(ci[e]);
+        bv.push_back(v[e]);
+        ++e;
+      }
+      cur[r] = e;
+      brp[r + 1] = int32_t(bci.size());
+    }
+    out.store.emplace_back(new CsrStore());
+    CsrDev ser, tree;
+    upload_csr(brp.data(), bci.data(), bv.data(), nrows, ncols, *out.store.back(), ser, tree);
+    out.blk.push_back(tree);
+  }
+  out.partial.reserve(sizeof(double) * size_t(nrows));
+}
+
+int Problem::launch_blocked_passes(cudaStream_t s, const Blocked& bk, const VecRef& x,
+                                   const DevState* S) {
+  int nodes = 0;
+  for (int b = 0; b + 1 < bk.nb(); ++b) {
+    prof_begin(s, "k_spmv_pass");
+    k_spmv_pass<<<bk.blk[b].grid(), kThreads, 0, s>>>(bk.blk[b], x, bk.partial.as<double>(),
+                                                     b == 0 ? 1 : 0, S);
+    prof_end(s);
+    AAPDHG_CUDA(cudaGetLastError());
+    ++nodes;
+  }
+  return nodes;
+}
+
 // out = A x (CSR-ordered row sums).
 int Problem::spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const RowsumArgs& o,
                   bool serial, const DevState* S, int pred, const int32_t* stop) {
@@ -341,6 +400,8 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   std::vector<double> tv;
   transpose_csr(k, trp, tci, tv);
   upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_store_, KTs_, KTt_);
+  build_blocks(k.row_ptr, k.col_idx, k.vals, m_, n_, kb_);
+  build_blocks(trp.data(), tci.data(), tv.data(), n_, m_, ktb_);
 
   bounds_ok_ = true;
   for (int j = 0; j < n_; ++j)
@@ -399,7 +460,9 @@ double Problem::device_dot(const double* a, const double* b, int64_t n, bool ser
 }
 
 void Problem::ensure_iter_buffers(int method, int cap) {
-  const int nblk1 = std::max(KTs_.grid(), KTt_.grid()), nblk2 = std::max(Ks_.grid(), Kt_.grid());
+  int nblk1 = std::max(KTs_.grid(), KTt_.grid()), nblk2 = std::max(Ks_.grid(), Kt_.grid());
+  for (const CsrDev& b : ktb_.blk) nblk1 = std::max(nblk1, b.grid());
+  for (const CsrDev& b : kb_.blk) nblk2 = std::max(nblk2, b.grid());
   upool_.reserve(sizeof(double) * 4 * std::max<int64_t>(N_, 1));
   kxpool_.reserve(sizeof(double) * 3 * std::max<int64_t>(m_, 1));
   T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
@@ -545,32 +608,41 @@ static void launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
 int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   int nodes = 0;
   const bool ser = su.serial, push = su.push;
+  // TREE with L2 column blocking: the earlier column passes first, the last
+  // block inside the fused kernel (rinit1 / rinit2 hold the partial sums)
+  const bool b1 = !ser && ktb_.nb() > 1, b2 = !ser && kb_.nb() > 1;
+  const CsrDev& K1m = b1 ? ktb_.blk.back() : KTm(ser);
+  const CsrDev& K2m = b2 ? kb_.blk.back() : Km(ser);
+  if (b1 && n_ > 0)
+    nodes += launch_blocked_passes(s, ktb_, VecRef{nullptr, su.B.upool, U_CUR, N_, n_}, su.S);
   // K'y: products of K' with y = u_cur[n:], then the fused dual-side rows
   if (n_ > 0) {
-    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else if (push && env_int("AAPDHG_K1VAR", 0) == 1) LAUNCH("k_dual_side", k_dual_side<false, true, 1><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else if (push && env_int("AAPDHG_K1VAR", 0) == 3) LAUNCH("k_dual_side", k_dual_side<false, true, 3><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else if (push && env_int("AAPDHG_K1VAR", 0) == 4) LAUNCH("k_dual_side", k_dual_side<false, true, 4><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else if (push && env_int("AAPDHG_K1VAR", 0) == 2) LAUNCH("k_dual_side", k_dual_side<false, true, 2><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
-    else LAUNCH("k_dual_side", k_dual_side<false, false><<<KTm(ser).grid(), kThreads, 0, s>>>(KTm(ser), su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
+    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
+    else if (push && env_int("AAPDHG_K1VAR", 0) == 1) LAUNCH("k_dual_side", k_dual_side<false, true, 1><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
+    else if (push && env_int("AAPDHG_K1VAR", 0) == 3) LAUNCH("k_dual_side", k_dual_side<false, true, 3><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
+    else if (push && env_int("AAPDHG_K1VAR", 0) == 4) LAUNCH("k_dual_side", k_dual_side<false, true, 4><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
+    else if (push && env_int("AAPDHG_K1VAR", 0) == 2) LAUNCH("k_dual_side", k_dual_side<false, true, 2><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
+    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
+    else LAUNCH("k_dual_side", k_dual_side<false, false><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
   }
+  if (b2 && m_ > 0)
+    nodes += launch_blocked_passes(s, kb_, VecRef{nullptr, su.B.upool, U_HAT, N_, 0}, su.S);
   // K xhat: products of K with xhat = u_hat[:n], then the fused dual step;
   // launched as a programmatic dependent of K1 (its CTAs load their slice
   // metadata while K1 drains, then wait for K1's xhat)
   if (m_ > 0) {
     const bool pdl = pdl_ && n_ > 0;
-    const dim3 g(Km(ser).grid());
+    const dim3 g(K2m.grid());
     auto kern = ser ? (push ? k_primal_side<true, true> : k_primal_side<true, false>)
                     : (push ? k_primal_side<false, true> : k_primal_side<false, false>);
-    LAUNCH("k_primal_side", launch_ex(kern, g, dim3(kThreads), 0, s, pdl, Km(ser), su.B, su.P, su.S));
+    LAUNCH("k_primal_side", launch_ex(kern, g, dim3(kThreads), 0, s, pdl, K2m, su.B, su.P, su.S));
   }
   if (ser) {
     LAUNCH("k_serial_control", k_serial_control<<<1, kSerThreads, kSerSmem, s>>>(su.B, su.P, su.S));
   } else if (su.B.fused_ctrl != 1) {  // (otherwise k_primal_side's last CTA)
-    LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), KTm(ser).grid(),
-                                                            part2_.as<double>(), Km(ser).grid(),
+    LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), K1m.grid(),
+                                                            part2_.as<double>(), K2m.grid(),
                                                             su.P, su.S));
   }
   AAPDHG_CUDA(cudaGetLastError());
@@ -809,8 +881,11 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.pow_len = ptab.size();
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
-  P.nblk1 = KTm(serial).grid();
-  P.nblk2 = Km(serial).grid();
+  const bool blk1 = !serial && ktb_.nb() > 1, blk2 = !serial && kb_.nb() > 1;
+  const CsrDev& K1m = blk1 ? ktb_.blk.back() : KTm(serial);
+  const CsrDev& K2m = blk2 ? kb_.blk.back() : Km(serial);
+  P.nblk1 = K1m.grid();
+  P.nblk2 = K2m.grid();
   P.ndot_blk = ndot_tile_;
 
   DevState S0{};
@@ -822,7 +897,9 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
 
   SolveSetup su;
   su.B = iter_bufs();
-  su.B.nu1 = n_ > 0 ? KTm(serial).grid() : 0;
+  su.B.nu1 = n_ > 0 ? K1m.grid() : 0;
+  su.B.rinit1 = blk1 ? ktb_.partial.as<double>() : nullptr;
+  su.B.rinit2 = blk2 ? kb_.partial.as<double>() : nullptr;
   su.B.fused_ctrl = (!serial && m_ > 0) ? env_int("AAPDHG_FUSED", 1) : 0;
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
                  partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
@@ -833,8 +910,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.push = method != AAPDHG_METHOD_PDHG;
   su.method = method;
   su.cap = cap;
-  su.nblk1 = KTm(serial).grid();
-  su.nblk2 = Km(serial).grid();
+  su.nblk1 = K1m.grid();
+  su.nblk2 = K2m.grid();
   su.ndot_blk = ndot_tile_;
   su.items_max = num_items_host(std::max(cap, 1), method);
 

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -187,6 +188,20 @@ class Problem {
   bool bounds_ok_ = true;
   CsrDev Ks_, Kt_, KTs_, KTt_;  // SERIAL (sf = 1) and TREE layouts
   CsrStore k_store_, t_store_;
+  // L2 column blocking (TREE mode) of a matrix whose gathered vector exceeds
+  // the L2 budget: the column blocks' CSRs, processed one pass each so the
+  // gathers of a pass hit an L2-resident slice of the vector
+  struct Blocked {
+    std::vector<CsrDev> blk;
+    std::vector<std::unique_ptr<CsrStore>> store;
+    DevBuf partial;  // row partial sums between passes
+    int nb() const { return int(blk.size()); }
+  };
+  Blocked kb_, ktb_;  // K (gathers xhat, n) and K' (gathers y, m)
+  void build_blocks(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
+                    Blocked& out);
+  int launch_blocked_passes(cudaStream_t s, const Blocked& bk, const VecRef& x,
+                            const DevState* S);
   size_t sell_bytes_ = 0;
   DevBuf c_, q_, l_, u_;
   double nrm_q_[2] = {0, 0}, nrm_c_[2] = {0, 0};  // [serial, tree]

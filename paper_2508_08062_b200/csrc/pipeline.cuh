@@ -447,6 +447,17 @@ __device__ __forceinline__ void fused_control_tail(const IterBufs& B, const DevP
   state_store(S, &ts.st);
 }
 
+// One column pass of an L2-blocked SpMV: part[row] (+)= the row's products
+// with the columns of this block (passes in block order: deterministic).
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+    k_spmv_pass(CsrDev A, VecRef xr, double* __restrict__ part, int first, const DevState* S) {
+  if (S && S->done) return;
+  const double* x = xr.get(S);
+  double s;
+  const int row = row_sum<false>(A, x, s);
+  if (row >= 0) part[row] = first ? s : __dadd_rn(part[row], s);
+}
+
 // ---------------------------------------------------------------------------
 // the fused PDHG halves
 // ---------------------------------------------------------------------------
@@ -465,8 +476,9 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
   double t;
-  const int j = row_sum<SERIAL, (VAR == 1 || VAR == 3) ? 8 : (VAR == 4 ? 16 : kUnroll),
-                        (VAR >= 3)>(KT, P->ygather ? P->ygather : x + P->n, t);
+  int j = row_sum<SERIAL, (VAR == 1 || VAR == 3) ? 8 : (VAR == 4 ? 16 : kUnroll),
+                  (VAR >= 3)>(KT, P->ygather ? P->ygather : x + P->n, t);
+  if (B.rinit1 && j >= 0) t = __dadd_rn(B.rinit1[j], t);  // earlier column passes
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
   if (VAR == 2) {  // experiment: SpMV only
     if (j >= 0) B.T[j] = t;
@@ -522,6 +534,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   double s;
   const int i = row_sum<SERIAL>(
       K, P->xgather ? P->xgather : B.upool + (int64_t)S->u_idx[U_HAT] * N, s);
+  if (B.rinit2 && i >= 0) s = __dadd_rn(B.rinit2[i], s);  // earlier column passes
   double acc[P2_COUNT] = {0.0, 0.0, 0.0};
   if (i >= 0) {
     const double yi = B.upool[(int64_t)S->u_idx[U_CUR] * N + n + i];

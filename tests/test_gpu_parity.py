@@ -321,3 +321,24 @@ def test_config3_zipf_rows(port, reduction):
     else:
         np.testing.assert_allclose(got.trajectory["g_norm"], ref.trajectory["g_norm"],
                                    rtol=1e-10)
+
+
+def test_l2_column_blocking_matches_unblocked(monkeypatch):
+    """TREE mode splits a matrix whose gathered vector exceeds the L2 budget
+    into column passes (engine.cu build_blocks). Forced on a small LP: the
+    trajectory matches the unblocked TREE solve to rounding (only the row sums
+    are re-associated, ((b0 + b1) + b2) ...)."""
+    p = problems.make_config(1, scale=0.05)
+    cfg = SolverConfig(method=Method.AA_PDHG, m=10, toll=1e-9, max_iters=60, tau=0.08,
+                       sigma=0.08, reduction="tree")
+    with Solver(p) as s:
+        ref = s.solve(cfg)
+    monkeypatch.setenv("AAPDHG_L2_BLOCK_MIN_KB", "0")
+    monkeypatch.setenv("AAPDHG_L2_BLOCK_KB", "16")  # 2048 columns per pass
+    with Solver(p) as s:
+        got = s.solve(cfg)
+    np.testing.assert_allclose(got.trajectory["g_norm"][:50], ref.trajectory["g_norm"][:50],
+                               rtol=1e-10)
+    assert np.array_equal(got.trajectory["aa_step"][:50], ref.trajectory["aa_step"][:50])
+    x, xr = got.result.u.x, ref.result.u.x
+    assert np.linalg.norm(x - xr) <= 1e-9 * np.linalg.norm(xr)
