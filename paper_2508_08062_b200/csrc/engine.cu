@@ -1203,6 +1203,9 @@ Problem::Problem(const ShardSpec& sp, int device) : device_(device) {
              k_store_, Ks_, Kt_);
   upload_csr(sp.t_rp.data(), sp.t_ci.data(), sp.t_v.data(), n_, int(sp.world * sp.maxr),
              t_store_, KTs_, KTt_);
+  // (relabelled indices stay ascending within a row: column blocks are in order)
+  build_blocks(sp.k_rp.data(), sp.k_ci.data(), sp.k_v.data(), m_, int(sp.world * sp.maxc), kb_);
+  build_blocks(sp.t_rp.data(), sp.t_ci.data(), sp.t_v.data(), n_, int(sp.world * sp.maxr), ktb_);
   init_vectors(sp.c.data(), sp.q.data(), sp.l.data(), sp.u.data());
   nrm_q_[0] = nrm_q_[1] = sp.nrm_q;
   nrm_c_[0] = nrm_c_[1] = sp.nrm_c;
@@ -1275,8 +1278,8 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   P.pow_len = ptab.size();
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
-  P.nblk1 = KTt_.grid();
-  P.nblk2 = Kt_.grid();
+  P.nblk1 = sh_k1m().grid();
+  P.nblk2 = sh_k2m().grid();
   P.ndot_blk = ndot_tile_;
   P.use_cond = 0;
   P.xgather = xg_.as<double>();
@@ -1294,8 +1297,10 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   if (!sh_su_) sh_su_ = new SolveSetup{};
   SolveSetup& su = *sh_su_;
   su.B = iter_bufs();
-  su.B.nu1 = KTt_.grid();
+  su.B.nu1 = sh_k1m().grid();
   su.B.fused_ctrl = 0;
+  su.B.rinit1 = ktb_.nb() > 1 ? ktb_.partial.as<double>() : nullptr;
+  su.B.rinit2 = kb_.nb() > 1 ? kb_.partial.as<double>() : nullptr;
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
                  partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
   su.W = SolveScratch{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
@@ -1305,8 +1310,8 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   su.push = method != AAPDHG_METHOD_PDHG;
   su.method = method;
   su.cap = cap;
-  su.nblk1 = KTt_.grid();
-  su.nblk2 = Kt_.grid();
+  su.nblk1 = sh_k1m().grid();
+  su.nblk2 = sh_k2m().grid();
   su.ndot_blk = ndot_tile_;
   su.items_max = num_items_host(std::max(cap, 1), method);
 
@@ -1345,22 +1350,26 @@ void Problem::sh_init_kx() {
 
 void Problem::sh_k1() {
   const SolveSetup& su = *sh_su_;
+  if (ktb_.nb() > 1) sh_launches_ += launch_blocked_passes(stream_, ktb_, vref(yg_.as<double>()), su.S);
+  const CsrDev& A = sh_k1m();
   if (su.push)
-    k_dual_side<false, true><<<KTt_.grid(), kThreads, 0, stream_>>>(KTt_, su.B, su.P, su.S);
+    k_dual_side<false, true><<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
   else
-    k_dual_side<false, false><<<KTt_.grid(), kThreads, 0, stream_>>>(KTt_, su.B, su.P, su.S);
+    k_dual_side<false, false><<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
   AAPDHG_CUDA(cudaGetLastError());
   ++sh_launches_;
 }
 
 void Problem::sh_k2_totals() {
   const SolveSetup& su = *sh_su_;
+  if (kb_.nb() > 1) sh_launches_ += launch_blocked_passes(stream_, kb_, vref(xg_.as<double>()), su.S);
+  const CsrDev& A = sh_k2m();
   if (su.push)
-    k_primal_side<false, true><<<Kt_.grid(), kThreads, 0, stream_>>>(Kt_, su.B, su.P, su.S);
+    k_primal_side<false, true><<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
   else
-    k_primal_side<false, false><<<Kt_.grid(), kThreads, 0, stream_>>>(Kt_, su.B, su.P, su.S);
-  k_local_totals<<<1, kThreads, 0, stream_>>>(part1_.as<double>(), KTt_.grid(),
-                                               part2_.as<double>(), Kt_.grid(), su.P, su.S,
+    k_primal_side<false, false><<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
+  k_local_totals<<<1, kThreads, 0, stream_>>>(part1_.as<double>(), sh_k1m().grid(),
+                                               part2_.as<double>(), A.grid(), su.P, su.S,
                                                scal_all_.as<double>() + shard_rank_ * 8);
   AAPDHG_CUDA(cudaGetLastError());
   sh_launches_ += 2;

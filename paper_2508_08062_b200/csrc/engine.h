@@ -141,6 +141,9 @@ class Problem {
   void upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
                   CsrStore& st, CsrDev& ser, CsrDev& tree);
   const CsrDev& Km(bool serial) const { return serial ? Ks_ : Kt_; }
+  // a shard's fused-kernel matrices: the last column block when blocked
+  const CsrDev& sh_k1m() const { return ktb_.nb() > 1 ? ktb_.blk.back() : KTt_; }
+  const CsrDev& sh_k2m() const { return kb_.nb() > 1 ? kb_.blk.back() : Kt_; }
   const CsrDev& KTm(bool serial) const { return serial ? KTs_ : KTt_; }
   void ensure_iter_buffers(int method, int cap);
   void upload_iterate(int slot, const double* x, const double* y);

@@ -141,3 +141,15 @@ def test_dist_errors():
                         type(s.select_step_sizes(SolverConfig()))(0.1, 0.1))
         with pytest.raises(InputError):
             s.solve(SolverConfig(m=0, method=Method.AA_PDHG))
+
+
+def test_loopback_with_l2_column_blocking(cfg1, monkeypatch):
+    """Shards also split their K / K' blocks into L2 column passes when the
+    gathered vector is large (forced here): same first iterates."""
+    p, tau, ref = cfg1
+    monkeypatch.setenv("AAPDHG_L2_BLOCK_MIN_KB", "0")
+    monkeypatch.setenv("AAPDHG_L2_BLOCK_KB", "16")
+    with Solver(p, dist=loopback(3)) as s:
+        got = s.solve(SolverConfig(method=Method.AA_PDHG, m=10, toll=1e-9, max_iters=60,
+                                   tau=tau, sigma=tau, reduction="tree"))
+    traj_close(got, ref, 50, 1e-10)
