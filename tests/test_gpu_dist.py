@@ -153,3 +153,42 @@ def test_loopback_with_l2_column_blocking(cfg1, monkeypatch):
         got = s.solve(SolverConfig(method=Method.AA_PDHG, m=10, toll=1e-9, max_iters=60,
                                    tau=tau, sigma=tau, reduction="tree"))
     traj_close(got, ref, 50, 1e-10)
+
+
+def test_loopback_inequality_rows_and_general_bounds():
+    """Inequality rows (m1 > 0) split across shards (each shard projects its
+    own leading block of them) and general bounds: free, negative lower and
+    finite upper — the lambda set and bound terms of kkt_metrics."""
+    from paper_2508_08062_b200 import ProblemData
+    base = problems.make_config(0, scale=0.3)
+    rng = np.random.default_rng(3)
+    n = base.n()
+    l = np.where(rng.random(n) < 0.3, -np.inf, np.where(rng.random(n) < 0.5, -1.0, 0.0))
+    u = np.where(rng.random(n) < 0.4, 2.0, np.inf)
+    p = ProblemData(base.k, base.k.nrows // 2 + 7, base.c, base.q, l, u, name="mixed")
+    cfg = SolverConfig(method=Method.AA_PDHG, m=5, toll=1e-9, max_iters=60, tau=0.05, sigma=0.05,
+                       reduction="tree")
+    with Solver(p) as s:
+        ref = s.solve(cfg)
+    for world in (2, 3):
+        with Solver(p, dist=loopback(world)) as s:
+            got = s.solve(cfg)
+        traj_close(got, ref, 50, 1e-10)
+        for f in ("r_gap", "r_primal", "r_dual"):
+            np.testing.assert_allclose(got.trajectory[f][:50], ref.trajectory[f][:50], rtol=1e-9,
+                                       atol=1e-14)
+        np.testing.assert_allclose(got.result.lambda_, ref.result.lambda_, rtol=1e-8, atol=1e-12)
+
+
+def test_loopback_setcover_faa():
+    """The reference's set-cover generator (all rows inequalities, finite
+    upper bounds), FAA with its default filter, on 3 shards."""
+    from golden_io import problem
+    p = problem("setcover")
+    cfg = SolverConfig(method=Method.FAA_PDHG, m=5, toll=1e-9, max_iters=60, tau=0.1, sigma=0.1,
+                       reduction="tree")
+    with Solver(p) as s:
+        ref = s.solve(cfg)
+    with Solver(p, dist=loopback(3)) as s:
+        got = s.solve(cfg)
+    traj_close(got, ref, 40, 1e-8)
