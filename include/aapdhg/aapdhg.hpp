@@ -248,6 +248,32 @@ class DeviceProblem {
   void* h_ = nullptr;
 };
 
+// ---- sweep mode ---------------------------------------------------------------
+// The CLI's --sweep-D/--sweep-eps/--sweep-m/--sweep-kappa-bar cross product
+// (proj/src/cli.cpp:155-180), with the same case names ("D0.5_eps1_m10" ...).
+struct SweepCase {
+  SolverConfig cfg;
+  std::string name;
+};
+std::vector<SweepCase> sweep_cases(const SolverConfig& base, const std::vector<double>& d,
+                                   const std::vector<double>& eps,
+                                   const std::vector<std::size_t>& m,
+                                   const std::vector<double>& kappa_bar);
+
+struct SweepOutcome {
+  bool ok = false;
+  std::string error;   // the exception message when !ok
+  SolveOutput output;  // valid when ok
+};
+// Runs the cases on `workers` threads (cli.cpp:184-209: AAPDHG_SWEEP_WORKERS
+// when workers == 0). Each worker keeps one DeviceProblem resident on its
+// device (devices are assigned round-robin; several workers per GPU run
+// concurrently on their own streams — small LPs leave a GPU mostly idle) and
+// takes cases from a shared counter. Outcomes are in case order.
+std::vector<SweepOutcome> solve_sweep(const ProblemData& p, const std::vector<SweepCase>& cases,
+                                      std::size_t workers = 0,
+                                      const std::vector<int>& devices = {0});
+
 // ---- report ------------------------------------------------------------------
 const char* status_name(SolveStatus s);
 const char* method_name(Method m);

@@ -8,11 +8,12 @@ from .api import (AAParams, CudaError, DimensionError, DistConfig, Error, Filter
                   InputError, Iterate, KktMetrics, Method, ProblemData, SingularError,
                   SolveOutput, SolveResult, SolveStatus, Solver, SolverConfig, SparseMatrix,
                   StepSizes, UnsupportedError, kkt_metrics, nccl_unique_id, partition,
-                  safeguard_pass, select_step_sizes, solve, vstack)
+                  safeguard_pass, select_step_sizes, solve, solve_sweep, sweep_cases,
+                  SweepCase, vstack)
 
 __all__ = [
     "AAParams", "CudaError", "DimensionError", "DistConfig", "Error", "FilterParams", "InputError", "Iterate",
     "KktMetrics", "Method", "ProblemData", "SingularError", "SolveOutput", "SolveResult",
     "SolveStatus", "Solver", "SolverConfig", "SparseMatrix", "StepSizes", "UnsupportedError",
-    "kkt_metrics", "nccl_unique_id", "partition", "safeguard_pass", "select_step_sizes", "solve", "vstack",
+    "kkt_metrics", "nccl_unique_id", "partition", "safeguard_pass", "select_step_sizes", "solve", "solve_sweep", "sweep_cases", "SweepCase", "vstack",
 ]

@@ -458,6 +458,89 @@ class Solver:
         return Iterate(xn, yn)
 
 
+@dataclass
+class SweepCase:
+    cfg: SolverConfig
+    name: str
+
+
+def sweep_cases(base: SolverConfig, d=(), eps=(), m=(), kappa_bar=()) -> list:
+    """The CLI's --sweep-D/--sweep-eps/--sweep-m/--sweep-kappa-bar cross
+    product with its case names (proj/src/cli.cpp:155-180)."""
+    import copy
+    out = []
+    for vd in (d or [None]):
+        for ve in (eps or [None]):
+            for vm in (m or [None]):
+                for vk in (kappa_bar or [None]):
+                    c = copy.deepcopy(base)
+                    parts = []
+                    if vd is not None:
+                        c.safeguard_d = vd
+                        parts.append("D%g" % vd)
+                    if ve is not None:
+                        c.safeguard_eps = ve
+                        parts.append("eps%g" % ve)
+                    if vm is not None:
+                        c.m = int(vm)
+                        parts.append("m%d" % int(vm))
+                    if vk is not None:
+                        c.filter = FilterParams(c_s=c.filter.c_s, kappa_bar=vk)
+                        parts.append("kappa%g" % vk)
+                    out.append(SweepCase(c, "_".join(parts)))
+    return out
+
+
+def solve_sweep(p: ProblemData, cases, workers: int = 0, devices=(0,)) -> list:
+    """Sweep mode (proj/src/cli.cpp:184-209): the cases on `workers` threads
+    (AAPDHG_SWEEP_WORKERS when 0), each keeping one resident handle on its
+    device (round-robin) and taking cases from a shared counter; several
+    workers per GPU run concurrently on their own streams. Returns
+    (ok, error, SolveOutput | None) per case, in case order."""
+    import itertools
+    import os
+    import threading
+    cases = list(cases)
+    if not devices:
+        raise InputError("solve_sweep: no devices")
+    if workers <= 0:
+        workers = max(1, int(os.environ.get("AAPDHG_SWEEP_WORKERS", "1") or 1))
+    workers = max(1, min(workers, len(cases)))
+    out = [None] * len(cases)
+    counter = itertools.count()
+    lock = threading.Lock()
+
+    def work(w):
+        try:
+            s = Solver(p, devices[w % len(devices)])
+        except Error as e:
+            s, err = None, str(e)
+        try:
+            while True:
+                with lock:
+                    idx = next(counter)
+                if idx >= len(cases):
+                    return
+                if s is None:
+                    out[idx] = (False, err, None)
+                    continue
+                c = cases[idx].cfg if isinstance(cases[idx], SweepCase) else cases[idx]
+                try:
+                    out[idx] = (True, "", s.solve(c))
+                except Error as e:
+                    out[idx] = (False, str(e), None)
+        finally:
+            if s is not None:
+                s.close()
+
+    threads = [threading.Thread(target=work, args=(w,)) for w in range(workers)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    return out
+
+
 def solve(p: ProblemData, cfg: SolverConfig, u0: Optional[Iterate] = None,
           device: int = 0) -> SolveOutput:
     """solve(p, cfg[, u0]) — proj/include/aapdhg/solver.hpp:93-99."""

@@ -156,6 +156,26 @@ int main() {
     threw = true;
   }
   put("input_error_thrown", threw ? "true" : "false");
+
+  // 7. sweep mode (cli.cpp:142-214): D x m cross product on 3 workers, each
+  // outcome equal to the same case solved alone
+  SolverConfig sb;
+  sb.method = Method::kAaPdhg;
+  sb.toll = 1e-4;
+  sb.tau = sb.sigma = 0.25;
+  const std::vector<SweepCase> cases = sweep_cases(sb, {1.0, 1e-300}, {}, {2, 5}, {});
+  const std::vector<SweepOutcome> sw = solve_sweep(t, cases, 3, {0});
+  bool sweep_ok = sw.size() == 4;
+  std::string names;
+  for (std::size_t i = 0; i < cases.size() && sweep_ok; ++i) {
+    names += (i ? "," : "") + cases[i].name;
+    const SolveOutput alone = solve(t, cases[i].cfg);
+    sweep_ok = sw[i].ok && sw[i].output.result.iterations == alone.result.iterations &&
+               sw[i].output.result.u.x == alone.result.u.x &&
+               sw[i].output.trajectory.size() == alone.trajectory.size();
+  }
+  put("sweep_ok", sweep_ok ? "true" : "false");
+  js += ", \"sweep_names\": \"" + names + "\"";
   js += "}";
   std::printf("%s\n", js.c_str());
   return 0;

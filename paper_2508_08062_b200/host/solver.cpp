@@ -4,7 +4,13 @@
 // reference signatures (proj/include/aapdhg/solver.hpp:81-99,
 // pdhg_core.hpp:33, sparse_linalg.hpp:34-47) and throw the reference's
 // exception types; all arithmetic runs in libaapdhg_cuda.so.
+#include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <memory>
+#include <thread>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -323,6 +329,92 @@ SolveOutput DeviceProblem::solve(const SolverConfig& cfg, const Iterate& u0) con
 
 SolveOutput DeviceProblem::solve(const SolverConfig& cfg) const {
   return run_solve(static_cast<aapdhg_handle*>(h_), *p_, cfg, nullptr);
+}
+
+// ---- sweep mode (proj/src/cli.cpp:142-214) ----------------------------------
+namespace {
+std::string short_num(double v) {
+  char buf[32];
+  std::snprintf(buf, sizeof buf, "%g", v);
+  return buf;
+}
+}  // namespace
+
+std::vector<SweepCase> sweep_cases(const SolverConfig& base, const std::vector<double>& d,
+                                   const std::vector<double>& eps,
+                                   const std::vector<std::size_t>& m,
+                                   const std::vector<double>& kappa_bar) {
+  std::vector<SweepCase> cases;
+  for (std::size_t id = 0; id < std::max<std::size_t>(1, d.size()); ++id)
+    for (std::size_t ie = 0; ie < std::max<std::size_t>(1, eps.size()); ++ie)
+      for (std::size_t im = 0; im < std::max<std::size_t>(1, m.size()); ++im)
+        for (std::size_t ik = 0; ik < std::max<std::size_t>(1, kappa_bar.size()); ++ik) {
+          SweepCase sc{base, ""};
+          std::string name;
+          if (!d.empty()) {
+            sc.cfg.safeguard_d = d[id];
+            name += "D" + short_num(d[id]);
+          }
+          if (!eps.empty()) {
+            sc.cfg.safeguard_eps = eps[ie];
+            name += std::string(name.empty() ? "" : "_") + "eps" + short_num(eps[ie]);
+          }
+          if (!m.empty()) {
+            sc.cfg.m = m[im];
+            name += std::string(name.empty() ? "" : "_") + "m" + std::to_string(m[im]);
+          }
+          if (!kappa_bar.empty()) {
+            sc.cfg.filter.kappa_bar = kappa_bar[ik];
+            name += std::string(name.empty() ? "" : "_") + "kappa" + short_num(kappa_bar[ik]);
+          }
+          sc.name = name;
+          cases.push_back(std::move(sc));
+        }
+  return cases;
+}
+
+std::vector<SweepOutcome> solve_sweep(const ProblemData& p, const std::vector<SweepCase>& cases,
+                                      std::size_t workers, const std::vector<int>& devices) {
+  if (devices.empty()) throw InputError("solve_sweep: no devices");
+  if (workers == 0) {
+    workers = 1;
+    if (const char* env = std::getenv("AAPDHG_SWEEP_WORKERS")) {
+      const long parsed = std::strtol(env, nullptr, 10);
+      if (parsed > 0) workers = std::size_t(parsed);
+    }
+  }
+  workers = std::max<std::size_t>(1, std::min(workers, cases.size()));
+  std::vector<SweepOutcome> out(cases.size());
+  std::atomic<std::size_t> next{0};
+  auto work = [&](std::size_t w) {
+    std::unique_ptr<DeviceProblem> dp;
+    std::string setup_error;
+    try {
+      dp.reset(new DeviceProblem(p, devices[w % devices.size()]));
+    } catch (const std::exception& e) {
+      setup_error = e.what();
+    }
+    for (std::size_t idx = next.fetch_add(1); idx < cases.size(); idx = next.fetch_add(1)) {
+      if (!dp) {
+        out[idx].error = setup_error;
+        continue;
+      }
+      try {
+        out[idx].output = dp->solve(cases[idx].cfg);
+        out[idx].ok = true;
+      } catch (const std::exception& e) {
+        out[idx].error = e.what();
+      }
+    }
+  };
+  if (workers == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (std::size_t w = 0; w < workers; ++w) pool.emplace_back(work, w);
+    for (std::thread& t : pool) t.join();
+  }
+  return out;
 }
 
 }  // namespace aapdhg

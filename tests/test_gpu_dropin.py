@@ -25,6 +25,7 @@ def test_cpp_dropin_end_to_end():
     assert r["transport_nnz"] >= 3200 and float(r["transport_best_ratio"]) <= 0.1
     assert r["csv_rows"] == 48 + 1 and r["summary_has_status"]
     assert r["input_error_thrown"]
+    assert r["sweep_ok"] and r["sweep_names"] == "D1_m2,D1_m5,D1e-300_m2,D1e-300_m5"
 
 
 def test_dropin_library_exports_api():
@@ -36,5 +37,6 @@ def test_dropin_library_exports_api():
     for name in ("aapdhg::solve(aapdhg::ProblemData const&, aapdhg::SolverConfig const&)",
                  "aapdhg::select_step_sizes(", "aapdhg::kkt_metrics(", "aapdhg::safeguard_pass(",
                  "aapdhg::pdhg_step(", "aapdhg::parse_mps(", "aapdhg::to_standard_form(",
-                 "aapdhg::trajectory_csv", "aapdhg::summary_json"):
+                 "aapdhg::trajectory_csv", "aapdhg::summary_json", "aapdhg::solve_sweep",
+                 "aapdhg::sweep_cases"):
         assert name in syms, name
