@@ -352,6 +352,9 @@ void Problem::init_device(int device) {
     throw CudaError(std::string("device ") + prop.name + " is not sm_100 class");
   AAPDHG_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
   stream_ = own_stream_;
+  AAPDHG_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   AAPDHG_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device));
   pdl_ = env_int("AAPDHG_PDL", 1) != 0;
 }
@@ -380,6 +383,8 @@ void Problem::init_vectors(const double* c, const double* q, const double* l, co
   AAPDHG_CUDA(cudaFuncSetAttribute(k_aa_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(aa_smem(kMaxMemory))));
   AAPDHG_CUDA(cudaFuncSetAttribute(k_serial_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kSerSmem)));
+  AAPDHG_CUDA(cudaFuncSetAttribute(k_serial_xchains, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(kSerSmem)));
 }
 
@@ -425,6 +430,9 @@ Problem::~Problem() {
   if (h_state_) cudaFreeHost(h_state_);
   if (h_batch_) cudaFreeHost(h_batch_);
   delete sh_su_;
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
+  if (side_) cudaStreamDestroy(side_);
   if (own_stream_) cudaStreamDestroy(own_stream_);
 }
 
@@ -626,6 +634,16 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
     else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
     else LAUNCH("k_dual_side", k_dual_side<false, false><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
   }
+  if (ser) {  // fork: the x-side serial chains run beside K2 on the side stream
+    AAPDHG_CUDA(cudaEventRecord(ev_fork_, s));
+    AAPDHG_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+    prof_begin(side_, "k_serial_xchains");
+    k_serial_xchains<<<1, kSerThreads, kSerSmem, side_>>>(su.B, su.P, su.S);
+    prof_end(side_);
+    AAPDHG_CUDA(cudaGetLastError());
+    AAPDHG_CUDA(cudaEventRecord(ev_join_, side_));
+    ++nodes;
+  }
   if (b2 && m_ > 0)
     nodes += launch_blocked_passes(s, kb_, VecRef{nullptr, su.B.upool, U_HAT, N_, 0}, su.S);
   // K xhat: products of K with xhat = u_hat[:n], then the fused dual step;
@@ -638,7 +656,8 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
                     : (push ? k_primal_side<false, true> : k_primal_side<false, false>);
     LAUNCH("k_primal_side", launch_ex(kern, g, dim3(kThreads), 0, s, pdl, K2m, su.B, su.P, su.S));
   }
-  if (ser) {
+  if (ser) {  // join, then the y-side chains and the control
+    AAPDHG_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
     LAUNCH("k_serial_control", k_serial_control<<<1, kSerThreads, kSerSmem, s>>>(su.B, su.P, su.S));
   } else if (su.B.fused_ctrl != 1) {  // (otherwise k_primal_side's last CTA)
     LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), K1m.grid(),

@@ -178,6 +178,8 @@ class Problem {
   bool pdl_ = true;  // AAPDHG_PDL=0 disables programmatic dependent launch
   cudaStream_t stream_ = nullptr;
   cudaStream_t own_stream_ = nullptr;
+  cudaStream_t side_ = nullptr;  // SERIAL: x-side chains beside K2 (fork/join)
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   int n_ = 0, m_ = 0, m1_ = 0;
   int64_t nnz_ = 0, N_ = 0, nglob_ = 0;
   // sharded solve

@@ -607,39 +607,33 @@ __global__ void __launch_bounds__(kCtrlThreads)
 // (fixed_point_residual pdhg_core.cpp:65-74; kkt_metrics solver.cpp:64-110),
 // one warp per chain (lane 0 sums), then the control logic.
 // ---------------------------------------------------------------------------
+// SERIAL mode, x side (runs beside K2: it needs only K1's outputs): the
+// index-ordered chains over j < n of ||xhat - x||^2 (the first part of
+// ||g||^2), the bound terms, c'x and ||c - K'y - lambda||^2 -> S->sres.
+// The elementwise terms of a chunk are formed by all threads in shared
+// memory; one lane per quantity adds them in order (bit for bit the
+// reference's loops, fixed_point_residual pdhg_core.cpp:65-74 and
+// kkt_metrics solver.cpp:64-110).
 __global__ void __launch_bounds__(kSerThreads)
-    k_serial_control(IterBufs B, const DevParams* __restrict__ P, DevState* S) {
-  if (S->done) {
-    if (threadIdx.x == 0 && P->use_cond) {
-      cudaGraphSetConditional(P->cond_aa, 0);
-      cudaGraphSetConditional(P->cond_loop, 0);
-    }
-    return;
-  }
-  // The elementwise terms of a chunk are formed by all threads into shared
-  // memory; one lane per quantity then adds them in index order, so the chain
-  // is only the dependent adds (the reference's loops, bit for bit).
-  extern __shared__ double terms[];                 // S_COUNT x kSerChunk
+    k_serial_xchains(IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+  if (S->done) return;
+  extern __shared__ double terms[];  // S_COUNT x kSerChunk
   unsigned char* take = reinterpret_cast<unsigned char*>(terms + S_COUNT * kSerChunk);
-  __shared__ double res[S_COUNT];
   const int64_t N = P->N;
-  const int n = P->n, mr = P->mrows, m1 = P->m1;
+  const int n = P->n;
   const double* u = B.upool + (int64_t)S->u_idx[U_CUR] * N;
   const double* uh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-  const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
   const double* T = B.T;
   const int w = threadIdx.x >> 5;
-  const bool chain = (threadIdx.x & 31) == 0 && w < S_COUNT;
-  const int64_t len = w == S_G2 ? N : (w == S_QY || w == S_INFEAS) ? mr : n;
+  // chains: warp 0 G2 (x part), 1 BOUND, 2 CX, 3 DUALSQ
+  const bool chain = (threadIdx.x & 31) == 0 && w < 4;
   double s = 0.0;
-  for (int64_t c0 = 0; c0 < N; c0 += kSerChunk) {
+  for (int c0 = 0; c0 < n; c0 += kSerChunk) {
     for (int t = threadIdx.x; t < kSerChunk; t += blockDim.x) {
-      const int64_t i = c0 + t;
-      if (i < N) {
+      const int i = c0 + t;
+      if (i < n) {
         const double d = __dsub_rn(uh[i], u[i]);
-        terms[S_G2 * kSerChunk + t] = __dmul_rn(d, d);
-      }
-      if (i < n) {  // pdhg_core.cpp:27-39 / solver.cpp:67-88,102-107
+        terms[0 * kSerChunk + t] = __dmul_rn(d, d);
         const double lj = B.l[i], uj = B.u[i], cj = B.c[i];
         const double rc = __dsub_rn(cj, T[i]);
         const double lam = project_lambda1(rc, lj, uj);
@@ -647,24 +641,18 @@ __global__ void __launch_bounds__(kSerThreads)
         unsigned char tk = 0;
         if (isfinite(lj) && lam > 0.0) { bt = __dmul_rn(lj, lam); tk = 1; }
         if (isfinite(uj) && lam < 0.0) { bt = __dmul_rn(uj, lam); tk = 1; }
-        terms[S_BOUND * kSerChunk + t] = bt;
+        terms[1 * kSerChunk + t] = bt;
         take[t] = tk;
-        terms[S_CX * kSerChunk + t] = __dmul_rn(cj, u[i]);
+        terms[2 * kSerChunk + t] = __dmul_rn(cj, u[i]);
         const double v = __dsub_rn(rc, lam);
-        terms[S_DUALSQ * kSerChunk + t] = __dmul_rn(v, v);
-      }
-      if (i < mr) {  // solver.cpp:90-100
-        terms[S_QY * kSerChunk + t] = __dmul_rn(B.q[i], u[n + i]);
-        double v = __dsub_rn(B.q[i], kx[i]);
-        if (i < m1) v = smax(v, 0.0);
-        terms[S_INFEAS * kSerChunk + t] = __dmul_rn(v, v);
+        terms[3 * kSerChunk + t] = __dmul_rn(v, v);
       }
     }
     __syncthreads();
-    if (chain && c0 < len) {
-      const int cnt = int(len - c0 < kSerChunk ? len - c0 : kSerChunk);
+    if (chain) {
+      const int cnt = n - c0 < kSerChunk ? n - c0 : kSerChunk;
       const double* tm = terms + w * kSerChunk;
-      if (w == S_BOUND) {
+      if (w == 1) {
         for (int k = 0; k < cnt; ++k)
           if (take[k]) s = __dadd_rn(s, tm[k]);
       } else {
@@ -681,14 +669,67 @@ __global__ void __launch_bounds__(kSerThreads)
     }
     __syncthreads();
   }
+  if (chain) S->sres[w] = s;  // 0 G2x, 1 BOUND, 2 CX, 3 DUALSQ
+}
+
+// SERIAL mode, y side + control (after K2 and k_serial_xchains): ||g||^2
+// continues the x-part chain over the y entries, then q'y and the primal
+// infeasibility, each in index order.
+__global__ void __launch_bounds__(kSerThreads)
+    k_serial_control(IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+  if (S->done) {
+    if (threadIdx.x == 0 && P->use_cond) {
+      cudaGraphSetConditional(P->cond_aa, 0);
+      cudaGraphSetConditional(P->cond_loop, 0);
+    }
+    return;
+  }
+  extern __shared__ double terms[];  // 3 x kSerChunk used
+  __shared__ double res[3];
+  const int64_t N = P->N;
+  const int n = P->n, mr = P->mrows, m1 = P->m1;
+  const double* u = B.upool + (int64_t)S->u_idx[U_CUR] * N;
+  const double* uh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
+  const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
+  const int w = threadIdx.x >> 5;
+  // chains: warp 0 G2 (continued), 1 QY, 2 INFEAS
+  const bool chain = (threadIdx.x & 31) == 0 && w < 3;
+  double s = (chain && w == 0) ? S->sres[0] : 0.0;
+  for (int c0 = 0; c0 < mr; c0 += kSerChunk) {
+    for (int t = threadIdx.x; t < kSerChunk; t += blockDim.x) {
+      const int i = c0 + t;
+      if (i < mr) {
+        const double d = __dsub_rn(uh[n + i], u[n + i]);
+        terms[0 * kSerChunk + t] = __dmul_rn(d, d);
+        terms[1 * kSerChunk + t] = __dmul_rn(B.q[i], u[n + i]);
+        double v = __dsub_rn(B.q[i], kx[i]);
+        if (i < m1) v = smax(v, 0.0);
+        terms[2 * kSerChunk + t] = __dmul_rn(v, v);
+      }
+    }
+    __syncthreads();
+    if (chain) {
+      const int cnt = mr - c0 < kSerChunk ? mr - c0 : kSerChunk;
+      const double* tm = terms + w * kSerChunk;
+      int k = 0;
+      for (; k + 8 <= cnt; k += 8) {
+        double p[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) p[q] = tm[k + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s = __dadd_rn(s, p[q]);
+      }
+      for (; k < cnt; ++k) s = __dadd_rn(s, tm[k]);
+    }
+    __syncthreads();
+  }
   if (chain) res[w] = s;
   __shared__ DevState sm;
   __shared__ DevParams sp;
   params_load(&sp, P);
-  state_load(&sm, S);  // (syncs: res[] complete)
+  state_load(&sm, S);  // (syncs: res[] complete; sres[] from k_serial_xchains)
   if (threadIdx.x == 0)
-    control_logic(&sp, &sm, res[S_G2], res[S_BOUND], res[S_QY], res[S_CX], res[S_INFEAS],
-                  res[S_DUALSQ]);
+    control_logic(&sp, &sm, res[0], sm.sres[1], res[1], sm.sres[2], res[2], sm.sres[3]);
   state_store(S, &sm);
 }
 
