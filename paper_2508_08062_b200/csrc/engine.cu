@@ -388,10 +388,26 @@ void Problem::init_vectors(const double* c, const double* q, const double* l, co
                                    int(kSerSmem)));
 }
 
+namespace {
+// AAPDHG_TIMING=1: problem_create phase times on stderr
+struct PhaseTimer {
+  bool on = env_int("AAPDHG_TIMING", 0) != 0;
+  Clock::time_point t = Clock::now();
+  void operator()(const char* what) {
+    if (!on) return;
+    std::fprintf(stderr, "[aapdhg] %-22s %8.3f s\n", what, secs(t));
+    t = Clock::now();
+  }
+};
+}  // namespace
+
 Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
+  PhaseTimer ph;
   validate_problem_view(v);
   const aapdhg_csr_view& k = v->k;
+  ph("validate");
   init_device(device);
+  ph("init_device");
   n_ = k.ncols;
   m_ = k.nrows;
   m1_ = v->m1;
@@ -401,27 +417,35 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   for (int64_t e = 0; e < nnz_ && all_zero_; ++e) all_zero_ = k.vals[e] == 0.0;
 
   upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
+  ph("upload K + SELL");
   std::vector<int32_t> trp, tci;
   std::vector<double> tv;
   transpose_csr(k, trp, tci, tv);
+  ph("transpose");
   upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_store_, KTs_, KTt_);
+  ph("upload K' + SELL");
   build_blocks(k.row_ptr, k.col_idx, k.vals, m_, n_, kb_);
   build_blocks(trp.data(), tci.data(), tv.data(), n_, m_, ktb_);
+  ph("L2 blocks");
 
   bounds_ok_ = true;
   for (int j = 0; j < n_; ++j)
     if (v->l[j] > v->u[j]) bounds_ok_ = false;
   init_vectors(v->c, v->q, v->l, v->u);
+  ph("vectors");
 
   // ||q|| and ||c|| under both reduction orders (constants of kkt_metrics)
   for (int serial = 0; serial < 2; ++serial) {
     nrm_q_[serial ? 0 : 1] = std::sqrt(device_dot(q_.as<double>(), nullptr, m_, serial != 0));
     nrm_c_[serial ? 0 : 1] = std::sqrt(device_dot(c_.as<double>(), nullptr, n_, serial != 0));
   }
+  ph("norms");
 }
 
 Problem::~Problem() {
+  PhaseTimer ph;
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  ph("destroy: graph");
   for (auto& e : event_pool_) cudaEventDestroy(e);
   for (auto& p : pending_) {
     cudaEventDestroy(p.a);
@@ -429,11 +453,13 @@ Problem::~Problem() {
   }
   if (h_state_) cudaFreeHost(h_state_);
   if (h_batch_) cudaFreeHost(h_batch_);
+  ph("destroy: pinned");
   delete sh_su_;
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
   if (side_) cudaStreamDestroy(side_);
   if (own_stream_) cudaStreamDestroy(own_stream_);
+  ph("destroy: streams");
 }
 
 void Problem::set_stream(cudaStream_t s) {
@@ -841,6 +867,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
                     aapdhg_solve_result* res, double* x_out, double* y_out, double* lam_out,
                     aapdhg_record_sink sink, void* ctx) {
   const auto t_start = Clock::now();
+  PhaseTimer ph;
   AAPDHG_CUDA(cudaSetDevice(device_));
   validate_config(prm);
   if (!bounds_ok_) throw StatusError(AAPDHG_ERR_INPUT, "build_lambda_set: l > u");
@@ -854,6 +881,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
       if (prm->d_hat[i] <= 0.0) throw StatusError(AAPDHG_ERR_INPUT, "aa: d_hat entries must be > 0");
   double tau, sigma;
   select_step_sizes(prm, &tau, &sigma);
+  ph("solve: step sizes");
 
   const bool serial = resolve_serial(prm->reduction);
   const int cap = method == AAPDHG_METHOD_PDHG ? 0 : int(prm->m);
@@ -871,6 +899,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
     h2d(pow_tab_.p, ptab.data(), sizeof(double) * len, stream_);
   }
 
+  ph("solve: buffers + pow table");
   DevParams P{};
   P.method = method;
   P.serial = serial ? 1 : 0;
@@ -955,6 +984,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
       graph_key_ = key;
     }
   }
+  ph("solve: graph");
   P.use_cond = use_graph ? 1 : 0;
   P.cond_aa = cond_aa_;
   P.cond_loop = cond_loop_;
@@ -974,6 +1004,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
                nullptr);
   AAPDHG_CUDA(cudaGetLastError());
 
+  ph("solve: start iterate");
   uint64_t flushed = 0;
   int batch = 8;  // iterations per launch, grows geometrically
   std::vector<aapdhg_record> host_recs;
@@ -1010,6 +1041,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
     batch = int(std::min<uint64_t>(uint64_t(batch) * 2, std::min<uint64_t>(kMaxBatch, rec_cap_ / 2)));
   }
   const DevState st = *h_state_;
+  ph("solve: iterations");
 
   // finish, solver.cpp:153-166
   const int slot = st.u_idx[st.final_role];
@@ -1042,6 +1074,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
                      (st.i + st.aa_failures) * uint64_t(aa_nodes_);
   else
     last_launches_ = st.loop_iters * uint64_t(core_nodes_ + aa_nodes_);
+  ph("solve: finish");
 }
 
 // ---- single-op entry points ----------------------------------------------
