@@ -86,131 +86,19 @@ struct SolveSetup {
 // SELL-32 slices of the short rows with split factor sf (see CsrDev):
 // slice = 32 / sf rows; element k of the slice's row rho sits at
 // sl_ptr + 32 (k / sf) + rho sf + (k % sf).
-void Problem::build_sell(const int32_t* rp, const int32_t* ci, const double* v,
-                         const std::vector<int32_t>& shorts_in, int sf, SellStore& st,
-                         CsrDev& out) {
-  const int R = 32 / sf;
-  // SELL-C-sigma: inside windows of one CTA's rows (sigma = 8 slices) the
-  // rows go by decreasing length, so a slice's lanes loop nearly equally
-  // often (ragged rows: Zipf lengths). Only the lane -> row map changes;
-  // every row is still summed in CSR order (bitwise unchanged).
-  std::vector<int32_t> shorts(shorts_in);
-  const int sigma = env_int("AAPDHG_SIGMA", kWarps * R);
-  if (sigma > 1)
-    for (size_t w0 = 0; w0 < shorts.size(); w0 += size_t(sigma)) {
-      const auto b = shorts.begin() + int64_t(w0);
-      const auto e = shorts.begin() + int64_t(std::min(shorts.size(), w0 + size_t(sigma)));
-      std::stable_sort(b, e, [&](int32_t a, int32_t c) {
-        return rp[a + 1] - rp[a] > rp[c + 1] - rp[c];
-      });
-    }
-  const int nslices = int((shorts.size() + R - 1) / R);
-  std::vector<int64_t> sl_ptr(size_t(std::max(nslices, 1)));
-  std::vector<int32_t> sl_len(size_t(std::max(nslices, 1))),
-      sl_row(size_t(std::max(nslices, 1)) * 32, -1);
-  int64_t total = 0;
-  for (int s = 0; s < nslices; ++s) {
-    int L = 0;
-    for (int r = 0; r < R && size_t(s) * R + r < shorts.size(); ++r) {
-      const int row = shorts[size_t(s) * R + r];
-      for (int j = 0; j < sf; ++j) sl_row[size_t(s) * 32 + r * sf + j] = row;
-      L = std::max(L, (rp[row + 1] - rp[row] + sf - 1) / sf);
-    }
-    sl_ptr[size_t(s)] = total;
-    sl_len[size_t(s)] = L;
-    total += int64_t(32) * L;
-  }
-  std::vector<int32_t> sci(size_t(std::max<int64_t>(total, 1)), 0);
-  std::vector<double> sv(size_t(std::max<int64_t>(total, 1)), 0.0);
-  for (int s = 0; s < nslices; ++s)
-    for (int r = 0; r < R && size_t(s) * R + r < shorts.size(); ++r) {
-      const int row = shorts[size_t(s) * R + r];
-      for (int k = 0; k < rp[row + 1] - rp[row]; ++k) {
-        const size_t dst = size_t(sl_ptr[size_t(s)] + 32 * int64_t(k / sf) + r * sf + k % sf);
-        sci[dst] = ci[rp[row] + k];
-        sv[dst] = v[rp[row] + k];
-      }
-    }
-  st.sl_ptr.reserve(sizeof(int64_t) * sl_ptr.size());
-  st.sl_len.reserve(sizeof(int32_t) * sl_len.size());
-  st.sl_row.reserve(sizeof(int32_t) * sl_row.size());
-  st.sci.reserve(sizeof(int32_t) * sci.size());
-  st.sv.reserve(sizeof(double) * sv.size());
-  h2d(st.sl_ptr.p, sl_ptr.data(), sizeof(int64_t) * sl_ptr.size(), stream_);
-  h2d(st.sl_len.p, sl_len.data(), sizeof(int32_t) * sl_len.size(), stream_);
-  h2d(st.sl_row.p, sl_row.data(), sizeof(int32_t) * sl_row.size(), stream_);
-  h2d(st.sci.p, sci.data(), sizeof(int32_t) * sci.size(), stream_);
-  h2d(st.sv.p, sv.data(), sizeof(double) * sv.size(), stream_);
-  sync();  // host staging vectors go out of scope
-  sell_bytes_ += (sizeof(int32_t) + sizeof(double)) * size_t(total);
-  out.nslices = nslices;
-  out.sl_ptr = st.sl_ptr.as<int64_t>();
-  out.sl_len = st.sl_len.as<int32_t>();
-  out.sl_row = st.sl_row.as<int32_t>();
-  out.sci = st.sci.as<int32_t>();
-  out.sv = st.sv.as<double>();
-  out.sf = sf;
-  // One wave: exactly kSpmvBlocksPerSM CTAs on every SM with the slices
-  // spread evenly over them (a ceil(nslices / 8) grid would leave some SMs
-  // one CTA more than others: ~20% idle tail). Several waves: 8 per CTA.
-  const int wave = num_sms_ * kSpmvBlocksPerSM;
-  out.nblk_short = int64_t(nslices) <= int64_t(wave) * kWarps ? std::min(nslices, wave)
-                                                              : (nslices + kWarps - 1) / kWarps;
-}
-
 // Uploads one CSR with its two sliced layouts: `ser` (sf = 1, CSR-ordered
 // row sums for the SERIAL mode) and `tree` (sf chosen so the slices fill
 // ~48 warps on every SM; aliases `ser` when sf = 1).
 void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows,
                          int ncols, CsrStore& st, CsrDev& ser, CsrDev& tree) {
   const int64_t nnz = rp[nrows];
-  std::vector<int32_t> shorts, longs;
-  shorts.reserve(size_t(nrows));
-  int64_t short_nnz = 0;
-  for (int r = 0; r < nrows; ++r) {
-    const int len = rp[r + 1] - rp[r];
-    if (len > kLongRow) {
-      longs.push_back(r);
-    } else {
-      shorts.push_back(r);
-      short_nnz += len;
-    }
-  }
-  // longest rows first: their CTAs start first (longest-processing-time
-  // order) and each CTA's warps get rows of similar length
-  std::stable_sort(longs.begin(), longs.end(), [&](int32_t a, int32_t b) {
-    return rp[a + 1] - rp[a] > rp[b + 1] - rp[b];
-  });
-  st.rp.reserve(sizeof(int32_t) * (nrows + 1));
-  st.ci.reserve(sizeof(int32_t) * nnz);
-  st.v.reserve(sizeof(double) * nnz);
-  st.longs.reserve(sizeof(int32_t) * std::max<size_t>(longs.size(), 1));
-  h2d(st.rp.p, rp, sizeof(int32_t) * (nrows + 1), stream_);
-  h2d(st.ci.p, ci, sizeof(int32_t) * nnz, stream_);
-  h2d(st.v.p, v, sizeof(double) * nnz, stream_);
-  h2d(st.longs.p, longs.data(), sizeof(int32_t) * longs.size(), stream_);
-  CsrDev base{};
-  base.nrows = nrows;
-  base.ncols = ncols;
-  base.nnz = nnz;
-  base.rp = st.rp.as<int32_t>();
-  base.ci = st.ci.as<int32_t>();
-  base.v = st.v.as<double>();
-  base.nlong = int32_t(longs.size());
-  base.long_rows = st.longs.as<int32_t>();
-  base.nblk_long = (base.nlong + kWarps - 1) / kWarps;
-  ser = base;
-  build_sell(rp, ci, v, shorts, 1, st.sell[0], ser);
-  // TREE layout: split rows over sf lanes only while the slices still fit in
-  // one wave of resident warps (a matrix with few rows, e.g. K of config 1)
-  const double mean = shorts.empty() ? 0.0 : double(short_nnz) / double(shorts.size());
-  const int64_t slots = int64_t(num_sms_) * kSpmvBlocksPerSM * kWarps;
-  int sf = 1;
-  while (sf < 8 && int64_t(ser.nslices) * 2 * sf <= slots && mean >= 8.0 * sf) sf *= 2;
-  sf = env_int("AAPDHG_SF", sf);
-  tree = base;
-  if (sf == 1) tree = ser;
-  else build_sell(rp, ci, v, shorts, sf, st.sell[1], tree);
+  st.rp.reserve(sizeof(int32_t) * (size_t(nrows) + 1));
+  st.ci.reserve(sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1)));
+  st.v.reserve(sizeof(double) * size_t(std::max<int64_t>(nnz, 1)));
+  h2d(st.rp.p, rp, sizeof(int32_t) * (size_t(nrows) + 1), stream_);
+  h2d(st.ci.p, ci, sizeof(int32_t) * size_t(nnz), stream_);
+  h2d(st.v.p, v, sizeof(double) * size_t(nnz), stream_);
+  finish_csr(nrows, ncols, nnz, st, ser, tree);  // layouts built on the device (ingest.cu)
 }
 
 // L2 column blocking (TREE mode only). A matrix whose gathered vector is
@@ -220,8 +108,7 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
 // pass gathers only from an L2-resident slice of the vector instead of one
 // DRAM sector per nonzero. Row sums become (((b0 + b1) + b2) + ...) — fixed
 // order, deterministic, not the CPU's association.
-void Problem::build_blocks(const int32_t* rp, const int32_t* ci, const double* v, int nrows,
-                           int ncols, Blocked& out) {
+void Problem::build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& out) {
   const int64_t kb = env_int("AAPDHG_L2_BLOCK_KB", 64 << 10);      // per block
   const int64_t min_kb = env_int("AAPDHG_L2_BLOCK_MIN_KB", 64 << 10);  // start above
   const int64_t vec_bytes = int64_t(ncols) * 8;
@@ -230,29 +117,13 @@ void Problem::build_blocks(const int32_t* rp, const int32_t* ci, const double* v
   const int nb = int((int64_t(ncols) + per - 1) / per);
   if (nb < 2) return;
   const int64_t W = (int64_t(ncols) + nb - 1) / nb;
-  std::vector<int32_t> cur(rp, rp + nrows);  // per-row cursor (rows sorted by column)
-  std::vector<int32_t> brp(static_cast<size_t>(nrows) + 1);
-  std::vector<int32_t> bci;
-  std::vector<double> bv;
   for (int b = 0; b < nb; ++b) {
-    const int64_t hi = std::min<int64_t>(int64_t(ncols), (b + 1) * W);
-    bci.clear();
-    bv.clear();
-    brp[0] = 0;
-    for (int r = 0; r < nrows; ++r) {
-      int32_t e = cur[r];
-      const int32_t end = rp[r + 1];
-      while (e < end && ci[e] < hi) {
-        bci.push_back(ci[e]);
-        bv.push_back(v[e]);
-        ++e;
-      }
-      cur[r] = e;
-      brp[r + 1] = int32_t(bci.size());
-    }
     out.store.emplace_back(new CsrStore());
+    int64_t nnz_b = 0;
+    device_block(src, nrows, b * W, std::min<int64_t>(int64_t(ncols), (b + 1) * W),
+                 *out.store.back(), &nnz_b);
     CsrDev ser, tree;
-    upload_csr(brp.data(), bci.data(), bv.data(), nrows, ncols, *out.store.back(), ser, tree);
+    finish_csr(nrows, ncols, nnz_b, *out.store.back(), ser, tree);
     out.blk.push_back(tree);
   }
   out.partial.reserve(sizeof(double) * size_t(nrows));
@@ -318,6 +189,11 @@ void validate_problem_view(const aapdhg_problem_view* v) {
   for (int64_t e = 0; e < k.nnz; ++e)
     if (k.col_idx[e] < 0 || k.col_idx[e] >= k.ncols)
       throw StatusError(AAPDHG_ERR_DIMENSION, "problem_create: column index out of range");
+  for (int r = 0; r < k.nrows; ++r)
+    for (int32_t e = k.row_ptr[r] + 1; e < k.row_ptr[r + 1]; ++e)
+      if (k.col_idx[e] <= k.col_idx[e - 1])
+        throw StatusError(AAPDHG_ERR_DIMENSION,
+                          "problem_create: column indices not strictly increasing in a row");
 }
 
 // K' as CSR with the entries of each row in ascending original row of K
@@ -418,14 +294,12 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
 
   upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
   ph("upload K + SELL");
-  std::vector<int32_t> trp, tci;
-  std::vector<double> tv;
-  transpose_csr(k, trp, tci, tv);
+  device_transpose(k_store_, m_, n_, nnz_, t_store_);
   ph("transpose");
-  upload_csr(trp.data(), tci.data(), tv.data(), n_, m_, t_store_, KTs_, KTt_);
-  ph("upload K' + SELL");
-  build_blocks(k.row_ptr, k.col_idx, k.vals, m_, n_, kb_);
-  build_blocks(trp.data(), tci.data(), tv.data(), n_, m_, ktb_);
+  finish_csr(n_, m_, nnz_, t_store_, KTs_, KTt_);
+  ph("K' SELL");
+  build_blocks(k_store_, m_, n_, kb_);
+  build_blocks(t_store_, n_, m_, ktb_);
   ph("L2 blocks");
 
   bounds_ok_ = true;
@@ -434,11 +308,17 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   init_vectors(v->c, v->q, v->l, v->u);
   ph("vectors");
 
-  // ||q|| and ||c|| under both reduction orders (constants of kkt_metrics)
-  for (int serial = 0; serial < 2; ++serial) {
-    nrm_q_[serial ? 0 : 1] = std::sqrt(device_dot(q_.as<double>(), nullptr, m_, serial != 0));
-    nrm_c_[serial ? 0 : 1] = std::sqrt(device_dot(c_.as<double>(), nullptr, n_, serial != 0));
-  }
+  // ||q|| and ||c|| (constants of kkt_metrics): SERIAL order is the
+  // reference's index-ordered dot (vec.hpp:16-29) — on the host, where the
+  // inputs are (x86-64 without FMA contraction: bitwise the same chain);
+  // TREE order on the device
+  double qq = 0.0, cc = 0.0;
+  for (int i = 0; i < m_; ++i) qq += v->q[i] * v->q[i];
+  for (int j = 0; j < n_; ++j) cc += v->c[j] * v->c[j];
+  nrm_q_[0] = std::sqrt(qq);
+  nrm_c_[0] = std::sqrt(cc);
+  nrm_q_[1] = std::sqrt(device_dot(q_.as<double>(), nullptr, m_, false));
+  nrm_c_[1] = std::sqrt(device_dot(c_.as<double>(), nullptr, n_, false));
   ph("norms");
 }
 
@@ -1256,8 +1136,8 @@ Problem::Problem(const ShardSpec& sp, int device) : device_(device) {
   upload_csr(sp.t_rp.data(), sp.t_ci.data(), sp.t_v.data(), n_, int(sp.world * sp.maxr),
              t_store_, KTs_, KTt_);
   // (relabelled indices stay ascending within a row: column blocks are in order)
-  build_blocks(sp.k_rp.data(), sp.k_ci.data(), sp.k_v.data(), m_, int(sp.world * sp.maxc), kb_);
-  build_blocks(sp.t_rp.data(), sp.t_ci.data(), sp.t_v.data(), n_, int(sp.world * sp.maxr), ktb_);
+  build_blocks(k_store_, m_, int(sp.world * sp.maxc), kb_);
+  build_blocks(t_store_, n_, int(sp.world * sp.maxr), ktb_);
   init_vectors(sp.c.data(), sp.q.data(), sp.l.data(), sp.u.data());
   nrm_q_[0] = nrm_q_[1] = sp.nrm_q;
   nrm_c_[0] = nrm_c_[1] = sp.nrm_c;

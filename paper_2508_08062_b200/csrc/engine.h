@@ -136,8 +136,13 @@ class Problem {
     DevBuf rp, ci, v, longs;
     SellStore sell[2];
   };
-  void build_sell(const int32_t* rp, const int32_t* ci, const double* v,
-                  const std::vector<int32_t>& shorts, int sf, SellStore& st, CsrDev& out);
+  // device-side ingestion (ingest.cu)
+  void finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev& ser, CsrDev& tree);
+  void device_sell(const int32_t* shorts, int nshort, const int32_t* len, int sf, CsrStore& st,
+                   SellStore& ss, CsrDev& out);
+  void device_transpose(const CsrStore& src, int nrows, int ncols, int64_t nnz, CsrStore& dst);
+  void device_block(const CsrStore& src, int nrows, int64_t c0, int64_t c1, CsrStore& dst,
+                    int64_t* nnz_out);
   void upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
                   CsrStore& st, CsrDev& ser, CsrDev& tree);
   const CsrDev& Km(bool serial) const { return serial ? Ks_ : Kt_; }
@@ -203,8 +208,7 @@ class Problem {
     int nb() const { return int(blk.size()); }
   };
   Blocked kb_, ktb_;  // K (gathers xhat, n) and K' (gathers y, m)
-  void build_blocks(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
-                    Blocked& out);
+  void build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& out);
   int launch_blocked_passes(cudaStream_t s, const Blocked& bk, const VecRef& x,
                             const DevState* S);
   size_t sell_bytes_ = 0;

@@ -1,0 +1,386 @@
+// ingest.cu — problem ingestion on the device: the
+// transpose K', the SELL-32 layouts and the L2 column blocks are built by
+// kernels and CUB primitives from the uploaded CSR instead of host loops
+// (config 4: 400M nonzeros). The layouts are exactly the ones the host
+// builder made: stable orders everywhere, so every row keeps its CSR order
+// and the SERIAL-mode sums stay bit-identical to the reference.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "engine.h"
+
+namespace aapdhg_b200 {
+
+namespace {
+
+constexpr int kT = 256;
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
+int blocks_for(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>((n + kT - 1) / kT, 1 << 20))); }
+
+__global__ void k_iota(int32_t* a, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    a[i] = int32_t(i);
+}
+
+__global__ void k_row_len(const int32_t* rp, int n, int32_t* len, char* is_long, char* is_short,
+                          int64_t* short_len, int thr) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t l = rp[i + 1] - rp[i];
+    len[i] = l;
+    is_long[i] = l > thr;
+    is_short[i] = l <= thr;
+    short_len[i] = l <= thr ? l : 0;
+  }
+}
+
+__global__ void k_gather_len(const int32_t* rows, int64_t n, const int32_t* len, int32_t* out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = len[rows[i]];
+}
+
+__global__ void k_seg_offsets(int32_t* off, int nseg, int sigma, int n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= nseg;
+       i += int64_t(gridDim.x) * blockDim.x)
+    off[i] = int32_t(i * int64_t(sigma) < n ? i * int64_t(sigma) : int64_t(n));
+}
+
+// slice s holds rows rows[s*R .. s*R+R) (R = 32/sf); lanes r*sf..r*sf+sf-1
+// share row r; sl_len = the slice's longest per-lane element count
+__global__ void k_sell_meta(const int32_t* rows, const int32_t* len, int64_t nshort, int sf,
+                            int nslices, int32_t* sl_row, int32_t* sl_len, int64_t* cnt) {
+  const int R = 32 / sf;
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < nslices;
+       s += int64_t(gridDim.x) * blockDim.x) {
+    int L = 0;
+    for (int r = 0; r < R; ++r) {
+      const int64_t k = s * R + r;
+      const int32_t row = k < nshort ? rows[k] : -1;
+      for (int j = 0; j < sf; ++j) sl_row[s * 32 + r * sf + j] = row;
+      if (row >= 0) L = max(L, (len[row] + sf - 1) / sf);
+    }
+    sl_len[s] = L;
+    cnt[s] = int64_t(32) * L;
+  }
+}
+
+// warp per slice: lane L = r*sf + j takes elements k = j, j+sf, ... of its row
+__global__ void k_sell_fill(const int32_t* rp, const int32_t* ci, const double* v,
+                            const int32_t* sl_row, const int64_t* sl_ptr, int nslices, int sf,
+                            int32_t* sci, double* sv) {
+  const int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nslices) return;
+  const int32_t row = sl_row[w * 32 + lane];
+  if (row < 0) return;
+  const int j = lane % sf;
+  const int32_t e0 = rp[row], len = rp[row + 1] - e0;
+  const int64_t base = sl_ptr[w] + lane;
+  for (int k = j; k < len; k += sf) {
+    const int64_t dst = base + 32 * int64_t(k / sf);
+    sci[dst] = ci[e0 + k];
+    sv[dst] = v[e0 + k];
+  }
+}
+
+__global__ void k_row_of(const int32_t* rp, int nrows, int64_t nnz, int32_t* row_of) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nnz;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int lo = 0, hi = nrows;  // last row with rp[row] <= e
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (rp[mid] <= e) lo = mid;
+      else hi = mid;
+    }
+    row_of[e] = lo;
+  }
+}
+
+__global__ void k_count(const int32_t* keys, int64_t n, int32_t* cnt) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(cnt + keys[i], 1);
+}
+
+__global__ void k_permute(const int32_t* perm, const int32_t* row_of, const double* v, int64_t n,
+                          int32_t* ci_out, double* v_out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t e = perm[i];
+    ci_out[i] = row_of[e];
+    v_out[i] = v[e];
+  }
+}
+
+__global__ void k_set(int32_t* p, int32_t v) { *p = v; }
+
+// first index in [lo, hi) with ci >= c (rows sorted by column)
+__device__ __forceinline__ int32_t lower(const int32_t* ci, int32_t lo, int32_t hi, int64_t c) {
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (ci[mid] < c) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_block_count(const int32_t* rp, const int32_t* ci, int nrows, int64_t c0,
+                              int64_t c1, int32_t* cnt) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < nrows;
+       r += int64_t(gridDim.x) * blockDim.x)
+    cnt[r] = lower(ci, rp[r], rp[r + 1], c1) - lower(ci, rp[r], rp[r + 1], c0);
+}
+
+__global__ void k_block_fill(const int32_t* rp, const int32_t* ci, const double* v, int nrows,
+                             int64_t c0, const int32_t* brp, int32_t* bci, double* bv) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < nrows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t s = lower(ci, rp[r], rp[r + 1], c0);
+    const int32_t d = brp[r], n = brp[r + 1] - d;
+    for (int32_t k = 0; k < n; ++k) {
+      bci[d + k] = ci[s + k];
+      bv[d + k] = v[s + k];
+    }
+  }
+}
+
+template <class T>
+T* tmp(DevBuf& b, size_t count) {
+  b.reserve(sizeof(T) * std::max<size_t>(count, 1));
+  return b.as<T>();
+}
+
+}  // namespace
+
+// exclusive scan of n int32 counts into out[0..n] (out[n] = total); returns total
+static int64_t scan_counts(const int32_t* cnt, int n, int32_t* out, cudaStream_t s) {
+  DevBuf t;
+  size_t bytes = 0;
+  AAPDHG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, cnt, out + 1, n, s));
+  AAPDHG_CUDA(cub::DeviceScan::InclusiveSum(tmp<char>(t, bytes), bytes, cnt, out + 1, n, s));
+  k_set<<<1, 1, 0, s>>>(out, 0);
+  int32_t total = 0;
+  if (n > 0) AAPDHG_CUDA(cudaMemcpyAsync(&total, out + n, sizeof total, cudaMemcpyDeviceToHost, s));
+  AAPDHG_CUDA(cudaStreamSynchronize(s));
+  return total;
+}
+
+// The row classification and the SELL layouts of a CSR already on the device
+// (st.rp / st.ci / st.v), as the host builder did: long rows (> kLongRow)
+// by decreasing length (stable), short rows in SELL-32 slices, sorted by
+// decreasing length inside windows of one CTA's rows (stable), split factor
+// sf for the TREE layout only while the slices fit one wave.
+void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev& ser,
+                         CsrDev& tree) {
+  cudaStream_t s = stream_;
+  DevBuf blen, blong, bshort, bslen, bsel, bcount, tsel;
+  int32_t* len = tmp<int32_t>(blen, nrows);
+  char* is_long = tmp<char>(blong, nrows);
+  char* is_short = tmp<char>(bshort, nrows);
+  int64_t* short_len = tmp<int64_t>(bslen, nrows);
+  if (nrows > 0)
+    k_row_len<<<blocks_for(nrows), kT, 0, s>>>(st.rp.as<int32_t>(), nrows, len, is_long, is_short,
+                                              short_len, kLongRow);
+  DevBuf biota, bshorts;
+  int32_t* iota = tmp<int32_t>(biota, nrows);
+  if (nrows > 0) k_iota<<<blocks_for(nrows), kT, 0, s>>>(iota, nrows);
+  int32_t* counts = tmp<int32_t>(bcount, 4);
+  int64_t* sums = reinterpret_cast<int64_t*>(tmp<int32_t>(bsel, 4));
+  int32_t* shorts = tmp<int32_t>(bshorts, nrows);
+  DevBuf blongs_unsorted;
+  int32_t* longs_u = tmp<int32_t>(blongs_unsorted, nrows);
+  size_t b1 = 0, b2 = 0, b3 = 0;
+  AAPDHG_CUDA(cub::DeviceSelect::Flagged(nullptr, b1, iota, is_short, shorts, counts, nrows, s));
+  AAPDHG_CUDA(cub::DeviceSelect::Flagged(nullptr, b2, iota, is_long, longs_u, counts + 1, nrows, s));
+  AAPDHG_CUDA(cub::DeviceReduce::Sum(nullptr, b3, short_len, sums, nrows, s));
+  char* t = tmp<char>(tsel, std::max(b1, std::max(b2, b3)));
+  AAPDHG_CUDA(cub::DeviceSelect::Flagged(t, b1, iota, is_short, shorts, counts, nrows, s));
+  AAPDHG_CUDA(cub::DeviceSelect::Flagged(t, b2, iota, is_long, longs_u, counts + 1, nrows, s));
+  AAPDHG_CUDA(cub::DeviceReduce::Sum(t, b3, short_len, sums, nrows, s));
+  int32_t hc[2] = {0, 0};
+  int64_t short_nnz = 0;
+  AAPDHG_CUDA(cudaMemcpyAsync(hc, counts, sizeof hc, cudaMemcpyDeviceToHost, s));
+  AAPDHG_CUDA(cudaMemcpyAsync(&short_nnz, sums, sizeof short_nnz, cudaMemcpyDeviceToHost, s));
+  AAPDHG_CUDA(cudaStreamSynchronize(s));
+  if (nrows == 0) hc[0] = hc[1] = 0;
+  const int nshort = hc[0], nlong = hc[1];
+
+  // long rows: longest first (stable)
+  st.longs.reserve(sizeof(int32_t) * std::max(nlong, 1));
+  if (nlong > 0) {
+    DevBuf bk, bk2, tt;
+    int32_t* klen = tmp<int32_t>(bk, nlong);
+    int32_t* klen2 = tmp<int32_t>(bk2, nlong);
+    k_gather_len<<<blocks_for(nlong), kT, 0, s>>>(longs_u, nlong, len, klen);
+    size_t bytes = 0;
+    AAPDHG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, klen, klen2, longs_u,
+                                                          st.longs.as<int32_t>(), nlong, 0, 32, s));
+    AAPDHG_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp<char>(tt, bytes), bytes, klen, klen2,
+                                                          longs_u, st.longs.as<int32_t>(), nlong,
+                                                          0, 32, s));
+  }
+  CsrDev base{};
+  base.nrows = nrows;
+  base.ncols = ncols;
+  base.nnz = nnz;
+  base.rp = st.rp.as<int32_t>();
+  base.ci = st.ci.as<int32_t>();
+  base.v = st.v.as<double>();
+  base.nlong = nlong;
+  base.long_rows = st.longs.as<int32_t>();
+  base.nblk_long = (nlong + kWarps - 1) / kWarps;
+  ser = base;
+  device_sell(shorts, nshort, len, 1, st, st.sell[0], ser);
+  const double mean = nshort == 0 ? 0.0 : double(short_nnz) / double(nshort);
+  const int64_t slots = int64_t(num_sms_) * kSpmvBlocksPerSM * kWarps;
+  int sf = 1;
+  while (sf < 8 && int64_t(ser.nslices) * 2 * sf <= slots && mean >= 8.0 * sf) sf *= 2;
+  sf = env_int("AAPDHG_SF", sf);
+  tree = base;
+  if (sf == 1) tree = ser;
+  else device_sell(shorts, nshort, len, sf, st, st.sell[1], tree);
+}
+
+void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* len, int sf,
+                          CsrStore& st, SellStore& ss, CsrDev& out) {
+  cudaStream_t s = stream_;
+  const int R = 32 / sf;
+  const int sigma = env_int("AAPDHG_SIGMA", kWarps * R);
+  DevBuf brows, bk, bk2, boff, tt;
+  int32_t* rows = tmp<int32_t>(brows, nshort);
+  if (sigma > 1 && nshort > 0) {  // stable sort by decreasing length inside each window
+    const int nseg = int((int64_t(nshort) + sigma - 1) / sigma);
+    int32_t* klen = tmp<int32_t>(bk, nshort);
+    int32_t* klen2 = tmp<int32_t>(bk2, nshort);
+    int32_t* off = tmp<int32_t>(boff, size_t(nseg) + 1);
+    k_gather_len<<<blocks_for(nshort), kT, 0, s>>>(shorts_in, nshort, len, klen);
+    k_seg_offsets<<<blocks_for(nseg + 1), kT, 0, s>>>(off, nseg, sigma, nshort);
+    size_t bytes = 0;
+    AAPDHG_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(
+        nullptr, bytes, klen, klen2, shorts_in, rows, nshort, nseg, off, off + 1, 0, 32, s));
+    AAPDHG_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(
+        tmp<char>(tt, bytes), bytes, klen, klen2, shorts_in, rows, nshort, nseg, off, off + 1, 0,
+        32, s));
+  } else if (nshort > 0) {
+    AAPDHG_CUDA(cudaMemcpyAsync(rows, shorts_in, sizeof(int32_t) * nshort,
+                                cudaMemcpyDeviceToDevice, s));
+  }
+  const int nslices = int((int64_t(nshort) + R - 1) / R);
+  ss.sl_ptr.reserve(sizeof(int64_t) * std::max(nslices, 1));
+  ss.sl_len.reserve(sizeof(int32_t) * std::max(nslices, 1));
+  ss.sl_row.reserve(sizeof(int32_t) * size_t(std::max(nslices, 1)) * 32);
+  DevBuf bcnt, tscan;
+  int64_t* cnt = tmp<int64_t>(bcnt, nslices);
+  int64_t total = 0;
+  if (nslices > 0) {
+    k_sell_meta<<<blocks_for(nslices), kT, 0, s>>>(rows, len, nshort, sf, nslices,
+                                                   ss.sl_row.as<int32_t>(), ss.sl_len.as<int32_t>(),
+                                                   cnt);
+    size_t bytes = 0;
+    AAPDHG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, ss.sl_ptr.as<int64_t>(), nslices, s));
+    AAPDHG_CUDA(cub::DeviceScan::ExclusiveSum(tmp<char>(tscan, bytes), bytes, cnt,
+                                              ss.sl_ptr.as<int64_t>(), nslices, s));
+    int64_t last[2] = {0, 0};
+    AAPDHG_CUDA(cudaMemcpyAsync(&last[0], ss.sl_ptr.as<int64_t>() + nslices - 1, sizeof(int64_t),
+                                cudaMemcpyDeviceToHost, s));
+    AAPDHG_CUDA(cudaMemcpyAsync(&last[1], cnt + nslices - 1, sizeof(int64_t),
+                                cudaMemcpyDeviceToHost, s));
+    AAPDHG_CUDA(cudaStreamSynchronize(s));
+    total = last[0] + last[1];
+  }
+  ss.sci.reserve(sizeof(int32_t) * size_t(std::max<int64_t>(total, 1)));
+  ss.sv.reserve(sizeof(double) * size_t(std::max<int64_t>(total, 1)));
+  AAPDHG_CUDA(cudaMemsetAsync(ss.sci.p, 0, ss.sci.bytes, s));
+  AAPDHG_CUDA(cudaMemsetAsync(ss.sv.p, 0, ss.sv.bytes, s));
+  if (nslices > 0)
+    k_sell_fill<<<int((int64_t(nslices) * 32 + kT - 1) / kT), kT, 0, s>>>(
+        st.rp.as<int32_t>(), st.ci.as<int32_t>(), st.v.as<double>(), ss.sl_row.as<int32_t>(),
+        ss.sl_ptr.as<int64_t>(), nslices, sf, ss.sci.as<int32_t>(), ss.sv.as<double>());
+  AAPDHG_CUDA(cudaGetLastError());
+  AAPDHG_CUDA(cudaStreamSynchronize(s));  // scratch buffers go out of scope
+  sell_bytes_ += (sizeof(int32_t) + sizeof(double)) * size_t(total);
+  out.nslices = nslices;
+  out.sl_ptr = ss.sl_ptr.as<int64_t>();
+  out.sl_len = ss.sl_len.as<int32_t>();
+  out.sl_row = ss.sl_row.as<int32_t>();
+  out.sci = ss.sci.as<int32_t>();
+  out.sv = ss.sv.as<double>();
+  out.sf = sf;
+  const int wave = num_sms_ * kSpmvBlocksPerSM;
+  out.nblk_short = int64_t(nslices) <= int64_t(wave) * kWarps ? std::min(nslices, wave)
+                                                              : (nslices + kWarps - 1) / kWarps;
+}
+
+// K' as CSR, entries of each row in ascending original row: a stable radix
+// sort of the entries by column (the order matvec_transpose accumulates in,
+// sparse_linalg.cpp:77-87).
+void Problem::device_transpose(const CsrStore& src, int nrows, int ncols, int64_t nnz,
+                               CsrStore& dst) {
+  cudaStream_t s = stream_;
+  dst.rp.reserve(sizeof(int32_t) * (size_t(ncols) + 1));
+  dst.ci.reserve(sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1)));
+  dst.v.reserve(sizeof(double) * size_t(std::max<int64_t>(nnz, 1)));
+  DevBuf bcnt;
+  int32_t* cnt = tmp<int32_t>(bcnt, ncols);
+  AAPDHG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * std::max(ncols, 1), s));
+  if (nnz > 0) k_count<<<blocks_for(nnz), kT, 0, s>>>(src.ci.as<int32_t>(), nnz, cnt);
+  scan_counts(cnt, ncols, dst.rp.as<int32_t>(), s);
+  if (nnz == 0) return;
+  DevBuf bk, bperm_in, bperm, brow, tt;
+  int32_t* keys_out = tmp<int32_t>(bk, nnz);
+  int32_t* perm_in = tmp<int32_t>(bperm_in, nnz);
+  int32_t* perm = tmp<int32_t>(bperm, nnz);
+  k_iota<<<blocks_for(nnz), kT, 0, s>>>(perm_in, nnz);
+  int bits = 1;
+  while (bits < 31 && (int64_t(1) << bits) < ncols) ++bits;
+  size_t bytes = 0;
+  AAPDHG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, src.ci.as<int32_t>(), keys_out,
+                                              perm_in, perm, nnz, 0, bits, s));
+  AAPDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp<char>(tt, bytes), bytes, src.ci.as<int32_t>(),
+                                              keys_out, perm_in, perm, nnz, 0, bits, s));
+  int32_t* row_of = tmp<int32_t>(brow, nnz);
+  k_row_of<<<blocks_for(nnz), kT, 0, s>>>(src.rp.as<int32_t>(), nrows, nnz, row_of);
+  k_permute<<<blocks_for(nnz), kT, 0, s>>>(perm, row_of, src.v.as<double>(), nnz,
+                                           dst.ci.as<int32_t>(), dst.v.as<double>());
+  AAPDHG_CUDA(cudaGetLastError());
+  AAPDHG_CUDA(cudaStreamSynchronize(s));
+}
+
+// One column block's CSR (the same rows restricted to [c0, c1), CSR order
+// kept) built on the device from the full CSR.
+void Problem::device_block(const CsrStore& src, int nrows, int64_t c0, int64_t c1,
+                           CsrStore& dst, int64_t* nnz_out) {
+  cudaStream_t s = stream_;
+  dst.rp.reserve(sizeof(int32_t) * (size_t(nrows) + 1));
+  DevBuf bcnt;
+  int32_t* cnt = tmp<int32_t>(bcnt, nrows);
+  if (nrows > 0)
+    k_block_count<<<blocks_for(nrows), kT, 0, s>>>(src.rp.as<int32_t>(), src.ci.as<int32_t>(),
+                                                   nrows, c0, c1, cnt);
+  const int64_t nnz = scan_counts(cnt, nrows, dst.rp.as<int32_t>(), s);
+  dst.ci.reserve(sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1)));
+  dst.v.reserve(sizeof(double) * size_t(std::max<int64_t>(nnz, 1)));
+  if (nrows > 0 && nnz > 0)
+    k_block_fill<<<blocks_for(nrows), kT, 0, s>>>(src.rp.as<int32_t>(), src.ci.as<int32_t>(),
+                                                  src.v.as<double>(), nrows, c0,
+                                                  dst.rp.as<int32_t>(), dst.ci.as<int32_t>(),
+                                                  dst.v.as<double>());
+  AAPDHG_CUDA(cudaGetLastError());
+  AAPDHG_CUDA(cudaStreamSynchronize(s));
+  *nnz_out = nnz;
+}
+
+}  // namespace aapdhg_b200
