@@ -212,6 +212,7 @@ class Problem {
   int launch_blocked_passes(cudaStream_t s, const Blocked& bk, const VecRef& x,
                             const DevState* S);
   size_t sell_bytes_ = 0;
+  bool sigma_global_ = false;  // device_sell: sort all short rows (ragged lengths)
   DevBuf c_, q_, l_, u_;
   double nrm_q_[2] = {0, 0}, nrm_c_[2] = {0, 0};  // [serial, tree]
 

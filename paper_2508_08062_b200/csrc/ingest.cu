@@ -11,6 +11,7 @@
 #include <cub/device/device_select.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "engine.h"
@@ -35,7 +36,7 @@ __global__ void k_iota(int32_t* a, int64_t n) {
 }
 
 __global__ void k_row_len(const int32_t* rp, int n, int32_t* len, char* is_long, char* is_short,
-                          int64_t* short_len, int thr) {
+                          int64_t* short_len, int64_t* short_sq, int thr) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t l = rp[i + 1] - rp[i];
@@ -43,6 +44,7 @@ __global__ void k_row_len(const int32_t* rp, int n, int32_t* len, char* is_long,
     is_long[i] = l > thr;
     is_short[i] = l <= thr;
     short_len[i] = l <= thr ? l : 0;
+    short_sq[i] = l <= thr ? int64_t(l) * l : 0;
   }
 }
 
@@ -191,14 +193,16 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
   char* is_long = tmp<char>(blong, nrows);
   char* is_short = tmp<char>(bshort, nrows);
   int64_t* short_len = tmp<int64_t>(bslen, nrows);
+  DevBuf bsq;
+  int64_t* short_sq = tmp<int64_t>(bsq, nrows);
   if (nrows > 0)
     k_row_len<<<blocks_for(nrows), kT, 0, s>>>(st.rp.as<int32_t>(), nrows, len, is_long, is_short,
-                                              short_len, kLongRow);
+                                              short_len, short_sq, kLongRow);
   DevBuf biota, bshorts;
   int32_t* iota = tmp<int32_t>(biota, nrows);
   if (nrows > 0) k_iota<<<blocks_for(nrows), kT, 0, s>>>(iota, nrows);
   int32_t* counts = tmp<int32_t>(bcount, 4);
-  int64_t* sums = reinterpret_cast<int64_t*>(tmp<int32_t>(bsel, 4));
+  int64_t* sums = reinterpret_cast<int64_t*>(tmp<int32_t>(bsel, 8));
   int32_t* shorts = tmp<int32_t>(bshorts, nrows);
   DevBuf blongs_unsorted;
   int32_t* longs_u = tmp<int32_t>(blongs_unsorted, nrows);
@@ -210,10 +214,13 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
   AAPDHG_CUDA(cub::DeviceSelect::Flagged(t, b1, iota, is_short, shorts, counts, nrows, s));
   AAPDHG_CUDA(cub::DeviceSelect::Flagged(t, b2, iota, is_long, longs_u, counts + 1, nrows, s));
   AAPDHG_CUDA(cub::DeviceReduce::Sum(t, b3, short_len, sums, nrows, s));
+  AAPDHG_CUDA(cub::DeviceReduce::Sum(t, b3, short_sq, sums + 1, nrows, s));
   int32_t hc[2] = {0, 0};
-  int64_t short_nnz = 0;
+  int64_t short_nnz = 0, short_sq_sum = 0;
   AAPDHG_CUDA(cudaMemcpyAsync(hc, counts, sizeof hc, cudaMemcpyDeviceToHost, s));
   AAPDHG_CUDA(cudaMemcpyAsync(&short_nnz, sums, sizeof short_nnz, cudaMemcpyDeviceToHost, s));
+  AAPDHG_CUDA(cudaMemcpyAsync(&short_sq_sum, sums + 1, sizeof short_sq_sum,
+                              cudaMemcpyDeviceToHost, s));
   AAPDHG_CUDA(cudaStreamSynchronize(s));
   if (nrows == 0) hc[0] = hc[1] = 0;
   const int nshort = hc[0], nlong = hc[1];
@@ -243,8 +250,15 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
   base.long_rows = st.longs.as<int32_t>();
   base.nblk_long = (nlong + kWarps - 1) / kWarps;
   ser = base;
-  device_sell(shorts, nshort, len, 1, st, st.sell[0], ser);
   const double mean = nshort == 0 ? 0.0 : double(short_nnz) / double(nshort);
+  // ragged rows (coefficient of variation > 1/2, e.g. Zipf lengths): sort all
+  // short rows by length, so the 8 slices of a CTA are alike too and no warp
+  // idles at the CTA's end; otherwise windows of one CTA keep the epilogue's
+  // vector accesses local
+  const double var = nshort == 0 ? 0.0 : double(short_sq_sum) / double(nshort) - mean * mean;
+  const bool ragged = mean > 0.0 && std::sqrt(std::max(var, 0.0)) > 0.5 * mean;
+  sigma_global_ = ragged;
+  device_sell(shorts, nshort, len, 1, st, st.sell[0], ser);
   const int64_t slots = int64_t(num_sms_) * kSpmvBlocksPerSM * kWarps;
   int sf = 1;
   while (sf < 8 && int64_t(ser.nslices) * 2 * sf <= slots && mean >= 8.0 * sf) sf *= 2;
@@ -258,7 +272,7 @@ void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* l
                           CsrStore& st, SellStore& ss, CsrDev& out) {
   cudaStream_t s = stream_;
   const int R = 32 / sf;
-  const int sigma = env_int("AAPDHG_SIGMA", kWarps * R);
+  const int sigma = env_int("AAPDHG_SIGMA", sigma_global_ ? std::max(nshort, 1) : kWarps * R);
   DevBuf brows, bk, bk2, boff, tt;
   int32_t* rows = tmp<int32_t>(brows, nshort);
   if (sigma > 1 && nshort > 0) {  // stable sort by decreasing length inside each window
