@@ -56,6 +56,12 @@ def _load(kind: str):
             raise FileNotFoundError(f"{REF_LIB} not built (needs /root/reference; make -C oracle ref)")
         lib = C.CDLL(str(REF_LIB))
         pre = "aapdhg_ref_"
+    elif kind.startswith("ref-"):  # rounding variants (oracle/Makefile `variants`)
+        path = ORACLE_DIR / "_ref" / "variants" / kind[4:] / "libaapdhg_ref.so"
+        if not path.exists():
+            raise FileNotFoundError(f"{path} not built (make -C oracle variants)")
+        lib = C.CDLL(str(path))
+        pre = "aapdhg_ref_"
     else:
         raise ValueError(kind)
     PV, SP = C.POINTER(_abi.ProblemView), C.POINTER(_abi.SolveParams)

@@ -102,3 +102,17 @@ def test_port_matches_reference_live(port):
                 assert np.array_equal(a.trajectory[f], b.trajectory[f]), (p.name, meth, f)
             assert np.array_equal(a.result.u.x, b.result.u.x)
             assert np.array_equal(a.result.lambda_, b.result.lambda_)
+
+
+@pytest.mark.parametrize("variant", ["ref-fast", "ref-assoc"])
+def test_reference_rounding_variants_load_and_solve(variant):
+    """The reference built under other rounding regimes (oracle/Makefile
+    `variants`, used for the iteration-count envelope) solves the toy LP."""
+    from oracle.pyoracle import ORACLE_DIR, Oracle
+    if not (ORACLE_DIR / "_ref" / "variants" / variant[4:] / "libaapdhg_ref.so").exists():
+        pytest.skip("reference variants not built (no /root/reference)")
+    from paper_2508_08062_b200 import Method, SolverConfig, SolveStatus, problems
+    out = Oracle(variant).solve(problems.toy(), SolverConfig(method=Method.AA_PDHG, toll=1e-4,
+                                                             tau=0.25, sigma=0.25))
+    assert out.result.status == SolveStatus.RESIDUAL_TOL
+    assert abs(out.result.u.x[0] - 3.0) < 1e-3
