@@ -62,13 +62,15 @@ struct CsrDev {
   const int32_t* sl_row = nullptr;
   const int32_t* sci = nullptr;
   const double* sv = nullptr;
-  const int32_t* long_rows = nullptr;
-  int32_t nblk_short = 0, nblk_long = 0;
+  const int32_t* long_rows = nullptr;  // longest first
+  int32_t nhuge = 0;  // TREE: the first nhuge long rows (>= kHugeRow) get a CTA each
+  int32_t nblk_short = 0, nblk_long = 0;  // nblk_long = nhuge + ceil((nlong - nhuge) / 8)
   int32_t sf = 1;  // lanes per row in the slices (1 = CSR-ordered row sums)
   int32_t grid() const { return nblk_short + nblk_long; }
 };
 
 constexpr int kLongRow = 256;        // rows longer than this get a warp each
+constexpr int kHugeRow = 1024;       // TREE: rows at least this long get a CTA each
 constexpr int kSpmvBlocksPerSM = 6;  // 48 warps/SM at <= 40 registers
 
 constexpr int kGroup = 64;           // CTAs per first-level partial group

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <vector>
 
 #include "engine.h"
 
@@ -227,6 +228,7 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
 
   // long rows: longest first (stable)
   st.longs.reserve(sizeof(int32_t) * std::max(nlong, 1));
+  int nhuge = 0;
   if (nlong > 0) {
     DevBuf bk, bk2, tt;
     int32_t* klen = tmp<int32_t>(bk, nlong);
@@ -238,6 +240,16 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
     AAPDHG_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp<char>(tt, bytes), bytes, klen, klen2,
                                                           longs_u, st.longs.as<int32_t>(), nlong,
                                                           0, 32, s));
+    std::vector<int32_t> hl(static_cast<size_t>(nlong));
+    AAPDHG_CUDA(cudaMemcpyAsync(hl.data(), klen2, sizeof(int32_t) * nlong, cudaMemcpyDeviceToHost, s));
+    AAPDHG_CUDA(cudaStreamSynchronize(s));
+    // only when the long rows alone cannot fill the GPU with warps (few long
+    // rows, e.g. transport K: 4,000 rows of 2,000): many long rows (Zipf)
+    // already give every SM enough warps, and a CTA per row only adds
+    // per-CTA overhead there
+    const int64_t slots = int64_t(num_sms_) * kSpmvBlocksPerSM * kWarps;
+    if (nlong < slots)
+      while (nhuge < nlong && hl[size_t(nhuge)] >= kHugeRow) ++nhuge;
   }
   CsrDev base{};
   base.nrows = nrows;
@@ -266,6 +278,9 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
   tree = base;
   if (sf == 1) tree = ser;
   else device_sell(shorts, nshort, len, sf, st, st.sell[1], tree);
+  // TREE: a CTA per huge row (the SERIAL layout keeps one lane-0 chain per row)
+  tree.nhuge = nhuge;
+  tree.nblk_long = nhuge + (nlong - nhuge + kWarps - 1) / kWarps;
 }
 
 void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* len, int sf,

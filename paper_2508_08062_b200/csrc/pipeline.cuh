@@ -298,7 +298,36 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     s = acc;
     return (row >= 0 && j == 0) ? row : -1;
   }
-  const int lr = blockIdx.x * kWarps + warp;  // long rows: the first CTAs
+  if (!SERIAL && (int)blockIdx.x < A.nhuge) {
+    // a huge row per CTA: thread-strided products, warp trees, then the 8
+    // warp sums in warp order (fixed shape: deterministic)
+    const int row = __ldg(A.long_rows + blockIdx.x);
+    const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
+    grid_dependency_wait();
+    double acc = 0.0;
+    for (int64_t c0 = e0 + threadIdx.x; c0 < e1; c0 += kThreads * kUnroll) {
+      double pr[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t e = c0 + kThreads * u;
+        pr[u] = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) acc = __dadd_rn(acc, pr[u]);
+    }
+    acc = warp_sum(acc);
+    __shared__ double hw[kWarps];
+    if (lane == 0) hw[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = hw[0];
+      for (int w = 1; w < kWarps; ++w) t = __dadd_rn(t, hw[w]);
+      s = t;
+    }
+    return threadIdx.x == 0 ? row : -1;
+  }
+  // the other long rows: a warp each, 8 per CTA, after the huge rows' CTAs
+  const int lr = A.nhuge + (int(blockIdx.x) - A.nhuge) * kWarps + warp;
   if (lr >= A.nlong) return -1;
   const int row = __ldg(A.long_rows + lr);
   const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);

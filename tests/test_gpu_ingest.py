@@ -47,6 +47,12 @@ def shapes():
     out["one_long"] = (rc, n)
     # every row long
     out["all_long"] = ([rng.choice(n, 300 + 40 * i, replace=False) for i in range(9)], n)
+    # rows at and past the CTA-per-row threshold (1024) beside warp-per-row
+    # and short rows
+    nh = 6000
+    rc = [rng.choice(nh, L, replace=False) for L in (5000, 1024, 1023, 2000, 300)]
+    rc += [rng.choice(nh, int(rng.integers(1, 40)), replace=False) for _ in range(60)]
+    out["huge"] = (rc, nh)
     return out
 
 
@@ -55,7 +61,7 @@ def port():
     return Oracle("port")
 
 
-@pytest.mark.parametrize("name", ["edges", "one_long", "all_long"])
+@pytest.mark.parametrize("name", ["edges", "one_long", "all_long", "huge"])
 def test_device_layouts_bitwise(name, port):
     rc, n = shapes()[name]
     p = lp_from_rows(rc, n, seed=len(name))
