@@ -60,6 +60,7 @@ struct CsrDev {
   const int64_t* sl_ptr = nullptr;
   const int32_t* sl_len = nullptr;
   const int32_t* sl_row = nullptr;
+  const int32_t* sl_cnt = nullptr;  // the lane's element count (no rp loads in the loop setup)
   const int32_t* sci = nullptr;
   const double* sv = nullptr;
   const int32_t* long_rows = nullptr;  // longest first

@@ -130,7 +130,7 @@ class Problem {
            const DevState* S, int pred, const int32_t* stop);
   static size_t aa_smem(int cap);
   struct SellStore {
-    DevBuf sl_ptr, sl_len, sl_row, sci, sv;
+    DevBuf sl_ptr, sl_len, sl_row, sl_cnt, sci, sv;
   };
   struct CsrStore {
     DevBuf rp, ci, v, longs;

@@ -64,7 +64,8 @@ __global__ void k_seg_offsets(int32_t* off, int nseg, int sigma, int n) {
 // slice s holds rows rows[s*R .. s*R+R) (R = 32/sf); lanes r*sf..r*sf+sf-1
 // share row r; sl_len = the slice's longest per-lane element count
 __global__ void k_sell_meta(const int32_t* rows, const int32_t* len, int64_t nshort, int sf,
-                            int nslices, int32_t* sl_row, int32_t* sl_len, int64_t* cnt) {
+                            int nslices, int32_t* sl_row, int32_t* sl_cnt, int32_t* sl_len,
+                            int64_t* cnt) {
   const int R = 32 / sf;
   for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < nslices;
        s += int64_t(gridDim.x) * blockDim.x) {
@@ -72,8 +73,12 @@ __global__ void k_sell_meta(const int32_t* rows, const int32_t* len, int64_t nsh
     for (int r = 0; r < R; ++r) {
       const int64_t k = s * R + r;
       const int32_t row = k < nshort ? rows[k] : -1;
-      for (int j = 0; j < sf; ++j) sl_row[s * 32 + r * sf + j] = row;
-      if (row >= 0) L = max(L, (len[row] + sf - 1) / sf);
+      const int32_t l = row >= 0 ? len[row] : 0;
+      for (int j = 0; j < sf; ++j) {
+        sl_row[s * 32 + r * sf + j] = row;
+        sl_cnt[s * 32 + r * sf + j] = (l - j + sf - 1) / sf;  // elements k = j, j+sf, ...
+      }
+      if (row >= 0) L = max(L, (l + sf - 1) / sf);
     }
     sl_len[s] = L;
     cnt[s] = int64_t(32) * L;
@@ -311,13 +316,14 @@ void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* l
   ss.sl_ptr.reserve(sizeof(int64_t) * std::max(nslices, 1));
   ss.sl_len.reserve(sizeof(int32_t) * std::max(nslices, 1));
   ss.sl_row.reserve(sizeof(int32_t) * size_t(std::max(nslices, 1)) * 32);
+  ss.sl_cnt.reserve(sizeof(int32_t) * size_t(std::max(nslices, 1)) * 32);
   DevBuf bcnt, tscan;
   int64_t* cnt = tmp<int64_t>(bcnt, nslices);
   int64_t total = 0;
   if (nslices > 0) {
     k_sell_meta<<<blocks_for(nslices), kT, 0, s>>>(rows, len, nshort, sf, nslices,
-                                                   ss.sl_row.as<int32_t>(), ss.sl_len.as<int32_t>(),
-                                                   cnt);
+                                                   ss.sl_row.as<int32_t>(), ss.sl_cnt.as<int32_t>(),
+                                                   ss.sl_len.as<int32_t>(), cnt);
     size_t bytes = 0;
     AAPDHG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, ss.sl_ptr.as<int64_t>(), nslices, s));
     AAPDHG_CUDA(cub::DeviceScan::ExclusiveSum(tmp<char>(tscan, bytes), bytes, cnt,
@@ -345,6 +351,7 @@ void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* l
   out.sl_ptr = ss.sl_ptr.as<int64_t>();
   out.sl_len = ss.sl_len.as<int32_t>();
   out.sl_row = ss.sl_row.as<int32_t>();
+  out.sl_cnt = ss.sl_cnt.as<int32_t>();
   out.sci = ss.sci.as<int32_t>();
   out.sv = ss.sv.as<double>();
   out.sf = sf;

@@ -247,8 +247,7 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     const int L = __ldg(A.sl_len + sl);
     const int64_t sbase = __ldg(A.sl_ptr + sl);
     const int row = __ldg(A.sl_row + sl * 32 + lane);
-    const int len = row >= 0 ? __ldg(A.rp + row + 1) - __ldg(A.rp + row) : 0;
-    const int cnt = (len - j + sf - 1) / sf;  // this lane's elements
+    const int cnt = __ldg(A.sl_cnt + sl * 32 + lane);  // this lane's elements
     const int64_t base = sbase + lane;
     const int32_t* __restrict__ cp = A.sci + base;
     const double* __restrict__ vp = A.sv + base;
