@@ -234,8 +234,20 @@ __device__ __forceinline__ bool skip_launch(const DevState* S, int pred_aa_ok,
 
 // Sum of the row this lane owns in this CTA's work; returns the row (-1 if
 // none): the sum is valid in the owning lane only.
-template <bool SERIAL, int UNROLL = kUnroll, bool STAGE_V = false>
-__device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, double& s) {
+struct NoPre {
+  __device__ __forceinline__ void operator()(int) const {}
+};
+__device__ __forceinline__ void l2_prefetch(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// pre(row): called in the row's owning lane right after the metadata loads
+// when the whole slice is one unroll group (short rows): the fused kernels
+// prefetch their epilogue operands into L2 so the epilogue does not pay a
+// DRAM round trip after the (short) SpMV chain.
+template <bool SERIAL, int UNROLL = kUnroll, bool STAGE_V = false, class Pre = NoPre>
+__device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, double& s,
+                                       Pre pre = Pre{}) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   s = 0.0;
   if ((int)blockIdx.x >= A.nblk_long) {
@@ -248,6 +260,7 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     const int64_t sbase = __ldg(A.sl_ptr + sl);
     const int row = __ldg(A.sl_row + sl * 32 + lane);
     const int cnt = __ldg(A.sl_cnt + sl * 32 + lane);  // this lane's elements
+    if (L <= UNROLL && row >= 0 && j == 0) pre(row);
     const int64_t base = sbase + lane;
     const int32_t* __restrict__ cp = A.sci + base;
     const double* __restrict__ vp = A.sv + base;
@@ -504,8 +517,17 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
   double t;
-  int j = row_sum<SERIAL, (VAR == 1 || VAR == 3) ? 8 : (VAR == 4 ? 16 : kUnroll),
-                  (VAR >= 3)>(KT, P->ygather ? P->ygather : x + P->n, t);
+  int j = row_sum<SERIAL, (VAR == 1 || VAR == 3) ? 8 : (VAR == 4 ? 16 : kUnroll), (VAR >= 3)>(
+      KT, P->ygather ? P->ygather : x + P->n, t, [&](int r) {
+        l2_prefetch(x + r);
+        l2_prefetch(B.c + r);
+        l2_prefetch(B.l + r);
+        l2_prefetch(B.u + r);
+        if constexpr (PUSH) {
+          l2_prefetch(B.upool + (int64_t)S->u_idx[U_PREV] * N + r);
+          l2_prefetch(B.gpool + (int64_t)S->g_idx[G_PREV] * N + r);
+        }
+      });
   if (B.rinit1 && j >= 0) t = __dadd_rn(B.rinit1[j], t);  // earlier column passes
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
   if (VAR == 2) {  // experiment: SpMV only
