@@ -84,6 +84,19 @@ SparseMatrix vstack(const SparseMatrix& a, const SparseMatrix& b);
 
 // Products on the device (CSR-ordered sums: bit-identical to the reference).
 void matvec(const SparseMatrix& m, const Vec& v, Vec& out);
+// Column-major dense matrix, sparse_linalg.hpp:46-58 (test support / small
+// algebra; the device path keeps its p x p systems in shared memory).
+struct DenseMatrix {
+  int nrows = 0;
+  int ncols = 0;
+  std::vector<double> data;  // nrows * ncols, column-major
+  DenseMatrix() = default;
+  DenseMatrix(int r, int c) : nrows(r), ncols(c), data(std::size_t(r) * std::size_t(c), 0.0) {}
+  double& at(int i, int j) { return data[std::size_t(j) * std::size_t(nrows) + std::size_t(i)]; }
+  double at(int i, int j) const { return data[std::size_t(j) * std::size_t(nrows) + std::size_t(i)]; }
+  static DenseMatrix identity(int n);
+};
+
 Vec matvec(const SparseMatrix& m, const Vec& v);
 void matvec_transpose(const SparseMatrix& m, const Vec& v, Vec& out);
 Vec matvec_transpose(const SparseMatrix& m, const Vec& v);
@@ -143,8 +156,16 @@ struct StepSizes {
   double sigma = 0.0;
 };
 
+// projections, pdhg_core.hpp (host helpers; the device path fuses them)
+Vec project_box(const Vec& x, const Vec& l, const Vec& u);
+Vec project_dual(const Vec& y, int m1);
+Vec project_lambda(const Vec& v, const LambdaSpec& spec);
+Iterate project_feasible(const Iterate& u, const ProblemData& p);
 Iterate pdhg_step(const Iterate& u, const ProblemData& p, const StepSizes& s);
 std::pair<Vec, double> fixed_point_residual(const Iterate& u, const Iterate& tu);
+// <Mu, v>, M = [[I, tau K'], [sigma K, I]], tau == sigma (pdhg_core.hpp:39-42;
+// a diagnostic of the reference, products on the device)
+double m_inner_product(const Vec& u, const Vec& v, const ProblemData& p, const StepSizes& s);
 Vec concat_iterate(const Iterate& u);
 Iterate split_iterate(const Vec& v, int n);
 

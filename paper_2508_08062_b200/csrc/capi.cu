@@ -192,7 +192,8 @@ int aapdhg_cuda_power_norm(aapdhg_handle* h, int32_t max_iters, double rel_tol, 
 int aapdhg_cuda_matvec(aapdhg_handle* h, const double* x, double* out, char* err,
                        size_t errlen) {
   if (int rc = whole(h, "matvec", err, errlen)) return rc;
-  if (int rc = need(h && out && (x || h->prob->n() == 0) ? h : nullptr, "matvec: null argument",
+  if (int rc = need(h && (out || h->prob->m() == 0) && (x || h->prob->n() == 0) ? h : nullptr,
+                    "matvec: null argument",
                     err, errlen))
     return rc;
   return guard(err, errlen, [&] {
@@ -204,7 +205,8 @@ int aapdhg_cuda_matvec(aapdhg_handle* h, const double* x, double* out, char* err
 int aapdhg_cuda_matvec_transpose(aapdhg_handle* h, const double* y, double* out, char* err,
                                  size_t errlen) {
   if (int rc = whole(h, "matvec_transpose", err, errlen)) return rc;
-  if (int rc = need(h && out ? h : nullptr, "matvec_transpose: null argument", err, errlen))
+  if (int rc = need(h && (out || h->prob->n() == 0) && (y || h->prob->m() == 0) ? h : nullptr,
+                    "matvec_transpose: null argument", err, errlen))
     return rc;
   return guard(err, errlen, [&] {
     h->prob->matvec_transpose(y, out);
@@ -215,7 +217,8 @@ int aapdhg_cuda_matvec_transpose(aapdhg_handle* h, const double* y, double* out,
 int aapdhg_cuda_pdhg_step(aapdhg_handle* h, double tau, double sigma, const double* x,
                           const double* y, double* xn, double* yn, char* err, size_t errlen) {
   if (int rc = whole(h, "pdhg_step", err, errlen)) return rc;
-  if (int rc = need(h && xn && yn ? h : nullptr, "pdhg_step: null argument", err, errlen))
+  if (int rc = need(h && (xn || h->prob->n() == 0) && (yn || h->prob->m() == 0) ? h : nullptr,
+                    "pdhg_step: null argument", err, errlen))
     return rc;
   return guard(err, errlen, [&] {
     h->prob->pdhg_step(tau, sigma, x, y, xn, yn);

@@ -331,6 +331,59 @@ SolveOutput DeviceProblem::solve(const SolverConfig& cfg) const {
   return run_solve(static_cast<aapdhg_handle*>(h_), *p_, cfg, nullptr);
 }
 
+double m_inner_product(const Vec& u, const Vec& v, const ProblemData& p, const StepSizes& s) {
+  if (s.tau != s.sigma) throw UnsupportedError("m_inner_product requires tau == sigma");
+  const std::size_t n = std::size_t(p.n()), m = std::size_t(p.m1() + p.m2());
+  if (u.size() != n + m || v.size() != n + m)
+    throw DimensionError("m_inner_product: size mismatch");
+  const Vec ux(u.begin(), u.begin() + long(n)), uy(u.begin() + long(n), u.end());
+  const Vec vx(v.begin(), v.begin() + long(n)), vy(v.begin() + long(n), v.end());
+  double out = dot(ux, vx) + dot(uy, vy);
+  out += s.tau * dot(matvec_transpose(p.k, uy), vx);
+  out += s.tau * dot(matvec(p.k, ux), vy);
+  return out;
+}
+
+// ---- host projections (pdhg_core.cpp:10-43 semantics: std::min/std::max, same
+// error types and messages) -----------------------------------------------------
+Vec project_box(const Vec& x, const Vec& l, const Vec& u) {
+  if (x.size() != l.size() || x.size() != u.size())
+    throw DimensionError("project_box: size mismatch");
+  Vec out(x.size());
+  for (std::size_t i = 0; i < x.size(); ++i) out[i] = std::min(std::max(x[i], l[i]), u[i]);
+  return out;
+}
+
+Vec project_dual(const Vec& y, int m1) {
+  if (m1 < 0 || std::size_t(m1) > y.size()) throw DimensionError("project_dual: bad m1");
+  Vec out = y;
+  for (std::size_t i = 0; i < std::size_t(m1); ++i) out[i] = std::max(out[i], 0.0);
+  return out;
+}
+
+Vec project_lambda(const Vec& v, const LambdaSpec& spec) {
+  if (v.size() != spec.size()) throw DimensionError("project_lambda: size mismatch");
+  Vec out(v.size());
+  for (std::size_t i = 0; i < v.size(); ++i) {
+    const LambdaTag t = spec[i];
+    out[i] = t == LambdaTag::kZero     ? 0.0
+             : t == LambdaTag::kNonpos ? std::min(v[i], 0.0)
+             : t == LambdaTag::kNonneg ? std::max(v[i], 0.0)
+                                       : v[i];
+  }
+  return out;
+}
+
+Iterate project_feasible(const Iterate& u, const ProblemData& p) {
+  return {project_box(u.x, p.l, p.u), project_dual(u.y, p.m1())};
+}
+
+DenseMatrix DenseMatrix::identity(int n) {
+  DenseMatrix m(n, n);
+  for (int i = 0; i < n; ++i) m.at(i, i) = 1.0;
+  return m;
+}
+
 // ---- sweep mode (proj/src/cli.cpp:142-214) ----------------------------------
 namespace {
 std::string short_num(double v) {
