@@ -533,9 +533,6 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   if (n_ > 0) {
     if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
     else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
-    else if (push && env_int("AAPDHG_K1VAR", 0) == 1) LAUNCH("k_dual_side", k_dual_side<false, true, 1><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
-    else if (push && env_int("AAPDHG_K1VAR", 0) == 3) LAUNCH("k_dual_side", k_dual_side<false, true, 3><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
-    else if (push && env_int("AAPDHG_K1VAR", 0) == 4) LAUNCH("k_dual_side", k_dual_side<false, true, 4><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
     else if (push && env_int("AAPDHG_K1VAR", 0) == 2) LAUNCH("k_dual_side", k_dual_side<false, true, 2><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
     else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
     else LAUNCH("k_dual_side", k_dual_side<false, false><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));

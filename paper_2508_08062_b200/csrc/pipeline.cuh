@@ -245,7 +245,7 @@ __device__ __forceinline__ void l2_prefetch(const void* p) {
 // when the whole slice is one unroll group (short rows): the fused kernels
 // prefetch their epilogue operands into L2 so the epilogue does not pay a
 // DRAM round trip after the (short) SpMV chain.
-template <bool SERIAL, int UNROLL = kUnroll, bool STAGE_V = false, class Pre = NoPre>
+template <bool SERIAL, int UNROLL = kUnroll, class Pre = NoPre>
 __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, double& s,
                                        Pre pre = Pre{}) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -266,29 +266,6 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     const double* __restrict__ vp = A.sv + base;
     grid_dependency_wait();  // x may be the previous kernel's output (PDL)
     double acc = 0.0;
-    if constexpr (STAGE_V) {
-      // values go global -> shared by cp.async (no registers held while the
-      // gathers are in flight): UNROLL gathers per lane in flight at the
-      // register cost of the column indices and the gathered values only
-      __shared__ double vst[kWarps * UNROLL * 32];
-      double* my = vst + warp * UNROLL * 32 + lane;
-      for (int t0 = 0; t0 < L; t0 += UNROLL) {
-        int c[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          const bool on = t0 + u < cnt;
-          if (on) cp_async8(my + 32 * u, vp + 32 * (t0 + u));
-          c[u] = on ? __ldcs(cp + 32 * (t0 + u)) : 0;
-        }
-        double g[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) g[u] = t0 + u < cnt ? __ldg(x + c[u]) : 0.0;
-        cp_async_wait_all();
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u)
-          if (t0 + u < cnt) acc = __dadd_rn(acc, __dmul_rn(my[32 * u], g[u]));
-      }
-    } else
     for (int t0 = 0; t0 < L; t0 += UNROLL) {
       int c[UNROLL];
       double v[UNROLL];
@@ -508,6 +485,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 //   lambda_j = P_Lambda(c_j - t)                           solver.cpp:67-71
 //   per-CTA partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
 //   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
+// VAR 2 (experiment, AAPDHG_K1VAR=2): the SpMV alone, no epilogue
 template <bool SERIAL, bool PUSH, int VAR = 0>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
@@ -517,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
   double t;
-  int j = row_sum<SERIAL, (VAR == 1 || VAR == 3) ? 8 : (VAR == 4 ? 16 : kUnroll), (VAR >= 3)>(
+  int j = row_sum<SERIAL, kUnroll>(
       KT, P->ygather ? P->ygather : x + P->n, t, [&](int r) {
         l2_prefetch(x + r);
         l2_prefetch(B.c + r);
