@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(1024)
     for (int t = 0; t < pm; ++t) S->w[t] = w[t];
     S->aa_ok = 1;
     S->i += 1;
-    if (!per_op) (P->rec + S->k % P->rec_cap)->aa_step = 1;
+    if (!per_op) (P->rec + (S->k & (P->rec_cap - 1)))->aa_step = 1;
   } else {
     S->aa_ok = 0;
     S->j += 1;

@@ -185,7 +185,7 @@ __device__ __forceinline__ void advance(const DevParams* P, DevState* S) {
 // SpMV core: SELL-32 slices, one per warp
 // ---------------------------------------------------------------------------
 //
-// Random-column SpMVs on B200 are bound by the L1TEX gather rate (~0.85
+// Random-column SpMVs on B200 are bound by the L1TEX gather rate (~1.2
 // cycles per random 8-byte gather per SM with thousands of gathers in flight;
 // measured, profiles/microbench/gather_bench.cu). The matrix is stored once,
 // on upload, in 32-lane slices (SELL-32): with split factor sf a slice holds
@@ -360,14 +360,152 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   if (row >= 0) out[row] = s;
 }
 
-// ---------------------------------------------------------------------------
-// TREE-mode control without a launch of its own
-// ---------------------------------------------------------------------------
+// KKT scalars of the CUR iterate from the reduced sums (solver.cpp:83-107).
+__device__ __forceinline__ void kkt_from_sums(double nrm_q, double nrm_c, double bound,
+                                              double qy, double cx, double infeas,
+                                              double dual_sq, double* kkt) {
+  const double dual_core = __dadd_rn(qy, bound);
+  const double primal_obj = cx;
+  kkt[0] = fabs(__dsub_rn(dual_core, primal_obj)) /
+           __dadd_rn(__dadd_rn(1.0, fabs(dual_core)), fabs(primal_obj));
+  kkt[1] = sqrt(infeas) / __dadd_rn(1.0, nrm_q);
+  kkt[2] = sqrt(dual_sq) / __dadd_rn(1.0, nrm_c);
+  kkt[3] = primal_obj;
+}
 
+__device__ __forceinline__ void finish_solve(DevState* S, int status, int role, double g) {
+  S->status = status;
+  S->final_role = role;
+  S->g_final = g;
+  S->done = 1;
+}
+
+// The scalar part of one iteration of solve() (solver.cpp:188-215,241-247),
+// in four pieces so the fused TREE tail can run them on two warps:
+//   control_kkt_records  KKT of u_k (kept for the finish), the KKT fields of
+//                        record k-1, the base fields of record k
+//   control_decide       termination (FIXED_POINT -> KKT_TOL -> RESIDUAL_TOL
+//                        -> MAX_ITERS -> TIMEOUT), safeguard, batch count
+//   control_commit       memory push, plain-step counter, role rotation
+//   control_setcond      the graph's IF / WHILE conditions
+// control_logic runs them in sequence (one thread). Records are read by the
+// host only below rec_complete, so record k's base fields may be written
+// even when the iteration terminates.
+struct Decision {
+  int attempt, left;
+};
+
+__device__ __noinline__ void control_kkt_records(const DevParams* P, DevState* S, uint64_t k,
+                                                    double g2, double bound, double qy, double cx,
+                                                    double infeas, double dual_sq,
+                                                    double elapsed_in) {
+  double kkt[4];
+  kkt_from_sums(P->nrm_q, P->nrm_c, bound, qy, cx, infeas, dual_sq, kkt);
+  for (int q = 0; q < 4; ++q) S->kkt[q] = kkt[q];
+  const uint64_t mask = P->rec_cap - 1;  // rec_cap is a power of two
+  if (k > 0) {  // the record of iterate k-1 takes the KKT of the produced iterate u_k
+    aapdhg_record* r = P->rec + ((k - 1) & mask);
+    r->r_gap = kkt[0];
+    r->r_primal = kkt[1];
+    r->r_dual = kkt[2];
+    r->objective = kkt[3];
+    r->elapsed_s = elapsed_in >= 0.0
+                       ? elapsed_in
+                       : (double)(globaltimer_ns() - S->t0_ns) * 1e-9 + P->wall_offset_s;
+  }
+  aapdhg_record* r = P->rec + (k & mask);
+  r->k = k;
+  r->g_norm = sqrt(g2);
+  r->aa_step = 0;
+  r->i = S->i;  // counters before this iteration's step
+  r->j = S->j;
+}
+
+__device__ __noinline__ Decision control_decide(const DevParams* P, DevState* S, uint64_t k,
+                                                   double g2, double bound, double qy, double cx,
+                                                   double infeas, double dual_sq,
+                                                   double elapsed_in, double pw_in) {
+  const double gkn = sqrt(g2);
+  S->gkn = gkn;
+  S->aa_attempt = 0;
+  S->aa_ok = 0;
+  const double elapsed = elapsed_in >= 0.0
+                             ? elapsed_in
+                             : (double)(globaltimer_ns() - S->t0_ns) * 1e-9 + P->wall_offset_s;
+  bool attempt = false;
+  do {
+    if (k == 0) {  // priming step, solver.cpp:168-172
+      S->g0n = gkn;
+      break;
+    }
+    S->rec_complete = k;
+    if (k == 1 && S->g0n == 0.0) { finish_solve(S, AAPDHG_SOLVE_FIXED_POINT_START, U_PREV, 0.0); break; }
+    if (P->kkt_terminate) {
+      double kkt[4];
+      kkt_from_sums(P->nrm_q, P->nrm_c, bound, qy, cx, infeas, dual_sq, kkt);
+      if (smax(smax(kkt[0], kkt[1]), kkt[2]) <= P->kkt_eps) {
+        finish_solve(S, AAPDHG_SOLVE_KKT_TOL, U_CUR, gkn);
+        break;
+      }
+    }
+    if (gkn < P->toll) { finish_solve(S, AAPDHG_SOLVE_RESIDUAL_TOL, U_CUR, gkn); break; }
+    if (S->i + S->j >= P->max_iters) { finish_solve(S, AAPDHG_SOLVE_MAX_ITERS, U_CUR, gkn); break; }
+    if (elapsed >= P->max_wall_s) { finish_solve(S, AAPDHG_SOLVE_TIMEOUT, U_CUR, gkn); break; }
+    if (P->method != AAPDHG_METHOD_PDHG) {
+      // safeguard_pass, solver.cpp:59-62, with the host std::pow table
+      const double pw = pw_in >= 0.0           ? pw_in
+                        : S->i < P->pow_len ? P->pow_tab[S->i]
+                                          : pow((double)S->i + 1.0, -(1.0 + P->safeguard_eps));
+      attempt = gkn <= __dmul_rn(__dmul_rn(P->safeguard_d, S->g0n), pw);
+    }
+  } while (false);
+  Decision d;
+  d.attempt = attempt ? 1 : 0;
+  d.left = S->done ? 0 : --S->batch_left;
+  return d;
+}
+
+__device__ __noinline__ void control_commit(const DevParams* P, DevState* S, uint64_t k,
+                                               Decision d) {
+  if (S->done) return;
+  if (k > 0) {
+    if (P->method != AAPDHG_METHOD_PDHG) {  // memory_push / FaaState::push
+      if (S->mem_size == P->cap) {
+        for (int t = 1; t < S->mem_size; ++t) S->mem_slots[t - 1] = S->mem_slots[t];
+        S->mem_slots[S->mem_size - 1] = S->push_slot;
+      } else {
+        S->mem_slots[S->mem_size++] = S->push_slot;
+      }
+    }
+    if (d.attempt) S->aa_attempt = 1;
+    else S->j += 1;
+  }
+  // no AA attempt: the iteration ends here (the AA branch commits otherwise)
+  if (!d.attempt) advance(P, S);
+}
+
+__device__ __noinline__ void control_setcond(const DevParams* P, Decision d) {
+  if (P->use_cond) {
+    cudaGraphSetConditional(P->cond_aa, d.attempt ? 1u : 0u);
+    cudaGraphSetConditional(P->cond_loop, d.left > 0 ? 1u : 0u);
+  }
+}
+
+// elapsed_in >= 0: the wall clock agreed by all shards (sharded solve)
 __device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2,
                                            double bound, double qy, double cx, double infeas,
                                            double dual_sq, double elapsed_in = -1.0,
-                                           double pw_in = -1.0);
+                                           double pw_in = -1.0) {
+  const uint64_t k = S->k;
+  control_kkt_records(P, S, k, g2, bound, qy, cx, infeas, dual_sq, elapsed_in);
+  const Decision d = control_decide(P, S, k, g2, bound, qy, cx, infeas, dual_sq, elapsed_in, pw_in);
+  control_commit(P, S, k, d);
+  control_setcond(P, d);
+}
+
+// ---------------------------------------------------------------------------
+// TREE-mode control without a launch of its own
+// ---------------------------------------------------------------------------
 
 // Sums NQ rows of per-CTA partials (row q at part[q * nu]) in a fixed shape:
 // thread-strided in CTA order, warp xor tree, warps in order. Result in
@@ -378,10 +516,22 @@ __device__ __forceinline__ void reduce_partial_rows(const double* part, int nu, 
   double v[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) v[q] = 0.0;
-#pragma unroll 4
-  for (int b = threadIdx.x; b < nu; b += blockDim.x)
+  // groups of 4 strides: every load of a group is in flight before the adds
+  // (the adds keep the CTA order b, b + blockDim, ...)
+  for (int b0 = threadIdx.x; b0 < nu; b0 += 4 * blockDim.x) {
+    double x[4][NQ];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) v[q] = __dadd_rn(v[q], __ldcg(part + q * nu + b));
+    for (int u = 0; u < 4; ++u) {
+      const int b = b0 + u * blockDim.x;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) x[u][q] = b < nu ? __ldcg(part + q * nu + b) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (b0 + u * int(blockDim.x) < nu)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) v[q] = __dadd_rn(v[q], x[u][q]);
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) v[q] = warp_sum(v[q]);
@@ -453,15 +603,31 @@ __device__ __forceinline__ void fused_control_tail(const IterBufs& B, const DevP
   reduce_partial_rows<P2_COUNT>(B.part2, gridDim.x, t2, red);
   cp_async_wait_all();
   __syncthreads();
+  // the control on two warps: KKT + records (warp 1) beside the decision and
+  // the graph conditions (warp 0); the commit needs the decision
+  __shared__ double sums[7];
+  __shared__ Decision dec;
   if (threadIdx.x == 0) {
-    DevState& sm = ts.st;
-    sm.ticket = 0;
-    double t1[P1_COUNT];
 #pragma unroll
-    for (int q = 0; q < P1_COUNT; ++q) t1[q] = __ldcg(&S->tot1[q]);
-    control_logic(&ts.pr, &sm, __dadd_rn(t1[P1_GX2], t2[P2_GY2]), t1[P1_BOUND], t2[P2_QY],
-                  t1[P1_CX], t2[P2_INFEAS], t1[P1_DUALSQ], -1.0, ts.pw);
+    for (int q = 0; q < P1_COUNT; ++q) sums[q] = __ldcg(&S->tot1[q]);
+#pragma unroll
+    for (int q = 0; q < P2_COUNT; ++q) sums[P1_COUNT + q] = t2[q];
   }
+  __syncthreads();
+  DevState& sm = ts.st;
+  const uint64_t k = sm.k;
+  const double g2 = __dadd_rn(sums[P1_GX2], sums[P1_COUNT + P2_GY2]);
+  const double bound = sums[P1_BOUND], qy = sums[P1_COUNT + P2_QY], cx = sums[P1_CX];
+  const double infeas = sums[P1_COUNT + P2_INFEAS], dsq = sums[P1_DUALSQ];
+  if (threadIdx.x == 32)
+    control_kkt_records(&ts.pr, &sm, k, g2, bound, qy, cx, infeas, dsq, -1.0);
+  if (threadIdx.x == 0) {
+    sm.ticket = 0;
+    dec = control_decide(&ts.pr, &sm, k, g2, bound, qy, cx, infeas, dsq, -1.0, ts.pw);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) control_setcond(&ts.pr, dec);
+  if (threadIdx.x == 32) control_commit(&ts.pr, &sm, k, dec);
   state_store(S, &ts.st);
 }
 
@@ -761,102 +927,5 @@ __global__ void __launch_bounds__(kSerThreads)
   state_store(S, &sm);
 }
 
-// KKT scalars of the CUR iterate from the reduced sums (solver.cpp:83-107).
-__device__ __forceinline__ void kkt_from_sums(double nrm_q, double nrm_c, double bound,
-                                              double qy, double cx, double infeas,
-                                              double dual_sq, double* kkt) {
-  const double dual_core = __dadd_rn(qy, bound);
-  const double primal_obj = cx;
-  kkt[0] = fabs(__dsub_rn(dual_core, primal_obj)) /
-           __dadd_rn(__dadd_rn(1.0, fabs(dual_core)), fabs(primal_obj));
-  kkt[1] = sqrt(infeas) / __dadd_rn(1.0, nrm_q);
-  kkt[2] = sqrt(dual_sq) / __dadd_rn(1.0, nrm_c);
-  kkt[3] = primal_obj;
-}
-
-__device__ __forceinline__ void finish_solve(DevState* S, int status, int role, double g) {
-  S->status = status;
-  S->final_role = role;
-  S->g_final = g;
-  S->done = 1;
-}
-
-// The scalar part of one iteration of solve() (solver.cpp:188-215,241-247),
-// run by a single thread after every sum of the iteration is known.
-// elapsed_in >= 0: the wall clock agreed by all shards (sharded solve)
-__device__ __noinline__ void control_logic(const DevParams* P, DevState* S, double g2, double bound, double qy,
-                              double cx, double infeas, double dual_sq, double elapsed_in,
-                              double pw_in) {
-  double kkt[4];
-  kkt_from_sums(P->nrm_q, P->nrm_c, bound, qy, cx, infeas, dual_sq, kkt);
-  for (int q = 0; q < 4; ++q) S->kkt[q] = kkt[q];
-  const double gkn = sqrt(g2);
-  S->gkn = gkn;
-  S->aa_attempt = 0;
-  S->aa_ok = 0;
-  const uint64_t k = S->k;
-  const double elapsed = elapsed_in >= 0.0
-                             ? elapsed_in
-                             : (double)(globaltimer_ns() - S->t0_ns) * 1e-9 + P->wall_offset_s;
-  bool attempt = false;
-  do {
-    if (k == 0) {  // priming step, solver.cpp:168-172
-      S->g0n = gkn;
-      aapdhg_record* r = P->rec;
-      r->k = 0;
-      r->g_norm = gkn;
-      r->aa_step = 0;
-      r->i = 0;
-      r->j = 0;
-      break;
-    }
-    {  // the record of iterate k-1 takes the KKT of the produced iterate u_k
-      aapdhg_record* r = P->rec + (k - 1) % P->rec_cap;
-      r->r_gap = kkt[0];
-      r->r_primal = kkt[1];
-      r->r_dual = kkt[2];
-      r->objective = kkt[3];
-      r->elapsed_s = elapsed;
-      S->rec_complete = k;
-    }
-    const double kmax = smax(smax(kkt[0], kkt[1]), kkt[2]);
-    if (k == 1 && S->g0n == 0.0) { finish_solve(S, AAPDHG_SOLVE_FIXED_POINT_START, U_PREV, 0.0); break; }
-    if (P->kkt_terminate && kmax <= P->kkt_eps) { finish_solve(S, AAPDHG_SOLVE_KKT_TOL, U_CUR, gkn); break; }
-    if (gkn < P->toll) { finish_solve(S, AAPDHG_SOLVE_RESIDUAL_TOL, U_CUR, gkn); break; }
-    if (S->i + S->j >= P->max_iters) { finish_solve(S, AAPDHG_SOLVE_MAX_ITERS, U_CUR, gkn); break; }
-    if (elapsed >= P->max_wall_s) { finish_solve(S, AAPDHG_SOLVE_TIMEOUT, U_CUR, gkn); break; }
-
-    if (P->method != AAPDHG_METHOD_PDHG) {  // memory_push / FaaState::push
-      if (S->mem_size == P->cap) {
-        for (int t = 1; t < S->mem_size; ++t) S->mem_slots[t - 1] = S->mem_slots[t];
-        S->mem_slots[S->mem_size - 1] = S->push_slot;
-      } else {
-        S->mem_slots[S->mem_size++] = S->push_slot;
-      }
-    }
-    aapdhg_record* r = P->rec + k % P->rec_cap;
-    r->k = k;
-    r->g_norm = gkn;
-    r->aa_step = 0;
-    r->i = S->i;
-    r->j = S->j;
-    if (P->method != AAPDHG_METHOD_PDHG) {
-      // safeguard_pass, solver.cpp:59-62, with the host std::pow table
-      const double pw = pw_in >= 0.0           ? pw_in
-                        : S->i < P->pow_len ? P->pow_tab[S->i]
-                                          : pow((double)S->i + 1.0, -(1.0 + P->safeguard_eps));
-      attempt = gkn <= __dmul_rn(__dmul_rn(P->safeguard_d, S->g0n), pw);
-    }
-    if (attempt) S->aa_attempt = 1;
-    else S->j += 1;
-  } while (false);
-  // no AA attempt: the iteration ends here (the AA branch commits otherwise)
-  if (!S->done && !attempt) advance(P, S);
-  const int left = S->done ? 0 : --S->batch_left;
-  if (P->use_cond) {
-    cudaGraphSetConditional(P->cond_aa, attempt ? 1u : 0u);
-    cudaGraphSetConditional(P->cond_loop, left > 0 ? 1u : 0u);
-  }
-}
 
 }  // namespace aapdhg_b200
