@@ -370,6 +370,22 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// g_k = T(u_k) - u_k of an iteration that attempts an AA step (the Gram
+// rhs and the mix read it; the next iteration's push reads it as g_{k-1}
+// when the candidate is accepted). K1/K2 do not store g: after a plain step
+// the push derives g_{k-1} from du (solver.cpp:204-209).
+__global__ void k_stage_g(const double* __restrict__ upool, double* __restrict__ gpool,
+                          const DevParams* __restrict__ P, const DevState* S) {
+  if (S->done || !S->aa_attempt) return;
+  const int64_t N = P->N;
+  const double* uh = upool + (int64_t)S->u_idx[U_HAT] * N;
+  const double* u = upool + (int64_t)S->u_idx[U_CUR] * N;
+  double* g = gpool + (int64_t)S->g_idx[G_CUR] * N;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N;
+       t += (int64_t)gridDim.x * blockDim.x)
+    g[t] = __dsub_rn(uh[t], u[t]);
+}
+
 // End of an iteration that attempted an AA step (the IF body of the graph):
 // rotate to the candidate (or to T(u) after a SingularError fallback).
 __global__ void k_aa_commit(const DevParams* __restrict__ P, DevState* S) {

@@ -124,6 +124,8 @@ struct DevState {
   uint64_t t0_ns;
   uint64_t loop_iters;             // iterations that did work (launch accounting)
   uint32_t ticket;                 // last-CTA election in k_primal_side
+  int32_t prev_plain;              // the previous step was T(u_{k-1}) (not an AA candidate)
+  int32_t pad_pp;
   int32_t batch_left;              // iterations left in this graph launch
 };
 

@@ -574,6 +574,7 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
 int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
   int nodes = 0;
   if (su.method == AAPDHG_METHOD_PDHG) return 0;
+  LAUNCH("k_stage_g", k_stage_g<<<grid_for(N_), kThreads, 0, s>>>(su.B.upool, su.B.gpool, su.P, su.S));
   if (su.serial) {
     const int blocks = (su.items_max * 32 + kThreads - 1) / kThreads;
     LAUNCH("k_serial_dots", k_serial_dots<<<blocks, kThreads, 0, s>>>(su.D, su.P, su.S));
@@ -814,6 +815,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.ndot_blk = ndot_tile_;
 
   DevState S0{};
+  S0.prev_plain = 1;
   for (int r = 0; r < 4; ++r) S0.u_idx[r] = r;
   for (int r = 0; r < 3; ++r) S0.kx_idx[r] = r;
   S0.g_idx[0] = 0;
@@ -975,6 +977,7 @@ void Problem::matvec_transpose(const double* y, double* out) {
 
 static DevState identity_state() {
   DevState S{};
+  S.prev_plain = 1;
   for (int r = 0; r < 4; ++r) S.u_idx[r] = r;
   for (int r = 0; r < 3; ++r) S.kx_idx[r] = r;
   S.g_idx[0] = 0;
@@ -1217,6 +1220,7 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   P.store_T = 1;
 
   DevState S0 = DevState{};
+  S0.prev_plain = 1;
   for (int r = 0; r < 4; ++r) S0.u_idx[r] = r;
   for (int r = 0; r < 3; ++r) S0.kx_idx[r] = r;
   S0.g_idx[0] = 0;
@@ -1318,6 +1322,8 @@ void Problem::sh_read_state(DevState* out) {
 
 void Problem::sh_aa_dots() {
   const SolveSetup& su = *sh_su_;
+  k_stage_g<<<grid_for(N_), kThreads, 0, stream_>>>(su.B.upool, su.B.gpool, su.P, su.S);
+  ++sh_launches_;
   k_tree_dots<<<su.ndot_blk, kThreads, 0, stream_>>>(su.D, su.P, su.S);
   k_dot_totals<<<1, 1024, 0, stream_>>>(su.D, su.P, su.S,
                                          dots_all_.as<double>() + shard_rank_ * dot_stride_);

@@ -174,6 +174,7 @@ __device__ __forceinline__ void advance(const DevParams* P, DevState* S) {
       S->push_slot = S->mem_slots[0];
     }
   }
+  S->prev_plain = S->aa_ok ? 0 : 1;
   S->aa_attempt = 0;
   S->aa_ok = 0;
   S->k += 1;
@@ -667,10 +668,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
         l2_prefetch(B.c + r);
         l2_prefetch(B.l + r);
         l2_prefetch(B.u + r);
-        if constexpr (PUSH) {
-          l2_prefetch(B.upool + (int64_t)S->u_idx[U_PREV] * N + r);
-          l2_prefetch(B.gpool + (int64_t)S->g_idx[G_PREV] * N + r);
-        }
+        if constexpr (PUSH) l2_prefetch(B.upool + (int64_t)S->u_idx[U_PREV] * N + r);
       });
   if (B.rinit1 && j >= 0) t = __dadd_rn(B.rinit1[j], t);  // earlier column passes
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
@@ -696,12 +694,14 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     acc[P1_DUALSQ] = __dmul_rn(dv, dv);
     acc[P1_CX] = __dmul_rn(cj, xj);
     if constexpr (PUSH) {
+      // after a plain step u_k = T(u_{k-1}) bit for bit, so g_{k-1} = u_k -
+      // u_{k-1} = du: g is only materialized (k_stage_g) for AA attempts
       const int64_t slot = S->push_slot;
       const double xp = B.upool[(int64_t)S->u_idx[U_PREV] * N + j];
-      const double gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + j];
-      B.du[slot * N + j] = __dsub_rn(xj, xp);
+      const double dx = __dsub_rn(xj, xp);
+      const double gp = S->prev_plain ? dx : B.gpool[(int64_t)S->g_idx[G_PREV] * N + j];
+      B.du[slot * N + j] = dx;
       B.dg[slot * N + j] = __dsub_rn(d, gp);
-      B.gpool[(int64_t)S->g_idx[G_CUR] * N + j] = d;
     }
     if (SERIAL || P->store_T) B.T[j] = t;
   }
@@ -748,10 +748,10 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     if constexpr (PUSH) {
       const int64_t slot = S->push_slot;
       const double yp = B.upool[(int64_t)S->u_idx[U_PREV] * N + n + i];
-      const double gp = B.gpool[(int64_t)S->g_idx[G_PREV] * N + n + i];
-      B.du[slot * N + n + i] = __dsub_rn(yi, yp);
+      const double dy = __dsub_rn(yi, yp);
+      const double gp = S->prev_plain ? dy : B.gpool[(int64_t)S->g_idx[G_PREV] * N + n + i];
+      B.du[slot * N + n + i] = dy;
       B.dg[slot * N + n + i] = __dsub_rn(d, gp);
-      B.gpool[(int64_t)S->g_idx[G_CUR] * N + n + i] = d;
     }
   }
   if (!SERIAL) {
