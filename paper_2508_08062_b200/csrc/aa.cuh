@@ -113,6 +113,54 @@ __device__ bool dev_cholesky_solve(int p, double* a, double* rhs) {
   return true;
 }
 
+// dev_cholesky_solve on a whole CTA (a, rhs in shared memory; every thread
+// calls it). Each entry sees exactly the operations of the one-thread
+// version in the same order — the row updates of a column run in parallel,
+// the forward substitution is applied column by column (each rhs_k still
+// subtracts A_k0 r0, A_k1 r1, ... in that order), the backward one stays
+// row by row — so the result is bit for bit the same.
+__device__ bool block_cholesky_solve(int p, double* a, double* rhs) {
+#define A_(i, j) a[(j) * p + (i)]
+  __shared__ double dsh;
+  __shared__ int bad;
+  for (int j = 0; j < p; ++j) {
+    if (threadIdx.x == 0) {
+      double d = A_(j, j);
+      for (int k = 0; k < j; ++k) d = __dsub_rn(d, __dmul_rn(A_(j, k), A_(j, k)));
+      bad = d <= 0.0;
+      if (!bad) {
+        d = sqrt(d);
+        A_(j, j) = d;
+      }
+      dsh = d;
+    }
+    __syncthreads();
+    if (bad) return false;
+    for (int i = j + 1 + int(threadIdx.x); i < p; i += blockDim.x) {
+      double s = A_(i, j);
+      for (int k = 0; k < j; ++k) s = __dsub_rn(s, __dmul_rn(A_(i, k), A_(j, k)));
+      A_(i, j) = s / dsh;
+    }
+    __syncthreads();
+  }
+  for (int i = 0; i < p; ++i) {
+    if (threadIdx.x == 0) rhs[i] = rhs[i] / A_(i, i);
+    __syncthreads();
+    for (int k = i + 1 + int(threadIdx.x); k < p; k += blockDim.x)
+      rhs[k] = __dsub_rn(rhs[k], __dmul_rn(A_(k, i), rhs[i]));
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int i = p - 1; i >= 0; --i) {
+      double s = rhs[i];
+      for (int k = i + 1; k < p; ++k) s = __dsub_rn(s, __dmul_rn(A_(k, i), rhs[k]));
+      rhs[i] = s / A_(i, i);
+    }
+  __syncthreads();
+#undef A_
+  return true;
+}
+
 // length_bounds, filtering.cpp:92-114 (fn_sq of the kept columns, newest first)
 __device__ void dev_length_bounds(int m, const double* fn_sq, double c_s, double* b) {
   if (m == 0) return;
@@ -175,37 +223,55 @@ __global__ void __launch_bounds__(1024)
     for (int it = warp; it < nit; it += nw) {
       const double* pp = D.part + (int64_t)it * P->ndot_blk;
       double s = 0.0;
-      for (int b = lane; b < P->ndot_blk; b += 32) s = __dadd_rn(s, pp[b]);
+      // groups of 8 strides: the loads of a group are in flight together,
+      // the adds keep the order b, b + 32, ...
+      for (int b0 = lane; b0 < P->ndot_blk; b0 += 32 * 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = b0 + 32 * u < P->ndot_blk ? __ldcg(pp + b0 + 32 * u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (b0 + 32 * u < P->ndot_blk) s = __dadd_rn(s, x[u]);
+      }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       if (lane == 0) vals[it] = s;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
   const int npair = p * (p + 1) / 2;
-  double* G = W.gram;  // p x p column-major, full symmetric
-  {
-    int it = 0;
-    for (int a = 0; a < p; ++a)
-      for (int b = a; b < p; ++b, ++it) {
-        G[b * p + a] = vals[it];
-        G[a * p + b] = vals[it];
-      }
+  double* G = W.gram;  // p x p column-major, full symmetric (item (a<=b) row-major upper)
+  for (int t = threadIdx.x; t < p * p; t += blockDim.x) {
+    const int r = t % p, c = t / p, lo = r < c ? r : c, hi = r < c ? c : r;
+    G[t] = vals[lo * p - lo * (lo - 1) / 2 + (hi - lo)];
   }
+  __syncthreads();
+  // AA: G + eta tr(G) I, factored by the whole CTA (anderson.cpp:106-128)
+  __shared__ int aa_solved;
+  if (P->method == AAPDHG_METHOD_AA) {
+    __shared__ double eta_eff_sh;
+    if (threadIdx.x == 0) {
+      double frob_sq = 0.0;
+      for (int i = 0; i < p; ++i) frob_sq = __dadd_rn(frob_sq, G[i * p + i]);
+      eta_eff_sh = __dmul_rn(P->eta, frob_sq);
+    }
+    __syncthreads();
+    double* A = W.work;
+    for (int t = threadIdx.x; t < p * p; t += blockDim.x)
+      A[t] = (t % p == t / p) ? __dadd_rn(G[t], eta_eff_sh) : G[t];
+    for (int i = threadIdx.x; i < p; i += blockDim.x) W.vec[i] = vals[npair + i];
+    __syncthreads();
+    const bool solved = block_cholesky_solve(p, A, W.vec);
+    if (threadIdx.x == 0) aa_solved = solved ? 1 : 0;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
   const double* rhs = vals + npair;
   double* w = W.vec;  // p
   bool ok = true;
   int pm = 0;         // mixed columns
   if (P->method == AAPDHG_METHOD_AA) {
-    double frob_sq = 0.0;
-    for (int i = 0; i < p; ++i) frob_sq = __dadd_rn(frob_sq, G[i * p + i]);
-    const double eta_eff = __dmul_rn(P->eta, frob_sq);
-    double* A = W.work;
-    for (int t = 0; t < p * p; ++t) A[t] = G[t];
-    for (int i = 0; i < p; ++i) A[i * p + i] = __dadd_rn(A[i * p + i], eta_eff);
-    for (int i = 0; i < p; ++i) w[i] = rhs[i];
-    ok = dev_cholesky_solve(p, A, w);
+    ok = aa_solved != 0;
     if (ok) {
       pm = p;
       for (int t = 0; t < p; ++t) S->mix_slots[t] = S->mem_slots[t];
