@@ -63,20 +63,136 @@ __global__ void k_serial_dots(DotBufs D, const DevParams* __restrict__ P, const 
 __global__ void __launch_bounds__(kThreads)
     k_tree_dots(DotBufs D, const DevParams* __restrict__ P, const DevState* S) {
   if (S->done || !S->aa_attempt) return;
-  const int p = S->mem_size;
+  // the memory's slot table once per CTA (not a dependent global load per item)
+  __shared__ int slots[kMaxMemory];
+  __shared__ int sh_p, sh_g;
+  if (threadIdx.x < kMaxMemory) slots[threadIdx.x] = S->mem_slots[threadIdx.x];
+  if (threadIdx.x == 0) {
+    sh_p = S->mem_size;
+    sh_g = S->g_idx[G_CUR];
+  }
+  __syncthreads();
+  const int p = sh_p;
   const int nit = num_items(p, P->method);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * kDotChunk;
   const int64_t N = P->N;
   const int cnt = (int)((N - base) < kDotChunk ? (N - base) : kDotChunk);
+  constexpr int kPer = kDotChunk / 32;
   for (int item = warp; item < nit; item += kThreads / 32) {
+    int kind, ia, ib;
+    decode_item(item, p, kind, ia, ib);
     const double *va, *vb;
-    item_vectors(D, P, S, item, p, va, vb);
+    if (kind == 0) { va = D.dg + slots[ia] * N; vb = D.dg + slots[ib] * N; }
+    else if (kind == 1) { va = D.dg + slots[ia] * N; vb = D.gpool + (int64_t)sh_g * N; }
+    else { va = D.du + slots[ia] * N; vb = va; }
+    // every load of the lane's share in flight before the adds (same order:
+    // t = lane, lane + 32, ...)
+    double x[kPer], y[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int t = lane + 32 * u;
+      x[u] = t < cnt ? va[base + t] : 0.0;
+      y[u] = t < cnt ? vb[base + t] : 0.0;
+    }
     double s = 0.0;
-    for (int t = lane; t < cnt; t += 32) s = __dadd_rn(s, __dmul_rn(va[base + t], vb[base + t]));
+#pragma unroll
+    for (int u = 0; u < kPer; ++u)
+      if (lane + 32 * u < cnt) s = __dadd_rn(s, __dmul_rn(x[u], y[u]));
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     if (lane == 0) D.part[(int64_t)item * P->ndot_blk + blockIdx.x] = s;
+  }
+}
+
+// TREE, memory capacity <= CAP (<= 10): the whole Gram / rhs / column-norm
+// set in registers. Each thread loads the p + 1 (FAA: 2p + 1) vectors at its
+// elements once — grid-stride, element order — and accumulates every item;
+// the CTA then reduces each item over its warps in a fixed shape into
+// part[item * gridDim.x + blockIdx.x]. One HBM read of each column instead of
+// one L1 read per item that uses it (k_tree_dots). Also stages g = T(u) - u
+// (k_stage_g), which the mix reads next.
+template <int CAP, bool FAA>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gram_dots(DotBufs D, double* __restrict__ upool, const DevParams* __restrict__ P,
+                const DevState* S) {
+  if (S->done || !S->aa_attempt) return;
+  constexpr int NPAIR = CAP * (CAP + 1) / 2;
+  constexpr int NACC = NPAIR + CAP + (FAA ? CAP : 0);
+  __shared__ int slots[CAP];
+  __shared__ int sh_p, sh_g, sh_h, sh_c;
+  if (threadIdx.x < CAP) slots[threadIdx.x] = S->mem_slots[threadIdx.x];
+  if (threadIdx.x == 0) {
+    sh_p = S->mem_size;
+    sh_g = S->g_idx[G_CUR];
+    sh_h = S->u_idx[U_HAT];
+    sh_c = S->u_idx[U_CUR];
+  }
+  __syncthreads();
+  const int p = sh_p;
+  const int64_t N = P->N;
+  const double* dgc[CAP];
+  const double* duc[CAP];
+#pragma unroll
+  for (int a = 0; a < CAP; ++a) {
+    dgc[a] = D.dg + (int64_t)(a < p ? slots[a] : 0) * N;
+    duc[a] = D.du + (int64_t)(a < p ? slots[a] : 0) * N;
+  }
+  const double* uh = upool + (int64_t)sh_h * N;
+  const double* uc = upool + (int64_t)sh_c * N;
+  double* g = const_cast<double*>(D.gpool) + (int64_t)sh_g * N;
+  double acc[NACC];
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const double gt = __dsub_rn(uh[t], uc[t]);
+    g[t] = gt;
+    double v[CAP];
+#pragma unroll
+    for (int a = 0; a < CAP; ++a) v[a] = a < p ? dgc[a][t] : 0.0;
+    int q = 0;
+#pragma unroll
+    for (int a = 0; a < CAP; ++a)
+#pragma unroll
+      for (int b = a; b < CAP; ++b, ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v[a], v[b]));
+#pragma unroll
+    for (int a = 0; a < CAP; ++a) acc[NPAIR + a] = __dadd_rn(acc[NPAIR + a], __dmul_rn(v[a], gt));
+    if constexpr (FAA) {
+#pragma unroll
+      for (int a = 0; a < CAP; ++a) {
+        const double e = a < p ? duc[a][t] : 0.0;
+        acc[NPAIR + CAP + a] = __dadd_rn(acc[NPAIR + CAP + a], __dmul_rn(e, e));
+      }
+    }
+  }
+  // fixed-shape CTA reduction of every live item, written in p-space order
+  __shared__ double red[kWarps][NACC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) {
+    const double s = warp_sum(acc[q]);
+    if (lane == 0) red[warp][q] = s;
+  }
+  __syncthreads();
+  const int np = p * (p + 1) / 2;
+  for (int q = threadIdx.x; q < NACC; q += blockDim.x) {
+    double s = red[0][q];
+    for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, red[w][q]);
+    int item = -1;
+    if (q < NPAIR) {  // (a, b) in CAP space -> p space
+      int a = 0, rem = q;
+      while (rem >= CAP - a) { rem -= CAP - a; ++a; }
+      const int b = a + rem;
+      if (b < p) item = a * p - a * (a - 1) / 2 + (b - a);
+    } else if (q < NPAIR + CAP) {
+      const int a = q - NPAIR;
+      if (a < p) item = np + a;
+    } else {
+      const int a = q - NPAIR - CAP;
+      if (a < p) item = np + p + a;
+    }
+    if (item >= 0) D.part[(int64_t)item * gridDim.x + blockIdx.x] = s;
   }
 }
 

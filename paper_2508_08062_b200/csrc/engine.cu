@@ -396,7 +396,7 @@ void Problem::ensure_iter_buffers(int method, int cap) {
     du_.reserve(sizeof(double) * size_t(cap) * std::max<int64_t>(N_, 1));
     dg_.reserve(sizeof(double) * size_t(cap) * std::max<int64_t>(N_, 1));
     const int items = num_items_host(cap, AAPDHG_METHOD_FAA);
-    partdot_.reserve(sizeof(double) * size_t(items) * std::max(ndot_tile_, 1));
+    partdot_.reserve(sizeof(double) * size_t(items) * std::max(std::max(ndot_tile_, num_sms_), 1));
   }
 }
 
@@ -574,12 +574,22 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
 int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
   int nodes = 0;
   if (su.method == AAPDHG_METHOD_PDHG) return 0;
-  LAUNCH("k_stage_g", k_stage_g<<<grid_for(N_), kThreads, 0, s>>>(su.B.upool, su.B.gpool, su.P, su.S));
-  if (su.serial) {
-    const int blocks = (su.items_max * 32 + kThreads - 1) / kThreads;
-    LAUNCH("k_serial_dots", k_serial_dots<<<blocks, kThreads, 0, s>>>(su.D, su.P, su.S));
+  if (!su.serial && su.cap <= 10) {  // g staged inside the register Gram
+    const int c = su.cap <= 4 ? 4 : su.cap <= 6 ? 6 : su.cap <= 8 ? 8 : 10;
+    const bool faa = su.method == AAPDHG_METHOD_FAA;
+    auto kern = faa ? (c == 4 ? k_gram_dots<4, true> : c == 6 ? k_gram_dots<6, true>
+                       : c == 8 ? k_gram_dots<8, true> : k_gram_dots<10, true>)
+                    : (c == 4 ? k_gram_dots<4, false> : c == 6 ? k_gram_dots<6, false>
+                       : c == 8 ? k_gram_dots<8, false> : k_gram_dots<10, false>);
+    LAUNCH("k_gram_dots", kern<<<su.ndot_blk, kThreads, 0, s>>>(su.D, su.B.upool, su.P, su.S));
   } else {
-    LAUNCH("k_tree_dots", k_tree_dots<<<su.ndot_blk, kThreads, 0, s>>>(su.D, su.P, su.S));
+    LAUNCH("k_stage_g", k_stage_g<<<grid_for(N_), kThreads, 0, s>>>(su.B.upool, su.B.gpool, su.P, su.S));
+    if (su.serial) {
+      const int blocks = (su.items_max * 32 + kThreads - 1) / kThreads;
+      LAUNCH("k_serial_dots", k_serial_dots<<<blocks, kThreads, 0, s>>>(su.D, su.P, su.S));
+    } else {
+      LAUNCH("k_tree_dots", k_tree_dots<<<su.ndot_blk, kThreads, 0, s>>>(su.D, su.P, su.S));
+    }
   }
   LAUNCH("k_aa_solve", k_aa_solve<<<1, 1024, aa_smem(su.cap), s>>>(su.D, su.P, su.S, 0));
   LAUNCH("k_mix", k_mix<<<grid_for(N_), kThreads, 0, s>>>(su.B, su.B.dg, su.P, su.S, 1));
@@ -812,7 +822,9 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   const CsrDev& K2m = blk2 ? kb_.blk.back() : Km(serial);
   P.nblk1 = K1m.grid();
   P.nblk2 = K2m.grid();
-  P.ndot_blk = ndot_tile_;
+  // TREE with memory <= 10: one CTA per SM for the register Gram
+  const int ndot = (!serial && cap <= 10) ? num_sms_ : ndot_tile_;
+  P.ndot_blk = ndot;
 
   DevState S0{};
   S0.prev_plain = 1;
@@ -839,7 +851,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.cap = cap;
   su.nblk1 = K1m.grid();
   su.nblk2 = K2m.grid();
-  su.ndot_blk = ndot_tile_;
+  su.ndot_blk = ndot;
   su.items_max = num_items_host(std::max(cap, 1), method);
 
   // executable graph, cached per launch layout
