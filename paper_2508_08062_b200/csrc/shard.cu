@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -358,11 +359,13 @@ void ShardGroup::solve(const aapdhg_solve_params* prm, const double* x0, const d
   allgather(XG);
   each([&](Problem& s) { s.sh_init_kx(); });
 
-  DevState st{};
-  uint64_t flushed = 0;
-  std::vector<aapdhg_record> recs;
-  uint64_t collectives = 1;
-  for (;;) {
+  // One iteration: the core and the AA branch. The AA kernels are predicated
+  // on the device (they return unless an attempt / an accepted step is
+  // flagged) and the branch's all-gathers always run, so the host never
+  // needs the decision: iterations are enqueued back to back — as one
+  // captured CUDA graph per iteration (AAPDHG_SHARD_GRAPH=0: eager) — and
+  // the state is read once per batch.
+  auto iteration = [&] {
     each([&](Problem& s) { s.sh_stage_y(U_CUR, 1); });
     allgather(YG);
     each([&](Problem& s) { s.sh_k1(); });
@@ -370,7 +373,39 @@ void ShardGroup::solve(const aapdhg_solve_params* prm, const double* x0, const d
     each([&](Problem& s) { s.sh_k2_totals(); });
     allgather(SCAL);
     each([&](Problem& s) { s.sh_control(world_); });
-    collectives += 3;
+    each([&](Problem& s) { s.sh_aa_dots(); });
+    allgather(DOTS);
+    each([&](Problem& s) { s.sh_aa_solve_mix(world_); });
+    allgather(XG);
+    each([&](Problem& s) { s.sh_aa_recache_commit(); });
+  };
+  const char* ge = std::getenv("AAPDHG_SHARD_GRAPH");
+  const bool use_graph = !(ge && ge[0] == '0');
+  cudaGraphExec_t exec = nullptr;
+  uint64_t per_iter = 0;
+  {
+    uint64_t before = 0, after = 0;
+    each([&](Problem& s) { before += s.sh_launches(); });
+    if (use_graph) {
+      AAPDHG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+      iteration();
+      cudaGraph_t g = nullptr;
+      AAPDHG_CUDA(cudaStreamEndCapture(stream_, &g));
+      AAPDHG_CUDA(cudaGraphInstantiate(&exec, g, 0));
+      cudaGraphDestroy(g);
+      each([&](Problem& s) { after += s.sh_launches(); });
+      per_iter = after - before;
+    }
+  }
+  DevState st{};
+  uint64_t flushed = 0;
+  std::vector<aapdhg_record> recs;
+  uint64_t batch = 8;
+  for (;;) {
+    for (uint64_t b = 0; b < batch; ++b) {
+      if (use_graph) AAPDHG_CUDA(cudaGraphLaunch(exec, stream_));
+      else iteration();
+    }
     shards_[0]->sh_read_state(&st);
     if (st.rec_complete > flushed) {
       const uint64_t cnt = st.rec_complete - flushed;
@@ -380,15 +415,9 @@ void ShardGroup::solve(const aapdhg_solve_params* prm, const double* x0, const d
       flushed = st.rec_complete;
     }
     if (st.done) break;
-    if (st.aa_attempt) {
-      each([&](Problem& s) { s.sh_aa_dots(); });
-      allgather(DOTS);
-      each([&](Problem& s) { s.sh_aa_solve_mix(world_); });
-      allgather(XG);
-      each([&](Problem& s) { s.sh_aa_recache_commit(); });
-      collectives += 2;
-    }
+    batch = std::min<uint64_t>(batch * 2, 4096);  // <= half the device record ring
   }
+  if (exec) cudaGraphExecDestroy(exec);
 
   // finish, solver.cpp:153-166: the final iterate, K'y-based lambda; the KKT
   // of the final iterate is the one its own control step evaluated
@@ -434,7 +463,7 @@ void ShardGroup::solve(const aapdhg_solve_params* prm, const double* x0, const d
   last_loop_iters_ = st.loop_iters;
   last_launches_ = 0;
   each([&](Problem& s) { last_launches_ += s.sh_launches(); });
-  (void)collectives;
+  if (use_graph) last_launches_ += per_iter * st.loop_iters;
 }
 
 }  // namespace aapdhg_b200
