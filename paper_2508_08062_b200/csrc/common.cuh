@@ -101,6 +101,7 @@ struct DevParams {
   const double* xgather;
   const double* ygather;
   double* xg_own;
+  double* yg_own;  // K2 writes yhat into this shard's chunk of ygather
   int32_t store_T, pad_sh;
   int64_t Nglob;  // n + m of the whole LP (FAA's QR row-count test)
 };
@@ -164,7 +165,9 @@ struct IterBufs {
   const double* rinit1;  // L2-blocked K': partial K'y of the earlier column passes
   const double* rinit2;  // L2-blocked K: partial K xhat of the earlier passes
   int32_t nu1;        // K1 CTAs (rows of part1)
-  int32_t fused_ctrl; // TREE solve: k_primal_side's last CTA runs the control
+  int32_t fused_ctrl; // TREE: k_primal_side's last CTA runs the control (1) or,
+                      // sharded, writes this shard's 8 totals to scal_own (2)
+  double* scal_own;
   const double* c;
   const double* q;
   const double* l;

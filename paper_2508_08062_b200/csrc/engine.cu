@@ -839,7 +839,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.B.nu1 = n_ > 0 ? K1m.grid() : 0;
   su.B.rinit1 = blk1 ? ktb_.partial.as<double>() : nullptr;
   su.B.rinit2 = blk2 ? kb_.partial.as<double>() : nullptr;
-  su.B.fused_ctrl = (!serial && m_ > 0) ? env_int("AAPDHG_FUSED", 1) : 0;
+  su.B.fused_ctrl = (!serial && m_ > 0 && env_int("AAPDHG_FUSED", 1) != 0) ? 1 : 0;
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
                  partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
   su.W = SolveScratch{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
@@ -1229,6 +1229,7 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   P.xgather = xg_.as<double>();
   P.ygather = yg_.as<double>();
   P.xg_own = xg_.as<double>() + int64_t(shard_rank_) * maxc_;
+  P.yg_own = yg_.as<double>() + int64_t(shard_rank_) * maxr_;
   P.store_T = 1;
 
   DevState S0 = DevState{};
@@ -1243,7 +1244,8 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   SolveSetup& su = *sh_su_;
   su.B = iter_bufs();
   su.B.nu1 = sh_k1m().grid();
-  su.B.fused_ctrl = 0;
+  su.B.fused_ctrl = 2;  // K2's last CTA writes this shard's totals
+  su.B.scal_own = scal_all_.as<double>() + shard_rank_ * 8;
   su.B.rinit1 = ktb_.nb() > 1 ? ktb_.partial.as<double>() : nullptr;
   su.B.rinit2 = kb_.nb() > 1 ? kb_.partial.as<double>() : nullptr;
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
@@ -1264,6 +1266,7 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   if (method != AAPDHG_METHOD_PDHG)
     AAPDHG_CUDA(cudaMemsetAsync(gpool_.p, 0, sizeof(double) * 2 * N_, stream_));
   upload_iterate(0, x0, y0);
+  sh_params_ = P;
   h2d(dparams_.p, &P, sizeof P, stream_);
   h2d(S, &S0, sizeof S0, stream_);
   k_project_start<<<grid_for(N_, kThreads, 1 << 30), kThreads, 0, stream_>>>(
@@ -1313,11 +1316,23 @@ void Problem::sh_k2_totals() {
     k_primal_side<false, true><<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
   else
     k_primal_side<false, false><<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
-  k_local_totals<<<1, kThreads, 0, stream_>>>(part1_.as<double>(), sh_k1m().grid(),
-                                               part2_.as<double>(), A.grid(), su.P, su.S,
-                                               scal_all_.as<double>() + shard_rank_ * 8);
   AAPDHG_CUDA(cudaGetLastError());
-  sh_launches_ += 2;
+  ++sh_launches_;  // (its last CTA writes this shard's totals: fused_ctrl = 2)
+}
+
+// The sharded graph's IF (AA branch) / WHILE (batch) conditions, set by the
+// replicated control of every shard (identical decisions on every shard).
+void Problem::sh_set_conditions(cudaGraphConditionalHandle aa, cudaGraphConditionalHandle loop) {
+  sh_params_.use_cond = (aa || loop) ? 1 : 0;
+  sh_params_.cond_aa = aa;
+  sh_params_.cond_loop = loop;
+  h2d(dparams_.p, &sh_params_, sizeof sh_params_, stream_);
+  sync();
+}
+
+void Problem::sh_set_batch(int32_t left) {
+  h_batch_[0] = left;
+  h2d(&sh_su_->S->batch_left, h_batch_, sizeof(int32_t), stream_);
 }
 
 void Problem::sh_control(int world) {
@@ -1350,7 +1365,8 @@ void Problem::sh_aa_solve_mix(int world) {
   k_mix<<<grid_for(N_), kThreads, 0, stream_>>>(su.B, su.B.dg, su.P, su.S, 1);
   AAPDHG_CUDA(cudaGetLastError());
   sh_launches_ += 2;
-  sh_stage_x(U_CAND, 2);
+  sh_stage_x(U_CAND, 2);  // an accepted candidate replaces xhat / yhat in the
+  sh_stage_y(U_CAND, 2);  // all-gather chunks (K1 / K2 wrote those)
 }
 
 void Problem::sh_aa_recache_commit() {

@@ -81,6 +81,8 @@ class Problem {
   void sh_k1();                         // K'y + xhat (+ own chunk of xg)
   void sh_k2_totals();                  // K xhat + yhat, then own iteration totals
   void sh_control(int world);           // after AG of scal
+  void sh_set_conditions(cudaGraphConditionalHandle aa, cudaGraphConditionalHandle loop);
+  void sh_set_batch(int32_t left);       // iterations the next graph launch may run
   void sh_read_state(DevState* out);    // synchronous
   void sh_aa_dots();                    // own dot totals (AA attempt)
   void sh_aa_solve_mix(int world);      // after AG of dots; candidate x -> xg
@@ -193,6 +195,7 @@ class Problem {
   int64_t maxc_ = 0, maxr_ = 0, dot_stride_ = 0;
   DevBuf xg_, yg_, lg_, scal_all_, dots_all_;
   SolveSetup* sh_su_ = nullptr;
+  DevParams sh_params_{};
   uint64_t sh_launches_ = 0;
   bool all_zero_ = true;
   bool bounds_ok_ = true;

@@ -604,6 +604,21 @@ __device__ __forceinline__ void fused_control_tail(const IterBufs& B, const DevP
   reduce_partial_rows<P2_COUNT>(B.part2, gridDim.x, t2, red);
   cp_async_wait_all();
   __syncthreads();
+  if (B.fused_ctrl == 2) {  // sharded: this shard's totals (k_local_totals' layout)
+    if (threadIdx.x == 0) {
+      double* own = B.scal_own;
+      own[0] = __ldcg(&S->tot1[P1_GX2]);
+      own[1] = __ldcg(&S->tot1[P1_BOUND]);
+      own[2] = __ldcg(&S->tot1[P1_CX]);
+      own[3] = __ldcg(&S->tot1[P1_DUALSQ]);
+      own[4] = t2[P2_GY2];
+      own[5] = t2[P2_QY];
+      own[6] = t2[P2_INFEAS];
+      own[7] = (double)(globaltimer_ns() - ts.st.t0_ns) * 1e-9 + ts.pr.wall_offset_s;
+      S->ticket = 0;
+    }
+    return;
+  }
   // the control on two warps: KKT + records (warp 1) beside the decision and
   // the graph conditions (warp 0); the commit needs the decision
   __shared__ double sums[7];
@@ -738,6 +753,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
         __dadd_rn(yi, __dmul_rn(P->sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
     if (i < P->m1) yn = smax(yn, 0.0);
     B.upool[(int64_t)S->u_idx[U_HAT] * N + n + i] = yn;
+    if (P->yg_own) P->yg_own[i] = yn;
     B.kxpool[(int64_t)S->kx_idx[KX_HAT] * mr + i] = s;
     const double d = __dsub_rn(yn, yi);
     double v = __dsub_rn(qi, kxi);

@@ -359,52 +359,125 @@ void ShardGroup::solve(const aapdhg_solve_params* prm, const double* x0, const d
   allgather(XG);
   each([&](Problem& s) { s.sh_init_kx(); });
 
-  // One iteration: the core and the AA branch. The AA kernels are predicated
-  // on the device (they return unless an attempt / an accepted step is
-  // flagged) and the branch's all-gathers always run, so the host never
-  // needs the decision: iterations are enqueued back to back — as one
-  // captured CUDA graph per iteration (AAPDHG_SHARD_GRAPH=0: eager) — and
-  // the state is read once per batch.
-  auto iteration = [&] {
-    each([&](Problem& s) { s.sh_stage_y(U_CUR, 1); });
+  // One iteration: the core, then the AA branch. Preferred form: the same
+  // graph as on one GPU — WHILE(batch) { core; IF(attempt) { AA branch } },
+  // both conditions set by the replicated control, NCCL all-gathers captured
+  // in the bodies — so the host launches one graph per batch. If the driver
+  // or NCCL cannot capture that, fall back to one captured graph per
+  // iteration with the AA branch predicated on the device (its all-gathers
+  // then always run).
+  auto core = [&] {
     allgather(YG);
     each([&](Problem& s) { s.sh_k1(); });
     allgather(XG);
     each([&](Problem& s) { s.sh_k2_totals(); });
     allgather(SCAL);
     each([&](Problem& s) { s.sh_control(world_); });
+  };
+  auto aa_branch = [&] {
     each([&](Problem& s) { s.sh_aa_dots(); });
     allgather(DOTS);
     each([&](Problem& s) { s.sh_aa_solve_mix(world_); });
     allgather(XG);
     each([&](Problem& s) { s.sh_aa_recache_commit(); });
   };
+  // y of the start iterate; afterwards K2 (yhat) or the accepted candidate
+  // writes each shard's chunk
+  each([&](Problem& s) { s.sh_stage_y(-1, 0); });
   const char* ge = std::getenv("AAPDHG_SHARD_GRAPH");
-  const bool use_graph = !(ge && ge[0] == '0');
+  const int mode = ge && *ge ? std::atoi(ge) : 2;  // 2 WHILE/IF, 1 per iteration, 0 eager
   cudaGraphExec_t exec = nullptr;
-  uint64_t per_iter = 0;
-  {
-    uint64_t before = 0, after = 0;
-    each([&](Problem& s) { before += s.sh_launches(); });
-    if (use_graph) {
-      AAPDHG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-      iteration();
-      cudaGraph_t g = nullptr;
-      AAPDHG_CUDA(cudaStreamEndCapture(stream_, &g));
+  bool cond_graph = false;
+  uint64_t core_nodes = 0, aa_nodes = 0;
+  auto launches = [&] {
+    uint64_t t = 0;
+    each([&](Problem& s) { t += s.sh_launches(); });
+    return t;
+  };
+  if (mode == 2) {
+    cudaGraph_t g = nullptr;
+    try {
+      const cudaStreamCaptureMode cm = cudaStreamCaptureModeThreadLocal;
+      AAPDHG_CUDA(cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle h_loop = 0, h_aa = 0;
+      AAPDHG_CUDA(cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams wp{};
+      wp.type = cudaGraphNodeTypeConditional;
+      wp.conditional.handle = h_loop;
+      wp.conditional.type = cudaGraphCondTypeWhile;
+      wp.conditional.size = 1;
+      cudaGraphNode_t wnode;
+      AAPDHG_CUDA(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+      cudaGraph_t body = wp.conditional.phGraph_out[0];
+      uint64_t l0 = launches();
+      AAPDHG_CUDA(cudaStreamBeginCaptureToGraph(stream_, body, nullptr, nullptr, 0, cm));
+      core();
+      cudaStreamCaptureStatus cst;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t ndeps = 0;
+      AAPDHG_CUDA(cudaStreamGetCaptureInfo(stream_, &cst, nullptr, nullptr, &deps, &ndeps));
+      std::vector<cudaGraphNode_t> tail(deps, deps + ndeps);
+      cudaGraph_t cap = nullptr;
+      AAPDHG_CUDA(cudaStreamEndCapture(stream_, &cap));
+      core_nodes = launches() - l0;
+      AAPDHG_CUDA(cudaGraphConditionalHandleCreate(&h_aa, body, 0, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams ip{};
+      ip.type = cudaGraphNodeTypeConditional;
+      ip.conditional.handle = h_aa;
+      ip.conditional.type = cudaGraphCondTypeIf;
+      ip.conditional.size = 1;
+      cudaGraphNode_t inode;
+      AAPDHG_CUDA(cudaGraphAddNode(&inode, body, tail.data(), tail.size(), &ip));
+      l0 = launches();
+      AAPDHG_CUDA(cudaStreamBeginCaptureToGraph(stream_, ip.conditional.phGraph_out[0], nullptr,
+                                                nullptr, 0, cm));
+      aa_branch();
+      AAPDHG_CUDA(cudaStreamEndCapture(stream_, &cap));
+      aa_nodes = launches() - l0;
       AAPDHG_CUDA(cudaGraphInstantiate(&exec, g, 0));
-      cudaGraphDestroy(g);
-      each([&](Problem& s) { after += s.sh_launches(); });
-      per_iter = after - before;
+      each([&](Problem& s) { s.sh_set_conditions(h_aa, h_loop); });
+      cond_graph = true;
+    } catch (const CudaError&) {
+      cudaStreamCaptureStatus cst;
+      if (cudaStreamIsCapturing(stream_, &cst) == cudaSuccess &&
+          cst != cudaStreamCaptureStatusNone) {
+        cudaGraph_t junk = nullptr;
+        cudaStreamEndCapture(stream_, &junk);
+        if (junk) cudaGraphDestroy(junk);
+      }
+      cudaGetLastError();
+      if (exec) cudaGraphExecDestroy(exec);
+      exec = nullptr;
     }
+    if (g) cudaGraphDestroy(g);
+  }
+  if (!cond_graph && mode >= 1) {
+    const uint64_t l0 = launches();
+    AAPDHG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    core();
+    aa_branch();
+    cudaGraph_t g = nullptr;
+    AAPDHG_CUDA(cudaStreamEndCapture(stream_, &g));
+    AAPDHG_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    cudaGraphDestroy(g);
+    core_nodes = launches() - l0;
   }
   DevState st{};
   uint64_t flushed = 0;
   std::vector<aapdhg_record> recs;
   uint64_t batch = 8;
   for (;;) {
-    for (uint64_t b = 0; b < batch; ++b) {
-      if (use_graph) AAPDHG_CUDA(cudaGraphLaunch(exec, stream_));
-      else iteration();
+    if (cond_graph) {
+      each([&](Problem& s) { s.sh_set_batch(int32_t(batch)); });
+      AAPDHG_CUDA(cudaGraphLaunch(exec, stream_));
+    } else {
+      for (uint64_t b = 0; b < batch; ++b) {
+        if (exec) AAPDHG_CUDA(cudaGraphLaunch(exec, stream_));
+        else {
+          core();
+          aa_branch();
+        }
+      }
     }
     shards_[0]->sh_read_state(&st);
     if (st.rec_complete > flushed) {
@@ -418,6 +491,12 @@ void ShardGroup::solve(const aapdhg_solve_params* prm, const double* x0, const d
     batch = std::min<uint64_t>(batch * 2, 4096);  // <= half the device record ring
   }
   if (exec) cudaGraphExecDestroy(exec);
+  if (cond_graph) {  // plain control again for later solves
+    each([&](Problem& s) { s.sh_set_conditions(0, 0); });
+  }
+  const uint64_t graph_launches =
+      cond_graph ? st.loop_iters * core_nodes + (st.i + st.aa_failures) * aa_nodes
+                 : (exec ? st.loop_iters * core_nodes : 0);
 
   // finish, solver.cpp:153-166: the final iterate, K'y-based lambda; the KKT
   // of the final iterate is the one its own control step evaluated
@@ -463,7 +542,7 @@ void ShardGroup::solve(const aapdhg_solve_params* prm, const double* x0, const d
   last_loop_iters_ = st.loop_iters;
   last_launches_ = 0;
   each([&](Problem& s) { last_launches_ += s.sh_launches(); });
-  if (use_graph) last_launches_ += per_iter * st.loop_iters;
+  last_launches_ += graph_launches;
 }
 
 }  // namespace aapdhg_b200

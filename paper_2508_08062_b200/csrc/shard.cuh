@@ -29,30 +29,6 @@ __global__ void k_stage(const double* __restrict__ upool, int role, int64_t N, i
     dst[t] = src[t];
 }
 
-// This shard's 7 partial sums of the iteration (K1 and K2 per-CTA partials
-// in CTA order) and its elapsed wall time, into own[0..8).
-__global__ void __launch_bounds__(kThreads)
-    k_local_totals(const double* __restrict__ part1, int nu1, const double* __restrict__ part2,
-                   int nu2, const DevParams* __restrict__ P, const DevState* S, double* own) {
-  if (S->done) return;
-  __shared__ double red[P1_COUNT * 32];
-  double t1[P1_COUNT], t2[P2_COUNT];
-  reduce_partial_rows<P1_COUNT>(part1, nu1, t1, red);
-  reduce_partial_rows<P2_COUNT>(part2, nu2, t2, red);
-  if (threadIdx.x == 0) {
-    if (nu1 == 0) t1[P1_GX2] = t1[P1_BOUND] = t1[P1_CX] = t1[P1_DUALSQ] = 0.0;
-    if (nu2 == 0) t2[P2_GY2] = t2[P2_QY] = t2[P2_INFEAS] = 0.0;
-    own[0] = t1[P1_GX2];
-    own[1] = t1[P1_BOUND];
-    own[2] = t1[P1_CX];
-    own[3] = t1[P1_DUALSQ];
-    own[4] = t2[P2_GY2];
-    own[5] = t2[P2_QY];
-    own[6] = t2[P2_INFEAS];
-    own[7] = (double)(globaltimer_ns() - S->t0_ns) * 1e-9 + P->wall_offset_s;
-  }
-}
-
 // Sums the all-gathered shard totals in rank order (elapsed: the maximum, so
 // a TIMEOUT is taken by every shard at the same iteration) and runs the
 // control logic.
