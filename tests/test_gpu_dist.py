@@ -92,7 +92,7 @@ def test_loopback_faa_long_rows():
         ref = s.solve(cfg)
     with Solver(p, dist=loopback(3)) as s:
         got = s.solve(cfg)
-    traj_close(got, ref, 40, 1e-8)
+    traj_close(got, ref, 40, 1e-10)
 
 
 def test_loopback_pdhg_start_iterate_and_lambda():
@@ -191,4 +191,4 @@ def test_loopback_setcover_faa():
         ref = s.solve(cfg)
     with Solver(p, dist=loopback(3)) as s:
         got = s.solve(cfg)
-    traj_close(got, ref, 40, 1e-8)
+    traj_close(got, ref, 40, 1e-10)

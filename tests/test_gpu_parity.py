@@ -5,7 +5,8 @@ Tolerances (north star, BASELINE.json): SERIAL reduction order is bit-exact
 (integer/ordering semantics of the reference reproduced: CSR-ordered row
 sums, index-ordered dots, no FMA). TREE order: first 50 iterates within 1e-10
 relative, final objective / KKT within 1e-6 relative. FAA uses a Gram-based R
-instead of Householder QR (not bitwise): per-op 1e-9 relative."""
+instead of Householder QR (not bitwise): per-op 1e-9 relative, and the first
+50 iterates of an FAA solve within 1e-10 relative (measured ~1e-14)."""
 import numpy as np
 import pytest
 
@@ -284,7 +285,8 @@ def test_config1_first_50_iterates(port):
 @pytest.mark.parametrize("reduction", ["serial", "tree"])
 def test_config2_transport_faa_long_rows(port, reduction):
     """BASELINE config 2 shape (transport, FAA m=10, cos>0.99, length 1e4),
-    scaled to 300 x 300: K rows of 300 nonzeros exercise the long-row path."""
+    scaled to 300 x 300: K rows of 300 nonzeros exercise the long-row path.
+    First 50 iterates within the north-star 1e-10 relative (measured 1.2e-14)."""
     p = problems.make_config(2, scale=0.15)
     assert np.diff(p.k.row_ptr).max() > 256
     spec = problems.CONFIGS[2]
@@ -298,8 +300,30 @@ def test_config2_transport_faa_long_rows(port, reduction):
     ref = port.solve(p, cfg)
     k = 50
     np.testing.assert_allclose(got.trajectory["g_norm"][:k], ref.trajectory["g_norm"][:k],
-                               rtol=1e-8)
+                               rtol=1e-10)
     assert np.array_equal(got.trajectory["aa_step"][:k], ref.trajectory["aa_step"][:k])
+
+
+@pytest.mark.parametrize("reduction", ["serial", "tree"])
+@pytest.mark.parametrize("cfg_id,scale,m", [(0, 0.3, 5), (1, 0.02, 10)])
+def test_faa_first_50_iterates(port, reduction, cfg_id, scale, m):
+    """FAA-PDHG (angle + length filters, Gram-based QR solve) on the configs
+    0 and 1 shapes: first 50 iterates (g_norm, objective, x at the end) within
+    1e-10 relative of the oracle and the same accepted-AA-step pattern."""
+    p = problems.make_config(cfg_id, scale=scale)
+    with Solver(p) as s:
+        tau = s.select_step_sizes(SolverConfig(reduction="serial")).tau
+        cfg = SolverConfig(method=Method.FAA_PDHG, m=m, toll=1e-12, max_iters=50, tau=tau,
+                           sigma=tau, reduction=reduction)
+        got = s.solve(cfg)
+    ref = port.solve(p, cfg)
+    assert got.result.iterations == ref.result.iterations
+    for f in ("g_norm", "objective"):
+        np.testing.assert_allclose(got.trajectory[f][:50], ref.trajectory[f][:50], rtol=1e-10,
+                                   atol=1e-300)
+    assert np.array_equal(got.trajectory["aa_step"][:50], ref.trajectory["aa_step"][:50])
+    x, xr = got.result.u.x, ref.result.u.x
+    assert np.linalg.norm(x - xr) <= 1e-10 * np.linalg.norm(xr)
 
 
 @pytest.mark.parametrize("reduction", ["serial", "tree"])
