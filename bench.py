@@ -111,11 +111,12 @@ def measured_peak():
 
 
 def ncu_traffic(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu --set full
-    capture (profiles/r01/traffic.json), or None."""
+    """dram bytes per launch of `kernel` (per iteration for k_plain_loop) from
+    the committed ncu --set full capture (profiles/r01/traffic.json), or None."""
     try:
         d = json.loads((ROOT / "profiles" / "r01" / "traffic.json").read_text())[kernel]
-        return float(d["dram_read_bytes"] + d["dram_write_bytes"])
+        b = float(d["dram_read_bytes"] + d["dram_write_bytes"])
+        return b / d["iterations"] if "iterations" in d else b
     except Exception:
         return None
 
@@ -128,6 +129,8 @@ def kernel_bytes(p, name):
         return 12 * nnz + 4 * (n + 1) + 8 * m + 8 * n * (4 + 1) + 8 * n * (2 + 3)
     if name == "k_primal_side":  # K xhat + yhat + KKT primal terms + push (y half)
         return 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m * (3 + 2) + 8 * m * (2 + 3)
+    if name == "k_plain_loop":  # one plain iteration: both halves
+        return kernel_bytes(p, "k_dual_side") + kernel_bytes(p, "k_primal_side")
     if name == "k_spmv_recache":
         return 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
     return None
@@ -240,15 +243,28 @@ def run_ours(args, rank, world, local_rank):
     iters = out.result.iterations
     launches, loop_iters = C.c_uint64(), C.c_uint64()
     lib.aapdhg_cuda_last_launch_count(s.h, C.byref(launches), C.byref(loop_iters))
+    plain = None
+    if not dist:
+        pi, ps, pl = C.c_uint64(), C.c_double(), C.c_uint64()
+        lib.aapdhg_cuda_last_plain_loop(s.h, C.byref(pi), C.byref(ps), C.byref(pl))
+        if pl.value:
+            plain = (int(pi.value), float(ps.value), int(pl.value))
     if dist:  # one iteration is one unit of the whole (sharded) job
         ms = allreduce_max(tdist, torch, ms, dev)
     total_iters = float(iters)
     value = total_iters / (ms / 1e3)
 
-    # ---- roofline of the dominant kernel: per-launch CUDA events -----------
+    # ---- roofline of the dominant kernel ------------------------------------
+    # k_plain_loop from its device clock over the timed region; the per-kernel
+    # graph's K1 / K2 (eager launches, CUDA events) beside it
     roofline = None
     if not dist:
-        roofline = kernel_roofline(args, p, s, lib, tau)
+        eager = kernel_roofline(args, p, s, lib, tau)
+        if plain:
+            roofline = plain_loop_roofline(args, p, plain, ms)
+            roofline["per_kernel_graph"] = eager
+        else:
+            roofline = eager
 
     # ---- time to tolerance (full solve to toll 1e-6, step sizes included) --
     ttt = None
@@ -298,6 +314,39 @@ def run_ours(args, rank, world, local_rank):
                 "clocks": clk.summary(), "gpu_launches": int(launches.value),
                 "gpu_loop_iterations": int(loop_iters.value)}
         print(json.dumps(line), flush=True)
+
+
+def plain_loop_roofline(args, p, plain, step_ms):
+    """Roofline of k_plain_loop, the persistent grid that runs every plain
+    iteration of the timed solve, from its own device clock over the timed
+    region (globaltimer from each launch's start to its stop, summed by the
+    control CTA; aapdhg_cuda_last_plain_loop)."""
+    iters, secs, launches = plain
+    per_it = kernel_bytes(p, "k_plain_loop")
+    achieved = per_it * iters / secs / 1e9
+    peak, peak_kind = measured_peak()
+    t_it = ncu_traffic("k_plain_loop")
+    return {"bound": "hbm", "kernel": "k_plain_loop", "achieved": achieved, "peak": peak,
+            "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": (t_it * iters / launches) if (t_it and args.traffic is None)
+            else args.traffic,
+            "traffic_source": "ncu --set full of one k_plain_loop launch (profiles/r01/"
+                              "traffic.json), dram bytes per iteration x iterations per launch",
+            "bytes_per_launch": per_it * iters / launches,
+            "bytes_per_iteration": per_it,
+            "avg_launch_us": 1e6 * secs / launches,
+            "iterations_per_launch": iters / launches,
+            "launches": launches,
+            "timing": "device globaltimer inside the timed region (launch start -> stop)",
+            "share_of_step": secs / (step_ms / 1e3),
+            "gather_roofline": {
+                "bound": "random 8-byte gathers (L1TEX sectors)",
+                "ceiling_gather_per_s": GATHER_CEILING,
+                "ceiling_source": "profiles/r01/gather.txt: 4M random gathers from an "
+                                  "L2-resident vector, 16.6 us on this pool's B200",
+                "gathers_per_iteration": 2 * int(p.k.nnz),
+                "achieved_gather_per_s": 2 * p.k.nnz * iters / secs,
+                "frac": 2 * p.k.nnz * iters / secs / GATHER_CEILING}}
 
 
 def kernel_roofline(args, p, s, lib, tau):

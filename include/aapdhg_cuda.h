@@ -285,6 +285,12 @@ int aapdhg_cuda_kernel_times(aapdhg_handle* h, char* names, size_t names_len,
  * nodes counted individually) and the iterations it ran. */
 int aapdhg_cuda_last_launch_count(aapdhg_handle* h, uint64_t* launches,
                                   uint64_t* loop_iterations);
+/* The persistent plain-step kernel (k_plain_loop) in the last solve: the
+ * iterations it completed, its device time (globaltimer from each launch's
+ * start to its stop, summed) and its launches; zeros when the solve ran on
+ * the per-kernel graph. Not for sharded handles. */
+int aapdhg_cuda_last_plain_loop(aapdhg_handle* h, uint64_t* iterations, double* seconds,
+                                uint64_t* launches);
 
 /* ---- sharded solve ------------------------------------------------------ */
 

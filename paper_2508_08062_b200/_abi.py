@@ -167,6 +167,8 @@ def _declare_cuda(lib):
                                              C.POINTER(H)] + E, C.c_int),
         "aapdhg_cuda_last_launch_count": ([H, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
                                           C.c_int),
+        "aapdhg_cuda_last_plain_loop": ([H, C.POINTER(C.c_uint64), _dp, C.POINTER(C.c_uint64)],
+                                        C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -183,7 +185,7 @@ CUDA_SYMBOLS = (
     "aapdhg_cuda_matvec_transpose", "aapdhg_cuda_pdhg_step", "aapdhg_cuda_kkt_metrics",
     "aapdhg_cuda_aa_apply", "aapdhg_cuda_filtered_aa_apply", "aapdhg_cuda_set_stream",
     "aapdhg_cuda_set_profiling",
-    "aapdhg_cuda_kernel_times", "aapdhg_cuda_last_launch_count",
+    "aapdhg_cuda_kernel_times", "aapdhg_cuda_last_launch_count", "aapdhg_cuda_last_plain_loop",
     "aapdhg_cuda_nccl_id", "aapdhg_cuda_partition", "aapdhg_cuda_problem_create_dist",
 )
 

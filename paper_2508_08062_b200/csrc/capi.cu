@@ -310,6 +310,18 @@ int aapdhg_cuda_kernel_times(aapdhg_handle* h, char* names, size_t names_len, do
   return AAPDHG_OK;
 }
 
+int aapdhg_cuda_last_plain_loop(aapdhg_handle* h, uint64_t* iterations, double* seconds,
+                                uint64_t* launches) {
+  if (!h || h->group) return AAPDHG_ERR_INPUT;
+  uint64_t it = 0, la = 0;
+  double sec = 0.0;
+  h->prob->last_plain_stats(&it, &sec, &la);
+  if (iterations) *iterations = it;
+  if (seconds) *seconds = sec;
+  if (launches) *launches = la;
+  return AAPDHG_OK;
+}
+
 int aapdhg_cuda_last_launch_count(aapdhg_handle* h, uint64_t* launches,
                                   uint64_t* loop_iterations) {
   if (!h) return AAPDHG_ERR_INPUT;

@@ -124,6 +124,9 @@ struct DevState {
   double tot1[4];                  // K1 partial totals (TREE, fused control)
   uint64_t t0_ns;
   uint64_t loop_iters;             // iterations that did work (launch accounting)
+  uint64_t loop_exits;             // k_plain_loop launches that ran (launch accounting)
+  uint64_t plain_iters;            // iterations k_plain_loop completed
+  uint64_t plain_ns;               // k_plain_loop time (globaltimer, launch start -> stop)
   uint32_t ticket;                 // last-CTA election in k_primal_side
   int32_t prev_plain;              // the previous step was T(u_{k-1}) (not an AA candidate)
   int32_t pad_pp;
@@ -208,6 +211,12 @@ __device__ __forceinline__ double project_lambda1(double v, double l, double u) 
 __device__ __forceinline__ double damp1(double beta, const double* d_hat, int64_t i, double v) {
   return d_hat ? beta * d_hat[i] * v : beta * v;
 }
+
+#ifdef AAPDHG_TAIL_STAMPS
+// experiment build only (make EXTRA=-DAAPDHG_TAIL_STAMPS): phase stamps of the
+// fused control tail, read by aapdhg_cuda_debug_stamps
+__device__ unsigned long long g_dbg[16];
+#endif
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;

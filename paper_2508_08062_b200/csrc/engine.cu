@@ -8,6 +8,7 @@
 // DevState mirror (pinned) between graph batches to stream trajectory
 // records out and to stop.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -81,6 +82,29 @@ struct SolveSetup {
   DevState* S;
   bool serial, push;
   int method, cap, nblk1, nblk2, ndot_blk, items_max;
+  bool persist = false;  // plain iterations in k_plain_loop (graph replay only)
+  int pgrid = 0;         // workers + the control CTA
+  CsrDev pk1, pk2;       // the K' / K layouts on <= pgrid - 1 worker CTAs
+  GridBar* gb = nullptr;
+};
+
+// k_plain_loop spins on grid barriers, so it must never share the GPU with a
+// second persistent grid (two partially resident grids would wait on each
+// other): one persistent solve per device at a time, the others take the
+// per-kernel graph.
+static std::atomic<int> g_persist_busy[64];
+struct PersistLock {
+  int dev = -1;
+  bool try_lock(int d) {
+    if (d < 0 || d >= 64) return false;
+    int z = 0;
+    if (!g_persist_busy[d].compare_exchange_strong(z, 1)) return false;
+    dev = d;
+    return true;
+  }
+  ~PersistLock() {
+    if (dev >= 0) g_persist_busy[dev].store(0);
+  }
 };
 
 // SELL-32 slices of the short rows with split factor sf (see CsrDev):
@@ -393,8 +417,10 @@ void Problem::ensure_iter_buffers(int method, int cap) {
   ndot_tile_ = int((N_ + kDotChunk - 1) / kDotChunk);
   if (method != AAPDHG_METHOD_PDHG) {
     gpool_.reserve(sizeof(double) * 2 * std::max<int64_t>(N_, 1));
-    du_.reserve(sizeof(double) * size_t(cap) * std::max<int64_t>(N_, 1));
-    dg_.reserve(sizeof(double) * size_t(cap) * std::max<int64_t>(N_, 1));
+    // cap + 1 slots: the next push never lands in a slot the memory holds
+    // (advance, pipeline.cuh)
+    du_.reserve(sizeof(double) * size_t(cap + 1) * std::max<int64_t>(N_, 1));
+    dg_.reserve(sizeof(double) * size_t(cap + 1) * std::max<int64_t>(N_, 1));
     const int items = num_items_host(cap, AAPDHG_METHOD_FAA);
     partdot_.reserve(sizeof(double) * size_t(items) * std::max(std::max(ndot_tile_, num_sms_), 1));
   }
@@ -522,6 +548,22 @@ static void launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
 int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   int nodes = 0;
   const bool ser = su.serial, push = su.push;
+  if (su.persist) {  // co-resident grid: cooperative launch
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(su.pgrid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    auto kern = push ? k_plain_loop<true> : k_plain_loop<false>;
+    LAUNCH("k_plain_loop", AAPDHG_CUDA(cudaLaunchKernelEx(&cfg, kern, su.pk1, su.pk2, su.B, su.P,
+                                                          su.S, su.gb, su.pk1.grid(),
+                                                          su.pk2.grid())));
+    return nodes;
+  }
   // TREE with L2 column blocking: the earlier column passes first, the last
   // block inside the fused kernel (rinit1 / rinit2 hold the partial sums)
   const bool b1 = !ser && ktb_.nb() > 1, b2 = !ser && kb_.nb() > 1;
@@ -606,9 +648,8 @@ int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
   return nodes;
 }
 
-void Problem::launch_iteration(cudaStream_t s, const SolveSetup& su) {
-  launch_core(s, su);
-  launch_aa(s, su);
+int Problem::launch_iteration(cudaStream_t s, const SolveSetup& su) {
+  return launch_core(s, su) + launch_aa(s, su);
 }
 
 // WHILE(batch) { core (+control); IF(aa_attempt) { aa (+commit) } } as one
@@ -862,10 +903,42 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
     return e && e[0] == '1';
   }();
   const bool use_graph = !profiling_ && !force_eager;
+  // plain iterations in one persistent grid (AAPDHG_PERSIST=0: per-kernel graph)
+  PersistLock plock;
+  // (eager stream launches of it only on request, AAPDHG_PERSIST_EAGER=1: ncu
+  // cannot profile kernels inside graphs that hold conditional nodes)
+  const bool persist_ok = use_graph || (!profiling_ && env_int("AAPDHG_PERSIST_EAGER", 0) != 0);
+  if (persist_ok && !serial && su.B.fused_ctrl == 1 && !blk1 && !blk2 && n_ > 0 && m_ > 0 &&
+      env_int("AAPDHG_PERSIST", 1) != 0) {
+    int per_sm = 0;
+    AAPDHG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, su.push ? k_plain_loop<true> : k_plain_loop<false>, kThreads, 0));
+    // one CTA of the co-resident grid is the control CTA: the short-row
+    // slices spread over one CTA fewer when the layout fills the wave
+    const int workers = per_sm * num_sms_ - 1;
+    auto fit = [&](CsrDev d) {
+      const int over = d.grid() - workers;
+      if (over > 0) d.nblk_short = d.nblk_short > over ? d.nblk_short - over : 0;
+      return d;
+    };
+    const CsrDev p1 = fit(K1m), p2 = fit(K2m);
+    if (workers >= 1 && p1.grid() <= workers && p2.grid() <= workers &&
+        (p1.nslices == 0 || p1.nblk_short > 0) && (p2.nslices == 0 || p2.nblk_short > 0) &&
+        plock.try_lock(device_)) {
+      gridbar_.reserve(sizeof(GridBar));
+      su.persist = true;
+      su.pk1 = p1;
+      su.pk2 = p2;
+      su.pgrid = std::max(p1.grid(), p2.grid()) + 1;
+      su.gb = gridbar_.as<GridBar>();
+      su.B.nu1 = p1.grid();
+    }
+  }
   if (use_graph) {
     char key[256];
-    std::snprintf(key, sizeof key, "%d/%d/%d/%p/%p/%p/%p/%p/%p", method, int(serial), cap,
-                  upool_.p, du_.p, partdot_.p, dparams_.p, rec_.p, stream_);
+    std::snprintf(key, sizeof key, "%d/%d/%d/%d/%p/%p/%p/%p/%p/%p/%p", method, int(serial), cap,
+                  int(su.persist), upool_.p, du_.p, partdot_.p, dparams_.p, rec_.p, stream_,
+                  gridbar_.p);
     if (graph_key_ != key || !graph_exec_) {
       if (graph_exec_) {
         cudaGraphExecDestroy(graph_exec_);
@@ -885,6 +958,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   if (method != AAPDHG_METHOD_PDHG) {
     AAPDHG_CUDA(cudaMemsetAsync(gpool_.p, 0, sizeof(double) * 2 * N_, stream_));
   }
+  if (su.persist) AAPDHG_CUDA(cudaMemsetAsync(gridbar_.p, 0, sizeof(GridBar), stream_));
   upload_iterate(0, x0, y0);
   P.wall_offset_s = secs(t_start);
   h2d(dparams_.p, &P, sizeof P, stream_);
@@ -896,7 +970,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   AAPDHG_CUDA(cudaGetLastError());
 
   ph("solve: start iterate");
-  uint64_t flushed = 0;
+  uint64_t flushed = 0, eager_launches = 0;
   int batch = 8;  // iterations per launch, grows geometrically
   std::vector<aapdhg_record> host_recs;
   const aapdhg_record* drec = rec_.as<aapdhg_record>();
@@ -906,7 +980,11 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
       h2d(&S->batch_left, h_batch_, sizeof(int32_t), stream_);
       AAPDHG_CUDA(cudaGraphLaunch(graph_exec_, stream_));
     } else {
-      for (int it = 0; it < batch; ++it) launch_iteration(stream_, su);
+      if (su.persist) {  // each launch runs until the control stops it
+        *h_batch_ = batch;
+        h2d(&S->batch_left, h_batch_, sizeof(int32_t), stream_);
+      }
+      for (int it = 0; it < batch; ++it) eager_launches += launch_iteration(stream_, su);
     }
     d2h(h_state_, S, sizeof(DevState), stream_);
     sync();
@@ -960,11 +1038,16 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   res->sigma = sigma;
   res->wall_seconds = secs(t_start);
   last_loop_iters_ = st.loop_iters;
-  if (use_graph)
+  last_plain_iters_ = st.plain_iters;
+  last_plain_launches_ = st.loop_exits;
+  last_plain_secs_ = double(st.plain_ns) * 1e-9;
+  if (!use_graph)  // eager: every launch issued, predicated or not
+    last_launches_ = eager_launches;
+  else if (su.persist)
+    last_launches_ = st.loop_exits + (st.i + st.aa_failures) * uint64_t(aa_nodes_);
+  else
     last_launches_ = st.loop_iters * uint64_t(core_nodes_) +
                      (st.i + st.aa_failures) * uint64_t(aa_nodes_);
-  else
-    last_launches_ = st.loop_iters * uint64_t(core_nodes_ + aa_nodes_);
   ph("solve: finish");
 }
 
@@ -1458,3 +1541,25 @@ double Problem::sh_read_scal(int world, int q) {
 }
 
 }  // namespace aapdhg_b200
+
+#ifdef AAPDHG_TAIL_STAMPS
+// experiment build only: averaged phase times (ns) of the fused control tail
+extern "C" int aapdhg_cuda_debug_stamps(double* out) {
+  unsigned long long v[16];
+  if (cudaMemcpyFromSymbol(v, aapdhg_b200::g_dbg, sizeof v) != cudaSuccess) return -1;
+  const double c = v[5] ? double(v[5]) : 1.0, c9 = v[9] ? double(v[9]) : 1.0;
+  out[0] = v[11] / c;  // persistent: K1 phase + barrier (CTA 0)
+  out[1] = v[1] / c;   // persistent: barrier passed (CTA 0) -> election won
+  out[2] = v[2] / c;   // -> partials reduced
+  out[3] = v[3] / c;   // -> decided
+  out[4] = v[4] / c;   // -> end of tail
+  out[5] = v[8] / c9;  // -> next K1 start (plain step)
+  out[6] = v[14] ? v[13] / double(v[14]) : 0.0;  // -> next K1 start (after the AA branch)
+  out[7] = c;
+  out[8] = v[9];
+  out[9] = v[14];
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(aapdhg_b200::g_dbg, z, sizeof z);
+  return 0;
+}
+#endif

@@ -124,6 +124,12 @@ class Problem {
   const std::map<std::string, KernelStat>& kernel_stats() const { return stats_; }
   uint64_t last_launches() const { return last_launches_; }
   uint64_t last_loop_iters() const { return last_loop_iters_; }
+  // k_plain_loop in the last solve: iterations, device seconds, launches
+  void last_plain_stats(uint64_t* iters, double* secs, uint64_t* launches) const {
+    *iters = last_plain_iters_;
+    *secs = last_plain_secs_;
+    *launches = last_plain_launches_;
+  }
 
  private:
   bool resolve_serial(int reduction) const;
@@ -161,7 +167,7 @@ class Problem {
   void kkt_eval(int slot, bool serial, double* kkt_dev_out, double* lam_dev);
   int launch_core(cudaStream_t s, const SolveSetup& su);
   int launch_aa(cudaStream_t s, const SolveSetup& su);
-  void launch_iteration(cudaStream_t s, const SolveSetup& su);
+  int launch_iteration(cudaStream_t s, const SolveSetup& su);
   void build_graph(const SolveSetup& su);
   void run_power(const double* x0_host, int max_iters, double rel_tol, bool serial, double* out,
                  int* rounds);
@@ -234,11 +240,14 @@ class Problem {
   std::string graph_key_;
   cudaGraphConditionalHandle cond_loop_ = 0, cond_aa_ = 0;
   int core_nodes_ = 0, aa_nodes_ = 0;
+  DevBuf gridbar_;  // k_plain_loop's barrier counters (GridBar)
   int32_t* h_batch_ = nullptr;  // pinned
 
   bool profiling_ = false;
   std::map<std::string, KernelStat> stats_;
   uint64_t last_launches_ = 0, last_loop_iters_ = 0;
+  uint64_t last_plain_iters_ = 0, last_plain_launches_ = 0;
+  double last_plain_secs_ = 0.0;
 };
 
 }  // namespace aapdhg_b200

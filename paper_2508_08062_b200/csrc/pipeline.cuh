@@ -162,17 +162,16 @@ __device__ __forceinline__ void advance(const DevParams* P, DevState* S) {
     const int t = S->g_idx[G_CUR];
     S->g_idx[G_CUR] = S->g_idx[G_PREV];
     S->g_idx[G_PREV] = t;
-    if (S->mem_size < P->cap) {  // first slot not in the memory
-      int slot = 0;
-      for (; slot < P->cap; ++slot) {
-        bool used = false;
-        for (int q = 0; q < S->mem_size; ++q) used |= S->mem_slots[q] == slot;
-        if (!used) break;
-      }
-      S->push_slot = slot;
-    } else {
-      S->push_slot = S->mem_slots[0];
+    // the first of the cap + 1 history slots not in the memory: the slot the
+    // next push evicts stays intact until the push commits (k_plain_loop
+    // writes the next push while the control still decides this iteration)
+    int slot = 0;
+    for (; slot < P->cap; ++slot) {
+      bool used = false;
+      for (int q = 0; q < S->mem_size; ++q) used |= S->mem_slots[q] == slot;
+      if (!used) break;
     }
+    S->push_slot = slot;
   }
   S->prev_plain = S->aa_ok ? 0 : 1;
   S->aa_attempt = 0;
@@ -246,14 +245,26 @@ __device__ __forceinline__ void l2_prefetch(const void* p) {
 // when the whole slice is one unroll group (short rows): the fused kernels
 // prefetch their epilogue operands into L2 so the epilogue does not pay a
 // DRAM round trip after the (short) SpMV chain.
-template <bool SERIAL, int UNROLL = kUnroll, class Pre = NoPre>
+//
+// COH (the persistent loop, k_plain_loop): the gathered vector changes while
+// the kernel runs, so it is read with ld.global.ca (L1 invalidated by the
+// grid barrier's acquire) instead of the read-only ld.global.nc path. bid is
+// the CTA's index in the layout (blockIdx.x unless the caller remaps it).
+template <bool COH>
+__device__ __forceinline__ double ldx(const double* p) {
+  if constexpr (COH) return __ldca(p);
+  else return __ldg(p);
+}
+
+template <bool SERIAL, int UNROLL = kUnroll, bool COH = false, class Pre = NoPre>
 __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, double& s,
-                                       Pre pre = Pre{}) {
+                                       Pre pre = Pre{}, int bid = -1) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (bid < 0) bid = int(blockIdx.x);
   s = 0.0;
-  if ((int)blockIdx.x >= A.nblk_long) {
+  if (bid >= A.nblk_long) {
     // CTA b owns slices [b * ns / nblk, (b + 1) * ns / nblk): <= kWarps each
-    const int b = int(blockIdx.x) - A.nblk_long;
+    const int b = bid - A.nblk_long;
     const int sl = int(int64_t(b) * A.nslices / A.nblk_short) + warp;
     if (sl >= int(int64_t(b + 1) * A.nslices / A.nblk_short)) return -1;
     const int sf = A.sf, j = lane & (sf - 1);
@@ -278,7 +289,7 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
       }
       double g[UNROLL];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) g[u] = t0 + u < cnt ? __ldg(x + c[u]) : 0.0;
+      for (int u = 0; u < UNROLL; ++u) g[u] = t0 + u < cnt ? ldx<COH>(x + c[u]) : 0.0;
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u)
         if (t0 + u < cnt) acc = __dadd_rn(acc, __dmul_rn(v[u], g[u]));
@@ -288,10 +299,10 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     s = acc;
     return (row >= 0 && j == 0) ? row : -1;
   }
-  if (!SERIAL && (int)blockIdx.x < A.nhuge) {
+  if (!SERIAL && bid < A.nhuge) {
     // a huge row per CTA: thread-strided products, warp trees, then the 8
     // warp sums in warp order (fixed shape: deterministic)
-    const int row = __ldg(A.long_rows + blockIdx.x);
+    const int row = __ldg(A.long_rows + bid);
     const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
     grid_dependency_wait();
     double acc = 0.0;
@@ -300,7 +311,7 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const int64_t e = c0 + kThreads * u;
-        pr[u] = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
+        pr[u] = e < e1 ? __dmul_rn(__ldcs(A.v + e), ldx<COH>(x + __ldcs(A.ci + e))) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) acc = __dadd_rn(acc, pr[u]);
@@ -317,7 +328,7 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     return threadIdx.x == 0 ? row : -1;
   }
   // the other long rows: a warp each, 8 per CTA, after the huge rows' CTAs
-  const int lr = A.nhuge + (int(blockIdx.x) - A.nhuge) * kWarps + warp;
+  const int lr = A.nhuge + (bid - A.nhuge) * kWarps + warp;
   if (lr >= A.nlong) return -1;
   const int row = __ldg(A.long_rows + lr);
   const int64_t e0 = __ldg(A.rp + row), e1 = __ldg(A.rp + row + 1);
@@ -326,7 +337,7 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
   if (SERIAL) {  // CSR order through lane 0
     for (int64_t c0 = e0; c0 < e1; c0 += 32) {
       const int64_t e = c0 + lane;
-      const double pr = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
+      const double pr = e < e1 ? __dmul_rn(__ldcs(A.v + e), ldx<COH>(x + __ldcs(A.ci + e))) : 0.0;
       const int n = (e1 - c0) < 32 ? (int)(e1 - c0) : 32;
       for (int q = 0; q < n; ++q) {
         const double t = __shfl_sync(0xffffffffu, pr, q);
@@ -339,7 +350,7 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const int64_t e = c0 + 32 * u;
-        pr[u] = e < e1 ? __dmul_rn(__ldcs(A.v + e), __ldg(x + __ldcs(A.ci + e))) : 0.0;
+        pr[u] = e < e1 ? __dmul_rn(__ldcs(A.v + e), ldx<COH>(x + __ldcs(A.ci + e))) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) acc = __dadd_rn(acc, pr[u]);
@@ -581,29 +592,33 @@ __device__ __forceinline__ void tail_prefetch(TailSmem& ts, const DevParams* P,
   }
 }
 
-__device__ __forceinline__ void fused_control_tail(const IterBufs& B, const DevParams* P,
-                                                   DevState* S, TailSmem& ts) {
-  __shared__ double red[P1_COUNT * 32];
-  __shared__ int last;
-  if (blockIdx.x == 0) {
-    double t1[P1_COUNT];
-    reduce_partial_rows<P1_COUNT>(B.part1, B.nu1, t1, red);
-    if (threadIdx.x == 0)
+// K1's per-CTA partials folded into S->tot1 by CTA 0 of k_primal_side (K1
+// finished before K2 started).
+__device__ __forceinline__ void tail_fold_k1(const IterBufs& B, DevState* S, double* red) {
+  double t1[P1_COUNT];
+  reduce_partial_rows<P1_COUNT>(B.part1, B.nu1, t1, red);
+  if (threadIdx.x == 0)
 #pragma unroll
-      for (int q = 0; q < P1_COUNT; ++q) S->tot1[q] = B.nu1 > 0 ? t1[q] : 0.0;
-  }
-  if (threadIdx.x == 0) {
-    unsigned prev;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                 : "=r"(prev) : "l"(&S->ticket) : "memory");
-    last = prev == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last) return;
+    for (int q = 0; q < P1_COUNT; ++q) S->tot1[q] = B.nu1 > 0 ? t1[q] : 0.0;
+}
+
+// The last CTA's part of the fused control: K2 partials (nu2 rows), then the
+// control logic on the prefetched shared copy of the state. persist: the
+// caller is k_plain_loop, which only hands the graph conditions over when it
+// stops (AA attempt, batch end, termination). Returns true when it stops.
+__device__ __noinline__ bool tail_control(const IterBufs& B, DevState* S, TailSmem& ts, int nu2,
+                                          bool persist, double* red) {
+#ifdef AAPDHG_TAIL_STAMPS
+  const uint64_t ts0 = globaltimer_ns();
+  if (threadIdx.x == 0 && persist) g_dbg[1] += ts0 - g_dbg[10];  // K2 phase -> election won
+#endif
   double t2[P2_COUNT];
-  reduce_partial_rows<P2_COUNT>(B.part2, gridDim.x, t2, red);
+  reduce_partial_rows<P2_COUNT>(B.part2, nu2, t2, red);
   cp_async_wait_all();
   __syncthreads();
+#ifdef AAPDHG_TAIL_STAMPS
+  const uint64_t ts1 = globaltimer_ns();
+#endif
   if (B.fused_ctrl == 2) {  // sharded: this shard's totals (k_local_totals' layout)
     if (threadIdx.x == 0) {
       double* own = B.scal_own;
@@ -617,7 +632,7 @@ __device__ __forceinline__ void fused_control_tail(const IterBufs& B, const DevP
       own[7] = (double)(globaltimer_ns() - ts.st.t0_ns) * 1e-9 + ts.pr.wall_offset_s;
       S->ticket = 0;
     }
-    return;
+    return true;
   }
   // the control on two warps: KKT + records (warp 1) beside the decision and
   // the graph conditions (warp 0); the commit needs the decision
@@ -642,9 +657,46 @@ __device__ __forceinline__ void fused_control_tail(const IterBufs& B, const DevP
     dec = control_decide(&ts.pr, &sm, k, g2, bound, qy, cx, infeas, dsq, -1.0, ts.pw);
   }
   __syncthreads();
-  if (threadIdx.x == 0) control_setcond(&ts.pr, dec);
+#ifdef AAPDHG_TAIL_STAMPS
+  const uint64_t ts2 = globaltimer_ns();
+#endif
+  const bool stop = !persist || dec.attempt || dec.left <= 0;
+  if (threadIdx.x == 0 && stop) {
+    control_setcond(&ts.pr, dec);
+    if (persist) sm.loop_exits += 1;
+  }
   if (threadIdx.x == 32) control_commit(&ts.pr, &sm, k, dec);
   state_store(S, &ts.st);
+#ifdef AAPDHG_TAIL_STAMPS
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t ts3 = globaltimer_ns();
+    g_dbg[2] += ts1 - ts0;  // K2 partials reduced
+    g_dbg[3] += ts2 - ts1;  // kkt/records + decide
+    g_dbg[4] += ts3 - ts2;  // setcond + commit + state store
+    g_dbg[5] += 1;
+    g_dbg[6] = ts3;
+    g_dbg[12] = dec.attempt;
+  }
+#endif
+  return stop;
+}
+
+// Fused TREE-mode control of k_primal_side: CTA 0 folds K1's partials, the
+// last CTA to finish (acq_rel ticket) runs tail_control.
+__device__ __forceinline__ void fused_control_tail(const IterBufs& B, DevState* S, TailSmem& ts) {
+  __shared__ double red[P1_COUNT * 32];
+  __shared__ int last;
+  if (blockIdx.x == 0) tail_fold_k1(B, S, red);
+  if (threadIdx.x == 0) {
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(prev) : "l"(&S->ticket) : "memory");
+    last = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  tail_control(B, S, ts, gridDim.x, false, red);
 }
 
 // One column pass of an L2-blocked SpMV: part[row] (+)= the row's products
@@ -667,24 +719,23 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 //   lambda_j = P_Lambda(c_j - t)                           solver.cpp:67-71
 //   per-CTA partials: (xhat-x)^2, bound term, (c-t-lambda)^2, c_j x_j
 //   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
-// VAR 2 (experiment, AAPDHG_K1VAR=2): the SpMV alone, no epilogue
-template <bool SERIAL, bool PUSH, int VAR = 0>
-__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
-    k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
-  launch_dependents();  // k_primal_side may start its prologue (PDL)
-  if (S->done) return;
-  __shared__ double red[P1_COUNT * kWarps];
+// VAR 2 (experiment, AAPDHG_K1VAR=2): the SpMV alone, no epilogue.
+// CTA bid of nb; red holds P1_COUNT * kWarps doubles.
+template <bool SERIAL, bool PUSH, int VAR = 0, bool COH = false>
+__device__ __forceinline__ void dual_side_rows(const CsrDev& KT, const IterBufs& B,
+                                               const DevParams* __restrict__ P, DevState* S,
+                                               int bid, int nb, double* red) {
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
   double t;
-  int j = row_sum<SERIAL, kUnroll>(
+  int j = row_sum<SERIAL, kUnroll, COH>(
       KT, P->ygather ? P->ygather : x + P->n, t, [&](int r) {
         l2_prefetch(x + r);
         l2_prefetch(B.c + r);
         l2_prefetch(B.l + r);
         l2_prefetch(B.u + r);
         if constexpr (PUSH) l2_prefetch(B.upool + (int64_t)S->u_idx[U_PREV] * N + r);
-      });
+      }, bid);
   if (B.rinit1 && j >= 0) t = __dadd_rn(B.rinit1[j], t);  // earlier column passes
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
   if (VAR == 2) {  // experiment: SpMV only
@@ -724,8 +775,25 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     block_sum<P1_COUNT>(acc, red);
     if (threadIdx.x == 0)
 #pragma unroll
-      for (int q = 0; q < P1_COUNT; ++q) B.part1[q * gridDim.x + blockIdx.x] = acc[q];
+      for (int q = 0; q < P1_COUNT; ++q) B.part1[q * nb + bid] = acc[q];
   }
+}
+
+template <bool SERIAL, bool PUSH, int VAR = 0>
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+    k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+  launch_dependents();  // k_primal_side may start its prologue (PDL)
+  if (S->done) return;
+#ifdef AAPDHG_TAIL_STAMPS
+  if (blockIdx.x == 0 && threadIdx.x == 0 && g_dbg[6]) {
+    const int a = g_dbg[12] ? 13 : 8;  // after an AA branch / a plain step
+    g_dbg[a] += globaltimer_ns() - g_dbg[6];  // K2 tail end -> next K1 CTA 0 start
+    g_dbg[a + 1] += 1;
+    g_dbg[6] = 0;
+  }
+#endif
+  __shared__ double red[P1_COUNT * kWarps];
+  dual_side_rows<SERIAL, PUSH, VAR>(KT, B, P, S, int(blockIdx.x), int(gridDim.x), red);
 }
 
 // K2 on K, s = (K xhat)_i:
@@ -733,18 +801,17 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 //                                                         pdhg_core.cpp:55-60
 //   K xhat cached as the next K x (solver.cpp:90 / pdhg_core.cpp:56)
 //   per-CTA partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
-template <bool SERIAL, bool PUSH>
-__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
-    k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
-  if (S->done) return;
-  __shared__ double red[P2_COUNT * kWarps];
+// The rows and epilogue; acc gets this thread's share of the partials.
+template <bool SERIAL, bool PUSH, bool COH = false>
+__device__ __forceinline__ void primal_side_rows(const CsrDev& K, const IterBufs& B,
+                                                 const DevParams* __restrict__ P, DevState* S,
+                                                 int bid, double (&acc)[P2_COUNT]) {
   const int64_t N = P->N;
   const int n = P->n, mr = P->mrows;
   double s;
-  const int i = row_sum<SERIAL>(
-      K, P->xgather ? P->xgather : B.upool + (int64_t)S->u_idx[U_HAT] * N, s);
+  const int i = row_sum<SERIAL, kUnroll, COH>(
+      K, P->xgather ? P->xgather : B.upool + (int64_t)S->u_idx[U_HAT] * N, s, NoPre{}, bid);
   if (B.rinit2 && i >= 0) s = __dadd_rn(B.rinit2[i], s);  // earlier column passes
-  double acc[P2_COUNT] = {0.0, 0.0, 0.0};
   if (i >= 0) {
     const double yi = B.upool[(int64_t)S->u_idx[U_CUR] * N + n + i];
     const double qi = __ldg(B.q + i);
@@ -770,6 +837,15 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
       B.dg[slot * N + n + i] = __dsub_rn(d, gp);
     }
   }
+}
+
+template <bool SERIAL, bool PUSH>
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+    k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+  if (S->done) return;
+  __shared__ double red[P2_COUNT * kWarps];
+  double acc[P2_COUNT] = {0.0, 0.0, 0.0};
+  primal_side_rows<SERIAL, PUSH>(K, B, P, S, int(blockIdx.x), acc);
   if (!SERIAL) {
     __shared__ __align__(16) TailSmem ts;
     if (B.fused_ctrl) tail_prefetch(ts, P, S);
@@ -778,10 +854,174 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 #pragma unroll
       for (int q = 0; q < P2_COUNT; ++q) B.part2[q * gridDim.x + blockIdx.x] = acc[q];
     }
-    if (B.fused_ctrl) fused_control_tail(B, P, S, ts);
+    if (B.fused_ctrl) fused_control_tail(B, S, ts);
   }
 }
 
+// ---------------------------------------------------------------------------
+// the persistent plain-step loop (TREE, fused control, graph replay)
+// ---------------------------------------------------------------------------
+//
+// Under graph replay every iteration otherwise pays the WHILE/IF node
+// overhead between K2's control and the next K1, and the last CTA's control
+// (~5 us) sits between K2 and the next K1 (globaltimer stamps,
+// profiles/exp_tail_stamps.py). k_plain_loop runs consecutive plain
+// iterations in one co-resident grid (cooperative launch): CTAs 0..W-1 are
+// workers that run K1 and K2 of each iteration (the same rows, epilogues and
+// partial layout as k_dual_side / k_primal_side), CTA W is the control CTA.
+// Per iteration k:
+//   workers   K1(k) | barrier 1 | K2(k) | barrier 2 | K1(k+1) ...
+//   control          barrier 1 -> fold K1 partials | barrier 2 -> K2 partials,
+//                    control(k) -> arrives at barrier 1 of k+1
+// A worker starts K1(k+1) right after barrier 2 on the roles of a plain step,
+// which it derives itself (control_commit + advance on its own copy of the
+// state), while the control CTA decides iteration k: the control leaves the
+// critical path. When the control stops the loop (AA attempt -> the graph's
+// IF branch, batch end, termination) it raises a flag with its barrier-1
+// arrival; the workers drop the speculative K1(k+1) and return. Nothing that
+// K1(k+1) wrote is read before it is rewritten: x-hat goes to the buffer of
+// u_{k-1} (no consumer after iteration k; at k = 1 the only exception, the
+// fixed-point start, rewrites u_0 with the identical T_x(u_0)), the x-half of
+// the push to the spare history slot (advance keeps cap + 1 slots), and the
+// K1 partials, which the control CTA folded before barrier 2. Results are
+// bit-identical to the per-kernel graph with the same CTA layout.
+struct GridBar {
+  unsigned long long arrive1;  // barrier 1: arrivals (low 40 bits) + stops (high bits)
+  unsigned long long arrive2;  // barrier 2: arrivals
+  unsigned long long pad[2];
+};
+constexpr unsigned long long kBarCount = (1ull << 40) - 1;
+constexpr unsigned long long kBarStop = 1ull << 40;
+
+__device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long long* p,
+                                                               unsigned long long v) {
+  unsigned long long prev;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;"
+               : "=l"(prev) : "l"(p), "l"(v) : "memory");
+  return prev;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Arrive at a barrier of nb participants and wait for the instance to fill.
+// Spins with relaxed loads (an acquire load invalidates the SM's L1 — under
+// CTAs still gathering — on every poll), then acquires once. Thread 0 only.
+__device__ __forceinline__ unsigned long long bar_arrive_wait(unsigned long long* p,
+                                                              unsigned long long add,
+                                                              unsigned long long nb) {
+  const unsigned long long prev = atom_add_acq_rel(p, add);
+  const unsigned long long target = ((prev & kBarCount) / nb + 1) * nb;
+  while ((ld_relaxed(p) & kBarCount) < target) {
+  }
+  return ld_acquire(p);
+}
+
+// The control CTA of k_plain_loop: state and parameters in shared memory for
+// the whole launch (it is the only writer of the state until it stops).
+__device__ __noinline__ void plain_loop_control(const IterBufs& B, const DevParams* P, DevState* S,
+                                                GridBar* gb, int nb1, int nb2, DevState& sm,
+                                                DevParams& pr, double* red) {
+  const unsigned long long G = gridDim.x;
+  __shared__ double t1s[P1_COUNT], t2s[P2_COUNT];
+  __shared__ Decision dec;
+  params_load(&pr, P);
+  __syncthreads();
+  const uint64_t t_start = globaltimer_ns();
+  uint64_t passes = 0;
+  for (;;) {
+    // barrier 1 of iteration k: K1(k) done -> fold its partials
+    if (threadIdx.x == 0) bar_arrive_wait(&gb->arrive1, 1, G);
+    __syncthreads();
+    double t1[P1_COUNT];
+    reduce_partial_rows<P1_COUNT>(B.part1, nb1, t1, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int q = 0; q < P1_COUNT; ++q) t1s[q] = t1[q];
+    // barrier 2: K2(k) done (the workers start K1(k+1) on plain-step roles)
+    if (threadIdx.x == 0) bar_arrive_wait(&gb->arrive2, 1, G);
+    __syncthreads();
+    double t2[P2_COUNT];
+    reduce_partial_rows<P2_COUNT>(B.part2, nb2, t2, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int q = 0; q < P2_COUNT; ++q) t2s[q] = t2[q];
+    __syncthreads();
+    const uint64_t k = sm.k;
+    const double g2 = __dadd_rn(t1s[P1_GX2], t2s[P2_GY2]);
+    const double bound = t1s[P1_BOUND], qy = t2s[P2_QY], cx = t1s[P1_CX];
+    const double infeas = t2s[P2_INFEAS], dsq = t1s[P1_DUALSQ];
+    if (threadIdx.x == 32) control_kkt_records(&pr, &sm, k, g2, bound, qy, cx, infeas, dsq, -1.0);
+    if (threadIdx.x == 0) dec = control_decide(&pr, &sm, k, g2, bound, qy, cx, infeas, dsq, -1.0, -1.0);
+    __syncthreads();
+    const bool stop = dec.attempt || dec.left <= 0;
+    ++passes;
+    if (threadIdx.x == 0 && stop) {
+      control_setcond(&pr, dec);
+      sm.loop_exits += 1;
+      sm.plain_iters += passes;
+      sm.plain_ns += globaltimer_ns() - t_start;
+    }
+    if (threadIdx.x == 32) control_commit(&pr, &sm, k, dec);
+    __syncthreads();
+    if (stop) {
+      // release the workers (they drop K1(k+1)), then hand the state over
+      if (threadIdx.x == 0) atom_add_acq_rel(&gb->arrive1, 1 + kBarStop);
+      state_store(S, &sm);
+      return;
+    }
+  }
+}
+
+template <bool PUSH>
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+    k_plain_loop(CsrDev KT, CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S,
+                 GridBar* gb, int nb1, int nb2) {
+  __shared__ __align__(16) DevState st;  // worker: roles of its iteration; control: the state
+  __shared__ double red[P1_COUNT * 32];
+  __shared__ int s_stop;
+  const int G = int(gridDim.x), W = G - 1, bid = int(blockIdx.x);
+  state_load(&st, S);
+  if (st.done || st.batch_left <= 0) return;  // (eager launches past the batch)
+  if (bid == W) {
+    __shared__ __align__(16) DevParams pr;
+    plain_loop_control(B, P, S, gb, nb1, nb2, st, pr, red);
+    return;
+  }
+  unsigned long long h0 = 0;  // stop flags raised before this launch
+  if (threadIdx.x == 0) h0 = ld_relaxed(&gb->arrive1) >> 40;
+  for (;;) {
+    if (bid < nb1) dual_side_rows<false, PUSH, 0, true>(KT, B, P, &st, bid, nb1, red);
+    __syncthreads();
+    if (threadIdx.x == 0) s_stop = (bar_arrive_wait(&gb->arrive1, 1, G) >> 40) != h0;
+    __syncthreads();
+    if (s_stop) return;  // the control stopped after the previous iteration
+    double acc[P2_COUNT] = {0.0, 0.0, 0.0};
+    if (bid < nb2) {
+      primal_side_rows<false, PUSH, true>(K, B, P, &st, bid, acc);
+      block_sum<P2_COUNT>(acc, red);
+      if (threadIdx.x == 0)
+#pragma unroll
+        for (int q = 0; q < P2_COUNT; ++q) B.part2[q * nb2 + bid] = acc[q];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bar_arrive_wait(&gb->arrive2, 1, G);
+      // the roles of iteration k+1 if iteration k is a plain step
+      st.aa_ok = 0;
+      control_commit(P, &st, st.k, Decision{0, 1});
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // TREE mode control: add the per-CTA partials of K1 (nu1 CTAs) and K2 (nu2)
 // in CTA order (thread-strided + fixed block tree), then run the control
 // logic on a shared-memory copy of the state.

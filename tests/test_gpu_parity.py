@@ -231,6 +231,56 @@ def test_fixed_point_start_and_budgets():
         assert out.trajectory.size == out.result.iterations + 1
 
 
+@pytest.mark.parametrize("method", [Method.AA_PDHG, Method.FAA_PDHG, Method.PDHG])
+def test_persistent_loop_matches_per_kernel_graph(monkeypatch, method):
+    """k_plain_loop (the persistent plain-step grid, pipeline.cuh) against the
+    per-kernel graph (AAPDHG_PERSIST=0). A layout below one wave keeps the
+    same CTA layout, so TREE results are bit-identical; on a wave-filling
+    layout the persistent grid spreads the slices over one CTA fewer (its
+    control CTA), so the K1/K2 partial sums re-associate: 1e-12 over the first
+    50 iterates and the same AA step pattern."""
+    for scale, exact in ((1.0, True), (0.05, False)):
+        p = problems.make_config(0 if exact else 1, scale=scale)
+        cfg = SolverConfig(method=method, m=5, toll=1e-12, max_iters=1500, tau=0.02, sigma=0.02,
+                           reduction="tree")
+        out = {}
+        for flag in ("0", "1"):
+            monkeypatch.setenv("AAPDHG_PERSIST", flag)
+            with Solver(p) as s:
+                out[flag] = s.solve(cfg)
+        a, b = out["0"], out["1"]
+        assert a.result.iterations == b.result.iterations == 1500
+        assert np.array_equal(a.trajectory["aa_step"], b.trajectory["aa_step"])
+        if exact:
+            assert np.array_equal(a.trajectory["g_norm"], b.trajectory["g_norm"])
+            assert np.array_equal(a.result.u.x, b.result.u.x)
+            assert np.array_equal(a.result.u.y, b.result.u.y)
+        else:
+            np.testing.assert_allclose(b.trajectory["g_norm"][:50], a.trajectory["g_norm"][:50],
+                                       rtol=1e-12)
+
+
+def test_persistent_loop_fixed_point_start_tree():
+    """The speculative K1 of k = 2 in k_plain_loop rewrites u_0's buffer while
+    the control decides k = 1. A fixed-point start (status FIXED_POINT_START,
+    answer u_0) on a wave-filling TREE layout must still return u_0 bit for
+    bit: x0 > 0 on 500 empty columns with c = 0, y0 = 0, q = 0."""
+    from paper_2508_08062_b200 import ProblemData, SparseMatrix
+    base = problems.make_config(1, scale=0.05).k
+    extra = 500
+    k = SparseMatrix(base.nrows, base.ncols + extra, base.row_ptr, base.col_idx, base.vals)
+    n = k.ncols
+    p = ProblemData(k, 0, np.zeros(n), np.zeros(k.nrows), np.zeros(n), np.full(n, np.inf))
+    x0 = np.zeros(n)
+    x0[base.ncols:] = np.random.default_rng(3).uniform(0.5, 2.0, extra)
+    with Solver(p) as s:
+        out = s.solve(SolverConfig(method=Method.AA_PDHG, reduction="tree", tau=0.05,
+                                   sigma=0.05), Iterate(x0, np.zeros(k.nrows)))
+    assert out.result.status == SolveStatus.FIXED_POINT_START
+    assert out.result.iterations == 0
+    assert np.array_equal(out.result.u.x, x0) and not out.result.u.y.any()
+
+
 def test_config_errors():
     toy = problems.toy()
     with Solver(toy) as s:
