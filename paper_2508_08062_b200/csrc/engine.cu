@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <cstdlib>
 #include <random>
@@ -257,6 +258,22 @@ void Problem::init_device(int device) {
   AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   AAPDHG_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device));
   pdl_ = env_int("AAPDHG_PDL", 1) != 0;
+  // the gather kernels want L1, not shared memory (a few KB per CTA): 10% of
+  // the shared-memory maximum keeps 6 CTAs/SM and leaves more L1 than the
+  // driver's default 64 KB carveout (configs[1]: 47.3 -> 46.5 us per plain
+  // iteration, profiles/exp_carveout.py); -1 = driver default
+  const int carve = env_int("AAPDHG_CARVEOUT", 10);
+  if (carve >= 0) {
+    auto set = [&](const void* f) {
+      AAPDHG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    };
+    set((const void*)k_plain_loop<true>);
+    set((const void*)k_plain_loop<false>);
+    set((const void*)k_dual_side<false, true>);
+    set((const void*)k_dual_side<false, false>);
+    set((const void*)k_primal_side<false, true>);
+    set((const void*)k_primal_side<false, false>);
+  }
 }
 
 // c, q, l, u on the device plus the scratch of power iteration / per-op /
@@ -598,7 +615,9 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
     const bool pdl = pdl_ && n_ > 0;
     const dim3 g(K2m.grid());
     auto kern = ser ? (push ? k_primal_side<true, true> : k_primal_side<true, false>)
-                    : (push ? k_primal_side<false, true> : k_primal_side<false, false>);
+                    : (push ? (env_int("AAPDHG_K2VAR", 0) == 2 ? k_primal_side<false, true, 2>
+                                                                : k_primal_side<false, true>)
+                            : k_primal_side<false, false>);
     LAUNCH("k_primal_side", launch_ex(kern, g, dim3(kThreads), 0, s, pdl, K2m, su.B, su.P, su.S));
   }
   if (ser) {  // join, then the y-side chains and the control
@@ -921,10 +940,16 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
       if (over > 0) d.nblk_short = d.nblk_short > over ? d.nblk_short - over : 0;
       return d;
     };
+    // (a warp owns one slice: every CTA keeps <= kWarps slices)
+    auto fits = [&](const CsrDev& d) {
+      return d.grid() <= workers &&
+             (d.nslices == 0 || int64_t(d.nblk_short) * kWarps >= int64_t(d.nslices));
+    };
     const CsrDev p1 = fit(K1m), p2 = fit(K2m);
-    if (workers >= 1 && p1.grid() <= workers && p2.grid() <= workers &&
-        (p1.nslices == 0 || p1.nblk_short > 0) && (p2.nslices == 0 || p2.nblk_short > 0) &&
-        plock.try_lock(device_)) {
+    if (env_int("AAPDHG_VERBOSE", 0))
+      std::fprintf(stderr, "aapdhg: k_plain_loop %d CTAs/SM, grids %d/%d -> %d/%d\n", per_sm,
+                   K1m.grid(), K2m.grid(), p1.grid(), p2.grid());
+    if (workers >= 1 && fits(p1) && fits(p2) && plock.try_lock(device_)) {
       gridbar_.reserve(sizeof(GridBar));
       su.persist = true;
       su.pk1 = p1;

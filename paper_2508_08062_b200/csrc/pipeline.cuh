@@ -839,10 +839,17 @@ __device__ __forceinline__ void primal_side_rows(const CsrDev& K, const IterBufs
   }
 }
 
-template <bool SERIAL, bool PUSH>
+// VAR 2 (experiment, AAPDHG_K2VAR=2): the SpMV alone, no epilogue or control
+template <bool SERIAL, bool PUSH, int VAR = 0>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
+  if constexpr (VAR == 2) {
+    double s;
+    const int i = row_sum<SERIAL>(K, B.upool + (int64_t)S->u_idx[U_HAT] * P->N, s);
+    if (i >= 0) B.kxpool[(int64_t)S->kx_idx[KX_HAT] * P->mrows + i] = s;
+    return;
+  }
   __shared__ double red[P2_COUNT * kWarps];
   double acc[P2_COUNT] = {0.0, 0.0, 0.0};
   primal_side_rows<SERIAL, PUSH>(K, B, P, S, int(blockIdx.x), acc);
