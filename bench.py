@@ -210,13 +210,25 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream(device=dev)
     if dist:
         # sharded solve: rank r owns K's row block R_r and
-        # column block C_r; NCCL all-gathers between the phases
+        # column block C_r; exchanges between the phases over peer memory
+        # (--transport p2p, the default: the kernels store into every rank's
+        # buffers, flag barriers) or NCCL all-gathers (--transport nccl)
         from paper_2508_08062_b200 import DistConfig, nccl_unique_id
+
+        transport = args.transport
+        if transport == "p2p":  # every rank must reach every peer (else NCCL)
+            ok = world <= 8 and all(torch.cuda.can_device_access_peer(dev, q)
+                                    for q in range(torch.cuda.device_count()) if q != dev)
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                                device=f"cuda:{dev}" if tdist.get_backend() == "nccl" else "cpu")
+            tdist.all_reduce(flag, op=tdist.ReduceOp.MIN)
+            transport = "p2p" if int(flag.item()) else "nccl"
+        args.transport = transport
 
         def dcfg():  # a fresh NCCL id per communicator (ids are single-use)
             box = [nccl_unique_id() if rank == 0 else None]
             tdist.broadcast_object_list(box, src=0)
-            return DistConfig(world=world, rank=rank, transport="nccl", nccl_id=box[0])
+            return DistConfig(world=world, rank=rank, transport=transport, nccl_id=box[0])
         s = Solver(p, device=dev, dist=dcfg())
     else:
         s = Solver(p, device=dev)
@@ -307,7 +319,8 @@ def run_ours(args, rank, world, local_rank):
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded planted-optimum generator, SURVEY.md 8(d))",
                 "config": dict(workload_config(p),
-                               parallelism=f"shard{world} (row/column blocks, NCCL all-gather)"
+                               parallelism=f"shard{world} (row/column blocks, "
+                                           f"{'peer-memory stores + flag barriers' if args.transport == 'p2p' else 'NCCL all-gather'})"
                                if dist else "single"),
                 "iterations_timed": iters, "aa_steps_timed": out.result.i,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt,
@@ -420,6 +433,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ttt", action="store_true")
     ap.add_argument("--ttt-cap", type=float, default=60.0)
+    ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
+                    help="sharded-solve exchanges: peer-memory stores (p2p, <= 8 GPUs) or NCCL")
     ap.add_argument("--shard", action="store_true",
                     help="use the sharded (NCCL) solve even at N=1 (exercises the N>1 path)")
     ap.add_argument("--traffic", type=float, default=None,

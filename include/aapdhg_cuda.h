@@ -156,10 +156,23 @@ typedef struct aapdhg_handle aapdhg_handle;
  *             aapdhg_cuda_nccl_id on rank 0 and broadcast by the caller).
  *   LOOPBACK: all `world` shards in this process on `device`, exchanging by
  *             device copies (tests the partitioned path on one GPU).
+ *   P2P:      as NCCL (same id, NCCL for setup and the non-iteration
+ *             exchanges), but inside the iteration every producing kernel
+ *             stores its chunk straight into every shard's buffer over
+ *             peer memory (CUDA IPC, NVLink / NVSwitch) and each exchange is
+ *             a flag barrier: no collective call on the iteration path.
+ *             world <= 8.
+ *   LOOPBACK_P2P: all shards in this process with the P2P exchanges (the
+ *             peers are the in-process shards' buffers).
  * No reference counterpart: the reference solve() is single-threaded
  * (proj/src/solver.cpp:125-253); results match it within the TREE-mode
  * tolerance (scalar sums meet in rank order). */
-enum { AAPDHG_DIST_NCCL = 0, AAPDHG_DIST_LOOPBACK = 1 };
+enum {
+  AAPDHG_DIST_NCCL = 0,
+  AAPDHG_DIST_LOOPBACK = 1,
+  AAPDHG_DIST_P2P = 2,          /* one shard per process; peer-memory exchanges */
+  AAPDHG_DIST_LOOPBACK_P2P = 3  /* all shards in this process; peer-memory exchanges */
+};
 #define AAPDHG_NCCL_ID_BYTES 128
 typedef struct aapdhg_dist_view {
   int32_t rank;       /* this process's shard (NCCL); ignored by LOOPBACK */

@@ -28,7 +28,7 @@ METHOD_PDHG, METHOD_AA, METHOD_FAA = 0, 1, 2
  SOLVE_FIXED_POINT_START) = range(5)
 REDUCE_AUTO, REDUCE_SERIAL, REDUCE_TREE = 0, 1, 2
 # sharded-solve transports
-DIST_NCCL, DIST_LOOPBACK = 0, 1
+DIST_NCCL, DIST_LOOPBACK, DIST_P2P, DIST_LOOPBACK_P2P = 0, 1, 2, 3
 NCCL_ID_BYTES = 128
 
 _dp = C.POINTER(C.c_double)

@@ -325,8 +325,11 @@ class DistConfig:
     """A sharded solve (include/aapdhg_cuda.h aapdhg_dist_view): `world`
     row/column blocks of the LP. transport "nccl": this process is shard
     `rank` on its own GPU, all ranks pass the same `nccl_id` (nccl_unique_id()
-    on rank 0, broadcast by the caller). "loopback": all shards in this
-    process on one device (exercises the partitioned path on one GPU)."""
+    on rank 0, broadcast by the caller). "p2p": as "nccl", but inside the
+    iteration the kernels store straight into every shard's buffers over peer
+    memory (CUDA IPC, NVLink) and each exchange is a flag barrier (<= 8
+    shards). "loopback" / "loopback_p2p": all shards in this process on one
+    device with copy / peer-store exchanges (the partitioned path on one GPU)."""
     world: int
     rank: int = 0
     transport: str = "nccl"
@@ -375,9 +378,11 @@ class Solver:
             dv = _abi.DistView()
             dv.rank = int(dist.rank)
             dv.world = int(dist.world)
-            if dist.transport not in ("nccl", "loopback"):
-                raise InputError("dist: transport must be 'nccl' or 'loopback'")
-            dv.transport = _abi.DIST_NCCL if dist.transport == "nccl" else _abi.DIST_LOOPBACK
+            transports = {"nccl": _abi.DIST_NCCL, "loopback": _abi.DIST_LOOPBACK,
+                          "p2p": _abi.DIST_P2P, "loopback_p2p": _abi.DIST_LOOPBACK_P2P}
+            if dist.transport not in transports:
+                raise InputError("dist: transport must be one of " + ", ".join(transports))
+            dv.transport = transports[dist.transport]
             self._id = None
             if dist.nccl_id is not None:
                 self._id = (C.c_uint8 * _abi.NCCL_ID_BYTES).from_buffer_copy(

@@ -27,6 +27,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMaxMemory = 64;       // largest AA memory capacity supported
 constexpr int kDotChunk = 512;       // elements per CTA in the tree multi-dot
 constexpr int kCtrlThreads = 1024;
+constexpr int kMaxPeers = 8;         // shards of a peer-memory (P2P) sharded solve
 
 // iterate roles
 enum { U_CUR = 0, U_PREV = 1, U_HAT = 2, U_CAND = 3 };
@@ -96,13 +97,21 @@ struct DevParams {
   cudaGraphConditionalHandle cond_aa;    // IF node of the AA branch
   cudaGraphConditionalHandle cond_loop;  // WHILE node of the iteration batch
   // sharded solve (nullptr / 0 on a single GPU): K1 gathers y from the
-  // all-gathered ygather, K2 gathers xhat from xgather; K1 also writes xhat
-  // into this shard's chunk of xgather (xg_own) and keeps K'y in T.
+  // all-gathered ygather, K2 gathers xhat from xgather. The producers write
+  // this shard's chunk of each exchanged buffer into ndst destinations: the
+  // shard's own buffer (NCCL / copy transports: ndst = 1, the all-gather
+  // follows), or every shard's buffer over peer memory (P2P transports:
+  // ndst = world, a flag barrier follows) — K1 xhat -> xg_dst, K2 yhat ->
+  // yg_dst, K2's last CTA the 8 shard totals -> scal_dst, the AA dot totals
+  // -> dots_dst. K1 also keeps K'y in T.
   const double* xgather;
   const double* ygather;
-  double* xg_own;
-  double* yg_own;  // K2 writes yhat into this shard's chunk of ygather
-  int32_t store_T, pad_sh;
+  int32_t ndst, store_T;
+  double* xg_dst[kMaxPeers];
+  double* yg_dst[kMaxPeers];
+  double* scal_dst[kMaxPeers];
+  double* dots_dst[kMaxPeers];
+  uint64_t p2p_epoch;  // barrier sequence base of this solve (high 32 bits)
   int64_t Nglob;  // n + m of the whole LP (FAA's QR row-count test)
 };
 
@@ -131,6 +140,7 @@ struct DevState {
   int32_t prev_plain;              // the previous step was T(u_{k-1}) (not an AA candidate)
   int32_t pad_pp;
   int32_t batch_left;              // iterations left in this graph launch
+  uint64_t p2p_seq[8];             // P2P flag barriers passed, per exchanged buffer
 };
 
 // Gathered vector: a plain pointer, or a role of the iterate pool resolved
@@ -169,8 +179,7 @@ struct IterBufs {
   const double* rinit2;  // L2-blocked K: partial K xhat of the earlier passes
   int32_t nu1;        // K1 CTAs (rows of part1)
   int32_t fused_ctrl; // TREE: k_primal_side's last CTA runs the control (1) or,
-                      // sharded, writes this shard's 8 totals to scal_own (2)
-  double* scal_own;
+                      // sharded, writes this shard's 8 totals to P->scal_dst (2)
   const double* c;
   const double* q;
   const double* l;

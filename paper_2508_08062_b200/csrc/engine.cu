@@ -1266,6 +1266,10 @@ Problem::Problem(const ShardSpec& sp, int device) : device_(device) {
   yg_.reserve(sizeof(double) * W * maxr_);
   lg_.reserve(sizeof(double) * W * maxc_);
   scal_all_.reserve(sizeof(double) * W * 8);
+  // the dots exchange buffer at its largest (peers may hold its address)
+  dots_all_.reserve(sizeof(double) * size_t(W) * size_t(num_items_host(kMaxMemory, AAPDHG_METHOD_FAA)));
+  p2p_flags_.reserve(sizeof(unsigned long long) * 8 * kMaxPeers);
+  AAPDHG_CUDA(cudaMemsetAsync(p2p_flags_.p, 0, p2p_flags_.bytes, stream_));
   AAPDHG_CUDA(cudaMemsetAsync(xg_.p, 0, xg_.bytes, stream_));
   AAPDHG_CUDA(cudaMemsetAsync(yg_.p, 0, yg_.bytes, stream_));
   AAPDHG_CUDA(cudaMemsetAsync(lg_.p, 0, lg_.bytes, stream_));
@@ -1275,8 +1279,29 @@ Problem::Problem(const ShardSpec& sp, int device) : device_(device) {
 }
 
 ShardBufs Problem::shard_bufs() const {
-  return ShardBufs{xg_.as<double>(), yg_.as<double>(), lg_.as<double>(), scal_all_.as<double>(),
-                   dots_all_.as<double>(), maxc_, maxr_, dot_stride_};
+  return ShardBufs{xg_.as<double>(),    yg_.as<double>(), lg_.as<double>(),
+                   scal_all_.as<double>(), dots_all_.as<double>(),
+                   p2p_flags_.as<unsigned long long>(), maxc_, maxr_, dot_stride_};
+}
+
+// P2P transports: every shard's exchange buffers, indexed by rank (this
+// shard's own entry included). The producers then write this shard's chunk
+// into all of them and the exchanges become flag barriers (k_p2p_barrier).
+void Problem::sh_set_peers(const std::vector<ShardBufs>& peers) {
+  if (peers.size() > size_t(kMaxPeers))
+    throw StatusError(AAPDHG_ERR_UNSUPPORTED, "p2p: more than 8 shards");
+  peers_ = peers;
+}
+
+void Problem::sh_p2p_barrier(int slot, int phase) {
+  P2pFlags F{};
+  for (size_t q = 0; q < peers_.size(); ++q) F.peer[q] = peers_[q].flags;
+  F.own = p2p_flags_.as<unsigned long long>();
+  F.world = int(peers_.size());
+  F.rank = shard_rank_;
+  k_p2p_barrier<<<1, 32, 0, stream_>>>(F, sh_su_->P, sh_su_->S, slot, phase);
+  AAPDHG_CUDA(cudaGetLastError());
+  ++sh_launches_;
 }
 
 void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
@@ -1286,8 +1311,7 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   const int method = prm->method;
   const int cap = method == AAPDHG_METHOD_PDHG ? 0 : int(prm->m);
   ensure_iter_buffers(method, std::max(cap, 1));
-  dot_stride_ = num_items_host(std::max(cap, 1), AAPDHG_METHOD_FAA);
-  dots_all_.reserve(sizeof(double) * size_t(shard_world_) * size_t(dot_stride_));
+  dot_stride_ = num_items_host(std::max(cap, 1), AAPDHG_METHOD_FAA);  // (<= the reserved stride)
   if (d_hat) {
     dhat_.reserve(sizeof(double) * std::max<int64_t>(N_, 1));
     h2d(dhat_.p, d_hat, sizeof(double) * N_, stream_);
@@ -1336,8 +1360,18 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   P.use_cond = 0;
   P.xgather = xg_.as<double>();
   P.ygather = yg_.as<double>();
-  P.xg_own = xg_.as<double>() + int64_t(shard_rank_) * maxc_;
-  P.yg_own = yg_.as<double>() + int64_t(shard_rank_) * maxr_;
+  // this shard's chunk of the exchange buffers: its own (then all-gathered)
+  // or, P2P, every shard's (then a flag barrier)
+  std::vector<ShardBufs> dst = peers_;
+  if (dst.empty()) dst.push_back(shard_bufs());
+  P.ndst = int32_t(dst.size());
+  for (size_t q = 0; q < dst.size(); ++q) {
+    P.xg_dst[q] = dst[q].xg + int64_t(shard_rank_) * maxc_;
+    P.yg_dst[q] = dst[q].yg + int64_t(shard_rank_) * maxr_;
+    P.scal_dst[q] = dst[q].scal + int64_t(shard_rank_) * 8;
+    P.dots_dst[q] = dst[q].dots + int64_t(shard_rank_) * dot_stride_;
+  }
+  P.p2p_epoch = ++p2p_epoch_;
   P.store_T = 1;
 
   DevState S0 = DevState{};
@@ -1352,8 +1386,7 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   SolveSetup& su = *sh_su_;
   su.B = iter_bufs();
   su.B.nu1 = sh_k1m().grid();
-  su.B.fused_ctrl = 2;  // K2's last CTA writes this shard's totals
-  su.B.scal_own = scal_all_.as<double>() + shard_rank_ * 8;
+  su.B.fused_ctrl = 2;  // K2's last CTA writes this shard's totals (P.scal_dst)
   su.B.rinit1 = ktb_.nb() > 1 ? ktb_.partial.as<double>() : nullptr;
   su.B.rinit2 = kb_.nb() > 1 ? kb_.partial.as<double>() : nullptr;
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
@@ -1383,20 +1416,29 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   sh_launches_ = 1;
 }
 
-void Problem::sh_stage_x(int role, int mode) {
-  k_stage<<<grid_for(n_), kThreads, 0, stream_>>>(upool_.as<double>(), role, N_, 0, n_,
-                                                   xg_.as<double>() + shard_rank_ * maxc_,
-                                                   sh_su_->S, mode);
-  AAPDHG_CUDA(cudaGetLastError());
-  ++sh_launches_;
+// peers: into every P2P destination (else this shard's own buffer)
+void Problem::sh_stage_x(int role, int mode, bool peers) {
+  const bool to_peers = peers && !peers_.empty();
+  const size_t nd = to_peers ? peers_.size() : 1;
+  for (size_t q = 0; q < nd; ++q) {
+    double* dst = to_peers ? peers_[q].xg : xg_.as<double>();
+    k_stage<<<grid_for(n_), kThreads, 0, stream_>>>(upool_.as<double>(), role, N_, 0, n_,
+                                                     dst + shard_rank_ * maxc_, sh_su_->S, mode);
+    AAPDHG_CUDA(cudaGetLastError());
+    ++sh_launches_;
+  }
 }
 
-void Problem::sh_stage_y(int role, int mode) {
-  k_stage<<<grid_for(m_), kThreads, 0, stream_>>>(upool_.as<double>(), role, N_, n_, m_,
-                                                   yg_.as<double>() + shard_rank_ * maxr_,
-                                                   sh_su_->S, mode);
-  AAPDHG_CUDA(cudaGetLastError());
-  ++sh_launches_;
+void Problem::sh_stage_y(int role, int mode, bool peers) {
+  const bool to_peers = peers && !peers_.empty();
+  const size_t nd = to_peers ? peers_.size() : 1;
+  for (size_t q = 0; q < nd; ++q) {
+    double* dst = to_peers ? peers_[q].yg : yg_.as<double>();
+    k_stage<<<grid_for(m_), kThreads, 0, stream_>>>(upool_.as<double>(), role, N_, n_, m_,
+                                                     dst + shard_rank_ * maxr_, sh_su_->S, mode);
+    AAPDHG_CUDA(cudaGetLastError());
+    ++sh_launches_;
+  }
 }
 
 void Problem::sh_init_kx() {
@@ -1460,8 +1502,7 @@ void Problem::sh_aa_dots() {
   k_stage_g<<<grid_for(N_), kThreads, 0, stream_>>>(su.B.upool, su.B.gpool, su.P, su.S);
   ++sh_launches_;
   k_tree_dots<<<su.ndot_blk, kThreads, 0, stream_>>>(su.D, su.P, su.S);
-  k_dot_totals<<<1, 1024, 0, stream_>>>(su.D, su.P, su.S,
-                                         dots_all_.as<double>() + shard_rank_ * dot_stride_);
+  k_dot_totals<<<1, 1024, 0, stream_>>>(su.D, su.P, su.S);
   AAPDHG_CUDA(cudaGetLastError());
   sh_launches_ += 2;
 }
@@ -1473,8 +1514,8 @@ void Problem::sh_aa_solve_mix(int world) {
   k_mix<<<grid_for(N_), kThreads, 0, stream_>>>(su.B, su.B.dg, su.P, su.S, 1);
   AAPDHG_CUDA(cudaGetLastError());
   sh_launches_ += 2;
-  sh_stage_x(U_CAND, 2);  // an accepted candidate replaces xhat / yhat in the
-  sh_stage_y(U_CAND, 2);  // all-gather chunks (K1 / K2 wrote those)
+  sh_stage_x(U_CAND, 2, true);  // an accepted candidate replaces xhat / yhat in
+  sh_stage_y(U_CAND, 2, true);  // the exchange chunks (K1 / K2 wrote those)
 }
 
 void Problem::sh_aa_recache_commit() {

@@ -59,6 +59,7 @@ struct ShardBufs {
   double* lg;    // world x maxc: lambda of the final iterate
   double* scal;  // world x 8: per-shard iteration totals / power-iteration norms
   double* dots;  // world x dot_stride: per-shard AA dot totals
+  unsigned long long* flags;  // P2P barrier arrivals: 8 exchanges x kMaxPeers shards
   int64_t maxc, maxr, dot_stride;
 };
 
@@ -75,8 +76,11 @@ class Problem {
   int shard_rank() const { return shard_rank_; }
   void sh_begin(const aapdhg_solve_params* prm, double tau, double sigma, const double* x0,
                 const double* y0, const double* d_hat, double wall_offset);
-  void sh_stage_x(int role, int mode);  // x-part of an iterate -> own chunk of xg
-  void sh_stage_y(int role, int mode);  // y-part -> own chunk of yg
+  // x-part of an iterate -> this shard's chunk of xg (peers: of every P2P peer's)
+  void sh_stage_x(int role, int mode, bool peers = false);
+  void sh_stage_y(int role, int mode, bool peers = false);  // y-part -> yg
+  void sh_set_peers(const std::vector<ShardBufs>& peers);    // P2P transports
+  void sh_p2p_barrier(int slot, int phase);                  // k_p2p_barrier
   void sh_init_kx();                    // K x of the start iterate (after AG of xg)
   void sh_k1();                         // K'y + xhat (+ own chunk of xg)
   void sh_k2_totals();                  // K xhat + yhat, then own iteration totals
@@ -199,7 +203,9 @@ class Problem {
   int shard_rank_ = -1;  // -1: a whole-LP handle
   int shard_world_ = 1;
   int64_t maxc_ = 0, maxr_ = 0, dot_stride_ = 0;
-  DevBuf xg_, yg_, lg_, scal_all_, dots_all_;
+  DevBuf xg_, yg_, lg_, scal_all_, dots_all_, p2p_flags_;
+  std::vector<ShardBufs> peers_;  // P2P: every shard's exchange buffers (by rank)
+  uint64_t p2p_epoch_ = 0;        // solves begun (barrier sequence base)
   SolveSetup* sh_su_ = nullptr;
   DevParams sh_params_{};
   uint64_t sh_launches_ = 0;

@@ -621,7 +621,7 @@ __device__ __noinline__ bool tail_control(const IterBufs& B, DevState* S, TailSm
 #endif
   if (B.fused_ctrl == 2) {  // sharded: this shard's totals (k_local_totals' layout)
     if (threadIdx.x == 0) {
-      double* own = B.scal_own;
+      double own[8];
       own[0] = __ldcg(&S->tot1[P1_GX2]);
       own[1] = __ldcg(&S->tot1[P1_BOUND]);
       own[2] = __ldcg(&S->tot1[P1_CX]);
@@ -630,6 +630,9 @@ __device__ __noinline__ bool tail_control(const IterBufs& B, DevState* S, TailSm
       own[5] = t2[P2_QY];
       own[6] = t2[P2_INFEAS];
       own[7] = (double)(globaltimer_ns() - ts.st.t0_ns) * 1e-9 + ts.pr.wall_offset_s;
+      for (int q = 0; q < ts.pr.ndst; ++q)  // own chunk / every peer's chunk
+#pragma unroll
+        for (int t = 0; t < 8; ++t) ts.pr.scal_dst[q][t] = own[t];
       S->ticket = 0;
     }
     return true;
@@ -747,7 +750,7 @@ __device__ __forceinline__ void dual_side_rows(const CsrDev& KT, const IterBufs&
     double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));
     xn = smin(smax(xn, lj), uj);
     B.upool[(int64_t)S->u_idx[U_HAT] * N + j] = xn;
-    if (P->xg_own) P->xg_own[j] = xn;
+    for (int q = 0; q < P->ndst; ++q) P->xg_dst[q][j] = xn;  // sharded: own / peers' chunks
     const double d = __dsub_rn(xn, xj);
     const double red_c = __dsub_rn(cj, t);
     const double lam = project_lambda1(red_c, lj, uj);
@@ -820,7 +823,7 @@ __device__ __forceinline__ void primal_side_rows(const CsrDev& K, const IterBufs
         __dadd_rn(yi, __dmul_rn(P->sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
     if (i < P->m1) yn = smax(yn, 0.0);
     B.upool[(int64_t)S->u_idx[U_HAT] * N + n + i] = yn;
-    if (P->yg_own) P->yg_own[i] = yn;
+    for (int q = 0; q < P->ndst; ++q) P->yg_dst[q][i] = yn;
     B.kxpool[(int64_t)S->kx_idx[KX_HAT] * mr + i] = s;
     const double d = __dsub_rn(yn, yi);
     double v = __dsub_rn(qi, kxi);

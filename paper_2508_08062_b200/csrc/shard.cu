@@ -130,13 +130,17 @@ ShardGroup::ShardGroup(const aapdhg_problem_view* v, int device, const aapdhg_di
   m_ = k.nrows;
   m1_ = v->m1;
   nnz_ = k.nnz;
-  if (transport_ != AAPDHG_DIST_NCCL && transport_ != AAPDHG_DIST_LOOPBACK)
+  if (transport_ < AAPDHG_DIST_NCCL || transport_ > AAPDHG_DIST_LOOPBACK_P2P)
     throw StatusError(AAPDHG_ERR_INPUT, "problem_create_dist: unknown transport");
+  multi_ = transport_ == AAPDHG_DIST_NCCL || transport_ == AAPDHG_DIST_P2P;
+  p2p_ = transport_ == AAPDHG_DIST_P2P || transport_ == AAPDHG_DIST_LOOPBACK_P2P;
+  if (p2p_ && world_ > kMaxPeers)
+    throw StatusError(AAPDHG_ERR_UNSUPPORTED, "problem_create_dist: P2P transports take <= 8 shards");
   if (world_ < 1) throw StatusError(AAPDHG_ERR_INPUT, "problem_create_dist: world < 1");
-  if (transport_ == AAPDHG_DIST_NCCL && (rank_ < 0 || rank_ >= world_))
+  if (multi_ && (rank_ < 0 || rank_ >= world_))
     throw StatusError(AAPDHG_ERR_INPUT, "problem_create_dist: rank out of range");
-  if (transport_ == AAPDHG_DIST_NCCL && !d->nccl_id)
-    throw StatusError(AAPDHG_ERR_INPUT, "problem_create_dist: NCCL transport needs nccl_id");
+  if (multi_ && !d->nccl_id)
+    throw StatusError(AAPDHG_ERR_INPUT, "problem_create_dist: NCCL / P2P transports need nccl_id");
   if (world_ > std::min(n_, m_))
     throw StatusError(AAPDHG_ERR_UNSUPPORTED,
                       "problem_create_dist: every shard needs at least one row and one column");
@@ -168,7 +172,7 @@ ShardGroup::ShardGroup(const aapdhg_problem_view* v, int device, const aapdhg_di
     throw StatusError(AAPDHG_ERR_UNSUPPORTED, "problem_create_dist: padded index overflow");
 
   std::vector<int> ranks;
-  if (transport_ == AAPDHG_DIST_NCCL) ranks.push_back(rank_);
+  if (multi_) ranks.push_back(rank_);
   else
     for (int r = 0; r < world_; ++r) ranks.push_back(r);
   for (int r : ranks) {
@@ -211,7 +215,7 @@ ShardGroup::ShardGroup(const aapdhg_problem_view* v, int device, const aapdhg_di
     shards_.emplace_back(new Problem(sp, device));
   }
   AAPDHG_CUDA(cudaSetDevice(device));
-  if (transport_ == AAPDHG_DIST_LOOPBACK) {
+  if (!multi_) {
     AAPDHG_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
     stream_ = own_stream_;
     each([&](Problem& s) { s.set_stream(stream_); });
@@ -223,10 +227,81 @@ ShardGroup::ShardGroup(const aapdhg_problem_view* v, int device, const aapdhg_di
     nccl_check(nccl().CommInitRank(&comm, world_, id, rank_), "ncclCommInitRank");
     comm_ = comm;
   }
+  if (p2p_) open_peers();
+}
+
+// P2P transports: every shard's exchange buffers as pointers this process can
+// store to. Loopback: the other in-process shards' buffers. One shard per
+// process: CUDA IPC handles of xg / yg / scal / dots / flags, all-gathered
+// once over NCCL, opened with peer access (NVLink / NVSwitch).
+void ShardGroup::open_peers() {
+  std::vector<ShardBufs> peers;
+  if (!multi_) {
+    for (auto& s : shards_) peers.push_back(s->shard_bufs());
+    each([&](Problem& s) { s.sh_set_peers(peers); });
+    return;
+  }
+  const ShardBufs mine = shards_[0]->shard_bufs();
+  constexpr int NB = 5;
+  struct Handles {
+    cudaIpcMemHandle_t h[NB];
+  };
+  Handles hm{};
+  void* bases[NB] = {mine.xg, mine.yg, mine.scal, mine.dots, mine.flags};
+  for (int b = 0; b < NB; ++b) AAPDHG_CUDA(cudaIpcGetMemHandle(&hm.h[b], bases[b]));
+  DevBuf dh;
+  dh.reserve(sizeof(Handles) * size_t(world_));
+  uint8_t* d = dh.as<uint8_t>();
+  AAPDHG_CUDA(cudaMemcpyAsync(d + rank_ * sizeof(Handles), &hm, sizeof(Handles),
+                              cudaMemcpyHostToDevice, stream_));
+  nccl_check(nccl().AllGather(d + rank_ * sizeof(Handles), d, sizeof(Handles), ncclUint8,
+                              static_cast<ncclComm_t>(comm_), stream_),
+             "ncclAllGather(ipc handles)");
+  std::vector<Handles> all(static_cast<size_t>(world_));
+  AAPDHG_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(Handles) * all.size(), cudaMemcpyDeviceToHost,
+                              stream_));
+  AAPDHG_CUDA(cudaStreamSynchronize(stream_));
+  for (int q = 0; q < world_; ++q) {
+    if (q == rank_) {
+      peers.push_back(mine);
+      continue;
+    }
+    void* p[NB];
+    for (int b = 0; b < NB; ++b) {
+      AAPDHG_CUDA(cudaIpcOpenMemHandle(&p[b], all[size_t(q)].h[b], cudaIpcMemLazyEnablePeerAccess));
+      ipc_opened_.push_back(p[b]);
+    }
+    ShardBufs sb = mine;
+    sb.xg = static_cast<double*>(p[0]);
+    sb.yg = static_cast<double*>(p[1]);
+    sb.scal = static_cast<double*>(p[2]);
+    sb.dots = static_cast<double*>(p[3]);
+    sb.flags = static_cast<unsigned long long*>(p[4]);
+    sb.lg = nullptr;  // (not exchanged over peer memory)
+    peers.push_back(sb);
+  }
+  shards_[0]->sh_set_peers(peers);
+}
+
+// The in-loop exchanges: P2P transports only synchronise (the producers
+// wrote every shard's buffer); otherwise the all-gather.
+void ShardGroup::exchange(Buf b) {
+  if (!p2p_) {
+    allgather(b);
+    return;
+  }
+  const int slot = int(b);
+  if (multi_) {
+    shards_[0]->sh_p2p_barrier(slot, 3);
+  } else {  // in-process shards: every arrival first, then the waits
+    each([&](Problem& s) { s.sh_p2p_barrier(slot, 1); });
+    each([&](Problem& s) { s.sh_p2p_barrier(slot, 2); });
+  }
 }
 
 ShardGroup::~ShardGroup() {
   if (stream_) cudaStreamSynchronize(stream_);
+  for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   if (comm_) nccl().CommDestroy(static_cast<ncclComm_t>(comm_));
   shards_.clear();
   if (own_stream_) cudaStreamDestroy(own_stream_);
@@ -242,14 +317,15 @@ void ShardGroup::set_stream(cudaStream_t s) {
 void ShardGroup::allgather(Buf b) {
   auto pick = [&](const ShardBufs& sb, int64_t& chunk) -> double* {
     switch (b) {
-      case XG: chunk = sb.maxc; return sb.xg;
+      case XG:
+      case XG2: chunk = sb.maxc; return sb.xg;
       case YG: chunk = sb.maxr; return sb.yg;
       case LG: chunk = sb.maxc; return sb.lg;
       case SCAL: chunk = 8; return sb.scal;
       default: chunk = sb.dot_stride; return sb.dots;
     }
   };
-  if (transport_ == AAPDHG_DIST_NCCL) {
+  if (multi_) {
     int64_t chunk = 0;
     double* buf = pick(shards_[0]->shard_bufs(), chunk);
     nccl_check(nccl().AllGather(buf + rank_ * chunk, buf, size_t(chunk), ncclDouble,
@@ -366,24 +442,28 @@ void ShardGroup::solve(const aapdhg_solve_params* prm, const double* x0, const d
   // or NCCL cannot capture that, fall back to one captured graph per
   // iteration with the AA branch predicated on the device (its all-gathers
   // then always run).
+  // (P2P transports: the producers store into every shard's buffer and each
+  // exchange is a flag barrier; the exchange points are where every shard
+  // has finished reading the buffer's previous contents — DESIGN.md §8)
   auto core = [&] {
-    allgather(YG);
+    exchange(YG);
     each([&](Problem& s) { s.sh_k1(); });
-    allgather(XG);
+    exchange(XG);
     each([&](Problem& s) { s.sh_k2_totals(); });
-    allgather(SCAL);
+    exchange(SCAL);
     each([&](Problem& s) { s.sh_control(world_); });
   };
   auto aa_branch = [&] {
     each([&](Problem& s) { s.sh_aa_dots(); });
-    allgather(DOTS);
+    exchange(DOTS);
     each([&](Problem& s) { s.sh_aa_solve_mix(world_); });
-    allgather(XG);
+    exchange(XG2);
     each([&](Problem& s) { s.sh_aa_recache_commit(); });
   };
   // y of the start iterate; afterwards K2 (yhat) or the accepted candidate
   // writes each shard's chunk
   each([&](Problem& s) { s.sh_stage_y(-1, 0); });
+  if (p2p_) allgather(YG);  // (the loop's first exchange(YG) only synchronises)
   const char* ge = std::getenv("AAPDHG_SHARD_GRAPH");
   const int mode = ge && *ge ? std::atoi(ge) : 2;  // 2 WHILE/IF, 1 per iteration, 0 eager
   cudaGraphExec_t exec = nullptr;

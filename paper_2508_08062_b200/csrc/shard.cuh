@@ -54,9 +54,10 @@ __global__ void __launch_bounds__(128)
 }
 
 // This shard's Gram / rhs / column-norm partial dots (k_tree_dots per-CTA
-// partials, summed in CTA order like k_aa_solve does) into own[items].
+// partials, summed in CTA order like k_aa_solve does) into its chunk of the
+// dots exchange buffer of every destination (P->dots_dst).
 __global__ void __launch_bounds__(1024)
-    k_dot_totals(DotBufs D, const DevParams* __restrict__ P, const DevState* S, double* own) {
+    k_dot_totals(DotBufs D, const DevParams* __restrict__ P, const DevState* S) {
   if (S->done || !S->aa_attempt) return;
   const int nit = num_items(S->mem_size, P->method);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -66,7 +67,54 @@ __global__ void __launch_bounds__(1024)
     for (int b = lane; b < P->ndot_blk; b += 32) s = __dadd_rn(s, pp[b]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) own[it] = s;
+    if (lane == 0)
+      for (int q = 0; q < P->ndst; ++q) P->dots_dst[q][it] = s;
+  }
+}
+
+// Peer-memory (P2P) exchange barrier. The producers already stored this
+// shard's chunk into every shard's buffer (P->*_dst); this publishes that and
+// waits until every shard has published the same exchange. Shard r's
+// arrival at barrier `slot` is flags[slot * kMaxPeers + r] = seq in every
+// shard's flag array, seq = (solve epoch << 32) + passes of this barrier
+// (identical on every shard: the replicated control takes the same branches).
+// The system-scope release orders this shard's earlier peer stores (kernels
+// before it in the stream: cumulativity) before the flag; the waiter's
+// acquire orders the flag before the consumer kernels after it.
+// phase 1: arrive, 2: wait, 3: both (one shard per process). In-process
+// loopback shards arrive all first, then wait (no kernel spins on a shard
+// that has not been launched).
+struct P2pFlags {
+  unsigned long long* peer[kMaxPeers];  // every shard's flag array
+  unsigned long long* own;
+  int32_t world, rank;
+};
+
+__global__ void k_p2p_barrier(P2pFlags F, const DevParams* __restrict__ P, DevState* S, int slot,
+                              int phase) {
+  if (threadIdx.x != 0) return;
+  if (phase & 1) {
+    const unsigned long long seq = (P->p2p_epoch << 32) | (++S->p2p_seq[slot]);
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (int q = 0; q < F.world; ++q)
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(F.peer[q] + slot * kMaxPeers + F.rank),
+                   "l"(seq)
+                   : "memory");
+  }
+  if (phase & 2) {
+    const unsigned long long seq = (P->p2p_epoch << 32) | S->p2p_seq[slot];
+    const uint64_t t0 = globaltimer_ns();
+    for (int r = 0; r < F.world; ++r) {
+      unsigned long long v;
+      for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(F.own + slot * kMaxPeers + r)
+                     : "memory");
+        if (v >= seq) break;
+        // a peer that never arrives (crashed rank): fail the launch instead
+        // of hanging the GPU
+        if (globaltimer_ns() - t0 > 30000000000ull) asm volatile("trap;");
+      }
+    }
   }
 }
 

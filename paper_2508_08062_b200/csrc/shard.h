@@ -38,8 +38,12 @@ class ShardGroup {
   uint64_t last_loop_iters() const { return last_loop_iters_; }
 
  private:
-  enum Buf { XG, YG, LG, SCAL, DOTS };
+  // exchanged buffers (XG2: the candidate x of an AA step; also the P2P
+  // barrier slot)
+  enum Buf { XG, YG, LG, SCAL, DOTS, XG2 };
   void allgather(Buf b);
+  void exchange(Buf b);
+  void open_peers();
   double power_norm(int max_iters, double rel_tol, uint64_t seed);
   template <class F>
   void each(F&& f) {
@@ -47,6 +51,9 @@ class ShardGroup {
   }
 
   int world_ = 1, transport_ = 0, rank_ = 0, device_ = 0;
+  bool multi_ = false;  // one shard per process (NCCL / P2P)
+  bool p2p_ = false;    // peer-memory exchanges (P2P / LOOPBACK_P2P)
+  std::vector<void*> ipc_opened_;
   int n_ = 0, m_ = 0, m1_ = 0;
   int64_t nnz_ = 0;
   bool all_zero_ = false, bounds_ok_ = true;

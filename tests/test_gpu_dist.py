@@ -1,9 +1,12 @@
 """GPU: the sharded (multi-GPU) solve, SURVEY.md §8(e).
 
-Only one GPU is available, so the partitioned path is exercised two ways:
+Only one GPU is available, so the partitioned path is exercised three ways:
   * LOOPBACK: `world` shards in one process on cuda:0, all-gathers as device
     copies on one stream (the same kernels and exchange schedule as NCCL);
-  * NCCL with world = 1: the real ncclCommInitRank / ncclAllGather calls.
+  * LOOPBACK_P2P: the same shards with the peer-memory exchanges (producers
+    store into every shard's buffer, flag barriers between the phases);
+  * NCCL / P2P with world = 1: the real ncclCommInitRank / ncclAllGather
+    calls, IPC handle export and the flag barrier on one rank.
 Bar (SURVEY.md §8(e) "Determinism / parity across G"): the SpMV row sums are
 the unsplit CSR rows, only the scalar sums meet across shards, so 1-vs-G
 agreement of the first 50 iterates within 1e-10 relative; full solves reach
@@ -37,10 +40,11 @@ def cfg1():
     return p, tau, ref
 
 
+@pytest.mark.parametrize("transport", ["loopback", "loopback_p2p"])
 @pytest.mark.parametrize("world", [1, 2, 3, 5])
-def test_loopback_first_iterates_match_one_gpu(cfg1, world):
+def test_loopback_first_iterates_match_one_gpu(cfg1, world, transport):
     p, tau, ref = cfg1
-    with Solver(p, dist=loopback(world)) as s:
+    with Solver(p, dist=DistConfig(world=world, transport=transport)) as s:
         got = s.solve(SolverConfig(method=Method.AA_PDHG, m=10, toll=1e-9, max_iters=60,
                                    tau=tau, sigma=tau, reduction="tree"))
     assert got.result.iterations == ref.result.iterations
@@ -79,7 +83,8 @@ def test_loopback_full_solve_config0():
     assert two.result.g_norm < 1e-6
 
 
-def test_loopback_faa_long_rows():
+@pytest.mark.parametrize("transport", ["loopback", "loopback_p2p"])
+def test_loopback_faa_long_rows(transport):
     """Config 2 shape (transport: K rows of 300 nnz on the long-row path),
     FAA m=10 with the BASELINE filter parameters, on 3 shards."""
     p = problems.make_config(2, scale=0.15)
@@ -90,12 +95,13 @@ def test_loopback_faa_long_rows():
         cfg = SolverConfig(method=Method.FAA_PDHG, m=10, toll=1e-9, max_iters=40, tau=tau,
                            sigma=tau, reduction="tree", filter=filt)
         ref = s.solve(cfg)
-    with Solver(p, dist=loopback(3)) as s:
+    with Solver(p, dist=DistConfig(world=3, transport=transport)) as s:
         got = s.solve(cfg)
     traj_close(got, ref, 40, 1e-10)
 
 
-def test_loopback_pdhg_start_iterate_and_lambda():
+@pytest.mark.parametrize("transport", ["loopback", "loopback_p2p"])
+def test_loopback_pdhg_start_iterate_and_lambda(transport):
     p = problems.make_config(0, scale=0.3)
     rng = np.random.default_rng(5)
     u0 = Iterate(rng.uniform(0, 1, p.n()), rng.normal(size=p.k.nrows))
@@ -103,7 +109,7 @@ def test_loopback_pdhg_start_iterate_and_lambda():
                        reduction="tree")
     with Solver(p) as s:
         ref = s.solve(cfg, u0)
-    with Solver(p, dist=loopback(2)) as s:
+    with Solver(p, dist=DistConfig(world=2, transport=transport)) as s:
         got = s.solve(cfg, u0)
     traj_close(got, ref, 30, 1e-10)
     np.testing.assert_allclose(got.result.lambda_, ref.result.lambda_, rtol=1e-9, atol=1e-12)
@@ -126,6 +132,41 @@ def test_nccl_world1_matches_one_gpu(cfg1):
     assert np.linalg.norm(x - xr) <= 1e-10 * np.linalg.norm(xr)
 
 
+def test_p2p_world1_matches_one_gpu(cfg1):
+    """The P2P transport with one rank: NCCL setup, IPC handle export, the
+    producers' peer-store path and the system-scope flag barriers."""
+    p, tau, ref = cfg1
+    nid = nccl_unique_id()
+    with Solver(p, dist=DistConfig(world=1, rank=0, transport="p2p", nccl_id=nid)) as s:
+        cfg = SolverConfig(method=Method.AA_PDHG, m=10, toll=1e-9, max_iters=60, tau=tau,
+                           sigma=tau, reduction="tree")
+        got = s.solve(cfg)
+        again = s.solve(cfg)  # a second solve: the next barrier epoch
+    for out in (got, again):
+        assert out.result.iterations == ref.result.iterations
+        traj_close(out, ref, 60, 1e-10)
+    assert np.array_equal(got.result.u.x, again.result.u.x)
+
+
+def test_loopback_p2p_repeated_solves_and_aa_branch(cfg1):
+    """Peer-memory exchanges across solves (barrier epochs) and through many
+    AA steps (the DOTS / candidate-x exchanges): 4 shards, 300 iterations,
+    against the copy transport."""
+    p, tau, _ = cfg1
+    cfg = SolverConfig(method=Method.AA_PDHG, m=10, toll=1e-12, max_iters=300, tau=tau,
+                       sigma=tau, reduction="tree")
+    with Solver(p, dist=DistConfig(world=4, transport="loopback")) as s:
+        ref = s.solve(cfg)
+    with Solver(p, dist=DistConfig(world=4, transport="loopback_p2p")) as s:
+        a = s.solve(cfg)
+        b = s.solve(cfg)
+    assert ref.result.i > 5  # AA steps taken
+    for out in (a, b):
+        assert np.array_equal(out.trajectory["g_norm"], ref.trajectory["g_norm"])
+        assert np.array_equal(out.result.u.x, ref.result.u.x)
+        assert np.array_equal(out.result.u.y, ref.result.u.y)
+
+
 def test_dist_errors():
     p = problems.toy()
     with pytest.raises(UnsupportedError):
@@ -134,6 +175,11 @@ def test_dist_errors():
         Solver(p, dist=DistConfig(world=2, rank=0, transport="nccl"))  # no id
     with pytest.raises(InputError):
         Solver(p, dist=DistConfig(world=1, transport="smoke-signals"))
+    with pytest.raises(InputError):
+        Solver(p, dist=DistConfig(world=1, rank=0, transport="p2p"))  # no id
+    big = problems.make_config(0, scale=0.2)
+    with pytest.raises(UnsupportedError):
+        Solver(big, dist=DistConfig(world=9, transport="loopback_p2p"))
     q = problems.make_config(0, scale=0.2)
     with Solver(q, dist=loopback(2)) as s:
         with pytest.raises(UnsupportedError):
@@ -180,7 +226,8 @@ def test_loopback_inequality_rows_and_general_bounds():
         np.testing.assert_allclose(got.result.lambda_, ref.result.lambda_, rtol=1e-8, atol=1e-12)
 
 
-def test_loopback_setcover_faa():
+@pytest.mark.parametrize("transport", ["loopback", "loopback_p2p"])
+def test_loopback_setcover_faa(transport):
     """The reference's set-cover generator (all rows inequalities, finite
     upper bounds), FAA with its default filter, on 3 shards."""
     from golden_io import problem
@@ -189,6 +236,6 @@ def test_loopback_setcover_faa():
                        reduction="tree")
     with Solver(p) as s:
         ref = s.solve(cfg)
-    with Solver(p, dist=loopback(3)) as s:
+    with Solver(p, dist=DistConfig(world=3, transport=transport)) as s:
         got = s.solve(cfg)
     traj_close(got, ref, 40, 1e-10)
