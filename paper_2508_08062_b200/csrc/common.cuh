@@ -112,6 +112,14 @@ struct DevParams {
   double* scal_dst[kMaxPeers];
   double* dots_dst[kMaxPeers];
   uint64_t p2p_epoch;  // barrier sequence base of this solve (high 32 bits)
+  // P2P transports with fused signals: K1 waits for the YG arrivals and its
+  // last CTA arrives at XG; K2 waits for XG and its last CTA arrives at YG
+  // (ŷ and the shard totals); the control waits for YG. Arrival of shard r
+  // at slot s: flag_peer[q][s * kMaxPeers + r] = (epoch << 32) + passes.
+  int32_t p2p_fused, p2p_world, p2p_rank;
+  int32_t p2p_sys;  // peers on other GPUs: system-scope fences before the arrivals
+  unsigned long long* flag_peer[kMaxPeers];
+  unsigned long long* flag_own;
   int64_t Nglob;  // n + m of the whole LP (FAA's QR row-count test)
 };
 
@@ -137,8 +145,8 @@ struct DevState {
   uint64_t plain_iters;            // iterations k_plain_loop completed
   uint64_t plain_ns;               // k_plain_loop time (globaltimer, launch start -> stop)
   uint32_t ticket;                 // last-CTA election in k_primal_side
+  uint32_t ticket1;                // last-CTA election in k_dual_side (P2P arrival)
   int32_t prev_plain;              // the previous step was T(u_{k-1}) (not an AA candidate)
-  int32_t pad_pp;
   int32_t batch_left;              // iterations left in this graph launch
   uint64_t p2p_seq[8];             // P2P flag barriers passed, per exchanged buffer
 };
@@ -180,6 +188,7 @@ struct IterBufs {
   int32_t nu1;        // K1 CTAs (rows of part1)
   int32_t fused_ctrl; // TREE: k_primal_side's last CTA runs the control (1) or,
                       // sharded, writes this shard's 8 totals to P->scal_dst (2)
+  int32_t p2p_sys;    // = DevParams::p2p_sys (read before the params are staged)
   const double* c;
   const double* q;
   const double* l;

@@ -1287,19 +1287,15 @@ ShardBufs Problem::shard_bufs() const {
 // P2P transports: every shard's exchange buffers, indexed by rank (this
 // shard's own entry included). The producers then write this shard's chunk
 // into all of them and the exchanges become flag barriers (k_p2p_barrier).
-void Problem::sh_set_peers(const std::vector<ShardBufs>& peers) {
+void Problem::sh_set_peers(const std::vector<ShardBufs>& peers, bool remote) {
   if (peers.size() > size_t(kMaxPeers))
     throw StatusError(AAPDHG_ERR_UNSUPPORTED, "p2p: more than 8 shards");
   peers_ = peers;
+  peers_remote_ = remote;
 }
 
 void Problem::sh_p2p_barrier(int slot, int phase) {
-  P2pFlags F{};
-  for (size_t q = 0; q < peers_.size(); ++q) F.peer[q] = peers_[q].flags;
-  F.own = p2p_flags_.as<unsigned long long>();
-  F.world = int(peers_.size());
-  F.rank = shard_rank_;
-  k_p2p_barrier<<<1, 32, 0, stream_>>>(F, sh_su_->P, sh_su_->S, slot, phase);
+  k_p2p_barrier<<<1, 32, 0, stream_>>>(sh_su_->P, sh_su_->S, slot, phase);
   AAPDHG_CUDA(cudaGetLastError());
   ++sh_launches_;
 }
@@ -1372,6 +1368,12 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
     P.dots_dst[q] = dst[q].dots + int64_t(shard_rank_) * dot_stride_;
   }
   P.p2p_epoch = ++p2p_epoch_;
+  P.p2p_fused = peers_.empty() ? 0 : 1;
+  P.p2p_world = int32_t(peers_.size());
+  P.p2p_rank = shard_rank_;
+  for (size_t q = 0; q < peers_.size(); ++q) P.flag_peer[q] = peers_[q].flags;
+  P.flag_own = p2p_flags_.as<unsigned long long>();
+  P.p2p_sys = peers_remote_ && peers_.size() > 1 ? 1 : 0;
   P.store_T = 1;
 
   DevState S0 = DevState{};
@@ -1387,6 +1389,7 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   su.B = iter_bufs();
   su.B.nu1 = sh_k1m().grid();
   su.B.fused_ctrl = 2;  // K2's last CTA writes this shard's totals (P.scal_dst)
+  su.B.p2p_sys = P.p2p_sys;
   su.B.rinit1 = ktb_.nb() > 1 ? ktb_.partial.as<double>() : nullptr;
   su.B.rinit2 = kb_.nb() > 1 ? kb_.partial.as<double>() : nullptr;
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),

@@ -79,7 +79,8 @@ class Problem {
   // x-part of an iterate -> this shard's chunk of xg (peers: of every P2P peer's)
   void sh_stage_x(int role, int mode, bool peers = false);
   void sh_stage_y(int role, int mode, bool peers = false);  // y-part -> yg
-  void sh_set_peers(const std::vector<ShardBufs>& peers);    // P2P transports
+  // P2P transports; remote: the peers are other processes' GPUs (IPC)
+  void sh_set_peers(const std::vector<ShardBufs>& peers, bool remote);
   void sh_p2p_barrier(int slot, int phase);                  // k_p2p_barrier
   void sh_init_kx();                    // K x of the start iterate (after AG of xg)
   void sh_k1();                         // K'y + xhat (+ own chunk of xg)
@@ -205,6 +206,7 @@ class Problem {
   int64_t maxc_ = 0, maxr_ = 0, dot_stride_ = 0;
   DevBuf xg_, yg_, lg_, scal_all_, dots_all_, p2p_flags_;
   std::vector<ShardBufs> peers_;  // P2P: every shard's exchange buffers (by rank)
+  bool peers_remote_ = false;
   uint64_t p2p_epoch_ = 0;        // solves begun (barrier sequence base)
   SolveSetup* sh_su_ = nullptr;
   DevParams sh_params_{};

@@ -361,6 +361,46 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
   return lane == 0 ? row : -1;
 }
 
+
+// ---------------------------------------------------------------------------
+// peer-memory exchange flags (sharded solve, P2P transports; shard.cuh)
+// ---------------------------------------------------------------------------
+// Slots of the exchanged buffers (ShardGroup::Buf, shard.h).
+enum { P2P_XG = 0, P2P_YG = 1, P2P_SCAL = 3, P2P_DOTS = 4, P2P_XG2 = 5 };
+
+// This shard arrives at exchange `slot` on every shard: one more pass, a
+// system-scope fence (cumulative over the stores this thread has observed —
+// the caller's CTA barrier / last-CTA ticket brings every store of the
+// kernel in), then the sequence number into every shard's flag array.
+// Thread 0 only.
+__device__ __forceinline__ void p2p_arrive(const DevParams* P, DevState* S, int slot) {
+  const unsigned long long seq = (P->p2p_epoch << 32) | (++S->p2p_seq[slot]);
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (int q = 0; q < P->p2p_world; ++q)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P->flag_peer[q] + slot * kMaxPeers +
+                                                             P->p2p_rank),
+                 "l"(seq)
+                 : "memory");
+}
+
+// Waits until every shard has arrived at `slot` as often as this one (its own
+// arrival came earlier in the stream). A shard that never arrives (crashed
+// rank) traps after 30 s instead of hanging the GPU. Thread 0 only; the
+// caller's CTA barrier then orders the CTA's reads after the acquire.
+__device__ __forceinline__ void p2p_wait(const DevParams* P, const DevState* S, int slot) {
+  const unsigned long long seq = (P->p2p_epoch << 32) | S->p2p_seq[slot];
+  const uint64_t t0 = globaltimer_ns();
+  for (int r = 0; r < P->p2p_world; ++r) {
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
+                   : "=l"(v) : "l"(P->flag_own + slot * kMaxPeers + r) : "memory");
+      if (v >= seq) break;
+      if (globaltimer_ns() - t0 > 30000000000ull) asm volatile("trap;");
+    }
+  }
+}
+
 template <bool SERIAL>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_spmv(CsrDev A, VecRef xr, RowsumArgs o, const DevState* S) {
@@ -634,6 +674,8 @@ __device__ __noinline__ bool tail_control(const IterBufs& B, DevState* S, TailSm
 #pragma unroll
         for (int t = 0; t < 8; ++t) ts.pr.scal_dst[q][t] = own[t];
       S->ticket = 0;
+      // P2P: publish yhat (every CTA's stores) and the totals
+      if (ts.pr.p2p_fused) p2p_arrive(&ts.pr, S, P2P_YG);
     }
     return true;
   }
@@ -692,6 +734,7 @@ __device__ __forceinline__ void fused_control_tail(const IterBufs& B, DevState* 
   __shared__ int last;
   if (blockIdx.x == 0) tail_fold_k1(B, S, red);
   if (threadIdx.x == 0) {
+    if (B.p2p_sys) __threadfence_system();  // P2P across GPUs: this CTA's peer stores first
     unsigned prev;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
                  : "=r"(prev) : "l"(&S->ticket) : "memory");
@@ -796,7 +839,29 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   }
 #endif
   __shared__ double red[P1_COUNT * kWarps];
+  const bool fused = !SERIAL && P->p2p_fused;
+  if (fused) {  // y of u_k: every shard's K2 (or AA branch) stored its chunk here
+    if (threadIdx.x == 0) p2p_wait(P, S, P2P_YG);
+    __syncthreads();
+  }
   dual_side_rows<SERIAL, PUSH, VAR>(KT, B, P, S, int(blockIdx.x), int(gridDim.x), red);
+  if (fused) {  // the last CTA publishes xhat (every CTA stored its chunk to every shard)
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // peers on other GPUs: this CTA's remote stores drain before the ticket
+      // (in-process peers: the ticket's gpu-scope release covers them)
+      if (P->p2p_sys) __threadfence_system();
+      unsigned prev;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                   : "=r"(prev) : "l"(&S->ticket1) : "memory");
+      last = prev == gridDim.x - 1;
+      if (last) {
+        S->ticket1 = 0;
+        p2p_arrive(P, S, P2P_XG);
+      }
+    }
+  }
 }
 
 // K2 on K, s = (K xhat)_i:
@@ -855,6 +920,10 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   }
   __shared__ double red[P2_COUNT * kWarps];
   double acc[P2_COUNT] = {0.0, 0.0, 0.0};
+  if (!SERIAL && P->p2p_fused) {  // xhat: every shard's K1 stored its chunk here
+    if (threadIdx.x == 0) p2p_wait(P, S, P2P_XG);
+    __syncthreads();
+  }
   primal_side_rows<SERIAL, PUSH>(K, B, P, S, int(blockIdx.x), acc);
   if (!SERIAL) {
     __shared__ __align__(16) TailSmem ts;

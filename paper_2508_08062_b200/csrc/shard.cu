@@ -238,7 +238,7 @@ void ShardGroup::open_peers() {
   std::vector<ShardBufs> peers;
   if (!multi_) {
     for (auto& s : shards_) peers.push_back(s->shard_bufs());
-    each([&](Problem& s) { s.sh_set_peers(peers); });
+    each([&](Problem& s) { s.sh_set_peers(peers, false); });
     return;
   }
   const ShardBufs mine = shards_[0]->shard_bufs();
@@ -280,7 +280,7 @@ void ShardGroup::open_peers() {
     sb.lg = nullptr;  // (not exchanged over peer memory)
     peers.push_back(sb);
   }
-  shards_[0]->sh_set_peers(peers);
+  shards_[0]->sh_set_peers(peers, true);
 }
 
 // The in-loop exchanges: P2P transports only synchronise (the producers
@@ -445,12 +445,17 @@ void ShardGroup::solve(const aapdhg_solve_params* prm, const double* x0, const d
   // (P2P transports: the producers store into every shard's buffer and each
   // exchange is a flag barrier; the exchange points are where every shard
   // has finished reading the buffer's previous contents — DESIGN.md §8)
+  // P2P: the plain iteration has no exchange launches at all — K1 waits for
+  // the YG arrivals and arrives at XG, K2 waits for XG and arrives at YG (its
+  // yhat and totals), the control waits for YG (fused signals, pipeline.cuh).
+  // The AA branch keeps barrier kernels and ends with a YG arrival, so the
+  // next K1 also waits for every shard's candidate (and its recache reads).
   auto core = [&] {
-    exchange(YG);
+    if (!p2p_) allgather(YG);
     each([&](Problem& s) { s.sh_k1(); });
-    exchange(XG);
+    if (!p2p_) allgather(XG);
     each([&](Problem& s) { s.sh_k2_totals(); });
-    exchange(SCAL);
+    if (!p2p_) allgather(SCAL);
     each([&](Problem& s) { s.sh_control(world_); });
   };
   auto aa_branch = [&] {
@@ -459,11 +464,15 @@ void ShardGroup::solve(const aapdhg_solve_params* prm, const double* x0, const d
     each([&](Problem& s) { s.sh_aa_solve_mix(world_); });
     exchange(XG2);
     each([&](Problem& s) { s.sh_aa_recache_commit(); });
+    if (p2p_) each([&](Problem& s) { s.sh_p2p_barrier(int(YG), 1); });
   };
   // y of the start iterate; afterwards K2 (yhat) or the accepted candidate
   // writes each shard's chunk
   each([&](Problem& s) { s.sh_stage_y(-1, 0); });
-  if (p2p_) allgather(YG);  // (the loop's first exchange(YG) only synchronises)
+  if (p2p_) {
+    allgather(YG);  // the start iterate's y, then the first YG arrival
+    exchange(YG);
+  }
   const char* ge = std::getenv("AAPDHG_SHARD_GRAPH");
   const int mode = ge && *ge ? std::atoi(ge) : 2;  // 2 WHILE/IF, 1 per iteration, 0 eager
   cudaGraphExec_t exec = nullptr;

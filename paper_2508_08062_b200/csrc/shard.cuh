@@ -36,6 +36,8 @@ __global__ void __launch_bounds__(128)
     k_control_dist(const double* __restrict__ all, int nranks, const DevParams* __restrict__ P,
                    DevState* S) {
   if (S->done) return;
+  if (P->p2p_fused && threadIdx.x == 0) p2p_wait(P, S, P2P_YG);  // every shard's totals
+  __syncthreads();
   __shared__ DevState sm;
   __shared__ DevParams sp;
   params_load(&sp, P);
@@ -72,50 +74,18 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
-// Peer-memory (P2P) exchange barrier. The producers already stored this
-// shard's chunk into every shard's buffer (P->*_dst); this publishes that and
-// waits until every shard has published the same exchange. Shard r's
-// arrival at barrier `slot` is flags[slot * kMaxPeers + r] = seq in every
-// shard's flag array, seq = (solve epoch << 32) + passes of this barrier
-// (identical on every shard: the replicated control takes the same branches).
-// The system-scope release orders this shard's earlier peer stores (kernels
-// before it in the stream: cumulativity) before the flag; the waiter's
-// acquire orders the flag before the consumer kernels after it.
-// phase 1: arrive, 2: wait, 3: both (one shard per process). In-process
-// loopback shards arrive all first, then wait (no kernel spins on a shard
-// that has not been launched).
-struct P2pFlags {
-  unsigned long long* peer[kMaxPeers];  // every shard's flag array
-  unsigned long long* own;
-  int32_t world, rank;
-};
-
-__global__ void k_p2p_barrier(P2pFlags F, const DevParams* __restrict__ P, DevState* S, int slot,
-                              int phase) {
+// Peer-memory (P2P) exchange barrier, for the exchanges that are not fused
+// into K1 / K2 / the control (the AA branch, the start iterate). The
+// producers already stored this shard's chunk into every shard's buffer
+// (P->*_dst); this publishes that and waits until every shard has published
+// the same exchange (p2p_arrive / p2p_wait, pipeline.cuh). phase 1: arrive,
+// 2: wait, 3: both (one shard per process). In-process loopback shards
+// arrive all first, then wait (no kernel spins on a shard that has not been
+// launched).
+__global__ void k_p2p_barrier(const DevParams* __restrict__ P, DevState* S, int slot, int phase) {
   if (threadIdx.x != 0) return;
-  if (phase & 1) {
-    const unsigned long long seq = (P->p2p_epoch << 32) | (++S->p2p_seq[slot]);
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
-    for (int q = 0; q < F.world; ++q)
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(F.peer[q] + slot * kMaxPeers + F.rank),
-                   "l"(seq)
-                   : "memory");
-  }
-  if (phase & 2) {
-    const unsigned long long seq = (P->p2p_epoch << 32) | S->p2p_seq[slot];
-    const uint64_t t0 = globaltimer_ns();
-    for (int r = 0; r < F.world; ++r) {
-      unsigned long long v;
-      for (;;) {
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(F.own + slot * kMaxPeers + r)
-                     : "memory");
-        if (v >= seq) break;
-        // a peer that never arrives (crashed rank): fail the launch instead
-        // of hanging the GPU
-        if (globaltimer_ns() - t0 > 30000000000ull) asm volatile("trap;");
-      }
-    }
-  }
+  if (phase & 1) p2p_arrive(P, S, slot);
+  if (phase & 2) p2p_wait(P, S, slot);
 }
 
 // lambda = P_Lambda(c - K'y) of the final iterate from the K'y kept by K1
