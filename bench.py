@@ -225,11 +225,26 @@ def run_ours(args, rank, world, local_rank):
             transport = "p2p" if int(flag.item()) else "nccl"
         args.transport = transport
 
-        def dcfg():  # a fresh NCCL id per communicator (ids are single-use)
+        def dcfg(tr):  # a fresh NCCL id per communicator (ids are single-use)
             box = [nccl_unique_id() if rank == 0 else None]
             tdist.broadcast_object_list(box, src=0)
-            return DistConfig(world=world, rank=rank, transport=transport, nccl_id=box[0])
-        s = Solver(p, device=dev, dist=dcfg())
+            return DistConfig(world=world, rank=rank, transport=tr, nccl_id=box[0])
+        s = Solver(p, device=dev, dist=dcfg(transport))
+        if transport == "p2p" and world > 1:
+            # self-check: the peer-memory exchanges must reproduce the NCCL
+            # all-gathers bit for bit (same kernels, same data) over 60
+            # iterations with AA steps; otherwise run on NCCL
+            chk = solver_config(tau=0.0775, max_iters=60)
+            a = s.solve(chk).trajectory["g_norm"]
+            with Solver(p, device=dev, dist=dcfg("nccl")) as s2:
+                b = s2.solve(chk).trajectory["g_norm"]
+            same = torch.tensor([1 if np.array_equal(a, b) else 0], dtype=torch.int32,
+                                device=f"cuda:{dev}" if tdist.get_backend() == "nccl" else "cpu")
+            tdist.all_reduce(same, op=tdist.ReduceOp.MIN)
+            if not int(same.item()):
+                s.close()
+                transport = args.transport = "nccl (p2p self-check failed)"
+                s = Solver(p, device=dev, dist=dcfg("nccl"))
     else:
         s = Solver(p, device=dev)
     lib = s.lib
@@ -320,7 +335,7 @@ def run_ours(args, rank, world, local_rank):
                 "data": "synthetic (seeded planted-optimum generator, SURVEY.md 8(d))",
                 "config": dict(workload_config(p),
                                parallelism=f"shard{world} (row/column blocks, "
-                                           f"{'peer-memory stores + flag barriers' if args.transport == 'p2p' else 'NCCL all-gather'})"
+                                           f"{'peer-memory stores + flag barriers' if args.transport == 'p2p' else args.transport})"
                                if dist else "single"),
                 "iterations_timed": iters, "aa_steps_timed": out.result.i,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt,
