@@ -139,3 +139,145 @@ def test_gloo_world2_exchange_schedule_matches_oracle(tmp_path):
                                                max_iters=iters, tau=tau, sigma=tau))
     want = ref.trajectory["g_norm"][:iters]
     np.testing.assert_allclose(got, want, rtol=1e-12)
+
+
+# ---- the P2P exchange protocol (shard.cu / pipeline.cuh p2p_arrive, p2p_wait) ----
+class _P2pModel:
+    """Ranks as threads running the exact order of the P2P sharded iteration:
+    producers store their chunk into every rank's buffer as soon as they run,
+    arrivals bump a per-slot sequence number into every rank's flag array, a
+    wait spins until every rank's flag has reached this rank's own count.
+    Every read checks the version tag of each chunk it consumes: a producer
+    that overwrote a buffer before its reader was done (a misplaced arrival
+    or wait) shows up as a newer tag."""
+
+    XG, YG, SCAL, DOTS, XG2 = 0, 1, 3, 4, 5
+
+    def __init__(self, world, iters, aa_every, seed):
+        import random
+        import threading
+        self.world, self.iters, self.aa_every = world, iters, aa_every
+        self.xg = [[None] * world for _ in range(world)]
+        self.yg = [[("y", 0)] * world for _ in range(world)]  # start iterate, all-gathered
+        self.scal = [[None] * world for _ in range(world)]
+        self.dots = [[None] * world for _ in range(world)]
+        self.flags = [[[0] * world for _ in range(8)] for _ in range(world)]
+        self.seq = [[0] * 8 for _ in range(world)]
+        self.rng = [random.Random(seed * 131 + r) for r in range(world)]
+        self.errors = []
+        self.lock = threading.Lock()
+
+    def jitter(self, r):
+        import time
+        if self.rng[r].random() < 0.5:
+            time.sleep(self.rng[r].random() * 2e-4)
+
+    def arrive(self, r, slot):
+        self.seq[r][slot] += 1
+        for q in range(self.world):
+            self.jitter(r)
+            self.flags[q][slot][r] = self.seq[r][slot]
+
+    def wait(self, r, slot):
+        import time
+        t0 = time.monotonic()
+        while any(self.flags[r][slot][p] < self.seq[r][slot] for p in range(self.world)):
+            time.sleep(1e-5)
+            if time.monotonic() - t0 > 20:
+                raise RuntimeError(f"rank {r} deadlocked at slot {slot}")
+
+    def store(self, r, buf, tag):
+        for q in range(self.world):
+            self.jitter(r)
+            buf[q][r] = tag
+
+    def read(self, r, buf, tag, what):
+        for p in range(self.world):
+            self.jitter(r)
+            if buf[r][p] != tag:
+                with self.lock:
+                    self.errors.append((r, what, p, buf[r][p], tag))
+
+    def rank(self, r):
+        try:
+            self.arrive(r, self.YG)  # the start iterate's exchange(YG)
+            self.wait(r, self.YG)
+            for k in range(self.iters):
+                self.wait(r, self.YG)                     # K1: y of u_k
+                self.read(r, self.yg, ("y", k), "K1 y")
+                self.store(r, self.xg, ("x", k))          # xhat_k
+                self.arrive(r, self.XG)                   # K1's last CTA
+                self.wait(r, self.XG)                     # K2
+                self.read(r, self.xg, ("x", k), "K2 xhat")
+                self.store(r, self.yg, ("y", k + 1))      # yhat (y of u_{k+1} if plain)
+                self.store(r, self.scal, k)
+                self.arrive(r, self.YG)                   # K2's last CTA
+                self.wait(r, self.YG)                     # control
+                self.read(r, self.scal, k, "control totals")
+                if k % self.aa_every == self.aa_every - 1:  # replicated decision: AA branch
+                    self.store(r, self.dots, k)
+                    self.arrive(r, self.DOTS)
+                    self.wait(r, self.DOTS)
+                    self.read(r, self.dots, k, "aa_solve dots")
+                    self.store(r, self.xg, ("c", k))      # candidate x
+                    self.store(r, self.yg, ("y", k + 1))  # candidate y
+                    self.arrive(r, self.XG2)
+                    self.wait(r, self.XG2)
+                    self.read(r, self.xg, ("c", k), "recache candidate")
+                    self.arrive(r, self.YG)               # end of the AA branch
+        except Exception as e:  # noqa: BLE001
+            with self.lock:
+                self.errors.append((r, repr(e)))
+
+    def run(self):
+        import threading
+        ts = [threading.Thread(target=self.rank, args=(r,)) for r in range(self.world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return self.errors
+
+
+@pytest.mark.parametrize("world,seed", [(2, 1), (3, 2), (4, 3), (8, 4)])
+def test_p2p_exchange_protocol_model(world, seed):
+    """The P2P transport's arrival / wait placement never lets
+    a rank overwrite a buffer another rank still reads, and never deadlocks,
+    under random interleavings of world ranks over plain and AA iterations."""
+    errors = _P2pModel(world, iters=24, aa_every=4, seed=seed).run()
+    assert not errors, errors[:5]
+
+
+def test_p2p_protocol_model_catches_a_missing_wait():
+    """The model is sharp: dropping K2's wait for the XG arrivals lets a rank
+    read xhat chunks its peers have not stored yet."""
+    class NoXgWait(_P2pModel):
+        def wait(self, r, slot):
+            if slot == self.XG:
+                return
+            super().wait(r, slot)
+    found = any(NoXgWait(4, iters=24, aa_every=4, seed=s).run() for s in range(6))
+    assert found
+
+
+def test_p2p_protocol_model_catches_a_missing_aa_arrival():
+    """... and dropping the AA branch's closing YG arrival lets a fast rank's
+    next K1 store xhat into a peer's xg while that peer's recache still reads
+    the candidate there."""
+    class NoAaArrival(_P2pModel):
+        def __init__(self, *a, **k):
+            super().__init__(*a, **k)
+            self.in_aa = [False] * self.world
+
+        def read(self, r, buf, tag, what):
+            super().read(r, buf, tag, what)
+            if what == "recache candidate":
+                self.in_aa[r] = True
+
+        def arrive(self, r, slot):
+            if slot == self.YG and self.in_aa[r]:
+                self.in_aa[r] = False
+                return
+            super().arrive(r, slot)
+    found = any(NoAaArrival(4, iters=24, aa_every=4, seed=s).run() for s in range(6))
+    assert found
