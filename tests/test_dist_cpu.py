@@ -7,7 +7,10 @@
   of y, K'y on the column block, all-gather of xhat, K xhat on the row block,
   all-gather of the scalar partials summed in rank order — checked against the
   oracle's PDHG trajectory. This pins the decomposition and the relabelling;
-  the kernels themselves are covered on the GPU (test_gpu_dist.py)."""
+  the kernels themselves are covered on the GPU (test_gpu_dist.py);
+* a threaded model of the P2P transport's exchange protocol (remote stores,
+  per-slot arrival sequences, waits) under random interleavings, with
+  negative controls showing it catches a misplaced wait or arrival."""
 import os
 import socket
 
