@@ -243,7 +243,8 @@ def run_ours(args, rank, world, local_rank):
             tdist.all_reduce(same, op=tdist.ReduceOp.MIN)
             if not int(same.item()):
                 s.close()
-                transport = args.transport = "nccl (p2p self-check failed)"
+                transport = "nccl"
+                args.transport = "nccl (p2p self-check failed)"
                 s = Solver(p, device=dev, dist=dcfg("nccl"))
     else:
         s = Solver(p, device=dev)
@@ -304,7 +305,7 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         tdist.barrier()
     t0 = time.perf_counter()
-    s2 = Solver(p, device=dev, dist=dcfg()) if dist else Solver(p, device=dev)
+    s2 = Solver(p, device=dev, dist=dcfg(transport)) if dist else Solver(p, device=dev)
     out2 = s2.solve(solver_config(tau=tau, max_iters=args.steps))  # x, y, lambda, records on host
     e2e_s = time.perf_counter() - t0
     s2.close()  # (freeing device memory is not part of the measured path)
