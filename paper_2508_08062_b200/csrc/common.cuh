@@ -68,6 +68,9 @@ struct CsrDev {
   int32_t nhuge = 0;  // TREE: the first nhuge long rows (>= kHugeRow) get a CTA each
   int32_t nblk_short = 0, nblk_long = 0;  // nblk_long = nhuge + ceil((nlong - nhuge) / 8)
   int32_t sf = 1;  // lanes per row in the slices (1 = CSR-ordered row sums)
+  // more slices than one wave of warps: slice s belongs to CTA s % nblk_short
+  // (one wave of CTAs), whose warps loop over theirs (row_sum `rep`)
+  int32_t interleave = 0;
   int32_t grid() const { return nblk_short + nblk_long; }
 };
 

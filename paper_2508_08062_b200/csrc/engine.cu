@@ -142,6 +142,7 @@ void Problem::build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& o
   const int nb = int((int64_t(ncols) + per - 1) / per);
   if (nb < 2) return;
   const int64_t W = (int64_t(ncols) + nb - 1) / nb;
+  building_blocks_ = true;
   for (int b = 0; b < nb; ++b) {
     out.store.emplace_back(new CsrStore());
     int64_t nnz_b = 0;
@@ -151,6 +152,7 @@ void Problem::build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& o
     finish_csr(nrows, ncols, nnz_b, *out.store.back(), ser, tree);
     out.blk.push_back(tree);
   }
+  building_blocks_ = false;
   out.partial.reserve(sizeof(double) * size_t(nrows));
 }
 
@@ -562,6 +564,18 @@ static void launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
 //   commit role rotation and loop bookkeeping
 // Eagerly the aa kernels are predicated on device flags; under graph replay
 // they sit in an IF node the control sets, inside a WHILE node commit drives.
+// K1 / K2 for a layout: the MULTI instantiation only for interleaved ones
+template <bool SER, bool PUSH>
+void launch_k1(const CsrDev& A, const IterBufs& B, const DevParams* P, DevState* S,
+               cudaStream_t s) {
+  if (A.interleave) k_dual_side<SER, PUSH, 0, true><<<A.grid(), kThreads, 0, s>>>(A, B, P, S);
+  else k_dual_side<SER, PUSH><<<A.grid(), kThreads, 0, s>>>(A, B, P, S);
+}
+template <bool SER, bool PUSH>
+auto k2_kernel(const CsrDev& A) {
+  return A.interleave ? k_primal_side<SER, PUSH, 0, true> : k_primal_side<SER, PUSH>;
+}
+
 int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   int nodes = 0;
   const bool ser = su.serial, push = su.push;
@@ -590,11 +604,11 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
     nodes += launch_blocked_passes(s, ktb_, VecRef{nullptr, su.B.upool, U_CUR, N_, n_}, su.S);
   // K'y: products of K' with y = u_cur[n:], then the fused dual-side rows
   if (n_ > 0) {
-    if (ser && push) LAUNCH("k_dual_side", k_dual_side<true, true><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
-    else if (ser) LAUNCH("k_dual_side", k_dual_side<true, false><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
+    if (ser && push) LAUNCH("k_dual_side", (launch_k1<true, true>(K1m, su.B, su.P, su.S, s)));
+    else if (ser) LAUNCH("k_dual_side", (launch_k1<true, false>(K1m, su.B, su.P, su.S, s)));
     else if (push && env_int("AAPDHG_K1VAR", 0) == 2) LAUNCH("k_dual_side", k_dual_side<false, true, 2><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
-    else if (push) LAUNCH("k_dual_side", k_dual_side<false, true><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
-    else LAUNCH("k_dual_side", k_dual_side<false, false><<<K1m.grid(), kThreads, 0, s>>>(K1m, su.B, su.P, su.S));
+    else if (push) LAUNCH("k_dual_side", (launch_k1<false, true>(K1m, su.B, su.P, su.S, s)));
+    else LAUNCH("k_dual_side", (launch_k1<false, false>(K1m, su.B, su.P, su.S, s)));
   }
   if (ser) {  // fork: the x-side serial chains run beside K2 on the side stream
     AAPDHG_CUDA(cudaEventRecord(ev_fork_, s));
@@ -614,10 +628,10 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   if (m_ > 0) {
     const bool pdl = pdl_ && n_ > 0;
     const dim3 g(K2m.grid());
-    auto kern = ser ? (push ? k_primal_side<true, true> : k_primal_side<true, false>)
+    auto kern = ser ? (push ? k2_kernel<true, true>(K2m) : k2_kernel<true, false>(K2m))
                     : (push ? (env_int("AAPDHG_K2VAR", 0) == 2 ? k_primal_side<false, true, 2>
-                                                                : k_primal_side<false, true>)
-                            : k_primal_side<false, false>);
+                                                                : k2_kernel<false, true>(K2m))
+                            : k2_kernel<false, false>(K2m));
     LAUNCH("k_primal_side", launch_ex(kern, g, dim3(kThreads), 0, s, pdl, K2m, su.B, su.P, su.S));
   }
   if (ser) {  // join, then the y-side chains and the control
@@ -1132,10 +1146,10 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
   const DevParams* Pd = dparams_.as<DevParams>();
   DevState* Sd = dstate_.as<DevState>();
   if (n_) {
-    k_dual_side<true, false><<<KTs_.grid(), kThreads, 0, stream_>>>(KTs_, B, Pd, Sd);
+    launch_k1<true, false>(KTs_, B, Pd, Sd, stream_);
   }
   if (m_) {
-    k_primal_side<true, false><<<Ks_.grid(), kThreads, 0, stream_>>>(Ks_, B, Pd, Sd);
+    k2_kernel<true, false>(Ks_)<<<Ks_.grid(), kThreads, 0, stream_>>>(Ks_, B, Pd, Sd);
   }
   AAPDHG_CUDA(cudaGetLastError());
   const double* hat = upool_.as<double>() + 2 * N_;
@@ -1454,9 +1468,9 @@ void Problem::sh_k1() {
   if (ktb_.nb() > 1) sh_launches_ += launch_blocked_passes(stream_, ktb_, vref(yg_.as<double>()), su.S);
   const CsrDev& A = sh_k1m();
   if (su.push)
-    k_dual_side<false, true><<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
+    launch_k1<false, true>(A, su.B, su.P, su.S, stream_);
   else
-    k_dual_side<false, false><<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
+    launch_k1<false, false>(A, su.B, su.P, su.S, stream_);
   AAPDHG_CUDA(cudaGetLastError());
   ++sh_launches_;
 }
@@ -1466,9 +1480,9 @@ void Problem::sh_k2_totals() {
   if (kb_.nb() > 1) sh_launches_ += launch_blocked_passes(stream_, kb_, vref(xg_.as<double>()), su.S);
   const CsrDev& A = sh_k2m();
   if (su.push)
-    k_primal_side<false, true><<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
+    k2_kernel<false, true>(A)<<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
   else
-    k_primal_side<false, false><<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
+    k2_kernel<false, false>(A)<<<A.grid(), kThreads, 0, stream_>>>(A, su.B, su.P, su.S);
   AAPDHG_CUDA(cudaGetLastError());
   ++sh_launches_;  // (its last CTA writes this shard's totals: fused_ctrl = 2)
 }

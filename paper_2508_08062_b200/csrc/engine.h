@@ -230,6 +230,8 @@ class Problem {
                             const DevState* S);
   size_t sell_bytes_ = 0;
   bool sigma_global_ = false;  // device_sell: sort all short rows (ragged lengths)
+  double short_mean_ = 0.0;    // device_sell: mean length of the short rows
+  bool building_blocks_ = false;  // device_sell: an L2 column block (never interleaved)
   DevBuf c_, q_, l_, u_;
   double nrm_q_[2] = {0, 0}, nrm_c_[2] = {0, 0};  // [serial, tree]
 

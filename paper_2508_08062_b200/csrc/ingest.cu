@@ -275,6 +275,7 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
   const double var = nshort == 0 ? 0.0 : double(short_sq_sum) / double(nshort) - mean * mean;
   const bool ragged = mean > 0.0 && std::sqrt(std::max(var, 0.0)) > 0.5 * mean;
   sigma_global_ = ragged;
+  short_mean_ = mean;
   device_sell(shorts, nshort, len, 1, st, st.sell[0], ser);
   const int64_t slots = int64_t(num_sms_) * kSpmvBlocksPerSM * kWarps;
   int sf = 1;
@@ -356,8 +357,22 @@ void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* l
   out.sv = ss.sv.as<double>();
   out.sf = sf;
   const int wave = num_sms_ * kSpmvBlocksPerSM;
-  out.nblk_short = int64_t(nslices) <= int64_t(wave) * kWarps ? std::min(nslices, wave)
-                                                              : (nslices + kWarps - 1) / kWarps;
+  const int64_t one_wave = int64_t(wave) * kWarps;
+  out.interleave = 0;
+  if (int64_t(nslices) <= one_wave) {
+    out.nblk_short = std::min(nslices, wave);
+  } else if (int64_t(nslices) >= 2 * one_wave &&
+             env_int("AAPDHG_INTERLEAVE", short_mean_ <= 4.0 && !building_blocks_ ? 1 : 0) != 0) {
+    // very short rows (config 2's K': 4M rows of 2): a slice is a few loads
+    // per lane, so CTA turnover dominates a CTA-per-8-slices grid. One wave
+    // of CTAs instead, every warp looping over slices w, w + wave*8, ...
+    // (K1 91 -> 72 us on config 2; longer rows lose: config 3 596 -> 671 us,
+    // config 4 1.4 -> 3.7 ms, profiles/r01/interleave.txt)
+    out.nblk_short = wave;
+    out.interleave = 1;
+  } else {
+    out.nblk_short = (nslices + kWarps - 1) / kWarps;
+  }
 }
 
 // K' as CSR, entries of each row in ascending original row: a stable radix

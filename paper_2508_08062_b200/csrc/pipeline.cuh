@@ -256,17 +256,25 @@ __device__ __forceinline__ double ldx(const double* p) {
   else return __ldg(p);
 }
 
+// rep: the warp's rep-th slice of an interleaved layout (returns -2 when the
+// warp has no more); otherwise only rep 0 exists.
 template <bool SERIAL, int UNROLL = kUnroll, bool COH = false, class Pre = NoPre>
 __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, double& s,
-                                       Pre pre = Pre{}, int bid = -1) {
+                                       Pre pre = Pre{}, int bid = -1, int rep = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (bid < 0) bid = int(blockIdx.x);
   s = 0.0;
+  if (rep > 0 && (!A.interleave || bid < A.nblk_long)) return -2;
   if (bid >= A.nblk_long) {
-    // CTA b owns slices [b * ns / nblk, (b + 1) * ns / nblk): <= kWarps each
     const int b = bid - A.nblk_long;
-    const int sl = int(int64_t(b) * A.nslices / A.nblk_short) + warp;
-    if (sl >= int(int64_t(b + 1) * A.nslices / A.nblk_short)) return -1;
+    int sl;
+    if (A.interleave) {  // slices b + nblk * (warp + kWarps * rep)
+      sl = int(b + int64_t(A.nblk_short) * (warp + kWarps * rep));
+      if (sl >= A.nslices) return -2;
+    } else {  // CTA b owns slices [b * ns / nblk, (b + 1) * ns / nblk): <= kWarps each
+      sl = int(int64_t(b) * A.nslices / A.nblk_short) + warp;
+      if (sl >= int(int64_t(b + 1) * A.nslices / A.nblk_short)) return -1;
+    }
     const int sf = A.sf, j = lane & (sf - 1);
     const int L = __ldg(A.sl_len + sl);
     const int64_t sbase = __ldg(A.sl_ptr + sl);
@@ -407,9 +415,12 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   if (skip_launch(S, o.pred_aa_ok, o.stop)) return;
   const double* x = xr.get(S);
   double* out = o.out_pool ? o.out_pool + (int64_t)S->kx_idx[o.out_role] * o.out_stride : o.out;
-  double s;
-  const int row = row_sum<SERIAL>(A, x, s);
-  if (row >= 0) out[row] = s;
+  for (int rep = 0;; ++rep) {
+    double s;
+    const int row = row_sum<SERIAL>(A, x, s, NoPre{}, -1, rep);
+    if (row == -2) break;
+    if (row >= 0) out[row] = s;
+  }
 }
 
 // KKT scalars of the CUR iterate from the reduced sums (solver.cpp:83-107).
@@ -751,9 +762,12 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_spmv_pass(CsrDev A, VecRef xr, double* __restrict__ part, int first, const DevState* S) {
   if (S && S->done) return;
   const double* x = xr.get(S);
-  double s;
-  const int row = row_sum<false>(A, x, s);
-  if (row >= 0) part[row] = first ? s : __dadd_rn(part[row], s);
+  for (int rep = 0;; ++rep) {
+    double s;
+    const int row = row_sum<false>(A, x, s, NoPre{}, -1, rep);
+    if (row == -2) break;
+    if (row >= 0) part[row] = first ? s : __dadd_rn(part[row], s);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -767,56 +781,76 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 //   PUSH: du_j = x_j - xprev_j, dg_j = g_j - gprev_j, g_j = xhat_j - x_j
 // VAR 2 (experiment, AAPDHG_K1VAR=2): the SpMV alone, no epilogue.
 // CTA bid of nb; red holds P1_COUNT * kWarps doubles.
-template <bool SERIAL, bool PUSH, int VAR = 0, bool COH = false>
+// dual_epilogue: column j given t = (K'y)_j; the terms of u_k are assigned
+// to acc[].
+template <bool SERIAL, bool PUSH>
+__device__ __forceinline__ void dual_epilogue(int j, double t, const double* __restrict__ x,
+                                              const IterBufs& B, const DevParams* __restrict__ P,
+                                              const DevState* S, double (&acc)[P1_COUNT]) {
+  const int64_t N = P->N;
+  const double xj = x[j], cj = __ldg(B.c + j), lj = __ldg(B.l + j), uj = __ldg(B.u + j);
+  double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));
+  xn = smin(smax(xn, lj), uj);
+  B.upool[(int64_t)S->u_idx[U_HAT] * N + j] = xn;
+  for (int q = 0; q < P->ndst; ++q) P->xg_dst[q][j] = xn;  // sharded: own / peers' chunks
+  const double d = __dsub_rn(xn, xj);
+  const double red_c = __dsub_rn(cj, t);
+  const double lam = project_lambda1(red_c, lj, uj);
+  double bt = 0.0;
+  if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
+  if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
+  const double dv = __dsub_rn(red_c, lam);
+  acc[P1_GX2] = __dmul_rn(d, d);
+  acc[P1_BOUND] = bt;
+  acc[P1_DUALSQ] = __dmul_rn(dv, dv);
+  acc[P1_CX] = __dmul_rn(cj, xj);
+  if constexpr (PUSH) {
+    // after a plain step u_k = T(u_{k-1}) bit for bit, so g_{k-1} = u_k -
+    // u_{k-1} = du: g is only materialized (k_stage_g) for AA attempts
+    const int64_t slot = S->push_slot;
+    const double xp = B.upool[(int64_t)S->u_idx[U_PREV] * N + j];
+    const double dx = __dsub_rn(xj, xp);
+    const double gp = S->prev_plain ? dx : B.gpool[(int64_t)S->g_idx[G_PREV] * N + j];
+    B.du[slot * N + j] = dx;
+    B.dg[slot * N + j] = __dsub_rn(d, gp);
+  }
+  if (SERIAL || P->store_T) B.T[j] = t;
+}
+
+template <bool SERIAL, bool PUSH, int VAR = 0, bool COH = false, bool MULTI = false>
 __device__ __forceinline__ void dual_side_rows(const CsrDev& KT, const IterBufs& B,
                                                const DevParams* __restrict__ P, DevState* S,
                                                int bid, int nb, double* red) {
   const int64_t N = P->N;
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-  double t;
-  int j = row_sum<SERIAL, kUnroll, COH>(
-      KT, P->ygather ? P->ygather : x + P->n, t, [&](int r) {
-        l2_prefetch(x + r);
-        l2_prefetch(B.c + r);
-        l2_prefetch(B.l + r);
-        l2_prefetch(B.u + r);
-        if constexpr (PUSH) l2_prefetch(B.upool + (int64_t)S->u_idx[U_PREV] * N + r);
-      }, bid);
-  if (B.rinit1 && j >= 0) t = __dadd_rn(B.rinit1[j], t);  // earlier column passes
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
-  if (VAR == 2) {  // experiment: SpMV only
-    if (j >= 0) B.T[j] = t;
-    return;
-  }
-  if (j >= 0) {
-    const double xj = x[j], cj = __ldg(B.c + j), lj = __ldg(B.l + j), uj = __ldg(B.u + j);
-    double xn = __dsub_rn(xj, __dmul_rn(P->tau, __dsub_rn(cj, t)));
-    xn = smin(smax(xn, lj), uj);
-    B.upool[(int64_t)S->u_idx[U_HAT] * N + j] = xn;
-    for (int q = 0; q < P->ndst; ++q) P->xg_dst[q][j] = xn;  // sharded: own / peers' chunks
-    const double d = __dsub_rn(xn, xj);
-    const double red_c = __dsub_rn(cj, t);
-    const double lam = project_lambda1(red_c, lj, uj);
-    double bt = 0.0;
-    if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
-    if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
-    const double dv = __dsub_rn(red_c, lam);
-    acc[P1_GX2] = __dmul_rn(d, d);
-    acc[P1_BOUND] = bt;
-    acc[P1_DUALSQ] = __dmul_rn(dv, dv);
-    acc[P1_CX] = __dmul_rn(cj, xj);
-    if constexpr (PUSH) {
-      // after a plain step u_k = T(u_{k-1}) bit for bit, so g_{k-1} = u_k -
-      // u_{k-1} = du: g is only materialized (k_stage_g) for AA attempts
-      const int64_t slot = S->push_slot;
-      const double xp = B.upool[(int64_t)S->u_idx[U_PREV] * N + j];
-      const double dx = __dsub_rn(xj, xp);
-      const double gp = S->prev_plain ? dx : B.gpool[(int64_t)S->g_idx[G_PREV] * N + j];
-      B.du[slot * N + j] = dx;
-      B.dg[slot * N + j] = __dsub_rn(d, gp);
+  bool first = true;  // one row per thread: the terms themselves (no add)
+  for (int rep = 0;; ++rep) {
+    double t;
+    const int j = row_sum<SERIAL, kUnroll, COH>(
+        KT, P->ygather ? P->ygather : x + P->n, t, [&](int r) {
+          l2_prefetch(x + r);
+          l2_prefetch(B.c + r);
+          l2_prefetch(B.l + r);
+          l2_prefetch(B.u + r);
+          if constexpr (PUSH) l2_prefetch(B.upool + (int64_t)S->u_idx[U_PREV] * N + r);
+        }, bid, rep);
+    if (j == -2) break;
+    if (B.rinit1 && j >= 0) t = __dadd_rn(B.rinit1[j], t);  // earlier column passes
+    if (VAR == 2) {  // experiment: SpMV only
+      if (j >= 0) B.T[j] = t;
+      continue;
     }
-    if (SERIAL || P->store_T) B.T[j] = t;
+    if (j >= 0) {
+      double term[P1_COUNT];
+      dual_epilogue<SERIAL, PUSH>(j, t, x, B, P, S, term);
+#pragma unroll
+      for (int q = 0; q < P1_COUNT; ++q) acc[q] = first ? term[q] : __dadd_rn(acc[q], term[q]);
+      first = false;
+    }
+    if constexpr (!MULTI) break;  // (one slice per warp: no loop state)
   }
+  if (VAR == 2) return;
   if (!SERIAL) {
     block_sum<P1_COUNT>(acc, red);
     if (threadIdx.x == 0)
@@ -825,7 +859,8 @@ __device__ __forceinline__ void dual_side_rows(const CsrDev& KT, const IterBufs&
   }
 }
 
-template <bool SERIAL, bool PUSH, int VAR = 0>
+// MULTI: the layout is interleaved (several slices per warp, CsrDev)
+template <bool SERIAL, bool PUSH, int VAR = 0, bool MULTI = false>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   launch_dependents();  // k_primal_side may start its prologue (PDL)
@@ -844,7 +879,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     if (threadIdx.x == 0) p2p_wait(P, S, P2P_YG);
     __syncthreads();
   }
-  dual_side_rows<SERIAL, PUSH, VAR>(KT, B, P, S, int(blockIdx.x), int(gridDim.x), red);
+  dual_side_rows<SERIAL, PUSH, VAR, false, MULTI>(KT, B, P, S, int(blockIdx.x), int(gridDim.x), red);
   if (fused) {  // the last CTA publishes xhat (every CTA stored its chunk to every shard)
     __shared__ int last;
     __syncthreads();
@@ -870,45 +905,65 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 //   K xhat cached as the next K x (solver.cpp:90 / pdhg_core.cpp:56)
 //   per-CTA partials: (yhat-y)^2, q_i y_i, primal infeasibility of u_k
 // The rows and epilogue; acc gets this thread's share of the partials.
-template <bool SERIAL, bool PUSH, bool COH = false>
+// primal_epilogue: row i given s = (K xhat)_i; the terms of u_k are
+// assigned to acc[].
+template <bool PUSH>
+__device__ __forceinline__ void primal_epilogue(int i, double s, const IterBufs& B,
+                                                const DevParams* __restrict__ P, const DevState* S,
+                                                double (&acc)[P2_COUNT]) {
+  const int64_t N = P->N;
+  const int n = P->n, mr = P->mrows;
+  const double yi = B.upool[(int64_t)S->u_idx[U_CUR] * N + n + i];
+  const double qi = __ldg(B.q + i);
+  const double kxi = B.kxpool[(int64_t)S->kx_idx[KX_CUR] * mr + i];
+  double yn =
+      __dadd_rn(yi, __dmul_rn(P->sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
+  if (i < P->m1) yn = smax(yn, 0.0);
+  B.upool[(int64_t)S->u_idx[U_HAT] * N + n + i] = yn;
+  for (int q = 0; q < P->ndst; ++q) P->yg_dst[q][i] = yn;
+  B.kxpool[(int64_t)S->kx_idx[KX_HAT] * mr + i] = s;
+  const double d = __dsub_rn(yn, yi);
+  double v = __dsub_rn(qi, kxi);
+  if (i < P->m1) v = smax(v, 0.0);
+  acc[P2_GY2] = __dmul_rn(d, d);
+  acc[P2_QY] = __dmul_rn(qi, yi);
+  acc[P2_INFEAS] = __dmul_rn(v, v);
+  if constexpr (PUSH) {
+    const int64_t slot = S->push_slot;
+    const double yp = B.upool[(int64_t)S->u_idx[U_PREV] * N + n + i];
+    const double dy = __dsub_rn(yi, yp);
+    const double gp = S->prev_plain ? dy : B.gpool[(int64_t)S->g_idx[G_PREV] * N + n + i];
+    B.du[slot * N + n + i] = dy;
+    B.dg[slot * N + n + i] = __dsub_rn(d, gp);
+  }
+}
+
+template <bool SERIAL, bool PUSH, bool COH = false, bool MULTI = false>
 __device__ __forceinline__ void primal_side_rows(const CsrDev& K, const IterBufs& B,
                                                  const DevParams* __restrict__ P, DevState* S,
                                                  int bid, double (&acc)[P2_COUNT]) {
   const int64_t N = P->N;
-  const int n = P->n, mr = P->mrows;
-  double s;
-  const int i = row_sum<SERIAL, kUnroll, COH>(
-      K, P->xgather ? P->xgather : B.upool + (int64_t)S->u_idx[U_HAT] * N, s, NoPre{}, bid);
-  if (B.rinit2 && i >= 0) s = __dadd_rn(B.rinit2[i], s);  // earlier column passes
-  if (i >= 0) {
-    const double yi = B.upool[(int64_t)S->u_idx[U_CUR] * N + n + i];
-    const double qi = __ldg(B.q + i);
-    const double kxi = B.kxpool[(int64_t)S->kx_idx[KX_CUR] * mr + i];
-    double yn =
-        __dadd_rn(yi, __dmul_rn(P->sigma, __dsub_rn(qi, __dsub_rn(__dmul_rn(2.0, s), kxi))));
-    if (i < P->m1) yn = smax(yn, 0.0);
-    B.upool[(int64_t)S->u_idx[U_HAT] * N + n + i] = yn;
-    for (int q = 0; q < P->ndst; ++q) P->yg_dst[q][i] = yn;
-    B.kxpool[(int64_t)S->kx_idx[KX_HAT] * mr + i] = s;
-    const double d = __dsub_rn(yn, yi);
-    double v = __dsub_rn(qi, kxi);
-    if (i < P->m1) v = smax(v, 0.0);
-    acc[P2_GY2] = __dmul_rn(d, d);
-    acc[P2_QY] = __dmul_rn(qi, yi);
-    acc[P2_INFEAS] = __dmul_rn(v, v);
-    if constexpr (PUSH) {
-      const int64_t slot = S->push_slot;
-      const double yp = B.upool[(int64_t)S->u_idx[U_PREV] * N + n + i];
-      const double dy = __dsub_rn(yi, yp);
-      const double gp = S->prev_plain ? dy : B.gpool[(int64_t)S->g_idx[G_PREV] * N + n + i];
-      B.du[slot * N + n + i] = dy;
-      B.dg[slot * N + n + i] = __dsub_rn(d, gp);
+  bool first = true;  // one row per thread: the terms themselves (no add)
+  for (int rep = 0;; ++rep) {
+    double s;
+    const int i = row_sum<SERIAL, kUnroll, COH>(
+        K, P->xgather ? P->xgather : B.upool + (int64_t)S->u_idx[U_HAT] * N, s, NoPre{}, bid,
+        rep);
+    if (i == -2) break;
+    if (B.rinit2 && i >= 0) s = __dadd_rn(B.rinit2[i], s);  // earlier column passes
+    if (i >= 0) {
+      double term[P2_COUNT];
+      primal_epilogue<PUSH>(i, s, B, P, S, term);
+#pragma unroll
+      for (int q = 0; q < P2_COUNT; ++q) acc[q] = first ? term[q] : __dadd_rn(acc[q], term[q]);
+      first = false;
     }
+    if constexpr (!MULTI) break;  // (one slice per warp: no loop state)
   }
 }
 
 // VAR 2 (experiment, AAPDHG_K2VAR=2): the SpMV alone, no epilogue or control
-template <bool SERIAL, bool PUSH, int VAR = 0>
+template <bool SERIAL, bool PUSH, int VAR = 0, bool MULTI = false>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
@@ -924,7 +979,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     if (threadIdx.x == 0) p2p_wait(P, S, P2P_XG);
     __syncthreads();
   }
-  primal_side_rows<SERIAL, PUSH>(K, B, P, S, int(blockIdx.x), acc);
+  primal_side_rows<SERIAL, PUSH, false, MULTI>(K, B, P, S, int(blockIdx.x), acc);
   if (!SERIAL) {
     __shared__ __align__(16) TailSmem ts;
     if (B.fused_ctrl) tail_prefetch(ts, P, S);

@@ -416,3 +416,32 @@ def test_l2_column_blocking_matches_unblocked(monkeypatch):
     assert np.array_equal(got.trajectory["aa_step"][:50], ref.trajectory["aa_step"][:50])
     x, xr = got.result.u.x, ref.result.u.x
     assert np.linalg.norm(x - xr) <= 1e-9 * np.linalg.norm(xr)
+
+
+@pytest.mark.parametrize("reduction", ["serial", "tree"])
+def test_interleaved_short_row_layout(port, monkeypatch, reduction):
+    """Very short rows in more slices than two waves of warps get the
+    interleaved SELL layout (one wave of CTAs, each warp looping over slices
+    w, w + wave*8, ...; ingest.cu device_sell): config 2 shape at 700 x 700,
+    K' = 490k rows of 2, AA-PDHG m=10. SERIAL stays bit-identical to the oracle (row sums
+    and index-ordered chains do not depend on the slice -> CTA map); TREE
+    within 1e-10 over the first 50 iterates, and within 1e-12 of the same
+    solve on the contiguous layout (AAPDHG_INTERLEAVE=0)."""
+    p = problems.make_config(2, scale=0.35)
+    cfg = SolverConfig(method=Method.AA_PDHG, m=10, toll=1e-12, max_iters=50, tau=0.0142,
+                       sigma=0.0142, reduction=reduction)
+    with Solver(p) as s:
+        got = s.solve(cfg)
+    ref = port.solve(p, cfg)
+    if reduction == "serial":
+        assert np.array_equal(got.trajectory["g_norm"], ref.trajectory["g_norm"])
+        assert np.array_equal(got.result.u.x, ref.result.u.x)
+    else:
+        np.testing.assert_allclose(got.trajectory["g_norm"], ref.trajectory["g_norm"],
+                                   rtol=1e-10)
+        monkeypatch.setenv("AAPDHG_INTERLEAVE", "0")
+        with Solver(p) as s:
+            flat = s.solve(cfg)
+        np.testing.assert_allclose(got.trajectory["g_norm"], flat.trajectory["g_norm"],
+                                   rtol=1e-12)
+        assert np.array_equal(got.trajectory["aa_step"], flat.trajectory["aa_step"])
