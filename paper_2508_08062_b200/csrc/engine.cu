@@ -1625,6 +1625,24 @@ double Problem::sh_read_scal(int world, int q) {
 
 }  // namespace aapdhg_b200
 
+#ifdef AAPDHG_PLAIN_STAMPS
+// experiment build only: k_plain_loop phases averaged over workers and
+// iterations (ns): K1, bar 1 wait, K2, bar 2 wait; then the maxima of K1 and
+// K2 over all workers and iterations, and the count
+extern "C" int aapdhg_cuda_plain_stamps(double* out) {
+  unsigned long long v[8];
+  if (cudaMemcpyFromSymbol(v, aapdhg_b200::g_plain_dbg, sizeof v) != cudaSuccess) return -1;
+  const double c = v[4] ? double(v[4]) : 1.0;
+  for (int i = 0; i < 4; ++i) out[i] = v[i] / c;
+  out[4] = double(v[5]);
+  out[5] = double(v[6]);
+  out[6] = c;
+  unsigned long long z[8] = {};
+  cudaMemcpyToSymbol(aapdhg_b200::g_plain_dbg, z, sizeof z);
+  return 0;
+}
+#endif
+
 #ifdef AAPDHG_TAIL_STAMPS
 // experiment build only: averaged phase times (ns) of the fused control tail
 extern "C" int aapdhg_cuda_debug_stamps(double* out) {

@@ -1019,6 +1019,9 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 // the push to the spare history slot (advance keeps cap + 1 slots), and the
 // K1 partials, which the control CTA folded before barrier 2. Results are
 // bit-identical to the per-kernel graph with the same CTA layout.
+#ifdef AAPDHG_PLAIN_STAMPS
+__device__ unsigned long long g_plain_dbg[8];
+#endif
 struct GridBar {
   unsigned long long arrive1;  // barrier 1: arrivals (low 40 bits) + stops (high bits)
   unsigned long long arrive2;  // barrier 2: arrivals
@@ -1130,12 +1133,23 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   }
   unsigned long long h0 = 0;  // stop flags raised before this launch
   if (threadIdx.x == 0) h0 = ld_relaxed(&gb->arrive1) >> 40;
+#ifdef AAPDHG_PLAIN_STAMPS
+  // experiment build only: per worker and iteration, the K1 phase, the bar 1
+  // wait, the K2 phase, the bar 2 wait (summed, aapdhg_cuda_plain_stamps)
+  uint64_t ps0 = globaltimer_ns(), ps1 = 0, ps2 = 0, ps3 = 0;
+#endif
   for (;;) {
     if (bid < nb1) dual_side_rows<false, PUSH, 0, true>(KT, B, P, &st, bid, nb1, red);
     __syncthreads();
+#ifdef AAPDHG_PLAIN_STAMPS
+    if (threadIdx.x == 0) ps1 = globaltimer_ns();
+#endif
     if (threadIdx.x == 0) s_stop = (bar_arrive_wait(&gb->arrive1, 1, G) >> 40) != h0;
     __syncthreads();
     if (s_stop) return;  // the control stopped after the previous iteration
+#ifdef AAPDHG_PLAIN_STAMPS
+    if (threadIdx.x == 0) ps2 = globaltimer_ns();
+#endif
     double acc[P2_COUNT] = {0.0, 0.0, 0.0};
     if (bid < nb2) {
       primal_side_rows<false, PUSH, true>(K, B, P, &st, bid, acc);
@@ -1145,6 +1159,9 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
         for (int q = 0; q < P2_COUNT; ++q) B.part2[q * nb2 + bid] = acc[q];
     }
     __syncthreads();
+#ifdef AAPDHG_PLAIN_STAMPS
+    if (threadIdx.x == 0) ps3 = globaltimer_ns();
+#endif
     if (threadIdx.x == 0) {
       bar_arrive_wait(&gb->arrive2, 1, G);
       // the roles of iteration k+1 if iteration k is a plain step
@@ -1152,6 +1169,19 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
       control_commit(P, &st, st.k, Decision{0, 1});
     }
     __syncthreads();
+#ifdef AAPDHG_PLAIN_STAMPS
+    if (threadIdx.x == 0) {
+      const uint64_t ps4 = globaltimer_ns();
+      atomicAdd(&g_plain_dbg[0], ps1 - ps0);
+      atomicAdd(&g_plain_dbg[1], ps2 - ps1);
+      atomicAdd(&g_plain_dbg[2], ps3 - ps2);
+      atomicAdd(&g_plain_dbg[3], ps4 - ps3);
+      atomicAdd(&g_plain_dbg[4], 1ull);
+      atomicMax(&g_plain_dbg[5], ps1 - ps0);
+      atomicMax(&g_plain_dbg[6], ps3 - ps2);
+      ps0 = ps4;
+    }
+#endif
   }
 }
 
