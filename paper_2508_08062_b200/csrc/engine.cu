@@ -35,7 +35,7 @@ constexpr uint64_t kRecCap = 1 << 16;  // device record ring
 constexpr uint64_t kPowTabMax = 1 << 22;
 constexpr int kPowerBatch = 8;
 
-// tuning overrides (experiments): AAPDHG_SF, AAPDHG_SPMV_WARPS
+// tuning overrides (experiments, INTEGRATION.md "Environment switches")
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return (v && *v) ? std::atoi(v) : dflt;
