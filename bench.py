@@ -452,7 +452,7 @@ def main():
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
                     help="sharded-solve exchanges: peer-memory stores (p2p, <= 8 GPUs) or NCCL")
     ap.add_argument("--shard", action="store_true",
-                    help="use the sharded (NCCL) solve even at N=1 (exercises the N>1 path)")
+                    help="use the sharded solve even at N=1 (exercises the N>1 path)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel, if captured")
     args = ap.parse_args()
