@@ -414,12 +414,23 @@ class Solver:
     def N(self) -> int:
         return self.p.n() + self.p.k.nrows
 
-    def solve(self, cfg: SolverConfig, u0: Optional[Iterate] = None) -> SolveOutput:
+    def solve(self, cfg: SolverConfig, u0: Optional[Iterate] = None,
+              out: Optional[tuple] = None) -> SolveOutput:
+        """``out`` = (x[n], y[m], lambda[n]) float64 buffers to fill (e.g.
+        page-locked host memory: the results are then DMA'd straight into
+        them); fresh arrays otherwise."""
         n, m = self.p.n(), self.p.k.nrows
         prm = cfg.to_params(n + m)
-        x = np.empty(n)
-        y = np.empty(m)
-        lam = np.empty(n)
+        if out is not None:
+            x, y, lam = out
+            for a, sz in ((x, n), (y, m), (lam, n)):
+                if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.shape == (sz,)
+                        and a.flags.c_contiguous and a.flags.writeable):
+                    raise DimensionError("solve: out buffers must be writable float64 (n, m, n)")
+        else:
+            x = np.empty(n)
+            y = np.empty(m)
+            lam = np.empty(n)
         x0 = y0 = None
         if u0 is not None:
             x0 = np.ascontiguousarray(u0.x, dtype=np.float64)

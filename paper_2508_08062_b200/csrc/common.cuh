@@ -74,6 +74,9 @@ struct CsrDev {
   int32_t grid() const { return nblk_short + nblk_long; }
 };
 
+// device validation flags (ingest.cu k_validate_*)
+enum { kCsrBadRowPtr = 1, kCsrBadColumn = 2, kCsrUnsorted = 4, kCsrNonzero = 8, kBoundsBad = 16 };
+
 constexpr int kLongRow = 256;        // rows longer than this get a warp each
 constexpr int kHugeRow = 1024;       // TREE: rows at least this long get a CTA each
 constexpr int kSpmvBlocksPerSM = 6;  // 48 warps/SM at <= 40 registers

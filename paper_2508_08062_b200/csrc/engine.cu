@@ -45,11 +45,14 @@ int num_items_host(int p, int method) {
   return p * (p + 1) / 2 + p + (method == AAPDHG_METHOD_FAA ? p : 0);
 }
 
+// host <-> device copies (memory.cu): pinned host buffers are DMA'd
+// directly, pageable ones staged through pinned chunks; d2h returns with the
+// data on the host
 void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  if (bytes) AAPDHG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  host_to_device(dst, src, bytes, s);
 }
 void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  if (bytes) AAPDHG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+  device_to_host(dst, src, bytes, s);
 }
 
 int grid_for(int64_t n, int per_block = kThreads, int cap = 148 * 8) {
@@ -61,17 +64,22 @@ int grid_for(int64_t n, int per_block = kThreads, int cap = 148 * 8) {
 
 }  // namespace
 
+// Device buffers come from the per-device block cache (memory.cu); a block
+// returns to it when its owner is done with it (owners synchronise first).
 DevBuf::~DevBuf() {
-  if (p) cudaFree(p);
+  if (p) cache_free(p, bytes);
 }
 
 void DevBuf::reserve(size_t b) {
   if (b == 0) b = 16;
   if (p && b <= bytes) return;
-  if (p) cudaFree(p);
+  if (p) {  // growth: work in flight may still read the old block
+    AAPDHG_CUDA(cudaDeviceSynchronize());
+    cache_free(p, bytes);
+  }
   p = nullptr;
   bytes = 0;
-  AAPDHG_CUDA(cudaMalloc(&p, b));
+  p = cache_alloc(b);
   bytes = b;
 }
 
@@ -123,6 +131,7 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
   h2d(st.rp.p, rp, sizeof(int32_t) * (size_t(nrows) + 1), stream_);
   h2d(st.ci.p, ci, sizeof(int32_t) * size_t(nnz), stream_);
   h2d(st.v.p, v, sizeof(double) * size_t(nnz), stream_);
+  device_validate(st, nrows, ncols, nnz);
   finish_csr(nrows, ncols, nnz, st, ser, tree);  // layouts built on the device (ingest.cu)
 }
 
@@ -196,7 +205,10 @@ size_t Problem::aa_smem(int cap) { return sizeof(double) * 2 * size_t(cap) * siz
 
 
 // ---------------------------------------------------------------------------
-void validate_problem_view(const aapdhg_problem_view* v) {
+// O(1) checks on the host; the O(nnz) ones run on the device after the
+// upload (Problem::device_validate) or, for the sharded path that slices
+// the LP on the host, in validate_problem_deep.
+void validate_problem_header(const aapdhg_problem_view* v) {
   if (!v) throw StatusError(AAPDHG_ERR_INPUT, "problem_create: null problem");
   const aapdhg_csr_view& k = v->k;
   if (k.nrows < 0 || k.ncols < 0 || k.nnz < 0)
@@ -210,17 +222,32 @@ void validate_problem_view(const aapdhg_problem_view* v) {
   if (k.ncols > 0 && (!v->c || !v->l || !v->u))
     throw StatusError(AAPDHG_ERR_INPUT, "problem_create: null c/l/u");
   if (k.nrows > 0 && !v->q) throw StatusError(AAPDHG_ERR_INPUT, "problem_create: null q");
+}
+
+const char* csr_flag_message(int flags) {
+  if (flags & kCsrBadRowPtr) return "problem_create: row_ptr not monotone";
+  if (flags & kCsrBadColumn) return "problem_create: column index out of range";
+  if (flags & kCsrUnsorted) return "problem_create: column indices not strictly increasing in a row";
+  return nullptr;
+}
+
+void validate_problem_deep(const aapdhg_problem_view* v) {
+  const aapdhg_csr_view& k = v->k;
+  int flags = 0;
   for (int r = 0; r < k.nrows; ++r)
-    if (k.row_ptr[r + 1] < k.row_ptr[r])
-      throw StatusError(AAPDHG_ERR_DIMENSION, "problem_create: row_ptr not monotone");
+    if (k.row_ptr[r + 1] < k.row_ptr[r]) flags |= kCsrBadRowPtr;
   for (int64_t e = 0; e < k.nnz; ++e)
-    if (k.col_idx[e] < 0 || k.col_idx[e] >= k.ncols)
-      throw StatusError(AAPDHG_ERR_DIMENSION, "problem_create: column index out of range");
-  for (int r = 0; r < k.nrows; ++r)
-    for (int32_t e = k.row_ptr[r] + 1; e < k.row_ptr[r + 1]; ++e)
-      if (k.col_idx[e] <= k.col_idx[e - 1])
-        throw StatusError(AAPDHG_ERR_DIMENSION,
-                          "problem_create: column indices not strictly increasing in a row");
+    if (k.col_idx[e] < 0 || k.col_idx[e] >= k.ncols) flags |= kCsrBadColumn;
+  if (!(flags & kCsrBadRowPtr))
+    for (int r = 0; r < k.nrows; ++r)
+      for (int32_t e = k.row_ptr[r] + 1; e < k.row_ptr[r + 1]; ++e)
+        if (k.col_idx[e] <= k.col_idx[e - 1]) flags |= kCsrUnsorted;
+  if (const char* msg = csr_flag_message(flags)) throw StatusError(AAPDHG_ERR_DIMENSION, msg);
+}
+
+void validate_problem_view(const aapdhg_problem_view* v) {
+  validate_problem_header(v);
+  validate_problem_deep(v);
 }
 
 // K' as CSR with the entries of each row in ascending original row of K
@@ -297,8 +324,9 @@ void Problem::init_vectors(const double* c, const double* q, const double* l, co
   scal_.reserve(sizeof(double) * 64);
   const int64_t nbig = std::max<int64_t>(std::max<int64_t>(n_, m_), 1);
   part_small_.reserve(sizeof(double) * 5 * (nbig / kThreads + 2));
-  AAPDHG_CUDA(cudaMallocHost(&h_state_, sizeof(DevState)));
-  AAPDHG_CUDA(cudaMallocHost(&h_batch_, sizeof(int32_t)));
+  static_assert(sizeof(DevState) <= 4096, "state mirror exceeds a pinned pool block");
+  h_state_ = static_cast<DevState*>(pinned_small_alloc(sizeof(DevState)));
+  h_batch_ = static_cast<int32_t*>(pinned_small_alloc(sizeof(int32_t)));
   AAPDHG_CUDA(cudaFuncSetAttribute(k_aa_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(aa_smem(kMaxMemory))));
   AAPDHG_CUDA(cudaFuncSetAttribute(k_serial_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -322,7 +350,7 @@ struct PhaseTimer {
 
 Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   PhaseTimer ph;
-  validate_problem_view(v);
+  validate_problem_header(v);
   const aapdhg_csr_view& k = v->k;
   ph("validate");
   init_device(device);
@@ -333,7 +361,6 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   nnz_ = k.nnz;
   N_ = int64_t(n_) + m_;
   nglob_ = N_;
-  for (int64_t e = 0; e < nnz_ && all_zero_; ++e) all_zero_ = k.vals[e] == 0.0;
 
   upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
   ph("upload K + SELL");
@@ -345,21 +372,11 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   build_blocks(t_store_, n_, m_, ktb_);
   ph("L2 blocks");
 
-  bounds_ok_ = true;
-  for (int j = 0; j < n_; ++j)
-    if (v->l[j] > v->u[j]) bounds_ok_ = false;
   init_vectors(v->c, v->q, v->l, v->u);
+  device_flags_vectors();
   ph("vectors");
-
-  // ||q|| and ||c|| (constants of kkt_metrics): SERIAL order is the
-  // reference's index-ordered dot (vec.hpp:16-29) — on the host, where the
-  // inputs are (x86-64 without FMA contraction: bitwise the same chain);
-  // TREE order on the device
-  double qq = 0.0, cc = 0.0;
-  for (int i = 0; i < m_; ++i) qq += v->q[i] * v->q[i];
-  for (int j = 0; j < n_; ++j) cc += v->c[j] * v->c[j];
-  nrm_q_[0] = std::sqrt(qq);
-  nrm_c_[0] = std::sqrt(cc);
+  // ||q|| and ||c|| (constants of kkt_metrics): TREE order on the device;
+  // the SERIAL (index-ordered, vec.hpp:16-29) ones on first use (serial_norms)
   nrm_q_[1] = std::sqrt(device_dot(q_.as<double>(), nullptr, m_, false));
   nrm_c_[1] = std::sqrt(device_dot(c_.as<double>(), nullptr, n_, false));
   ph("norms");
@@ -367,6 +384,9 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
 
 Problem::~Problem() {
   PhaseTimer ph;
+  // the device buffers go back to the block cache: nothing may still use them
+  cudaSetDevice(device_);
+  cudaDeviceSynchronize();
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   ph("destroy: graph");
   for (auto& e : event_pool_) cudaEventDestroy(e);
@@ -374,8 +394,8 @@ Problem::~Problem() {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
   }
-  if (h_state_) cudaFreeHost(h_state_);
-  if (h_batch_) cudaFreeHost(h_batch_);
+  pinned_small_free(h_state_);
+  pinned_small_free(h_batch_);
   ph("destroy: pinned");
   delete sh_su_;
   if (ev_fork_) cudaEventDestroy(ev_fork_);
@@ -414,6 +434,41 @@ double Problem::device_dot(const double* a, const double* b, int64_t n, bool ser
   d2h(&out, scal_.as<double>() + 40, sizeof(double), stream_);
   sync();
   return out;
+}
+
+// (i+1)^-(1+eps) for i < need (at most kPowTabMax; device pow() beyond),
+// host std::pow as the reference's safeguard_pass (solver.cpp:59-62). The
+// table is kept across solves and grown lazily, so a solve uploads only the
+// entries its launches can reach.
+void Problem::ensure_pow_table(double eps, uint64_t need) {
+  need = std::min<uint64_t>(std::max<uint64_t>(need, 1), kPowTabMax);
+  if (!(eps == pow_eps_)) {
+    pow_host_.clear();
+    pow_len_ = 0;
+    pow_eps_ = eps;
+  }
+  if (need <= pow_len_) return;
+  const uint64_t from = pow_len_;
+  const uint64_t len = std::min<uint64_t>(std::max<uint64_t>(need, 2 * from), kPowTabMax);
+  pow_host_.resize(len);
+  for (uint64_t i = from; i < len; ++i) pow_host_[i] = std::pow(double(i) + 1.0, -(1.0 + eps));
+  if (sizeof(double) * len > pow_tab_.bytes) {  // new block: upload everything
+    pow_tab_.reserve(sizeof(double) * len);
+    h2d(pow_tab_.p, pow_host_.data(), sizeof(double) * len, stream_);
+  } else {
+    h2d(pow_tab_.as<double>() + from, pow_host_.data() + from, sizeof(double) * (len - from),
+        stream_);
+  }
+  pow_len_ = len;
+}
+
+// the SERIAL-order ||q||, ||c|| (index-ordered chains, bitwise the
+// reference's dot, vec.hpp:16-29), computed on first SERIAL use
+void Problem::ensure_serial_norms() {
+  if (serial_norms_) return;
+  nrm_q_[0] = std::sqrt(device_dot(q_.as<double>(), nullptr, m_, true));
+  nrm_c_[0] = std::sqrt(device_dot(c_.as<double>(), nullptr, n_, true));
+  serial_norms_ = true;
 }
 
 void Problem::ensure_iter_buffers(int method, int cap) {
@@ -474,6 +529,7 @@ void Problem::upload_iterate(int slot, const double* x, const double* y) {
 void Problem::kkt_eval(int slot, bool serial, double* out_dev, double* lam_dev) {
   const double* x = upool_.as<double>() + int64_t(slot) * N_;
   const double* y = x + n_;
+  if (serial) ensure_serial_norms();
   double* T = T_.as<double>();
   double* KX = pw_mx_.as<double>();
   if (n_) spmv(stream_, KTm(serial), vref(y), rout(T), serial, nullptr, 0, nullptr);
@@ -852,14 +908,24 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
     dhat_.reserve(sizeof(double) * N_);
     h2d(dhat_.p, prm->d_hat, sizeof(double) * N_, stream_);
   }
-  std::vector<double> ptab;
-  if (method != AAPDHG_METHOD_PDHG) {
-    const uint64_t len = std::min<uint64_t>(prm->max_iters + 1, kPowTabMax);
-    ptab.resize(len);
-    for (uint64_t i = 0; i < len; ++i) ptab[i] = std::pow(double(i) + 1.0, -(1.0 + prm->safeguard_eps));
-    pow_tab_.reserve(sizeof(double) * len);
-    h2d(pow_tab_.p, ptab.data(), sizeof(double) * len, stream_);
-  }
+  // executable graph, cached per launch layout
+  // AAPDHG_EAGER=1 forces stream launches (ncu cannot profile kernels inside
+  // graphs that hold conditional nodes)
+  static const bool force_eager = [] {
+    const char* e = std::getenv("AAPDHG_EAGER");
+    return e && e[0] == '1';
+  }();
+  const bool use_graph = !profiling_ && !force_eager;
+  // graph launches run up to `batch` iterations; the first one covers a
+  // short solve whole (eager launching keeps small batches: every launched
+  // iteration is issued even when predicated off)
+  const uint64_t max_it_sat = prm->max_iters >= (UINT64_MAX >> 1) ? (UINT64_MAX >> 1)
+                                                                   : prm->max_iters;
+  const uint64_t ring_batch = std::min<uint64_t>(kMaxBatch, rec_cap_ / 2);
+  int batch = use_graph ? int(std::min<uint64_t>(max_it_sat + 2, ring_batch)) : 8;
+  // the safeguard's (i+1)^-(1+eps) for every i the first launch can reach
+  if (method != AAPDHG_METHOD_PDHG)
+    ensure_pow_table(prm->safeguard_eps, std::min<uint64_t>(max_it_sat, uint64_t(batch)) + 2);
 
   ph("solve: buffers + pow table");
   DevParams P{};
@@ -884,11 +950,12 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.sigma = sigma;
   P.max_iters = prm->max_iters;
   P.max_wall_s = prm->max_wall_seconds;
+  if (serial) ensure_serial_norms();
   P.nrm_q = nrm_q_[serial ? 0 : 1];
   P.nrm_c = nrm_c_[serial ? 0 : 1];
   P.d_hat = prm->d_hat ? dhat_.as<double>() : nullptr;
-  P.pow_tab = ptab.empty() ? nullptr : pow_tab_.as<double>();
-  P.pow_len = ptab.size();
+  P.pow_tab = method == AAPDHG_METHOD_PDHG ? nullptr : pow_tab_.as<double>();
+  P.pow_len = method == AAPDHG_METHOD_PDHG ? 0 : pow_len_;
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
   const bool blk1 = !serial && ktb_.nb() > 1, blk2 = !serial && kb_.nb() > 1;
@@ -928,14 +995,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.ndot_blk = ndot;
   su.items_max = num_items_host(std::max(cap, 1), method);
 
-  // executable graph, cached per launch layout
-  // AAPDHG_EAGER=1 forces stream launches (ncu cannot profile kernels inside
-  // graphs that hold conditional nodes)
-  static const bool force_eager = [] {
-    const char* e = std::getenv("AAPDHG_EAGER");
-    return e && e[0] == '1';
-  }();
-  const bool use_graph = !profiling_ && !force_eager;
+  // executable graph, cached per launch layout (use_graph above)
   // plain iterations in one persistent grid (AAPDHG_PERSIST=0: per-kernel graph)
   PersistLock plock;
   // (eager stream launches of it only on request, AAPDHG_PERSIST_EAGER=1: ncu
@@ -1010,10 +1070,23 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
 
   ph("solve: start iterate");
   uint64_t flushed = 0, eager_launches = 0;
-  int batch = 8;  // iterations per launch, grows geometrically
   std::vector<aapdhg_record> host_recs;
   const aapdhg_record* drec = rec_.as<aapdhg_record>();
-  for (;;) {
+  for (bool first = true;; first = false) {
+    if (!first && method != AAPDHG_METHOD_PDHG) {
+      // i grows by at most one per iteration: cover the next launch
+      const uint64_t cap_before = pow_len_;
+      const double* tab_before = pow_tab_.as<double>();
+      ensure_pow_table(prm->safeguard_eps,
+                       std::min<uint64_t>(max_it_sat, h_state_->i + uint64_t(batch)) + 2);
+      if (pow_len_ != cap_before || pow_tab_.as<double>() != tab_before) {
+        DevParams* Pd = dparams_.as<DevParams>();
+        const double* tp = pow_tab_.as<double>();
+        const uint64_t tl = pow_len_;
+        h2d(&Pd->pow_tab, &tp, sizeof tp, stream_);
+        h2d(&Pd->pow_len, &tl, sizeof tl, stream_);
+      }
+    }
     if (use_graph) {
       *h_batch_ = batch;
       h2d(&S->batch_left, h_batch_, sizeof(int32_t), stream_);
@@ -1046,7 +1119,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
     }
     if (h_state_->done) break;
     // ring safety: a launch never runs further ahead than half the ring
-    batch = int(std::min<uint64_t>(uint64_t(batch) * 2, std::min<uint64_t>(kMaxBatch, rec_cap_ / 2)));
+    batch = int(std::min<uint64_t>(uint64_t(batch) * 2, ring_batch));
   }
   const DevState st = *h_state_;
   ph("solve: iterations");
@@ -1275,6 +1348,7 @@ Problem::Problem(const ShardSpec& sp, int device) : device_(device) {
   init_vectors(sp.c.data(), sp.q.data(), sp.l.data(), sp.u.data());
   nrm_q_[0] = nrm_q_[1] = sp.nrm_q;
   nrm_c_[0] = nrm_c_[1] = sp.nrm_c;
+  serial_norms_ = true;
   const int64_t W = sp.world;
   xg_.reserve(sizeof(double) * W * maxc_);
   yg_.reserve(sizeof(double) * W * maxr_);
@@ -1326,14 +1400,10 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
     dhat_.reserve(sizeof(double) * std::max<int64_t>(N_, 1));
     h2d(dhat_.p, d_hat, sizeof(double) * N_, stream_);
   }
-  std::vector<double> ptab;
-  if (method != AAPDHG_METHOD_PDHG) {
-    const uint64_t len = std::min<uint64_t>(prm->max_iters + 1, kPowTabMax);
-    ptab.resize(len);
-    for (uint64_t i = 0; i < len; ++i) ptab[i] = std::pow(double(i) + 1.0, -(1.0 + prm->safeguard_eps));
-    pow_tab_.reserve(sizeof(double) * len);
-    h2d(pow_tab_.p, ptab.data(), sizeof(double) * len, stream_);
-  }
+  // the safeguard table for every i the solve can reach (cached across solves)
+  if (method != AAPDHG_METHOD_PDHG)
+    ensure_pow_table(prm->safeguard_eps,
+                     (prm->max_iters >= kPowTabMax ? kPowTabMax : prm->max_iters) + 1);
   DevParams P{};
   P.method = method;
   P.serial = 0;
@@ -1360,8 +1430,8 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   P.nrm_q = nrm_q_[1];
   P.nrm_c = nrm_c_[1];
   P.d_hat = d_hat ? dhat_.as<double>() : nullptr;
-  P.pow_tab = ptab.empty() ? nullptr : pow_tab_.as<double>();
-  P.pow_len = ptab.size();
+  P.pow_tab = method == AAPDHG_METHOD_PDHG ? nullptr : pow_tab_.as<double>();
+  P.pow_len = method == AAPDHG_METHOD_PDHG ? 0 : pow_len_;
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
   P.nblk1 = sh_k1m().grid();

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "memory.h"
 
 namespace aapdhg_b200 {
 
@@ -30,7 +31,9 @@ struct KernelStat {
 
 struct SolveSetup;
 
-void validate_problem_view(const aapdhg_problem_view* v);
+void validate_problem_view(const aapdhg_problem_view* v);    // header + deep (host)
+void validate_problem_header(const aapdhg_problem_view* v);  // O(1) host checks
+const char* csr_flag_message(int flags);  // kCsr* flags -> the error message, or null
 void validate_config(const aapdhg_solve_params* c);
 void transpose_csr(const aapdhg_csr_view& k, std::vector<int32_t>& trp, std::vector<int32_t>& tci,
                    std::vector<double>& tv);
@@ -234,6 +237,16 @@ class Problem {
   bool building_blocks_ = false;  // device_sell: an L2 column block (never interleaved)
   DevBuf c_, q_, l_, u_;
   double nrm_q_[2] = {0, 0}, nrm_c_[2] = {0, 0};  // [serial, tree]
+  bool serial_norms_ = false;
+  double pow_eps_ = -1.0;            // the safeguard table's eps (NaN-free: validated)
+  uint64_t pow_len_ = 0;             // entries valid on the device
+  std::vector<double> pow_host_;
+  void ensure_pow_table(double eps, uint64_t need);
+  void ensure_serial_norms();
+  // O(nnz) checks of the uploaded CSR, l <= u and the all-zero test on the
+  // device (ingest.cu); throws the host validator's messages
+  void device_validate(const CsrStore& st, int nrows, int ncols, int64_t nnz);
+  void device_flags_vectors();
 
   // iteration buffers
   int buf_method_ = -1, buf_cap_ = 0;

@@ -135,6 +135,47 @@ __global__ void k_permute(const int32_t* perm, const int32_t* row_of, const doub
 
 __global__ void k_set(int32_t* p, int32_t v) { *p = v; }
 
+// warp per row: row_ptr monotone and inside [0, nnz], columns in range and
+// strictly increasing within the row (the host validator's checks)
+__global__ void k_validate_rows(const int32_t* rp, const int32_t* ci, int nrows, int ncols,
+                                int64_t nnz, int* flags) {
+  const int lane = threadIdx.x & 31;
+  int f = 0;
+  for (int64_t r = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; r < nrows;
+       r += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const int32_t a = rp[r], b = rp[r + 1];
+    if (b < a || a < 0 || int64_t(b) > nnz) {
+      f |= kCsrBadRowPtr;
+      continue;
+    }
+    for (int32_t e = a + lane; e < b; e += 32) {
+      const int32_t c = ci[e];
+      if (c < 0 || c >= ncols) f |= kCsrBadColumn;
+      if (e > a && c <= ci[e - 1]) f |= kCsrUnsorted;
+    }
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (lane == 0 && f) atomicOr(flags, f);
+}
+
+__global__ void k_validate_vals(const double* v, int64_t nnz, int* flags) {
+  int f = 0;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nnz;
+       e += int64_t(gridDim.x) * blockDim.x)
+    if (v[e] != 0.0) f = kCsrNonzero;
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+__global__ void k_validate_bounds(const double* l, const double* u, int n, int* flags) {
+  int f = 0;
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n;
+       j += int64_t(gridDim.x) * blockDim.x)
+    if (l[j] > u[j]) f = kBoundsBad;
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
 // first index in [lo, hi) with ci >= c (rows sorted by column)
 __device__ __forceinline__ int32_t lower(const int32_t* ci, int32_t lo, int32_t hi, int64_t c) {
   while (lo < hi) {
@@ -172,6 +213,42 @@ T* tmp(DevBuf& b, size_t count) {
 }
 
 }  // namespace
+
+// The O(nnz) input checks on the uploaded CSR (validate_problem_deep's, in
+// the same priority order) and the all-zero test of power_iteration_norm.
+void Problem::device_validate(const CsrStore& st, int nrows, int ncols, int64_t nnz) {
+  cudaStream_t s = stream_;
+  DevBuf bf;
+  int* flags = tmp<int>(bf, 1);
+  AAPDHG_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), s));
+  if (nrows > 0)
+    k_validate_rows<<<blocks_for(int64_t(nrows) * 32), kT, 0, s>>>(
+        st.rp.as<int32_t>(), st.ci.as<int32_t>(), nrows, ncols, nnz, flags);
+  if (nnz > 0)
+    k_validate_vals<<<std::min(blocks_for(nnz), 148 * 8), kT, 0, s>>>(st.v.as<double>(), nnz,
+                                                                     flags);
+  AAPDHG_CUDA(cudaGetLastError());
+  int h = 0;
+  AAPDHG_CUDA(cudaMemcpyAsync(&h, flags, sizeof h, cudaMemcpyDeviceToHost, s));
+  AAPDHG_CUDA(cudaStreamSynchronize(s));
+  if (const char* msg = csr_flag_message(h)) throw StatusError(AAPDHG_ERR_DIMENSION, msg);
+  if (shard_rank_ < 0) all_zero_ = !(h & kCsrNonzero);  // a shard's comes from the whole LP
+}
+
+void Problem::device_flags_vectors() {
+  cudaStream_t s = stream_;
+  DevBuf bf;
+  int* flags = tmp<int>(bf, 1);
+  AAPDHG_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), s));
+  if (n_ > 0)
+    k_validate_bounds<<<std::min(blocks_for(n_), 148 * 8), kT, 0, s>>>(l_.as<double>(),
+                                                                      u_.as<double>(), n_, flags);
+  AAPDHG_CUDA(cudaGetLastError());
+  int h = 0;
+  AAPDHG_CUDA(cudaMemcpyAsync(&h, flags, sizeof h, cudaMemcpyDeviceToHost, s));
+  AAPDHG_CUDA(cudaStreamSynchronize(s));
+  bounds_ok_ = !(h & kBoundsBad);
+}
 
 // exclusive scan of n int32 counts into out[0..n] (out[n] = total); returns total
 static int64_t scan_counts(const int32_t* cnt, int n, int32_t* out, cudaStream_t s) {

@@ -5,6 +5,12 @@ m=10): iterations until max KKT <= 1e-6 (kkt_terminate, the metric's
 order. All arms use the reference's own step size (select_step_sizes).
   python profiles/exp_config1_kkt.py ref|ref-fast|ref-assoc   (CPU: ~30 min each)
   python profiles/exp_config1_kkt.py gpu                       (the B200 arms)
+  python profiles/exp_config1_kkt.py ref@+1 ref@-2 ...         (the reference at tau shifted
+                                                                by +1 / -2 ulp: the spread of
+                                                                its own count under a last-bit
+                                                                change of tau)
+  python profiles/exp_config1_kkt.py gpu@-3:3                  (the B200 TREE arm at each
+                                                                shift in -3..3 ulp)
 Each arm prints one JSON line."""
 import json
 import sys
@@ -29,9 +35,37 @@ def row(arm, r, dt):
             "kkt": [r.result.kkt.r_gap, r.result.kkt.r_primal, r.result.kkt.r_dual], "seconds": dt}
 
 
+def shifted(tau, ulps):
+    import numpy as np
+    for _ in range(abs(ulps)):
+        tau = float(np.nextafter(tau, np.inf if ulps > 0 else -np.inf))
+    return tau
+
+
 def main():
     arm = sys.argv[1]
     p = problems.make_config(1)
+    if arm.startswith("gpu@"):
+        from paper_2508_08062_b200 import Solver
+        lo, hi = (int(v) for v in arm[4:].split(":"))
+        with Solver(p) as s:
+            tau0 = s.select_step_sizes(SolverConfig(reduction="serial")).tau
+            for u in range(lo, hi + 1):
+                tau = shifted(tau0, u)
+                t0 = time.perf_counter()
+                r = s.solve(cfg(tau, "tree"))
+                print(json.dumps(dict(row(f"gpu-tree@{u:+d}", r, time.perf_counter() - t0),
+                                      tau=tau)), flush=True)
+        return
+    if "@" in arm:
+        from oracle.pyoracle import Oracle
+        kind, u = arm.split("@")
+        orc = Oracle(kind)
+        tau = shifted(orc.select_step_sizes(p, SolverConfig()).tau, int(u))
+        t0 = time.perf_counter()
+        r = orc.solve(p, cfg(tau))
+        print(json.dumps(dict(row(arm, r, time.perf_counter() - t0), tau=tau)), flush=True)
+        return
     if arm == "gpu":
         from paper_2508_08062_b200 import Solver
         with Solver(p) as s:
