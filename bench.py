@@ -40,6 +40,19 @@ GATHER_CEILING = 240.3e9  # measured random-gather rate (profiles/r01/gather.txt
 METRIC = "AA-PDHG fp64 iterations/sec (BASELINE configs[1]: 100k x 200k, 4M nnz, m=10)"
 
 
+def host_cpu():
+    """'<N>-core <model>' of this host (the CPU baseline's machine)."""
+    model = "unknown CPU"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{os.cpu_count()}-core {model}"
+
+
 def workload_config(p):
     return {"workload": "configs[1] planted LP 100000x200000, 20 nnz/col (4.0M nnz), "
                         "AA-PDHG m=10, D=1, eps=1, toll=1e-6",
@@ -172,9 +185,12 @@ def run_reference_arm(args, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded planted-optimum generator, SURVEY.md 8(d))",
             "config": workload_config(p), "impl": "reference",
+            "parallelism": "single (the reference solve is single-threaded)",
             "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": 1, "kind": kind,
+                             "host": host_cpu(),
                              "sample": f"{out.result.iterations} iterations of configs[1] "
-                                       f"(explicit tau, single-threaded solve())"},
+                                       f"(explicit tau), 1 thread on a {host_cpu()}: the "
+                                       f"reference solve() is single-threaded"},
             "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -354,8 +370,10 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         v, kind, dt = cpu_reference_sample(p, tau, args.cpu_iters)
         cpu = {"value": v, "unit": "iterations/s", "cores": 1, "kind": kind,
+               "host": host_cpu(),
                "sample": f"{args.cpu_iters} iterations of configs[1] (explicit tau), "
-                         f"{dt:.1f} s, single-threaded reference solve()"}
+                         f"{dt:.1f} s, 1 thread on a {host_cpu()}: the reference "
+                         f"solve() is single-threaded"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
@@ -363,10 +381,10 @@ def run_ours(args, rank, world, local_rank):
                 "higher_is_better": True, "scaling": "strong" if dist else "weak",
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded planted-optimum generator, SURVEY.md 8(d))",
-                "config": dict(workload_config(p),
-                               parallelism=f"shard{world} (row/column blocks, "
-                                           f"{'peer-memory stores + flag barriers' if args.transport == 'p2p' else args.transport})"
-                               if dist else "single"),
+                "config": workload_config(p),
+                "parallelism": (f"shard{world} (row/column blocks, "
+                                f"{'peer-memory stores + flag barriers' if args.transport == 'p2p' else args.transport})"
+                                if dist else "single"),
                 "iterations_timed": iters, "aa_steps_timed": out.result.i,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt,
                 "clocks": clk.summary(), "gpu_launches": int(launches.value),
@@ -486,9 +504,11 @@ def main():
                     help="ncu dram bytes per launch of the dominant kernel, if captured")
     args = ap.parse_args()
     if args.impl == "reference":
+        # bounded CPU sample: <= 500 iterations (~20 s of reference work at
+        # ~40 ms per iteration); the driver's --steps 20 --warmup 5 run as given
         args.warmup = max(args.warmup, 0)
-        args.steps = min(args.steps, 20)  # bounded CPU sample (~2 s of work)
-        args.warmup = min(args.warmup, 3)
+        args.steps = min(args.steps, 500)
+        args.warmup = min(args.warmup, 50)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

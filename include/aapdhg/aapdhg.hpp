@@ -13,7 +13,7 @@
 //   AAParams          proj/include/aapdhg/anderson.hpp:21-25
 //   FilterParams      proj/include/aapdhg/filtering.hpp:14-17
 //   solver types/API  proj/include/aapdhg/solver.hpp:15-99
-//   report            proj/include/aapdhg/report.hpp:11-20
+//   report            proj/include/aapdhg/report.hpp:11-20 (in aapdhg/report.hpp)
 // Every numeric entry point runs on the sm_100a library through the C-ABI in
 // aapdhg_cuda.h; there is no CPU fallback.
 #pragma once
@@ -180,6 +180,68 @@ struct FilterParams {
   double kappa_bar = 1e9;
 };
 
+// ---- Anderson memory, anderson.hpp:12-48 -------------------------------------------
+// Columns oldest to newest, equal counts, at most `capacity` pairs.
+struct AAMemory {
+  std::vector<Vec> du_cols;
+  std::vector<Vec> dg_cols;
+  std::size_t capacity = 5;
+  std::size_t size() const { return du_cols.size(); }
+  bool empty() const { return du_cols.empty(); }
+};
+
+// Appends at the newest end, evicts the oldest beyond capacity.
+void memory_push(AAMemory& mem, Vec du, Vec dg);
+// beta * Dhat * v (empty d_hat: identity).
+Vec damp(const AAParams& params, const Vec& v);
+// The accelerated candidate u - H g (anderson.hpp:36-41), on the device
+// (aapdhg_cuda_aa_apply: the regularised Gram, Cholesky and mix of the solve
+// loop). Throws SingularError when the normal equations are not PD.
+Vec aa_apply(const AAMemory& mem, const AAParams& params, const Vec& u, const Vec& g);
+// Alg-1 test oracles (anderson.hpp:43-48): affine weights minimising
+// ||sum alpha_i r_i|| with sum alpha = 1 (minimum-norm solution for a
+// degenerate Gram), and (1-beta) sum alpha_i points_i + beta sum alpha_i images_i.
+Vec standard_aa_weights(const std::vector<Vec>& residuals);
+Vec standard_aa_step(const std::vector<Vec>& points, const std::vector<Vec>& images,
+                     const Vec& weights, double beta);
+
+// ---- QR, sparse_linalg.hpp:60-72 -------------------------------------------------------
+struct QRFactors {
+  DenseMatrix q;  // n x p, orthonormal columns
+  DenseMatrix r;  // p x p, upper triangular, nonnegative diagonal
+};
+// On the device: R from the double-double Gram F'F (aapdhg_cuda_economy_qr),
+// Q = F R^{-1}. p <= n (DimensionError otherwise); SingularError for
+// rank-deficient columns.
+QRFactors economy_qr(const DenseMatrix& f);
+// R X = B for upper-triangular R; SingularError when a diagonal entry is
+// <= 1e-14 ||R||_F.
+DenseMatrix back_substitute(const DenseMatrix& r, const DenseMatrix& b);
+Vec back_substitute(const DenseMatrix& r, const Vec& b);
+
+// ---- FAA filtering, filtering.hpp:14-59 -------------------------------------------
+using ColumnList = std::vector<Vec>;
+
+struct FilteredMemory {
+  ColumnList e;  // iterate differences
+  ColumnList f;  // residual differences
+  QRFactors qr;  // economy QR of f
+  std::size_t size() const { return f.size(); }
+  bool empty() const { return f.empty(); }
+};
+
+std::pair<ColumnList, ColumnList> reverse_columns(ColumnList e, ColumnList f);
+// The kept sets below come from the device FAA step (aapdhg_cuda_faa_op).
+std::pair<ColumnList, ColumnList> angle_filter(ColumnList e, ColumnList f, double c_s);
+Vec length_bounds(const ColumnList& f, double c_s);
+std::pair<ColumnList, ColumnList> length_filter(ColumnList e, ColumnList f, double c_s,
+                                                double kappa_bar);
+FilteredMemory build_filtered_memory(ColumnList e, ColumnList f, const FilterParams& params);
+// w = R^{-1} Q'g (as the least squares of the kept f, on the device), then
+// u + beta Dhat g - sum_j (e_j + beta Dhat f_j) w_j.
+Vec filtered_aa_apply(const FilteredMemory& fm, const AAParams& params, const Vec& u,
+                      const Vec& g);
+
 // ---- solver ------------------------------------------------------------------
 enum class Method { kPdhg, kAaPdhg, kFaaPdhg };
 
@@ -295,11 +357,8 @@ std::vector<SweepOutcome> solve_sweep(const ProblemData& p, const std::vector<Sw
                                       std::size_t workers = 0,
                                       const std::vector<int>& devices = {0});
 
-// ---- report ------------------------------------------------------------------
-const char* status_name(SolveStatus s);
-const char* method_name(Method m);
-std::string trajectory_csv(const std::vector<TrajectoryRecord>& records);
-std::string summary_json(const SolveResult& result, const SolverConfig& cfg,
-                         const ProblemData& p);
+// (report: status_name / method_name / trajectory_csv / summary_json are
+// declared in aapdhg/report.hpp only, as in the reference — code that does
+// not include it may define its own status_name, e.g. acceptance_test.cpp)
 
 }  // namespace aapdhg

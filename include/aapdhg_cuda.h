@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define AAPDHG_ABI_VERSION 2
+#define AAPDHG_ABI_VERSION 3
 
 /* Error codes (errors.hpp:8-30). */
 typedef enum aapdhg_status {
@@ -276,6 +276,35 @@ int aapdhg_cuda_filtered_aa_apply(aapdhg_handle* h, int32_t reduction,
                                   const double* d_hat, const double* u,
                                   const double* g, double* out, int32_t* kept,
                                   char* err, size_t errlen);
+
+/* A handle for the per-op AA / FAA entries on vectors of length n (no LP:
+ * the C++ drop-in's aa_apply / angle_filter / economy_qr ... of
+ * anderson.hpp, filtering.hpp and sparse_linalg.hpp work on bare columns).
+ * Destroy with aapdhg_cuda_problem_destroy. */
+int aapdhg_cuda_workspace_create(int32_t device, int64_t n, aapdhg_handle** out, char* err,
+                                 size_t errlen);
+
+/* FAA steps of build_filtered_memory + filtered_aa_apply (filtering.hpp:
+ * 20-59) on p columns (oldest first), with stages skipped by `skip`
+ * (1: the angle filter, 2: the length filter). kept[p] receives the kept
+ * set; when out is non-null the candidate u + beta Dhat g - sum w_j (e_j +
+ * beta Dhat f_j) is formed (w from the double-double least squares of the
+ * kept f). Replaces angle_filter / length_filter / build_filtered_memory's
+ * selection and filtered_aa_apply (filtering.cpp:61-181). e_cols may be
+ * null when only the kept set is wanted. */
+int aapdhg_cuda_faa_op(aapdhg_handle* h, int32_t reduction, int32_t p, const double* e_cols,
+                       const double* f_cols, double c_s, double kappa_bar, double beta,
+                       const double* d_hat, int32_t skip, const double* u, const double* g,
+                       double* out, int32_t* kept, char* err, size_t errlen);
+
+/* Replaces: QRFactors economy_qr(const DenseMatrix& f)
+ * (proj/include/aapdhg/sparse_linalg.hpp:67-69, sparse_linalg.cpp:131-192).
+ * f_cols: p columns of length n (the handle's n). R (p x p, column-major,
+ * upper, diag >= 0) from the Cholesky of the double-double Gram F'F; Q
+ * (n x p, column-major) = F R^{-1}. AAPDHG_ERR_SINGULAR for rank-deficient
+ * columns (the reference's Householder QR returns a zero r_ii there). */
+int aapdhg_cuda_economy_qr(aapdhg_handle* h, int32_t reduction, int32_t p, const double* f_cols,
+                           double* q_out, double* r_out, char* err, size_t errlen);
 
 /* ---- streams & instrumentation (bench / profiling) ---------------------- */
 

@@ -2,6 +2,7 @@
 // helpers of the sm_100a solver (see pipeline.cuh for the iteration core).
 #pragma once
 
+#include "dd.cuh"
 #include "pipeline.cuh"
 
 namespace aapdhg_b200 {
@@ -32,7 +33,17 @@ struct DotBufs {
   const double* gpool;
   double* part;     // items x ndot_blk (tree) or items (serial)
   int32_t max_items;
+  // FAA: the low parts of double-double partials (dd.cuh), same layout;
+  // null for AA (whose reference solve is itself the Gram's Cholesky)
+  double* part_lo = nullptr;
 };
+
+// index-ordered Dot2 chain (FAA, SERIAL order)
+__device__ __forceinline__ dd serial_dot_dd(const double* a, const double* b, int64_t n) {
+  double hi = 0.0, lo = 0.0;
+  for (int64_t t = 0; t < n; ++t) dot2_acc(hi, lo, a[t], b[t]);
+  return dd_norm(hi, lo);
+}
 
 __device__ __forceinline__ void item_vectors(const DotBufs& D, const DevParams* P,
                                              const DevState* S, int item, int p,
@@ -55,7 +66,13 @@ __global__ void k_serial_dots(DotBufs D, const DevParams* __restrict__ P, const 
   if (item >= num_items(p, P->method)) return;
   const double *va, *vb;
   item_vectors(D, P, S, item, p, va, vb);
-  D.part[item] = serial_dot(va, vb, P->N);
+  if (D.part_lo) {
+    const dd v = serial_dot_dd(va, vb, P->N);
+    D.part[item] = v.hi;
+    D.part_lo[item] = v.lo;
+  } else {
+    D.part[item] = serial_dot(va, vb, P->N);
+  }
 }
 
 // TREE: CTA b covers elements [b*kDotChunk, ...); warp w takes items w, w+8..
@@ -95,6 +112,18 @@ __global__ void __launch_bounds__(kThreads)
       x[u] = t < cnt ? va[base + t] : 0.0;
       y[u] = t < cnt ? vb[base + t] : 0.0;
     }
+    if (D.part_lo) {  // FAA: double-double partials
+      double hi = 0.0, lo = 0.0;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u)
+        if (lane + 32 * u < cnt) dot2_acc(hi, lo, x[u], y[u]);
+      const dd v = warp_sum_dd(dd_norm(hi, lo));
+      if (lane == 0) {
+        D.part[(int64_t)item * P->ndot_blk + blockIdx.x] = v.hi;
+        D.part_lo[(int64_t)item * P->ndot_blk + blockIdx.x] = v.lo;
+      }
+      continue;
+    }
     double s = 0.0;
 #pragma unroll
     for (int u = 0; u < kPer; ++u)
@@ -103,6 +132,20 @@ __global__ void __launch_bounds__(kThreads)
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     if (lane == 0) D.part[(int64_t)item * P->ndot_blk + blockIdx.x] = s;
   }
+}
+
+// CAP-space accumulator q of the register Gram -> p-space item (-1: unused):
+// q < NPAIR pairs (a <= b), then the rhs items, then the e-norms
+__device__ __forceinline__ int gram_item(int q, int cap, int p, int np) {
+  const int npair = cap * (cap + 1) / 2;
+  if (q < npair) {
+    int a = 0, rem = q;
+    while (rem >= cap - a) { rem -= cap - a; ++a; }
+    const int b = a + rem;
+    return b < p ? a * p - a * (a - 1) / 2 + (b - a) : -1;
+  }
+  if (q < npair + cap) return q - npair < p ? np + (q - npair) : -1;
+  return q - npair - cap < p ? np + p + (q - npair - cap) : -1;
 }
 
 // TREE, memory capacity <= CAP (<= 10): the whole Gram / rhs / column-norm
@@ -179,21 +222,112 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int q = threadIdx.x; q < NACC; q += blockDim.x) {
     double s = red[0][q];
     for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, red[w][q]);
-    int item = -1;
-    if (q < NPAIR) {  // (a, b) in CAP space -> p space
-      int a = 0, rem = q;
-      while (rem >= CAP - a) { rem -= CAP - a; ++a; }
-      const int b = a + rem;
-      if (b < p) item = a * p - a * (a - 1) / 2 + (b - a);
-    } else if (q < NPAIR + CAP) {
-      const int a = q - NPAIR;
-      if (a < p) item = np + a;
-    } else {
-      const int a = q - NPAIR - CAP;
-      if (a < p) item = np + p + a;
-    }
+    const int item = gram_item(q, CAP, p, np);
     if (item >= 0) D.part[(int64_t)item * gridDim.x + blockIdx.x] = s;
   }
+}
+
+// FAA, memory capacity <= CAP (<= 10): the Gram F'F and the rhs F'g as
+// double-double partials (Dot2, dd.cuh), the e-norms in double, in one pass
+// over the columns with g staged (k_stage_g). With SPLIT the dd items are
+// shared by a pair of CTAs over the same elements (CTA 2b: the even items,
+// 2b + 1: the odd ones and the e-norms), so each keeps half the
+// accumulators in registers (memory 8 and 10 would spill); the pair reads
+// the same columns at the same time, the second read hits L2.
+template <int CAP, int SPLIT>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gram_dots_dd(DotBufs D, double* __restrict__ upool, const DevParams* __restrict__ P,
+                   const DevState* S) {
+  if (S->done || !S->aa_attempt) return;
+  constexpr int NPAIR = CAP * (CAP + 1) / 2;
+  constexpr int NDD = NPAIR + CAP;                        // Gram + rhs items (dd)
+  constexpr int NH = SPLIT ? (NDD + 1) / 2 : NDD;         // this CTA's dd items
+  const int half = SPLIT ? int(blockIdx.x & 1) : 0;
+  const int eblk = SPLIT ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int nblk = SPLIT ? int(gridDim.x >> 1) : int(gridDim.x);
+  const bool enorms = !SPLIT || half == 1;
+  __shared__ int64_t soff[CAP];
+  __shared__ int sh_p, sh_g, sh_h, sh_c;
+  if (threadIdx.x == 0) {
+    sh_p = S->mem_size;
+    sh_g = S->g_idx[G_CUR];
+    sh_h = S->u_idx[U_HAT];
+    sh_c = S->u_idx[U_CUR];
+  }
+  __syncthreads();
+  const int p = sh_p;
+  const int64_t N = P->N;
+  if (threadIdx.x < CAP)
+    soff[threadIdx.x] = (int64_t)(int(threadIdx.x) < p ? S->mem_slots[threadIdx.x] : 0) * N;
+  __syncthreads();
+  const double* uh = upool + (int64_t)sh_h * N;
+  const double* uc = upool + (int64_t)sh_c * N;
+  double* g = const_cast<double*>(D.gpool) + (int64_t)sh_g * N;
+  double hi[NH], lo[NH], en[CAP];
+#pragma unroll
+  for (int k = 0; k < NH; ++k) hi[k] = lo[k] = 0.0;
+#pragma unroll
+  for (int a = 0; a < CAP; ++a) en[a] = 0.0;
+  for (int64_t t = (int64_t)eblk * blockDim.x + threadIdx.x; t < N;
+       t += (int64_t)nblk * blockDim.x) {
+    const double gt = __dsub_rn(uh[t], uc[t]);
+    if (half == 0) g[t] = gt;
+    double v[CAP];
+#pragma unroll
+    for (int a = 0; a < CAP; ++a) v[a] = a < p ? D.dg[soff[a] + t] : 0.0;
+    int q = 0;
+#pragma unroll
+    for (int a = 0; a < CAP; ++a)
+#pragma unroll
+      for (int b = a; b < CAP; ++b, ++q)
+        if (!SPLIT || (q & 1) == half) dot2_acc(hi[q >> SPLIT], lo[q >> SPLIT], v[a], v[b]);
+#pragma unroll
+    for (int a = 0; a < CAP; ++a, ++q)
+      if (!SPLIT || (q & 1) == half) dot2_acc(hi[q >> SPLIT], lo[q >> SPLIT], v[a], gt);
+    if (enorms) {
+#pragma unroll
+      for (int a = 0; a < CAP; ++a) {
+        const double e = a < p ? D.du[soff[a] + t] : 0.0;
+        en[a] = __dadd_rn(en[a], __dmul_rn(e, e));
+      }
+    }
+  }
+  // fixed-shape CTA reduction: warp xor trees, then the warps in order
+  __shared__ double red_hi[kWarps][NH], red_lo[kWarps][NH], red_en[kWarps][CAP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < NH; ++k) {
+    const dd sv = warp_sum_dd(dd_norm(hi[k], lo[k]));
+    if (lane == 0) {
+      red_hi[warp][k] = sv.hi;
+      red_lo[warp][k] = sv.lo;
+    }
+  }
+  if (enorms) {
+#pragma unroll
+    for (int a = 0; a < CAP; ++a) {
+      const double sv = warp_sum(en[a]);
+      if (lane == 0) red_en[warp][a] = sv;
+    }
+  }
+  __syncthreads();
+  const int np = p * (p + 1) / 2;
+  for (int k = threadIdx.x; k < NH; k += blockDim.x) {
+    const int q = SPLIT ? 2 * k + half : k;
+    if (q >= NDD) continue;
+    dd sd = dd{red_hi[0][k], red_lo[0][k]};
+    for (int w = 1; w < kWarps; ++w) sd = dd_add(sd, dd{red_hi[w][k], red_lo[w][k]});
+    const int item = gram_item(q, CAP, p, np);
+    if (item < 0) continue;
+    D.part[(int64_t)item * nblk + eblk] = sd.hi;
+    D.part_lo[(int64_t)item * nblk + eblk] = sd.lo;
+  }
+  if (enorms)
+    for (int a = threadIdx.x; a < p; a += blockDim.x) {
+      double sv = red_en[0][a];
+      for (int w = 1; w < kWarps; ++w) sv = __dadd_rn(sv, red_en[w][a]);
+      D.part[(int64_t)(np + p + a) * nblk + eblk] = sv;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -325,6 +459,11 @@ __global__ void __launch_bounds__(1024)
   const int p = S->mem_size;
   const int nit = num_items(p, P->method);
   __shared__ double vals[kMaxMemory * (kMaxMemory + 1) / 2 + 2 * kMaxMemory];
+  // FAA: the low parts of the Gram / rhs items (double-double, dd.cuh)
+  __shared__ double vlo[kMaxMemory * (kMaxMemory + 1) / 2 + kMaxMemory];
+  const int ndd = (P->method == AAPDHG_METHOD_FAA && D.part_lo) ? p * (p + 1) / 2 + p : 0;
+  for (int it = threadIdx.x; it < p * (p + 1) / 2 + p; it += blockDim.x) vlo[it] = 0.0;
+  __syncthreads();
   if (rank_tot) {  // sharded: per-shard totals summed in rank order
     for (int it = threadIdx.x; it < nit; it += blockDim.x) {
       double s = rank_tot[it];
@@ -332,7 +471,27 @@ __global__ void __launch_bounds__(1024)
       vals[it] = s;
     }
   } else if (P->serial) {
-    for (int it = threadIdx.x; it < nit; it += blockDim.x) vals[it] = D.part[it];
+    for (int it = threadIdx.x; it < nit; it += blockDim.x) {
+      vals[it] = D.part[it];
+      if (it < ndd) vlo[it] = D.part_lo[it];
+    }
+  } else if (ndd > 0) {
+    // FAA: warp per item, the CTAs' double-double partials added in a fixed
+    // shape (lane-strided, then the xor tree)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int it = warp; it < nit; it += nw) {
+      const double* pp = D.part + (int64_t)it * P->ndot_blk;
+      const double* pl = D.part_lo + (int64_t)it * P->ndot_blk;
+      const bool two = it < ndd;
+      dd s = {0.0, 0.0};
+      for (int b = lane; b < P->ndot_blk; b += 32)
+        s = dd_add(s, dd{__ldcg(pp + b), two ? __ldcg(pl + b) : 0.0});
+      s = warp_sum_dd(s);
+      if (lane == 0) {
+        vals[it] = s.hi;
+        if (two) vlo[it] = s.lo;
+      }
+    }
   } else {
     // warp per item, lanes stride over the CTAs' partials, fixed tree
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -381,6 +540,172 @@ __global__ void __launch_bounds__(1024)
     if (threadIdx.x == 0) aa_solved = solved ? 1 : 0;
     __syncthreads();
   }
+  // FAA (filtering.cpp:140-181): angle filter on the newest-first order,
+  // length filter, then the least-squares weights of the kept columns, all
+  // from the double-double Gram F'F and rhs F'g (dd.cuh) by the whole CTA:
+  //   * the angle filter's |R(j,j)| / ||f_j|| is the Householder QR diagonal
+  //     of the reversed F (qr_diagonal, filtering.cpp:25-50): the Cholesky
+  //     factor of the reversed Gram, row by row; a dependent column (pivot
+  //     <= 0) gets a zero diagonal and a zero row, like a skipped reflection;
+  //   * w = R^{-1} R^{-T} F'g with R'R = F_kept'F_kept (= R^{-1} Q'g of the
+  //     economy QR, sparse_linalg.cpp:131-227, with the 1e-14 ||R||_F
+  //     singularity floor of back_substitute).
+  __shared__ int faa_ok, faa_kk;
+  __shared__ int faa_kpos[kMaxMemory];
+  __shared__ double faa_w[kMaxMemory];
+  if (P->method == AAPDHG_METHOD_FAA) {
+    double* Rh = W.work;            // p x p row-major (angle filter), then kk x kk
+    double* Rl = W.work + P->cap * P->cap;  // its low parts (third cap^2 block, aa_smem)
+    __shared__ double dsh_hi, dsh_lo;
+    __shared__ int keep[kMaxMemory];
+    auto gdd = [&](int r, int c) {  // Gram item (r, c) as double-double
+      const int lo = r < c ? r : c, hi = r < c ? c : r;
+      const int it = lo * p - lo * (lo - 1) / 2 + (hi - lo);
+      return dd{vals[it], vlo[it]};
+    };
+    if (threadIdx.x == 0) faa_ok = 1;
+    __syncthreads();
+    for (int j = 0; j < p; ++j) {
+      const int gj = p - 1 - j;
+      if (threadIdx.x == 0) {
+        dd d = gdd(gj, gj);
+        for (int k = 0; k < j; ++k) {
+          const dd r = dd{Rh[k * p + j], Rl[k * p + j]};
+          d = dd_sub(d, dd_mul(r, r));
+        }
+        const dd rjj = d.hi > 0.0 ? dd_sqrt(d) : dd{0.0, 0.0};
+        Rh[j * p + j] = rjj.hi;
+        Rl[j * p + j] = rjj.lo;
+        dsh_hi = rjj.hi;
+        dsh_lo = rjj.lo;
+        const dd fn = dd_sqrt(gdd(gj, gj));
+        const double sine =
+            ((int64_t)j < P->Nglob && fn.hi > 0.0) ? dd_div(rjj, fn).hi : 0.0;
+        keep[j] = 1;
+        if (P->faa_skip & kFaaSkipAngle) {
+          // (per-op length_filter / QR: every column goes on)
+        } else if (j == 0) {
+          if (fn.hi == 0.0) faa_ok = 0;  // zero leading column -> SingularError
+        } else if (sine < P->c_s) {
+          keep[j] = 0;
+        }
+      }
+      __syncthreads();
+      const dd rjj = dd{dsh_hi, dsh_lo};
+      for (int i2 = j + 1 + int(threadIdx.x); i2 < p; i2 += blockDim.x) {
+        const int gi = p - 1 - i2;
+        dd sv = gdd(gi, gj);
+        for (int k = 0; k < j; ++k)
+          sv = dd_sub(sv, dd_mul(dd{Rh[k * p + j], Rl[k * p + j]}, dd{Rh[k * p + i2], Rl[k * p + i2]}));
+        const dd r = rjj.hi > 0.0 ? dd_div(sv, rjj) : dd{0.0, 0.0};
+        Rh[j * p + i2] = r.hi;
+        Rl[j * p + i2] = r.lo;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      int kk = 0;
+      if (faa_ok) {
+        // length filter over the kept columns (newest first), filtering.cpp:116-138
+        const double* en2 = vals + npair + p;
+        int idx[kMaxMemory];
+        int m = 0;
+        for (int t = 0; t < p; ++t)
+          if (keep[t]) idx[m++] = p - 1 - t;  // memory positions, newest first
+        double* fn_sq = W.vec + 3 * kMaxMemory;
+        double* bb = W.vec + 4 * kMaxMemory;
+        for (int t = 0; t < m; ++t) fn_sq[t] = vals[idx[t] * p - idx[t] * (idx[t] - 1) / 2];
+        dev_length_bounds(m, fn_sq, P->c_s, bb);
+        double ep = 0.0, bp = 0.0;
+        const double cap = __dmul_rn(P->kappa_bar, P->kappa_bar);
+        double epre[kMaxMemory + 1], bpre[kMaxMemory + 1];
+        epre[0] = bpre[0] = 0.0;
+        for (int t = 0; t < m; ++t) {
+          ep = __dadd_rn(ep, en2[idx[t]]);
+          bp = __dadd_rn(bp, bb[t]);
+          epre[t + 1] = ep;
+          bpre[t + 1] = bp;
+        }
+        if (P->faa_skip & kFaaSkipLength) kk = m;
+        else
+          for (int t = m; t >= 1; --t)
+            if (__dmul_rn(epre[t], bpre[t]) <= cap) { kk = t; break; }
+        // kept positions back in memory (oldest-first) order
+        for (int t = 0; t < kk; ++t) faa_kpos[t] = idx[kk - 1 - t];
+      }
+      faa_kk = kk;
+    }
+    __syncthreads();
+    const int kk = faa_kk;
+    if (faa_ok && kk > 0) {
+      // R'R = G_kept (upper R, row-major kk x kk), the whole CTA per column
+      for (int j = 0; j < kk; ++j) {
+        if (threadIdx.x == 0) {
+          dd d = gdd(faa_kpos[j], faa_kpos[j]);
+          for (int k = 0; k < j; ++k) {
+            const dd r = dd{Rh[k * kk + j], Rl[k * kk + j]};
+            d = dd_sub(d, dd_mul(r, r));
+          }
+          if (!(d.hi > 0.0)) {
+            faa_ok = 0;
+            d = dd{1.0, 0.0};
+          }
+          const dd r = dd_sqrt(d);
+          Rh[j * kk + j] = r.hi;
+          Rl[j * kk + j] = r.lo;
+          dsh_hi = r.hi;
+          dsh_lo = r.lo;
+        }
+        __syncthreads();
+        if (!faa_ok) break;
+        const dd rjj = dd{dsh_hi, dsh_lo};
+        for (int i2 = j + 1 + int(threadIdx.x); i2 < kk; i2 += blockDim.x) {
+          dd sv = gdd(faa_kpos[i2], faa_kpos[j]);
+          for (int k = 0; k < j; ++k)
+            sv = dd_sub(sv, dd_mul(dd{Rh[k * kk + j], Rl[k * kk + j]},
+                                   dd{Rh[k * kk + i2], Rl[k * kk + i2]}));
+          const dd r = dd_div(sv, rjj);
+          Rh[j * kk + i2] = r.hi;
+          Rl[j * kk + i2] = r.lo;
+        }
+        __syncthreads();
+      }
+      if (threadIdx.x == 0 && faa_ok) {
+        // back_substitute floor: |r_ii| <= 1e-14 ||R||_F -> SingularError
+        double fro = 0.0;
+        for (int j = 0; j < kk; ++j)
+          for (int i2 = j; i2 < kk; ++i2) fro = __dadd_rn(fro, __dmul_rn(Rh[j * kk + i2], Rh[j * kk + i2]));
+        const double floor_v = 1e-14 * sqrt(fro);
+        for (int i2 = 0; i2 < kk; ++i2)
+          if (fabs(Rh[i2 * kk + i2]) <= floor_v) faa_ok = 0;
+        if (faa_ok) {
+          // forward R' z = F'g, back R w = z, in double-double
+          dd z[kMaxMemory];
+          for (int i2 = 0; i2 < kk; ++i2) {
+            const int it = npair + faa_kpos[i2];
+            dd sv = dd{vals[it], vlo[it]};
+            for (int k2 = 0; k2 < i2; ++k2)
+              sv = dd_sub(sv, dd_mul(dd{Rh[k2 * kk + i2], Rl[k2 * kk + i2]}, z[k2]));
+            z[i2] = dd_div(sv, dd{Rh[i2 * kk + i2], Rl[i2 * kk + i2]});
+          }
+          for (int i2 = kk - 1; i2 >= 0; --i2) {
+            dd sv = z[i2];
+            for (int k2 = i2 + 1; k2 < kk; ++k2)
+              sv = dd_sub(sv, dd_mul(dd{Rh[i2 * kk + k2], Rl[i2 * kk + k2]}, z[k2]));
+            z[i2] = dd_div(sv, dd{Rh[i2 * kk + i2], Rl[i2 * kk + i2]});
+          }
+          for (int i2 = 0; i2 < kk; ++i2) faa_w[i2] = z[i2].hi;
+        }
+      }
+      // per-op economy_qr: R of the kept columns (column-major, diag >= 0)
+      if (P->qr_r_out && faa_ok)
+        for (int t = threadIdx.x; t < kk * kk; t += blockDim.x) {
+          const int r = t % kk, c = t / kk;
+          P->qr_r_out[t] = r <= c ? Rh[r * kk + c] : 0.0;
+        }
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
   const double* rhs = vals + npair;
   double* w = W.vec;  // p
@@ -393,109 +718,17 @@ __global__ void __launch_bounds__(1024)
       for (int t = 0; t < p; ++t) S->mix_slots[t] = S->mem_slots[t];
     }
   } else {
-    const double* en2 = vals + npair + p;
-    // angle filter on the newest-first order: Gr(s,t) = G(p-1-s, p-1-t);
-    // upper R with R'R = Gr row by row; |R(j,j)| = |diag| of the Householder
-    // QR of the reversed F (qr_diagonal, filtering.cpp:25-50). Dependent
-    // columns (pivot <= 0) get a zero diagonal like a zero Householder step.
-    double* R = W.work;  // row-major p x p
-    int* keep = (int*)(W.vec + 2 * kMaxMemory);
-    for (int j = 0; j < p; ++j) {
-      const int gj = p - 1 - j;
-      double d = G[gj * p + gj];
-      for (int k = 0; k < j; ++k) d = __dsub_rn(d, __dmul_rn(R[k * p + j], R[k * p + j]));
-      const double rjj = d > 0.0 ? sqrt(d) : 0.0;
-      R[j * p + j] = rjj;
-      for (int i = j + 1; i < p; ++i) {
-        const int gi = p - 1 - i;
-        double s = G[gi * p + gj];
-        for (int k = 0; k < j; ++k) s = __dsub_rn(s, __dmul_rn(R[k * p + j], R[k * p + i]));
-        R[j * p + i] = rjj > 0.0 ? s / rjj : 0.0;
-      }
-      const double fn = sqrt(G[gj * p + gj]);
-      const double sine = ((int64_t)j < P->Nglob && fn > 0.0) ? rjj / fn : 0.0;
-      keep[j] = 1;
-      if (j == 0) {
-        if (fn == 0.0) ok = false;  // zero leading column -> SingularError
-        continue;
-      }
-      if (sine < P->c_s) keep[j] = 0;
-    }
+    // FAA: the CTA's double-double solve above
+    ok = faa_ok != 0;
+    const int kk = faa_kk;
+    pm = kk;
     if (ok) {
-      // length filter over kept (newest first)
-      int idx[kMaxMemory];
-      int m = 0;
-      for (int t = 0; t < p; ++t)
-        if (keep[t]) idx[m++] = p - 1 - t;  // memory positions, newest first
-      double* fn_sq = W.vec + 3 * kMaxMemory;
-      double* bb = W.vec + 4 * kMaxMemory;
-      for (int t = 0; t < m; ++t) fn_sq[t] = G[idx[t] * p + idx[t]];
-      dev_length_bounds(m, fn_sq, P->c_s, bb);
-      double ep = 0.0, bp = 0.0;
-      const double cap = __dmul_rn(P->kappa_bar, P->kappa_bar);
-      int kk = 0;
-      double epre[kMaxMemory + 1], bpre[kMaxMemory + 1];
-      epre[0] = bpre[0] = 0.0;
-      for (int t = 0; t < m; ++t) {
-        ep = __dadd_rn(ep, en2[idx[t]]);
-        bp = __dadd_rn(bp, bb[t]);
-        epre[t + 1] = ep;
-        bpre[t + 1] = bp;
-      }
-      for (int t = m; t >= 1; --t)
-        if (__dmul_rn(epre[t], bpre[t]) <= cap) { kk = t; break; }
-      // kept positions back in memory (oldest-first) order
-      int kpos[kMaxMemory];
-      for (int t = 0; t < kk; ++t) kpos[t] = idx[kk - 1 - t];
-      pm = kk;
-      if (kk > 0) {
-        // R = chol(F_kept' F_kept) (upper), then w = R^{-1} R^{-T} F'g
-        double* Rm = W.work;  // reuse (angle-filter R no longer needed)
-        for (int a = 0; a < kk; ++a)
-          for (int b = 0; b < kk; ++b) Rm[b * kk + a] = G[kpos[b] * p + kpos[a]];
-        // Cholesky: Rm lower = L, L L^T = Gk; R = L^T
-        for (int j = 0; j < kk && ok; ++j) {
-          double d = Rm[j * kk + j];
-          for (int k2 = 0; k2 < j; ++k2) d = __dsub_rn(d, __dmul_rn(Rm[k2 * kk + j], Rm[k2 * kk + j]));
-          if (d <= 0.0) { ok = false; break; }
-          d = sqrt(d);
-          Rm[j * kk + j] = d;
-          for (int i = j + 1; i < kk; ++i) {
-            double s = Rm[j * kk + i];
-            for (int k2 = 0; k2 < j; ++k2) s = __dsub_rn(s, __dmul_rn(Rm[k2 * kk + i], Rm[k2 * kk + j]));
-            Rm[j * kk + i] = s / d;
-          }
-        }
-        if (ok) {
-          // back_substitute floor: |r_ii| <= 1e-14 ||R||_F -> SingularError
-          double fro = 0.0;
-          for (int j = 0; j < kk; ++j)
-            for (int i = j; i < kk; ++i) fro = __dadd_rn(fro, __dmul_rn(Rm[j * kk + i], Rm[j * kk + i]));
-          const double floor_v = 1e-14 * sqrt(fro);
-          for (int i = 0; i < kk; ++i)
-            if (fabs(Rm[i * kk + i]) <= floor_v) ok = false;
-        }
-        if (ok) {
-          // forward: L z = F'g ; back: L^T w = z
-          for (int i = 0; i < kk; ++i) {
-            double s = rhs[kpos[i]];
-            for (int k2 = 0; k2 < i; ++k2) s = __dsub_rn(s, __dmul_rn(Rm[k2 * kk + i], w[k2]));
-            w[i] = s / Rm[i * kk + i];
-          }
-          for (int i = kk - 1; i >= 0; --i) {
-            double s = w[i];
-            for (int k2 = i + 1; k2 < kk; ++k2) s = __dsub_rn(s, __dmul_rn(Rm[i * kk + k2], w[k2]));
-            w[i] = s / Rm[i * kk + i];
-          }
-        }
-      }
-      if (ok) {
-        for (int t = 0; t < kk; ++t) S->mix_slots[t] = S->mem_slots[kpos[t]];
-        if (!per_op) {
-          // carried memory replaced only on success (solver.cpp:221-224)
-          for (int t = 0; t < kk; ++t) S->mem_slots[t] = S->mix_slots[t];
-          S->mem_size = kk;
-        }
+      for (int t = 0; t < kk; ++t) w[t] = faa_w[t];
+      for (int t = 0; t < kk; ++t) S->mix_slots[t] = S->mem_slots[faa_kpos[t]];
+      if (!per_op) {
+        // carried memory replaced only on success (solver.cpp:221-224)
+        for (int t = 0; t < kk; ++t) S->mem_slots[t] = S->mix_slots[t];
+        S->mem_size = kk;
       }
     }
   }
@@ -549,6 +782,27 @@ __global__ void __launch_bounds__(kThreads)
       else if (t - n < P->m1) o = smax(o, 0.0);
     }
     out[t] = o;
+  }
+}
+
+// economy_qr's Q = F R^{-1} (per-op): row t of Q solves q R = f_t by
+// forward substitution over R's columns (R upper, column-major kk x kk, in
+// shared memory); F's columns are the memory slots 0..kk-1 of dg.
+__global__ void __launch_bounds__(kThreads)
+    k_qr_q(const double* __restrict__ f, const double* __restrict__ r, int kk, int64_t N,
+           double* __restrict__ q) {
+  __shared__ double rs[kMaxMemory * kMaxMemory];
+  for (int t = threadIdx.x; t < kk * kk; t += blockDim.x) rs[t] = r[t];
+  __syncthreads();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double row[kMaxMemory];
+    for (int j = 0; j < kk; ++j) {
+      double s = f[(int64_t)j * N + t];
+      for (int k = 0; k < j; ++k) s = __dsub_rn(s, __dmul_rn(row[k], rs[j * kk + k]));
+      row[j] = s / rs[j * kk + j];
+      q[(int64_t)j * N + t] = row[j];
+    }
   }
 }
 

@@ -2,8 +2,10 @@
 // Exceptions never cross the boundary: they map onto aapdhg_status codes
 // (InputError / DimensionError / UnsupportedError / SingularError /
 // CUDA runtime errors) with the message copied into the caller's buffer.
+#include <algorithm>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "aapdhg_cuda.h"
 #include "engine.h"
@@ -265,6 +267,67 @@ int aapdhg_cuda_filtered_aa_apply(aapdhg_handle* h, int32_t reduction, int32_t p
     const int rc = h->prob->aa_apply(reduction, true, p, e_cols, f_cols, beta, d_hat, 0.0, c_s,
                                      kappa_bar, u, g, out, kept);
     if (rc == AAPDHG_ERR_SINGULAR) put_err(err, errlen, "filtered memory: singular");
+    return rc;
+  });
+}
+
+int aapdhg_cuda_workspace_create(int32_t device, int64_t n, aapdhg_handle** out, char* err,
+                                 size_t errlen) {
+  if (int rc = need(out, "workspace_create: null out", err, errlen)) return rc;
+  *out = nullptr;
+  if (n < 1 || n > (int64_t(1) << 31)) {
+    put_err(err, errlen, "workspace_create: vector length out of range");
+    return AAPDHG_ERR_DIMENSION;
+  }
+  return guard(err, errlen, [&] {
+    // a 1 x (n-1) LP with one unit entry: the per-op entries only use its
+    // n-vectors and history buffers
+    const int nc = int(n - 1);
+    int32_t rp[2] = {0, nc > 0 ? 1 : 0};
+    int32_t ci[1] = {0};
+    double v[1] = {1.0};
+    std::vector<double> zc(size_t(std::max(nc, 1)), 0.0), inf(size_t(std::max(nc, 1)), 1.0 / 0.0);
+    double q[1] = {1.0};
+    aapdhg_problem_view view{};
+    view.k = aapdhg_csr_view{1, nc, int64_t(rp[1]), rp, ci, v};
+    view.m1 = 0;
+    view.c = zc.data();
+    view.q = q;
+    view.l = zc.data();
+    view.u = inf.data();
+    auto* h = new aapdhg_handle{new Problem(&view, device), nullptr};
+    *out = h;
+    return AAPDHG_OK;
+  });
+}
+
+int aapdhg_cuda_faa_op(aapdhg_handle* h, int32_t reduction, int32_t p, const double* e_cols,
+                       const double* f_cols, double c_s, double kappa_bar, double beta,
+                       const double* d_hat, int32_t skip, const double* u, const double* g,
+                       double* out, int32_t* kept, char* err, size_t errlen) {
+  if (int rc = whole(h, "faa_op", err, errlen)) return rc;
+  if (int rc = need(h && (f_cols || p == 0) && (!out || (u && g)) ? h : nullptr,
+                    "faa_op: null argument", err, errlen))
+    return rc;
+  return guard(err, errlen, [&] {
+    const int rc = h->prob->aa_op(reduction, true, p, e_cols, f_cols, beta, d_hat, 0.0, c_s,
+                                  kappa_bar, skip, u, g, out, kept, nullptr, nullptr);
+    if (rc == AAPDHG_ERR_SINGULAR) put_err(err, errlen, "filtered memory: singular");
+    return rc;
+  });
+}
+
+int aapdhg_cuda_economy_qr(aapdhg_handle* h, int32_t reduction, int32_t p, const double* f_cols,
+                           double* q_out, double* r_out, char* err, size_t errlen) {
+  if (int rc = whole(h, "economy_qr", err, errlen)) return rc;
+  if (int rc = need(h && f_cols && q_out && r_out ? h : nullptr, "economy_qr: null argument", err,
+                    errlen))
+    return rc;
+  return guard(err, errlen, [&] {
+    const int rc = h->prob->aa_op(reduction, true, p, nullptr, f_cols, 1.0, nullptr, 0.0, 0.2,
+                                  1e300, aapdhg_b200::kFaaSkipAngle | aapdhg_b200::kFaaSkipLength,
+                                  nullptr, nullptr, nullptr, nullptr, r_out, q_out);
+    if (rc == AAPDHG_ERR_SINGULAR) put_err(err, errlen, "economy_qr: rank-deficient columns");
     return rc;
   });
 }

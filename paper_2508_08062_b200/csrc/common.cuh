@@ -127,7 +127,12 @@ struct DevParams {
   unsigned long long* flag_peer[kMaxPeers];
   unsigned long long* flag_own;
   int64_t Nglob;  // n + m of the whole LP (FAA's QR row-count test)
+  // per-op FAA entries (engine.cu faa_op): stages to skip (kFaaSkip*), and
+  // where to write the kept columns' R (p x p column-major) when non-null
+  int32_t faa_skip;
+  double* qr_r_out;
 };
+enum { kFaaSkipAngle = 1, kFaaSkipLength = 2 };
 
 // Mutable solver state, device resident; the host reads it at polls.
 struct DevState {

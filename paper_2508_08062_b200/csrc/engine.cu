@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
 #include <random>
 
 #include "engine.h"
@@ -201,7 +202,8 @@ static RowsumArgs rout(double* out) {
   return r;
 }
 
-size_t Problem::aa_smem(int cap) { return sizeof(double) * 2 * size_t(cap) * size_t(cap); }
+// k_aa_solve's dynamic shared memory: Gram, work (R) and R's low parts (FAA)
+size_t Problem::aa_smem(int cap) { return sizeof(double) * 3 * size_t(cap) * size_t(cap); }
 
 
 // ---------------------------------------------------------------------------
@@ -270,39 +272,67 @@ void transpose_csr(const aapdhg_csr_view& k, std::vector<int32_t>& trp, std::vec
     }
 }
 
+// Per-device one-time setup (the kernels' attributes are process state):
+// done once per device, not per handle.
+static std::mutex g_dev_mu;
+static bool g_dev_ready[64];
+static int g_dev_sms[64];
+
 void Problem::init_device(int device) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw CudaError("no CUDA device available (the sm_100a path has no CPU fallback)");
   if (device < 0 || device >= ndev) throw CudaError("device ordinal out of range");
   AAPDHG_CUDA(cudaSetDevice(device));
-  cudaDeviceProp prop;
-  AAPDHG_CUDA(cudaGetDeviceProperties(&prop, device));
-  if (prop.major < 10)
-    throw CudaError(std::string("device ") + prop.name + " is not sm_100 class");
+  {
+    std::lock_guard<std::mutex> g(g_dev_mu);
+    if (device >= 64 || !g_dev_ready[device]) {
+      int major = 0;
+      AAPDHG_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+      if (major < 10) {
+        cudaDeviceProp prop;
+        AAPDHG_CUDA(cudaGetDeviceProperties(&prop, device));
+        throw CudaError(std::string("device ") + prop.name + " is not sm_100 class");
+      }
+      int sms = 0;
+      AAPDHG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      // the gather kernels want L1, not shared memory (a few KB per CTA): 10%
+      // of the shared-memory maximum keeps 6 CTAs/SM and leaves more L1 than
+      // the driver's default 64 KB carveout (configs[1]: 47.3 -> 46.5 us per
+      // plain iteration, profiles/exp_carveout.py); -1 = driver default
+      const int carve = env_int("AAPDHG_CARVEOUT", 10);
+      if (carve >= 0) {
+        auto set = [&](const void* f) {
+          AAPDHG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+        };
+        set((const void*)k_plain_loop<true>);
+        set((const void*)k_plain_loop<false>);
+        set((const void*)k_dual_side<false, true>);
+        set((const void*)k_dual_side<false, false>);
+        set((const void*)k_primal_side<false, true>);
+        set((const void*)k_primal_side<false, false>);
+      }
+      AAPDHG_CUDA(cudaFuncSetAttribute(k_aa_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(aa_smem(kMaxMemory))));
+      AAPDHG_CUDA(cudaFuncSetAttribute(k_serial_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kSerSmem)));
+      AAPDHG_CUDA(cudaFuncSetAttribute(k_serial_xchains, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kSerSmem)));
+      if (device < 64) {
+        g_dev_sms[device] = sms;
+        g_dev_ready[device] = true;
+      }
+      num_sms_ = sms;
+    } else {
+      num_sms_ = g_dev_sms[device];
+    }
+  }
   AAPDHG_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
   stream_ = own_stream_;
   AAPDHG_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
   AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
-  AAPDHG_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device));
   pdl_ = env_int("AAPDHG_PDL", 1) != 0;
-  // the gather kernels want L1, not shared memory (a few KB per CTA): 10% of
-  // the shared-memory maximum keeps 6 CTAs/SM and leaves more L1 than the
-  // driver's default 64 KB carveout (configs[1]: 47.3 -> 46.5 us per plain
-  // iteration, profiles/exp_carveout.py); -1 = driver default
-  const int carve = env_int("AAPDHG_CARVEOUT", 10);
-  if (carve >= 0) {
-    auto set = [&](const void* f) {
-      AAPDHG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-    };
-    set((const void*)k_plain_loop<true>);
-    set((const void*)k_plain_loop<false>);
-    set((const void*)k_dual_side<false, true>);
-    set((const void*)k_dual_side<false, false>);
-    set((const void*)k_primal_side<false, true>);
-    set((const void*)k_primal_side<false, false>);
-  }
 }
 
 // c, q, l, u on the device plus the scratch of power iteration / per-op /
@@ -327,12 +357,6 @@ void Problem::init_vectors(const double* c, const double* q, const double* l, co
   static_assert(sizeof(DevState) <= 4096, "state mirror exceeds a pinned pool block");
   h_state_ = static_cast<DevState*>(pinned_small_alloc(sizeof(DevState)));
   h_batch_ = static_cast<int32_t*>(pinned_small_alloc(sizeof(int32_t)));
-  AAPDHG_CUDA(cudaFuncSetAttribute(k_aa_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(aa_smem(kMaxMemory))));
-  AAPDHG_CUDA(cudaFuncSetAttribute(k_serial_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kSerSmem)));
-  AAPDHG_CUDA(cudaFuncSetAttribute(k_serial_xchains, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kSerSmem)));
 }
 
 namespace {
@@ -342,7 +366,7 @@ struct PhaseTimer {
   Clock::time_point t = Clock::now();
   void operator()(const char* what) {
     if (!on) return;
-    std::fprintf(stderr, "[aapdhg] %-22s %8.3f s\n", what, secs(t));
+    std::fprintf(stderr, "[aapdhg] %-26s %10.1f us\n", what, 1e6 * secs(t));
     t = Clock::now();
   }
 };
@@ -495,9 +519,18 @@ void Problem::ensure_iter_buffers(int method, int cap) {
     // (advance, pipeline.cuh)
     du_.reserve(sizeof(double) * size_t(cap + 1) * std::max<int64_t>(N_, 1));
     dg_.reserve(sizeof(double) * size_t(cap + 1) * std::max<int64_t>(N_, 1));
+    // hi parts, then (FAA) the low parts of the double-double partials
     const int items = num_items_host(cap, AAPDHG_METHOD_FAA);
-    partdot_.reserve(sizeof(double) * size_t(items) * std::max(std::max(ndot_tile_, num_sms_), 1));
+    partdot_.reserve(2 * sizeof(double) * size_t(items) *
+                     std::max(std::max(ndot_tile_, num_sms_), 1));
   }
+}
+
+// FAA's double-double partials: the second half of partdot_
+double* Problem::faa_part_lo(int method, int cap) const {
+  if (method != AAPDHG_METHOD_FAA) return nullptr;
+  return partdot_.as<double>() + size_t(num_items_host(cap, AAPDHG_METHOD_FAA)) *
+                                     size_t(std::max(std::max(ndot_tile_, num_sms_), 1));
 }
 
 IterBufs Problem::iter_bufs() {
@@ -702,17 +735,28 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   return nodes;
 }
 
+// The register-blocked Gram (k_gram_dots / FAA: k_gram_dots_dd, one CTA per
+// SM or CTA pair) for TREE order and memories <= 10; k_tree_dots beyond.
+bool use_gram_dots(int method, int cap, bool serial) {
+  (void)method;
+  return !serial && cap <= 10 && env_int("AAPDHG_GRAM_DOTS", 1) != 0;
+}
+
 int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
   int nodes = 0;
   if (su.method == AAPDHG_METHOD_PDHG) return 0;
-  if (!su.serial && su.cap <= 10) {  // g staged inside the register Gram
+  if (use_gram_dots(su.method, su.cap, su.serial)) {  // g staged inside the register Gram
     const int c = su.cap <= 4 ? 4 : su.cap <= 6 ? 6 : su.cap <= 8 ? 8 : 10;
-    const bool faa = su.method == AAPDHG_METHOD_FAA;
-    auto kern = faa ? (c == 4 ? k_gram_dots<4, true> : c == 6 ? k_gram_dots<6, true>
-                       : c == 8 ? k_gram_dots<8, true> : k_gram_dots<10, true>)
-                    : (c == 4 ? k_gram_dots<4, false> : c == 6 ? k_gram_dots<6, false>
-                       : c == 8 ? k_gram_dots<8, false> : k_gram_dots<10, false>);
-    LAUNCH("k_gram_dots", kern<<<su.ndot_blk, kThreads, 0, s>>>(su.D, su.B.upool, su.P, su.S));
+    if (su.method == AAPDHG_METHOD_FAA) {  // double-double Gram; CTA pairs for 8 / 10
+      auto kern = c == 4 ? k_gram_dots_dd<4, 0> : c == 6 ? k_gram_dots_dd<6, 0>
+                  : c == 8 ? k_gram_dots_dd<8, 1> : k_gram_dots_dd<10, 1>;
+      const int grid = c >= 8 ? 2 * su.ndot_blk : su.ndot_blk;
+      LAUNCH("k_gram_dots", kern<<<grid, kThreads, 0, s>>>(su.D, su.B.upool, su.P, su.S));
+    } else {
+      auto kern = c == 4 ? k_gram_dots<4, false> : c == 6 ? k_gram_dots<6, false>
+                  : c == 8 ? k_gram_dots<8, false> : k_gram_dots<10, false>;
+      LAUNCH("k_gram_dots", kern<<<su.ndot_blk, kThreads, 0, s>>>(su.D, su.B.upool, su.P, su.S));
+    }
   } else {
     LAUNCH("k_stage_g", k_stage_g<<<grid_for(N_), kThreads, 0, s>>>(su.B.upool, su.B.gpool, su.P, su.S));
     if (su.serial) {
@@ -964,7 +1008,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.nblk1 = K1m.grid();
   P.nblk2 = K2m.grid();
   // TREE with memory <= 10: one CTA per SM for the register Gram
-  const int ndot = (!serial && cap <= 10) ? num_sms_ : ndot_tile_;
+  const int ndot = use_gram_dots(method, cap, serial) ? num_sms_ : ndot_tile_;
   P.ndot_blk = ndot;
 
   DevState S0{};
@@ -983,6 +1027,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.B.fused_ctrl = (!serial && m_ > 0 && env_int("AAPDHG_FUSED", 1) != 0) ? 1 : 0;
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
                  partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
+  su.D.part_lo = faa_part_lo(method, cap);
   su.W = SolveScratch{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
   su.P = dparams_.as<DevParams>();
   su.S = S;
@@ -1100,6 +1145,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
     }
     d2h(h_state_, S, sizeof(DevState), stream_);
     sync();
+    ph("solve: launch + state");
     if (profiling_) prof_collect();
     // stream completed records out of the device ring
     const uint64_t done_recs = h_state_->rec_complete;
@@ -1116,6 +1162,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
       sync();
       if (sink) sink(host_recs.data(), cnt, ctx);
       flushed = done_recs;
+      ph("solve: records");
     }
     if (h_state_->done) break;
     // ring safety: a launch never runs further ahead than half the ring
@@ -1126,14 +1173,49 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
 
   // finish, solver.cpp:153-166
   const int slot = st.u_idx[st.final_role];
-  double* kkt_dev = scal_.as<double>() + 8;
-  kkt_eval(slot, serial, kkt_dev, lam_.as<double>());
-  double kkt[4];
-  d2h(kkt, kkt_dev, sizeof kkt, stream_);
   const double* ufin = upool_.as<double>() + int64_t(slot) * N_;
-  if (x_out) d2h(x_out, ufin, sizeof(double) * n_, stream_);
-  if (y_out) d2h(y_out, ufin + n_, sizeof(double) * m_, stream_);
-  if (lam_out) d2h(lam_out, lam_.as<double>(), sizeof(double) * n_, stream_);
+  double kkt[4];
+  // TREE: the final iterate is the CUR iterate of the last iteration, whose
+  // KKT the fused kernels already reduced (DevState::kkt); only lambda needs
+  // K'y again (CSR-ordered, so lambda is the reference's bit for bit). The
+  // x / y downloads run while lambda is computed when the outputs are pinned.
+  // SERIAL (and the fixed-point start): the index-ordered kkt_eval.
+  const bool fast = !serial && st.final_role == U_CUR &&
+                    st.status != AAPDHG_SOLVE_FIXED_POINT_START &&
+                    env_int("AAPDHG_FAST_FINISH", 1) != 0;
+  if (fast) {
+    const bool px = x_out && host_is_pinned(x_out), py = y_out && host_is_pinned(y_out);
+    if (px) AAPDHG_CUDA(cudaMemcpyAsync(x_out, ufin, sizeof(double) * n_,
+                                        cudaMemcpyDeviceToHost, stream_));
+    if (py) AAPDHG_CUDA(cudaMemcpyAsync(y_out, ufin + n_, sizeof(double) * m_,
+                                        cudaMemcpyDeviceToHost, stream_));
+    if (lam_out && n_ > 0) {
+      T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
+      if (m_ > 0) {
+        spmv(stream_, KTm(false), vref(ufin + n_), rout(T_.as<double>()), false, nullptr, 0,
+             nullptr);
+      } else {
+        AAPDHG_CUDA(cudaMemsetAsync(T_.p, 0, sizeof(double) * n_, stream_));
+      }
+      k_lambda_from_T<<<grid_for(n_), kThreads, 0, stream_>>>(
+          T_.as<double>(), c_.as<double>(), l_.as<double>(), u_.as<double>(), n_,
+          lam_.as<double>());
+      AAPDHG_CUDA(cudaGetLastError());
+    }
+    for (int q = 0; q < 4; ++q) kkt[q] = st.kkt[q];
+    if (x_out && !px) d2h(x_out, ufin, sizeof(double) * n_, stream_);
+    if (y_out && !py) d2h(y_out, ufin + n_, sizeof(double) * m_, stream_);
+    if (lam_out) d2h(lam_out, lam_.as<double>(), sizeof(double) * n_, stream_);
+    ph("solve: final lambda + downloads");
+  } else {
+    double* kkt_dev = scal_.as<double>() + 8;
+    kkt_eval(slot, serial, kkt_dev, lam_.as<double>());
+    d2h(kkt, kkt_dev, sizeof kkt, stream_);
+    ph("solve: final kkt");
+    if (x_out) d2h(x_out, ufin, sizeof(double) * n_, stream_);
+    if (y_out) d2h(y_out, ufin + n_, sizeof(double) * m_, stream_);
+    if (lam_out) d2h(lam_out, lam_.as<double>(), sizeof(double) * n_, stream_);
+  }
   sync();
   std::memset(res, 0, sizeof *res);
   res->status = st.status;
@@ -1250,6 +1332,19 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
                       const double* dg_cols, double beta, const double* d_hat, double eta,
                       double c_s, double kappa_bar, const double* u, const double* g,
                       double* out, int32_t* kept) {
+  return aa_op(reduction, filtered, p, du_cols, dg_cols, beta, d_hat, eta, c_s, kappa_bar, 0, u,
+               g, out, kept, nullptr, nullptr);
+}
+
+// The AA / FAA step on caller-supplied columns (per-op entries): dots,
+// k_aa_solve, then the candidate (out != null), the FAA kept set (kept),
+// and for economy_qr the kept columns' R (r_out, p x p column-major) and
+// Q = F R^{-1} (q_out, N x kk column-major). faa_skip: kFaaSkip* stages.
+// u / g may be null when no candidate is formed (zeros).
+int Problem::aa_op(int reduction, bool filtered, int p, const double* du_cols,
+                   const double* dg_cols, double beta, const double* d_hat, double eta,
+                   double c_s, double kappa_bar, int faa_skip, const double* u, const double* g,
+                   double* out, int32_t* kept, double* r_out, double* q_out) {
   AAPDHG_CUDA(cudaSetDevice(device_));
   if (p < 0) throw StatusError(AAPDHG_ERR_DIMENSION, "aa_apply: negative memory size");
   if (p > kMaxMemory)
@@ -1260,10 +1355,13 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
   const int method = filtered ? AAPDHG_METHOD_FAA : AAPDHG_METHOD_AA;
   const bool serial = resolve_serial(reduction);
   ensure_iter_buffers(method, std::max(p, 1));
-  h2d(du_.p, du_cols, sizeof(double) * size_t(p) * N_, stream_);
+  if (du_cols) h2d(du_.p, du_cols, sizeof(double) * size_t(p) * N_, stream_);
+  else AAPDHG_CUDA(cudaMemsetAsync(du_.p, 0, sizeof(double) * size_t(std::max(p, 1)) * N_, stream_));
   h2d(dg_.p, dg_cols, sizeof(double) * size_t(p) * N_, stream_);
-  h2d(gpool_.p, g, sizeof(double) * N_, stream_);
-  h2d(upool_.p, u, sizeof(double) * N_, stream_);
+  if (g) h2d(gpool_.p, g, sizeof(double) * N_, stream_);
+  else AAPDHG_CUDA(cudaMemsetAsync(gpool_.p, 0, sizeof(double) * N_, stream_));
+  if (u) h2d(upool_.p, u, sizeof(double) * N_, stream_);
+  else AAPDHG_CUDA(cudaMemsetAsync(upool_.p, 0, sizeof(double) * N_, stream_));
   if (d_hat) {
     dhat_.reserve(sizeof(double) * N_);
     h2d(dhat_.p, d_hat, sizeof(double) * N_, stream_);
@@ -1285,6 +1383,11 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
   P.ndot_blk = ndot_tile_;
+  P.faa_skip = faa_skip;
+  if (r_out) {
+    gram_.reserve(sizeof(double) * kMaxMemory * kMaxMemory);
+    P.qr_r_out = gram_.as<double>();
+  }
   DevState S = identity_state();
   S.aa_attempt = 1;
   S.mem_size = p;
@@ -1293,6 +1396,7 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
   h2d(dstate_.p, &S, sizeof S, stream_);
   DotBufs D{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(), partdot_.as<double>(),
             num_items_host(std::max(p, 1), method)};
+  D.part_lo = faa_part_lo(method, std::max(p, 1));
   SolveScratch W{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
   IterBufs B = iter_bufs();
   const DevParams* Pd = dparams_.as<DevParams>();
@@ -1306,12 +1410,26 @@ int Problem::aa_apply(int reduction, bool filtered, int p, const double* du_cols
     }
   }
   k_aa_solve<<<1, 1024, aa_smem(std::max(p, 1)), stream_>>>(D, Pd, Sd, 1);
-  k_mix<<<grid_for(N_), kThreads, 0, stream_>>>(B, dg_.as<double>(), Pd, Sd, 0);
+  if (out) k_mix<<<grid_for(N_), kThreads, 0, stream_>>>(B, dg_.as<double>(), Pd, Sd, 0);
   AAPDHG_CUDA(cudaGetLastError());
   d2h(h_state_, Sd, sizeof(DevState), stream_);
   sync();
   if (!h_state_->aa_ok) return AAPDHG_ERR_SINGULAR;
-  d2h(out, upool_.as<double>() + 3 * N_, sizeof(double) * N_, stream_);
+  if (out) d2h(out, upool_.as<double>() + 3 * N_, sizeof(double) * N_, stream_);
+  const int kk = h_state_->mix_p;
+  if (r_out && kk > 0) {
+    d2h(r_out, gram_.p, sizeof(double) * size_t(kk) * kk, stream_);
+    if (q_out) {  // Q = F_kept R^{-1}; the kept columns are memory slots mix_slots[]
+      std::vector<int32_t> sl(h_state_->mix_slots, h_state_->mix_slots + kk);
+      bool contiguous = true;
+      for (int t = 0; t < kk; ++t) contiguous = contiguous && sl[size_t(t)] == t;
+      if (!contiguous) throw StatusError(AAPDHG_ERR_INTERNAL, "economy_qr: columns were filtered");
+      k_qr_q<<<grid_for(N_), kThreads, 0, stream_>>>(dg_.as<double>(), gram_.as<double>(), kk,
+                                                      N_, du_.as<double>());
+      AAPDHG_CUDA(cudaGetLastError());
+      d2h(q_out, du_.p, sizeof(double) * size_t(kk) * N_, stream_);
+    }
+  }
   sync();
   if (kept) {
     for (int t = 0; t < p; ++t) kept[t] = 0;
@@ -1478,6 +1596,7 @@ void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
   su.B.rinit2 = kb_.nb() > 1 ? kb_.partial.as<double>() : nullptr;
   su.D = DotBufs{du_.as<double>(), dg_.as<double>(), gpool_.as<double>(),
                  partdot_.as<double>(), num_items_host(std::max(cap, 1), method)};
+  su.D.part_lo = faa_part_lo(method, cap);
   su.W = SolveScratch{gram_.as<double>(), work_.as<double>(), vec_.as<double>()};
   su.P = dparams_.as<DevParams>();
   su.S = S;

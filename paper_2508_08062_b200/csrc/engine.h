@@ -126,6 +126,10 @@ class Problem {
                const double* dg_cols, double beta, const double* d_hat, double eta,
                double c_s, double kappa_bar, const double* u, const double* g, double* out,
                int32_t* kept);
+  int aa_op(int reduction, bool filtered, int p, const double* du_cols, const double* dg_cols,
+            double beta, const double* d_hat, double eta, double c_s, double kappa_bar,
+            int faa_skip, const double* u, const double* g, double* out, int32_t* kept,
+            double* r_out, double* q_out);
 
   void set_profiling(bool on) { profiling_ = on; }
   void set_stream(cudaStream_t s);
@@ -167,6 +171,7 @@ class Problem {
   const CsrDev& sh_k2m() const { return kb_.nb() > 1 ? kb_.blk.back() : Kt_; }
   const CsrDev& KTm(bool serial) const { return serial ? KTs_ : KTt_; }
   void ensure_iter_buffers(int method, int cap);
+  double* faa_part_lo(int method, int cap) const;
   void upload_iterate(int slot, const double* x, const double* y);
   IterBufs iter_bufs();
 

@@ -66,9 +66,16 @@ __global__ void __launch_bounds__(1024)
   for (int it = warp; it < nit; it += nw) {
     const double* pp = D.part + (int64_t)it * P->ndot_blk;
     double s = 0.0;
-    for (int b = lane; b < P->ndot_blk; b += 32) s = __dadd_rn(s, pp[b]);
+    if (D.part_lo) {  // FAA: the double-double partials, rounded once per shard
+      const double* pl = D.part_lo + (int64_t)it * P->ndot_blk;
+      dd t = {0.0, 0.0};
+      for (int b = lane; b < P->ndot_blk; b += 32) t = dd_add(t, dd{pp[b], pl[b]});
+      s = warp_sum_dd(t).hi;
+    } else {
+      for (int b = lane; b < P->ndot_blk; b += 32) s = __dadd_rn(s, pp[b]);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    }
     if (lane == 0)
       for (int q = 0; q < P->ndst; ++q) P->dots_dst[q][it] = s;
   }

@@ -4,9 +4,10 @@ golden fixtures made from the reference itself.
 Tolerances (north star, BASELINE.json): SERIAL reduction order is bit-exact
 (integer/ordering semantics of the reference reproduced: CSR-ordered row
 sums, index-ordered dots, no FMA). TREE order: first 50 iterates within 1e-10
-relative, final objective / KKT within 1e-6 relative. FAA uses a Gram-based R
-instead of Householder QR (not bitwise): per-op 1e-9 relative, and the first
-50 iterates of an FAA solve within 1e-10 relative (measured ~1e-14)."""
+relative, final objective / KKT within 1e-6 relative. FAA solves its least
+squares from a double-double Gram instead of Householder QR (not bitwise,
+more accurate: aa.cuh / dd.cuh): per-op 1e-12 relative, and the first 50
+iterates of an FAA solve within 1e-10 relative."""
 import numpy as np
 import pytest
 
@@ -121,7 +122,39 @@ def test_aa_apply_parity(k):
                 assert rc == a["frc"]
                 assert kept.tolist() == a["kept"]
                 if a["fout"] is not None:
-                    assert rel(out, unhex(a["fout"])) < 1e-9
+                    assert rel(out, unhex(a["fout"])) < 1e-12
+
+
+def _faa_illcond_cases():
+    import json
+    from pathlib import Path
+    f = Path(__file__).resolve().parent / "golden" / "faa_illcond.json"
+    return json.loads(f.read_text())["cases"]
+
+
+@pytest.mark.parametrize("case", _faa_illcond_cases(),
+                         ids=lambda c: f"p{c['p']}-k{c['kappa']:.0e}-cs{c['c_s']:g}")
+def test_faa_illconditioned_histories(case):
+    """FAA per op on histories with kappa(F) = 1e2 .. 1e8 (fixtures from the
+    reference plus the exact answer, tests/golden/make_faa_illcond.py): the
+    same kept set as the reference's filters, and a candidate within 1e-12
+    relative of the exact one — at least as close as the reference's own
+    Householder solve (whose error grows like kappa u: up to ~1e-8 here)."""
+    p_, N = case["p"], case["N"]
+    du, dg = unhex(case["du"]).reshape(p_, N), unhex(case["dg"]).reshape(p_, N)
+    u, g = unhex(case["u"]), unhex(case["g"])
+    with Solver(_dummy_problem(N)) as s:
+        for red in ("serial", "tree"):
+            rc, out, kept = _aa_call(s, True, red, du, dg, u, g, c_s=case["c_s"],
+                                     kappa_bar=case["kappa_bar"])
+            assert rc == case["rc"]
+            assert kept.tolist() == case["kept"]
+            if case["exact"] is None:
+                continue
+            ex, ref = unhex(case["exact"]), unhex(case["ref"])
+            err_gpu, err_ref = rel(out, ex), rel(ref, ex)
+            assert err_gpu <= 1e-12, (red, err_gpu, err_ref)
+            assert err_gpu <= max(err_ref, 1e-14), (red, err_gpu, err_ref)
 
 
 def test_aa_singular_maps_to_singular_error():
@@ -136,6 +169,12 @@ def test_aa_singular_maps_to_singular_error():
 
 
 # ---- full solves ----------------------------------------------------------
+def _faa_envelope():
+    import json
+    from pathlib import Path
+    return json.loads((Path(__file__).resolve().parent / "golden" / "faa_envelope.json").read_text())
+
+
 @pytest.mark.parametrize("case", golden()["solves"], ids=lambda c: c["name"])
 def test_golden_solves(case):
     p = problem(case["problem"])
@@ -156,14 +195,25 @@ def test_golden_solves(case):
             assert np.array_equal(r.u.y, unhex(case["y"]))
         assert_traj_equal(out.trajectory, case)
     else:
-        # FAA: Gram-based R (not bitwise) — counts within 2%, objective 1e-6
+        # FAA: double-double Gram solve instead of Householder (not bitwise):
+        # count within 2% of the reference's own rounding envelope (strict /
+        # FMA / reassociated builds, tests/golden/make_faa_envelope.py),
+        # objective 1e-6, first 50 iterates 1e-10
         assert int(r.status) == case["status"]
-        assert abs(r.iterations - case["iterations"]) <= max(2, 0.02 * case["iterations"])
+        env = _faa_envelope()[case["name"]]
+        counts = [env[k] for k in ("ref", "ref-fast", "ref-assoc")]
+        lo, hi = min(counts), max(counts)
+        assert env["ref"] == case["iterations"]
+        assert lo - max(2, 0.02 * lo) <= r.iterations <= hi + max(2, 0.02 * hi), (r.iterations, env)
         obj = float.fromhex(case["objective"])
         assert abs(r.objective - obj) <= 1e-6 * max(1.0, abs(obj))
+        # first 50 iterates: 1e-10, or twice the reference's own spread under
+        # rounding changes where that is larger (transport20: 1.8e-10 at k=49)
         k = min(50, len(case["traj"]["g_norm"]), out.trajectory.size)
+        tol = max(1e-10, 2.0 * env["g_norm_spread_50"])
         np.testing.assert_allclose(out.trajectory["g_norm"][:k], unhex(case["traj"]["g_norm"])[:k],
-                                   rtol=1e-8)
+                                   rtol=tol)
+        assert np.array_equal(out.trajectory["aa_step"][:k], np.array(case["traj"]["aa_step"][:k]))
 
 
 @pytest.mark.parametrize("case", [c for c in golden()["solves"]
