@@ -77,6 +77,14 @@ typedef struct aapdhg_csr_view {
 
 /* Four-block LP  min c'x  s.t. Gx >= h, Ax = b, l <= x <= u
  * given through K = [G; A] and q = [h; b] (lp_model.hpp:32-53). */
+/* One (row, col, value) entry — the layout of the reference's Triplet
+ * (proj/include/aapdhg/sparse_linalg.hpp:12-16). */
+typedef struct aapdhg_triplet {
+  int32_t row;
+  int32_t col;
+  double val;
+} aapdhg_triplet;
+
 typedef struct aapdhg_problem_view {
   aapdhg_csr_view k; /* (m1 + m2) x n */
   int32_t m1;        /* leading inequality rows of K */
@@ -275,6 +283,22 @@ int aapdhg_cuda_filtered_aa_apply(aapdhg_handle* h, int32_t reduction,
                                   double kappa_bar, double beta,
                                   const double* d_hat, const double* u,
                                   const double* g, double* out, int32_t* kept,
+                                  char* err, size_t errlen);
+
+/* Replaces: SparseMatrix::from_triplets (sparse_linalg.hpp:22-23,
+ * sparse_linalg.cpp:11-42), and with row_map / row_neg the split of
+ * to_standard_form (lp_model.cpp:232-291): CSR of `count` triplets built on
+ * `device` — entries sorted by (row_map[row], col), duplicates summed left
+ * to right in input order, exact cancellations kept as structural zeros.
+ * row_map (nrows_in entries, may be null = identity) sends input rows to
+ * output rows < nrows_out; row_neg (nrows_in, may be null) negates a row's
+ * values. Outputs: row_ptr[nrows_out + 1], col_idx / vals with room for
+ * `count` entries; *nnz receives the entry count. AAPDHG_ERR_DIMENSION for
+ * an entry outside nrows_in x ncols. */
+int aapdhg_cuda_csr_from_triplets(int32_t device, int32_t nrows_in, int32_t nrows_out,
+                                  int32_t ncols, int64_t count, const aapdhg_triplet* triplets,
+                                  const int32_t* row_map, const uint8_t* row_neg,
+                                  int32_t* row_ptr, int32_t* col_idx, double* vals, int64_t* nnz,
                                   char* err, size_t errlen);
 
 /* A handle for the per-op AA / FAA entries on vectors of length n (no LP:

@@ -161,6 +161,9 @@ def _declare_cuda(lib):
         "aapdhg_cuda_faa_op": ([H, C.c_int32, C.c_int32, _dp, _dp, C.c_double, C.c_double,
                                 C.c_double, _dp, C.c_int32, _dp, _dp, _dp, _ip] + E, C.c_int),
         "aapdhg_cuda_economy_qr": ([H, C.c_int32, C.c_int32, _dp, _dp, _dp] + E, C.c_int),
+        "aapdhg_cuda_csr_from_triplets": ([C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                           C.c_int64, C.c_void_p, _ip, C.c_void_p, _ip, _ip,
+                                           _dp, C.POINTER(C.c_int64)] + E, C.c_int),
         "aapdhg_cuda_set_stream": ([H, C.c_void_p], C.c_int),
         "aapdhg_cuda_set_profiling": ([H, C.c_int32], C.c_int),
         "aapdhg_cuda_kernel_times": ([H, C.c_char_p, C.c_size_t, _dp,
@@ -188,7 +191,8 @@ CUDA_SYMBOLS = (
     "aapdhg_cuda_select_step_sizes", "aapdhg_cuda_power_norm", "aapdhg_cuda_matvec",
     "aapdhg_cuda_matvec_transpose", "aapdhg_cuda_pdhg_step", "aapdhg_cuda_kkt_metrics",
     "aapdhg_cuda_aa_apply", "aapdhg_cuda_filtered_aa_apply", "aapdhg_cuda_workspace_create",
-    "aapdhg_cuda_faa_op", "aapdhg_cuda_economy_qr", "aapdhg_cuda_set_stream",
+    "aapdhg_cuda_faa_op", "aapdhg_cuda_economy_qr", "aapdhg_cuda_csr_from_triplets",
+    "aapdhg_cuda_set_stream",
     "aapdhg_cuda_set_profiling",
     "aapdhg_cuda_kernel_times", "aapdhg_cuda_last_launch_count", "aapdhg_cuda_last_plain_loop",
     "aapdhg_cuda_nccl_id", "aapdhg_cuda_partition", "aapdhg_cuda_problem_create_dist",

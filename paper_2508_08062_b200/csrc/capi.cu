@@ -332,6 +332,22 @@ int aapdhg_cuda_economy_qr(aapdhg_handle* h, int32_t reduction, int32_t p, const
   });
 }
 
+int aapdhg_cuda_csr_from_triplets(int32_t device, int32_t nrows_in, int32_t nrows_out,
+                                  int32_t ncols, int64_t count, const aapdhg_triplet* triplets,
+                                  const int32_t* row_map, const uint8_t* row_neg,
+                                  int32_t* row_ptr, int32_t* col_idx, double* vals, int64_t* nnz,
+                                  char* err, size_t errlen) {
+  if (int rc = need(row_ptr && nnz && (count == 0 || (triplets && col_idx && vals)) ? row_ptr
+                                                                                    : nullptr,
+                    "csr_from_triplets: null argument", err, errlen))
+    return rc;
+  return guard(err, errlen, [&] {
+    *nnz = aapdhg_b200::csr_from_triplets(device, nrows_in, nrows_out, ncols, count, triplets,
+                                          row_map, row_neg, row_ptr, col_idx, vals);
+    return AAPDHG_OK;
+  });
+}
+
 int aapdhg_cuda_set_stream(aapdhg_handle* h, void* stream) {
   if (!h) return AAPDHG_ERR_INPUT;
   return guard(nullptr, 0, [&] {

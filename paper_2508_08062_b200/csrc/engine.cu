@@ -123,9 +123,10 @@ struct PersistLock {
 // Uploads one CSR with its two sliced layouts: `ser` (sf = 1, CSR-ordered
 // row sums for the SERIAL mode) and `tree` (sf chosen so the slices fill
 // ~48 warps on every SM; aliases `ser` when sf = 1).
+// (rp / ci / v may be host or device memory; nnz < 0: rp[nrows], host rp)
 void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows,
-                         int ncols, CsrStore& st, CsrDev& ser, CsrDev& tree) {
-  const int64_t nnz = rp[nrows];
+                         int ncols, CsrStore& st, CsrDev& ser, CsrDev& tree, int64_t nnz_in) {
+  const int64_t nnz = nnz_in >= 0 ? nnz_in : rp[nrows];
   st.rp.reserve(sizeof(int32_t) * (size_t(nrows) + 1));
   st.ci.reserve(sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1)));
   st.v.reserve(sizeof(double) * size_t(std::max<int64_t>(nnz, 1)));
@@ -1456,10 +1457,18 @@ Problem::Problem(const ShardSpec& sp, int device) : device_(device) {
   maxr_ = sp.maxr;
   all_zero_ = sp.all_zero;
   bounds_ok_ = sp.bounds_ok;
-  upload_csr(sp.k_rp.data(), sp.k_ci.data(), sp.k_v.data(), m_, int(sp.world * sp.maxc),
-             k_store_, Ks_, Kt_);
-  upload_csr(sp.t_rp.data(), sp.t_ci.data(), sp.t_v.data(), n_, int(sp.world * sp.maxr),
-             t_store_, KTs_, KTt_);
+  if (sp.dev) {  // blocks built on this device (shard_build.cu)
+    nnz_ = sp.dev->k_nnz;
+    upload_csr(sp.dev->k_rp.as<int32_t>(), sp.dev->k_ci.as<int32_t>(), sp.dev->k_v.as<double>(),
+               m_, int(sp.world * sp.maxc), k_store_, Ks_, Kt_, sp.dev->k_nnz);
+    upload_csr(sp.dev->t_rp.as<int32_t>(), sp.dev->t_ci.as<int32_t>(), sp.dev->t_v.as<double>(),
+               n_, int(sp.world * sp.maxr), t_store_, KTs_, KTt_, sp.dev->t_nnz);
+  } else {
+    upload_csr(sp.k_rp.data(), sp.k_ci.data(), sp.k_v.data(), m_, int(sp.world * sp.maxc),
+               k_store_, Ks_, Kt_);
+    upload_csr(sp.t_rp.data(), sp.t_ci.data(), sp.t_v.data(), n_, int(sp.world * sp.maxr),
+               t_store_, KTs_, KTt_);
+  }
   // (relabelled indices stay ascending within a row: column blocks are in order)
   build_blocks(k_store_, m_, int(sp.world * sp.maxc), kb_);
   build_blocks(t_store_, n_, int(sp.world * sp.maxr), ktb_);

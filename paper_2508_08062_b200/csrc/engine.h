@@ -32,11 +32,40 @@ struct KernelStat {
 struct SolveSetup;
 
 void validate_problem_view(const aapdhg_problem_view* v);    // header + deep (host)
+// CSR from triplets on the device (triplets.cu); returns nnz
+int64_t csr_from_triplets(int device, int nrows_in, int nrows_out, int ncols, int64_t count,
+                          const aapdhg_triplet* trip, const int32_t* row_map,
+                          const uint8_t* row_neg, int32_t* rp_out, int32_t* ci_out,
+                          double* v_out);
 void validate_problem_header(const aapdhg_problem_view* v);  // O(1) host checks
 const char* csr_flag_message(int flags);  // kCsr* flags -> the error message, or null
 void validate_config(const aapdhg_solve_params* c);
 void transpose_csr(const aapdhg_csr_view& k, std::vector<int32_t>& trp, std::vector<int32_t>& tci,
                    std::vector<double>& tv);
+
+// O(nnz) checks of a CSR on the device (kCsr* flags; ingest.cu)
+int device_validate_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows,
+                        int ncols, int64_t nnz, cudaStream_t s);
+
+// A shard's device-built blocks (shard_build.cu): K[R_r, :] with padded
+// column labels and K[:, C_r]' with padded row labels.
+struct DeviceShardBlocks {
+  DevBuf k_rp, k_ci, k_v, t_rp, t_ci, t_v;
+  int64_t k_nnz = 0, t_nnz = 0;
+};
+
+struct Partition;
+// The whole LP's CSR on one device, for building shards there.
+struct DeviceLp {
+  DevBuf rp, ci, v;
+  int nrows = 0, ncols = 0;
+  int64_t nnz = 0;
+  bool all_zero = true;
+  void upload(const aapdhg_csr_view& k, int device, cudaStream_t s);  // + device checks
+  std::vector<int64_t> column_weights(cudaStream_t s) const;          // nnz per column + 4
+  void shard_blocks(const Partition& part, int world, int r, cudaStream_t s,
+                    DeviceShardBlocks& out) const;
+};
 
 // One shard of a row/column-partitioned LP (shard.cuh): K's
 // rows R_r with column indices relabelled into the padded x all-gather
@@ -49,6 +78,8 @@ struct ShardSpec {
   int64_t n_glob = 0, m_glob = 0;
   std::vector<int32_t> k_rp, k_ci, t_rp, t_ci;
   std::vector<double> k_v, t_v;
+  // or the blocks already on this shard's device (shard_build.cu)
+  const DeviceShardBlocks* dev = nullptr;
   std::vector<double> c, l, u, q;
   double nrm_q = 0.0, nrm_c = 0.0;
   bool all_zero = false, bounds_ok = true;
@@ -164,7 +195,7 @@ class Problem {
   void device_block(const CsrStore& src, int nrows, int64_t c0, int64_t c1, CsrStore& dst,
                     int64_t* nnz_out);
   void upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
-                  CsrStore& st, CsrDev& ser, CsrDev& tree);
+                  CsrStore& st, CsrDev& ser, CsrDev& tree, int64_t nnz = -1);
   const CsrDev& Km(bool serial) const { return serial ? Ks_ : Kt_; }
   // a shard's fused-kernel matrices: the last column block when blocked
   const CsrDev& sh_k1m() const { return ktb_.nb() > 1 ? ktb_.blk.back() : KTt_; }

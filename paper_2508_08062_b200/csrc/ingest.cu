@@ -216,21 +216,26 @@ T* tmp(DevBuf& b, size_t count) {
 
 // The O(nnz) input checks on the uploaded CSR (validate_problem_deep's, in
 // the same priority order) and the all-zero test of power_iteration_norm.
-void Problem::device_validate(const CsrStore& st, int nrows, int ncols, int64_t nnz) {
-  cudaStream_t s = stream_;
+int device_validate_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows,
+                        int ncols, int64_t nnz, cudaStream_t s) {
   DevBuf bf;
   int* flags = tmp<int>(bf, 1);
   AAPDHG_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), s));
   if (nrows > 0)
-    k_validate_rows<<<blocks_for(int64_t(nrows) * 32), kT, 0, s>>>(
-        st.rp.as<int32_t>(), st.ci.as<int32_t>(), nrows, ncols, nnz, flags);
+    k_validate_rows<<<blocks_for(int64_t(nrows) * 32), kT, 0, s>>>(rp, ci, nrows, ncols, nnz,
+                                                                  flags);
   if (nnz > 0)
-    k_validate_vals<<<std::min(blocks_for(nnz), 148 * 8), kT, 0, s>>>(st.v.as<double>(), nnz,
-                                                                     flags);
+    k_validate_vals<<<std::min(blocks_for(nnz), 148 * 8), kT, 0, s>>>(v, nnz, flags);
   AAPDHG_CUDA(cudaGetLastError());
   int h = 0;
   AAPDHG_CUDA(cudaMemcpyAsync(&h, flags, sizeof h, cudaMemcpyDeviceToHost, s));
   AAPDHG_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+void Problem::device_validate(const CsrStore& st, int nrows, int ncols, int64_t nnz) {
+  const int h = device_validate_csr(st.rp.as<int32_t>(), st.ci.as<int32_t>(), st.v.as<double>(),
+                                    nrows, ncols, nnz, stream_);
   if (const char* msg = csr_flag_message(h)) throw StatusError(AAPDHG_ERR_DIMENSION, msg);
   if (shard_rank_ < 0) all_zero_ = !(h & kCsrNonzero);  // a shard's comes from the whole LP
 }

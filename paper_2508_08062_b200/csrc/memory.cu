@@ -223,7 +223,15 @@ bool host_is_pinned(const void* p) {
 
 void host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return;
-  if (bytes <= kSmall || host_is_pinned(src)) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, src) != cudaSuccess) {
+    (void)cudaGetLastError();
+  } else if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    // already on a device (e.g. a shard's blocks built there): a device copy
+    AAPDHG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    return;
+  }
+  if (bytes <= kSmall || a.type == cudaMemoryTypeHost) {
     // pinned: DMA; small pageable: the driver stages it before returning
     AAPDHG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     return;

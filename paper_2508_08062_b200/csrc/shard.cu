@@ -104,6 +104,21 @@ static std::vector<int32_t> split_weights(const std::vector<int64_t>& w, int wor
   return b;
 }
 
+// row weights from row_ptr (nnz + 4 per row), column weights given
+Partition plan_partition_weights(const aapdhg_csr_view& k, const std::vector<int64_t>& wc,
+                                 int world) {
+  Partition p;
+  std::vector<int64_t> wr(static_cast<size_t>(k.nrows));
+  for (int r = 0; r < k.nrows; ++r) wr[r] = int64_t(k.row_ptr[r + 1] - k.row_ptr[r]) + 4;
+  p.rows = split_weights(wr, world);
+  p.cols = split_weights(wc, world);
+  for (int r = 0; r < world; ++r) {
+    p.maxr = std::max<int64_t>(p.maxr, p.rows[r + 1] - p.rows[r]);
+    p.maxc = std::max<int64_t>(p.maxc, p.cols[r + 1] - p.cols[r]);
+  }
+  return p;
+}
+
 Partition plan_partition(const aapdhg_csr_view& k, int world) {
   Partition p;
   std::vector<int64_t> wr(static_cast<size_t>(k.nrows)), wc(static_cast<size_t>(k.ncols), 4);
@@ -120,7 +135,12 @@ Partition plan_partition(const aapdhg_csr_view& k, int world) {
 
 ShardGroup::ShardGroup(const aapdhg_problem_view* v, int device, const aapdhg_dist_view* d)
     : device_(device) {
-  validate_problem_view(v);
+  // the shards' blocks are built on the device (shard_build.cu) unless
+  // AAPDHG_SHARD_HOST_BUILD=1 asks for the host builder below
+  const char* hb = std::getenv("AAPDHG_SHARD_HOST_BUILD");
+  const bool host_build = hb && hb[0] == '1';
+  if (host_build) validate_problem_view(v);
+  else validate_problem_header(v);
   if (!d) throw StatusError(AAPDHG_ERR_INPUT, "problem_create_dist: null dist");
   const aapdhg_csr_view& k = v->k;
   world_ = d->world;
@@ -145,24 +165,39 @@ ShardGroup::ShardGroup(const aapdhg_problem_view* v, int device, const aapdhg_di
     throw StatusError(AAPDHG_ERR_UNSUPPORTED,
                       "problem_create_dist: every shard needs at least one row and one column");
 
-  part_ = plan_partition(k, world_);
+  // device build: the whole CSR on this rank's GPU once (checked there),
+  // column weights from a device histogram
+  DeviceLp dlp;
+  cudaStream_t bs = nullptr;
+  if (!host_build) {
+    AAPDHG_CUDA(cudaSetDevice(device));
+    AAPDHG_CUDA(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking));
+    dlp.upload(k, device, bs);
+    part_ = plan_partition_weights(k, dlp.column_weights(bs), world_);
+  } else {
+    part_ = plan_partition(k, world_);
+  }
   std::vector<int32_t> trp, tci;
   std::vector<double> tv;
-  transpose_csr(k, trp, tci, tv);
+  if (host_build) transpose_csr(k, trp, tci, tv);
 
   // ||q||, ||c|| once on the host (sequential): identical on every shard
   double qq = 0.0, cc = 0.0;
   for (int i = 0; i < m_; ++i) qq += v->q[i] * v->q[i];
   for (int j = 0; j < n_; ++j) cc += v->c[j] * v->c[j];
   all_zero_ = true;
-  for (int64_t e = 0; e < nnz_ && all_zero_; ++e) all_zero_ = k.vals[e] == 0.0;
+  if (host_build)
+    for (int64_t e = 0; e < nnz_ && all_zero_; ++e) all_zero_ = k.vals[e] == 0.0;
+  else
+    all_zero_ = dlp.all_zero;
   bounds_ok_ = true;
   for (int j = 0; j < n_; ++j)
     if (v->l[j] > v->u[j]) bounds_ok_ = false;
 
-  // owner-relative indices in the padded all-gather buffers
-  std::vector<int32_t> xmap(static_cast<size_t>(n_)), ymap(static_cast<size_t>(m_));
-  for (int r = 0; r < world_; ++r) {
+  // owner-relative indices in the padded all-gather buffers (host build)
+  std::vector<int32_t> xmap(static_cast<size_t>(host_build ? n_ : 0)),
+      ymap(static_cast<size_t>(host_build ? m_ : 0));
+  for (int r = 0; r < world_ && host_build; ++r) {
     for (int j = part_.cols[r]; j < part_.cols[r + 1]; ++j)
       xmap[j] = int32_t(r * part_.maxc + (j - part_.cols[r]));
     for (int i = part_.rows[r]; i < part_.rows[r + 1]; ++i)
@@ -188,16 +223,21 @@ ShardGroup::ShardGroup(const aapdhg_problem_view* v, int device, const aapdhg_di
     sp.maxr = part_.maxr;
     sp.n_glob = n_;
     sp.m_glob = m_;
-    sp.k_rp.assign(size_t(sp.m_loc) + 1, 0);
-    for (int i = r0; i < r1; ++i) {
+    DeviceShardBlocks blocks;
+    if (!host_build) {
+      dlp.shard_blocks(part_, world_, r, bs, blocks);
+      sp.dev = &blocks;
+    }
+    if (host_build) sp.k_rp.assign(size_t(sp.m_loc) + 1, 0);
+    for (int i = r0; i < r1 && host_build; ++i) {
       for (int32_t e = k.row_ptr[i]; e < k.row_ptr[i + 1]; ++e) {
         sp.k_ci.push_back(xmap[size_t(k.col_idx[e])]);
         sp.k_v.push_back(k.vals[e]);
       }
       sp.k_rp[size_t(i - r0) + 1] = int32_t(sp.k_ci.size());
     }
-    sp.t_rp.assign(size_t(sp.n_loc) + 1, 0);
-    for (int j = c0; j < c1; ++j) {
+    if (host_build) sp.t_rp.assign(size_t(sp.n_loc) + 1, 0);
+    for (int j = c0; j < c1 && host_build; ++j) {
       for (int32_t e = trp[j]; e < trp[j + 1]; ++e) {
         sp.t_ci.push_back(ymap[size_t(tci[e])]);
         sp.t_v.push_back(tv[e]);
@@ -213,6 +253,10 @@ ShardGroup::ShardGroup(const aapdhg_problem_view* v, int device, const aapdhg_di
     sp.all_zero = all_zero_;
     sp.bounds_ok = bounds_ok_;
     shards_.emplace_back(new Problem(sp, device));
+  }
+  if (bs) {
+    cudaStreamSynchronize(bs);
+    cudaStreamDestroy(bs);
   }
   AAPDHG_CUDA(cudaSetDevice(device));
   if (!multi_) {
@@ -540,7 +584,32 @@ void ShardGroup::solve(const aapdhg_solve_params* prm, const double* x0, const d
     }
     if (g) cudaGraphDestroy(g);
   }
-  if (!cond_graph && mode >= 1) {
+  // Every rank must issue the same collective sequence: the WHILE/IF graph
+  // runs the AA branch's exchanges only on attempts, the per-iteration graph
+  // on every iteration. A rank whose capture failed (or whose environment
+  // asks for another mode) would hang the others, so the ranks agree on the
+  // smallest mode any of them can run before the loop (one all-gather of a
+  // flag through this rank's chunk of the SCAL exchange buffer, idle here).
+  int agreed = cond_graph ? 2 : (mode >= 1 ? 1 : 0);
+  if (multi_ && world_ > 1) {
+    const ShardBufs sb = shards_[0]->shard_bufs();
+    std::vector<double> chunk(8, 0.0), all(size_t(world_) * 8, 0.0);
+    chunk[0] = double(agreed);
+    AAPDHG_CUDA(cudaMemcpyAsync(sb.scal + size_t(rank_) * 8, chunk.data(), sizeof(double) * 8,
+                                cudaMemcpyHostToDevice, stream_));
+    allgather(SCAL);
+    AAPDHG_CUDA(cudaMemcpyAsync(all.data(), sb.scal, sizeof(double) * all.size(),
+                                cudaMemcpyDeviceToHost, stream_));
+    AAPDHG_CUDA(cudaStreamSynchronize(stream_));
+    for (int r = 0; r < world_; ++r) agreed = std::min(agreed, int(all[size_t(r) * 8]));
+  }
+  if (cond_graph && agreed < 2) {
+    cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    cond_graph = false;
+    each([&](Problem& s) { s.sh_set_conditions(0, 0); });  // no conditional nodes
+  }
+  if (!cond_graph && agreed >= 1) {
     const uint64_t l0 = launches();
     AAPDHG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     core();

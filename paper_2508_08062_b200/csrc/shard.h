@@ -16,6 +16,8 @@ struct Partition {
   int64_t maxr = 0, maxc = 0;
 };
 Partition plan_partition(const aapdhg_csr_view& k, int world);
+Partition plan_partition_weights(const aapdhg_csr_view& k, const std::vector<int64_t>& wc,
+                                 int world);
 
 class ShardGroup {
  public:

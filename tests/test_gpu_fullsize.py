@@ -92,3 +92,34 @@ def test_fullsize_first_iterates_match_reference(cfg_id):
         assert np.max(np.abs(v[idx] - want)) <= 1e-10 * max(np.max(np.abs(want)), 1e-300)
     # the device's own step size (seeded power iteration) agrees with the reference's
     assert abs(own_tau - tau) <= 1e-10 * tau, (own_tau, tau)
+
+
+def test_config1_iterations_to_kkt_1e6_within_reference_envelope():
+    """BASELINE configs[1] to max KKT <= 1e-6 (the metric's time-to-1e-6 KKT),
+    TREE order (the bench path), at the reference's tau and at tau shifted by
+    +-1 ulp. AA-PDHG is chaotic under rounding: the reference's own count
+    spans [32,566, 35,588] over its strict / FMA / reassociated builds and
+    +-1-2 ulp changes of tau (tests/golden/config1_envelope.json). Every GPU
+    count must fall within that envelope widened by the north-star 2%, with
+    KKT <= 1e-6 and the objective within 1e-6 of the planted optimum
+    (c'x* = b'y*) and of the reference's final objective."""
+    env = json.loads((GOLDEN / "config1_envelope.json").read_text())
+    lo, hi = env["envelope"]
+    ref = env["arms"]["ref"]
+    p = problems.make_config(1)
+    counts = []
+    with Solver(p) as s:
+        tau0 = ref["tau"]
+        for ulps in (0, 1, -1):
+            tau = float(np.nextafter(tau0, np.inf if ulps > 0 else -np.inf)) if ulps else tau0
+            cfg = SolverConfig(method=Method.AA_PDHG, m=10, toll=1e-12, kkt_eps=1e-6,
+                               kkt_terminate=True, max_iters=200000, max_wall_seconds=600.0,
+                               tau=tau, sigma=tau, reduction="tree")
+            r = s.solve(cfg).result
+            assert r.status.name == "KKT_TOL"
+            assert r.kkt.max() <= 1e-6
+            assert abs(r.objective - p.planted_objective) <= 1e-6 * abs(p.planted_objective)
+            assert abs(r.objective - ref["objective"]) <= 1e-6 * abs(ref["objective"])
+            counts.append(r.iterations)
+    for c in counts:
+        assert 0.98 * lo <= c <= 1.02 * hi, (counts, env["envelope"])
