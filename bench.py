@@ -33,11 +33,51 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CONFIG_ID = 1
+CONFIG_ID = 1  # the workload (select_workload)
 MEMORY = 10
 TOLL = 1e-6
 GATHER_CEILING = 240.3e9  # measured random-gather rate (profiles/r01/gather.txt)
-METRIC = "AA-PDHG fp64 iterations/sec (BASELINE configs[1]: 100k x 200k, 4M nnz, m=10)"
+METRICS = {
+    1: "AA-PDHG fp64 iterations/sec (BASELINE configs[1]: 100k x 200k, 4M nnz, m=10)",
+    4: "AA-PDHG fp64 iterations/sec (BASELINE configs[4]: 20M x 40M, 400M nnz, m=10)",
+}
+METRIC = METRICS[1]
+WORKLOADS = {
+    1: "configs[1] planted LP 100000x200000, 20 nnz/col (4.0M nnz), AA-PDHG m=10, D=1, eps=1, "
+       "toll=1e-6",
+    4: "configs[4] planted LP 20000000x40000000, 10 nnz/col (400M nnz), AA-PDHG m=10, D=1, "
+       "eps=1, toll=1e-6",
+}
+
+
+def select_workload(args, world):
+    """configs[1] at N = 1 (the metric's single-GPU config, BASELINE.json),
+    configs[4] at N > 1 (the north-star scaling LP) unless --workload says."""
+    global CONFIG_ID, METRIC
+    if args.workload == "config1":
+        CONFIG_ID = 1
+    elif args.workload == "config4":
+        CONFIG_ID = 4
+    else:
+        CONFIG_ID = 1 if world == 1 and not args.loopback else 4
+    METRIC = METRICS[CONFIG_ID]
+
+
+def load_workload(cfg_id, rank=0, world=1, barrier=None, torch_sort=True):
+    """The seeded instance; configs[4] through the on-disk cache
+    (problems.cached_config): local rank 0 generates it once, every rank
+    memory-maps the same file."""
+    from paper_2508_08062_b200 import problems
+    if cfg_id != 4:
+        return problems.make_config(cfg_id)
+    if not torch_sort:  # (the reference arm generates without the GPU)
+        os.environ["AAPDHG_GEN_NO_TORCH"] = "1"
+    if world > 1 and barrier is not None:
+        if int(os.environ.get("LOCAL_RANK", "0")) == 0:
+            problems.cached_config(4)
+        barrier()
+        return problems.cached_config(4, generate=False)
+    return problems.cached_config(4)
 
 
 def host_cpu():
@@ -53,9 +93,9 @@ def host_cpu():
     return f"{os.cpu_count()}-core {model}"
 
 
-def workload_config(p):
-    return {"workload": "configs[1] planted LP 100000x200000, 20 nnz/col (4.0M nnz), "
-                        "AA-PDHG m=10, D=1, eps=1, toll=1e-6",
+def workload_config(p, cfg_id=None):
+    cfg_id = CONFIG_ID if cfg_id is None else cfg_id
+    return {"workload": WORKLOADS[cfg_id],
             "rows": p.k.nrows, "cols": p.n(), "nnz": p.k.nnz, "memory": MEMORY,
             "l2": "working set > 126 MB L2 (K + K' + history >= 150 MB), no flush"}
 
@@ -164,10 +204,12 @@ def cpu_reference_sample(p, tau, iters):
 
 
 def run_reference_arm(args, rank, world):
-    from paper_2508_08062_b200 import problems
     if rank != 0:
         return
-    p = problems.make_config(CONFIG_ID)
+    p = load_workload(CONFIG_ID, torch_sort=False)
+    if CONFIG_ID == 4:  # ~50 s per reference iteration: a bounded sample
+        args.steps = min(args.steps, 2)
+        args.warmup = min(args.warmup, 1)
     from oracle.pyoracle import Oracle, ref_available
     kind = "reference" if ref_available() else "port"
     orc = Oracle("ref" if kind == "reference" else "port")
@@ -188,9 +230,9 @@ def run_reference_arm(args, rank, world):
             "parallelism": "single (the reference solve is single-threaded)",
             "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": 1, "kind": kind,
                              "host": host_cpu(),
-                             "sample": f"{out.result.iterations} iterations of configs[1] "
-                                       f"(explicit tau), 1 thread on a {host_cpu()}: the "
-                                       f"reference solve() is single-threaded"},
+                             "sample": f"{out.result.iterations} iterations of "
+                                       f"configs[{CONFIG_ID}] (explicit tau), 1 thread on a "
+                                       f"{host_cpu()}: the reference solve() is single-threaded"},
             "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -205,7 +247,8 @@ def pinned_problem(torch, p):
 
     def pin(a):
         a = np.ascontiguousarray(a)
-        t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+        t = torch.empty(a.shape, dtype=torch.from_numpy(np.empty(0, a.dtype)).dtype,
+                        pin_memory=True)
         keep.append(t)
         v = t.numpy()
         v[...] = a
@@ -237,8 +280,12 @@ def run_ours(args, rank, world, local_rank):
 
     dev = local_rank
     torch.cuda.set_device(dev)
-    p = problems.make_config(CONFIG_ID)
-    dist = world > 1 or args.shard
+    dist = world > 1 or args.shard or args.loopback
+    if world > 1:
+        import torch.distributed as tdist
+        p = load_workload(CONFIG_ID, rank, world, barrier=tdist.barrier)
+    else:
+        p = load_workload(CONFIG_ID)
     if dist:
         import torch.distributed as tdist
         if not tdist.is_initialized():  # --shard at N=1
@@ -255,7 +302,9 @@ def run_ours(args, rank, world, local_rank):
         from paper_2508_08062_b200 import DistConfig, nccl_unique_id
 
         transport = args.transport
-        if transport == "p2p":  # every rank must reach every peer (else NCCL)
+        if args.loopback:  # every shard in this process, on this one GPU (a dry run)
+            transport = "loopback_p2p" if transport == "p2p" else "loopback"
+        elif transport == "p2p":  # every rank must reach every peer (else NCCL)
             ok = world <= 8 and all(torch.cuda.can_device_access_peer(dev, q)
                                     for q in range(torch.cuda.device_count()) if q != dev)
             flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
@@ -265,15 +314,19 @@ def run_ours(args, rank, world, local_rank):
         args.transport = transport
 
         def dcfg(tr):  # a fresh NCCL id per communicator (ids are single-use)
+            if tr.startswith("loopback"):
+                return DistConfig(world=args.loopback, rank=0, transport=tr)
             box = [nccl_unique_id() if rank == 0 else None]
             tdist.broadcast_object_list(box, src=0)
             return DistConfig(world=world, rank=rank, transport=tr, nccl_id=box[0])
+        t_create = time.perf_counter()
         s = Solver(p, device=dev, dist=dcfg(transport))
+        t_create = time.perf_counter() - t_create
         if transport == "p2p" and world > 1:
             # self-check: the peer-memory exchanges must reproduce the NCCL
             # all-gathers bit for bit (same kernels, same data) over 60
             # iterations with AA steps; otherwise run on NCCL
-            chk = solver_config(tau=0.0775, max_iters=60)
+            chk = solver_config(tau=s.select_step_sizes(solver_config()).tau, max_iters=60)
             a = s.solve(chk).trajectory["g_norm"]
             with Solver(p, device=dev, dist=dcfg("nccl")) as s2:
                 b = s2.solve(chk).trajectory["g_norm"]
@@ -286,7 +339,9 @@ def run_ours(args, rank, world, local_rank):
                 args.transport = "nccl (p2p self-check failed)"
                 s = Solver(p, device=dev, dist=dcfg("nccl"))
     else:
+        t_create = time.perf_counter()
         s = Solver(p, device=dev)
+        t_create = time.perf_counter() - t_create
     lib = s.lib
     check(lib.aapdhg_cuda_set_stream(s.h, C.c_void_p(stream.cuda_stream)), errbuf())
     tau = s.select_step_sizes(solver_config()).tau
@@ -337,7 +392,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- time to tolerance (full solve to toll 1e-6, step sizes included) --
     ttt = None
-    if not args.no_ttt:
+    if not args.no_ttt and CONFIG_ID == 1:
         ttt = time_to_tol(args, p, s)
     s.close()
 
@@ -367,13 +422,18 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- CPU baseline on this host (rank 0, N=1 only) ----------------------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and CONFIG_ID == 1:
         v, kind, dt = cpu_reference_sample(p, tau, args.cpu_iters)
         cpu = {"value": v, "unit": "iterations/s", "cores": 1, "kind": kind,
                "host": host_cpu(),
                "sample": f"{args.cpu_iters} iterations of configs[1] (explicit tau), "
                          f"{dt:.1f} s, 1 thread on a {host_cpu()}: the reference "
                          f"solve() is single-threaded"}
+
+    # ---- configs[4] (20M x 40M, 400M nnz) on this one GPU -----------------
+    c4 = None
+    if rank == 0 and world == 1 and CONFIG_ID == 1 and not args.no_config4 and not dist:
+        c4 = config4_leg(args, torch, dev, stream)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
@@ -388,8 +448,91 @@ def run_ours(args, rank, world, local_rank):
                 "iterations_timed": iters, "aa_steps_timed": out.result.i,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "time_to_tol": ttt,
                 "clocks": clk.summary(), "gpu_launches": int(launches.value),
-                "gpu_loop_iterations": int(loop_iters.value)}
+                "gpu_loop_iterations": int(loop_iters.value),
+                "create_s": t_create}
+        if args.loopback:
+            line["parallelism"] = (f"loopback{args.loopback}: {args.loopback} shards in one "
+                                   f"process on one GPU ({args.transport} exchanges) — a dry "
+                                   f"run of the sharded path, not a multi-GPU measurement")
+        if c4 is not None:
+            line["config4"] = c4
         print(json.dumps(line), flush=True)
+
+
+def iteration_bytes(p, iters, aa_steps, memory=MEMORY):
+    """Algorithmic bytes of `iters` iterations of which `aa_steps` took an AA
+    step: every iteration K1 + K2 with the history push; an
+    AA step adds the Gram pass 8N(p+3), the mix 8N(2p+3) and the K x
+    recache 12 nnz + 4(m+1) + 8n + 8m."""
+    n, m, nnz = p.n(), p.k.nrows, p.k.nnz
+    N = n + m
+    aa = 8 * N * (memory + 3) + 8 * N * (2 * memory + 3) + 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
+    return iters * kernel_bytes(p, "k_plain_loop") + aa_steps * aa
+
+
+def config4_leg(args, torch, dev, stream):
+    """configs[4] — the largest LP of BASELINE.json, the north-star scaling
+    LP — on this single GPU: generation (cached on disk), device ingestion,
+    `steps` resident iterations (device events), the iteration roofline, the
+    per-kernel times and the e2e path from page-locked buffers."""
+    import ctypes as C
+
+    from paper_2508_08062_b200 import Solver
+    from paper_2508_08062_b200.api import check, errbuf
+    t0 = time.perf_counter()
+    p = load_workload(4)
+    gen_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    s = Solver(p, device=dev)
+    create_s = time.perf_counter() - t0
+    lib = s.lib
+    check(lib.aapdhg_cuda_set_stream(s.h, C.c_void_p(stream.cuda_stream)), errbuf())
+    tau = s.select_step_sizes(solver_config()).tau
+    s.solve(solver_config(tau=tau, max_iters=max(args.warmup, 3)))
+    n, m = p.n(), p.k.nrows
+    outs = tuple(torch.empty(k, dtype=torch.float64, pin_memory=True).numpy() for k in (n, m, n))
+    cfg = solver_config(tau=tau, max_iters=args.steps)
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        out = s.solve(cfg, out=outs)
+        ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1)
+    iters, aa = out.result.iterations, out.result.i
+    peak, peak_kind = measured_peak()
+    byts = iteration_bytes(p, iters, aa)
+    per_kernel = kernel_roofline(args, p, s, lib, tau).get("per_kernel_us")
+    s.close()
+    del outs
+    # e2e: the LP in page-locked buffers, create + solve + download
+    hp, hout = pinned_problem(torch, p)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    s2 = Solver(hp, device=dev)
+    out2 = s2.solve(solver_config(tau=tau, max_iters=args.steps), out=hout)
+    e2e_s = time.perf_counter() - t0
+    s2.close()
+    h2d = sum(a.nbytes for a in (p.k.row_ptr, p.k.col_idx, p.k.vals, p.c, p.q, p.l, p.u))
+    d2h = (p.n() * 16 + p.k.nrows * 8) + out2.trajectory.nbytes
+    return {"workload": WORKLOADS[4], "rows": m, "cols": n, "nnz": int(p.k.nnz),
+            "value": iters / (ms / 1e3), "unit": "iterations/s", "ms_per_step": ms / max(iters, 1),
+            "iterations_timed": iters, "aa_steps_timed": aa,
+            "roofline": {"bound": "hbm", "scope": "whole iteration (all kernels of the timed "
+                                                  "solve, device events)",
+                         "achieved": byts / (ms / 1e3) / 1e9, "peak": peak,
+                         "peak_source": peak_kind, "unit": "GB/s",
+                         "frac": byts / (ms / 1e3) / 1e9 / peak,
+                         "bytes": byts, "bytes_per_plain_iteration": kernel_bytes(p, "k_plain_loop")},
+            "per_kernel_us": per_kernel,
+            "e2e": {"value": out2.result.iterations / e2e_s, "unit": "iterations/s",
+                    "seconds": e2e_s, "h2d_bytes_per_step": h2d / max(out2.result.iterations, 1),
+                    "d2h_bytes_per_step": d2h / max(out2.result.iterations, 1)},
+            "generate_or_map_s": gen_s, "create_s": create_s,
+            "cpu_reference_note": "reference solve() on configs[4]: ~50 s per iteration on one "
+                                  "core and ~30 GB RAM (tests/golden/fullsize_cfg4.json: 20 "
+                                  "iterations in 1036 s in the build container); not re-run here"}
 
 
 def plain_loop_roofline(args, p, plain, step_ms):
@@ -502,6 +645,12 @@ def main():
                     help="use the sharded solve even at N=1 (exercises the N>1 path)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel, if captured")
+    ap.add_argument("--workload", choices=["auto", "config1", "config4"], default="auto",
+                    help="auto: configs[1] at N=1, configs[4] (the scaling LP) at N>1")
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="dry run of the sharded solve: K in-process shards on this one GPU")
+    ap.add_argument("--no-config4", action="store_true",
+                    help="skip the configs[4] single-GPU leg of the N=1 line")
     args = ap.parse_args()
     if args.impl == "reference":
         # bounded CPU sample: <= 500 iterations (~20 s of reference work at
@@ -512,6 +661,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    select_workload(args, world)
     if world > 1 and args.impl == "ours":
         import torch
         import torch.distributed as tdist

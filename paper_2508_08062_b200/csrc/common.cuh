@@ -130,6 +130,8 @@ struct DevParams {
   // per-op FAA entries (engine.cu faa_op): stages to skip (kFaaSkip*), and
   // where to write the kept columns' R (p x p column-major) when non-null
   int32_t faa_skip;
+  int32_t no_stop_predict;  // k_plain_loop always speculates (AAPDHG_STOP_PREDICT=1: predicts)
+  int32_t phase_prefetch;   // k_plain_loop: L2 bulk prefetch of the next phase's slice streams
   double* qr_r_out;
 };
 enum { kFaaSkipAngle = 1, kFaaSkipLength = 2 };

@@ -1003,6 +1003,13 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.pow_len = method == AAPDHG_METHOD_PDHG ? 0 : pow_len_;
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
+  // predicted stops in k_plain_loop (stop_likely): measured a net loss on
+  // configs[1] (20,000 iterations: 17.3k vs 18.9k it/s; 20: within noise),
+  // so off unless AAPDHG_STOP_PREDICT=1
+  P.no_stop_predict = env_int("AAPDHG_STOP_PREDICT", 0) == 0 ? 1 : 0;
+  // one-phase-ahead L2 prefetch of the slice streams (prefetch_slice_streams):
+  // measured a loss on configs[1] (17.2k vs 18.6k it/s), opt-in experiment
+  P.phase_prefetch = env_int("AAPDHG_PREFETCH", 0);
   const bool blk1 = !serial && ktb_.nb() > 1, blk2 = !serial && kb_.nb() > 1;
   const CsrDev& K1m = blk1 ? ktb_.blk.back() : KTm(serial);
   const CsrDev& K2m = blk2 ? kb_.blk.back() : Km(serial);

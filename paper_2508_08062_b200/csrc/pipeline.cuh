@@ -241,6 +241,25 @@ __device__ __forceinline__ void l2_prefetch(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// One phase ahead (k_plain_loop): lane 0 of each warp asks L2 for the
+// (column, value) stream of the warp's slice of the OTHER matrix, so the
+// next phase's dependent stream -> gather chains start from L2 instead of
+// DRAM. A slice's streams are contiguous: 32 L int32 and 32 L doubles at a
+// 32-element-aligned offset (bulk prefetches need 16-byte granules).
+__device__ __forceinline__ void prefetch_slice_streams(const CsrDev& A, int bid) {
+  if ((threadIdx.x & 31) != 0 || bid < A.nblk_long || A.interleave) return;
+  const int b = bid - A.nblk_long, warp = threadIdx.x >> 5;
+  const int sl = int(int64_t(b) * A.nslices / A.nblk_short) + warp;
+  if (sl >= int(int64_t(b + 1) * A.nslices / A.nblk_short)) return;
+  const int L = __ldg(A.sl_len + sl);
+  const int64_t base = __ldg(A.sl_ptr + sl);
+  if (L <= 0) return;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.sci + base),
+               "r"(uint32_t(128 * L)) : "memory");
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.sv + base),
+               "r"(uint32_t(256 * L)) : "memory");
+}
+
 // pre(row): called in the row's owning lane right after the metadata loads
 // when the whole slice is one unroll group (short rows): the fused kernels
 // prefetch their epilogue operands into L2 so the epilogue does not pay a
@@ -766,7 +785,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     double s;
     const int row = row_sum<false>(A, x, s, NoPre{}, -1, rep);
     if (row == -2) break;
-    if (row >= 0) part[row] = first ? s : __dadd_rn(part[row], s);
+    if (row >= 0) __stcs(part + row, first ? s : __dadd_rn(__ldcs(part + row), s));
   }
 }
 
@@ -1025,7 +1044,12 @@ __device__ unsigned long long g_plain_dbg[8];
 struct GridBar {
   unsigned long long arrive1;  // barrier 1: arrivals (low 40 bits) + stops (high bits)
   unsigned long long arrive2;  // barrier 2: arrivals
-  unsigned long long pad[2];
+  // predicted stops: the control publishes, after its barrier-1 arrival,
+  // decided = k + 1 for iteration k, and before it the last two ||g|| and
+  // the safeguard threshold D ||g0|| (i+1)^-(1+eps) of the current i
+  unsigned long long decided;
+  unsigned long long pad0;
+  double g_last, g_prev, thr, pad1;
 };
 constexpr unsigned long long kBarCount = (1ull << 40) - 1;
 constexpr unsigned long long kBarStop = 1ull << 40;
@@ -1047,6 +1071,9 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 // Arrive at a barrier of nb participants and wait for the instance to fill.
 // Spins with relaxed loads (an acquire load invalidates the SM's L1 — under
 // CTAs still gathering — on every poll), then acquires once. Thread 0 only.
@@ -1058,6 +1085,27 @@ __device__ __forceinline__ unsigned long long bar_arrive_wait(unsigned long long
   while ((ld_relaxed(p) & kBarCount) < target) {
   }
   return ld_acquire(p);
+}
+
+// A worker's guess, after barrier 2 of iteration k = st.k, that the control
+// will stop the launch after k (st: the state before k's commit; wp:
+// iterations already decided in this launch). Exact for the batch end and
+// max_iters; for the safeguard and the tolerance, ||g_k|| is extrapolated
+// geometrically from the last two published norms (between AA steps the
+// residual decays smoothly: configs[1] trajectories predict every AA step)
+// with a 0.5% margin. A wrong guess costs the wait for the decision only.
+__device__ __forceinline__ bool stop_likely(const DevParams* P, const GridBar* gb,
+                                            const DevState& st, int wp) {
+  if (P->no_stop_predict) return false;
+  if (st.batch_left - (wp + 1) <= 0) return true;
+  if (st.k > 0 && st.i + st.j >= P->max_iters) return true;
+  if (wp == 0 || st.k < 2) return false;  // first iteration after a launch: no history
+  const double g1 = __ldcg(&gb->g_last), g2 = __ldcg(&gb->g_prev);
+  if (!(g1 > 0.0) || !(g2 > 0.0)) return false;
+  const double gp = g1 < g2 ? g1 * (g1 / g2) : g1;
+  if (gp < 1.005 * P->toll) return true;
+  const double thr = __ldcg(&gb->thr);
+  return thr > 0.0 && gp <= 1.005 * thr;
 }
 
 // The control CTA of k_plain_loop: state and parameters in shared memory for
@@ -1072,9 +1120,19 @@ __device__ __noinline__ void plain_loop_control(const IterBufs& B, const DevPara
   __syncthreads();
   const uint64_t t_start = globaltimer_ns();
   uint64_t passes = 0;
+  unsigned long long target1 = 0;  // barrier-1 instance this CTA arrived at early (0: none)
   for (;;) {
-    // barrier 1 of iteration k: K1(k) done -> fold its partials
-    if (threadIdx.x == 0) bar_arrive_wait(&gb->arrive1, 1, G);
+    // barrier 1 of iteration k: K1(k) done -> fold its partials (after a
+    // plain decision the control has already arrived: it only waits)
+    if (threadIdx.x == 0) {
+      if (target1) {
+        while ((ld_relaxed(&gb->arrive1) & kBarCount) < target1) {
+        }
+        ld_acquire(&gb->arrive1);
+      } else {
+        bar_arrive_wait(&gb->arrive1, 1, G);
+      }
+    }
     __syncthreads();
     double t1[P1_COUNT];
     reduce_partial_rows<P1_COUNT>(B.part1, nb1, t1, red);
@@ -1106,12 +1164,29 @@ __device__ __noinline__ void plain_loop_control(const IterBufs& B, const DevPara
       sm.plain_ns += globaltimer_ns() - t_start;
     }
     if (threadIdx.x == 32) control_commit(&pr, &sm, k, dec);
+    if (threadIdx.x == 0 && !sm.done) {  // for the workers' stop prediction
+      const double pw = sm.i < pr.pow_len ? pr.pow_tab[sm.i]
+                                          : pow((double)sm.i + 1.0, -(1.0 + pr.safeguard_eps));
+      gb->g_prev = gb->g_last;
+      gb->g_last = sm.gkn;
+      gb->thr = pr.method != AAPDHG_METHOD_PDHG ? __dmul_rn(__dmul_rn(pr.safeguard_d, sm.g0n), pw)
+                                                : 0.0;
+    }
     __syncthreads();
     if (stop) {
-      // release the workers (they drop K1(k+1)), then hand the state over
-      if (threadIdx.x == 0) atom_add_acq_rel(&gb->arrive1, 1 + kBarStop);
+      // release the workers (they drop K1(k+1), or skip it on a predicted
+      // stop), then hand the state over
+      if (threadIdx.x == 0) {
+        atom_add_acq_rel(&gb->arrive1, 1 + kBarStop);
+        st_release(&gb->decided, k + 1);
+      }
       state_store(S, &sm);
       return;
+    }
+    if (threadIdx.x == 0) {  // plain: arrive at barrier 1 of k+1 now, then publish
+      const unsigned long long prev = atom_add_acq_rel(&gb->arrive1, 1);
+      target1 = ((prev & kBarCount) / G + 1) * G;
+      st_release(&gb->decided, k + 1);
     }
   }
 }
@@ -1133,12 +1208,15 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   }
   unsigned long long h0 = 0;  // stop flags raised before this launch
   if (threadIdx.x == 0) h0 = ld_relaxed(&gb->arrive1) >> 40;
+  int wp = 0;  // iterations decided in this launch (thread 0)
 #ifdef AAPDHG_PLAIN_STAMPS
   // experiment build only: per worker and iteration, the K1 phase, the bar 1
   // wait, the K2 phase, the bar 2 wait (summed, aapdhg_cuda_plain_stamps)
   uint64_t ps0 = globaltimer_ns(), ps1 = 0, ps2 = 0, ps3 = 0;
 #endif
+  const bool pf = P->phase_prefetch != 0;
   for (;;) {
+    if (pf && bid < nb2) prefetch_slice_streams(K, bid);  // K2's streams, one phase ahead
     if (bid < nb1) dual_side_rows<false, PUSH, 0, true>(KT, B, P, &st, bid, nb1, red);
     __syncthreads();
 #ifdef AAPDHG_PLAIN_STAMPS
@@ -1150,6 +1228,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 #ifdef AAPDHG_PLAIN_STAMPS
     if (threadIdx.x == 0) ps2 = globaltimer_ns();
 #endif
+    if (pf && bid < nb1) prefetch_slice_streams(KT, bid);  // the next K1's streams
     double acc[P2_COUNT] = {0.0, 0.0, 0.0};
     if (bid < nb2) {
       primal_side_rows<false, PUSH, true>(K, B, P, &st, bid, acc);
@@ -1164,11 +1243,27 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 #endif
     if (threadIdx.x == 0) {
       bar_arrive_wait(&gb->arrive2, 1, G);
+      s_stop = 0;
+      // Predicted stop: the control is about to end the launch after
+      // iteration k (batch end, max_iters, or ||g_k|| extrapolated from the
+      // last two reaching the safeguard threshold — an AA attempt — or the
+      // tolerance). Then K1(k+1) would be dropped: wait for the decision
+      // instead (decided >= k + 1), and leave if it is a stop.
+      if (stop_likely(P, gb, st, wp)) {
+        while (ld_acquire(&gb->decided) < st.k + 1) {
+        }
+        if ((ld_relaxed(&gb->arrive1) >> 40) != h0) {
+          atom_add_acq_rel(&gb->arrive1, 1);  // (keeps the barrier count whole)
+          s_stop = 1;
+        }
+      }
+      ++wp;
       // the roles of iteration k+1 if iteration k is a plain step
       st.aa_ok = 0;
       control_commit(P, &st, st.k, Decision{0, 1});
     }
     __syncthreads();
+    if (s_stop) return;
 #ifdef AAPDHG_PLAIN_STAMPS
     if (threadIdx.x == 0) {
       const uint64_t ps4 = globaltimer_ns();

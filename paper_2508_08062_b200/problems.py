@@ -32,7 +32,8 @@ def _argsort_distinct(key: np.ndarray) -> np.ndarray:
     """The sorting permutation of distinct int64 keys (unique, so any sort
     gives it): on a CUDA device when one is present and the array is large
     (config 4: 400M keys, minutes in numpy), numpy otherwise."""
-    if key.size > (16 << 20):
+    import os
+    if key.size > (16 << 20) and os.environ.get("AAPDHG_GEN_NO_TORCH") != "1":
         try:
             import torch
             if torch.cuda.is_available():
@@ -180,3 +181,60 @@ def toy() -> ProblemData:
     k = SparseMatrix(1, 1, np.array([0, 1]), np.array([0]), np.array([1.0]))
     return ProblemData(k, 0, np.zeros(1), np.array([3.0]), np.zeros(1), np.full(1, np.inf),
                        name="toy")
+
+
+# ---------------------------------------------------------------------------
+# On-disk instances (config 4 takes minutes to generate and ~5 GB): generated
+# once per box into a cache directory and memory-mapped by every process
+# that needs it (every rank of a sharded run maps the same pages).
+
+GENERATOR_VERSION = 1  # bump when a generator's output changes
+
+
+def cache_dir(cfg: int, scale: float = 1.0) -> "Path":
+    import os
+    from pathlib import Path
+    root = Path(os.environ.get("AAPDHG_INSTANCE_CACHE", "/tmp/aapdhg_instances"))
+    return root / f"cfg{cfg}_s{scale:g}_v{GENERATOR_VERSION}"
+
+
+_FIELDS = ("row_ptr", "col_idx", "vals", "c", "q", "l", "u")
+
+
+def save_instance(p: ProblemData, d) -> None:
+    """Writes the arrays as .npy files, then a `complete` marker (written
+    last, so a reader never maps a half-written instance)."""
+    import json
+    d.mkdir(parents=True, exist_ok=True)
+    arrays = dict(row_ptr=p.k.row_ptr, col_idx=p.k.col_idx, vals=p.k.vals, c=p.c, q=p.q,
+                  l=p.l, u=p.u)
+    for k, a in arrays.items():
+        np.save(d / f"{k}.npy.tmp.npy", a)
+        (d / f"{k}.npy.tmp.npy").replace(d / f"{k}.npy")
+    meta = dict(m=int(p.k.nrows), n=int(p.k.ncols), m1=int(p.m1), name=p.name,
+                planted_objective=getattr(p, "planted_objective", None))
+    (d / "meta.json").write_text(json.dumps(meta))
+    (d / "complete").write_text("ok")
+
+
+def load_instance(d) -> ProblemData:
+    """Memory-maps a saved instance (read-only pages, shared between processes)."""
+    import json
+    meta = json.loads((d / "meta.json").read_text())
+    a = {k: np.load(d / f"{k}.npy", mmap_mode="r") for k in _FIELDS}
+    k = SparseMatrix(meta["m"], meta["n"], a["row_ptr"], a["col_idx"], a["vals"])
+    p = ProblemData(k, meta["m1"], a["c"], a["q"], a["l"], a["u"], name=meta["name"])
+    if meta.get("planted_objective") is not None:
+        p.planted_objective = meta["planted_objective"]
+    return p
+
+
+def cached_config(cfg: int, scale: float = 1.0, generate: bool = True) -> ProblemData:
+    """make_config(cfg, scale) through the on-disk cache: generated (by the
+    caller with generate=True) when absent, memory-mapped afterwards."""
+    d = cache_dir(cfg, scale)
+    if not (d / "complete").exists():
+        if not generate:
+            raise FileNotFoundError(f"instance {d} is not generated yet")
+        save_instance(make_config(cfg, scale), d)
+    return load_instance(d)
