@@ -832,6 +832,47 @@ __global__ void k_aa_commit(const DevParams* __restrict__ P, DevState* S) {
   state_store(S, &sm);
 }
 
+// The K x recache of an accepted candidate with the AA branch's commit in
+// its last CTA (one launch instead of k_spmv + k_aa_commit). Every CTA
+// reads the roles when it starts; the last one to finish (ticket) rotates
+// them, so no reader sees the new roles. A SingularError fallback has no
+// candidate: CTA 0 only commits.
+template <bool SERIAL>
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+    k_spmv_commit(CsrDev A, VecRef xr, RowsumArgs o, const DevParams* __restrict__ P,
+                  DevState* S, unsigned int* ticket) {
+  if (S->done || !S->aa_attempt) return;
+  __shared__ DevState sm;
+  if (!S->aa_ok) {
+    if (blockIdx.x == 0) {
+      state_load(&sm, S);
+      if (threadIdx.x == 0) advance(P, &sm);
+      state_store(S, &sm);
+    }
+    return;
+  }
+  const double* x = xr.get(S);
+  double* out = o.out_pool + (int64_t)S->kx_idx[o.out_role] * o.out_stride;
+  for (int rep = 0;; ++rep) {
+    double v;
+    const int row = row_sum<SERIAL>(A, x, v, NoPre{}, -1, rep);
+    if (row == -2) break;
+    if (row >= 0) out[row] = v;
+  }
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  if (threadIdx.x == 0) *ticket = 0u;
+  state_load(&sm, S);
+  if (threadIdx.x == 0) advance(P, &sm);
+  state_store(S, &sm);
+}
+
 // ---------------------------------------------------------------------------
 // setup / finishing / power iteration helpers
 // ---------------------------------------------------------------------------

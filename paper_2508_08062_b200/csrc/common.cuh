@@ -194,6 +194,8 @@ struct IterBufs {
   double* du;      // cap x N
   double* dg;      // cap x N
   double* T;       // n
+  double* T2;      // n: SERIAL k_plain_loop, K'y of odd iterations (the control reads
+                   // iteration k's while the speculative K1(k+1) writes the other)
   double* part1;   // P1_COUNT x nblk1 (per CTA)
   double* part2;   // P2_COUNT x nblk2
   const double* rinit1;  // L2-blocked K': partial K'y of the earlier column passes

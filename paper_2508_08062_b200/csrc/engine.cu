@@ -503,6 +503,7 @@ void Problem::ensure_iter_buffers(int method, int cap) {
   upool_.reserve(sizeof(double) * 4 * std::max<int64_t>(N_, 1));
   kxpool_.reserve(sizeof(double) * 3 * std::max<int64_t>(m_, 1));
   T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
+  T2_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
   part1_.reserve(sizeof(double) * P1_COUNT * std::max(nblk1, 1));
   part2_.reserve(sizeof(double) * P2_COUNT * std::max(nblk2, 1));
 
@@ -513,6 +514,10 @@ void Problem::ensure_iter_buffers(int method, int cap) {
   rec_cap_ = kRecCap;
   dparams_.reserve(sizeof(DevParams));
   dstate_.reserve(sizeof(DevState));
+  if (!ticket_.p) {  // k_spmv_commit's last-CTA ticket (returns to 0 after each launch)
+    ticket_.reserve(sizeof(unsigned int) * 4);
+    AAPDHG_CUDA(cudaMemsetAsync(ticket_.p, 0, ticket_.bytes, stream_));
+  }
   ndot_tile_ = int((N_ + kDotChunk - 1) / kDotChunk);
   if (method != AAPDHG_METHOD_PDHG) {
     gpool_.reserve(sizeof(double) * 2 * std::max<int64_t>(N_, 1));
@@ -542,6 +547,7 @@ IterBufs Problem::iter_bufs() {
   B.du = du_.as<double>();
   B.dg = dg_.as<double>();
   B.T = T_.as<double>();
+  B.T2 = T2_.as<double>();
   B.part1 = part1_.as<double>();
   B.part2 = part2_.as<double>();
   B.c = c_.as<double>();
@@ -666,6 +672,14 @@ auto k2_kernel(const CsrDev& A) {
   return A.interleave ? k_primal_side<SER, PUSH, 0, true> : k_primal_side<SER, PUSH>;
 }
 
+// the persistent plain-iteration grid for a push / reduction order
+using PlainLoopKernel = void (*)(CsrDev, CsrDev, IterBufs, const DevParams*, DevState*, GridBar*,
+                                 int, int);
+static PlainLoopKernel plain_loop_kernel(bool push, bool serial) {
+  return serial ? (push ? k_plain_loop<true, true> : k_plain_loop<false, true>)
+                : (push ? k_plain_loop<true, false> : k_plain_loop<false, false>);
+}
+
 int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
   int nodes = 0;
   const bool ser = su.serial, push = su.push;
@@ -679,7 +693,7 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    auto kern = push ? k_plain_loop<true> : k_plain_loop<false>;
+    auto kern = plain_loop_kernel(push, ser);
     LAUNCH("k_plain_loop", AAPDHG_CUDA(cudaLaunchKernelEx(&cfg, kern, su.pk1, su.pk2, su.B, su.P,
                                                           su.S, su.gb, su.pk1.grid(),
                                                           su.pk2.grid())));
@@ -769,15 +783,22 @@ int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
   }
   LAUNCH("k_aa_solve", k_aa_solve<<<1, 1024, aa_smem(su.cap), s>>>(su.D, su.P, su.S, 0));
   LAUNCH("k_mix", k_mix<<<grid_for(N_), kThreads, 0, s>>>(su.B, su.B.dg, su.P, su.S, 1));
-  if (m_ > 0) {  // K x recache of the accepted candidate
+  if (m_ > 0 && Km(su.serial).grid() > 0) {
+    // K x recache of the accepted candidate, the commit in its last CTA
     RowsumArgs r{};
     r.out_pool = su.B.kxpool;
     r.out_role = KX_CAND;
     r.out_stride = m_;
-    nodes += spmv(s, Km(su.serial), VecRef{nullptr, su.B.upool, U_CAND, N_, 0}, r, su.serial, su.S, 1,
-                  nullptr);
+    const CsrDev& A = Km(su.serial);
+    const VecRef xr{nullptr, su.B.upool, U_CAND, N_, 0};
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(ticket_.p);
+    if (su.serial)
+      LAUNCH("k_spmv", (k_spmv_commit<true><<<A.grid(), kThreads, 0, s>>>(A, xr, r, su.P, su.S, ticket)));
+    else
+      LAUNCH("k_spmv", (k_spmv_commit<false><<<A.grid(), kThreads, 0, s>>>(A, xr, r, su.P, su.S, ticket)));
+  } else {
+    LAUNCH("k_aa_commit", k_aa_commit<<<1, 128, 0, s>>>(su.P, su.S));
   }
-  LAUNCH("k_aa_commit", k_aa_commit<<<1, 128, 0, s>>>(su.P, su.S));
   AAPDHG_CUDA(cudaGetLastError());
   return nodes;
 }
@@ -1054,11 +1075,15 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   // (eager stream launches of it only on request, AAPDHG_PERSIST_EAGER=1: ncu
   // cannot profile kernels inside graphs that hold conditional nodes)
   const bool persist_ok = use_graph || (!profiling_ && env_int("AAPDHG_PERSIST_EAGER", 0) != 0);
-  if (persist_ok && !serial && su.B.fused_ctrl == 1 && !blk1 && !blk2 && n_ > 0 && m_ > 0 &&
+  // (SERIAL too: the control CTA runs the index-ordered chains while the
+  // workers run ahead; AAPDHG_SERIAL_PERSIST=0 keeps the per-kernel graph)
+  const bool persist_mode =
+      serial ? env_int("AAPDHG_SERIAL_PERSIST", 1) != 0 : su.B.fused_ctrl == 1;
+  if (persist_ok && persist_mode && !blk1 && !blk2 && n_ > 0 && m_ > 0 &&
       env_int("AAPDHG_PERSIST", 1) != 0) {
     int per_sm = 0;
     AAPDHG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, su.push ? k_plain_loop<true> : k_plain_loop<false>, kThreads, 0));
+        &per_sm, plain_loop_kernel(su.push, serial), kThreads, 0));
     // one CTA of the co-resident grid is the control CTA: the short-row
     // slices spread over one CTA fewer when the layout fills the wave
     const int workers = per_sm * num_sms_ - 1;

@@ -286,7 +286,7 @@ class Problem {
 
   // iteration buffers
   int buf_method_ = -1, buf_cap_ = 0;
-  DevBuf upool_, kxpool_, gpool_, du_, dg_, T_, part1_, part2_, partdot_,
+  DevBuf upool_, kxpool_, gpool_, du_, dg_, T_, T2_, part1_, part2_, partdot_,
       gram_, work_, vec_;
   DevBuf rec_, pow_tab_, dparams_, dstate_, dhat_, scal_, part_small_, lam_, pw_x_, pw_mx_,
       pw_mtmx_, pw_state_;
@@ -300,6 +300,7 @@ class Problem {
   cudaGraphConditionalHandle cond_loop_ = 0, cond_aa_ = 0;
   int core_nodes_ = 0, aa_nodes_ = 0;
   DevBuf gridbar_;  // k_plain_loop's barrier counters (GridBar)
+  DevBuf ticket_;   // k_spmv_commit's last-CTA counter
   int32_t* h_batch_ = nullptr;  // pinned
 
   bool profiling_ = false;

@@ -1110,11 +1110,118 @@ __device__ __forceinline__ bool stop_likely(const DevParams* P, const GridBar* g
 
 // The control CTA of k_plain_loop: state and parameters in shared memory for
 // the whole launch (it is the only writer of the state until it stops).
+// One lane adds tm[0..cnt) to s in index order (a dependent chain; each
+// group's 8 shared-memory loads are issued before its adds).
+__device__ __forceinline__ double chain_add(double s, const double* tm, int cnt) {
+  int k = 0;
+  for (; k + 8 <= cnt; k += 8) {
+    double p[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) p[q] = tm[k + q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s = __dadd_rn(s, p[q]);
+  }
+  for (; k < cnt; ++k) s = __dadd_rn(s, tm[k]);
+  return s;
+}
+
+// SERIAL-order chains, by a whole CTA: the elementwise terms of a chunk of CH
+// entries are formed by all threads into shared memory, then one lane per
+// quantity adds them in index order (fixed_point_residual pdhg_core.cpp:
+// 65-74, kkt_metrics solver.cpp:64-110; vec.hpp dot). Roles from `st`.
+// x side: out[0] ||xhat - x||^2, [1] bound term, [2] c'x, [3] ||c - K'y - lambda||^2
+template <int CH>
+__device__ void serial_xchains_cta(const IterBufs& B, const double* __restrict__ T,
+                                   const DevParams* __restrict__ P, const DevState& st,
+                                   double* terms, unsigned char* take, double* out) {
+  const int64_t N = P->N;
+  const int n = P->n;
+  const double* u = B.upool + (int64_t)st.u_idx[U_CUR] * N;
+  const double* uh = B.upool + (int64_t)st.u_idx[U_HAT] * N;
+  const int w = threadIdx.x >> 5;
+  const bool chain = (threadIdx.x & 31) == 0 && w < 4;
+  double s = 0.0;
+  for (int c0 = 0; c0 < n; c0 += CH) {
+    for (int t = threadIdx.x; t < CH; t += blockDim.x) {
+      const int i = c0 + t;
+      if (i < n) {
+        const double d = __dsub_rn(uh[i], u[i]);
+        terms[0 * CH + t] = __dmul_rn(d, d);
+        const double lj = B.l[i], uj = B.u[i], cj = B.c[i];
+        const double rc = __dsub_rn(cj, T[i]);
+        const double lam = project_lambda1(rc, lj, uj);
+        // kkt_metrics adds l*lambda / u*lambda only where they apply; a
+        // skipped term is -0.0, the exact identity of IEEE addition (x + -0 =
+        // x for every x, -0 included), so the chain adds unconditionally
+        double bt = -0.0;
+        if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
+        if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
+        terms[1 * CH + t] = bt;
+        terms[2 * CH + t] = __dmul_rn(cj, u[i]);
+        const double v = __dsub_rn(rc, lam);
+        terms[3 * CH + t] = __dmul_rn(v, v);
+      }
+    }
+    __syncthreads();
+    if (chain) {
+      const int cnt = n - c0 < CH ? n - c0 : CH;
+      s = chain_add(s, terms + w * CH, cnt);
+    }
+    __syncthreads();
+  }
+  if (chain) out[w] = s;  // 0 G2x, 1 BOUND, 2 CX, 3 DUALSQ
+  __syncthreads();
+}
+
+// y side: out[0] ||ghat||^2 continued from the x part g2x, [1] q'y,
+// [2] primal infeasibility ||((h - Gx)_+; b - Ax)||^2
+template <int CH>
+__device__ void serial_ychains_cta(const IterBufs& B, const DevParams* __restrict__ P,
+                                   const DevState& st, double g2x, double* terms, double* out) {
+  const int64_t N = P->N;
+  const int n = P->n, mr = P->mrows, m1 = P->m1;
+  const double* u = B.upool + (int64_t)st.u_idx[U_CUR] * N;
+  const double* uh = B.upool + (int64_t)st.u_idx[U_HAT] * N;
+  const double* kx = B.kxpool + (int64_t)st.kx_idx[KX_CUR] * mr;
+  const int w = threadIdx.x >> 5;
+  const bool chain = (threadIdx.x & 31) == 0 && w < 3;
+  double s = (chain && w == 0) ? g2x : 0.0;
+  for (int c0 = 0; c0 < mr; c0 += CH) {
+    for (int t = threadIdx.x; t < CH; t += blockDim.x) {
+      const int i = c0 + t;
+      if (i < mr) {
+        const double d = __dsub_rn(uh[n + i], u[n + i]);
+        terms[0 * CH + t] = __dmul_rn(d, d);
+        terms[1 * CH + t] = __dmul_rn(B.q[i], u[n + i]);
+        double v = __dsub_rn(B.q[i], kx[i]);
+        if (i < m1) v = smax(v, 0.0);
+        terms[2 * CH + t] = __dmul_rn(v, v);
+      }
+    }
+    __syncthreads();
+    if (chain) {
+      const int cnt = mr - c0 < CH ? mr - c0 : CH;
+      s = chain_add(s, terms + w * CH, cnt);
+    }
+    __syncthreads();
+  }
+  if (chain) out[w] = s;
+  __syncthreads();
+}
+
+constexpr int kPlainSerChunk = 1024;  // SERIAL control CTA: terms staged per chain pass (33 KB)
+
+template <bool SERIAL>
 __device__ __noinline__ void plain_loop_control(const IterBufs& B, const DevParams* P, DevState* S,
                                                 GridBar* gb, int nb1, int nb2, DevState& sm,
                                                 DevParams& pr, double* red) {
   const unsigned long long G = gridDim.x;
   __shared__ double t1s[P1_COUNT], t2s[P2_COUNT];
+  // SERIAL: the index-ordered chains of iteration k by this CTA (x side after
+  // barrier 1, y side after barrier 2) while the workers run ahead
+  __shared__ double sterms[SERIAL ? 4 * kPlainSerChunk : 1];
+  __shared__ unsigned char stake[SERIAL ? kPlainSerChunk : 1];
+  __shared__ double xres[4], yres[3];
   __shared__ Decision dec;
   params_load(&pr, P);
   __syncthreads();
@@ -1134,24 +1241,37 @@ __device__ __noinline__ void plain_loop_control(const IterBufs& B, const DevPara
       }
     }
     __syncthreads();
-    double t1[P1_COUNT];
-    reduce_partial_rows<P1_COUNT>(B.part1, nb1, t1, red);
-    if (threadIdx.x == 0)
+    if constexpr (SERIAL) {
+      serial_xchains_cta<kPlainSerChunk>(B, (sm.k & 1) ? B.T2 : B.T, &pr, sm, sterms, stake,
+                                         xres);
+    } else {
+      double t1[P1_COUNT];
+      reduce_partial_rows<P1_COUNT>(B.part1, nb1, t1, red);
+      if (threadIdx.x == 0)
 #pragma unroll
-      for (int q = 0; q < P1_COUNT; ++q) t1s[q] = t1[q];
+        for (int q = 0; q < P1_COUNT; ++q) t1s[q] = t1[q];
+    }
     // barrier 2: K2(k) done (the workers start K1(k+1) on plain-step roles)
     if (threadIdx.x == 0) bar_arrive_wait(&gb->arrive2, 1, G);
     __syncthreads();
-    double t2[P2_COUNT];
-    reduce_partial_rows<P2_COUNT>(B.part2, nb2, t2, red);
-    if (threadIdx.x == 0)
+    if constexpr (SERIAL) {
+      serial_ychains_cta<kPlainSerChunk>(B, &pr, sm, xres[0], sterms, yres);
+    } else {
+      double t2[P2_COUNT];
+      reduce_partial_rows<P2_COUNT>(B.part2, nb2, t2, red);
+      if (threadIdx.x == 0)
 #pragma unroll
-      for (int q = 0; q < P2_COUNT; ++q) t2s[q] = t2[q];
+        for (int q = 0; q < P2_COUNT; ++q) t2s[q] = t2[q];
+    }
     __syncthreads();
     const uint64_t k = sm.k;
-    const double g2 = __dadd_rn(t1s[P1_GX2], t2s[P2_GY2]);
-    const double bound = t1s[P1_BOUND], qy = t2s[P2_QY], cx = t1s[P1_CX];
-    const double infeas = t2s[P2_INFEAS], dsq = t1s[P1_DUALSQ];
+    // (SERIAL: ||g||^2 is the x chain continued over y, as solver.cpp's)
+    const double g2 = SERIAL ? yres[0] : __dadd_rn(t1s[P1_GX2], t2s[P2_GY2]);
+    const double bound = SERIAL ? xres[1] : t1s[P1_BOUND];
+    const double qy = SERIAL ? yres[1] : t2s[P2_QY];
+    const double cx = SERIAL ? xres[2] : t1s[P1_CX];
+    const double infeas = SERIAL ? yres[2] : t2s[P2_INFEAS];
+    const double dsq = SERIAL ? xres[3] : t1s[P1_DUALSQ];
     if (threadIdx.x == 32) control_kkt_records(&pr, &sm, k, g2, bound, qy, cx, infeas, dsq, -1.0);
     if (threadIdx.x == 0) dec = control_decide(&pr, &sm, k, g2, bound, qy, cx, infeas, dsq, -1.0, -1.0);
     __syncthreads();
@@ -1191,7 +1311,7 @@ __device__ __noinline__ void plain_loop_control(const IterBufs& B, const DevPara
   }
 }
 
-template <bool PUSH>
+template <bool PUSH, bool SERIAL = false>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_plain_loop(CsrDev KT, CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S,
                  GridBar* gb, int nb1, int nb2) {
@@ -1203,7 +1323,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   if (st.done || st.batch_left <= 0) return;  // (eager launches past the batch)
   if (bid == W) {
     __shared__ __align__(16) DevParams pr;
-    plain_loop_control(B, P, S, gb, nb1, nb2, st, pr, red);
+    plain_loop_control<SERIAL>(B, P, S, gb, nb1, nb2, st, pr, red);
     return;
   }
   unsigned long long h0 = 0;  // stop flags raised before this launch
@@ -1217,7 +1337,13 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   const bool pf = P->phase_prefetch != 0;
   for (;;) {
     if (pf && bid < nb2) prefetch_slice_streams(K, bid);  // K2's streams, one phase ahead
-    if (bid < nb1) dual_side_rows<false, PUSH, 0, true>(KT, B, P, &st, bid, nb1, red);
+    if constexpr (SERIAL) {  // K'y of iteration k into its parity buffer (the control's chains)
+      IterBufs Bk = B;
+      Bk.T = (st.k & 1) ? B.T2 : B.T;
+      if (bid < nb1) dual_side_rows<true, PUSH, 0, true>(KT, Bk, P, &st, bid, nb1, red);
+    } else {
+      if (bid < nb1) dual_side_rows<false, PUSH, 0, true>(KT, B, P, &st, bid, nb1, red);
+    }
     __syncthreads();
 #ifdef AAPDHG_PLAIN_STAMPS
     if (threadIdx.x == 0) ps1 = globaltimer_ns();
@@ -1231,11 +1357,13 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     if (pf && bid < nb1) prefetch_slice_streams(KT, bid);  // the next K1's streams
     double acc[P2_COUNT] = {0.0, 0.0, 0.0};
     if (bid < nb2) {
-      primal_side_rows<false, PUSH, true>(K, B, P, &st, bid, acc);
-      block_sum<P2_COUNT>(acc, red);
-      if (threadIdx.x == 0)
+      primal_side_rows<SERIAL, PUSH, true>(K, B, P, &st, bid, acc);
+      if constexpr (!SERIAL) {
+        block_sum<P2_COUNT>(acc, red);
+        if (threadIdx.x == 0)
 #pragma unroll
-        for (int q = 0; q < P2_COUNT; ++q) B.part2[q * nb2 + bid] = acc[q];
+          for (int q = 0; q < P2_COUNT; ++q) B.part2[q * nb2 + bid] = acc[q];
+      }
     }
     __syncthreads();
 #ifdef AAPDHG_PLAIN_STAMPS
@@ -1328,57 +1456,11 @@ __global__ void __launch_bounds__(kSerThreads)
   if (S->done) return;
   extern __shared__ double terms[];  // S_COUNT x kSerChunk
   unsigned char* take = reinterpret_cast<unsigned char*>(terms + S_COUNT * kSerChunk);
-  const int64_t N = P->N;
-  const int n = P->n;
-  const double* u = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-  const double* uh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-  const double* T = B.T;
-  const int w = threadIdx.x >> 5;
-  // chains: warp 0 G2 (x part), 1 BOUND, 2 CX, 3 DUALSQ
-  const bool chain = (threadIdx.x & 31) == 0 && w < 4;
-  double s = 0.0;
-  for (int c0 = 0; c0 < n; c0 += kSerChunk) {
-    for (int t = threadIdx.x; t < kSerChunk; t += blockDim.x) {
-      const int i = c0 + t;
-      if (i < n) {
-        const double d = __dsub_rn(uh[i], u[i]);
-        terms[0 * kSerChunk + t] = __dmul_rn(d, d);
-        const double lj = B.l[i], uj = B.u[i], cj = B.c[i];
-        const double rc = __dsub_rn(cj, T[i]);
-        const double lam = project_lambda1(rc, lj, uj);
-        double bt = 0.0;
-        unsigned char tk = 0;
-        if (isfinite(lj) && lam > 0.0) { bt = __dmul_rn(lj, lam); tk = 1; }
-        if (isfinite(uj) && lam < 0.0) { bt = __dmul_rn(uj, lam); tk = 1; }
-        terms[1 * kSerChunk + t] = bt;
-        take[t] = tk;
-        terms[2 * kSerChunk + t] = __dmul_rn(cj, u[i]);
-        const double v = __dsub_rn(rc, lam);
-        terms[3 * kSerChunk + t] = __dmul_rn(v, v);
-      }
-    }
-    __syncthreads();
-    if (chain) {
-      const int cnt = n - c0 < kSerChunk ? n - c0 : kSerChunk;
-      const double* tm = terms + w * kSerChunk;
-      if (w == 1) {
-        for (int k = 0; k < cnt; ++k)
-          if (take[k]) s = __dadd_rn(s, tm[k]);
-      } else {
-        int k = 0;
-        for (; k + 8 <= cnt; k += 8) {
-          double p[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) p[q] = tm[k + q];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) s = __dadd_rn(s, p[q]);
-        }
-        for (; k < cnt; ++k) s = __dadd_rn(s, tm[k]);
-      }
-    }
-    __syncthreads();
-  }
-  if (chain) S->sres[w] = s;  // 0 G2x, 1 BOUND, 2 CX, 3 DUALSQ
+  __shared__ double out[4];
+  __shared__ DevState st;
+  state_load(&st, S);
+  serial_xchains_cta<kSerChunk>(B, B.T, P, st, terms, take, out);
+  if (threadIdx.x < 4) S->sres[threadIdx.x] = out[threadIdx.x];  // G2x, BOUND, CX, DUALSQ
 }
 
 // SERIAL mode, y side + control (after K2 and k_serial_xchains): ||g||^2
@@ -1395,48 +1477,11 @@ __global__ void __launch_bounds__(kSerThreads)
   }
   extern __shared__ double terms[];  // 3 x kSerChunk used
   __shared__ double res[3];
-  const int64_t N = P->N;
-  const int n = P->n, mr = P->mrows, m1 = P->m1;
-  const double* u = B.upool + (int64_t)S->u_idx[U_CUR] * N;
-  const double* uh = B.upool + (int64_t)S->u_idx[U_HAT] * N;
-  const double* kx = B.kxpool + (int64_t)S->kx_idx[KX_CUR] * mr;
-  const int w = threadIdx.x >> 5;
-  // chains: warp 0 G2 (continued), 1 QY, 2 INFEAS
-  const bool chain = (threadIdx.x & 31) == 0 && w < 3;
-  double s = (chain && w == 0) ? S->sres[0] : 0.0;
-  for (int c0 = 0; c0 < mr; c0 += kSerChunk) {
-    for (int t = threadIdx.x; t < kSerChunk; t += blockDim.x) {
-      const int i = c0 + t;
-      if (i < mr) {
-        const double d = __dsub_rn(uh[n + i], u[n + i]);
-        terms[0 * kSerChunk + t] = __dmul_rn(d, d);
-        terms[1 * kSerChunk + t] = __dmul_rn(B.q[i], u[n + i]);
-        double v = __dsub_rn(B.q[i], kx[i]);
-        if (i < m1) v = smax(v, 0.0);
-        terms[2 * kSerChunk + t] = __dmul_rn(v, v);
-      }
-    }
-    __syncthreads();
-    if (chain) {
-      const int cnt = mr - c0 < kSerChunk ? mr - c0 : kSerChunk;
-      const double* tm = terms + w * kSerChunk;
-      int k = 0;
-      for (; k + 8 <= cnt; k += 8) {
-        double p[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) p[q] = tm[k + q];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) s = __dadd_rn(s, p[q]);
-      }
-      for (; k < cnt; ++k) s = __dadd_rn(s, tm[k]);
-    }
-    __syncthreads();
-  }
-  if (chain) res[w] = s;
   __shared__ DevState sm;
   __shared__ DevParams sp;
   params_load(&sp, P);
-  state_load(&sm, S);  // (syncs: res[] complete; sres[] from k_serial_xchains)
+  state_load(&sm, S);  // (syncs; sres[] from k_serial_xchains)
+  serial_ychains_cta<kSerChunk>(B, P, sm, sm.sres[0], terms, res);
   if (threadIdx.x == 0)
     control_logic(&sp, &sm, res[0], sm.sres[1], res[1], sm.sres[2], res[2], sm.sres[3]);
   state_store(S, &sm);

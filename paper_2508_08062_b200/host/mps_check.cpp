@@ -5,6 +5,7 @@
 // tokenising) and to_standard_form (device CSR assembly), and checks the
 // result equals the original exactly. Prints one JSON line.
 //   mps_check <rows> <cols> <nnz_per_col> <seed> <path>
+//   mps_check parse <path>        (the reader alone, host only)
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -18,7 +19,47 @@
 
 using namespace aapdhg;
 
+// `mps_check parse <path>`: the reader alone (host only, no device): the
+// RawLP as JSON, or {"error": kind, "what": message}
+static int parse_only(const char* path) {
+  try {
+    const RawLP lp = parse_mps_file(path);
+    double osum = 0.0, esum = 0.0, rsum = 0.0;
+    long long rowsum = 0, colsum = 0;
+    for (double v : lp.obj_coeffs) osum += v;
+    for (const Triplet& t : lp.entries) {
+      esum += t.val;
+      rowsum += t.row;
+      colsum += t.col;
+    }
+    for (double v : lp.rhs) rsum += v;
+    int nint = 0;
+    for (bool b : lp.is_integer) nint += b;
+    int ninf_lo = 0, ninf_up = 0;
+    for (double v : lp.lower) ninf_lo += std::isinf(v);
+    for (double v : lp.upper) ninf_up += std::isinf(v);
+    std::string senses(lp.row_sense.begin(), lp.row_sense.end());
+    std::printf("{\"name\": \"%s\", \"objective\": \"%s\", \"maximize\": %s, \"rows\": %zu, "
+                "\"cols\": %zu, \"entries\": %zu, \"senses\": \"%s\", \"obj_sum\": %.17g, "
+                "\"entry_sum\": %.17g, \"rhs_sum\": %.17g, \"row_index_sum\": %lld, "
+                "\"col_index_sum\": %lld, \"integer\": %d, \"inf_lower\": %d, "
+                "\"inf_upper\": %d, \"first_col\": \"%s\", \"last_col\": \"%s\"}\n",
+                lp.name.c_str(), lp.objective_name.c_str(), lp.maximize ? "true" : "false",
+                lp.row_names.size(), lp.col_names.size(), lp.entries.size(), senses.c_str(), osum,
+                esum, rsum, rowsum, colsum, nint, ninf_lo, ninf_up,
+                lp.col_names.empty() ? "" : lp.col_names.front().c_str(),
+                lp.col_names.empty() ? "" : lp.col_names.back().c_str());
+    return 0;
+  } catch (const UnsupportedError& e) {
+    std::printf("{\"error\": \"UnsupportedError\", \"what\": \"%s\"}\n", e.what());
+  } catch (const InputError& e) {
+    std::printf("{\"error\": \"InputError\", \"what\": \"%s\"}\n", e.what());
+  }
+  return 3;
+}
+
 int main(int argc, char** argv) {
+  if (argc == 3 && std::string(argv[1]) == "parse") return parse_only(argv[2]);
   if (argc != 6) {
     std::fprintf(stderr, "usage: mps_check <rows> <cols> <nnz_per_col> <seed> <path>\n");
     return 2;
