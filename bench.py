@@ -165,9 +165,9 @@ def measured_peak():
 
 def ncu_traffic(kernel):
     """dram bytes per launch of `kernel` (per iteration for k_plain_loop) from
-    the committed ncu --set full capture (profiles/r01/traffic.json), or None."""
+    the committed ncu --set full capture (profiles/r02/traffic.json), or None."""
     try:
-        d = json.loads((ROOT / "profiles" / "r01" / "traffic.json").read_text())[kernel]
+        d = json.loads((ROOT / "profiles" / "r02" / "traffic.json").read_text())[kernel]
         b = float(d["dram_read_bytes"] + d["dram_write_bytes"])
         return b / d["iterations"] if "iterations" in d else b
     except Exception:
@@ -549,7 +549,7 @@ def plain_loop_roofline(args, p, plain, step_ms):
             "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
             "traffic": (t_it * iters / launches) if (t_it and args.traffic is None)
             else args.traffic,
-            "traffic_source": "ncu --set full of one k_plain_loop launch (profiles/r01/"
+            "traffic_source": "ncu --set full of one k_plain_loop launch (profiles/r02/"
                               "traffic.json), dram bytes per iteration x iterations per launch",
             "bytes_per_launch": per_it * iters / launches,
             "bytes_per_iteration": per_it,
@@ -588,7 +588,7 @@ def kernel_roofline(args, p, s, lib, tau):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": args.traffic if args.traffic is not None else ncu_traffic(dom),
-                "traffic_source": "ncu --set full (profiles/r01/traffic.json), cold caches",
+                "traffic_source": "ncu --set full (profiles/r02/traffic.json), cold caches",
                 "bytes_per_launch": kernel_bytes(p, dom),
                 "avg_launch_us": avg_ms * 1e3,
                 "share_of_step": kstats[dom][0] / tot_ms if tot_ms else None,
