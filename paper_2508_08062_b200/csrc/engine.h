@@ -1,6 +1,7 @@
 // engine.h — host side of the sm_100a solver: one Problem per handle.
 #pragma once
 
+#include <atomic>
 #include <map>
 #include <memory>
 #include <string>
@@ -188,10 +189,15 @@ class Problem {
     SellStore sell[2];
   };
   // device-side ingestion (ingest.cu)
-  void finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev& ser, CsrDev& tree);
+  // (s: the stream to build on, null = stream_; the K' build runs on side_
+  // in a second host thread while K's layouts build on stream_)
+  void finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev& ser, CsrDev& tree,
+                  cudaStream_t s = nullptr);
   void device_sell(const int32_t* shorts, int nshort, const int32_t* len, int sf, CsrStore& st,
-                   SellStore& ss, CsrDev& out);
-  void device_transpose(const CsrStore& src, int nrows, int ncols, int64_t nnz, CsrStore& dst);
+                   SellStore& ss, CsrDev& out, cudaStream_t s, bool sigma_global,
+                   double short_mean);
+  void device_transpose(const CsrStore& src, int nrows, int ncols, int64_t nnz, CsrStore& dst,
+                        cudaStream_t s = nullptr);
   void device_block(const CsrStore& src, int nrows, int64_t c0, int64_t c1, CsrStore& dst,
                     int64_t* nnz_out);
   void upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
@@ -267,9 +273,7 @@ class Problem {
   void build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& out);
   int launch_blocked_passes(cudaStream_t s, const Blocked& bk, const VecRef& x,
                             const DevState* S);
-  size_t sell_bytes_ = 0;
-  bool sigma_global_ = false;  // device_sell: sort all short rows (ragged lengths)
-  double short_mean_ = 0.0;    // device_sell: mean length of the short rows
+  std::atomic<size_t> sell_bytes_{0};
   bool building_blocks_ = false;  // device_sell: an L2 column block (never interleaved)
   DevBuf c_, q_, l_, u_;
   double nrm_q_[2] = {0, 0}, nrm_c_[2] = {0, 0};  // [serial, tree]

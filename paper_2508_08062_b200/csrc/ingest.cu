@@ -274,8 +274,8 @@ static int64_t scan_counts(const int32_t* cnt, int n, int32_t* out, cudaStream_t
 // decreasing length inside windows of one CTA's rows (stable), split factor
 // sf for the TREE layout only while the slices fit one wave.
 void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev& ser,
-                         CsrDev& tree) {
-  cudaStream_t s = stream_;
+                         CsrDev& tree, cudaStream_t s) {
+  if (!s) s = stream_;
   DevBuf blen, blong, bshort, bslen, bsel, bcount, tsel;
   int32_t* len = tmp<int32_t>(blen, nrows);
   char* is_long = tmp<char>(blong, nrows);
@@ -356,26 +356,24 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
   // vector accesses local
   const double var = nshort == 0 ? 0.0 : double(short_sq_sum) / double(nshort) - mean * mean;
   const bool ragged = mean > 0.0 && std::sqrt(std::max(var, 0.0)) > 0.5 * mean;
-  sigma_global_ = ragged;
-  short_mean_ = mean;
-  device_sell(shorts, nshort, len, 1, st, st.sell[0], ser);
+  device_sell(shorts, nshort, len, 1, st, st.sell[0], ser, s, ragged, mean);
   const int64_t slots = int64_t(num_sms_) * kSpmvBlocksPerSM * kWarps;
   int sf = 1;
   while (sf < 8 && int64_t(ser.nslices) * 2 * sf <= slots && mean >= 8.0 * sf) sf *= 2;
   sf = env_int("AAPDHG_SF", sf);
   tree = base;
   if (sf == 1) tree = ser;
-  else device_sell(shorts, nshort, len, sf, st, st.sell[1], tree);
+  else device_sell(shorts, nshort, len, sf, st, st.sell[1], tree, s, ragged, mean);
   // TREE: a CTA per huge row (the SERIAL layout keeps one lane-0 chain per row)
   tree.nhuge = nhuge;
   tree.nblk_long = nhuge + (nlong - nhuge + kWarps - 1) / kWarps;
 }
 
 void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* len, int sf,
-                          CsrStore& st, SellStore& ss, CsrDev& out) {
-  cudaStream_t s = stream_;
+                          CsrStore& st, SellStore& ss, CsrDev& out, cudaStream_t s,
+                          bool sigma_global, double short_mean) {
   const int R = 32 / sf;
-  const int sigma = env_int("AAPDHG_SIGMA", sigma_global_ ? std::max(nshort, 1) : kWarps * R);
+  const int sigma = env_int("AAPDHG_SIGMA", sigma_global ? std::max(nshort, 1) : kWarps * R);
   DevBuf brows, bk, bk2, boff, tt;
   int32_t* rows = tmp<int32_t>(brows, nshort);
   if (sigma > 1 && nshort > 0) {  // stable sort by decreasing length inside each window
@@ -444,7 +442,7 @@ void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* l
   if (int64_t(nslices) <= one_wave) {
     out.nblk_short = std::min(nslices, wave);
   } else if (int64_t(nslices) >= 2 * one_wave &&
-             env_int("AAPDHG_INTERLEAVE", short_mean_ <= 4.0 && !building_blocks_ ? 1 : 0) != 0) {
+             env_int("AAPDHG_INTERLEAVE", short_mean <= 4.0 && !building_blocks_ ? 1 : 0) != 0) {
     // very short rows (config 2's K': 4M rows of 2): a slice is a few loads
     // per lane, so CTA turnover dominates a CTA-per-8-slices grid. One wave
     // of CTAs instead, every warp looping over slices w, w + wave*8, ...
@@ -461,8 +459,8 @@ void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* l
 // sort of the entries by column (the order matvec_transpose accumulates in,
 // sparse_linalg.cpp:77-87).
 void Problem::device_transpose(const CsrStore& src, int nrows, int ncols, int64_t nnz,
-                               CsrStore& dst) {
-  cudaStream_t s = stream_;
+                               CsrStore& dst, cudaStream_t s) {
+  if (!s) s = stream_;
   dst.rp.reserve(sizeof(int32_t) * (size_t(ncols) + 1));
   dst.ci.reserve(sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1)));
   dst.v.reserve(sizeof(double) * size_t(std::max<int64_t>(nnz, 1)));

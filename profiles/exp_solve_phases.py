@@ -17,8 +17,9 @@ from paper_2508_08062_b200 import Method, Solver, SolverConfig, problems  # noqa
 
 
 def main():
-    iters = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    iters = int(args[0]) if len(args) > 0 else 20
+    reps = int(args[1]) if len(args) > 1 else 3
     p = problems.make_config(1)
     n, m = p.n(), p.k.nrows
     import torch
@@ -35,6 +36,10 @@ def main():
             dt = time.perf_counter() - t0
             print(f"python wall {1e6 * dt:.1f} us, {out.result.iterations} it, "
                   f"{out.result.i} aa, {iters / dt:.0f} it/s", file=sys.stderr, flush=True)
+    if "--pinned" in sys.argv:  # the bench's e2e: the LP in page-locked buffers
+        sys.path.insert(0, str(ROOT))
+        import bench
+        p, _ = bench.pinned_problem(torch, p)
     for r in range(reps):
         t0 = time.perf_counter()
         with Solver(p) as s2:
