@@ -389,40 +389,15 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   N_ = int64_t(n_) + m_;
   nglob_ = N_;
 
-  // K uploaded and checked; then K's layouts (stream_) and K' — transpose
-  // and layouts, side_ — are built concurrently from two host threads (each
-  // build is a chain of small kernels and host syncs: overlapped, the SMs
-  // take both)
-  {
-    const int64_t nnz = k.nnz;
-    k_store_.rp.reserve(sizeof(int32_t) * (size_t(m_) + 1));
-    k_store_.ci.reserve(sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1)));
-    k_store_.v.reserve(sizeof(double) * size_t(std::max<int64_t>(nnz, 1)));
-    h2d(k_store_.rp.p, k.row_ptr, sizeof(int32_t) * (size_t(m_) + 1), stream_);
-    h2d(k_store_.ci.p, k.col_idx, sizeof(int32_t) * size_t(nnz), stream_);
-    h2d(k_store_.v.p, k.vals, sizeof(double) * size_t(nnz), stream_);
-    device_validate(k_store_, m_, n_, nnz);  // (syncs stream_)
-    ph("upload + checks");
-    std::exception_ptr err;
-    std::thread kt([&] {
-      try {
-        AAPDHG_CUDA(cudaSetDevice(device_));
-        device_transpose(k_store_, m_, n_, nnz_, t_store_, side_);
-        finish_csr(n_, m_, nnz_, t_store_, KTs_, KTt_, side_);
-      } catch (...) {
-        err = std::current_exception();
-      }
-    });
-    try {
-      finish_csr(m_, n_, nnz, k_store_, Ks_, Kt_, stream_);
-    } catch (...) {
-      kt.join();
-      throw;
-    }
-    kt.join();
-    if (err) std::rethrow_exception(err);
-  }
-  ph("K + K' layouts");
+  // K uploaded and checked on the device, then K's layouts, the transpose
+  // K' and its layouts (a second host thread building K' on side_ was
+  // measured: no gain inside the bench's process, more variance)
+  upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
+  ph("upload K + SELL");
+  device_transpose(k_store_, m_, n_, nnz_, t_store_);
+  ph("transpose");
+  finish_csr(n_, m_, nnz_, t_store_, KTs_, KTt_);
+  ph("K' SELL");
   build_blocks(k_store_, m_, n_, kb_);
   build_blocks(t_store_, n_, m_, ktb_);
   ph("L2 blocks");

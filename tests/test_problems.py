@@ -85,3 +85,42 @@ def test_config_params_validation():
     cfg = SolverConfig(aa=type(SolverConfig().aa)(d_hat=np.ones(3)))
     with pytest.raises(DimensionError):
         cfg.to_params(4)
+
+
+def test_instance_cache_round_trip(tmp_path, monkeypatch):
+    """problems.cached_config: generated once into .npy files (a completion
+    marker written last), memory-mapped afterwards; identical to make_config."""
+    monkeypatch.setenv("AAPDHG_INSTANCE_CACHE", str(tmp_path))
+    a = problems.cached_config(1, 0.05)
+    d = problems.cache_dir(1, 0.05)
+    assert (d / "complete").exists()
+    b = problems.cached_config(1, 0.05, generate=False)  # mapped, not regenerated
+    ref = problems.make_config(1, 0.05)
+    for x in (a, b):
+        assert np.array_equal(x.k.row_ptr, ref.k.row_ptr)
+        assert np.array_equal(x.k.col_idx, ref.k.col_idx)
+        assert np.array_equal(x.k.vals, ref.k.vals)
+        for f in ("c", "q", "l", "u"):
+            assert np.array_equal(getattr(x, f), getattr(ref, f))
+        assert x.planted_objective == ref.planted_objective
+    with pytest.raises(FileNotFoundError):
+        problems.cached_config(1, 0.07, generate=False)
+
+
+def test_bench_iteration_bytes_and_workload_selection():
+    import argparse
+    import bench
+    p = problems.make_config(1, 0.05)
+    n, m, nnz = p.n(), p.k.nrows, p.k.nnz
+    plain = bench.kernel_bytes(p, "k_plain_loop")
+    assert plain == (12 * nnz + 4 * (n + 1) + 8 * m + 80 * n) + (12 * nnz + 4 * (m + 1) + 8 * n + 80 * m)
+    N = n + m
+    aa = 8 * N * 13 + 8 * N * 23 + 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
+    assert bench.iteration_bytes(p, 20, 3) == 20 * plain + 3 * aa
+    args = argparse.Namespace(workload="auto", loopback=0)
+    bench.select_workload(args, 1)
+    assert bench.CONFIG_ID == 1 and "configs[1]" in bench.METRIC
+    bench.select_workload(args, 8)
+    assert bench.CONFIG_ID == 4 and "configs[4]" in bench.METRIC
+    bench.select_workload(argparse.Namespace(workload="config1", loopback=0), 8)
+    assert bench.CONFIG_ID == 1
