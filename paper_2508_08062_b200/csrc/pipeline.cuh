@@ -880,7 +880,10 @@ __device__ __forceinline__ void dual_side_rows(const CsrDev& KT, const IterBufs&
 
 // MULTI: the layout is interleaved (several slices per warp, CsrDev)
 template <bool SERIAL, bool PUSH, int VAR = 0, bool MULTI = false>
-__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+#ifndef AAPDHG_K12_MINBLOCKS
+#define AAPDHG_K12_MINBLOCKS kSpmvBlocksPerSM
+#endif
+__global__ void __launch_bounds__(kThreads, AAPDHG_K12_MINBLOCKS)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   launch_dependents();  // k_primal_side may start its prologue (PDL)
   if (S->done) return;
@@ -983,7 +986,7 @@ __device__ __forceinline__ void primal_side_rows(const CsrDev& K, const IterBufs
 
 // VAR 2 (experiment, AAPDHG_K2VAR=2): the SpMV alone, no epilogue or control
 template <bool SERIAL, bool PUSH, int VAR = 0, bool MULTI = false>
-__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+__global__ void __launch_bounds__(kThreads, AAPDHG_K12_MINBLOCKS)
     k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
   if (S->done) return;
   if constexpr (VAR == 2) {

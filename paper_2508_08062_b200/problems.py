@@ -28,25 +28,36 @@ CONFIGS = {
 }
 
 
-def _argsort_distinct(key: np.ndarray) -> np.ndarray:
-    """The sorting permutation of distinct int64 keys (unique, so any sort
-    gives it): on a CUDA device when one is present and the array is large
-    (config 4: 400M keys, minutes in numpy), numpy otherwise."""
+def _argsort_stable(key: np.ndarray, use_torch: bool | None = None) -> np.ndarray:
+    """The stable sorting permutation of int64 keys — unique whatever sort
+    produces it (equal keys keep their input order) — on a CUDA device when
+    one is present and the array is large (config 3/4: 150-400M keys,
+    minutes in numpy), numpy otherwise. use_torch forces the torch path
+    (tests compare the two)."""
     import os
-    if key.size > (16 << 20) and os.environ.get("AAPDHG_GEN_NO_TORCH") != "1":
+    if use_torch is None:
+        use_torch = key.size > (16 << 20) and os.environ.get("AAPDHG_GEN_NO_TORCH") != "1"
+    if use_torch:
         try:
             import torch
-            if torch.cuda.is_available():
-                t = torch.from_numpy(key).cuda()
+            dev = "cuda" if torch.cuda.is_available() else None
+            if dev is not None or use_torch is True:
+                t = torch.from_numpy(key)
+                if dev is not None and key.size > (16 << 20):
+                    t = t.cuda()
                 order = torch.argsort(t, stable=True)
                 del t
                 out = order.cpu().numpy()
                 del order
-                torch.cuda.empty_cache()
+                if dev is not None:
+                    torch.cuda.empty_cache()
                 return out
-        except Exception:  # no usable device: the numpy sort below
+        except Exception:  # no usable torch / device: the numpy sort below
             pass
     return np.argsort(key, kind="stable")
+
+
+_argsort_distinct = _argsort_stable
 
 
 def _csr_from_coo(m, n, rows, cols, vals) -> SparseMatrix:
@@ -84,7 +95,8 @@ def _distinct_per_group(rng, groups: int, k, universe: int):
                 return grp, v.reshape(-1)
             v[dup] = rng.integers(0, universe, size=nd, dtype=np.int64)
     while True:
-        order = np.lexsort((val, grp))
+        # = np.lexsort((val, grp)): one stable sort of the combined key
+        order = _argsort_stable(grp * np.int64(universe) + val)
         g2, v2 = grp[order], val[order]
         dup = np.zeros(total, dtype=bool)
         dup[1:] = (g2[1:] == g2[:-1]) & (v2[1:] == v2[:-1])

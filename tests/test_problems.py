@@ -124,3 +124,17 @@ def test_bench_iteration_bytes_and_workload_selection():
     assert bench.CONFIG_ID == 4 and "configs[4]" in bench.METRIC
     bench.select_workload(argparse.Namespace(workload="config1", loopback=0), 8)
     assert bench.CONFIG_ID == 1
+
+
+def test_stable_argsort_paths_agree():
+    """problems._argsort_stable: the torch path (used on a GPU box for the
+    150-400M-key sorts of configs 3 and 4) gives numpy's stable permutation,
+    equal keys included, and np.lexsort((val, grp)) equals the combined-key
+    sort the generator uses."""
+    rng = np.random.default_rng(11)
+    grp = np.repeat(np.arange(3000, dtype=np.int64), rng.integers(1, 60, 3000))
+    val = rng.integers(0, 40, grp.size)
+    key = grp * np.int64(40) + val
+    want = np.lexsort((val, grp))
+    assert np.array_equal(problems._argsort_stable(key, use_torch=False), want)
+    assert np.array_equal(problems._argsort_stable(key, use_torch=True), want)
