@@ -855,7 +855,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   double* out = o.out_pool + (int64_t)S->kx_idx[o.out_role] * o.out_stride;
   for (int rep = 0;; ++rep) {
     double v;
-    const int row = row_sum<SERIAL>(A, x, v, NoPre{}, -1, rep);
+    const int row = row_sum<SERIAL, kUnroll, false, false>(A, x, v, NoPre{}, -1, rep);
     if (row == -2) break;
     if (row >= 0) out[row] = v;
   }

@@ -71,6 +71,11 @@ struct CsrDev {
   // more slices than one wave of warps: slice s belongs to CTA s % nblk_short
   // (one wave of CTAs), whose warps loop over theirs (row_sum `rep`)
   int32_t interleave = 0;
+  // k_plain_loop with a calibrated partition (TREE, no long rows, not
+  // interleaved): CTA b owns slices [sl_start[b], sl_start[b + 1]) (<= kWarps),
+  // and the partial sums are per slice (part[q * nslices + slice]), so the
+  // reduction does not depend on which CTA ran a slice
+  const int32_t* sl_start = nullptr;
   int32_t grid() const { return nblk_short + nblk_long; }
 };
 

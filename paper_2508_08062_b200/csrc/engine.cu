@@ -98,7 +98,182 @@ struct SolveSetup {
   int pgrid = 0;         // workers + the control CTA
   CsrDev pk1, pk2;       // the K' / K layouts on <= pgrid - 1 worker CTAs
   GridBar* gb = nullptr;
+  int np1 = 0, np2 = 0;  // partial rows: CTAs, or slices (calibrated partition)
+  unsigned long long* bal = nullptr;  // per-CTA phase times (calibrating)
 };
+
+// ---- k_plain_loop partition calibration ------------------------------------
+// The worker CTAs of the persistent grid sit on the same SMs launch after
+// launch, and some SMs gather measurably slower than others (up to ~20% on
+// configs[1]: profiles/exp_sm_balance.py). Each barrier waits for the slowest
+// SM, so the slices are shared out per SM in proportion to the rate each SM
+// achieved in earlier launches (slices per microsecond of its slowest CTA),
+// evenly over the SM's CTAs (<= kWarps each). The partials are per slice
+// (CsrDev::sl_start), so every partition gives the same bits. The partition
+// is kept per device and layout shape, so a new handle of the same LP starts
+// calibrated; it is refined after each of the first AAPDHG_BALANCE_ROUNDS
+// (default 3) solves that ran at least kBalMinIters plain iterations.
+namespace {
+constexpr uint64_t kBalMinIters = 16;
+struct BalEntry {
+  std::vector<int32_t> s1, s2;  // slice starts per worker CTA (workers + 1)
+  std::vector<int32_t> w1, w2;  // slice work (per-lane lengths) of K' / K
+  int rounds = 0;
+};
+std::mutex g_bal_mu;
+std::map<std::string, BalEntry> g_bal;
+
+std::string bal_key(int device, const CsrDev& a, const CsrDev& b, int workers) {
+  char k[160];
+  std::snprintf(k, sizeof k, "%d/%d/%d/%d/%d/%d/%d/%lld/%lld", device, workers, a.nslices, a.sf,
+                b.nslices, b.sf, a.nrows, (long long)a.nnz, (long long)b.nnz);
+  return k;
+}
+
+std::vector<int32_t> proportional_starts(int ns, int workers) {
+  std::vector<int32_t> st(static_cast<size_t>(workers) + 1);
+  for (int w = 0; w <= workers; ++w) st[size_t(w)] = int32_t(int64_t(w) * ns / workers);
+  return st;
+}
+
+// new starts from one phase's measurements: t[w] mean phase time of worker w,
+// sm[w] its SM, cur the current starts, wt[s] the work of slice s (its
+// per-lane length). Each SM gets work in proportion to the rate it showed
+// (work per microsecond of its slowest CTA), split evenly over its CTAs; the
+// slices go to the CTAs in order, <= kWarps each.
+std::vector<int32_t> rebalance(const std::vector<int32_t>& cur, const std::vector<double>& t,
+                               const std::vector<int>& sm, const std::vector<int32_t>& wt) {
+  const int W = int(cur.size()) - 1;
+  const int ns = int(wt.size());
+  int nsm = 0;
+  for (int w = 0; w < W; ++w) nsm = std::max(nsm, sm[size_t(w)] + 1);
+  std::vector<double> work(static_cast<size_t>(nsm), 0.0), tmax(static_cast<size_t>(nsm), 0.0);
+  std::vector<int> nct(static_cast<size_t>(nsm), 0);
+  for (int w = 0; w < W; ++w) {
+    const int q = sm[size_t(w)];
+    for (int32_t x = cur[size_t(w)]; x < cur[size_t(w) + 1]; ++x) work[size_t(q)] += wt[size_t(x)];
+    tmax[size_t(q)] = std::max(tmax[size_t(q)], t[size_t(w)]);
+    ++nct[size_t(q)];
+  }
+  std::vector<double> rate(static_cast<size_t>(nsm), 0.0);
+  double rmean = 0.0;
+  int nr = 0;
+  for (int q = 0; q < nsm; ++q)
+    if (work[size_t(q)] > 0 && tmax[size_t(q)] > 0) {
+      rate[size_t(q)] = work[size_t(q)] / tmax[size_t(q)];
+      rmean += rate[size_t(q)];
+      ++nr;
+    }
+  if (nr == 0) return cur;
+  rmean /= nr;
+  double rsum = 0.0, wtot = 0.0;
+  for (int q = 0; q < nsm; ++q) {
+    if (nct[size_t(q)] == 0) rate[size_t(q)] = 0.0;
+    else if (rate[size_t(q)] == 0.0) rate[size_t(q)] = rmean;  // (idle last time)
+    rsum += rate[size_t(q)];
+  }
+  for (int x = 0; x < ns; ++x) wtot += wt[size_t(x)];
+  // cumulative work targets in CTA order; a slice goes to the CTA whose
+  // target range holds its midpoint
+  std::vector<int32_t> st(static_cast<size_t>(W) + 1, 0);
+  double target = 0.0, cum = 0.0;
+  int x = 0;
+  for (int w = 0; w < W; ++w) {
+    const int q = sm[size_t(w)];
+    target += wtot * rate[size_t(q)] / rsum / nct[size_t(q)];
+    int took = 0;
+    while (x < ns && took < kWarps && (w == W - 1 || cum + 0.5 * wt[size_t(x)] <= target)) {
+      cum += wt[size_t(x)];
+      ++x;
+      ++took;
+    }
+    st[size_t(w) + 1] = x;
+  }
+  // slices the caps left over: move the boundaries down from the end (each
+  // CTA still <= kWarps slices)
+  st[size_t(W)] = ns;
+  for (int w = W - 1; w >= 0; --w)
+    st[size_t(w)] = std::min(st[size_t(w) + 1], std::max(st[size_t(w)], st[size_t(w) + 1] - kWarps));
+  if (st[0] != 0) return cur;  // (infeasible: keep the partition)
+  return st;
+}
+}  // namespace
+
+// Before a persistent launch: the partition (cached for this device and
+// layout shape, else proportional) into bal_start1_ / bal_start2_; *measure:
+// whether this solve records phase times (bal_stats_).
+void Problem::bal_setup(const CsrDev& a, const CsrDev& b, int workers, bool* measure) {
+  const std::string key = bal_key(device_, a, b, workers);
+  BalEntry e;
+  {
+    std::lock_guard<std::mutex> g(g_bal_mu);
+    auto it = g_bal.find(key);
+    if (it != g_bal.end()) e = it->second;
+  }
+  if (e.s1.empty()) {
+    e.s1 = proportional_starts(a.nslices, workers);
+    e.s2 = proportional_starts(b.nslices, workers);
+    e.w1.resize(size_t(a.nslices));
+    e.w2.resize(size_t(b.nslices));
+    d2h(e.w1.data(), a.sl_len, sizeof(int32_t) * e.w1.size(), stream_);
+    d2h(e.w2.data(), b.sl_len, sizeof(int32_t) * e.w2.size(), stream_);
+    sync();
+    std::lock_guard<std::mutex> g(g_bal_mu);
+    g_bal[key] = e;
+  }
+  bal_start1_.reserve(sizeof(int32_t) * (size_t(workers) + 1));
+  bal_start2_.reserve(sizeof(int32_t) * (size_t(workers) + 1));
+  h2d(bal_start1_.p, e.s1.data(), sizeof(int32_t) * e.s1.size(), stream_);
+  h2d(bal_start2_.p, e.s2.data(), sizeof(int32_t) * e.s2.size(), stream_);
+  *measure = e.rounds < env_int("AAPDHG_BALANCE_ROUNDS", 3);
+  if (*measure) {
+    bal_stats_.reserve(sizeof(unsigned long long) * 4 * size_t(workers));
+    AAPDHG_CUDA(cudaMemsetAsync(bal_stats_.p, 0, bal_stats_.bytes, stream_));
+  }
+}
+
+// After a measured solve: the per-CTA phase times -> a new partition for the
+// next launch on this device and layout shape.
+void Problem::bal_collect(const CsrDev& a, const CsrDev& b, int workers) {
+  std::vector<unsigned long long> st(4 * static_cast<size_t>(workers));
+  d2h(st.data(), bal_stats_.p, sizeof(unsigned long long) * st.size(), stream_);
+  sync();
+  std::vector<double> t1(static_cast<size_t>(workers)), t2(static_cast<size_t>(workers));
+  std::vector<int> sm(static_cast<size_t>(workers));
+  for (int w = 0; w < workers; ++w) {
+    const unsigned long long c = st[4 * size_t(w) + 2];
+    if (c < kBalMinIters) return;  // too few iterations: keep the partition
+    t1[size_t(w)] = double(st[4 * size_t(w)]) / double(c);
+    t2[size_t(w)] = double(st[4 * size_t(w) + 1]) / double(c);
+    sm[size_t(w)] = int(st[4 * size_t(w) + 3]);
+  }
+  const std::string key = bal_key(device_, a, b, workers);
+  std::lock_guard<std::mutex> g(g_bal_mu);
+  auto it = g_bal.find(key);
+  if (it == g_bal.end()) return;
+  BalEntry& e = it->second;
+  const auto n1 = rebalance(e.s1, t1, sm, e.w1), n2 = rebalance(e.s2, t2, sm, e.w2);
+  if (env_int("AAPDHG_VERBOSE", 0)) {
+    auto moved = [](const std::vector<int32_t>& a, const std::vector<int32_t>& b) {
+      int c = 0;
+      for (size_t i = 0; i < a.size(); ++i) c += a[i] != b[i];
+      return c;
+    };
+    double m1 = 0, m2 = 0, a1 = 0, a2 = 0;
+    for (int w = 0; w < workers; ++w) {
+      m1 = std::max(m1, t1[size_t(w)]);
+      m2 = std::max(m2, t2[size_t(w)]);
+      a1 += t1[size_t(w)] / workers;
+      a2 += t2[size_t(w)] / workers;
+    }
+    std::fprintf(stderr, "aapdhg: balance round %d: K1 mean %.2f max %.2f us, K2 mean %.2f max "
+                 "%.2f us; boundaries moved %d / %d\n", e.rounds, a1 / 1e3, m1 / 1e3, a2 / 1e3,
+                 m2 / 1e3, moved(n1, e.s1), moved(n2, e.s2));
+  }
+  e.s1 = n1;
+  e.s2 = n2;
+  ++e.rounds;
+}
 
 // k_plain_loop spins on grid barriers, so it must never share the GPU with a
 // second persistent grid (two partially resident grids would wait on each
@@ -679,7 +854,7 @@ auto k2_kernel(const CsrDev& A) {
 
 // the persistent plain-iteration grid for a push / reduction order
 using PlainLoopKernel = void (*)(CsrDev, CsrDev, IterBufs, const DevParams*, DevState*, GridBar*,
-                                 int, int);
+                                 int, int, int, int, unsigned long long*);
 static PlainLoopKernel plain_loop_kernel(bool push, bool serial) {
   return serial ? (push ? k_plain_loop<true, true> : k_plain_loop<false, true>)
                 : (push ? k_plain_loop<true, false> : k_plain_loop<false, false>);
@@ -701,7 +876,8 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
     auto kern = plain_loop_kernel(push, ser);
     LAUNCH("k_plain_loop", AAPDHG_CUDA(cudaLaunchKernelEx(&cfg, kern, su.pk1, su.pk2, su.B, su.P,
                                                           su.S, su.gb, su.pk1.grid(),
-                                                          su.pk2.grid())));
+                                                          su.pk2.grid(), su.np1, su.np2,
+                                                          su.bal)));
     return nodes;
   }
   // TREE with L2 column blocking: the earlier column passes first, the last
@@ -1114,13 +1290,39 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
       su.pgrid = std::max(p1.grid(), p2.grid()) + 1;
       su.gb = gridbar_.as<GridBar>();
       su.B.nu1 = p1.grid();
+      su.np1 = p1.grid();
+      su.np2 = p2.grid();
+      // TREE: the calibrated partition over every worker CTA (no long rows,
+      // not interleaved, more slices than workers; AAPDHG_BALANCE=0: off)
+      auto plain = [&](const CsrDev& d) {
+        return d.nlong == 0 && !d.interleave && d.nslices >= workers &&
+               int64_t(d.nslices) <= int64_t(kWarps) * workers;
+      };
+      if (!serial && plain(p1) && plain(p2) && env_int("AAPDHG_BALANCE", 1) != 0) {
+        bool measure = false;
+        bal_setup(p1, p2, workers, &measure);
+        part1_.reserve(sizeof(double) * P1_COUNT * size_t(p1.nslices));
+        part2_.reserve(sizeof(double) * P2_COUNT * size_t(p2.nslices));
+        su.B.part1 = part1_.as<double>();
+        su.B.part2 = part2_.as<double>();
+        su.pk1.sl_start = bal_start1_.as<int32_t>();
+        su.pk2.sl_start = bal_start2_.as<int32_t>();
+        su.pk1.nblk_short = su.pk2.nblk_short = workers;
+        su.pgrid = workers + 1;
+        su.B.nu1 = workers;
+        su.np1 = p1.nslices;
+        su.np2 = p2.nslices;
+        su.bal = measure ? bal_stats_.as<unsigned long long>() : nullptr;
+        bal_measuring_ = measure;
+      }
     }
   }
   if (use_graph) {
     char key[256];
-    std::snprintf(key, sizeof key, "%d/%d/%d/%d/%p/%p/%p/%p/%p/%p/%p", method, int(serial), cap,
-                  int(su.persist), upool_.p, du_.p, partdot_.p, dparams_.p, rec_.p, stream_,
-                  gridbar_.p);
+    std::snprintf(key, sizeof key, "%d/%d/%d/%d/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p", method,
+                  int(serial), cap, int(su.persist), upool_.p, du_.p, partdot_.p, dparams_.p,
+                  rec_.p, stream_, gridbar_.p, (const void*)su.pk1.sl_start, (void*)su.bal,
+                  su.B.part1, su.B.part2);
     if (graph_key_ != key || !graph_exec_) {
       if (graph_exec_) {
         cudaGraphExecDestroy(graph_exec_);
@@ -1208,6 +1410,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   }
   const DevState st = *h_state_;
   ph("solve: iterations");
+  if (su.bal) bal_collect(su.pk1, su.pk2, su.pgrid - 1);
 
   // finish, solver.cpp:153-166
   const int slot = st.u_idx[st.final_role];
@@ -1874,6 +2077,19 @@ extern "C" int aapdhg_cuda_plain_stamps(double* out) {
   out[6] = c;
   unsigned long long z[8] = {};
   cudaMemcpyToSymbol(aapdhg_b200::g_plain_dbg, z, sizeof z);
+  return 0;
+}
+#endif
+
+#ifdef AAPDHG_PLAIN_STAMPS
+// experiment build only: per worker CTA (up to 1024) the K1 / K2 phase sums
+// (ns), the iteration count and the SM it ran on; reset after the read
+extern "C" int aapdhg_cuda_plain_stamps_cta(double* out) {
+  static unsigned long long v[1024 * 4];
+  if (cudaMemcpyFromSymbol(v, aapdhg_b200::g_plain_cta, sizeof v) != cudaSuccess) return -1;
+  for (int i = 0; i < 1024 * 4; ++i) out[i] = double(v[i]);
+  static unsigned long long z[1024 * 4] = {};
+  cudaMemcpyToSymbol(aapdhg_b200::g_plain_cta, z, sizeof z);
   return 0;
 }
 #endif

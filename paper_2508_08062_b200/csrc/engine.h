@@ -304,6 +304,12 @@ class Problem {
   cudaGraphConditionalHandle cond_loop_ = 0, cond_aa_ = 0;
   int core_nodes_ = 0, aa_nodes_ = 0;
   DevBuf gridbar_;  // k_plain_loop's barrier counters (GridBar)
+  // k_plain_loop's calibrated partition (CsrDev::sl_start): slice starts per
+  // worker CTA for K' and K, and the per-CTA phase times of the last launches
+  DevBuf bal_start1_, bal_start2_, bal_stats_;
+  bool bal_measuring_ = false;
+  void bal_setup(const CsrDev& a, const CsrDev& b, int workers, bool* measure);
+  void bal_collect(const CsrDev& a, const CsrDev& b, int workers);
   DevBuf ticket_;   // k_spmv_commit's last-CTA counter
   int32_t* h_batch_ = nullptr;  // pinned
 

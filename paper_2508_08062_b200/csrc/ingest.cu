@@ -361,9 +361,16 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
   int sf = 1;
   while (sf < 8 && int64_t(ser.nslices) * 2 * sf <= slots && mean >= 8.0 * sf) sf *= 2;
   sf = env_int("AAPDHG_SF", sf);
+  // a TREE layout that k_plain_loop can run with its calibrated partition
+  // (no long rows, at most one wave of slices: engine.cu bal_setup) sorts
+  // all rows by length too: each CTA then holds slices of one length, and the
+  // partition weighs the slices (configs[1] K2: 19.4 -> 18.5 us per phase)
+  const int64_t tree_slices = (int64_t(nshort) + 32 / sf - 1) / (32 / sf);
+  const bool tree_global = ragged || (nlong == 0 && !building_blocks_ &&
+                                      tree_slices <= slots && env_int("AAPDHG_BALANCE", 1) != 0);
   tree = base;
   if (sf == 1) tree = ser;
-  else device_sell(shorts, nshort, len, sf, st, st.sell[1], tree, s, ragged, mean);
+  else device_sell(shorts, nshort, len, sf, st, st.sell[1], tree, s, tree_global, mean);
   // TREE: a CTA per huge row (the SERIAL layout keeps one lane-0 chain per row)
   tree.nhuge = nhuge;
   tree.nblk_long = nhuge + (nlong - nhuge + kWarps - 1) / kWarps;

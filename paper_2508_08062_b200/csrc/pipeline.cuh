@@ -275,9 +275,25 @@ __device__ __forceinline__ double ldx(const double* p) {
   else return __ldg(p);
 }
 
+// Calibrated partition (CsrDev::sl_start): the warp's slice terms, summed by a
+// fixed warp tree, stored as the slice's partial row (lane 0).
+template <int NQ>
+__device__ __forceinline__ void slice_partials(const CsrDev& A, int b, double (&acc)[NQ],
+                                               double* part) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sl = __ldg(A.sl_start + b) + warp;
+  const bool own = sl < __ldg(A.sl_start + b + 1);
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const double v = warp_sum(acc[q]);
+    if (lane == 0 && own) part[q * A.nslices + sl] = v;
+  }
+}
+
 // rep: the warp's rep-th slice of an interleaved layout (returns -2 when the
 // warp has no more); otherwise only rep 0 exists.
-template <bool SERIAL, int UNROLL = kUnroll, bool COH = false, class Pre = NoPre>
+template <bool SERIAL, int UNROLL = kUnroll, bool COH = false, bool BAL = true,
+          class Pre = NoPre>
 __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, double& s,
                                        Pre pre = Pre{}, int bid = -1, int rep = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -290,6 +306,9 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     if (A.interleave) {  // slices b + nblk * (warp + kWarps * rep)
       sl = int(b + int64_t(A.nblk_short) * (warp + kWarps * rep));
       if (sl >= A.nslices) return -2;
+    } else if (BAL && A.sl_start) {  // calibrated partition (k_plain_loop)
+      sl = __ldg(A.sl_start + b) + warp;
+      if (sl >= __ldg(A.sl_start + b + 1)) return -1;
     } else {  // CTA b owns slices [b * ns / nblk, (b + 1) * ns / nblk): <= kWarps each
       sl = int(int64_t(b) * A.nslices / A.nblk_short) + warp;
       if (sl >= int(int64_t(b + 1) * A.nslices / A.nblk_short)) return -1;
@@ -436,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   double* out = o.out_pool ? o.out_pool + (int64_t)S->kx_idx[o.out_role] * o.out_stride : o.out;
   for (int rep = 0;; ++rep) {
     double s;
-    const int row = row_sum<SERIAL>(A, x, s, NoPre{}, -1, rep);
+    const int row = row_sum<SERIAL, kUnroll, false, false>(A, x, s, NoPre{}, -1, rep);
     if (row == -2) break;
     if (row >= 0) out[row] = s;
   }
@@ -783,7 +802,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   const double* x = xr.get(S);
   for (int rep = 0;; ++rep) {
     double s;
-    const int row = row_sum<false>(A, x, s, NoPre{}, -1, rep);
+    const int row = row_sum<false, kUnroll, false, false>(A, x, s, NoPre{}, -1, rep);
     if (row == -2) break;
     if (row >= 0) __stcs(part + row, first ? s : __dadd_rn(__ldcs(part + row), s));
   }
@@ -846,7 +865,7 @@ __device__ __forceinline__ void dual_side_rows(const CsrDev& KT, const IterBufs&
   bool first = true;  // one row per thread: the terms themselves (no add)
   for (int rep = 0;; ++rep) {
     double t;
-    const int j = row_sum<SERIAL, kUnroll, COH>(
+    const int j = row_sum<SERIAL, kUnroll, COH, !MULTI>(
         KT, P->ygather ? P->ygather : x + P->n, t, [&](int r) {
           l2_prefetch(x + r);
           l2_prefetch(B.c + r);
@@ -870,6 +889,12 @@ __device__ __forceinline__ void dual_side_rows(const CsrDev& KT, const IterBufs&
     if constexpr (!MULTI) break;  // (one slice per warp: no loop state)
   }
   if (VAR == 2) return;
+  if constexpr (!SERIAL && !MULTI) {
+    if (KT.sl_start) {
+      slice_partials<P1_COUNT>(KT, bid, acc, B.part1);
+      return;
+    }
+  }
   if (!SERIAL) {
     block_sum<P1_COUNT>(acc, red);
     if (threadIdx.x == 0)
@@ -968,7 +993,7 @@ __device__ __forceinline__ void primal_side_rows(const CsrDev& K, const IterBufs
   bool first = true;  // one row per thread: the terms themselves (no add)
   for (int rep = 0;; ++rep) {
     double s;
-    const int i = row_sum<SERIAL, kUnroll, COH>(
+    const int i = row_sum<SERIAL, kUnroll, COH, !MULTI>(
         K, P->xgather ? P->xgather : B.upool + (int64_t)S->u_idx[U_HAT] * N, s, NoPre{}, bid,
         rep);
     if (i == -2) break;
@@ -991,7 +1016,7 @@ __global__ void __launch_bounds__(kThreads, AAPDHG_K12_MINBLOCKS)
   if (S->done) return;
   if constexpr (VAR == 2) {
     double s;
-    const int i = row_sum<SERIAL>(K, B.upool + (int64_t)S->u_idx[U_HAT] * P->N, s);
+    const int i = row_sum<SERIAL, kUnroll, false, false>(K, B.upool + (int64_t)S->u_idx[U_HAT] * P->N, s);
     if (i >= 0) B.kxpool[(int64_t)S->kx_idx[KX_HAT] * P->mrows + i] = s;
     return;
   }
@@ -1043,6 +1068,8 @@ __global__ void __launch_bounds__(kThreads, AAPDHG_K12_MINBLOCKS)
 // bit-identical to the per-kernel graph with the same CTA layout.
 #ifdef AAPDHG_PLAIN_STAMPS
 __device__ unsigned long long g_plain_dbg[8];
+// experiment build: per CTA (k_plain_loop worker) K1 / K2 phase sums, count, SM id
+__device__ unsigned long long g_plain_cta[1024 * 4];
 #endif
 struct GridBar {
   unsigned long long arrive1;  // barrier 1: arrivals (low 40 bits) + stops (high bits)
@@ -1317,7 +1344,8 @@ __device__ __noinline__ void plain_loop_control(const IterBufs& B, const DevPara
 template <bool PUSH, bool SERIAL = false>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_plain_loop(CsrDev KT, CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S,
-                 GridBar* gb, int nb1, int nb2) {
+                 GridBar* gb, int nb1, int nb2, int np1, int np2,
+                 unsigned long long* __restrict__ bal) {
   __shared__ __align__(16) DevState st;  // worker: roles of its iteration; control: the state
   __shared__ double red[P1_COUNT * 32];
   __shared__ int s_stop;
@@ -1326,7 +1354,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   if (st.done || st.batch_left <= 0) return;  // (eager launches past the batch)
   if (bid == W) {
     __shared__ __align__(16) DevParams pr;
-    plain_loop_control<SERIAL>(B, P, S, gb, nb1, nb2, st, pr, red);
+    plain_loop_control<SERIAL>(B, P, S, gb, np1, np2, st, pr, red);
     return;
   }
   unsigned long long h0 = 0;  // stop flags raised before this launch
@@ -1338,6 +1366,10 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   uint64_t ps0 = globaltimer_ns(), ps1 = 0, ps2 = 0, ps3 = 0;
 #endif
   const bool pf = P->phase_prefetch != 0;
+  // calibration (bal): this CTA's K1 / K2 phase times (start of its rows to
+  // its barrier arrival), iterations and SM, for the host's partition
+  uint64_t tb0 = 0, tb1 = 0, tb2 = 0;
+  if (bal && threadIdx.x == 0) tb0 = globaltimer_ns();
   for (;;) {
     if (pf && bid < nb2) prefetch_slice_streams(K, bid);  // K2's streams, one phase ahead
     if constexpr (SERIAL) {  // K'y of iteration k into its parity buffer (the control's chains)
@@ -1351,9 +1383,11 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 #ifdef AAPDHG_PLAIN_STAMPS
     if (threadIdx.x == 0) ps1 = globaltimer_ns();
 #endif
+    if (bal && threadIdx.x == 0) tb1 = globaltimer_ns();
     if (threadIdx.x == 0) s_stop = (bar_arrive_wait(&gb->arrive1, 1, G) >> 40) != h0;
     __syncthreads();
     if (s_stop) return;  // the control stopped after the previous iteration
+    if (bal && threadIdx.x == 0) tb2 = globaltimer_ns();
 #ifdef AAPDHG_PLAIN_STAMPS
     if (threadIdx.x == 0) ps2 = globaltimer_ns();
 #endif
@@ -1362,13 +1396,26 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     if (bid < nb2) {
       primal_side_rows<SERIAL, PUSH, true>(K, B, P, &st, bid, acc);
       if constexpr (!SERIAL) {
-        block_sum<P2_COUNT>(acc, red);
-        if (threadIdx.x == 0)
+        if (K.sl_start) {
+          slice_partials<P2_COUNT>(K, bid, acc, B.part2);
+        } else {
+          block_sum<P2_COUNT>(acc, red);
+          if (threadIdx.x == 0)
 #pragma unroll
-          for (int q = 0; q < P2_COUNT; ++q) B.part2[q * nb2 + bid] = acc[q];
+            for (int q = 0; q < P2_COUNT; ++q) B.part2[q * nb2 + bid] = acc[q];
+        }
       }
     }
     __syncthreads();
+    if (bal && threadIdx.x == 0) {
+      const uint64_t t3 = globaltimer_ns();
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      bal[4 * bid + 0] += tb1 - tb0;
+      bal[4 * bid + 1] += t3 - tb2;
+      bal[4 * bid + 2] += 1;
+      bal[4 * bid + 3] = smid;
+    }
 #ifdef AAPDHG_PLAIN_STAMPS
     if (threadIdx.x == 0) ps3 = globaltimer_ns();
 #endif
@@ -1395,6 +1442,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     }
     __syncthreads();
     if (s_stop) return;
+    if (bal && threadIdx.x == 0) tb0 = globaltimer_ns();
 #ifdef AAPDHG_PLAIN_STAMPS
     if (threadIdx.x == 0) {
       const uint64_t ps4 = globaltimer_ns();
@@ -1403,6 +1451,14 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
       atomicAdd(&g_plain_dbg[2], ps3 - ps2);
       atomicAdd(&g_plain_dbg[3], ps4 - ps3);
       atomicAdd(&g_plain_dbg[4], 1ull);
+      if (bid < 1024) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_plain_cta[bid * 4 + 0] += ps1 - ps0;
+        g_plain_cta[bid * 4 + 1] += ps3 - ps2;
+        g_plain_cta[bid * 4 + 2] += 1;
+        g_plain_cta[bid * 4 + 3] = smid;
+      }
       atomicMax(&g_plain_dbg[5], ps1 - ps0);
       atomicMax(&g_plain_dbg[6], ps3 - ps2);
       ps0 = ps4;

@@ -310,6 +310,33 @@ def test_persistent_loop_matches_per_kernel_graph(monkeypatch, method):
                                        rtol=1e-12)
 
 
+def test_persistent_loop_calibrated_partition_is_bitwise_neutral(monkeypatch):
+    """k_plain_loop shares the slices out per SM from measured phase times
+    (engine.cu rebalance) and keeps its partials per slice, so the partition
+    never changes the bits: the first solve of a layout shape (proportional
+    partition) equals solves after three calibration rounds bit for bit, and
+    the per-CTA partials of AAPDHG_BALANCE=0 agree to rounding."""
+    p = problems.make_config(1, scale=0.21)  # (a shape no other test calibrates)
+    cfg = SolverConfig(method=Method.AA_PDHG, m=10, toll=1e-12, max_iters=300, tau=0.05,
+                       sigma=0.05, reduction="tree")
+    with Solver(p) as s:
+        first = s.solve(cfg)
+        for _ in range(3):
+            s.solve(cfg)
+        again = s.solve(cfg)
+    assert first.result.i > 0
+    for f in ("g_norm", "r_gap", "r_primal", "r_dual", "objective", "aa_step"):
+        assert np.array_equal(first.trajectory[f], again.trajectory[f]), f
+    assert np.array_equal(first.result.u.x, again.result.u.x)
+    assert np.array_equal(first.result.u.y, again.result.u.y)
+    monkeypatch.setenv("AAPDHG_BALANCE", "0")
+    with Solver(p) as s:
+        plain = s.solve(cfg)
+    assert np.array_equal(plain.trajectory["aa_step"], first.trajectory["aa_step"])
+    np.testing.assert_allclose(plain.trajectory["g_norm"][:50], first.trajectory["g_norm"][:50],
+                               rtol=1e-12)
+
+
 def test_persistent_loop_fixed_point_start_tree():
     """The speculative K1 of k = 2 in k_plain_loop rewrites u_0's buffer while
     the control decides k = 1. A fixed-point start (status FIXED_POINT_START,
