@@ -1,11 +1,16 @@
-"""Benchmark: AA-PDHG fp64 iterations/sec on BASELINE.json configs[1].
+"""Benchmark: AA-PDHG fp64 iterations/sec on BASELINE.json configs[4] (the
+north-star scaling LP) at every N, with configs[1] as an extra key.
 
-Workload (BASELINE.json configs[1]): planted-optimum LP,
-100,000 rows x 200,000 cols, exactly 20 distinct uniform rows per column
-(4.0M nnz), N(0,1) values, AA-PDHG with memory m = 10, D = 1, eps = 1,
-beta = 1, eta = 1e-10, toll = 1e-6. Synthetic seeded data (the reference
-publishes no instance files). One "step" = one solver iteration (PDHG map +
-history push + safeguard, the AA candidate on accepted steps, KKT records).
+Workload (BASELINE.json configs[4]): planted-optimum LP,
+20,000,000 rows x 40,000,000 cols, 10 distinct uniform rows per column (400M
+nnz), N(0,1) values, AA-PDHG with memory m = 10, D = 1, eps = 1, beta = 1,
+eta = 1e-10, toll = 1e-6 — the largest BASELINE config that fits one B200
+and the LP north_star scales over 1/2/4/8 GPUs, so BENCH (N=1) and the
+scaling curve share one workload. The `config1` key holds the
+same measurements on configs[1] (100k x 200k, 4M nnz, m = 10; "Single GPU")
+with its time to 1e-6 KKT. Synthetic seeded data (the reference publishes no
+instance files). One "step" = one solver iteration (PDHG map + history push +
+safeguard, the AA candidate on accepted steps, KKT records).
 
 Arms
   ours (default)      the sm_100a C-ABI (paper_2508_08062_b200/lib/libaapdhg_cuda.so)
@@ -33,7 +38,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CONFIG_ID = 1  # the workload (select_workload)
+CONFIG_ID = 4  # the workload (select_workload)
 MEMORY = 10
 TOLL = 1e-6
 GATHER_CEILING = 240.3e9  # measured random-gather rate (profiles/r01/gather.txt)
@@ -41,7 +46,7 @@ METRICS = {
     1: "AA-PDHG fp64 iterations/sec (BASELINE configs[1]: 100k x 200k, 4M nnz, m=10)",
     4: "AA-PDHG fp64 iterations/sec (BASELINE configs[4]: 20M x 40M, 400M nnz, m=10)",
 }
-METRIC = METRICS[1]
+METRIC = METRICS[4]
 WORKLOADS = {
     1: "configs[1] planted LP 100000x200000, 20 nnz/col (4.0M nnz), AA-PDHG m=10, D=1, eps=1, "
        "toll=1e-6",
@@ -51,15 +56,10 @@ WORKLOADS = {
 
 
 def select_workload(args, world):
-    """configs[1] at N = 1 (the metric's single-GPU config, BASELINE.json),
-    configs[4] at N > 1 (the north-star scaling LP) unless --workload says."""
+    """configs[4] (the north-star scaling LP) at every N unless --workload
+    config1 says otherwise."""
     global CONFIG_ID, METRIC
-    if args.workload == "config1":
-        CONFIG_ID = 1
-    elif args.workload == "config4":
-        CONFIG_ID = 4
-    else:
-        CONFIG_ID = 1 if world == 1 and not args.loopback else 4
+    CONFIG_ID = 1 if args.workload == "config1" else 4
     METRIC = METRICS[CONFIG_ID]
 
 
@@ -186,6 +186,16 @@ def kernel_bytes(p, name):
         return kernel_bytes(p, "k_dual_side") + kernel_bytes(p, "k_primal_side")
     if name == "k_spmv_recache":
         return 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
+    if name == "k_spmv_pass":  # mean over the column passes (engine.cu build_blocks)
+        per = []
+        for rows, cols in ((n, m), (m, n)):  # K' gathers y (m), K gathers x (n)
+            nb = -(-cols * 8 // (80 << 20))  # (engine.cu build_blocks: 80 MB blocks
+            if cols * 8 <= (64 << 20) or nb < 2:  # above 64 MB vectors)
+                continue
+            w = -(-cols // nb)
+            for b in range(nb - 1):  # the last block is fused into K1 / K2
+                per.append(12 * nnz * w / cols + 8 * w + 8 * rows * (1 if b == 0 else 2))
+        return sum(per) / len(per) if per else None
     return None
 
 
@@ -214,8 +224,18 @@ def run_reference_arm(args, rank, world):
     kind = "reference" if ref_available() else "port"
     orc = Oracle("ref" if kind == "reference" else "port")
     # step sizes once (the reference's seeded power iteration), then time
-    # `steps` iterations per sample after `warmup` untimed iterations
-    tau = orc.select_step_sizes(p, solver_config()).tau
+    # `steps` iterations per sample after `warmup` untimed iterations;
+    # configs[4]: the reference's own tau from its fixture run
+    # (tests/golden/fullsize_cfg4.json, select_step_sizes ~1,000 s on one core)
+    tau = None
+    if CONFIG_ID == 4:
+        try:
+            tau = float.fromhex(json.loads(
+                (ROOT / "tests" / "golden" / "fullsize_cfg4.json").read_text())["tau"])
+        except Exception:
+            tau = None
+    if tau is None:
+        tau = orc.select_step_sizes(p, solver_config()).tau
     iters_per_step = 1
     orc.solve(p, solver_config(tau=tau, max_iters=max(args.warmup, 1)))
     t0 = time.perf_counter()
@@ -387,6 +407,8 @@ def run_ours(args, rank, world, local_rank):
         if plain:
             roofline = plain_loop_roofline(args, p, plain, ms)
             roofline["per_kernel_graph"] = eager
+        elif CONFIG_ID == 4:  # the whole iteration (column passes + fused halves)
+            roofline = iteration_roofline(p, iters, out.result.i, ms, eager)
         else:
             roofline = eager
 
@@ -422,18 +444,19 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- CPU baseline on this host (rank 0, N=1 only) ----------------------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and CONFIG_ID == 1:
-        v, kind, dt = cpu_reference_sample(p, tau, args.cpu_iters)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu_iters = 1 if CONFIG_ID == 4 else args.cpu_iters  # (~50 s per configs[4] iteration)
+        v, kind, dt = cpu_reference_sample(p, tau, cpu_iters)
         cpu = {"value": v, "unit": "iterations/s", "cores": 1, "kind": kind,
                "host": host_cpu(),
-               "sample": f"{args.cpu_iters} iterations of configs[1] (explicit tau), "
+               "sample": f"{cpu_iters} iteration(s) of configs[{CONFIG_ID}] (explicit tau), "
                          f"{dt:.1f} s, 1 thread on a {host_cpu()}: the reference "
                          f"solve() is single-threaded"}
 
-    # ---- configs[4] (20M x 40M, 400M nnz) on this one GPU -----------------
-    c4 = None
-    if rank == 0 and world == 1 and CONFIG_ID == 1 and not args.no_config4 and not dist:
-        c4 = config4_leg(args, torch, dev, stream)
+    # ---- configs[1] (100k x 200k, 4M nnz) on this one GPU -----------------
+    c1 = None
+    if rank == 0 and world == 1 and CONFIG_ID == 4 and not args.no_config1 and not dist:
+        c1 = config1_leg(args, torch, dev, stream)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
@@ -454,8 +477,8 @@ def run_ours(args, rank, world, local_rank):
             line["parallelism"] = (f"loopback{args.loopback}: {args.loopback} shards in one "
                                    f"process on one GPU ({args.transport} exchanges) — a dry "
                                    f"run of the sharded path, not a multi-GPU measurement")
-        if c4 is not None:
-            line["config4"] = c4
+        if c1 is not None:
+            line["config1"] = c1
         print(json.dumps(line), flush=True)
 
 
@@ -470,73 +493,90 @@ def iteration_bytes(p, iters, aa_steps, memory=MEMORY):
     return iters * kernel_bytes(p, "k_plain_loop") + aa_steps * aa
 
 
-def config4_leg(args, torch, dev, stream):
-    """configs[4] — the largest LP of BASELINE.json, the north-star scaling
-    LP — on this single GPU: generation (cached on disk), device ingestion,
-    `steps` resident iterations (device events), the iteration roofline, the
-    per-kernel times and the e2e path from page-locked buffers."""
+def iteration_roofline(p, iters, aa_steps, ms, eager):
+    """configs[4]'s roofline: the algorithmic bytes of the timed iterations
+    (iteration_bytes: K1 + K2 with the push per iteration, plus the Gram, the
+    mix and the recache per AA step) over the device time of the timed solve
+    (CUDA events on the solver's stream); the per-kernel table and the
+    dominant kernel's own figure from the eager profile beside it."""
+    peak, peak_kind = measured_peak()
+    byts = iteration_bytes(p, iters, aa_steps)
+    ach = byts / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": "iteration (k_spmv_pass x4 + k_dual_side + k_primal_side"
+                                      " per plain step; + AA branch)",
+            "achieved": ach, "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
+            "frac": ach / peak, "traffic": None,
+            "bytes": byts, "bytes_per_plain_iteration": kernel_bytes(p, "k_plain_loop"),
+            "timing": "CUDA events on the solver stream around the timed solve",
+            "dominant_kernel": eager}
+
+
+def config1_leg(args, torch, dev, stream):
+    """configs[1] (100k x 200k, 4M nnz, AA m=10; BASELINE's "Single GPU"
+    config) on this GPU: the same measurements as the headline (resident
+    iterations/s, k_plain_loop roofline, e2e from page-locked buffers, the
+    reference CPU baseline) plus the time to max KKT <= 1e-6."""
     import ctypes as C
 
     from paper_2508_08062_b200 import Solver
     from paper_2508_08062_b200.api import check, errbuf
-    t0 = time.perf_counter()
-    p = load_workload(4)
-    gen_s = time.perf_counter() - t0
+    p = load_workload(1)
     t0 = time.perf_counter()
     s = Solver(p, device=dev)
     create_s = time.perf_counter() - t0
     lib = s.lib
     check(lib.aapdhg_cuda_set_stream(s.h, C.c_void_p(stream.cuda_stream)), errbuf())
     tau = s.select_step_sizes(solver_config()).tau
-    s.solve(solver_config(tau=tau, max_iters=max(args.warmup, 3)))
-    n, m = p.n(), p.k.nrows
-    outs = tuple(torch.empty(k, dtype=torch.float64, pin_memory=True).numpy() for k in (n, m, n))
-    steps = min(args.steps, 200)  # (~10 ms per iteration: a bounded leg)
-    cfg = solver_config(tau=tau, max_iters=steps)
+    # warm-up: graph instantiation and the persistent grid's first partition
+    # calibration (engine.cu rebalance: a solve of >= 16 iterations)
+    s.solve(solver_config(tau=tau, max_iters=max(args.warmup, 64)))
+    hp, hout = pinned_problem(torch, p)
+    cfg = solver_config(tau=tau, max_iters=args.steps)
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         ev0.record(stream)
-        out = s.solve(cfg, out=outs)
+        out = s.solve(cfg, out=hout)
         ev1.record(stream)
     torch.cuda.synchronize(dev)
     ms = ev0.elapsed_time(ev1)
-    iters, aa = out.result.iterations, out.result.i
-    peak, peak_kind = measured_peak()
-    byts = iteration_bytes(p, iters, aa)
-    import copy
-    a2 = copy.copy(args)
-    a2.steps = steps
-    per_kernel = kernel_roofline(a2, p, s, lib, tau).get("per_kernel_us")
+    iters = out.result.iterations
+    pi, ps, pl = C.c_uint64(), C.c_double(), C.c_uint64()
+    lib.aapdhg_cuda_last_plain_loop(s.h, C.byref(pi), C.byref(ps), C.byref(pl))
+    eager = kernel_roofline(args, p, s, lib, tau)
+    if pl.value:
+        roofline = plain_loop_roofline(args, p, (int(pi.value), float(ps.value), int(pl.value)),
+                                       ms)
+        roofline["per_kernel_graph"] = eager
+    else:
+        roofline = eager
+    ttt = None if args.no_ttt else time_to_tol(args, p, s)
     s.close()
-    del outs
-    # e2e: the LP in page-locked buffers, create + solve + download
-    hp, hout = pinned_problem(torch, p)
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     s2 = Solver(hp, device=dev)
-    out2 = s2.solve(solver_config(tau=tau, max_iters=steps), out=hout)
+    out2 = s2.solve(solver_config(tau=tau, max_iters=args.steps), out=hout)
     e2e_s = time.perf_counter() - t0
     s2.close()
     h2d = sum(a.nbytes for a in (p.k.row_ptr, p.k.col_idx, p.k.vals, p.c, p.q, p.l, p.u))
     d2h = (p.n() * 16 + p.k.nrows * 8) + out2.trajectory.nbytes
-    return {"workload": WORKLOADS[4], "rows": m, "cols": n, "nnz": int(p.k.nnz),
-            "value": iters / (ms / 1e3), "unit": "iterations/s", "ms_per_step": ms / max(iters, 1),
-            "iterations_timed": iters, "aa_steps_timed": aa,
-            "roofline": {"bound": "hbm", "scope": "whole iteration (all kernels of the timed "
-                                                  "solve, device events)",
-                         "achieved": byts / (ms / 1e3) / 1e9, "peak": peak,
-                         "peak_source": peak_kind, "unit": "GB/s",
-                         "frac": byts / (ms / 1e3) / 1e9 / peak,
-                         "bytes": byts, "bytes_per_plain_iteration": kernel_bytes(p, "k_plain_loop")},
-            "per_kernel_us": per_kernel,
+    cpu = None
+    if not args.no_cpu:
+        v, kind, dt = cpu_reference_sample(p, tau, args.cpu_iters)
+        cpu = {"value": v, "unit": "iterations/s", "cores": 1, "kind": kind, "host": host_cpu(),
+               "sample": f"{args.cpu_iters} iterations of configs[1] (explicit tau), {dt:.1f} s,"
+                         f" 1 thread on a {host_cpu()}: the reference solve() is "
+                         f"single-threaded"}
+    return {"metric": METRICS[1], "workload": WORKLOADS[1], "rows": p.k.nrows, "cols": p.n(),
+            "nnz": int(p.k.nnz), "value": iters / (ms / 1e3), "unit": "iterations/s",
+            "ms_per_step": ms / max(iters, 1), "iterations_timed": iters,
+            "aa_steps_timed": out.result.i, "roofline": roofline,
             "e2e": {"value": out2.result.iterations / e2e_s, "unit": "iterations/s",
                     "seconds": e2e_s, "h2d_bytes_per_step": h2d / max(out2.result.iterations, 1),
-                    "d2h_bytes_per_step": d2h / max(out2.result.iterations, 1)},
-            "generate_or_map_s": gen_s, "create_s": create_s,
-            "cpu_reference_note": "reference solve() on configs[4]: ~50 s per iteration on one "
-                                  "core and ~30 GB RAM (tests/golden/fullsize_cfg4.json: 20 "
-                                  "iterations in 1036 s in the build container); not re-run here"}
+                    "d2h_bytes_per_step": d2h / max(out2.result.iterations, 1),
+                    "path": "aapdhg_cuda_problem_create + aapdhg_cuda_solve (explicit tau) + "
+                            "result download; LP and results in page-locked host buffers"},
+            "cpu_baseline": cpu, "time_to_tol": ttt, "create_s": create_s}
 
 
 def plain_loop_roofline(args, p, plain, step_ms):
@@ -602,7 +642,7 @@ def kernel_roofline(args, p, s, lib, tau):
     # x[col], one per nonzero, against the measured B200 ceiling
     gr = {}
     for k in ("k_dual_side", "k_primal_side"):
-        if k in kstats:
+        if k in kstats and "k_spmv_pass" not in kstats:  # (blocked: a launch gathers one block)
             us = 1e3 * kstats[k][0] / max(kstats[k][1], 1)
             gr[k] = {"gathers_per_launch": int(p.k.nnz), "avg_launch_us": us,
                      "achieved_gather_per_s": p.k.nnz / (us * 1e-6),
@@ -649,12 +689,12 @@ def main():
                     help="use the sharded solve even at N=1 (exercises the N>1 path)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel, if captured")
-    ap.add_argument("--workload", choices=["auto", "config1", "config4"], default="auto",
-                    help="auto: configs[1] at N=1, configs[4] (the scaling LP) at N>1")
+    ap.add_argument("--workload", choices=["config4", "config1"], default="config4",
+                    help="the timed LP (configs[4] at every N by default)")
     ap.add_argument("--loopback", type=int, default=0,
                     help="dry run of the sharded solve: K in-process shards on this one GPU")
-    ap.add_argument("--no-config4", action="store_true",
-                    help="skip the configs[4] single-GPU leg of the N=1 line")
+    ap.add_argument("--no-config1", action="store_true",
+                    help="skip the configs[1] leg of the N=1 line")
     args = ap.parse_args()
     if args.impl == "reference":
         # bounded CPU sample: <= 500 iterations (~20 s of reference work at

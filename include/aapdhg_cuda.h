@@ -342,7 +342,9 @@ int aapdhg_cuda_set_stream(aapdhg_handle* h, void* stream);
  * the handle's own stream around each launch. Enabling it switches the
  * solve loop from CUDA-graph replay to eager launches for that call. */
 int aapdhg_cuda_set_profiling(aapdhg_handle* h, int32_t enable);
-/* names: '\n'-separated kernel names; ms[k]/launches[k] accumulated totals.
+/* names: '\n'-separated kernel names; ms[k]/launches[k] accumulated totals
+ * over the launches that did work (a launch under 30% of the kernel's longest
+ * is taken for a device-predicated no-op and left out).
  * Returns the number of kernels in *count. */
 int aapdhg_cuda_kernel_times(aapdhg_handle* h, char* names, size_t names_len,
                              double* ms, uint64_t* launches, int32_t cap,

@@ -79,6 +79,7 @@ __global__ void k_serial_dots(DotBufs D, const DevParams* __restrict__ P, const 
 // Column chunks are re-read from L1 across items; HBM sees each once.
 __global__ void __launch_bounds__(kThreads)
     k_tree_dots(DotBufs D, const DevParams* __restrict__ P, const DevState* S) {
+  TL_MARK(19);
   if (S->done || !S->aa_attempt) return;
   // the memory's slot table once per CTA (not a dependent global load per item)
   __shared__ int slots[kMaxMemory];
@@ -159,6 +160,7 @@ template <int CAP, bool FAA>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gram_dots(DotBufs D, double* __restrict__ upool, const DevParams* __restrict__ P,
                 const DevState* S) {
+  TL_MARK(10);
   if (S->done || !S->aa_attempt) return;
   constexpr int NPAIR = CAP * (CAP + 1) / 2;
   constexpr int NACC = NPAIR + CAP + (FAA ? CAP : 0);
@@ -238,6 +240,7 @@ template <int CAP, int SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gram_dots_dd(DotBufs D, double* __restrict__ upool, const DevParams* __restrict__ P,
                    const DevState* S) {
+  TL_MARK(11);
   if (S->done || !S->aa_attempt) return;
   constexpr int NPAIR = CAP * (CAP + 1) / 2;
   constexpr int NDD = NPAIR + CAP;                        // Gram + rhs items (dd)
@@ -369,7 +372,68 @@ __device__ bool dev_cholesky_solve(int p, double* a, double* rhs) {
 // the forward substitution is applied column by column (each rhs_k still
 // subtracts A_k0 r0, A_k1 r1, ... in that order), the backward one stays
 // row by row — so the result is bit for bit the same.
+// p <= 32: the same factorization and solves by warp 0 alone (lane i owns row
+// i; the operation order of every element is the one above, so the bits are
+// too), with warp shuffles instead of CTA barriers between the columns.
+__device__ bool warp_cholesky_solve(int p, double* a, double* rhs) {
+#define A_(i, j) a[(j) * p + (i)]
+  __shared__ int ok_sh;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    bool ok = true;
+    for (int j = 0; j < p && ok; ++j) {
+      double d = 0.0;
+      int bad = 0;
+      if (lane == 0) {
+        d = A_(j, j);
+        for (int k = 0; k < j; ++k) d = __dsub_rn(d, __dmul_rn(A_(j, k), A_(j, k)));
+        bad = d <= 0.0;
+        if (!bad) {
+          d = sqrt(d);
+          A_(j, j) = d;
+        }
+      }
+      d = __shfl_sync(0xffffffffu, d, 0);
+      bad = __shfl_sync(0xffffffffu, bad, 0);
+      __syncwarp();
+      if (bad) {
+        ok = false;
+        break;
+      }
+      const int i = j + 1 + lane;
+      if (i < p) {
+        double s = A_(i, j);
+        for (int k = 0; k < j; ++k) s = __dsub_rn(s, __dmul_rn(A_(i, k), A_(j, k)));
+        A_(i, j) = s / d;
+      }
+      __syncwarp();
+    }
+    if (ok) {
+      double r = lane < p ? rhs[lane] : 0.0;  // lane k holds rhs[k]
+      for (int i = 0; i < p; ++i) {
+        double ri = __shfl_sync(0xffffffffu, r, i);
+        ri = ri / A_(i, i);
+        if (lane == i) r = ri;
+        if (lane > i && lane < p) r = __dsub_rn(r, __dmul_rn(A_(lane, i), ri));
+      }
+      if (lane < p) rhs[lane] = r;
+      __syncwarp();
+      if (lane == 0)
+        for (int i = p - 1; i >= 0; --i) {
+          double t = rhs[i];
+          for (int k = i + 1; k < p; ++k) t = __dsub_rn(t, __dmul_rn(A_(k, i), rhs[k]));
+          rhs[i] = t / A_(i, i);
+        }
+    }
+    if (lane == 0) ok_sh = ok ? 1 : 0;
+  }
+  __syncthreads();
+#undef A_
+  return ok_sh != 0;
+}
+
 __device__ bool block_cholesky_solve(int p, double* a, double* rhs) {
+  if (p <= 32) return warp_cholesky_solve(p, a, rhs);
 #define A_(i, j) a[(j) * p + (i)]
   __shared__ double dsh;
   __shared__ int bad;
@@ -448,6 +512,7 @@ __global__ void __launch_bounds__(1024)
     k_aa_solve(DotBufs D, const DevParams* __restrict__ P, DevState* Sg, int per_op,
                const double* __restrict__ rank_tot = nullptr, int nranks = 0,
                int rank_stride = 0) {
+  TL_MARK(12);
   if (Sg->done || !Sg->aa_attempt) return;
   __shared__ DevState smS;
   state_load(&smS, Sg);
@@ -514,6 +579,7 @@ __global__ void __launch_bounds__(1024)
     }
   }
   __syncthreads();
+  TL_MARK(24);
   const int npair = p * (p + 1) / 2;
   double* G = W.gram;  // p x p column-major, full symmetric (item (a<=b) row-major upper)
   for (int t = threadIdx.x; t < p * p; t += blockDim.x) {
@@ -539,6 +605,7 @@ __global__ void __launch_bounds__(1024)
     const bool solved = block_cholesky_solve(p, A, W.vec);
     if (threadIdx.x == 0) aa_solved = solved ? 1 : 0;
     __syncthreads();
+    TL_MARK(25);
   }
   // FAA (filtering.cpp:140-181): angle filter on the newest-first order,
   // length filter, then the least-squares weights of the kept columns, all
@@ -745,6 +812,7 @@ __global__ void __launch_bounds__(1024)
   }
   }  // thread 0
   state_store(Sg, &smS);
+  TL_MARK(23);
 }
 
 // cand = P_feasible(u + damp(g) - sum_j w_j (du_j + damp(dg_j)))
@@ -752,6 +820,7 @@ __global__ void __launch_bounds__(1024)
 __global__ void __launch_bounds__(kThreads)
     k_mix(IterBufs B, const double* __restrict__ dg, const DevParams* __restrict__ P,
           const DevState* S, int project) {
+  TL_MARK(13);
   if (S->done || !S->aa_ok) return;
   const int64_t N = P->N;
   const int n = P->n;
@@ -812,6 +881,7 @@ __global__ void __launch_bounds__(kThreads)
 // the push derives g_{k-1} from du (solver.cpp:204-209).
 __global__ void k_stage_g(const double* __restrict__ upool, double* __restrict__ gpool,
                           const DevParams* __restrict__ P, const DevState* S) {
+  TL_MARK(18);
   if (S->done || !S->aa_attempt) return;
   const int64_t N = P->N;
   const double* uh = upool + (int64_t)S->u_idx[U_HAT] * N;
@@ -825,6 +895,7 @@ __global__ void k_stage_g(const double* __restrict__ upool, double* __restrict__
 // End of an iteration that attempted an AA step (the IF body of the graph):
 // rotate to the candidate (or to T(u) after a SingularError fallback).
 __global__ void k_aa_commit(const DevParams* __restrict__ P, DevState* S) {
+  TL_MARK(21);
   if (S->done || !S->aa_attempt) return;
   __shared__ DevState sm;
   state_load(&sm, S);
@@ -841,6 +912,7 @@ template <bool SERIAL>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_spmv_commit(CsrDev A, VecRef xr, RowsumArgs o, const DevParams* __restrict__ P,
                   DevState* S, unsigned int* ticket) {
+  TL_MARK(15);
   if (S->done || !S->aa_attempt) return;
   __shared__ DevState sm;
   if (!S->aa_ok) {
@@ -857,7 +929,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     double v;
     const int row = row_sum<SERIAL, kUnroll, false, false>(A, x, v, NoPre{}, -1, rep);
     if (row == -2) break;
-    if (row >= 0) out[row] = v;
+    if (row >= 0) out[row] = o.rinit ? __dadd_rn(o.rinit[row], v) : v;
   }
   __shared__ int last;
   __syncthreads();
@@ -880,6 +952,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
 // u0 -> P_feasible(u0) in place (pdhg_core.cpp:41-43); records t0.
 __global__ void k_project_start(double* u, const double* l, const double* uu, int n,
                                 int64_t N, int m1, DevState* S) {
+  TL_MARK(22);
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t == 0 && S) S->t0_ns = globaltimer_ns();
   if (t >= N) return;

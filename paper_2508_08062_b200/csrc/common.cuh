@@ -190,6 +190,7 @@ struct RowsumArgs {
   int64_t out_stride;
   int32_t pred_aa_ok;
   const int32_t* stop;
+  const double* rinit;  // L2-blocked: the earlier column passes' partial sums (or null)
 };
 
 struct IterBufs {
@@ -261,5 +262,27 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+
+// Experiment build only (EXTRA=-DAAPDHG_TIMELINE): CTA 0 of each kernel
+// stamps (kernel id, globaltimer) on entry; aapdhg_cuda_timeline reads them.
+#ifdef AAPDHG_TIMELINE
+__device__ unsigned long long g_tl[2 * 8192];
+__device__ unsigned int g_tl_n;
+__device__ __forceinline__ void tl_mark(unsigned long long id) {
+  const unsigned i = atomicAdd(&g_tl_n, 1u);
+  if (i < 8192) {
+    g_tl[2 * i] = id;
+    g_tl[2 * i + 1] = globaltimer_ns();
+  }
+}
+#define TL_MARK(id)                                          \
+  do {                                                       \
+    if (blockIdx.x == 0 && threadIdx.x == 0) tl_mark(id);    \
+  } while (0)
+#else
+#define TL_MARK(id) \
+  do {              \
+  } while (0)
+#endif
 
 }  // namespace aapdhg_b200

@@ -315,14 +315,16 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
 }
 
 // L2 column blocking (TREE mode only). A matrix whose gathered vector is
-// larger than the L2 budget (AAPDHG_L2_BLOCK_KB, default 64 MB per block;
+// larger than the L2 budget (AAPDHG_L2_BLOCK_KB, default 80 MB per block:
+// configs[4]'s x in 4 passes, y in 2 — fewer passes beat the extra gather
+// misses of a block above L2's clean ~48 MB, profiles/r02/cfg4_l2_persist.txt;
 // blocking starts above AAPDHG_L2_BLOCK_MIN_KB, default 64 MB) is split into column blocks; each block's
 // rows are the same rows restricted to its columns (CSR order kept), so a
 // pass gathers only from an L2-resident slice of the vector instead of one
 // DRAM sector per nonzero. Row sums become (((b0 + b1) + b2) + ...) — fixed
 // order, deterministic, not the CPU's association.
 void Problem::build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& out) {
-  const int64_t kb = env_int("AAPDHG_L2_BLOCK_KB", 64 << 10);      // per block
+  const int64_t kb = env_int("AAPDHG_L2_BLOCK_KB", 80 << 10);      // per block
   const int64_t min_kb = env_int("AAPDHG_L2_BLOCK_MIN_KB", 64 << 10);  // start above
   const int64_t vec_bytes = int64_t(ncols) * 8;
   if (kb <= 0 || nrows == 0 || vec_bytes <= (min_kb << 10)) return;
@@ -345,12 +347,12 @@ void Problem::build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& o
 }
 
 int Problem::launch_blocked_passes(cudaStream_t s, const Blocked& bk, const VecRef& x,
-                                   const DevState* S) {
+                                   const DevState* S, int pred_aa, const int32_t* stop) {
   int nodes = 0;
   for (int b = 0; b + 1 < bk.nb(); ++b) {
     prof_begin(s, "k_spmv_pass");
     k_spmv_pass<<<bk.blk[b].grid(), kThreads, 0, s>>>(bk.blk[b], x, bk.partial.as<double>(),
-                                                     b == 0 ? 1 : 0, S);
+                                                     b == 0 ? 1 : 0, S, pred_aa, stop);
     prof_end(s);
     AAPDHG_CUDA(cudaGetLastError());
     ++nodes;
@@ -371,6 +373,19 @@ int Problem::spmv(cudaStream_t s, const CsrDev& A, const VecRef& x, const Rowsum
   prof_end(s);
   AAPDHG_CUDA(cudaGetLastError());
   return 1;
+}
+
+// out = K x (transpose: K'y), through the L2 column blocks when the TREE
+// layout has them (the passes, then the last block on their partial sums)
+int Problem::spmv_any(cudaStream_t s, bool transpose, const VecRef& x, RowsumArgs r, bool serial,
+                      const DevState* S, const int32_t* stop) {
+  const Blocked& bk = transpose ? ktb_ : kb_;
+  if (!serial && bk.nb() > 1) {
+    const int nodes = launch_blocked_passes(s, bk, x, S, 0, stop);
+    r.rinit = bk.partial.as<double>();
+    return nodes + spmv(s, bk.blk.back(), x, r, false, S, 0, stop);
+  }
+  return spmv(s, transpose ? KTm(serial) : Km(serial), x, r, serial, S, 0, stop);
 }
 
 static VecRef vref(const double* p) { return VecRef{p, nullptr, 0, 0, 0}; }
@@ -800,8 +815,7 @@ void Problem::prof_collect() {
     AAPDHG_CUDA(cudaEventSynchronize(p.b));
     AAPDHG_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
     KernelStat& st = stats_[p.name];
-    st.ms += ms;
-    st.launches += 1;
+    st.each.push_back(ms);
     event_pool_.push_back(p.a);
     event_pool_.push_back(p.b);
   }
@@ -970,8 +984,13 @@ int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
     r.out_pool = su.B.kxpool;
     r.out_role = KX_CAND;
     r.out_stride = m_;
-    const CsrDev& A = Km(su.serial);
     const VecRef xr{nullptr, su.B.upool, U_CAND, N_, 0};
+    const bool blk = !su.serial && kb_.nb() > 1;  // L2-blocked K: passes, then the last block
+    if (blk) {
+      nodes += launch_blocked_passes(s, kb_, xr, su.S, 1);
+      r.rinit = kb_.partial.as<double>();
+    }
+    const CsrDev& A = blk ? kb_.blk.back() : Km(su.serial);
     unsigned int* ticket = reinterpret_cast<unsigned int*>(ticket_.p);
     if (su.serial)
       LAUNCH("k_spmv", (k_spmv_commit<true><<<A.grid(), kThreads, 0, s>>>(A, xr, r, su.P, su.S, ticket)));
@@ -1077,8 +1096,8 @@ void Problem::run_power(const double* x0, int max_iters, double rel_tol, bool se
   PowerState hs{};
   for (;;) {
     for (int r = 0; r < kPowerBatch; ++r) {
-      spmv(stream_, Km(serial), vref(x), rout(mx), serial, nullptr, 0, &ps->done);
-      spmv(stream_, KTm(serial), vref(mx), rout(mtmx), serial, nullptr, 0, &ps->done);
+      spmv_any(stream_, false, vref(x), rout(mx), serial, nullptr, &ps->done);
+      spmv_any(stream_, true, vref(mx), rout(mtmx), serial, nullptr, &ps->done);
       if (!serial) k_sumsq_partials<<<nb, kThreads, 0, stream_>>>(mtmx, nullptr, n_, part, &ps->done);
       k_power_ctrl<<<1, kCtrlThreads, 0, stream_>>>(mtmx, n_, part, nb, serial, ps);
       k_scale<<<grid_for(n_), kThreads, 0, stream_>>>(x, mtmx, n_, ps, nullptr);
@@ -1349,8 +1368,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   h2d(S, &S0, sizeof S0, stream_);
   k_project_start<<<grid_for(N_, kThreads, 1 << 30), kThreads, 0, stream_>>>(
       upool_.as<double>(), l_.as<double>(), u_.as<double>(), n_, N_, m1_, S);
-  if (m_) spmv(stream_, Km(serial), vref(upool_.as<double>()), rout(kxpool_.as<double>()), serial, nullptr, 0,
-               nullptr);
+  if (m_) spmv_any(stream_, false, vref(upool_.as<double>()), rout(kxpool_.as<double>()), serial,
+                   nullptr, nullptr);
   AAPDHG_CUDA(cudaGetLastError());
 
   ph("solve: start iterate");
@@ -1433,8 +1452,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
     if (lam_out && n_ > 0) {
       T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
       if (m_ > 0) {
-        spmv(stream_, KTm(false), vref(ufin + n_), rout(T_.as<double>()), false, nullptr, 0,
-             nullptr);
+        spmv_any(stream_, true, vref(ufin + n_), rout(T_.as<double>()), false, nullptr, nullptr);
       } else {
         AAPDHG_CUDA(cudaMemsetAsync(T_.p, 0, sizeof(double) * n_, stream_));
       }
@@ -2091,6 +2109,23 @@ extern "C" int aapdhg_cuda_plain_stamps_cta(double* out) {
   static unsigned long long z[1024 * 4] = {};
   cudaMemcpyToSymbol(aapdhg_b200::g_plain_cta, z, sizeof z);
   return 0;
+}
+#endif
+
+#ifdef AAPDHG_TIMELINE
+// experiment build only: the (kernel id, globaltimer ns) entry stamps since
+// the last read; returns their count
+extern "C" int aapdhg_cuda_timeline(double* out, int max) {
+  unsigned n = 0;
+  if (cudaMemcpyFromSymbol(&n, aapdhg_b200::g_tl_n, sizeof n) != cudaSuccess) return -1;
+  n = n > 8192 ? 8192 : n;
+  static unsigned long long v[2 * 8192];
+  cudaMemcpyFromSymbol(v, aapdhg_b200::g_tl, sizeof(unsigned long long) * 2 * n);
+  const int k = int(n) < max ? int(n) : max;
+  for (int i = 0; i < 2 * k; ++i) out[i] = double(v[i]);
+  unsigned z = 0;
+  cudaMemcpyToSymbol(aapdhg_b200::g_tl_n, &z, sizeof z);
+  return k;
 }
 #endif
 

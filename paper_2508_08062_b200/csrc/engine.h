@@ -28,6 +28,7 @@ struct DevBuf {
 struct KernelStat {
   double ms = 0.0;
   uint64_t launches = 0;
+  std::vector<float> each;  // per-launch ms (predicated-off launches filtered at read)
 };
 
 struct SolveSetup;
@@ -272,7 +273,9 @@ class Problem {
   Blocked kb_, ktb_;  // K (gathers xhat, n) and K' (gathers y, m)
   void build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& out);
   int launch_blocked_passes(cudaStream_t s, const Blocked& bk, const VecRef& x,
-                            const DevState* S);
+                            const DevState* S, int pred_aa = 0, const int32_t* stop = nullptr);
+  int spmv_any(cudaStream_t s, bool transpose, const VecRef& x, RowsumArgs r, bool serial,
+               const DevState* S, const int32_t* stop);
   std::atomic<size_t> sell_bytes_{0};
   bool building_blocks_ = false;  // device_sell: an L2 column block (never interleaved)
   DevBuf c_, q_, l_, u_;

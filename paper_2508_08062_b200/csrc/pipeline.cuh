@@ -450,6 +450,7 @@ __device__ __forceinline__ void p2p_wait(const DevParams* P, const DevState* S, 
 template <bool SERIAL>
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     k_spmv(CsrDev A, VecRef xr, RowsumArgs o, const DevState* S) {
+  TL_MARK(14);
   if (skip_launch(S, o.pred_aa_ok, o.stop)) return;
   const double* x = xr.get(S);
   double* out = o.out_pool ? o.out_pool + (int64_t)S->kx_idx[o.out_role] * o.out_stride : o.out;
@@ -457,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     double s;
     const int row = row_sum<SERIAL, kUnroll, false, false>(A, x, s, NoPre{}, -1, rep);
     if (row == -2) break;
-    if (row >= 0) out[row] = s;
+    if (row >= 0) out[row] = o.rinit ? __dadd_rn(o.rinit[row], s) : s;
   }
 }
 
@@ -797,8 +798,11 @@ __device__ __forceinline__ void fused_control_tail(const IterBufs& B, DevState* 
 // One column pass of an L2-blocked SpMV: part[row] (+)= the row's products
 // with the columns of this block (passes in block order: deterministic).
 __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
-    k_spmv_pass(CsrDev A, VecRef xr, double* __restrict__ part, int first, const DevState* S) {
-  if (S && S->done) return;
+    k_spmv_pass(CsrDev A, VecRef xr, double* __restrict__ part, int first, const DevState* S,
+                int pred_aa, const int32_t* stop) {
+  TL_MARK(20);
+  if (skip_launch(S, 0, stop)) return;
+  if (S && pred_aa == 1 && (!S->aa_attempt || !S->aa_ok)) return;  // (AA recache passes)
   const double* x = xr.get(S);
   for (int rep = 0;; ++rep) {
     double s;
@@ -910,6 +914,7 @@ template <bool SERIAL, bool PUSH, int VAR = 0, bool MULTI = false>
 #endif
 __global__ void __launch_bounds__(kThreads, AAPDHG_K12_MINBLOCKS)
     k_dual_side(CsrDev KT, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+  TL_MARK(16);
   launch_dependents();  // k_primal_side may start its prologue (PDL)
   if (S->done) return;
 #ifdef AAPDHG_TAIL_STAMPS
@@ -1013,6 +1018,7 @@ __device__ __forceinline__ void primal_side_rows(const CsrDev& K, const IterBufs
 template <bool SERIAL, bool PUSH, int VAR = 0, bool MULTI = false>
 __global__ void __launch_bounds__(kThreads, AAPDHG_K12_MINBLOCKS)
     k_primal_side(CsrDev K, IterBufs B, const DevParams* __restrict__ P, DevState* S) {
+  TL_MARK(17);
   if (S->done) return;
   if constexpr (VAR == 2) {
     double s;
@@ -1350,11 +1356,15 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   __shared__ double red[P1_COUNT * 32];
   __shared__ int s_stop;
   const int G = int(gridDim.x), W = G - 1, bid = int(blockIdx.x);
+  TL_MARK(1);
   state_load(&st, S);
   if (st.done || st.batch_left <= 0) return;  // (eager launches past the batch)
   if (bid == W) {
     __shared__ __align__(16) DevParams pr;
     plain_loop_control<SERIAL>(B, P, S, gb, np1, np2, st, pr, red);
+#ifdef AAPDHG_TIMELINE
+    if (threadIdx.x == 0) tl_mark(2);
+#endif
     return;
   }
   unsigned long long h0 = 0;  // stop flags raised before this launch

@@ -23,12 +23,17 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
             t0 = time.perf_counter()
             s.solve(cfg)
             t[it] = time.perf_counter() - t0
-        tag = " ".join(f"{k}={os.environ.get(k, '-')}" for k in ("AAPDHG_L2_BLOCK_KB",
-                                                                  "AAPDHG_L2_PERSIST"))
+        tag = " ".join(f"{k}={os.environ.get(k, '-')}" for k in (
+            "AAPDHG_L2_BLOCK_KB", "AAPDHG_L2_BLOCK_MIN_KB", "AAPDHG_L2_PERSIST"))
         print(f"{tag}: create {create:.2f} s, marginal PDHG "
               f"{1e3 * (t[40] - t[10]) / 30:.2f} ms/iteration", flush=True)
     sys.exit(0)
+# KB[,PERSIST[,MIN_KB]]: MIN_KB = the vector size blocking starts above (the
+# default 64 MB blocks both y (156,250 KB) and x (312,500 KB); 200000 leaves
+# K'y unblocked)
 combos = [a.split(",") for a in (sys.argv[1:] or ["65536,0", "65536,1", "81920,0", "81920,1"])]
-for kb, persist in combos:
+for c in combos:
+    kb, persist, mn = (c + ["0", "65536"])[:3] if len(c) == 1 else (c + ["65536"])[:3]
     subprocess.run([sys.executable, __file__, "child"],
-                   env=dict(os.environ, AAPDHG_L2_BLOCK_KB=kb, AAPDHG_L2_PERSIST=persist))
+                   env=dict(os.environ, AAPDHG_L2_BLOCK_KB=kb, AAPDHG_L2_PERSIST=persist,
+                            AAPDHG_L2_BLOCK_MIN_KB=mn))

@@ -117,13 +117,23 @@ def test_bench_iteration_bytes_and_workload_selection():
     N = n + m
     aa = 8 * N * 13 + 8 * N * 23 + 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
     assert bench.iteration_bytes(p, 20, 3) == 20 * plain + 3 * aa
-    args = argparse.Namespace(workload="auto", loopback=0)
+    # configs[4] at every N (BENCH and the scaling curve share the LP)
+    args = argparse.Namespace(workload="config4", loopback=0)
     bench.select_workload(args, 1)
-    assert bench.CONFIG_ID == 1 and "configs[1]" in bench.METRIC
+    assert bench.CONFIG_ID == 4 and "configs[4]" in bench.METRIC
     bench.select_workload(args, 8)
     assert bench.CONFIG_ID == 4 and "configs[4]" in bench.METRIC
-    bench.select_workload(argparse.Namespace(workload="config1", loopback=0), 8)
-    assert bench.CONFIG_ID == 1
+    bench.select_workload(argparse.Namespace(workload="config1", loopback=0), 1)
+    assert bench.CONFIG_ID == 1 and "configs[1]" in bench.METRIC
+    # the column-pass bytes of configs[4]'s layout (K': 3 blocks of y, K: 5 of x)
+    class _K:
+        nrows, nnz = 20_000_000, 400_000_000
+    class _P:
+        k = _K()
+        def n(self):
+            return 40_000_000
+    pb = bench.kernel_bytes(_P(), "k_spmv_pass")
+    assert 1.0e9 < pb < 2.5e9
 
 
 def test_stable_argsort_paths_agree():
