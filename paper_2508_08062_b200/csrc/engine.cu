@@ -99,6 +99,8 @@ struct SolveSetup {
   CsrDev pk1, pk2;       // the K' / K layouts on <= pgrid - 1 worker CTAs
   GridBar* gb = nullptr;
   int np1 = 0, np2 = 0;  // partial rows: CTAs, or slices (calibrated partition)
+  bool split = false;    // L2-blocked TREE: all blocks as passes, then k_dual_epi / k_primal_epi
+  int epi = 0;           // their grid (grid-stride rows)
   unsigned long long* bal = nullptr;  // per-CTA phase times (calibrating)
 };
 
@@ -347,9 +349,10 @@ void Problem::build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& o
 }
 
 int Problem::launch_blocked_passes(cudaStream_t s, const Blocked& bk, const VecRef& x,
-                                   const DevState* S, int pred_aa, const int32_t* stop) {
+                                   const DevState* S, int pred_aa, const int32_t* stop,
+                                   bool all) {
   int nodes = 0;
-  for (int b = 0; b + 1 < bk.nb(); ++b) {
+  for (int b = 0; b + (all ? 0 : 1) < bk.nb(); ++b) {
     prof_begin(s, "k_spmv_pass");
     k_spmv_pass<<<bk.blk[b].grid(), kThreads, 0, s>>>(bk.blk[b], x, bk.partial.as<double>(),
                                                      b == 0 ? 1 : 0, S, pred_aa, stop);
@@ -699,6 +702,8 @@ void Problem::ensure_iter_buffers(int method, int cap) {
   kxpool_.reserve(sizeof(double) * 3 * std::max<int64_t>(m_, 1));
   T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
   T2_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
+  nblk1 = std::max(nblk1, num_sms_ * kSpmvBlocksPerSM);  // (k_dual_epi / k_primal_epi)
+  nblk2 = std::max(nblk2, num_sms_ * kSpmvBlocksPerSM);
   part1_.reserve(sizeof(double) * P1_COUNT * std::max(nblk1, 1));
   part2_.reserve(sizeof(double) * P2_COUNT * std::max(nblk2, 1));
 
@@ -892,6 +897,25 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
                                                           su.S, su.gb, su.pk1.grid(),
                                                           su.pk2.grid(), su.np1, su.np2,
                                                           su.bal)));
+    return nodes;
+  }
+  if (su.split) {  // L2-blocked TREE: every block a pass, then the row-order epilogues
+    if (n_ > 0) {
+      nodes += launch_blocked_passes(s, ktb_, VecRef{nullptr, su.B.upool, U_CUR, N_, n_}, su.S, 0,
+                                     nullptr, true);
+      if (push) LAUNCH("k_dual_epi", (k_dual_epi<true><<<su.epi, kThreads, 0, s>>>(ktb_.partial.as<double>(), su.B, su.P, su.S)));
+      else LAUNCH("k_dual_epi", (k_dual_epi<false><<<su.epi, kThreads, 0, s>>>(ktb_.partial.as<double>(), su.B, su.P, su.S)));
+    }
+    if (m_ > 0) {
+      nodes += launch_blocked_passes(s, kb_, VecRef{nullptr, su.B.upool, U_HAT, N_, 0}, su.S, 0,
+                                     nullptr, true);
+      if (push) LAUNCH("k_primal_epi", (k_primal_epi<true><<<su.epi, kThreads, 0, s>>>(kb_.partial.as<double>(), su.B, su.P, su.S)));
+      else LAUNCH("k_primal_epi", (k_primal_epi<false><<<su.epi, kThreads, 0, s>>>(kb_.partial.as<double>(), su.B, su.P, su.S)));
+    }
+    if (su.B.fused_ctrl != 1)
+      LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), n_ > 0 ? su.epi : 0,
+                                                              part2_.as<double>(), su.epi, su.P, su.S));
+    AAPDHG_CUDA(cudaGetLastError());
     return nodes;
   }
   // TREE with L2 column blocking: the earlier column passes first, the last
@@ -1268,6 +1292,15 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.nblk2 = K2m.grid();
   su.ndot_blk = ndot;
   su.items_max = num_items_host(std::max(cap, 1), method);
+  // L2-blocked TREE (configs[4]): the epilogues in row order after all the
+  // column passes (AAPDHG_SPLIT_EPI=0: the last block fused with them)
+  if (blk1 && blk2 && n_ > 0 && m_ > 0 && env_int("AAPDHG_SPLIT_EPI", 1) != 0) {
+    su.split = true;
+    su.epi = num_sms_ * kSpmvBlocksPerSM;
+    su.B.nu1 = su.epi;
+    su.nblk1 = su.nblk2 = su.epi;
+    P.nblk1 = P.nblk2 = su.epi;
+  }
 
   // executable graph, cached per launch layout (use_graph above)
   // plain iterations in one persistent grid (AAPDHG_PERSIST=0: per-kernel graph)
@@ -1338,8 +1371,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   }
   if (use_graph) {
     char key[256];
-    std::snprintf(key, sizeof key, "%d/%d/%d/%d/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p", method,
-                  int(serial), cap, int(su.persist), upool_.p, du_.p, partdot_.p, dparams_.p,
+    std::snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p", method,
+                  int(serial), cap, int(su.persist), int(su.split), upool_.p, du_.p, partdot_.p, dparams_.p,
                   rec_.p, stream_, gridbar_.p, (const void*)su.pk1.sl_start, (void*)su.bal,
                   su.B.part1, su.B.part2);
     if (graph_key_ != key || !graph_exec_) {

@@ -273,7 +273,8 @@ class Problem {
   Blocked kb_, ktb_;  // K (gathers xhat, n) and K' (gathers y, m)
   void build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& out);
   int launch_blocked_passes(cudaStream_t s, const Blocked& bk, const VecRef& x,
-                            const DevState* S, int pred_aa = 0, const int32_t* stop = nullptr);
+                            const DevState* S, int pred_aa = 0, const int32_t* stop = nullptr,
+                            bool all = false);
   int spmv_any(cudaStream_t s, bool transpose, const VecRef& x, RowsumArgs r, bool serial,
                const DevState* S, const int32_t* stop);
   std::atomic<size_t> sell_bytes_{0};

@@ -1046,6 +1046,64 @@ __global__ void __launch_bounds__(kThreads, AAPDHG_K12_MINBLOCKS)
 }
 
 // ---------------------------------------------------------------------------
+// L2-blocked TREE layouts (configs[4]): every column block of K' and of K runs
+// as a plain pass (k_spmv_pass; the last one leaves the finished sums, added
+// in block order as the fused kernels add them), then the epilogues in row
+// order over those sums: the vector operands stream coalesced instead of in
+// the slices' length-sorted order, and no block's gathers share L2 with them.
+// Grid-stride rows; each thread's terms in row order, then the fixed CTA tree.
+// ---------------------------------------------------------------------------
+template <bool PUSH>
+__global__ void __launch_bounds__(kThreads)
+    k_dual_epi(const double* __restrict__ T, IterBufs B, const DevParams* __restrict__ P,
+               DevState* S) {
+  TL_MARK(26);
+  if (S->done) return;
+  __shared__ double red[P1_COUNT * kWarps];
+  const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * P->N;
+  double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
+  bool first = true;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P->n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double term[P1_COUNT];
+    dual_epilogue<false, PUSH>(int(j), T[j], x, B, P, S, term);
+#pragma unroll
+    for (int q = 0; q < P1_COUNT; ++q) acc[q] = first ? term[q] : __dadd_rn(acc[q], term[q]);
+    first = false;
+  }
+  block_sum<P1_COUNT>(acc, red);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < P1_COUNT; ++q) B.part1[q * gridDim.x + blockIdx.x] = acc[q];
+}
+
+template <bool PUSH>
+__global__ void __launch_bounds__(kThreads)
+    k_primal_epi(const double* __restrict__ Kx, IterBufs B, const DevParams* __restrict__ P,
+                 DevState* S) {
+  TL_MARK(27);
+  if (S->done) return;
+  __shared__ double red[P2_COUNT * kWarps];
+  double acc[P2_COUNT] = {0.0, 0.0, 0.0};
+  bool first = true;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P->mrows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double term[P2_COUNT];
+    primal_epilogue<PUSH>(int(i), Kx[i], B, P, S, term);
+#pragma unroll
+    for (int q = 0; q < P2_COUNT; ++q) acc[q] = first ? term[q] : __dadd_rn(acc[q], term[q]);
+    first = false;
+  }
+  __shared__ __align__(16) TailSmem ts;
+  if (B.fused_ctrl) tail_prefetch(ts, P, S);
+  block_sum<P2_COUNT>(acc, red);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < P2_COUNT; ++q) B.part2[q * gridDim.x + blockIdx.x] = acc[q];
+  if (B.fused_ctrl) fused_control_tail(B, S, ts);
+}
+
+// ---------------------------------------------------------------------------
 // the persistent plain-step loop (TREE, fused control, graph replay)
 // ---------------------------------------------------------------------------
 //

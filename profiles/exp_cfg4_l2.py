@@ -24,7 +24,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
             s.solve(cfg)
             t[it] = time.perf_counter() - t0
         tag = " ".join(f"{k}={os.environ.get(k, '-')}" for k in (
-            "AAPDHG_L2_BLOCK_KB", "AAPDHG_L2_BLOCK_MIN_KB", "AAPDHG_L2_PERSIST"))
+            "AAPDHG_L2_BLOCK_KB", "AAPDHG_L2_BLOCK_MIN_KB", "AAPDHG_L2_PERSIST",
+            "AAPDHG_SPLIT_EPI"))
         print(f"{tag}: create {create:.2f} s, marginal PDHG "
               f"{1e3 * (t[40] - t[10]) / 30:.2f} ms/iteration", flush=True)
     sys.exit(0)

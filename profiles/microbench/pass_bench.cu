@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(256, 6) pass(Sell A, const double* __restrict_
   uint64_t plast = 0, pfirst = 0;
   if (V & 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(plast));
   if (V & 16) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pfirst));
+  uint64_t sfirst = 0;
+  if (V & 64) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(sfirst));
   const int L = __ldg(A.sl_len + sl);
   const int64_t sbase = __ldg(A.sl_ptr + sl);
   int row, cnt;
@@ -62,8 +64,21 @@ __global__ void __launch_bounds__(256, 6) pass(Sell A, const double* __restrict_
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool on = t0 + u < cnt;
-      c[u] = on ? __ldcs(cp + 32 * (t0 + u)) : 0;
-      v[u] = on ? __ldcs(vp + 32 * (t0 + u)) : 0.0;
+      if (V & 64) {
+        int ci = 0;
+        double vi = 0.0;
+        if (on) {
+          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+                       : "=r"(ci) : "l"(cp + 32 * (t0 + u)), "l"(sfirst));
+          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                       : "=d"(vi) : "l"(vp + 32 * (t0 + u)), "l"(sfirst));
+        }
+        c[u] = ci;
+        v[u] = vi;
+      } else {
+        c[u] = on ? __ldcs(cp + 32 * (t0 + u)) : 0;
+        v[u] = on ? __ldcs(vp + 32 * (t0 + u)) : 0.0;
+      }
     }
     double g[U];
 #pragma unroll
@@ -369,8 +384,8 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
-  const int variants[] = {1, 3, 7, 37, 39};
-  for (int mb : {64, 80, 96}) {
+  const int variants[] = {1, 65, 81, 67, 83};
+  for (int mb : {48, 64, 80}) {
     const int64_t nx = (int64_t(mb) << 20) / 8;
     for (int64_t e = 0; e < tot; ++e) sci[e] = int(rnd() % nx);
     CK(cudaMemcpy(d_sci, sci.data(), tot * 4, cudaMemcpyHostToDevice));
@@ -410,6 +425,10 @@ int main(int argc, char** argv) {
           case 3: launch<3>(A, x, part, r == 0, s0); break;
           case 5: launch<1>(A, x, part, r == 0, s0); break;
           case 7: launch<3>(A, x, part, r == 0, s0); break;
+          case 65: launch<65>(A, x, part, r == 0, s0); break;
+          case 81: launch<81>(A, x, part, r == 0, s0); break;
+          case 67: launch<67>(A, x, part, r == 0, s0); break;
+          case 83: launch<83>(A, x, part, r == 0, s0); break;
           case 37: launch<1>(A, x, part, r == 0, s0); break;
           case 39: launch<3>(A, x, part, r == 0, s0); break;
           case 9: launch<9>(A, x, part, r == 0, s0); break;
