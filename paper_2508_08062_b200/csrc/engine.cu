@@ -1248,9 +1248,11 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   P.pow_len = method == AAPDHG_METHOD_PDHG ? 0 : pow_len_;
   P.rec = rec_.as<aapdhg_record>();
   P.rec_cap = rec_cap_;
-  // predicted stops in k_plain_loop (stop_likely): measured a net loss on
-  // configs[1] (20,000 iterations: 17.3k vs 18.9k it/s; 20: within noise),
-  // so off unless AAPDHG_STOP_PREDICT=1
+  // predicted stops in k_plain_loop (stop_likely, exact from the x part of
+  // ||g_k||^2): measured a net loss on configs[1] AA-PDHG (52.0 -> 61.5 us
+  // per iteration: ||g_x|| alone rarely rules an attempt out, so the workers
+  // wait for most decisions; profiles/r02b/stop_predict.txt), so off unless
+  // AAPDHG_STOP_PREDICT=1 (round 1's extrapolated prediction lost too)
   P.no_stop_predict = env_int("AAPDHG_STOP_PREDICT", 0) == 0 ? 1 : 0;
   // one-phase-ahead L2 prefetch of the slice streams (prefetch_slice_streams):
   // measured a loss on configs[1] (17.2k vs 18.6k it/s), opt-in experiment

@@ -1139,10 +1139,11 @@ struct GridBar {
   unsigned long long arrive1;  // barrier 1: arrivals (low 40 bits) + stops (high bits)
   unsigned long long arrive2;  // barrier 2: arrivals
   // predicted stops: the control publishes, after its barrier-1 arrival,
-  // decided = k + 1 for iteration k, and before it the last two ||g|| and
-  // the safeguard threshold D ||g0|| (i+1)^-(1+eps) of the current i
+  // decided = k + 1 for iteration k; before its barrier-2 arrival, maystop =
+  // (k << 1) | flag: flag 0 when the x part of ||g_k||^2 alone already rules
+  // out an AA attempt and the residual tolerance (stop_likely)
   unsigned long long decided;
-  unsigned long long pad0;
+  unsigned long long maystop;
   double g_last, g_prev, thr, pad1;
 };
 constexpr unsigned long long kBarCount = (1ull << 40) - 1;
@@ -1184,22 +1185,34 @@ __device__ __forceinline__ unsigned long long bar_arrive_wait(unsigned long long
 // A worker's guess, after barrier 2 of iteration k = st.k, that the control
 // will stop the launch after k (st: the state before k's commit; wp:
 // iterations already decided in this launch). Exact for the batch end and
-// max_iters; for the safeguard and the tolerance, ||g_k|| is extrapolated
-// geometrically from the last two published norms (between AA steps the
-// residual decays smoothly: configs[1] trajectories predict every AA step)
-// with a 0.5% margin. A wrong guess costs the wait for the decision only.
+// max_iters; for the safeguard and the residual tolerance the control CTA
+// publishes before barrier 2 whether the x part of ||g_k||^2 (known since
+// barrier 1) leaves them possible: ||g_k|| >= ||g_x|| (a sum of non-negative
+// terms), so flag 0 is exact. Only then do the workers wait for the decision;
+// the rare KKT / wall-clock stops stay speculative (a dropped K1).
 __device__ __forceinline__ bool stop_likely(const DevParams* P, const GridBar* gb,
                                             const DevState& st, int wp) {
   if (P->no_stop_predict) return false;
   if (st.batch_left - (wp + 1) <= 0) return true;
   if (st.k > 0 && st.i + st.j >= P->max_iters) return true;
-  if (wp == 0 || st.k < 2) return false;  // first iteration after a launch: no history
-  const double g1 = __ldcg(&gb->g_last), g2 = __ldcg(&gb->g_prev);
-  if (!(g1 > 0.0) || !(g2 > 0.0)) return false;
-  const double gp = g1 < g2 ? g1 * (g1 / g2) : g1;
-  if (gp < 1.005 * P->toll) return true;
-  const double thr = __ldcg(&gb->thr);
-  return thr > 0.0 && gp <= 1.005 * thr;
+  if (st.k < 2) return true;  // priming / fixed-point start
+  const unsigned long long ms = ld_relaxed(&gb->maystop);
+  return (ms >> 1) != st.k || (ms & 1ull);
+}
+
+// The control CTA's maystop flag of iteration k (stop_likely): can the
+// decision be an AA attempt or the residual tolerance, given the x part gx2
+// of ||g_k||^2? Thread 0.
+__device__ __forceinline__ void publish_maystop(const DevParams& pr, const DevState& sm,
+                                                GridBar* gb, double gx2) {
+  const double gx = sqrt(gx2);
+  bool may = gx < pr.toll;
+  if (pr.method != AAPDHG_METHOD_PDHG) {
+    const double pw = sm.i < pr.pow_len ? pr.pow_tab[sm.i]
+                                        : pow((double)sm.i + 1.0, -(1.0 + pr.safeguard_eps));
+    may = may || gx <= __dmul_rn(__dmul_rn(pr.safeguard_d, sm.g0n), pw);
+  }
+  gb->maystop = (sm.k << 1) | (may ? 1ull : 0ull);
 }
 
 // The control CTA of k_plain_loop: state and parameters in shared memory for
@@ -1345,8 +1358,13 @@ __device__ __noinline__ void plain_loop_control(const IterBufs& B, const DevPara
 #pragma unroll
         for (int q = 0; q < P1_COUNT; ++q) t1s[q] = t1[q];
     }
-    // barrier 2: K2(k) done (the workers start K1(k+1) on plain-step roles)
-    if (threadIdx.x == 0) bar_arrive_wait(&gb->arrive2, 1, G);
+    // barrier 2: K2(k) done (the workers start K1(k+1) on plain-step roles,
+    // or wait for the decision when maystop says it can stop the loop)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      publish_maystop(pr, sm, gb, SERIAL ? xres[0] : t1s[P1_GX2]);
+      bar_arrive_wait(&gb->arrive2, 1, G);
+    }
     __syncthreads();
     if constexpr (SERIAL) {
       serial_ychains_cta<kPlainSerChunk>(B, &pr, sm, xres[0], sterms, yres);
