@@ -56,7 +56,7 @@ out = {
         "dram_read_bytes": plain["dram__bytes_read.sum"],
         "dram_write_bytes": plain["dram__bytes_write.sum"], "iterations": 8,
         "duration_us": plain["gpu__time_duration.sum"] * 1e6,
-        "source": "profiles/profile_plain.py: 8 plain iterations plus the dropped speculative K1"},
+        "source": "profiles/profile_plain.py 24 3 (--launch-skip 360: the first launch of the solve after three calibration solves): 8 plain iterations plus the dropped speculative K1"},
     "config4_iteration": {
         "kernels": [{"kernel": r["Kernel Name"].split("(")[0], "grid": r["Grid Size"],
                      "duration_us": r["gpu__time_duration.sum"] * 1e6,

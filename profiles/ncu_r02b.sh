@@ -8,7 +8,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 ncu --set full --clock-control none --import-source on -k regex:"k_spmv_pass|k_dual_epi|k_primal_epi" -c 8 -o gpurun_out/ncu/cfg4_r02b python profiles/profile_cfg.py 4 1.0 2 > gpurun_out/ncu/cfg4.log 2>&1
 ncu -i gpurun_out/ncu/cfg4_r02b.ncu-rep --page raw --csv > gpurun_out/ncu/cfg4_r02b_raw.csv 2>&1
 # 3. k_plain_loop (configs[1]), one launch: 8 plain iterations + the dropped speculative K1
-ncu --set full --clock-control none --import-source on -k regex:k_plain_loop -c 1 -o gpurun_out/ncu/plain_r02b python profiles/profile_plain.py 24 > gpurun_out/ncu/plain.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_plain_loop --launch-skip ${PLAIN_SKIP:-360} -c 1 -o gpurun_out/ncu/plain_r02b python profiles/profile_plain.py 24 ${PLAIN_WARM:-3} > gpurun_out/ncu/plain.log 2>&1
 ncu -i gpurun_out/ncu/plain_r02b.ncu-rep --page raw --csv > gpurun_out/ncu/plain_r02b_raw.csv 2>&1
 ncu -i gpurun_out/ncu/plain_r02b.ncu-rep --page details --csv > gpurun_out/ncu/plain_r02b_details.csv 2>&1
 ls -la gpurun_out/ncu

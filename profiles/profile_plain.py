@@ -17,8 +17,12 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2508_08062_b200 import Method, Solver, SolverConfig, problems  # noqa: E402
 
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+warm = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # calibration solves of 64 iterations first
 p = problems.make_config(1)
 with Solver(p) as s:
+    for _ in range(warm):  # (each: 4 k_plain_loop launches, batches 8+16+32+64 -> ncu --launch-skip 4*warm)
+        s.solve(SolverConfig(method=Method.AA_PDHG, m=10, safeguard_d=1e-300, toll=1e-12,
+                             max_iters=64, tau=0.0775, sigma=0.0775, reduction="tree"))
     out = s.solve(SolverConfig(method=Method.AA_PDHG, m=10, safeguard_d=1e-300, toll=1e-12,
                                max_iters=iters, tau=0.0775, sigma=0.0775, reduction="tree"))
     import ctypes as C
