@@ -11,7 +11,9 @@
 #include <cub/device/device_select.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -53,6 +55,34 @@ __global__ void k_gather_len(const int32_t* rows, int64_t n, const int32_t* len,
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
     out[i] = len[rows[i]];
+}
+
+// Stable sort of each window of sigma (<= 256) consecutive entries of rows_in
+// by decreasing len[row], one CTA per window: entry t goes to rank = #longer
+// + #equal before it, the permutation CUB's stable descending radix sort gives.
+__global__ void __launch_bounds__(256) k_window_sort_desc(const int32_t* __restrict__ rows_in,
+                                                          const int32_t* __restrict__ len,
+                                                          int64_t n, int sigma,
+                                                          int32_t* __restrict__ rows_out) {
+  __shared__ int32_t sl[256];
+  const int64_t w0 = int64_t(blockIdx.x) * sigma;
+  const int cnt = int(n - w0 < sigma ? n - w0 : sigma);
+  const int t = threadIdx.x;
+  int mylen = 0, myrow = 0;
+  if (t < cnt) {
+    myrow = rows_in[w0 + t];
+    mylen = len[myrow];
+    sl[t] = mylen;
+  }
+  __syncthreads();
+  if (t < cnt) {
+    int rank = 0;
+    for (int j = 0; j < cnt; ++j) {
+      const int lj = sl[j];
+      rank += (lj > mylen) | ((lj == mylen) & (j < t));
+    }
+    rows_out[w0 + rank] = myrow;
+  }
 }
 
 __global__ void k_seg_offsets(int32_t* off, int nseg, int sigma, int n) {
@@ -256,6 +286,23 @@ void Problem::device_flags_vectors() {
 }
 
 // exclusive scan of n int32 counts into out[0..n] (out[n] = total); returns total
+// AAPDHG_TIMING=2: ingestion sub-phases on stderr (the host clock after a
+// stream synchronize, so each phase includes its device work)
+static void ingest_ph(cudaStream_t s, const char* what) {
+  static const bool on = [] {
+    const char* e = std::getenv("AAPDHG_TIMING");
+    return e && std::atoi(e) >= 2;
+  }();
+  if (!on) return;
+  using C = std::chrono::steady_clock;
+  static thread_local C::time_point t = C::now();
+  cudaStreamSynchronize(s);
+  const C::time_point now = C::now();
+  std::fprintf(stderr, "[aapdhg]   %-24s %10.1f us\n", what,
+               1e6 * std::chrono::duration<double>(now - t).count());
+  t = now;
+}
+
 static int64_t scan_counts(const int32_t* cnt, int n, int32_t* out, cudaStream_t s) {
   DevBuf t;
   size_t bytes = 0;
@@ -276,6 +323,7 @@ static int64_t scan_counts(const int32_t* cnt, int n, int32_t* out, cudaStream_t
 void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev& ser,
                          CsrDev& tree, cudaStream_t s) {
   if (!s) s = stream_;
+  ingest_ph(s, "(finish_csr start)");
   DevBuf blen, blong, bshort, bslen, bsel, bcount, tsel;
   int32_t* len = tmp<int32_t>(blen, nrows);
   char* is_long = tmp<char>(blong, nrows);
@@ -312,6 +360,7 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
   AAPDHG_CUDA(cudaStreamSynchronize(s));
   if (nrows == 0) hc[0] = hc[1] = 0;
   const int nshort = hc[0], nlong = hc[1];
+  ingest_ph(s, "classify rows");
 
   // long rows: longest first (stable)
   st.longs.reserve(sizeof(int32_t) * std::max(nlong, 1));
@@ -383,7 +432,12 @@ void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* l
   const int sigma = env_int("AAPDHG_SIGMA", sigma_global ? std::max(nshort, 1) : kWarps * R);
   DevBuf brows, bk, bk2, boff, tt;
   int32_t* rows = tmp<int32_t>(brows, nshort);
-  if (sigma > 1 && nshort > 0) {  // stable sort by decreasing length inside each window
+  if (sigma > 1 && sigma <= 256 && nshort > 0) {  // windows of one CTA: k_window_sort_desc
+    const int nseg = int((int64_t(nshort) + sigma - 1) / sigma);
+    k_window_sort_desc<<<nseg, 256, 0, s>>>(shorts_in, len, nshort, sigma, rows);
+    AAPDHG_CUDA(cudaGetLastError());
+    ingest_ph(s, "sell: length sort (windows)");
+  } else if (sigma > 1 && nshort > 0) {  // stable sort by decreasing length inside each window
     const int nseg = int((int64_t(nshort) + sigma - 1) / sigma);
     int32_t* klen = tmp<int32_t>(bk, nshort);
     int32_t* klen2 = tmp<int32_t>(bk2, nshort);
@@ -396,6 +450,7 @@ void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* l
     AAPDHG_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(
         tmp<char>(tt, bytes), bytes, klen, klen2, shorts_in, rows, nshort, nseg, off, off + 1, 0,
         32, s));
+    ingest_ph(s, "sell: length sort");
   } else if (nshort > 0) {
     AAPDHG_CUDA(cudaMemcpyAsync(rows, shorts_in, sizeof(int32_t) * nshort,
                                 cudaMemcpyDeviceToDevice, s));
@@ -434,6 +489,7 @@ void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* l
         ss.sl_ptr.as<int64_t>(), nslices, sf, ss.sci.as<int32_t>(), ss.sv.as<double>());
   AAPDHG_CUDA(cudaGetLastError());
   AAPDHG_CUDA(cudaStreamSynchronize(s));  // scratch buffers go out of scope
+  ingest_ph(s, "sell: meta + fill");
   sell_bytes_ += (sizeof(int32_t) + sizeof(double)) * size_t(total);
   out.nslices = nslices;
   out.sl_ptr = ss.sl_ptr.as<int64_t>();
@@ -518,6 +574,7 @@ void Problem::device_block(const CsrStore& src, int nrows, int64_t c0, int64_t c
                                                   dst.v.as<double>());
   AAPDHG_CUDA(cudaGetLastError());
   AAPDHG_CUDA(cudaStreamSynchronize(s));
+  ingest_ph(s, "block: count + fill");
   *nnz_out = nnz;
 }
 
