@@ -533,15 +533,29 @@ void Problem::init_device(int device) {
 
 // c, q, l, u on the device plus the scratch of power iteration / per-op /
 // KKT evaluation.
-void Problem::init_vectors(const double* c, const double* q, const double* l, const double* u) {
+// c, q, l, u to the device. Page-locked sources go on side_ (copy engine)
+// while the device builds the layouts on stream_ (the caller joins with
+// join_vectors); pageable ones are staged on stream_ (host memcpy).
+void Problem::upload_vectors(const double* c, const double* q, const double* l, const double* u) {
   c_.reserve(sizeof(double) * n_);
   q_.reserve(sizeof(double) * m_);
   l_.reserve(sizeof(double) * n_);
   u_.reserve(sizeof(double) * n_);
-  h2d(c_.p, c, sizeof(double) * n_, stream_);
-  h2d(q_.p, q, sizeof(double) * m_, stream_);
-  h2d(l_.p, l, sizeof(double) * n_, stream_);
-  h2d(u_.p, u, sizeof(double) * n_, stream_);
+  vec_async_ = host_is_pinned(c) && host_is_pinned(q) && host_is_pinned(l) && host_is_pinned(u);
+  cudaStream_t s = vec_async_ ? side_ : stream_;
+  if (vec_async_) {  // (the reservations above may have used stream_-ordered memsets)
+    AAPDHG_CUDA(cudaEventRecord(ev_fork_, stream_));
+    AAPDHG_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+  }
+  h2d(c_.p, c, sizeof(double) * n_, s);
+  h2d(q_.p, q, sizeof(double) * m_, s);
+  h2d(l_.p, l, sizeof(double) * n_, s);
+  h2d(u_.p, u, sizeof(double) * n_, s);
+  if (vec_async_) AAPDHG_CUDA(cudaEventRecord(ev_join_, side_));
+}
+
+void Problem::init_vectors() {
+  if (vec_async_) AAPDHG_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
   pw_x_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
   pw_mx_.reserve(sizeof(double) * std::max<int64_t>(m_, 1));
   pw_mtmx_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
@@ -587,6 +601,8 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   // measured: no gain inside the bench's process, more variance)
   upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
   ph("upload K + SELL");
+  upload_vectors(v->c, v->q, v->l, v->u);  // (page-locked: beside the layout builds)
+  ph("vectors (issued)");
   device_transpose(k_store_, m_, n_, nnz_, t_store_);
   ph("transpose");
   finish_csr(n_, m_, nnz_, t_store_, KTs_, KTt_);
@@ -595,7 +611,7 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   build_blocks(t_store_, n_, m_, ktb_);
   ph("L2 blocks");
 
-  init_vectors(v->c, v->q, v->l, v->u);
+  init_vectors();
   device_flags_vectors();
   ph("vectors");
   // ||q|| and ||c|| (constants of kkt_metrics): TREE order on the device;
@@ -1765,7 +1781,8 @@ Problem::Problem(const ShardSpec& sp, int device) : device_(device) {
   // (relabelled indices stay ascending within a row: column blocks are in order)
   build_blocks(k_store_, m_, int(sp.world * sp.maxc), kb_);
   build_blocks(t_store_, n_, int(sp.world * sp.maxr), ktb_);
-  init_vectors(sp.c.data(), sp.q.data(), sp.l.data(), sp.u.data());
+  upload_vectors(sp.c.data(), sp.q.data(), sp.l.data(), sp.u.data());
+  init_vectors();
   nrm_q_[0] = nrm_q_[1] = sp.nrm_q;
   nrm_c_[0] = nrm_c_[1] = sp.nrm_c;
   serial_norms_ = true;

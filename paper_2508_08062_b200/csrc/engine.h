@@ -214,7 +214,9 @@ class Problem {
   IterBufs iter_bufs();
 
   void init_device(int device);
-  void init_vectors(const double* c, const double* q, const double* l, const double* u);
+  void upload_vectors(const double* c, const double* q, const double* l, const double* u);
+  void init_vectors();  // (after upload_vectors: joins its copies, the other buffers)
+  bool vec_async_ = false;
   void kkt_eval(int slot, bool serial, double* kkt_dev_out, double* lam_dev);
   int launch_core(cudaStream_t s, const SolveSetup& su);
   int launch_aa(cudaStream_t s, const SolveSetup& su);
