@@ -598,13 +598,42 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
 
   // K uploaded and checked on the device, then K's layouts, the transpose
   // K' and its layouts (a second host thread building K' on side_ was
-  // measured: no gain inside the bench's process, more variance)
-  upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
-  ph("upload K + SELL");
-  upload_vectors(v->c, v->q, v->l, v->u);  // (page-locked: beside the layout builds)
-  ph("vectors (issued)");
-  device_transpose(k_store_, m_, n_, nnz_, t_store_);
-  ph("transpose");
+  // measured: no gain inside the bench's process, more variance). Page-
+  // locked values go over PCIe on side_ while stream_ sorts the transpose's
+  // keys (it needs the structure only); then c, q, l, u the same way beside
+  // the layout builds.
+  const bool vpin = nnz_ > 0 && host_is_pinned(k.vals) && env_int("AAPDHG_INGEST_OVERLAP", 1);
+  if (vpin) {
+    k_store_.rp.reserve(sizeof(int32_t) * (size_t(m_) + 1));
+    k_store_.ci.reserve(sizeof(int32_t) * size_t(nnz_));
+    k_store_.v.reserve(sizeof(double) * size_t(nnz_));
+    h2d(k_store_.rp.p, k.row_ptr, sizeof(int32_t) * (size_t(m_) + 1), stream_);
+    h2d(k_store_.ci.p, k.col_idx, sizeof(int32_t) * size_t(nnz_), stream_);
+    AAPDHG_CUDA(cudaEventRecord(ev_fork_, stream_));
+    AAPDHG_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+    h2d(k_store_.v.p, k.vals, sizeof(double) * size_t(nnz_), side_);
+    AAPDHG_CUDA(cudaEventRecord(ev_join_, side_));
+    device_validate(k_store_, m_, n_, nnz_, false);
+    ph("upload K structure");
+    TransposeScratch ts;
+    device_transpose_sort(k_store_, m_, n_, nnz_, t_store_, ts);
+    ph("transpose sort");
+    AAPDHG_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+    device_validate_values(k_store_, nnz_);
+    ph("K values");
+    finish_csr(m_, n_, nnz_, k_store_, Ks_, Kt_);
+    ph("K SELL");
+    upload_vectors(v->c, v->q, v->l, v->u);  // (page-locked: beside the layout builds)
+    device_transpose_permute(k_store_, nnz_, t_store_, ts);
+    ph("transpose permute");
+  } else {
+    upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
+    ph("upload K + SELL");
+    upload_vectors(v->c, v->q, v->l, v->u);  // (page-locked: beside the layout builds)
+    ph("vectors (issued)");
+    device_transpose(k_store_, m_, n_, nnz_, t_store_);
+    ph("transpose");
+  }
   finish_csr(n_, m_, nnz_, t_store_, KTs_, KTt_);
   ph("K' SELL");
   build_blocks(k_store_, m_, n_, kb_);

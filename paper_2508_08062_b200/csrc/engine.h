@@ -199,6 +199,14 @@ class Problem {
                    double short_mean);
   void device_transpose(const CsrStore& src, int nrows, int ncols, int64_t nnz, CsrStore& dst,
                         cudaStream_t s = nullptr);
+  struct TransposeScratch {
+    DevBuf perm, row_of;
+  };
+  void device_transpose_sort(const CsrStore& src, int nrows, int ncols, int64_t nnz,
+                             CsrStore& dst, TransposeScratch& ts, cudaStream_t s = nullptr);
+  void device_transpose_permute(const CsrStore& src, int64_t nnz, CsrStore& dst,
+                                TransposeScratch& ts, cudaStream_t s = nullptr);
+  void device_validate_values(const CsrStore& st, int64_t nnz);
   void device_block(const CsrStore& src, int nrows, int64_t c0, int64_t c1, CsrStore& dst,
                     int64_t* nnz_out);
   void upload_csr(const int32_t* rp, const int32_t* ci, const double* v, int nrows, int ncols,
@@ -291,7 +299,8 @@ class Problem {
   void ensure_serial_norms();
   // O(nnz) checks of the uploaded CSR, l <= u and the all-zero test on the
   // device (ingest.cu); throws the host validator's messages
-  void device_validate(const CsrStore& st, int nrows, int ncols, int64_t nnz);
+  void device_validate(const CsrStore& st, int nrows, int ncols, int64_t nnz,
+                       bool values = true);
   void device_flags_vectors();
 
   // iteration buffers

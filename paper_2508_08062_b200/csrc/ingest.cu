@@ -254,7 +254,7 @@ int device_validate_csr(const int32_t* rp, const int32_t* ci, const double* v, i
   if (nrows > 0)
     k_validate_rows<<<blocks_for(int64_t(nrows) * 32), kT, 0, s>>>(rp, ci, nrows, ncols, nnz,
                                                                   flags);
-  if (nnz > 0)
+  if (nnz > 0 && v)  // (v null: the structure only)
     k_validate_vals<<<std::min(blocks_for(nnz), 148 * 8), kT, 0, s>>>(v, nnz, flags);
   AAPDHG_CUDA(cudaGetLastError());
   int h = 0;
@@ -263,11 +263,27 @@ int device_validate_csr(const int32_t* rp, const int32_t* ci, const double* v, i
   return h;
 }
 
-void Problem::device_validate(const CsrStore& st, int nrows, int ncols, int64_t nnz) {
-  const int h = device_validate_csr(st.rp.as<int32_t>(), st.ci.as<int32_t>(), st.v.as<double>(),
-                                    nrows, ncols, nnz, stream_);
+void Problem::device_validate(const CsrStore& st, int nrows, int ncols, int64_t nnz,
+                              bool values) {
+  const int h = device_validate_csr(st.rp.as<int32_t>(), st.ci.as<int32_t>(),
+                                    values ? st.v.as<double>() : nullptr, nrows, ncols, nnz,
+                                    stream_);
   if (const char* msg = csr_flag_message(h)) throw StatusError(AAPDHG_ERR_DIMENSION, msg);
-  if (shard_rank_ < 0) all_zero_ = !(h & kCsrNonzero);  // a shard's comes from the whole LP
+  if (values && shard_rank_ < 0) all_zero_ = !(h & kCsrNonzero);  // a shard's comes from the whole LP
+}
+
+void Problem::device_validate_values(const CsrStore& st, int64_t nnz) {
+  DevBuf bf;
+  int* flags = tmp<int>(bf, 1);
+  AAPDHG_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), stream_));
+  if (nnz > 0)
+    k_validate_vals<<<std::min(blocks_for(nnz), 148 * 8), kT, 0, stream_>>>(st.v.as<double>(),
+                                                                            nnz, flags);
+  AAPDHG_CUDA(cudaGetLastError());
+  int h = 0;
+  AAPDHG_CUDA(cudaMemcpyAsync(&h, flags, sizeof h, cudaMemcpyDeviceToHost, stream_));
+  AAPDHG_CUDA(cudaStreamSynchronize(stream_));
+  if (shard_rank_ < 0) all_zero_ = !(h & kCsrNonzero);
 }
 
 void Problem::device_flags_vectors() {
@@ -523,6 +539,15 @@ void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* l
 // sparse_linalg.cpp:77-87).
 void Problem::device_transpose(const CsrStore& src, int nrows, int ncols, int64_t nnz,
                                CsrStore& dst, cudaStream_t s) {
+  TransposeScratch ts;
+  device_transpose_sort(src, nrows, ncols, nnz, dst, ts, s);
+  device_transpose_permute(src, nnz, dst, ts, s);
+}
+
+// The part that needs only the structure (rp, ci): K' row pointers, the
+// stable sort of the entries by column (perm) and each entry's row.
+void Problem::device_transpose_sort(const CsrStore& src, int nrows, int ncols, int64_t nnz,
+                                    CsrStore& dst, TransposeScratch& ts, cudaStream_t s) {
   if (!s) s = stream_;
   dst.rp.reserve(sizeof(int32_t) * (size_t(ncols) + 1));
   dst.ci.reserve(sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1)));
@@ -533,10 +558,10 @@ void Problem::device_transpose(const CsrStore& src, int nrows, int ncols, int64_
   if (nnz > 0) k_count<<<blocks_for(nnz), kT, 0, s>>>(src.ci.as<int32_t>(), nnz, cnt);
   scan_counts(cnt, ncols, dst.rp.as<int32_t>(), s);
   if (nnz == 0) return;
-  DevBuf bk, bperm_in, bperm, brow, tt;
+  DevBuf bk, bperm_in, tt;
   int32_t* keys_out = tmp<int32_t>(bk, nnz);
   int32_t* perm_in = tmp<int32_t>(bperm_in, nnz);
-  int32_t* perm = tmp<int32_t>(bperm, nnz);
+  int32_t* perm = tmp<int32_t>(ts.perm, nnz);
   k_iota<<<blocks_for(nnz), kT, 0, s>>>(perm_in, nnz);
   int bits = 1;
   while (bits < 31 && (int64_t(1) << bits) < ncols) ++bits;
@@ -545,10 +570,20 @@ void Problem::device_transpose(const CsrStore& src, int nrows, int ncols, int64_
                                               perm_in, perm, nnz, 0, bits, s));
   AAPDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp<char>(tt, bytes), bytes, src.ci.as<int32_t>(),
                                               keys_out, perm_in, perm, nnz, 0, bits, s));
-  int32_t* row_of = tmp<int32_t>(brow, nnz);
+  int32_t* row_of = tmp<int32_t>(ts.row_of, nnz);
   k_row_of<<<blocks_for(nnz), kT, 0, s>>>(src.rp.as<int32_t>(), nrows, nnz, row_of);
-  k_permute<<<blocks_for(nnz), kT, 0, s>>>(perm, row_of, src.v.as<double>(), nnz,
-                                           dst.ci.as<int32_t>(), dst.v.as<double>());
+  AAPDHG_CUDA(cudaGetLastError());
+  AAPDHG_CUDA(cudaStreamSynchronize(s));  // (the sort's scratch goes out of scope)
+}
+
+// K' columns and values in the sorted order (needs the values).
+void Problem::device_transpose_permute(const CsrStore& src, int64_t nnz, CsrStore& dst,
+                                       TransposeScratch& ts, cudaStream_t s) {
+  if (!s) s = stream_;
+  if (nnz == 0) return;
+  k_permute<<<blocks_for(nnz), kT, 0, s>>>(ts.perm.as<int32_t>(), ts.row_of.as<int32_t>(),
+                                           src.v.as<double>(), nnz, dst.ci.as<int32_t>(),
+                                           dst.v.as<double>());
   AAPDHG_CUDA(cudaGetLastError());
   AAPDHG_CUDA(cudaStreamSynchronize(s));
 }
