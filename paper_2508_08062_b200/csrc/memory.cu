@@ -3,6 +3,8 @@
 #include "memory.h"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -71,7 +73,16 @@ void* cache_alloc(size_t bytes) {
     }
   }
   void* p = nullptr;
+  static const bool trace = [] {
+    const char* t = std::getenv("AAPDHG_ALLOC_TRACE");
+    return t && t[0] == '1';
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaMalloc(&p, rb);
+  if (trace)
+    std::fprintf(stderr, "[aapdhg] cudaMalloc %zu B: %.1f us (cache holds %zu B)\n", rb,
+                 1e6 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
+                 cache().held);
   if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back, retry
     (void)cudaGetLastError();
     cache_release_all();
