@@ -395,12 +395,13 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
     std::vector<int32_t> hl(static_cast<size_t>(nlong));
     AAPDHG_CUDA(cudaMemcpyAsync(hl.data(), klen2, sizeof(int32_t) * nlong, cudaMemcpyDeviceToHost, s));
     AAPDHG_CUDA(cudaStreamSynchronize(s));
-    // only when the long rows alone cannot fill the GPU with warps (few long
-    // rows, e.g. transport K: 4,000 rows of 2,000): many long rows (Zipf)
+    // only when the long rows are too few to occupy a quarter of the GPU's
+    // warp slots: more long rows (Zipf; transport K's 4,000 rows of 2,000:
+    // K2 75.3 -> 66.2 us with a warp per row, profiles/r02b/huge_rows.txt)
     // already give every SM enough warps, and a CTA per row only adds
     // per-CTA overhead there
     const int64_t slots = int64_t(num_sms_) * kSpmvBlocksPerSM * kWarps;
-    if (nlong < slots)
+    if (4 * int64_t(nlong) < slots && env_int("AAPDHG_HUGE", 1) != 0)
       while (nhuge < nlong && hl[size_t(nhuge)] >= kHugeRow) ++nhuge;
   }
   CsrDev base{};
