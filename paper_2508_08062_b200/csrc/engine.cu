@@ -325,8 +325,9 @@ void Problem::upload_csr(const int32_t* rp, const int32_t* ci, const double* v, 
 // pass gathers only from an L2-resident slice of the vector instead of one
 // DRAM sector per nonzero. Row sums become (((b0 + b1) + b2) + ...) — fixed
 // order, deterministic, not the CPU's association.
-void Problem::build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& out) {
-  const int64_t kb = env_int("AAPDHG_L2_BLOCK_KB", 80 << 10);      // per block
+void Problem::build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& out,
+                           const char* kb_env) {
+  const int64_t kb = env_int(kb_env, env_int("AAPDHG_L2_BLOCK_KB", 80 << 10));  // per block
   const int64_t min_kb = env_int("AAPDHG_L2_BLOCK_MIN_KB", 64 << 10);  // start above
   const int64_t vec_bytes = int64_t(ncols) * 8;
   if (kb <= 0 || nrows == 0 || vec_bytes <= (min_kb << 10)) return;
@@ -636,8 +637,8 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   }
   finish_csr(n_, m_, nnz_, t_store_, KTs_, KTt_);
   ph("K' SELL");
-  build_blocks(k_store_, m_, n_, kb_);
-  build_blocks(t_store_, n_, m_, ktb_);
+  build_blocks(k_store_, m_, n_, kb_, "AAPDHG_L2_BLOCK_KB_K");    // K x: blocks of x
+  build_blocks(t_store_, n_, m_, ktb_, "AAPDHG_L2_BLOCK_KB_KT");  // K'y: blocks of y
   ph("L2 blocks");
 
   init_vectors();

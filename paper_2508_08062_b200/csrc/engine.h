@@ -281,7 +281,8 @@ class Problem {
     int nb() const { return int(blk.size()); }
   };
   Blocked kb_, ktb_;  // K (gathers xhat, n) and K' (gathers y, m)
-  void build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& out);
+  void build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& out,
+                    const char* kb_env = "AAPDHG_L2_BLOCK_KB");
   int launch_blocked_passes(cudaStream_t s, const Blocked& bk, const VecRef& x,
                             const DevState* S, int pred_aa = 0, const int32_t* stop = nullptr,
                             bool all = false);
