@@ -219,6 +219,15 @@ def cpu_reference_sample(p, tau, iters):
     return out.result.iterations / dt, kind, dt
 
 
+def cpu_reference_setup_s(p):
+    """The reference's select_step_sizes (seeded power iteration) on this host, seconds."""
+    from oracle.pyoracle import Oracle, ref_available
+    orc = Oracle("ref" if ref_available() else "port")
+    t0 = time.perf_counter()
+    orc.select_step_sizes(p, solver_config())
+    return time.perf_counter() - t0
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
@@ -589,6 +598,15 @@ def config1_leg(args, torch, dev, stream):
                "sample": f"{args.cpu_iters} iterations of configs[1] (explicit tau), {dt:.1f} s,"
                          f" 1 thread on a {host_cpu()}: the reference solve() is "
                          f"single-threaded"}
+    if cpu is not None and ttt is not None and ttt.get("first_kkt_le_1e-6"):
+        # the reference's time to tolerance, extrapolated as
+        # its step-size setup + the GPU's iteration count x its s/iteration
+        setup = cpu_reference_setup_s(p)
+        k_tol = ttt["first_kkt_le_1e-6"]["k"]
+        cpu["time_to_tol_extrapolated_s"] = setup + k_tol / cpu["value"]
+        cpu["time_to_tol_note"] = (f"extrapolated: select_step_sizes {setup:.1f} s (measured) + "
+                                   f"{k_tol} iterations (the GPU's count to max KKT <= 1e-6) "
+                                   f"x {1 / cpu['value']:.4f} s per reference iteration")
     return {"metric": METRICS[1], "workload": WORKLOADS[1], "rows": p.k.nrows, "cols": p.n(),
             "nnz": int(p.k.nnz), "value": iters / (ms / 1e3), "unit": "iterations/s",
             "ms_per_step": ms / max(iters, 1), "iterations_timed": iters,
