@@ -66,6 +66,18 @@ struct CsrDev {
   const double* sv = nullptr;
   const int32_t* long_rows = nullptr;  // longest first
   int32_t nhuge = 0;  // TREE: the first nhuge long rows (>= kHugeRow) get a CTA each
+  // TREE, many long rows: rows longer than 2 kLongChunk are cut into chunks of
+  // kLongChunk entries, one warp each (task t: long row lt_row[t], chunk
+  // lt_chunk[t]); a row's chunk sums go to lt_part[lt_base[row] + chunk] and
+  // the chunk that finishes last (ticket lt_ticket[row]) adds them in chunk
+  // order and owns the row's result. ntask = 0: a warp per long row.
+  int32_t ntask = 0;
+  const int32_t* lt_row = nullptr;
+  const int32_t* lt_chunk = nullptr;
+  const int32_t* lt_base = nullptr;
+  const int32_t* lt_nch = nullptr;
+  double* lt_part = nullptr;
+  unsigned int* lt_ticket = nullptr;
   int32_t nblk_short = 0, nblk_long = 0;  // nblk_long = nhuge + ceil((nlong - nhuge) / 8)
   int32_t sf = 1;  // lanes per row in the slices (1 = CSR-ordered row sums)
   // more slices than one wave of warps: slice s belongs to CTA s % nblk_short
@@ -84,6 +96,7 @@ enum { kCsrBadRowPtr = 1, kCsrBadColumn = 2, kCsrUnsorted = 4, kCsrNonzero = 8, 
 
 constexpr int kLongRow = 256;        // rows longer than this get a warp each
 constexpr int kHugeRow = 1024;       // TREE: rows at least this long get a CTA each
+constexpr int kLongChunk = 512;      // TREE: long-row chunk per warp (CsrDev::ntask)
 constexpr int kSpmvBlocksPerSM = 6;  // 48 warps/SM at <= 40 registers
 
 constexpr int kGroup = 64;           // CTAs per first-level partial group

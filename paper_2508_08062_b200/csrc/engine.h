@@ -188,6 +188,7 @@ class Problem {
   struct CsrStore {
     DevBuf rp, ci, v, longs;
     SellStore sell[2];
+    DevBuf lt_row, lt_chunk, lt_base, lt_nch, lt_part, lt_ticket;  // chunked long rows (TREE)
   };
   // device-side ingestion (ingest.cu)
   // (s: the stream to build on, null = stream_; the K' build runs on side_

@@ -380,7 +380,7 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
 
   // long rows: longest first (stable)
   st.longs.reserve(sizeof(int32_t) * std::max(nlong, 1));
-  int nhuge = 0;
+  int nhuge = 0, ntask = 0;
   if (nlong > 0) {
     DevBuf bk, bk2, tt;
     int32_t* klen = tmp<int32_t>(bk, nlong);
@@ -403,6 +403,40 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
     const int64_t slots = int64_t(num_sms_) * kSpmvBlocksPerSM * kWarps;
     if (4 * int64_t(nlong) < slots && env_int("AAPDHG_HUGE", 1) != 0)
       while (nhuge < nlong && hl[size_t(nhuge)] >= kHugeRow) ++nhuge;
+    // TREE without CTA-per-row rows, opt-in (AAPDHG_LONG_CHUNK=1): chunks of
+    // kLongChunk per warp for rows longer than two chunks (CsrDev::ntask).
+    // Measured slower: configs[2] K2 67.8 -> 81.0 us, configs[3] K2 842 ->
+    // 1064 us (profiles/r02b/long_chunks.txt): a warp per long row keeps up
+    if (nhuge == 0 && hl[0] > 2 * kLongChunk && env_int("AAPDHG_LONG_CHUNK", 0) != 0) {
+      std::vector<int32_t> trow, tch, base(static_cast<size_t>(nlong)),
+          nch(static_cast<size_t>(nlong));
+      int32_t parts = 0;
+      for (int lr = 0; lr < nlong; ++lr) {
+        const int32_t l = hl[size_t(lr)];
+        const int32_t c = l > 2 * kLongChunk ? (l + kLongChunk - 1) / kLongChunk : 1;
+        nch[size_t(lr)] = c;
+        base[size_t(lr)] = parts;
+        parts += c > 1 ? c : 0;
+        for (int32_t k = 0; k < c; ++k) {
+          trow.push_back(lr);
+          tch.push_back(c > 1 ? k : 0);
+        }
+      }
+      const size_t nt = trow.size();
+      st.lt_row.reserve(sizeof(int32_t) * nt);
+      st.lt_chunk.reserve(sizeof(int32_t) * nt);
+      st.lt_base.reserve(sizeof(int32_t) * size_t(nlong));
+      st.lt_nch.reserve(sizeof(int32_t) * size_t(nlong));
+      st.lt_part.reserve(sizeof(double) * size_t(std::max(parts, 1)));
+      st.lt_ticket.reserve(sizeof(unsigned int) * size_t(nlong));
+      host_to_device(st.lt_row.p, trow.data(), sizeof(int32_t) * nt, s);
+      host_to_device(st.lt_chunk.p, tch.data(), sizeof(int32_t) * nt, s);
+      host_to_device(st.lt_base.p, base.data(), sizeof(int32_t) * size_t(nlong), s);
+      host_to_device(st.lt_nch.p, nch.data(), sizeof(int32_t) * size_t(nlong), s);
+      AAPDHG_CUDA(cudaStreamSynchronize(s));  // (the host vectors go out of scope)
+      AAPDHG_CUDA(cudaMemsetAsync(st.lt_ticket.p, 0, sizeof(unsigned int) * size_t(nlong), s));
+      ntask = int(nt);
+    }
   }
   CsrDev base{};
   base.nrows = nrows;
@@ -440,6 +474,16 @@ void Problem::finish_csr(int nrows, int ncols, int64_t nnz, CsrStore& st, CsrDev
   // TREE: a CTA per huge row (the SERIAL layout keeps one lane-0 chain per row)
   tree.nhuge = nhuge;
   tree.nblk_long = nhuge + (nlong - nhuge + kWarps - 1) / kWarps;
+  if (ntask > 0) {
+    tree.ntask = ntask;
+    tree.lt_row = st.lt_row.as<int32_t>();
+    tree.lt_chunk = st.lt_chunk.as<int32_t>();
+    tree.lt_base = st.lt_base.as<int32_t>();
+    tree.lt_nch = st.lt_nch.as<int32_t>();
+    tree.lt_part = st.lt_part.as<double>();
+    tree.lt_ticket = st.lt_ticket.as<unsigned int>();
+    tree.nblk_long = (ntask + kWarps - 1) / kWarps;
+  }
 }
 
 void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* len, int sf,

@@ -373,6 +373,50 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     }
     return threadIdx.x == 0 ? row : -1;
   }
+  if (!SERIAL && A.ntask > 0) {
+    // chunked long rows: a warp per chunk; the chunk that finishes its row
+    // last adds the row's chunk sums in chunk order (deterministic)
+    const int t = (bid - A.nhuge) * kWarps + warp;
+    if (t >= A.ntask) return -1;
+    const int lr = __ldg(A.lt_row + t), ch = __ldg(A.lt_chunk + t);
+    const int row = __ldg(A.long_rows + lr);
+    const int64_t r0 = __ldg(A.rp + row), r1 = __ldg(A.rp + row + 1);
+    const int64_t e0 = r0 + int64_t(ch) * kLongChunk;
+    const int64_t e1 = e0 + kLongChunk < r1 ? e0 + kLongChunk : r1;
+    grid_dependency_wait();
+    double acc = 0.0;
+    for (int64_t c0 = e0 + lane; c0 < e1; c0 += 32 * kUnroll) {
+      double pr[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t e = c0 + 32 * u;
+        pr[u] = e < e1 ? __dmul_rn(__ldcs(A.v + e), ldx<COH>(x + __ldcs(A.ci + e))) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) acc = __dadd_rn(acc, pr[u]);
+    }
+    acc = warp_sum(acc);
+    const int nch = __ldg(A.lt_nch + lr);
+    if (nch == 1) {
+      s = acc;
+      return lane == 0 ? row : -1;
+    }
+    unsigned last = 0;
+    if (lane == 0) {
+      const int base = __ldg(A.lt_base + lr);
+      __stcg(A.lt_part + base + ch, acc);
+      __threadfence();
+      last = atomicAdd(A.lt_ticket + lr, 1u) == unsigned(nch - 1);
+      if (last) {
+        __threadfence();
+        double t2 = __ldcg(A.lt_part + base);
+        for (int c = 1; c < nch; ++c) t2 = __dadd_rn(t2, __ldcg(A.lt_part + base + c));
+        A.lt_ticket[lr] = 0u;  // (ready for the next launch)
+        s = t2;
+      }
+    }
+    return (lane == 0 && last) ? row : -1;
+  }
   // the other long rows: a warp each, 8 per CTA, after the huge rows' CTAs
   const int lr = A.nhuge + (bid - A.nhuge) * kWarps + warp;
   if (lr >= A.nlong) return -1;
