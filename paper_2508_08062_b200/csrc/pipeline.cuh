@@ -379,10 +379,11 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     const int t = (bid - A.nhuge) * kWarps + warp;
     if (t >= A.ntask) return -1;
     const int lr = __ldg(A.lt_row + t), ch = __ldg(A.lt_chunk + t);
+    const int nch = __ldg(A.lt_nch + lr);
     const int row = __ldg(A.long_rows + lr);
     const int64_t r0 = __ldg(A.rp + row), r1 = __ldg(A.rp + row + 1);
-    const int64_t e0 = r0 + int64_t(ch) * kLongChunk;
-    const int64_t e1 = e0 + kLongChunk < r1 ? e0 + kLongChunk : r1;
+    const int64_t e0 = r0 + int64_t(ch) * kLongChunk;  // (one chunk: the whole row)
+    const int64_t e1 = nch > 1 && e0 + kLongChunk < r1 ? e0 + kLongChunk : r1;
     grid_dependency_wait();
     double acc = 0.0;
     for (int64_t c0 = e0 + lane; c0 < e1; c0 += 32 * kUnroll) {
@@ -396,7 +397,6 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
       for (int u = 0; u < kUnroll; ++u) acc = __dadd_rn(acc, pr[u]);
     }
     acc = warp_sum(acc);
-    const int nch = __ldg(A.lt_nch + lr);
     if (nch == 1) {
       s = acc;
       return lane == 0 ? row : -1;

@@ -90,6 +90,28 @@ def test_device_layouts_bitwise(name, port):
                                            ref.trajectory["g_norm"][:30], rtol=1e-10)
 
 
+@pytest.mark.parametrize("name", ["huge", "all_long", "one_long"])
+def test_long_row_paths_agree(name, monkeypatch, port):
+    """The TREE long-row paths — a CTA per row (AAPDHG_HUGE), a warp per row,
+    a warp per 512-entry chunk with the last chunk adding the chunk sums in
+    order (AAPDHG_LONG_CHUNK=1, opt-in) — on rows of 300..5000 entries, the
+    first 30 iterates against the oracle at 1e-10."""
+    rc, n = shapes()[name]
+    p = lp_from_rows(rc, n, seed=len(name))
+    cfg = SolverConfig(method=Method.AA_PDHG, m=5, toll=1e-12, max_iters=40, tau=0.01,
+                       sigma=0.01, reduction="tree")
+    ref = port.solve(p, cfg)
+    for huge, chunk in (("1", "0"), ("0", "0"), ("0", "1")):
+        monkeypatch.setenv("AAPDHG_HUGE", huge)
+        monkeypatch.setenv("AAPDHG_LONG_CHUNK", chunk)
+        with Solver(p) as s:
+            got = s.solve(cfg)
+            got2 = s.solve(cfg)  # (the chunk tickets reset for the next launch)
+        np.testing.assert_allclose(got.trajectory["g_norm"][:30], ref.trajectory["g_norm"][:30],
+                                   rtol=1e-10, err_msg=f"HUGE={huge} LONG_CHUNK={chunk}")
+        assert np.array_equal(got.trajectory["g_norm"], got2.trajectory["g_norm"])
+
+
 def test_no_nonzeros(port):
     m, n = 4, 6
     k = SparseMatrix(m, n, np.zeros(m + 1, dtype=np.int32), np.zeros(0, dtype=np.int32),
