@@ -1404,11 +1404,11 @@ __device__ __noinline__ void plain_loop_control(const IterBufs& B, const DevPara
     }
     // barrier 2: K2(k) done (the workers start K1(k+1) on plain-step roles,
     // or wait for the decision when maystop says it can stop the loop)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      publish_maystop(pr, sm, gb, SERIAL ? xres[0] : t1s[P1_GX2]);
-      bar_arrive_wait(&gb->arrive2, 1, G);
+    if (!pr.no_stop_predict) {  // (opt-in, stop_likely)
+      __syncthreads();
+      if (threadIdx.x == 0) publish_maystop(pr, sm, gb, SERIAL ? xres[0] : t1s[P1_GX2]);
     }
+    if (threadIdx.x == 0) bar_arrive_wait(&gb->arrive2, 1, G);
     __syncthreads();
     if constexpr (SERIAL) {
       serial_ychains_cta<kPlainSerChunk>(B, &pr, sm, xres[0], sterms, yres);
