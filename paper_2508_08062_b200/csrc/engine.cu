@@ -67,6 +67,12 @@ int grid_for(int64_t n, int per_block = kThreads, int cap = 148 * 8) {
 
 }  // namespace
 
+// The streams of the handle this thread is working for (Problem::enter):
+// a growing buffer waits for them only, never for the whole device — a
+// device-wide synchronize would break another thread's graph capture
+// (concurrent handles: solve_sweep).
+thread_local cudaStream_t g_tls_sync[2] = {nullptr, nullptr};
+
 // Device buffers come from the per-device block cache (memory.cu); a block
 // returns to it when its owner is done with it (owners synchronise first).
 DevBuf::~DevBuf() {
@@ -77,7 +83,12 @@ void DevBuf::reserve(size_t b) {
   if (b == 0) b = 16;
   if (p && b <= bytes) return;
   if (p) {  // growth: work in flight may still read the old block
-    AAPDHG_CUDA(cudaDeviceSynchronize());
+    if (g_tls_sync[0] || g_tls_sync[1]) {
+      for (cudaStream_t st : g_tls_sync)
+        if (st) AAPDHG_CUDA(cudaStreamSynchronize(st));
+    } else {
+      AAPDHG_CUDA(cudaDeviceSynchronize());
+    }
     cache_free(p, bytes);
   }
   p = nullptr;
@@ -101,6 +112,7 @@ struct SolveSetup {
   int np1 = 0, np2 = 0;  // partial rows: CTAs, or slices (calibrated partition)
   bool split = false;    // L2-blocked TREE: all blocks as passes, then k_dual_epi / k_primal_epi
   int epi = 0;           // their grid (grid-stride rows)
+  bool epi_pipe = false; // k_dual_epi per K column block, K's passes beside it (side_)
   unsigned long long* bal = nullptr;  // per-CTA phase times (calibrating)
 };
 
@@ -335,6 +347,7 @@ void Problem::build_blocks(const CsrStore& src, int nrows, int ncols, Blocked& o
   const int nb = int((int64_t(ncols) + per - 1) / per);
   if (nb < 2) return;
   const int64_t W = (int64_t(ncols) + nb - 1) / nb;
+  out.width = W;
   building_blocks_ = true;
   for (int b = 0; b < nb; ++b) {
     out.store.emplace_back(new CsrStore());
@@ -527,8 +540,11 @@ void Problem::init_device(int device) {
   AAPDHG_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
   stream_ = own_stream_;
   AAPDHG_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  g_tls_sync[0] = stream_;
+  g_tls_sync[1] = side_;
   AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  for (auto& e : ev_blk_) AAPDHG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   pdl_ = env_int("AAPDHG_PDL", 1) != 0;
 }
 
@@ -651,11 +667,20 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
   ph("norms");
 }
 
+void Problem::enter() {
+  AAPDHG_CUDA(cudaSetDevice(device_));
+  g_tls_sync[0] = stream_;
+  g_tls_sync[1] = side_;
+}
+
 Problem::~Problem() {
   PhaseTimer ph;
   // the device buffers go back to the block cache: nothing may still use them
+  // (this handle's streams; not the device: another thread may be capturing)
   cudaSetDevice(device_);
-  cudaDeviceSynchronize();
+  if (stream_) cudaStreamSynchronize(stream_);
+  if (side_) cudaStreamSynchronize(side_);
+  if (g_tls_sync[0] == stream_ || g_tls_sync[1] == side_) g_tls_sync[0] = g_tls_sync[1] = nullptr;
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   ph("destroy: graph");
   for (auto& e : event_pool_) cudaEventDestroy(e);
@@ -669,13 +694,15 @@ Problem::~Problem() {
   delete sh_su_;
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
+  for (auto& e : ev_blk_)
+    if (e) cudaEventDestroy(e);
   if (side_) cudaStreamDestroy(side_);
   if (own_stream_) cudaStreamDestroy(own_stream_);
   ph("destroy: streams");
 }
 
 void Problem::set_stream(cudaStream_t s) {
-  AAPDHG_CUDA(cudaSetDevice(device_));
+  enter();
   AAPDHG_CUDA(cudaStreamSynchronize(stream_));
   stream_ = s ? s : own_stream_;
   if (graph_exec_) {  // a graph is replayed on whatever stream; keep it
@@ -748,7 +775,7 @@ void Problem::ensure_iter_buffers(int method, int cap) {
   kxpool_.reserve(sizeof(double) * 3 * std::max<int64_t>(m_, 1));
   T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
   T2_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
-  nblk1 = std::max(nblk1, num_sms_ * kSpmvBlocksPerSM);  // (k_dual_epi / k_primal_epi)
+  nblk1 = std::max(nblk1, num_sms_ * kSpmvBlocksPerSM * std::max(kb_.nb(), 1));  // (k_dual_epi per K block)
   nblk2 = std::max(nblk2, num_sms_ * kSpmvBlocksPerSM);
   part1_.reserve(sizeof(double) * P1_COUNT * std::max(nblk1, 1));
   part2_.reserve(sizeof(double) * P2_COUNT * std::max(nblk2, 1));
@@ -949,17 +976,46 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
     if (n_ > 0) {
       nodes += launch_blocked_passes(s, ktb_, VecRef{nullptr, su.B.upool, U_CUR, N_, n_}, su.S, 0,
                                      nullptr, true);
-      if (push) LAUNCH("k_dual_epi", (k_dual_epi<true><<<su.epi, kThreads, 0, s>>>(ktb_.partial.as<double>(), su.B, su.P, su.S)));
-      else LAUNCH("k_dual_epi", (k_dual_epi<false><<<su.epi, kThreads, 0, s>>>(ktb_.partial.as<double>(), su.B, su.P, su.S)));
+    }
+    // the dual epilogue per column block of K (xhat of block b) on s; K's
+    // pass b on side_ right after it, beside the epilogue of block b + 1
+    // (AAPDHG_EPI_PIPE=0: one epilogue launch, then the passes on s)
+    const int nbk = kb_.nb();
+    const bool pipe = su.epi_pipe && m_ > 0 && n_ > 0 && nbk <= kMaxPipe;
+    if (n_ > 0) {
+      const int parts = pipe ? nbk : 1;
+      for (int b = 0; b < parts; ++b) {
+        const int j0 = pipe ? int(int64_t(b) * kb_.width) : 0;
+        const int j1 = pipe ? int(std::min<int64_t>(n_, int64_t(b + 1) * kb_.width)) : n_;
+        const int off = b * su.epi;
+        if (push) LAUNCH("k_dual_epi", (k_dual_epi<true><<<su.epi, kThreads, 0, s>>>(ktb_.partial.as<double>(), su.B, su.P, su.S, j0, j1, off, parts * su.epi)));
+        else LAUNCH("k_dual_epi", (k_dual_epi<false><<<su.epi, kThreads, 0, s>>>(ktb_.partial.as<double>(), su.B, su.P, su.S, j0, j1, off, parts * su.epi)));
+        if (pipe) AAPDHG_CUDA(cudaEventRecord(ev_blk_[b], s));
+      }
+    }
+    if (pipe) {
+      for (int b = 0; b < nbk; ++b) {
+        AAPDHG_CUDA(cudaStreamWaitEvent(side_, ev_blk_[b], 0));
+        prof_begin(side_, "k_spmv_pass");
+        k_spmv_pass<<<kb_.blk[b].grid(), kThreads, 0, side_>>>(
+            kb_.blk[b], VecRef{nullptr, su.B.upool, U_HAT, N_, 0}, kb_.partial.as<double>(),
+            b == 0 ? 1 : 0, su.S, 0, nullptr);
+        prof_end(side_);
+        AAPDHG_CUDA(cudaGetLastError());
+        ++nodes;
+      }
+      AAPDHG_CUDA(cudaEventRecord(ev_join_, side_));
+      AAPDHG_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
     }
     if (m_ > 0) {
-      nodes += launch_blocked_passes(s, kb_, VecRef{nullptr, su.B.upool, U_HAT, N_, 0}, su.S, 0,
-                                     nullptr, true);
+      if (!pipe)
+        nodes += launch_blocked_passes(s, kb_, VecRef{nullptr, su.B.upool, U_HAT, N_, 0}, su.S, 0,
+                                       nullptr, true);
       if (push) LAUNCH("k_primal_epi", (k_primal_epi<true><<<su.epi, kThreads, 0, s>>>(kb_.partial.as<double>(), su.B, su.P, su.S)));
       else LAUNCH("k_primal_epi", (k_primal_epi<false><<<su.epi, kThreads, 0, s>>>(kb_.partial.as<double>(), su.B, su.P, su.S)));
     }
     if (su.B.fused_ctrl != 1)
-      LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), n_ > 0 ? su.epi : 0,
+      LAUNCH("k_control", k_control<<<1, kCtrlThreads, 0, s>>>(part1_.as<double>(), n_ > 0 ? su.B.nu1 : 0,
                                                               part2_.as<double>(), su.epi, su.P, su.S));
     AAPDHG_CUDA(cudaGetLastError());
     return nodes;
@@ -1185,7 +1241,7 @@ void Problem::run_power(const double* x0, int max_iters, double rel_tol, bool se
 // host with the same std::mt19937_64 + uniform_real_distribution(-1, 1)).
 double Problem::power_norm(int max_iters, double rel_tol, uint64_t seed, bool serial,
                            int* rounds) {
-  AAPDHG_CUDA(cudaSetDevice(device_));
+  enter();
   if (rounds) *rounds = 0;
   if (all_zero_ || n_ == 0) return 0.0;
   if (max_iters <= 0) return 0.0;
@@ -1222,7 +1278,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
                     aapdhg_record_sink sink, void* ctx) {
   const auto t_start = Clock::now();
   PhaseTimer ph;
-  AAPDHG_CUDA(cudaSetDevice(device_));
+  enter();
   validate_config(prm);
   if (!bounds_ok_) throw StatusError(AAPDHG_ERR_INPUT, "build_lambda_set: l > u");
   const int method = prm->method;
@@ -1345,9 +1401,12 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   if (blk1 && blk2 && n_ > 0 && m_ > 0 && env_int("AAPDHG_SPLIT_EPI", 1) != 0) {
     su.split = true;
     su.epi = num_sms_ * kSpmvBlocksPerSM;
-    su.B.nu1 = su.epi;
-    su.nblk1 = su.nblk2 = su.epi;
-    P.nblk1 = P.nblk2 = su.epi;
+    su.epi_pipe = env_int("AAPDHG_EPI_PIPE", 1) != 0 && kb_.nb() <= kMaxPipe;
+    su.B.nu1 = su.epi * (su.epi_pipe ? kb_.nb() : 1);
+    su.nblk1 = su.B.nu1;
+    su.nblk2 = su.epi;
+    P.nblk1 = su.nblk1;
+    P.nblk2 = su.epi;
   }
 
   // executable graph, cached per launch layout (use_graph above)
@@ -1587,7 +1646,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
 
 // ---- single-op entry points ----------------------------------------------
 void Problem::matvec(const double* x, double* out) {
-  AAPDHG_CUDA(cudaSetDevice(device_));
+  enter();
   h2d(pw_x_.p, x, sizeof(double) * n_, stream_);
   spmv(stream_, Ks_, vref(pw_x_.as<double>()), rout(pw_mx_.as<double>()), true, nullptr, 0,
        nullptr);
@@ -1596,7 +1655,7 @@ void Problem::matvec(const double* x, double* out) {
 }
 
 void Problem::matvec_transpose(const double* y, double* out) {
-  AAPDHG_CUDA(cudaSetDevice(device_));
+  enter();
   h2d(pw_mx_.p, y, sizeof(double) * m_, stream_);
   spmv(stream_, KTs_, vref(pw_mx_.as<double>()), rout(pw_mtmx_.as<double>()), true, nullptr, 0,
        nullptr);
@@ -1617,7 +1676,7 @@ static DevState identity_state() {
 // pdhg_step, pdhg_core.cpp:45-63, through the fused K1/K2 kernels
 void Problem::pdhg_step(double tau, double sigma, const double* x, const double* y,
                         double* xn, double* yn) {
-  AAPDHG_CUDA(cudaSetDevice(device_));
+  enter();
   ensure_iter_buffers(AAPDHG_METHOD_PDHG, 1);
   upload_iterate(0, x, y);
   spmv(stream_, Ks_, vref(upool_.as<double>()), rout(kxpool_.as<double>()), true, nullptr, 0,
@@ -1655,7 +1714,7 @@ void Problem::pdhg_step(double tau, double sigma, const double* x, const double*
 
 void Problem::kkt_metrics(int reduction, const double* x, const double* y, double* kkt,
                           double* lam) {
-  AAPDHG_CUDA(cudaSetDevice(device_));
+  enter();
   ensure_iter_buffers(AAPDHG_METHOD_PDHG, 1);
   upload_iterate(0, x, y);
   double* kd = scal_.as<double>() + 16;
@@ -1685,7 +1744,7 @@ int Problem::aa_op(int reduction, bool filtered, int p, const double* du_cols,
                    const double* dg_cols, double beta, const double* d_hat, double eta,
                    double c_s, double kappa_bar, int faa_skip, const double* u, const double* g,
                    double* out, int32_t* kept, double* r_out, double* q_out) {
-  AAPDHG_CUDA(cudaSetDevice(device_));
+  enter();
   if (p < 0) throw StatusError(AAPDHG_ERR_DIMENSION, "aa_apply: negative memory size");
   if (p > kMaxMemory)
     throw StatusError(AAPDHG_ERR_UNSUPPORTED, "aa_apply: memory larger than supported");
@@ -1858,7 +1917,7 @@ void Problem::sh_p2p_barrier(int slot, int phase) {
 void Problem::sh_begin(const aapdhg_solve_params* prm, double tau, double sigma,
                        const double* x0, const double* y0, const double* d_hat,
                        double wall_offset) {
-  AAPDHG_CUDA(cudaSetDevice(device_));
+  enter();
   const int method = prm->method;
   const int cap = method == AAPDHG_METHOD_PDHG ? 0 : int(prm->m);
   ensure_iter_buffers(method, std::max(cap, 1));
@@ -2106,7 +2165,7 @@ void Problem::sh_records(uint64_t from, uint64_t cnt, aapdhg_record* out) {
 
 // power_iteration_norm (sparse_linalg.cpp:95-123) phases of one shard
 void Problem::sh_pw_init(const double* x0_loc) {
-  AAPDHG_CUDA(cudaSetDevice(device_));
+  enter();
   double* x = pw_x_.as<double>();
   h2d(x, x0_loc, sizeof(double) * n_, stream_);
   const int nb = grid_for(n_);

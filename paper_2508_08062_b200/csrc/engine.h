@@ -165,6 +165,7 @@ class Problem {
             double* r_out, double* q_out);
 
   void set_profiling(bool on) { profiling_ = on; }
+  void enter();  // cudaSetDevice + this handle's streams for DevBuf growth (this thread)
   void set_stream(cudaStream_t s);
   const std::map<std::string, KernelStat>& kernel_stats() const { return stats_; }
   uint64_t last_launches() const { return last_launches_; }
@@ -255,6 +256,10 @@ class Problem {
   cudaStream_t own_stream_ = nullptr;
   cudaStream_t side_ = nullptr;  // SERIAL: x-side chains beside K2 (fork/join)
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  // L2-blocked TREE: k_dual_epi per column block of K on stream_, each K
+  // column pass on side_ as soon as its block of xhat is out
+  static constexpr int kMaxPipe = 16;
+  cudaEvent_t ev_blk_[kMaxPipe] = {};
   int n_ = 0, m_ = 0, m1_ = 0;
   int64_t nnz_ = 0, N_ = 0, nglob_ = 0;
   // sharded solve
@@ -279,6 +284,7 @@ class Problem {
     std::vector<CsrDev> blk;
     std::vector<std::unique_ptr<CsrStore>> store;
     DevBuf partial;  // row partial sums between passes
+    int64_t width = 0;  // columns per block (block b: [b width, (b + 1) width))
     int nb() const { return int(blk.size()); }
   };
   Blocked kb_, ktb_;  // K (gathers xhat, n) and K' (gathers y, m)

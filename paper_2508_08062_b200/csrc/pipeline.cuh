@@ -1100,14 +1100,14 @@ __global__ void __launch_bounds__(kThreads, AAPDHG_K12_MINBLOCKS)
 template <bool PUSH>
 __global__ void __launch_bounds__(kThreads)
     k_dual_epi(const double* __restrict__ T, IterBufs B, const DevParams* __restrict__ P,
-               DevState* S) {
+               DevState* S, int j0, int j1, int part_off, int part_rows) {
   TL_MARK(26);
   if (S->done) return;
   __shared__ double red[P1_COUNT * kWarps];
   const double* x = B.upool + (int64_t)S->u_idx[U_CUR] * P->N;
   double acc[P1_COUNT] = {0.0, 0.0, 0.0, 0.0};
   bool first = true;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P->n;
+  for (int64_t j = j0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < j1;
        j += (int64_t)gridDim.x * blockDim.x) {
     double term[P1_COUNT];
     dual_epilogue<false, PUSH>(int(j), T[j], x, B, P, S, term);
@@ -1118,7 +1118,7 @@ __global__ void __launch_bounds__(kThreads)
   block_sum<P1_COUNT>(acc, red);
   if (threadIdx.x == 0)
 #pragma unroll
-    for (int q = 0; q < P1_COUNT; ++q) B.part1[q * gridDim.x + blockIdx.x] = acc[q];
+    for (int q = 0; q < P1_COUNT; ++q) B.part1[q * part_rows + part_off + blockIdx.x] = acc[q];
 }
 
 template <bool PUSH>

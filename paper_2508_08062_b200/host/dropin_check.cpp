@@ -173,6 +173,11 @@ int main() {
     sweep_ok = sw[i].ok && sw[i].output.result.iterations == alone.result.iterations &&
                sw[i].output.result.u.x == alone.result.u.x &&
                sw[i].output.trajectory.size() == alone.trajectory.size();
+    if (!sweep_ok)
+      std::fprintf(stderr, "sweep case %s: ok %d error '%s' iterations %zu vs %zu alone, records %zu vs %zu\n",
+                   cases[i].name.c_str(), int(sw[i].ok), sw[i].error.c_str(),
+                   sw[i].output.result.iterations, alone.result.iterations,
+                   sw[i].output.trajectory.size(), alone.trajectory.size());
   }
   put("sweep_ok", sweep_ok ? "true" : "false");
   js += ", \"sweep_names\": \"" + names + "\"";
