@@ -629,20 +629,30 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
     AAPDHG_CUDA(cudaEventRecord(ev_fork_, stream_));
     AAPDHG_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
     h2d(k_store_.v.p, k.vals, sizeof(double) * size_t(nnz_), side_);
-    AAPDHG_CUDA(cudaEventRecord(ev_join_, side_));
+    AAPDHG_CUDA(cudaEventRecord(ev_blk_[0], side_));
+    upload_vectors(v->c, v->q, v->l, v->u);  // (side_, behind the values)
     device_validate(k_store_, m_, n_, nnz_, false);
     ph("upload K structure");
+    // the structure of every layout while the values are in flight (the
+    // SELL fills and the blocks' value copies queued: defer_fills_)
     TransposeScratch ts;
     device_transpose_sort(k_store_, m_, n_, nnz_, t_store_, ts);
-    ph("transpose sort");
-    AAPDHG_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+    device_transpose_permute(k_store_, nnz_, t_store_, ts, nullptr, 1);
+    ph("transpose structure");
+    defer_fills_ = true;
+    finish_csr(m_, n_, nnz_, k_store_, Ks_, Kt_);
+    finish_csr(n_, m_, nnz_, t_store_, KTs_, KTt_);
+    ph("K, K' SELL structure");
+    build_blocks(k_store_, m_, n_, kb_, "AAPDHG_L2_BLOCK_KB_K");
+    build_blocks(t_store_, n_, m_, ktb_, "AAPDHG_L2_BLOCK_KB_KT");
+    defer_fills_ = false;
+    ph("L2 blocks structure");
+    AAPDHG_CUDA(cudaStreamWaitEvent(stream_, ev_blk_[0], 0));  // the values are on the device
     device_validate_values(k_store_, nnz_);
     ph("K values");
-    finish_csr(m_, n_, nnz_, k_store_, Ks_, Kt_);
-    ph("K SELL");
-    upload_vectors(v->c, v->q, v->l, v->u);  // (page-locked: beside the layout builds)
-    device_transpose_permute(k_store_, nnz_, t_store_, ts);
-    ph("transpose permute");
+    device_transpose_permute(k_store_, nnz_, t_store_, ts, nullptr, 2);
+    flush_fills();
+    ph("value fills");
   } else {
     upload_csr(k.row_ptr, k.col_idx, k.vals, m_, n_, k_store_, Ks_, Kt_);
     ph("upload K + SELL");
@@ -650,12 +660,12 @@ Problem::Problem(const aapdhg_problem_view* v, int device) : device_(device) {
     ph("vectors (issued)");
     device_transpose(k_store_, m_, n_, nnz_, t_store_);
     ph("transpose");
+    finish_csr(n_, m_, nnz_, t_store_, KTs_, KTt_);
+    ph("K' SELL");
+    build_blocks(k_store_, m_, n_, kb_, "AAPDHG_L2_BLOCK_KB_K");    // K x: blocks of x
+    build_blocks(t_store_, n_, m_, ktb_, "AAPDHG_L2_BLOCK_KB_KT");  // K'y: blocks of y
+    ph("L2 blocks");
   }
-  finish_csr(n_, m_, nnz_, t_store_, KTs_, KTt_);
-  ph("K' SELL");
-  build_blocks(k_store_, m_, n_, kb_, "AAPDHG_L2_BLOCK_KB_K");    // K x: blocks of x
-  build_blocks(t_store_, n_, m_, ktb_, "AAPDHG_L2_BLOCK_KB_KT");  // K'y: blocks of y
-  ph("L2 blocks");
 
   init_vectors();
   device_flags_vectors();

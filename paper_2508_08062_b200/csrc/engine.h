@@ -207,7 +207,22 @@ class Problem {
   void device_transpose_sort(const CsrStore& src, int nrows, int ncols, int64_t nnz,
                              CsrStore& dst, TransposeScratch& ts, cudaStream_t s = nullptr);
   void device_transpose_permute(const CsrStore& src, int64_t nnz, CsrStore& dst,
-                                TransposeScratch& ts, cudaStream_t s = nullptr);
+                                TransposeScratch& ts, cudaStream_t s = nullptr, int part = 3);
+  // ingestion in two phases (page-locked values arrive while the structure is
+  // built): with defer_fills_ the SELL fills and the blocks' value copies are
+  // queued, flush_fills runs them once the values are on the device
+  struct PendingFill {
+    int kind;  // 0: SELL fill of st into ss; 1: the values of block st from src
+    CsrStore* st;
+    SellStore* ss;
+    int nslices, sf;
+    const CsrStore* src;
+    int64_t c0;
+    int nrows;
+  };
+  bool defer_fills_ = false;
+  std::vector<PendingFill> pending_fills_;
+  void flush_fills(cudaStream_t s = nullptr);
   void device_validate_values(const CsrStore& st, int64_t nnz);
   void device_block(const CsrStore& src, int nrows, int64_t c0, int64_t c1, CsrStore& dst,
                     int64_t* nnz_out);

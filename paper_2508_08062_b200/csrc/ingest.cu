@@ -153,13 +153,14 @@ __global__ void k_count(const int32_t* keys, int64_t n, int32_t* cnt) {
     atomicAdd(cnt + keys[i], 1);
 }
 
+// (ci_out / v_out null: that half later, ingestion's structure / value phases)
 __global__ void k_permute(const int32_t* perm, const int32_t* row_of, const double* v, int64_t n,
                           int32_t* ci_out, double* v_out) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t e = perm[i];
-    ci_out[i] = row_of[e];
-    v_out[i] = v[e];
+    if (ci_out) ci_out[i] = row_of[e];
+    if (v_out) v_out[i] = v[e];
   }
 }
 
@@ -229,9 +230,9 @@ __global__ void k_block_fill(const int32_t* rp, const int32_t* ci, const double*
        r += int64_t(gridDim.x) * blockDim.x) {
     const int32_t s = lower(ci, rp[r], rp[r + 1], c0);
     const int32_t d = brp[r], n = brp[r + 1] - d;
-    for (int32_t k = 0; k < n; ++k) {
-      bci[d + k] = ci[s + k];
-      bv[d + k] = v[s + k];
+    for (int32_t k = 0; k < n; ++k) {  // (bci / bv null: that half later)
+      if (bci) bci[d + k] = ci[s + k];
+      if (bv) bv[d + k] = v[s + k];
     }
   }
 }
@@ -544,10 +545,15 @@ void Problem::device_sell(const int32_t* shorts_in, int nshort, const int32_t* l
   ss.sv.reserve(sizeof(double) * size_t(std::max<int64_t>(total, 1)));
   AAPDHG_CUDA(cudaMemsetAsync(ss.sci.p, 0, ss.sci.bytes, s));
   AAPDHG_CUDA(cudaMemsetAsync(ss.sv.p, 0, ss.sv.bytes, s));
-  if (nslices > 0)
-    k_sell_fill<<<int((int64_t(nslices) * 32 + kT - 1) / kT), kT, 0, s>>>(
-        st.rp.as<int32_t>(), st.ci.as<int32_t>(), st.v.as<double>(), ss.sl_row.as<int32_t>(),
-        ss.sl_ptr.as<int64_t>(), nslices, sf, ss.sci.as<int32_t>(), ss.sv.as<double>());
+  if (nslices > 0) {
+    if (defer_fills_) {  // (the values are not on the device yet: flush_fills)
+      pending_fills_.push_back(PendingFill{0, &st, &ss, nslices, sf, nullptr, 0, 0});
+    } else {
+      k_sell_fill<<<int((int64_t(nslices) * 32 + kT - 1) / kT), kT, 0, s>>>(
+          st.rp.as<int32_t>(), st.ci.as<int32_t>(), st.v.as<double>(), ss.sl_row.as<int32_t>(),
+          ss.sl_ptr.as<int64_t>(), nslices, sf, ss.sci.as<int32_t>(), ss.sv.as<double>());
+    }
+  }
   AAPDHG_CUDA(cudaGetLastError());
   AAPDHG_CUDA(cudaStreamSynchronize(s));  // scratch buffers go out of scope
   ingest_ph(s, "sell: meta + fill");
@@ -623,14 +629,36 @@ void Problem::device_transpose_sort(const CsrStore& src, int nrows, int ncols, i
 
 // K' columns and values in the sorted order (needs the values).
 void Problem::device_transpose_permute(const CsrStore& src, int64_t nnz, CsrStore& dst,
-                                       TransposeScratch& ts, cudaStream_t s) {
+                                       TransposeScratch& ts, cudaStream_t s, int part) {
   if (!s) s = stream_;
   if (nnz == 0) return;
+  // part: 3 = columns and values, 1 = columns (structure), 2 = values
   k_permute<<<blocks_for(nnz), kT, 0, s>>>(ts.perm.as<int32_t>(), ts.row_of.as<int32_t>(),
-                                           src.v.as<double>(), nnz, dst.ci.as<int32_t>(),
-                                           dst.v.as<double>());
+                                           src.v.as<double>(), nnz,
+                                           (part & 1) ? dst.ci.as<int32_t>() : nullptr,
+                                           (part & 2) ? dst.v.as<double>() : nullptr);
   AAPDHG_CUDA(cudaGetLastError());
   AAPDHG_CUDA(cudaStreamSynchronize(s));
+}
+
+// The value work deferred while the structure was built (defer_fills_): the
+// blocks' values (in block order), then every SELL fill, in the order queued.
+void Problem::flush_fills(cudaStream_t s) {
+  if (!s) s = stream_;
+  for (const PendingFill& f : pending_fills_)
+    if (f.kind == 1 && f.nrows > 0)
+      k_block_fill<<<blocks_for(f.nrows), kT, 0, s>>>(
+          f.src->rp.as<int32_t>(), f.src->ci.as<int32_t>(), f.src->v.as<double>(), f.nrows, f.c0,
+          f.st->rp.as<int32_t>(), nullptr, f.st->v.as<double>());
+  for (const PendingFill& f : pending_fills_)
+    if (f.kind == 0)
+      k_sell_fill<<<int((int64_t(f.nslices) * 32 + kT - 1) / kT), kT, 0, s>>>(
+          f.st->rp.as<int32_t>(), f.st->ci.as<int32_t>(), f.st->v.as<double>(),
+          f.ss->sl_row.as<int32_t>(), f.ss->sl_ptr.as<int64_t>(), f.nslices, f.sf,
+          f.ss->sci.as<int32_t>(), f.ss->sv.as<double>());
+  AAPDHG_CUDA(cudaGetLastError());
+  AAPDHG_CUDA(cudaStreamSynchronize(s));
+  pending_fills_.clear();
 }
 
 // One column block's CSR (the same rows restricted to [c0, c1), CSR order
@@ -647,11 +675,14 @@ void Problem::device_block(const CsrStore& src, int nrows, int64_t c0, int64_t c
   const int64_t nnz = scan_counts(cnt, nrows, dst.rp.as<int32_t>(), s);
   dst.ci.reserve(sizeof(int32_t) * size_t(std::max<int64_t>(nnz, 1)));
   dst.v.reserve(sizeof(double) * size_t(std::max<int64_t>(nnz, 1)));
-  if (nrows > 0 && nnz > 0)
+  if (nrows > 0 && nnz > 0) {
     k_block_fill<<<blocks_for(nrows), kT, 0, s>>>(src.rp.as<int32_t>(), src.ci.as<int32_t>(),
                                                   src.v.as<double>(), nrows, c0,
                                                   dst.rp.as<int32_t>(), dst.ci.as<int32_t>(),
-                                                  dst.v.as<double>());
+                                                  defer_fills_ ? nullptr : dst.v.as<double>());
+    if (defer_fills_)  // (the block's values once src's are on the device: flush_fills)
+      pending_fills_.push_back(PendingFill{1, &dst, nullptr, 0, 0, &src, c0, nrows});
+  }
   AAPDHG_CUDA(cudaGetLastError());
   AAPDHG_CUDA(cudaStreamSynchronize(s));
   ingest_ph(s, "block: count + fill");

@@ -34,8 +34,16 @@ def test_block_cache_across_handles_of_different_shapes():
             same(s.solve(cfg()), want[sc])
 
 
-def test_pinned_and_pageable_inputs_and_outputs_agree():
+@pytest.mark.parametrize("blocks", [False, True])
+def test_pinned_and_pageable_inputs_and_outputs_agree(blocks, monkeypatch):
+    """Page-locked inputs take the two-phase ingestion (the values over PCIe on
+    a side stream while every layout's structure is built, then the value
+    fills); pageable ones the one-phase path: identical solves. `blocks`: with
+    L2 column blocks (tiny ones) so the blocks' structure / value split runs."""
     import torch
+    if blocks:
+        monkeypatch.setenv("AAPDHG_L2_BLOCK_MIN_KB", "0")
+        monkeypatch.setenv("AAPDHG_L2_BLOCK_KB", "16")
     p = problems.make_config(1, scale=0.05)
     with Solver(p) as s:
         a = s.solve(cfg())
