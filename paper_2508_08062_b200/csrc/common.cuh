@@ -92,7 +92,8 @@ struct CsrDev {
 };
 
 // device validation flags (ingest.cu k_validate_*)
-enum { kCsrBadRowPtr = 1, kCsrBadColumn = 2, kCsrUnsorted = 4, kCsrNonzero = 8, kBoundsBad = 16 };
+enum { kCsrBadRowPtr = 1, kCsrBadColumn = 2, kCsrUnsorted = 4, kCsrNonzero = 8, kBoundsBad = 16,
+       kZeroOutside = 32 };  // (some [l_j, u_j] does not hold 0: the start P(0) is not 0)
 
 constexpr int kLongRow = 256;        // rows longer than this get a warp each
 constexpr int kHugeRow = 1024;       // TREE: rows at least this long get a CTA each

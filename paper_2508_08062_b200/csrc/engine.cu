@@ -1518,8 +1518,13 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   h2d(S, &S0, sizeof S0, stream_);
   k_project_start<<<grid_for(N_, kThreads, 1 << 30), kThreads, 0, stream_>>>(
       upool_.as<double>(), l_.as<double>(), u_.as<double>(), n_, N_, m1_, S);
-  if (m_) spmv_any(stream_, false, vref(upool_.as<double>()), rout(kxpool_.as<double>()), serial,
-                   nullptr, nullptr);
+  // K x of the start: the default start P(0) has x = +0 when every box holds
+  // 0, and then every row sum (started at +0, adding +-0 products) is +0
+  if (m_ && !x0 && zero_start_ && env_int("AAPDHG_ZERO_START", 1) != 0)
+    AAPDHG_CUDA(cudaMemsetAsync(kxpool_.p, 0, sizeof(double) * m_, stream_));
+  else if (m_)
+    spmv_any(stream_, false, vref(upool_.as<double>()), rout(kxpool_.as<double>()), serial,
+             nullptr, nullptr);
   AAPDHG_CUDA(cudaGetLastError());
 
   ph("solve: start iterate");

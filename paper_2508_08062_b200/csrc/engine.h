@@ -290,6 +290,7 @@ class Problem {
   uint64_t sh_launches_ = 0;
   bool all_zero_ = true;
   bool bounds_ok_ = true;
+  bool zero_start_ = false;  // every [l_j, u_j] holds 0: the default start P(0) has x = 0
   CsrDev Ks_, Kt_, KTs_, KTt_;  // SERIAL (sf = 1) and TREE layouts
   CsrStore k_store_, t_store_;
   // L2 column blocking (TREE mode) of a matrix whose gathered vector exceeds

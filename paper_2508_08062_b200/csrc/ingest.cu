@@ -201,8 +201,10 @@ __global__ void k_validate_vals(const double* v, int64_t nnz, int* flags) {
 __global__ void k_validate_bounds(const double* l, const double* u, int n, int* flags) {
   int f = 0;
   for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n;
-       j += int64_t(gridDim.x) * blockDim.x)
-    if (l[j] > u[j]) f = kBoundsBad;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    if (l[j] > u[j]) f |= kBoundsBad;
+    if (!(l[j] <= 0.0 && 0.0 <= u[j])) f |= kZeroOutside;
+  }
   f = __reduce_or_sync(0xffffffffu, f);
   if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
 }
@@ -300,6 +302,7 @@ void Problem::device_flags_vectors() {
   AAPDHG_CUDA(cudaMemcpyAsync(&h, flags, sizeof h, cudaMemcpyDeviceToHost, s));
   AAPDHG_CUDA(cudaStreamSynchronize(s));
   bounds_ok_ = !(h & kBoundsBad);
+  zero_start_ = !(h & kZeroOutside);
 }
 
 // exclusive scan of n int32 counts into out[0..n] (out[n] = total); returns total
