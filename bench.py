@@ -585,6 +585,19 @@ def config1_leg(args, torch, dev, stream):
         roofline["per_kernel_graph"] = eager
     else:
         roofline = eager
+    # the same roofline in steady state: a 2,000-iteration solve (the 20-step
+    # solve above carries the solve's start, one launch per AA step and the
+    # dropped speculative K1 of each stop)
+    sol = s.solve(solver_config(tau=tau, max_iters=2000))
+    lib.aapdhg_cuda_last_plain_loop(s.h, C.byref(pi), C.byref(ps), C.byref(pl))
+    if pl.value:
+        st = plain_loop_roofline(args, p, (int(pi.value), float(ps.value), int(pl.value)), 1.0)
+        roofline["steady_state"] = {
+            "iterations": sol.result.iterations, "aa_steps": sol.result.i,
+            "plain_iterations": int(pi.value), "launches": int(pl.value),
+            "us_per_plain_iteration": 1e6 * float(ps.value) / max(int(pi.value), 1),
+            "achieved": st["achieved"], "frac": st["frac"],
+            "gather_frac": st["gather_roofline"]["frac"]}
     ttt = None if args.no_ttt else time_to_tol(args, p, s)
     s.close()
     e2e_s, e2e_runs, out2 = time_e2e(lambda: Solver(hp, device=dev),
