@@ -1281,44 +1281,69 @@ __device__ __forceinline__ double chain_add(double s, const double* tm, int cnt)
 // quantity adds them in index order (fixed_point_residual pdhg_core.cpp:
 // 65-74, kkt_metrics solver.cpp:64-110; vec.hpp dot). Roles from `st`.
 // x side: out[0] ||xhat - x||^2, [1] bound term, [2] c'x, [3] ||c - K'y - lambda||^2
+// The chunks are double-buffered: while the chain lanes (lane 0 of warps
+// 0..3 / 0..2) add chunk c, warps 4.. stage chunk c + 1 into the other half
+// of `terms` (two buffers of CH / 2 entries per quantity).
+template <int CH>
+__device__ __forceinline__ void stage_x_terms(const IterBufs& B, const double* __restrict__ T,
+                                              const double* u, const double* uh, int n, int c0,
+                                              double* buf, int t0, int nt) {
+  constexpr int H = CH / 2;
+  for (int t = t0; t < H; t += nt) {
+    const int i = c0 + t;
+    if (i < n) {
+      const double d = __dsub_rn(uh[i], u[i]);
+      buf[0 * H + t] = __dmul_rn(d, d);
+      const double lj = B.l[i], uj = B.u[i], cj = B.c[i];
+      const double rc = __dsub_rn(cj, T[i]);
+      const double lam = project_lambda1(rc, lj, uj);
+      // kkt_metrics adds l*lambda / u*lambda only where they apply; a
+      // skipped term is -0.0, the exact identity of IEEE addition (x + -0 =
+      // x for every x, -0 included), so the chain adds unconditionally
+      double bt = -0.0;
+      if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
+      if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
+      buf[1 * H + t] = bt;
+      buf[2 * H + t] = __dmul_rn(cj, u[i]);
+      const double v = __dsub_rn(rc, lam);
+      buf[3 * H + t] = __dmul_rn(v, v);
+    }
+  }
+}
+
 template <int CH>
 __device__ void serial_xchains_cta(const IterBufs& B, const double* __restrict__ T,
                                    const DevParams* __restrict__ P, const DevState& st,
                                    double* terms, unsigned char* take, double* out) {
+  constexpr int H = CH / 2;
   const int64_t N = P->N;
   const int n = P->n;
   const double* u = B.upool + (int64_t)st.u_idx[U_CUR] * N;
   const double* uh = B.upool + (int64_t)st.u_idx[U_HAT] * N;
   const int w = threadIdx.x >> 5;
   const bool chain = (threadIdx.x & 31) == 0 && w < 4;
+  const int nw = blockDim.x >> 5;
+  const bool stager = w >= 4 && nw > 4;
   double s = 0.0;
-  for (int c0 = 0; c0 < n; c0 += CH) {
-    for (int t = threadIdx.x; t < CH; t += blockDim.x) {
-      const int i = c0 + t;
-      if (i < n) {
-        const double d = __dsub_rn(uh[i], u[i]);
-        terms[0 * CH + t] = __dmul_rn(d, d);
-        const double lj = B.l[i], uj = B.u[i], cj = B.c[i];
-        const double rc = __dsub_rn(cj, T[i]);
-        const double lam = project_lambda1(rc, lj, uj);
-        // kkt_metrics adds l*lambda / u*lambda only where they apply; a
-        // skipped term is -0.0, the exact identity of IEEE addition (x + -0 =
-        // x for every x, -0 included), so the chain adds unconditionally
-        double bt = -0.0;
-        if (isfinite(lj) && lam > 0.0) bt = __dmul_rn(lj, lam);
-        if (isfinite(uj) && lam < 0.0) bt = __dmul_rn(uj, lam);
-        terms[1 * CH + t] = bt;
-        terms[2 * CH + t] = __dmul_rn(cj, u[i]);
-        const double v = __dsub_rn(rc, lam);
-        terms[3 * CH + t] = __dmul_rn(v, v);
-      }
-    }
-    __syncthreads();
+  const int nch = (n + H - 1) / H;
+  stage_x_terms<CH>(B, T, u, uh, n, 0, terms, threadIdx.x, blockDim.x);
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    double* cur = terms + (c & 1) * 4 * H;
     if (chain) {
-      const int cnt = n - c0 < CH ? n - c0 : CH;
-      s = chain_add(s, terms + w * CH, cnt);
+      const int c0 = c * H;
+      const int cnt = n - c0 < H ? n - c0 : H;
+      s = chain_add(s, cur + w * H, cnt);
+    } else if (stager && c + 1 < nch) {
+      stage_x_terms<CH>(B, T, u, uh, n, (c + 1) * H, terms + ((c + 1) & 1) * 4 * H,
+                        threadIdx.x - 128, blockDim.x - 128);
     }
     __syncthreads();
+    if (nw <= 4 && c + 1 < nch) {  // (no spare warps: stage after the chain)
+      stage_x_terms<CH>(B, T, u, uh, n, (c + 1) * H, terms + ((c + 1) & 1) * 4 * H, threadIdx.x,
+                        blockDim.x);
+      __syncthreads();
+    }
   }
   if (chain) out[w] = s;  // 0 G2x, 1 BOUND, 2 CX, 3 DUALSQ
   __syncthreads();
@@ -1327,8 +1352,27 @@ __device__ void serial_xchains_cta(const IterBufs& B, const double* __restrict__
 // y side: out[0] ||ghat||^2 continued from the x part g2x, [1] q'y,
 // [2] primal infeasibility ||((h - Gx)_+; b - Ax)||^2
 template <int CH>
+__device__ __forceinline__ void stage_y_terms(const IterBufs& B, const double* u, const double* uh,
+                                              const double* kx, int n, int mr, int m1, int c0,
+                                              double* buf, int t0, int nt) {
+  constexpr int H = CH / 2;
+  for (int t = t0; t < H; t += nt) {
+    const int i = c0 + t;
+    if (i < mr) {
+      const double d = __dsub_rn(uh[n + i], u[n + i]);
+      buf[0 * H + t] = __dmul_rn(d, d);
+      buf[1 * H + t] = __dmul_rn(B.q[i], u[n + i]);
+      double v = __dsub_rn(B.q[i], kx[i]);
+      if (i < m1) v = smax(v, 0.0);
+      buf[2 * H + t] = __dmul_rn(v, v);
+    }
+  }
+}
+
+template <int CH>
 __device__ void serial_ychains_cta(const IterBufs& B, const DevParams* __restrict__ P,
                                    const DevState& st, double g2x, double* terms, double* out) {
+  constexpr int H = CH / 2;
   const int64_t N = P->N;
   const int n = P->n, mr = P->mrows, m1 = P->m1;
   const double* u = B.upool + (int64_t)st.u_idx[U_CUR] * N;
@@ -1336,25 +1380,28 @@ __device__ void serial_ychains_cta(const IterBufs& B, const DevParams* __restric
   const double* kx = B.kxpool + (int64_t)st.kx_idx[KX_CUR] * mr;
   const int w = threadIdx.x >> 5;
   const bool chain = (threadIdx.x & 31) == 0 && w < 3;
+  const int nw = blockDim.x >> 5;
+  const bool stager = w >= 4 && nw > 4;
   double s = (chain && w == 0) ? g2x : 0.0;
-  for (int c0 = 0; c0 < mr; c0 += CH) {
-    for (int t = threadIdx.x; t < CH; t += blockDim.x) {
-      const int i = c0 + t;
-      if (i < mr) {
-        const double d = __dsub_rn(uh[n + i], u[n + i]);
-        terms[0 * CH + t] = __dmul_rn(d, d);
-        terms[1 * CH + t] = __dmul_rn(B.q[i], u[n + i]);
-        double v = __dsub_rn(B.q[i], kx[i]);
-        if (i < m1) v = smax(v, 0.0);
-        terms[2 * CH + t] = __dmul_rn(v, v);
-      }
-    }
-    __syncthreads();
+  const int nch = (mr + H - 1) / H;
+  stage_y_terms<CH>(B, u, uh, kx, n, mr, m1, 0, terms, threadIdx.x, blockDim.x);
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    double* cur = terms + (c & 1) * 4 * H;
     if (chain) {
-      const int cnt = mr - c0 < CH ? mr - c0 : CH;
-      s = chain_add(s, terms + w * CH, cnt);
+      const int c0 = c * H;
+      const int cnt = mr - c0 < H ? mr - c0 : H;
+      s = chain_add(s, cur + w * H, cnt);
+    } else if (stager && c + 1 < nch) {
+      stage_y_terms<CH>(B, u, uh, kx, n, mr, m1, (c + 1) * H, terms + ((c + 1) & 1) * 4 * H,
+                        threadIdx.x - 128, blockDim.x - 128);
     }
     __syncthreads();
+    if (nw <= 4 && c + 1 < nch) {
+      stage_y_terms<CH>(B, u, uh, kx, n, mr, m1, (c + 1) * H, terms + ((c + 1) & 1) * 4 * H,
+                        threadIdx.x, blockDim.x);
+      __syncthreads();
+    }
   }
   if (chain) out[w] = s;
   __syncthreads();
