@@ -189,13 +189,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   double acc[NACC];
 #pragma unroll
   for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const double gt = __dsub_rn(uh[t], uc[t]);
-    g[t] = gt;
-    double v[CAP];
+  // software-pipelined (AA): the next element's loads are in flight while
+  // this one accumulates (the same element order, so the same sums)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double nv[CAP], nh = 0.0, nc = 0.0;
+  if (!FAA && t < N) {
+    nh = uh[t];
+    nc = uc[t];
 #pragma unroll
-    for (int a = 0; a < CAP; ++a) v[a] = a < p ? dgc[a][t] : 0.0;
+    for (int a = 0; a < CAP; ++a) nv[a] = a < p ? dgc[a][t] : 0.0;
+  }
+  for (; t < N; t += stride) {
+    double v[CAP];
+    double gt;
+    if constexpr (!FAA) {
+      gt = __dsub_rn(nh, nc);
+#pragma unroll
+      for (int a = 0; a < CAP; ++a) v[a] = nv[a];
+      const int64_t tn = t + stride;
+      if (tn < N) {
+        nh = uh[tn];
+        nc = uc[tn];
+#pragma unroll
+        for (int a = 0; a < CAP; ++a) nv[a] = a < p ? dgc[a][tn] : 0.0;
+      }
+    } else {
+      gt = __dsub_rn(uh[t], uc[t]);
+#pragma unroll
+      for (int a = 0; a < CAP; ++a) v[a] = a < p ? dgc[a][t] : 0.0;
+    }
+    g[t] = gt;
     int q = 0;
 #pragma unroll
     for (int a = 0; a < CAP; ++a)

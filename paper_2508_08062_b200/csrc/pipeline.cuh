@@ -1525,6 +1525,9 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   const int G = int(gridDim.x), W = G - 1, bid = int(blockIdx.x);
   TL_MARK(1);
   state_load(&st, S);
+#ifdef AAPDHG_TIMELINE
+  if (bid == 0 && threadIdx.x == 0) tl_mark(4);  // state loaded
+#endif
   if (st.done || st.batch_left <= 0) return;  // (eager launches past the batch)
   if (bid == W) {
     __shared__ __align__(16) DevParams pr;
@@ -1564,6 +1567,9 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
     if (threadIdx.x == 0) s_stop = (bar_arrive_wait(&gb->arrive1, 1, G) >> 40) != h0;
     __syncthreads();
     if (s_stop) return;  // the control stopped after the previous iteration
+#ifdef AAPDHG_TIMELINE
+    if (bid == 0 && threadIdx.x == 0 && wp == 0) tl_mark(3);  // first barrier 1 passed
+#endif
     if (bal && threadIdx.x == 0) tb2 = globaltimer_ns();
 #ifdef AAPDHG_PLAIN_STAMPS
     if (threadIdx.x == 0) ps2 = globaltimer_ns();
