@@ -365,6 +365,15 @@ int aapdhg_cuda_last_plain_loop(aapdhg_handle* h, uint64_t* iterations, double* 
 /* Fills out[0..AAPDHG_NCCL_ID_BYTES) with a fresh NCCL unique id.
  * AAPDHG_ERR_UNSUPPORTED when libnccl.so.2 cannot be loaded. */
 int aapdhg_cuda_nccl_id(uint8_t* out, size_t len, char* err, size_t errlen);
+/* k_plain_loop's calibrated partition (host only, no GPU needed; engine.cu
+ * rebalance_partition): from the current slice starts per worker CTA
+ * cur_starts[workers + 1], each worker's mean phase time phase_ns[workers], its
+ * SM sm[workers] and the work of each slice slice_work[nslices], the new
+ * starts (each SM's share in proportion to the rate it showed, <= 8 slices per
+ * worker) in new_starts[workers + 1]. */
+int aapdhg_cuda_balance_partition(int32_t workers, int32_t nslices, const int32_t* cur_starts,
+                                  const double* phase_ns, const int32_t* sm,
+                                  const int32_t* slice_work, int32_t* new_starts);
 /* The row / column blocks a world-way sharded solve uses (host only, no GPU
  * needed): row_bounds[world + 1], col_bounds[world + 1]. */
 int aapdhg_cuda_partition(const aapdhg_csr_view* k, int32_t world, int32_t* row_bounds,

@@ -170,6 +170,8 @@ def _declare_cuda(lib):
                                       C.POINTER(C.c_uint64), C.c_int32, _ip], C.c_int),
         "aapdhg_cuda_nccl_id": ([C.POINTER(C.c_uint8), C.c_size_t] + E, C.c_int),
         "aapdhg_cuda_partition": ([C.POINTER(CsrView), C.c_int32, _ip, _ip], C.c_int),
+        "aapdhg_cuda_balance_partition": ([C.c_int32, C.c_int32, _ip, _dp, _ip, _ip, _ip],
+                                          C.c_int),
         "aapdhg_cuda_problem_create_dist": ([C.POINTER(ProblemView), C.c_int, C.POINTER(DistView),
                                              C.POINTER(H)] + E, C.c_int),
         "aapdhg_cuda_last_launch_count": ([H, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
@@ -196,6 +198,7 @@ CUDA_SYMBOLS = (
     "aapdhg_cuda_set_profiling",
     "aapdhg_cuda_kernel_times", "aapdhg_cuda_last_launch_count", "aapdhg_cuda_last_plain_loop",
     "aapdhg_cuda_nccl_id", "aapdhg_cuda_partition", "aapdhg_cuda_problem_create_dist",
+    "aapdhg_cuda_balance_partition",
 )
 
 _cuda_lib = None

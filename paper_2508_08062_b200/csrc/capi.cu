@@ -110,6 +110,25 @@ int aapdhg_cuda_nccl_id(uint8_t* out, size_t len, char* err, size_t errlen) {
   });
 }
 
+int aapdhg_cuda_balance_partition(int32_t workers, int32_t nslices, const int32_t* cur_starts,
+                                  const double* phase_ns, const int32_t* sm,
+                                  const int32_t* slice_work, int32_t* new_starts) {
+  if (workers <= 0 || nslices < 0 || !cur_starts || !phase_ns || !sm || !slice_work ||
+      !new_starts)
+    return AAPDHG_ERR_INPUT;
+  try {
+    std::vector<int32_t> cur(cur_starts, cur_starts + workers + 1);
+    std::vector<double> t(phase_ns, phase_ns + workers);
+    std::vector<int> s(sm, sm + workers);
+    std::vector<int32_t> wt(slice_work, slice_work + nslices);
+    const std::vector<int32_t> out = aapdhg_b200::rebalance_partition(cur, t, s, wt);
+    for (int32_t w = 0; w <= workers; ++w) new_starts[w] = out[size_t(w)];
+    return AAPDHG_OK;
+  } catch (...) {
+    return AAPDHG_ERR_INPUT;
+  }
+}
+
 int aapdhg_cuda_partition(const aapdhg_csr_view* k, int32_t world, int32_t* row_bounds,
                           int32_t* col_bounds) {
   if (!k || !row_bounds || !col_bounds || world < 1) return AAPDHG_ERR_INPUT;

@@ -155,7 +155,9 @@ std::vector<int32_t> proportional_starts(int ns, int workers) {
 // per-lane length). Each SM gets work in proportion to the rate it showed
 // (work per microsecond of its slowest CTA), split evenly over its CTAs; the
 // slices go to the CTAs in order, <= kWarps each.
-std::vector<int32_t> rebalance(const std::vector<int32_t>& cur, const std::vector<double>& t,
+}  // namespace
+
+std::vector<int32_t> rebalance_partition(const std::vector<int32_t>& cur, const std::vector<double>& t,
                                const std::vector<int>& sm, const std::vector<int32_t>& wt) {
   const int W = int(cur.size()) - 1;
   const int ns = int(wt.size());
@@ -211,7 +213,7 @@ std::vector<int32_t> rebalance(const std::vector<int32_t>& cur, const std::vecto
   if (st[0] != 0) return cur;  // (infeasible: keep the partition)
   return st;
 }
-}  // namespace
+
 
 // Before a persistent launch: the partition (cached for this device and
 // layout shape, else proportional) into bal_start1_ / bal_start2_; *measure:
@@ -266,7 +268,8 @@ void Problem::bal_collect(const CsrDev& a, const CsrDev& b, int workers) {
   auto it = g_bal.find(key);
   if (it == g_bal.end()) return;
   BalEntry& e = it->second;
-  const auto n1 = rebalance(e.s1, t1, sm, e.w1), n2 = rebalance(e.s2, t2, sm, e.w2);
+  const auto n1 = rebalance_partition(e.s1, t1, sm, e.w1),
+             n2 = rebalance_partition(e.s2, t2, sm, e.w2);
   if (env_int("AAPDHG_VERBOSE", 0)) {
     auto moved = [](const std::vector<int32_t>& a, const std::vector<int32_t>& b) {
       int c = 0;

@@ -359,4 +359,11 @@ class Problem {
   double last_plain_secs_ = 0.0;
 };
 
+// k_plain_loop's calibrated partition (engine.cu): new slice starts per worker
+// CTA from the current ones, each worker's mean phase time, its SM and the
+// work of each slice (host only)
+std::vector<int32_t> rebalance_partition(const std::vector<int32_t>& cur,
+                                         const std::vector<double>& t, const std::vector<int>& sm,
+                                         const std::vector<int32_t>& wt);
+
 }  // namespace aapdhg_b200

@@ -88,3 +88,40 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setenv("AAPDHG_CUDA_LIB", str(tmp_path / "nope.so"))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         _abi.cuda_lib()
+
+
+def test_balance_partition_follows_the_sm_rates():
+    """k_plain_loop's calibrated partition (engine.cu rebalance_partition, host
+    only): from a proportional start and per-SM rates spread +-20%, the new
+    slice starts cover every slice once, give no worker more than 8, share
+    the work per SM in proportion to the rates (work = slice lengths), and
+    cut the slowest SM's predicted time below the proportional partition's."""
+    lib = _abi.cuda_lib()
+    rng = np.random.default_rng(5)
+    nsm, per_sm, ns = 148, 6, 6250
+    workers = nsm * per_sm - 1                      # (the control CTA takes a slot)
+    sm = np.array([w % nsm for w in range(workers)], dtype=np.int32)
+    work = rng.integers(15, 26, ns).astype(np.int32)  # slice lengths
+    cur = np.array([w * ns // workers for w in range(workers + 1)], dtype=np.int32)
+    rate = rng.uniform(0.8, 1.2, nsm)                # work per ns, per SM
+
+    def sm_time(starts):
+        w_sm = np.zeros(nsm)
+        for w in range(workers):
+            w_sm[sm[w]] += work[starts[w]:starts[w + 1]].sum()
+        return w_sm / rate, w_sm
+
+    t0, _ = sm_time(cur)
+    phase = np.array([t0[sm[w]] for w in range(workers)], dtype=np.float64)
+    new = np.empty(workers + 1, dtype=np.int32)
+    rc = lib.aapdhg_cuda_balance_partition(
+        workers, ns, cur.ctypes.data_as(C.POINTER(C.c_int32)),
+        phase.ctypes.data_as(C.POINTER(C.c_double)), sm.ctypes.data_as(C.POINTER(C.c_int32)),
+        work.ctypes.data_as(C.POINTER(C.c_int32)), new.ctypes.data_as(C.POINTER(C.c_int32)))
+    assert rc == 0
+    assert new[0] == 0 and new[-1] == ns
+    d = np.diff(new)
+    assert d.min() >= 0 and d.max() <= 8
+    t1, w_sm = sm_time(new)
+    assert np.corrcoef(w_sm, rate)[0, 1] > 0.9
+    assert t1.max() < 0.95 * t0.max()
