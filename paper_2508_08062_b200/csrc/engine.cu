@@ -547,6 +547,8 @@ void Problem::init_device(int device) {
   g_tls_sync[1] = side_;
   AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_out_, cudaEventDisableTiming));
+  AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_out_done_, cudaEventDisableTiming));
   for (auto& e : ev_blk_) AAPDHG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   pdl_ = env_int("AAPDHG_PDL", 1) != 0;
 }
@@ -707,6 +709,8 @@ Problem::~Problem() {
   delete sh_su_;
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
+  if (ev_out_) cudaEventDestroy(ev_out_);
+  if (ev_out_done_) cudaEventDestroy(ev_out_done_);
   for (auto& e : ev_blk_)
     if (e) cudaEventDestroy(e);
   if (side_) cudaStreamDestroy(side_);
@@ -1531,10 +1535,44 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   AAPDHG_CUDA(cudaGetLastError());
 
   ph("solve: start iterate");
+  // Result download beside the last iteration (large LPs, page-locked x / y,
+  // TREE, graph launches): the launches stop one iteration short of
+  // max_iters. Every stop the last iteration can take finishes on its CUR
+  // iterate (KKT of u_k, residual, max_iters, timeout: solver.cpp:182-199),
+  // which is then known, so x / y cross PCIe on side_ while the device
+  // computes its residual, KKT and lambda. A solve that stops earlier, or a
+  // final role other than CUR, takes the usual downloads.
+  const bool px_pin = x_out && n_ > 0 && host_is_pinned(x_out);
+  const bool py_pin = y_out && m_ > 0 && host_is_pinned(y_out);
+  const bool out_ovl = use_graph && !serial && (px_pin || py_pin) &&
+                       max_it_sat < (UINT64_MAX >> 1) &&
+                       int64_t(sizeof(double)) * N_ >= (int64_t(env_int("AAPDHG_OUT_OVERLAP_MB", 32)) << 20);
+  if (out_ovl) batch = int(std::min<uint64_t>(max_it_sat + 1, ring_batch));
+  int early_slot = -1;  // the slot whose x / y are on their way
   uint64_t flushed = 0, eager_launches = 0;
   std::vector<aapdhg_record> host_recs;
   const aapdhg_record* drec = rec_.as<aapdhg_record>();
   for (bool first = true;; first = false) {
+    if (!first && out_ovl) {
+      const uint64_t ij = h_state_->i + h_state_->j;
+      if (ij >= prm->max_iters) {  // the next iteration is the last one
+        batch = 1;
+        if (early_slot < 0) {
+          early_slot = h_state_->u_idx[U_CUR];
+          const double* uc = upool_.as<double>() + int64_t(early_slot) * N_;
+          AAPDHG_CUDA(cudaEventRecord(ev_out_, stream_));
+          AAPDHG_CUDA(cudaStreamWaitEvent(side_, ev_out_, 0));
+          if (px_pin)
+            AAPDHG_CUDA(cudaMemcpyAsync(x_out, uc, sizeof(double) * n_, cudaMemcpyDeviceToHost, side_));
+          if (py_pin)
+            AAPDHG_CUDA(cudaMemcpyAsync(y_out, uc + n_, sizeof(double) * m_, cudaMemcpyDeviceToHost,
+                                        side_));
+          AAPDHG_CUDA(cudaEventRecord(ev_out_done_, side_));
+        }
+      } else {
+        batch = int(std::min<uint64_t>(uint64_t(batch), prm->max_iters - ij));
+      }
+    }
     if (!first && method != AAPDHG_METHOD_PDHG) {
       // i grows by at most one per iteration: cover the next launch
       const uint64_t cap_before = pow_len_;
@@ -1601,12 +1639,22 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   const bool fast = !serial && st.final_role == U_CUR &&
                     st.status != AAPDHG_SOLVE_FIXED_POINT_START &&
                     env_int("AAPDHG_FAST_FINISH", 1) != 0;
+  bool side_copies = early_slot >= 0;
   if (fast) {
+    // page-locked x / y go over PCIe on side_ while lambda is computed (the
+    // last iteration's CUR slot may already be on its way, above)
     const bool px = x_out && host_is_pinned(x_out), py = y_out && host_is_pinned(y_out);
-    if (px) AAPDHG_CUDA(cudaMemcpyAsync(x_out, ufin, sizeof(double) * n_,
-                                        cudaMemcpyDeviceToHost, stream_));
-    if (py) AAPDHG_CUDA(cudaMemcpyAsync(y_out, ufin + n_, sizeof(double) * m_,
-                                        cudaMemcpyDeviceToHost, stream_));
+    if ((px || py) && early_slot != slot) {
+      if (early_slot >= 0) AAPDHG_CUDA(cudaStreamWaitEvent(stream_, ev_out_done_, 0));
+      AAPDHG_CUDA(cudaEventRecord(ev_out_, stream_));
+      AAPDHG_CUDA(cudaStreamWaitEvent(side_, ev_out_, 0));
+      if (px) AAPDHG_CUDA(cudaMemcpyAsync(x_out, ufin, sizeof(double) * n_,
+                                          cudaMemcpyDeviceToHost, side_));
+      if (py) AAPDHG_CUDA(cudaMemcpyAsync(y_out, ufin + n_, sizeof(double) * m_,
+                                          cudaMemcpyDeviceToHost, side_));
+      AAPDHG_CUDA(cudaEventRecord(ev_out_done_, side_));
+      side_copies = true;
+    }
     if (lam_out && n_ > 0) {
       T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
       if (m_ > 0) {
@@ -1625,6 +1673,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
     if (lam_out) d2h(lam_out, lam_.as<double>(), sizeof(double) * n_, stream_);
     ph("solve: final lambda + downloads");
   } else {
+    // (an early download of another slot must land before these copies)
+    if (early_slot >= 0) AAPDHG_CUDA(cudaStreamWaitEvent(stream_, ev_out_done_, 0));
     double* kkt_dev = scal_.as<double>() + 8;
     kkt_eval(slot, serial, kkt_dev, lam_.as<double>());
     d2h(kkt, kkt_dev, sizeof kkt, stream_);
@@ -1633,6 +1683,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
     if (y_out) d2h(y_out, ufin + n_, sizeof(double) * m_, stream_);
     if (lam_out) d2h(lam_out, lam_.as<double>(), sizeof(double) * n_, stream_);
   }
+  if (side_copies) AAPDHG_CUDA(cudaStreamWaitEvent(stream_, ev_out_done_, 0));
   sync();
   std::memset(res, 0, sizeof *res);
   res->status = st.status;

@@ -271,6 +271,8 @@ class Problem {
   cudaStream_t own_stream_ = nullptr;
   cudaStream_t side_ = nullptr;  // SERIAL: x-side chains beside K2 (fork/join)
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  // the final iterate's x / y download on side_ beside the last iteration
+  cudaEvent_t ev_out_ = nullptr, ev_out_done_ = nullptr;
   // L2-blocked TREE: k_dual_epi per column block of K on stream_, each K
   // column pass on side_ as soon as its block of xhat is out
   static constexpr int kMaxPipe = 16;

@@ -67,6 +67,41 @@ def test_pinned_and_pageable_inputs_and_outputs_agree(blocks, monkeypatch):
     assert np.array_equal(a.result.lambda_, b.result.lambda_)
 
 
+@pytest.mark.parametrize("blocks", [False, True])
+@pytest.mark.parametrize("method", [Method.AA_PDHG, Method.PDHG])
+def test_result_download_beside_the_last_iteration(blocks, method, monkeypatch):
+    """Page-locked x / y of a large LP leave on a side stream while the last
+    iteration runs (engine.cu: the launches stop one short of max_iters);
+    forced on a small LP (AAPDHG_OUT_OVERLAP_MB=0). TREE solves that stop on
+    max_iters (0, 1, 7, 40), on the residual, or on KKT must equal the same
+    solves into pageable buffers bit for bit (the overlap off)."""
+    import torch
+    if blocks:
+        monkeypatch.setenv("AAPDHG_L2_BLOCK_MIN_KB", "0")
+        monkeypatch.setenv("AAPDHG_L2_BLOCK_KB", "16")
+    p = problems.make_config(1, scale=0.05)
+    n, m = p.n(), p.k.nrows
+    outs = tuple(torch.empty(k, dtype=torch.float64, pin_memory=True).numpy() for k in (n, m, n))
+    cases = [dict(max_iters=mi) for mi in (0, 1, 7, 40)]
+    cases += [dict(max_iters=5000, toll=1e-4), dict(max_iters=5000, kkt_terminate=True, kkt_eps=1e-3)]
+    with Solver(p) as s:
+        for kw in cases:
+            c = SolverConfig(method=method, m=5, reduction="tree", **{"toll": 1e-12, **kw})
+            monkeypatch.setenv("AAPDHG_OUT_OVERLAP_MB", "1000000")
+            a = s.solve(c)
+            monkeypatch.setenv("AAPDHG_OUT_OVERLAP_MB", "0")
+            for v in outs:
+                v[...] = np.nan
+            b = s.solve(c, out=outs)
+            assert a.result.status == b.result.status, kw
+            assert a.result.iterations == b.result.iterations, kw
+            assert np.array_equal(a.trajectory["g_norm"], b.trajectory["g_norm"]), kw
+            assert np.array_equal(a.result.u.x, b.result.u.x), kw
+            assert np.array_equal(a.result.u.y, b.result.u.y), kw
+            assert np.array_equal(a.result.lambda_, b.result.lambda_), kw
+            assert a.result.g_norm == b.result.g_norm and a.result.objective == b.result.objective
+
+
 def test_safeguard_table_grows_and_max_iters_saturates():
     """A 7,575-iteration solve with 473 AA steps (config 0 at scale 0.1,
     toll 1e-5): launches after the first grow the table; then the same solve
