@@ -184,10 +184,13 @@ def kernel_bytes(p, name):
     """Algorithmic bytes per launch: CSR streams + compulsory
     gathers (each gathered element counted once) + vector reads/writes."""
     n, m, nnz = p.n(), p.k.nrows, p.k.nnz
-    if name == "k_dual_side":   # K'y + xhat + KKT dual terms + history push (x half)
-        return 12 * nnz + 4 * (n + 1) + 8 * m + 8 * n * (4 + 1) + 8 * n * (2 + 3)
-    if name == "k_primal_side":  # K xhat + yhat + KKT primal terms + push (y half)
-        return 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m * (3 + 2) + 8 * m * (2 + 3)
+    # (the AA history is the ring of g (pipeline.cuh ring_push): one 8-byte
+    # store per element and iteration, where the pushed pair read u_{k-1}
+    # and stored du, dg)
+    if name == "k_dual_side":   # K'y + xhat + KKT dual terms + g_k (x half)
+        return 12 * nnz + 4 * (n + 1) + 8 * m + 8 * n * (4 + 1) + 8 * n
+    if name == "k_primal_side":  # K xhat + yhat + KKT primal terms + g_k (y half)
+        return 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m * (3 + 2) + 8 * m
     if name == "k_plain_loop":  # one plain iteration: both halves
         return kernel_bytes(p, "k_dual_side") + kernel_bytes(p, "k_primal_side")
     if name == "k_spmv_recache":
@@ -516,12 +519,13 @@ def run_ours(args, rank, world, local_rank):
 
 def iteration_bytes(p, iters, aa_steps, memory=MEMORY):
     """Algorithmic bytes of `iters` iterations of which `aa_steps` took an AA
-    step: every iteration K1 + K2 with the history push; an
-    AA step adds the Gram pass 8N(p+3), the mix 8N(2p+3) and the K x
-    recache 12 nnz + 4(m+1) + 8n + 8m."""
+    step: every iteration K1 + K2 with g_k into the history
+    ring; an AA step adds the Gram pass over the window 8N(p+1), the mix
+    8N(p+4) (window, u, candidate and its du) and the K x recache
+    12 nnz + 4(m+1) + 8n + 8m."""
     n, m, nnz = p.n(), p.k.nrows, p.k.nnz
     N = n + m
-    aa = 8 * N * (memory + 3) + 8 * N * (2 * memory + 3) + 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
+    aa = 8 * N * (memory + 1) + 8 * N * (memory + 4) + 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
     return iters * kernel_bytes(p, "k_plain_loop") + aa_steps * aa
 
 

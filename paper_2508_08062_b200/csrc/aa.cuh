@@ -64,6 +64,23 @@ __global__ void k_serial_dots(DotBufs D, const DevParams* __restrict__ P, const 
   if ((threadIdx.x & 31) != 0) return;
   const int p = S->mem_size;
   if (item >= num_items(p, P->method)) return;
+  if (P->ring) {  // ring history: dg_a = g(a+1) - g(a) in the chain, the same order
+    int kind, a, b;
+    decode_item(item, p, kind, a, b);
+    const int64_t N = P->N;
+    const double* a1 = D.gpool + (int64_t)S->gw[a + 1] * N;
+    const double* a0 = D.gpool + (int64_t)S->gw[a] * N;
+    const double* b1 = D.gpool + (int64_t)S->gw[kind == 0 ? b + 1 : p] * N;
+    const double* b0 = D.gpool + (int64_t)S->gw[b] * N;
+    double s = 0.0;
+    for (int64_t t = 0; t < N; ++t) {
+      const double x = __dsub_rn(a1[t], a0[t]);
+      const double y = kind == 0 ? __dsub_rn(b1[t], b0[t]) : b1[t];
+      s = __dadd_rn(s, __dmul_rn(x, y));
+    }
+    D.part[item] = s;
+    return;
+  }
   const double *va, *vb;
   item_vectors(D, P, S, item, p, va, vb);
   if (D.part_lo) {
@@ -82,9 +99,11 @@ __global__ void __launch_bounds__(kThreads)
   TL_MARK(19);
   if (S->done || !S->aa_attempt) return;
   // the memory's slot table once per CTA (not a dependent global load per item)
-  __shared__ int slots[kMaxMemory];
+  __shared__ int slots[kMaxMemory + 1];
   __shared__ int sh_p, sh_g;
-  if (threadIdx.x < kMaxMemory) slots[threadIdx.x] = S->mem_slots[threadIdx.x];
+  const bool ring = P->ring != 0;
+  if (threadIdx.x < kMaxMemory + 1)
+    slots[threadIdx.x] = ring ? S->gw[threadIdx.x] : threadIdx.x < kMaxMemory ? S->mem_slots[threadIdx.x] : 0;
   if (threadIdx.x == 0) {
     sh_p = S->mem_size;
     sh_g = S->g_idx[G_CUR];
@@ -101,17 +120,30 @@ __global__ void __launch_bounds__(kThreads)
     int kind, ia, ib;
     decode_item(item, p, kind, ia, ib);
     const double *va, *vb;
-    if (kind == 0) { va = D.dg + slots[ia] * N; vb = D.dg + slots[ib] * N; }
-    else if (kind == 1) { va = D.dg + slots[ia] * N; vb = D.gpool + (int64_t)sh_g * N; }
-    else { va = D.du + slots[ia] * N; vb = va; }
-    // every load of the lane's share in flight before the adds (same order:
-    // t = lane, lane + 32, ...)
     double x[kPer], y[kPer];
+    if (ring) {  // ring history: the differences of the window's g columns
+      const double* a1 = D.gpool + (int64_t)slots[ia + 1] * N + base;
+      const double* a0 = D.gpool + (int64_t)slots[ia] * N + base;
+      const double* b1 = D.gpool + (int64_t)slots[kind == 0 ? ib + 1 : p] * N + base;
+      const double* b0 = D.gpool + (int64_t)slots[ib] * N + base;
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int t = lane + 32 * u;
-      x[u] = t < cnt ? va[base + t] : 0.0;
-      y[u] = t < cnt ? vb[base + t] : 0.0;
+      for (int u = 0; u < kPer; ++u) {
+        const int t = lane + 32 * u;
+        x[u] = t < cnt ? __dsub_rn(a1[t], a0[t]) : 0.0;
+        y[u] = t < cnt ? (kind == 0 ? __dsub_rn(b1[t], b0[t]) : b1[t]) : 0.0;
+      }
+    } else {
+      if (kind == 0) { va = D.dg + slots[ia] * N; vb = D.dg + slots[ib] * N; }
+      else if (kind == 1) { va = D.dg + slots[ia] * N; vb = D.gpool + (int64_t)sh_g * N; }
+      else { va = D.du + slots[ia] * N; vb = va; }
+      // every load of the lane's share in flight before the adds (same order:
+      // t = lane, lane + 32, ...)
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int t = lane + 32 * u;
+        x[u] = t < cnt ? va[base + t] : 0.0;
+        y[u] = t < cnt ? vb[base + t] : 0.0;
+      }
     }
     if (D.part_lo) {  // FAA: double-double partials
       double hi = 0.0, lo = 0.0;
@@ -236,6 +268,77 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   // fixed-shape CTA reduction of every live item, written in p-space order
+  __shared__ double red[kWarps][NACC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) {
+    const double s = warp_sum(acc[q]);
+    if (lane == 0) red[warp][q] = s;
+  }
+  __syncthreads();
+  const int np = p * (p + 1) / 2;
+  for (int q = threadIdx.x; q < NACC; q += blockDim.x) {
+    double s = red[0][q];
+    for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, red[w][q]);
+    const int item = gram_item(q, CAP, p, np);
+    if (item >= 0) D.part[(int64_t)item * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// k_gram_dots of the ring history (DevParams::ring, AA): the p + 1 window
+// columns g_{k-p}..g_k are loaded per element (one HBM read each, software
+// pipelined like k_gram_dots) and differenced in registers, dg_a = g(a+1) -
+// g(a) — the pushed dg bit for bit; the rhs item is dg_a . g_k. Nothing is
+// staged: the epilogues stored g_k.
+template <int CAP>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gram_dots_ring(DotBufs D, const DevParams* __restrict__ P, const DevState* S) {
+  TL_MARK(10);
+  if (S->done || !S->aa_attempt) return;
+  constexpr int NPAIR = CAP * (CAP + 1) / 2;
+  constexpr int NACC = NPAIR + CAP;
+  __shared__ int slots[CAP + 1];
+  __shared__ int sh_p;
+  if (threadIdx.x <= CAP) slots[threadIdx.x] = S->gw[threadIdx.x];
+  if (threadIdx.x == 0) sh_p = S->mem_size;
+  __syncthreads();
+  const int p = sh_p;
+  const int64_t N = P->N;
+  const double* gc[CAP + 1];
+#pragma unroll
+  for (int a = 0; a <= CAP; ++a) gc[a] = D.gpool + (int64_t)(a <= p ? slots[a] : slots[0]) * N;
+  double acc[NACC];
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double nv[CAP + 1];
+#pragma unroll
+  for (int a = 0; a <= CAP; ++a) nv[a] = (a <= p && t < N) ? gc[a][t] : 0.0;
+  for (; t < N; t += stride) {
+    double w[CAP + 1];
+#pragma unroll
+    for (int a = 0; a <= CAP; ++a) w[a] = nv[a];
+    const int64_t tn = t + stride;
+    if (tn < N) {
+#pragma unroll
+      for (int a = 0; a <= CAP; ++a) nv[a] = a <= p ? gc[a][tn] : 0.0;
+    }
+    double v[CAP];
+    double gt = 0.0;
+#pragma unroll
+    for (int a = 0; a < CAP; ++a) v[a] = a < p ? __dsub_rn(w[a + 1], w[a]) : 0.0;
+#pragma unroll
+    for (int a = 0; a <= CAP; ++a)
+      if (a == p) gt = w[a];
+    int q = 0;
+#pragma unroll
+    for (int a = 0; a < CAP; ++a)
+#pragma unroll
+      for (int b = a; b < CAP; ++b, ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(v[a], v[b]));
+#pragma unroll
+    for (int a = 0; a < CAP; ++a) acc[NPAIR + a] = __dadd_rn(acc[NPAIR + a], __dmul_rn(v[a], gt));
+  }
   __shared__ double red[kWarps][NACC];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
@@ -861,6 +964,42 @@ __global__ void __launch_bounds__(kThreads)
     sls[jj] = S->mix_slots[jj];
   }
   __syncthreads();
+  if (P->ring) {
+    // ring history: du_j / dg_j from the window (pipeline.cuh ring_push), and
+    // the candidate's own du_{k+1} = cand - u_k into du at the slot g_{k+1}
+    // takes (ring_free_slot), used when the candidate is accepted
+    __shared__ int64_t gsl[kMaxMemory + 1];
+    __shared__ uint8_t gx[kMaxMemory + 1];
+    __shared__ int64_t nxt;
+    for (int q = threadIdx.x; q <= pm; q += blockDim.x) {
+      gsl[q] = (int64_t)S->gw[q] * N;
+      gx[q] = S->gdux[q];
+    }
+    if (threadIdx.x == 0) nxt = (int64_t)ring_free_slot(P, S) * N;
+    __syncthreads();
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N;
+         t += (int64_t)gridDim.x * blockDim.x) {
+      const double gk = B.gpool[gsl[pm] + t];
+      const double ut = u[t];
+      double o = __dadd_rn(ut, damp1(beta, dh, t, gk));
+      double gp = B.gpool[gsl[0] + t];
+      for (int jj = 0; jj < pm; ++jj) {
+        const double a = nw[jj];
+        const double gc = jj + 1 == pm ? gk : B.gpool[gsl[jj + 1] + t];
+        const double du = gx[jj + 1] ? B.du[gsl[jj + 1] + t] : gp;
+        o = __dadd_rn(o, __dmul_rn(a, du));
+        o = __dadd_rn(o, __dmul_rn(a, damp1(beta, dh, t, __dsub_rn(gc, gp))));
+        gp = gc;
+      }
+      if (project) {
+        if (t < n) o = smin(smax(o, B.l[t]), B.u[t]);
+        else if (t - n < P->m1) o = smax(o, 0.0);
+      }
+      out[t] = o;
+      B.du[nxt + t] = __dsub_rn(o, ut);
+    }
+    return;
+  }
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N;
        t += (int64_t)gridDim.x * blockDim.x) {
     double o = __dadd_rn(u[t], damp1(beta, dh, t, g[t]));
@@ -906,7 +1045,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void k_stage_g(const double* __restrict__ upool, double* __restrict__ gpool,
                           const DevParams* __restrict__ P, const DevState* S) {
   TL_MARK(18);
-  if (S->done || !S->aa_attempt) return;
+  if (S->done || !S->aa_attempt || P->ring) return;  // (the ring holds g_k)
   const int64_t N = P->N;
   const double* uh = upool + (int64_t)S->u_idx[U_HAT] * N;
   const double* u = upool + (int64_t)S->u_idx[U_CUR] * N;

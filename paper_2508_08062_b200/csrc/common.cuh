@@ -151,6 +151,9 @@ struct DevParams {
   int32_t faa_skip;
   int32_t no_stop_predict;  // k_plain_loop always speculates (AAPDHG_STOP_PREDICT=1: predicts)
   int32_t phase_prefetch;   // k_plain_loop: L2 bulk prefetch of the next phase's slice streams
+  // ring history (AA-PDHG on one GPU, pipeline.cuh ring_free_slot): the
+  // epilogues store g_k, the AA kernels difference it (0: du / dg pushed)
+  int32_t ring;
   double* qr_r_out;
 };
 enum { kFaaSkipAngle = 1, kFaaSkipLength = 2 };
@@ -181,6 +184,12 @@ struct DevState {
   int32_t prev_plain;              // the previous step was T(u_{k-1}) (not an AA candidate)
   int32_t batch_left;              // iterations left in this graph launch
   uint64_t p2p_seq[8];             // P2P flag barriers passed, per exchanged buffer
+  // ring history (DevParams::ring): ring slots of g_{k-p}..g_k, oldest first
+  // (gw_n = p + 1 entries once iteration 0 committed); gdux[q]: the column
+  // ending at gw[q] has its du stored (u_t was an AA candidate)
+  int32_t gw_n;
+  int32_t gw[kMaxMemory + 1];
+  uint8_t gdux[kMaxMemory + 3];
 };
 
 // Gathered vector: a plain pointer, or a role of the iterate pool resolved
@@ -210,9 +219,9 @@ struct RowsumArgs {
 struct IterBufs {
   double* upool;   // 4 x N
   double* kxpool;  // 3 x m
-  double* gpool;   // 2 x N
-  double* du;      // cap x N
-  double* dg;      // cap x N
+  double* gpool;   // 2 x N (ring history: cap + 2 slots of g)
+  double* du;      // cap + 1 x N (ring history: cap + 2, indexed like gpool)
+  double* dg;      // cap + 1 x N (unused by the ring history)
   double* T;       // n
   double* T2;      // n: SERIAL k_plain_loop, K'y of odd iterations (the control reads
                    // iteration k's while the speculative K1(k+1) writes the other)

@@ -104,6 +104,7 @@ struct SolveSetup {
   const DevParams* P;
   DevState* S;
   bool serial, push;
+  bool ring = false;     // AA-PDHG's ring history (DevParams::ring)
   int method, cap, nblk1, nblk2, ndot_blk, items_max;
   bool persist = false;  // plain iterations in k_plain_loop (graph replay only)
   int pgrid = 0;         // workers + the control CTA
@@ -784,7 +785,7 @@ void Problem::ensure_serial_norms() {
   serial_norms_ = true;
 }
 
-void Problem::ensure_iter_buffers(int method, int cap) {
+void Problem::ensure_iter_buffers(int method, int cap, bool ring) {
   int nblk1 = std::max(KTs_.grid(), KTt_.grid()), nblk2 = std::max(Ks_.grid(), Kt_.grid());
   for (const CsrDev& b : ktb_.blk) nblk1 = std::max(nblk1, b.grid());
   for (const CsrDev& b : kb_.blk) nblk2 = std::max(nblk2, b.grid());
@@ -810,11 +811,18 @@ void Problem::ensure_iter_buffers(int method, int cap) {
   }
   ndot_tile_ = int((N_ + kDotChunk - 1) / kDotChunk);
   if (method != AAPDHG_METHOD_PDHG) {
-    gpool_.reserve(sizeof(double) * 2 * std::max<int64_t>(N_, 1));
-    // cap + 1 slots: the next push never lands in a slot the memory holds
-    // (advance, pipeline.cuh)
-    du_.reserve(sizeof(double) * size_t(cap + 1) * std::max<int64_t>(N_, 1));
-    dg_.reserve(sizeof(double) * size_t(cap + 1) * std::max<int64_t>(N_, 1));
+    if (ring) {
+      // the ring history: cap + 2 slots of g and of the stored du (ring_push,
+      // pipeline.cuh); no dg columns
+      gpool_.reserve(sizeof(double) * size_t(cap + 2) * std::max<int64_t>(N_, 1));
+      du_.reserve(sizeof(double) * size_t(cap + 2) * std::max<int64_t>(N_, 1));
+    } else {
+      gpool_.reserve(sizeof(double) * 2 * std::max<int64_t>(N_, 1));
+      // cap + 1 slots: the next push never lands in a slot the memory holds
+      // (advance, pipeline.cuh)
+      du_.reserve(sizeof(double) * size_t(cap + 1) * std::max<int64_t>(N_, 1));
+      dg_.reserve(sizeof(double) * size_t(cap + 1) * std::max<int64_t>(N_, 1));
+    }
     // hi parts, then (FAA) the low parts of the double-double partials
     const int items = num_items_host(cap, AAPDHG_METHOD_FAA);
     partdot_.reserve(2 * sizeof(double) * size_t(items) *
@@ -1105,6 +1113,10 @@ int Problem::launch_aa(cudaStream_t s, const SolveSetup& su) {
                   : c == 8 ? k_gram_dots_dd<8, 1> : k_gram_dots_dd<10, 1>;
       const int grid = c >= 8 ? 2 * su.ndot_blk : su.ndot_blk;
       LAUNCH("k_gram_dots", kern<<<grid, kThreads, 0, s>>>(su.D, su.B.upool, su.P, su.S));
+    } else if (su.ring) {  // g_k is in the ring already
+      auto kern = c == 4 ? k_gram_dots_ring<4> : c == 6 ? k_gram_dots_ring<6>
+                  : c == 8 ? k_gram_dots_ring<8> : k_gram_dots_ring<10>;
+      LAUNCH("k_gram_dots", kern<<<su.ndot_blk, kThreads, 0, s>>>(su.D, su.P, su.S));
     } else {
       auto kern = c == 4 ? k_gram_dots<4, false> : c == 6 ? k_gram_dots<6, false>
                   : c == 8 ? k_gram_dots<8, false> : k_gram_dots<10, false>;
@@ -1312,7 +1324,10 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
 
   const bool serial = resolve_serial(prm->reduction);
   const int cap = method == AAPDHG_METHOD_PDHG ? 0 : int(prm->m);
-  ensure_iter_buffers(method, std::max(cap, 1));
+  // AA-PDHG keeps its history as a ring of g (ring_push, pipeline.cuh;
+  // AAPDHG_RING=0: the pushed du / dg columns)
+  const bool ring = method == AAPDHG_METHOD_AA && env_int("AAPDHG_RING", 1) != 0;
+  ensure_iter_buffers(method, std::max(cap, 1), ring);
   if (prm->d_hat) {
     dhat_.reserve(sizeof(double) * N_);
     h2d(dhat_.p, prm->d_hat, sizeof(double) * N_, stream_);
@@ -1376,6 +1391,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   // one-phase-ahead L2 prefetch of the slice streams (prefetch_slice_streams):
   // measured a loss on configs[1] (17.2k vs 18.6k it/s), opt-in experiment
   P.phase_prefetch = env_int("AAPDHG_PREFETCH", 0);
+  P.ring = ring ? 1 : 0;
   const bool blk1 = !serial && ktb_.nb() > 1, blk2 = !serial && kb_.nb() > 1;
   const CsrDev& K1m = blk1 ? ktb_.blk.back() : KTm(serial);
   const CsrDev& K2m = blk2 ? kb_.blk.back() : Km(serial);
@@ -1407,6 +1423,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   su.S = S;
   su.serial = serial;
   su.push = method != AAPDHG_METHOD_PDHG;
+  su.ring = ring;
   su.method = method;
   su.cap = cap;
   su.nblk1 = K1m.grid();
@@ -1495,8 +1512,8 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
   }
   if (use_graph) {
     char key[256];
-    std::snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p", method,
-                  int(serial), cap, int(su.persist), int(su.split), upool_.p, du_.p, partdot_.p, dparams_.p,
+    std::snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%d/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p", method,
+                  int(serial), cap, int(su.persist), int(su.split), int(su.ring), upool_.p, gpool_.p, dg_.p, du_.p, partdot_.p, dparams_.p,
                   rec_.p, stream_, gridbar_.p, (const void*)su.pk1.sl_start, (void*)su.bal,
                   su.B.part1, su.B.part2);
     if (graph_key_ != key || !graph_exec_) {
@@ -1515,7 +1532,7 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
 
   // start iterate P(u0) in slot 0, its K x cached in kx slot 0; fresh pools
   AAPDHG_CUDA(cudaMemsetAsync(upool_.p, 0, sizeof(double) * 4 * N_, stream_));
-  if (method != AAPDHG_METHOD_PDHG) {
+  if (method != AAPDHG_METHOD_PDHG && !ring) {  // (the ring's slots are written before read)
     AAPDHG_CUDA(cudaMemsetAsync(gpool_.p, 0, sizeof(double) * 2 * N_, stream_));
   }
   if (su.persist) AAPDHG_CUDA(cudaMemsetAsync(gridbar_.p, 0, sizeof(GridBar), stream_));

@@ -233,7 +233,7 @@ class Problem {
   const CsrDev& sh_k1m() const { return ktb_.nb() > 1 ? ktb_.blk.back() : KTt_; }
   const CsrDev& sh_k2m() const { return kb_.nb() > 1 ? kb_.blk.back() : Kt_; }
   const CsrDev& KTm(bool serial) const { return serial ? KTs_ : KTt_; }
-  void ensure_iter_buffers(int method, int cap);
+  void ensure_iter_buffers(int method, int cap, bool ring = false);
   double* faa_part_lo(int method, int cap) const;
   void upload_iterate(int slot, const double* x, const double* y);
   IterBufs iter_bufs();

@@ -139,6 +139,45 @@ __device__ __forceinline__ void state_store(DevState* g, const DevState* sm) {
   for (int i = threadIdx.x; i < W; i += blockDim.x) d[i] = s[i];
 }
 
+// Ring history (DevParams::ring; AA-PDHG on one GPU). Every iteration k
+// stores g_k = T(u_k) - u_k (the K1 / K2 epilogues, both halves) into ring
+// slot push_slot instead of pushing the pair (du_k, dg_k) (solver.cpp:
+// 204-209): with the window gw[0..p] = slots of g_{k-p}..g_k, column t of
+// the memory is dg_t = g_t - g_{t-1} and du_t = u_t - u_{t-1}, which is
+// g_{t-1} bit for bit after a plain step (u_t = T(u_{t-1})) and is stored by
+// k_mix (in du, at g_t's slot) after an accepted candidate — the same
+// roundings as the pushed pair. A plain iteration writes 8 bytes per element
+// instead of reading u_{k-1} and writing 16. cap + 2 slots: the window holds
+// up to cap + 1, and the speculative K1(k+1) of k_plain_loop writes the next
+// one before iteration k is decided. The next slot: the first one outside
+// the window.
+__device__ __forceinline__ int ring_free_slot(const DevParams* P, const DevState* S) {
+  int slot = 0;
+  for (; slot < P->cap + 1; ++slot) {
+    bool used = false;
+    for (int q = 0; q < S->gw_n; ++q) used |= S->gw[q] == slot;
+    if (!used) break;
+  }
+  return slot;
+}
+
+// memory_push of the ring (control_commit): g_k's slot joins the window, the
+// oldest leaves a full one (cap + 1 entries = cap columns)
+__device__ __forceinline__ void ring_push(const DevParams* P, DevState* S) {
+  int n = S->gw_n;
+  if (n == P->cap + 1) {
+    for (int q = 1; q < n; ++q) {
+      S->gw[q - 1] = S->gw[q];
+      S->gdux[q - 1] = S->gdux[q];
+    }
+    --n;
+  }
+  S->gw[n] = S->push_slot;
+  S->gdux[n] = S->prev_plain ? 0 : 1;
+  S->gw_n = n + 1;
+  S->mem_size = n;
+}
+
 // Role rotation at the end of an iteration (solver.cpp:249-251) and the
 // next push slot: u_prev <- u, u <- u_next (the AA candidate or T(u)).
 __device__ __forceinline__ void advance(const DevParams* P, DevState* S) {
@@ -158,7 +197,9 @@ __device__ __forceinline__ void advance(const DevParams* P, DevState* S) {
     KX[KX_CUR] = KX[KX_HAT];
     KX[KX_HAT] = okx;
   }
-  if (P->method != AAPDHG_METHOD_PDHG) {
+  if (P->ring) {
+    S->push_slot = ring_free_slot(P, S);
+  } else if (P->method != AAPDHG_METHOD_PDHG) {
     const int t = S->g_idx[G_CUR];
     S->g_idx[G_CUR] = S->g_idx[G_PREV];
     S->g_idx[G_PREV] = t;
@@ -614,8 +655,9 @@ __device__ __noinline__ Decision control_decide(const DevParams* P, DevState* S,
 __device__ __noinline__ void control_commit(const DevParams* P, DevState* S, uint64_t k,
                                                Decision d) {
   if (S->done) return;
+  if (P->ring) ring_push(P, S);  // (g_0 opens the window at k = 0)
   if (k > 0) {
-    if (P->method != AAPDHG_METHOD_PDHG) {  // memory_push / FaaState::push
+    if (P->method != AAPDHG_METHOD_PDHG && !P->ring) {  // memory_push / FaaState::push
       if (S->mem_size == P->cap) {
         for (int t = 1; t < S->mem_size; ++t) S->mem_slots[t - 1] = S->mem_slots[t];
         S->mem_slots[S->mem_size - 1] = S->push_slot;
@@ -890,7 +932,9 @@ __device__ __forceinline__ void dual_epilogue(int j, double t, const double* __r
   acc[P1_BOUND] = bt;
   acc[P1_DUALSQ] = __dmul_rn(dv, dv);
   acc[P1_CX] = __dmul_rn(cj, xj);
-  if constexpr (PUSH) {
+  if (PUSH && P->ring) {  // ring history: g_k only
+    B.gpool[(int64_t)S->push_slot * N + j] = d;
+  } else if constexpr (PUSH) {
     // after a plain step u_k = T(u_{k-1}) bit for bit, so g_{k-1} = u_k -
     // u_{k-1} = du: g is only materialized (k_stage_g) for AA attempts
     const int64_t slot = S->push_slot;
@@ -919,7 +963,7 @@ __device__ __forceinline__ void dual_side_rows(const CsrDev& KT, const IterBufs&
           l2_prefetch(B.c + r);
           l2_prefetch(B.l + r);
           l2_prefetch(B.u + r);
-          if constexpr (PUSH) l2_prefetch(B.upool + (int64_t)S->u_idx[U_PREV] * N + r);
+          if (PUSH && !P->ring) l2_prefetch(B.upool + (int64_t)S->u_idx[U_PREV] * N + r);
         }, bid, rep);
     if (j == -2) break;
     if (B.rinit1 && j >= 0) t = __dadd_rn(B.rinit1[j], t);  // earlier column passes
@@ -1024,7 +1068,9 @@ __device__ __forceinline__ void primal_epilogue(int i, double s, const IterBufs&
   acc[P2_GY2] = __dmul_rn(d, d);
   acc[P2_QY] = __dmul_rn(qi, yi);
   acc[P2_INFEAS] = __dmul_rn(v, v);
-  if constexpr (PUSH) {
+  if (PUSH && P->ring) {  // ring history: g_k only
+    B.gpool[(int64_t)S->push_slot * N + n + i] = d;
+  } else if constexpr (PUSH) {
     const int64_t slot = S->push_slot;
     const double yp = B.upool[(int64_t)S->u_idx[U_PREV] * N + n + i];
     const double dy = __dsub_rn(yi, yp);
