@@ -113,9 +113,10 @@ def test_bench_iteration_bytes_and_workload_selection():
     p = problems.make_config(1, 0.05)
     n, m, nnz = p.n(), p.k.nrows, p.k.nnz
     plain = bench.kernel_bytes(p, "k_plain_loop")
-    assert plain == (12 * nnz + 4 * (n + 1) + 8 * m + 80 * n) + (12 * nnz + 4 * (m + 1) + 8 * n + 80 * m)
+    # (the ring history: g_k stored, 8 bytes per element and iteration)
+    assert plain == (12 * nnz + 4 * (n + 1) + 8 * m + 48 * n) + (12 * nnz + 4 * (m + 1) + 8 * n + 48 * m)
     N = n + m
-    aa = 8 * N * 13 + 8 * N * 23 + 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
+    aa = 8 * N * 11 + 8 * N * 14 + 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
     assert bench.iteration_bytes(p, 20, 3) == 20 * plain + 3 * aa
     # configs[4] at every N (BENCH and the scaling curve share the LP)
     args = argparse.Namespace(workload="config4", loopback=0)
