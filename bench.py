@@ -166,9 +166,9 @@ def measured_peak():
 def ncu_traffic(kernel):
     """dram bytes per launch of `kernel` (per iteration for k_plain_loop and
     for configs[4]'s "config4_iteration") from the committed ncu --set full
-    captures (profiles/r02b/traffic.json, made by profiles/make_traffic.py;
-    profiles/r02/traffic.json for the kernels not re-captured), or None."""
-    for rel in ("r02b", "r02"):
+    captures (profiles/r02d/traffic.json, made by profiles/make_traffic.py;
+    the earlier rounds' files for the kernels not re-captured), or None."""
+    for rel in ("r02d", "r02b", "r02"):
         try:
             d = json.loads((ROOT / "profiles" / rel / "traffic.json").read_text())[kernel]
         except Exception:
@@ -543,7 +543,7 @@ def iteration_roofline(p, iters, aa_steps, ms, eager):
             "achieved": ach, "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
             "frac": ach / peak, "traffic": ncu_traffic("config4_iteration"),
             "traffic_source": "ncu --set full of one plain iteration's kernels, dram bytes "
-                              "(profiles/r02b/traffic.json): per plain iteration, against "
+                              "(profiles/r02d/traffic.json): per plain iteration, against "
                               "bytes_per_plain_iteration",
             "bytes": byts, "bytes_per_plain_iteration": kernel_bytes(p, "k_plain_loop"),
             "timing": "CUDA events on the solver stream around the timed solve",
@@ -652,7 +652,7 @@ def plain_loop_roofline(args, p, plain, step_ms):
             "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
             "traffic": (t_it * iters / launches) if (t_it and args.traffic is None)
             else args.traffic,
-            "traffic_source": "ncu --set full of one k_plain_loop launch (profiles/r02b/"
+            "traffic_source": "ncu --set full of one k_plain_loop launch (profiles/r02d/"
                               "traffic.json), dram bytes per iteration x iterations per launch",
             "bytes_per_launch": per_it * iters / launches,
             "bytes_per_iteration": per_it,

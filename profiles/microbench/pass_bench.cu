@@ -317,6 +317,150 @@ __global__ void __launch_bounds__(256, MB) passw2(Sell A, const int* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Variant 300+: TMA-staged pass. One wave of persistent CTAs; CTA b owns the
+// contiguous chunks [b * cpc, (b + 1) * cpc), a chunk = CW consecutive slices
+// (one per consumer warp). A producer lane (warp CW) bulk-copies each chunk's
+// slice pointers, lane metadata (sl_row, sl_cnt) and (column, value) streams
+// into a shared-memory stage (cp.async.bulk + mbarrier, STAGES deep), so a
+// consumer warp's dependent chain is smem -> gather (L2) -> partial (loaded
+// before the gathers) instead of metadata -> stream -> gather -> partial from
+// DRAM, and no stream element lives in a register: 8 gathers in flight.
+// Same per-row operation order as pass<> (bitwise equal partials).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tLAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT;\n\t}" ::"r"(smem_u32(b)), "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+template <int CW, int EC>
+struct StageLayout {
+  static constexpr int kPtr = 0;                       // CW + 1 int64 (padded to 16 B units)
+  static constexpr int kPtrB = ((CW + 1) * 8 + 127) / 128 * 128;
+  static constexpr int kRow = kPtrB;                   // CW x 32 int
+  static constexpr int kCnt = kRow + CW * 128;
+  static constexpr int kCi = kCnt + CW * 128;          // EC int
+  static constexpr int kV = kCi + 4 * EC;              // EC double
+  static constexpr int kBytes = kV + 8 * EC;
+};
+
+template <int STAGES, int CW, int EC, int MB>
+__global__ void __launch_bounds__(32 * (CW + 1), MB)
+    pass_tma(Sell A, const double* __restrict__ x, double* __restrict__ part, int first, int cpc) {
+  using SL = StageLayout<CW, EC>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nchunks = (A.nslices + CW - 1) / CW;
+  const int q0 = blockIdx.x * cpc, q1 = min(nchunks, q0 + cpc);
+  if (threadIdx.x == 0)
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CW);
+    }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (warp == CW) {  // producer
+    if (lane != 0 || q0 >= q1) return;
+    int64_t pa = __ldg(A.sl_ptr + min(A.nslices, q0 * CW));
+    int64_t pb = __ldg(A.sl_ptr + min(A.nslices, (q0 + 1) * CW));
+    for (int q = q0; q < q1; ++q) {
+      const int64_t pc = __ldg(A.sl_ptr + min(A.nslices, (q + 2) * CW));  // (used next round)
+      const int it = q - q0, s = it % STAGES;
+      if (it >= STAGES) mbar_wait(&empty[s], unsigned((it / STAGES - 1) & 1));
+      unsigned char* st = smem + size_t(s) * SL::kBytes;
+      const unsigned E = unsigned(pb - pa);
+      constexpr unsigned kPtrCopy = ((CW + 1) * 8 + 15) / 16 * 16;
+      mbar_expect_tx(&full[s], kPtrCopy + 2u * CW * 128u + 12u * E);
+      bulk_g2s(st + SL::kPtr, A.sl_ptr + q * CW, kPtrCopy, &full[s]);
+      bulk_g2s(st + SL::kRow, A.sl_row + size_t(q) * CW * 32, CW * 128u, &full[s]);
+      bulk_g2s(st + SL::kCnt, A.sl_cnt + size_t(q) * CW * 32, CW * 128u, &full[s]);
+      if (E) {
+        bulk_g2s(st + SL::kCi, A.sci + pa, 4u * E, &full[s]);
+        bulk_g2s(st + SL::kV, A.sv + pa, 8u * E, &full[s]);
+      }
+      pa = pb;
+      pb = pc;
+    }
+    return;
+  }
+  for (int q = q0; q < q1; ++q) {
+    const int it = q - q0, s = it % STAGES;
+    mbar_wait(&full[s], unsigned((it / STAGES) & 1));
+    const unsigned char* st = smem + size_t(s) * SL::kBytes;
+    const int64_t* sp = reinterpret_cast<const int64_t*>(st + SL::kPtr);
+    const int sl = q * CW + warp;
+    if (sl < A.nslices) {
+      const int off = int(sp[warp] - sp[0]);
+      const int L = int(sp[warp + 1] - sp[warp]) >> 5;
+      const int row = reinterpret_cast<const int*>(st + SL::kRow)[warp * 32 + lane];
+      const int cnt = reinterpret_cast<const int*>(st + SL::kCnt)[warp * 32 + lane];
+      double prev = 0.0;
+      if (!first && row >= 0) prev = __ldcs(part + row);
+      const int* cc = reinterpret_cast<const int*>(st + SL::kCi) + off + lane;
+      const double* vv = reinterpret_cast<const double*>(st + SL::kV) + off + lane;
+      double acc = 0.0;
+      for (int t0 = 0; t0 < L; t0 += 8) {
+        double g[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) g[u] = t0 + u < cnt ? __ldg(x + cc[32 * (t0 + u)]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (t0 + u < cnt) acc = __dadd_rn(acc, __dmul_rn(vv[32 * (t0 + u)], g[u]));
+      }
+      if (row >= 0) __stcs(part + row, first ? acc : __dadd_rn(prev, acc));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+template <int STAGES, int CW, int EC, int MB>
+void launch_tma(const Sell& A, const double* x, double* part, int first, cudaStream_t st) {
+  using SL = StageLayout<CW, EC>;
+  static bool once = false;
+  const int bytes = STAGES * SL::kBytes;
+  if (!once) {
+    CK(cudaFuncSetAttribute(pass_tma<STAGES, CW, EC, MB>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(pass_tma<STAGES, CW, EC, MB>,
+                            cudaFuncAttributePreferredSharedMemoryCarveout,
+                            cudaSharedmemCarveoutMaxShared));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_tma<STAGES, CW, EC, MB>,
+                                                     32 * (CW + 1), bytes));
+    printf("pass_tma<%d,%d,%d,%d>: %d bytes smem, %d CTAs/SM resident\n", STAGES, CW, EC, MB,
+           bytes, occ);
+    once = true;
+  }
+  const int grid = 148 * MB;
+  const int nchunks = (A.nslices + CW - 1) / CW;
+  const int cpc = (nchunks + grid - 1) / grid;
+  pass_tma<STAGES, CW, EC, MB><<<grid, 32 * (CW + 1), bytes, st>>>(A, x, part, first, cpc);
+}
+
 int main(int argc, char** argv) {
   const int rows = 20000000;
   const int win = 256;
@@ -332,8 +476,8 @@ int main(int argc, char** argv) {
     for (int i = 0; i < w1 - w0; ++i) rowid[w0 + i] = idx[i];
   }
   const int ns = (rows + 31) / 32;
-  std::vector<int64_t> sl_ptr(ns);
-  std::vector<int> sl_len(ns), sl_row(size_t(ns) * 32, -1), sl_cnt(size_t(ns) * 32, 0);
+  std::vector<int64_t> sl_ptr(ns + 32);
+  std::vector<int> sl_len(ns), sl_row(size_t(ns + 32) * 32, -1), sl_cnt(size_t(ns + 32) * 32, 0);
   int64_t tot = 0;
   for (int s = 0; s < ns; ++s) {
     int L = 0;
@@ -348,25 +492,31 @@ int main(int argc, char** argv) {
     sl_len[s] = L;
     tot += 32LL * L;
   }
+  for (int s = ns; s < ns + 32; ++s) sl_ptr[s] = tot;
   printf("slices %d, stored entries %lld (nnz ~%lld)\n", ns, (long long)tot, 4LL * rows);
   std::vector<int> sci(tot);
-  std::vector<double> sv(tot, 1.0);
+  std::vector<double> sv(tot);
+  for (int64_t e = 0; e < tot; ++e) sv[e] = double(int(rnd() % 2001) - 1000) / 512.0;
   int *d_sl_len, *d_sl_row, *d_sl_cnt, *d_sci;
   int64_t* d_sl_ptr;
   double *d_sv, *x, *part;
-  CK(cudaMalloc(&d_sl_ptr, ns * 8));
+  CK(cudaMalloc(&d_sl_ptr, (ns + 32) * 8));
   CK(cudaMalloc(&d_sl_len, ns * 4));
-  CK(cudaMalloc(&d_sl_row, size_t(ns) * 128));
-  CK(cudaMalloc(&d_sl_cnt, size_t(ns) * 128));
-  CK(cudaMalloc(&d_sci, tot * 4));
-  CK(cudaMalloc(&d_sv, tot * 8));
+  CK(cudaMalloc(&d_sl_row, size_t(ns + 32) * 128));
+  CK(cudaMalloc(&d_sl_cnt, size_t(ns + 32) * 128));
+  CK(cudaMalloc(&d_sci, tot * 4 + 4096));
+  CK(cudaMalloc(&d_sv, tot * 8 + 4096));
   CK(cudaMalloc(&x, 128LL << 20));
   CK(cudaMalloc(&part, size_t(rows) * 8));
-  CK(cudaMemset(x, 0, 128LL << 20));
-  CK(cudaMemcpy(d_sl_ptr, sl_ptr.data(), ns * 8, cudaMemcpyHostToDevice));
+  {
+    std::vector<double> hx((128LL << 20) / 8);
+    for (auto& v : hx) v = double(int(rnd() % 2001) - 1000) / 1024.0;
+    CK(cudaMemcpy(x, hx.data(), 128LL << 20, cudaMemcpyHostToDevice));
+  }
+  CK(cudaMemcpy(d_sl_ptr, sl_ptr.data(), (ns + 32) * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d_sl_len, sl_len.data(), ns * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_sl_row, sl_row.data(), size_t(ns) * 128, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_sl_cnt, sl_cnt.data(), size_t(ns) * 128, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_sl_row, sl_row.data(), size_t(ns + 32) * 128, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_sl_cnt, sl_cnt.data(), size_t(ns + 32) * 128, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d_sv, sv.data(), tot * 8, cudaMemcpyHostToDevice));
   std::vector<int> meta(size_t(ns) * 32, -1);
   for (size_t i = 0; i < meta.size(); ++i)
@@ -384,8 +534,11 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
-  const int variants[] = {1, 65, 81, 67, 83};
-  for (int mb : {48, 64, 80}) {
+  std::vector<int> variants;
+  for (int i = 1; i < argc; ++i) variants.push_back(atoi(argv[i]));
+  if (variants.empty()) variants = {1, 300, 301, 302, 303, 304, 305};
+  std::vector<double> ref(rows), got(rows);
+  for (int mb : {40, 48, 64, 80}) {
     const int64_t nx = (int64_t(mb) << 20) / 8;
     for (int64_t e = 0; e < tot; ++e) sci[e] = int(rnd() % nx);
     CK(cudaMemcpy(d_sci, sci.data(), tot * 4, cudaMemcpyHostToDevice));
@@ -422,6 +575,12 @@ int main(int argc, char** argv) {
           case 104: launch2<2, 6, 5>(A, x, part, r == 0, s0); break;
           case 105: launch2<3, 6, 4>(A, x, part, r == 0, s0); break;
           case 1: launch<1>(A, x, part, r == 0, s0); break;
+          case 300: launch_tma<2, 8, 2048, 4>(A, x, part, r == 0, s0); break;
+          case 301: launch_tma<3, 8, 2048, 2>(A, x, part, r == 0, s0); break;
+          case 302: launch_tma<2, 16, 4096, 2>(A, x, part, r == 0, s0); break;
+          case 303: launch_tma<4, 8, 2048, 2>(A, x, part, r == 0, s0); break;
+          case 304: launch_tma<3, 16, 4096, 1>(A, x, part, r == 0, s0); break;
+          case 305: launch_tma<2, 8, 2048, 3>(A, x, part, r == 0, s0); break;
           case 3: launch<3>(A, x, part, r == 0, s0); break;
           case 5: launch<1>(A, x, part, r == 0, s0); break;
           case 7: launch<3>(A, x, part, r == 0, s0); break;
@@ -450,8 +609,14 @@ int main(int argc, char** argv) {
         CK(cudaCtxResetPersistingL2Cache());
         CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
       }
-      printf("block %3d MB variant %2d: %8.1f us  %.1f G gathers/s\n", mb, V, best * 1e3,
-             4.0 * rows / (best * 1e-3) / 1e9);
+      // 1 first pass + 4 accumulating passes: the partials must equal variant 1's bit for bit
+      CK(cudaMemcpy(got.data(), part, size_t(rows) * 8, cudaMemcpyDeviceToHost));
+      size_t bad = 0;
+      if (V == 1) ref = got;
+      else if (variants[0] == 1)
+        for (int r = 0; r < rows; ++r) bad += ref[r] != got[r];
+      printf("block %3d MB variant %2d: %8.1f us  %.1f G gathers/s  mismatches %zu\n", mb, V,
+             best * 1e3, 4.0 * rows / (best * 1e-3) / 1e9, bad);
     }
   }
   return 0;
