@@ -942,6 +942,8 @@ __global__ void __launch_bounds__(1024)
   TL_MARK(23);
 }
 
+constexpr int kMixGroup = 4;  // k_mix: history columns whose loads are in flight together
+
 // cand = P_feasible(u + damp(g) - sum_j w_j (du_j + damp(dg_j)))
 // (anderson.cpp:109,130-133 / filtering.cpp:165,176-179; solver.cpp:226)
 __global__ void __launch_bounds__(kThreads)
@@ -983,13 +985,33 @@ __global__ void __launch_bounds__(kThreads)
       const double ut = u[t];
       double o = __dadd_rn(ut, damp1(beta, dh, t, gk));
       double gp = B.gpool[gsl[0] + t];
-      for (int jj = 0; jj < pm; ++jj) {
-        const double a = nw[jj];
-        const double gc = jj + 1 == pm ? gk : B.gpool[gsl[jj + 1] + t];
-        const double du = gx[jj + 1] ? B.du[gsl[jj + 1] + t] : gp;
-        o = __dadd_rn(o, __dmul_rn(a, du));
-        o = __dadd_rn(o, __dmul_rn(a, damp1(beta, dh, t, __dsub_rn(gc, gp))));
-        gp = gc;
+      // columns in groups of kMixGroup: the group's loads are all issued
+      // before its (ordered) adds, so a thread keeps up to 2 kMixGroup loads
+      // in flight instead of one (same operations in the same order)
+      for (int j0 = 0; j0 < pm; j0 += kMixGroup) {
+        double gc[kMixGroup], dv[kMixGroup];
+#pragma unroll
+        for (int q = 0; q < kMixGroup; ++q) {
+          const int jj = j0 + q;
+          gc[q] = 0.0;
+          dv[q] = 0.0;
+          if (jj < pm) {
+            if (jj + 1 < pm) gc[q] = B.gpool[gsl[jj + 1] + t];
+            if (gx[jj + 1]) dv[q] = B.du[gsl[jj + 1] + t];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kMixGroup; ++q) {
+          const int jj = j0 + q;
+          if (jj < pm) {
+            const double a = nw[jj];
+            const double gcq = jj + 1 == pm ? gk : gc[q];
+            const double du = gx[jj + 1] ? dv[q] : gp;
+            o = __dadd_rn(o, __dmul_rn(a, du));
+            o = __dadd_rn(o, __dmul_rn(a, damp1(beta, dh, t, __dsub_rn(gcq, gp))));
+            gp = gcq;
+          }
+        }
       }
       if (project) {
         if (t < n) o = smin(smax(o, B.l[t]), B.u[t]);
@@ -1003,11 +1025,23 @@ __global__ void __launch_bounds__(kThreads)
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N;
        t += (int64_t)gridDim.x * blockDim.x) {
     double o = __dadd_rn(u[t], damp1(beta, dh, t, g[t]));
-    for (int jj = 0; jj < pm; ++jj) {
-      const int64_t sl = sls[jj];
-      const double a = nw[jj];
-      o = __dadd_rn(o, __dmul_rn(a, B.du[sl * N + t]));
-      o = __dadd_rn(o, __dmul_rn(a, damp1(beta, dh, t, dg[sl * N + t])));
+    for (int j0 = 0; j0 < pm; j0 += kMixGroup) {  // (grouped loads, as above)
+      double uv[kMixGroup], gv[kMixGroup];
+#pragma unroll
+      for (int q = 0; q < kMixGroup; ++q) {
+        const int jj = j0 + q;
+        uv[q] = jj < pm ? B.du[sls[jj] * N + t] : 0.0;
+        gv[q] = jj < pm ? dg[sls[jj] * N + t] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kMixGroup; ++q) {
+        const int jj = j0 + q;
+        if (jj < pm) {
+          const double a = nw[jj];
+          o = __dadd_rn(o, __dmul_rn(a, uv[q]));
+          o = __dadd_rn(o, __dmul_rn(a, damp1(beta, dh, t, gv[q])));
+        }
+      }
     }
     if (project) {
       if (t < n) o = smin(smax(o, B.l[t]), B.u[t]);
