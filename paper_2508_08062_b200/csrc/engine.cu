@@ -1674,13 +1674,22 @@ void Problem::solve(const aapdhg_solve_params* prm, const double* x0, const doub
     }
     if (lam_out && n_ > 0) {
       T_.reserve(sizeof(double) * std::max<int64_t>(n_, 1));
-      if (m_ > 0) {
+      // L2-blocked split iteration: the last evaluation's K' passes left the
+      // finished K'y of its CUR iterate — this final iterate — in the row
+      // partials (launch_core: every block a pass; nothing after the stop
+      // writes them: the AA recache runs K's passes), the same sums in the
+      // same block order spmv_any would form again (AAPDHG_LAMBDA_REUSE=0)
+      const bool reuse = m_ > 0 && su.split && ktb_.nb() > 1 &&
+                         env_int("AAPDHG_LAMBDA_REUSE", 1) != 0;
+      const double* kty = reuse ? ktb_.partial.as<double>() : T_.as<double>();
+      if (reuse) {
+      } else if (m_ > 0) {
         spmv_any(stream_, true, vref(ufin + n_), rout(T_.as<double>()), false, nullptr, nullptr);
       } else {
         AAPDHG_CUDA(cudaMemsetAsync(T_.p, 0, sizeof(double) * n_, stream_));
       }
       k_lambda_from_T<<<grid_for(n_), kThreads, 0, stream_>>>(
-          T_.as<double>(), c_.as<double>(), l_.as<double>(), u_.as<double>(), n_,
+          kty, c_.as<double>(), l_.as<double>(), u_.as<double>(), n_,
           lam_.as<double>());
       AAPDHG_CUDA(cudaGetLastError());
     }

@@ -495,6 +495,38 @@ def test_l2_column_blocking_matches_unblocked(monkeypatch):
     assert np.linalg.norm(x - xr) <= 1e-9 * np.linalg.norm(xr)
 
 
+@pytest.mark.parametrize("stop", ["max_iters", "residual"])
+def test_l2_blocked_final_lambda_reuses_the_last_pass_sums(monkeypatch, stop):
+    """L2-blocked split iteration: the final lambda = P_Lambda(c - K'y) comes
+    from the row partials the last evaluation's K' passes left (engine.cu
+    fast finish) instead of two more passes over K'. Bit-identical to the
+    recomputed lambda (AAPDHG_LAMBDA_REUSE=0), with an AA step inside the
+    solve (its recache runs K's passes) and for both kinds of stop."""
+    p = problems.make_config(1, scale=0.05)
+    cfg = SolverConfig(method=Method.AA_PDHG, m=10, toll=1e-9, max_iters=40, tau=0.08,
+                       sigma=0.08, reduction="tree")
+    monkeypatch.setenv("AAPDHG_L2_BLOCK_MIN_KB", "0")
+    monkeypatch.setenv("AAPDHG_L2_BLOCK_KB", "16")
+    monkeypatch.setenv("AAPDHG_LAMBDA_REUSE", "0")
+    if stop == "residual":  # a tolerance the residual first meets around iteration 30
+        with Solver(p) as s:
+            g = s.solve(cfg).trajectory["g_norm"]
+        cfg = SolverConfig(method=Method.AA_PDHG, m=10, toll=float(g[1:31].min()) * (1 + 1e-9),
+                           max_iters=40, tau=0.08, sigma=0.08, reduction="tree")
+    with Solver(p) as s:
+        ref = s.solve(cfg)
+    monkeypatch.setenv("AAPDHG_LAMBDA_REUSE", "1")
+    with Solver(p) as s:
+        got = s.solve(cfg)
+    assert got.result.status == ref.result.status
+    assert got.result.iterations == ref.result.iterations
+    assert (got.result.iterations < 40) == (stop == "residual")
+    assert stop == "residual" or got.result.i >= 1
+    assert np.array_equal(got.result.u.x, ref.result.u.x)
+    assert np.array_equal(got.result.lambda_, ref.result.lambda_)
+    assert np.any(got.result.lambda_ != 0.0)
+
+
 @pytest.mark.parametrize("reduction", ["serial", "tree"])
 def test_interleaved_short_row_layout(port, monkeypatch, reduction):
     """Very short rows in more slices than two waves of warps get the
