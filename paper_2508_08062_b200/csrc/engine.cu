@@ -373,7 +373,7 @@ int Problem::launch_blocked_passes(cudaStream_t s, const Blocked& bk, const VecR
   for (int b = 0; b + (all ? 0 : 1) < bk.nb(); ++b) {
     prof_begin(s, "k_spmv_pass");
     k_spmv_pass<<<bk.blk[b].grid(), kThreads, 0, s>>>(bk.blk[b], x, bk.partial.as<double>(),
-                                                     b == 0 ? 1 : 0, S, pred_aa, stop);
+                                                     b == 0 ? 1 : pass_prefetch_, S, pred_aa, stop);
     prof_end(s);
     AAPDHG_CUDA(cudaGetLastError());
     ++nodes;
@@ -552,6 +552,8 @@ void Problem::init_device(int device) {
   AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_out_done_, cudaEventDisableTiming));
   for (auto& e : ev_blk_) AAPDHG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   pdl_ = env_int("AAPDHG_PDL", 1) != 0;
+  pass_prefetch_ = env_int("AAPDHG_PASS_PREFETCH", 0);  // 0, 2 (L2 prefetch) or 3 (register)
+  if (pass_prefetch_ != 2 && pass_prefetch_ != 3) pass_prefetch_ = 0;
 }
 
 // c, q, l, u on the device plus the scratch of power iteration / per-op /
@@ -1024,7 +1026,7 @@ int Problem::launch_core(cudaStream_t s, const SolveSetup& su) {
         prof_begin(side_, "k_spmv_pass");
         k_spmv_pass<<<kb_.blk[b].grid(), kThreads, 0, side_>>>(
             kb_.blk[b], VecRef{nullptr, su.B.upool, U_HAT, N_, 0}, kb_.partial.as<double>(),
-            b == 0 ? 1 : 0, su.S, 0, nullptr);
+            b == 0 ? 1 : pass_prefetch_, su.S, 0, nullptr);
         prof_end(side_);
         AAPDHG_CUDA(cudaGetLastError());
         ++nodes;

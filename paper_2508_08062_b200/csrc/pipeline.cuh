@@ -334,7 +334,7 @@ __device__ __forceinline__ void slice_partials(const CsrDev& A, int b, double (&
 // rep: the warp's rep-th slice of an interleaved layout (returns -2 when the
 // warp has no more); otherwise only rep 0 exists.
 template <bool SERIAL, int UNROLL = kUnroll, bool COH = false, bool BAL = true,
-          class Pre = NoPre>
+          class Pre = NoPre, bool PRE_ALL = false>
 __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict__ x, double& s,
                                        Pre pre = Pre{}, int bid = -1, int rep = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -359,7 +359,7 @@ __device__ __forceinline__ int row_sum(const CsrDev& A, const double* __restrict
     const int64_t sbase = __ldg(A.sl_ptr + sl);
     const int row = __ldg(A.sl_row + sl * 32 + lane);
     const int cnt = __ldg(A.sl_cnt + sl * 32 + lane);  // this lane's elements
-    if (L <= UNROLL && row >= 0 && j == 0) pre(row);
+    if ((PRE_ALL || L <= UNROLL) && row >= 0 && j == 0) pre(row);
     const int64_t base = sbase + lane;
     const int32_t* __restrict__ cp = A.sci + base;
     const double* __restrict__ vp = A.sv + base;
@@ -892,9 +892,18 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
   const double* x = xr.get(S);
   for (int rep = 0;; ++rep) {
     double s;
-    const int row = row_sum<false, kUnroll, false, false>(A, x, s, NoPre{}, -1, rep);
+    // later passes (first = 0): mode 2 asks the row's partial into L2 with the
+    // metadata, mode 3 loads it into a register there, so the read-add-store
+    // after the gather chain does not wait for a DRAM round trip
+    double prev = 0.0;
+    auto pre = [&](int r) {
+      if (first == 2) l2_prefetch(part + r);
+      else if (first == 3) prev = __ldcs(part + r);
+    };
+    const int row = row_sum<false, kUnroll, false, false, decltype(pre), true>(A, x, s, pre, -1, rep);
     if (row == -2) break;
-    if (row >= 0) __stcs(part + row, first ? s : __dadd_rn(__ldcs(part + row), s));
+    if (row >= 0)
+      __stcs(part + row, first == 1 ? s : __dadd_rn(first == 3 ? prev : __ldcs(part + row), s));
   }
 }
 

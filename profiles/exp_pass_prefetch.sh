@@ -1,9 +1,16 @@
+# A/B of AAPDHG_PASS_PREFETCH (0 off, 2 L2 prefetch, 3 register preload of a later pass's row
+# partial) on configs[4]: per-iteration device timestamps of the bench's solves (exp_cfg4_iters.py)
 mkdir -p gpurun_out/r02d
-python -c "import sys; sys.path.insert(0,'.'); from paper_2508_08062_b200 import problems; problems.cached_config(4)"
-for rep in 1 2; do
-for pf in 0 1; do
-for blk in "81920 81920" "81920 55000" "65536 55000" "49152 40960" "40960 40960"; do
-set -- $blk
-echo "PASS_PREFETCH=$pf K=$1 KT=$2" 
-AAPDHG_PASS_PREFETCH=$pf AAPDHG_L2_BLOCK_KB_K=$1 AAPDHG_L2_BLOCK_KB_KT=$2 python profiles/exp_cfg4_l2.py 81920,0
-done; done; done > gpurun_out/r02d/pass_prefetch.txt 2>&1
+for rep in 1 2; do for pf in 0 2 3; do
+  echo "=== AAPDHG_PASS_PREFETCH=$pf (rep $rep)"
+  AAPDHG_PASS_PREFETCH=$pf python profiles/exp_cfg4_iters.py 2>/dev/null | python -c "
+import sys, statistics
+plain = []; 
+for l in sys.stdin:
+    if l.startswith('---'): print(l.strip())
+    elif ' aa=0 ' in l and '+' in l:
+        k = int(l.split('k=')[1].split()[0]); d = float(l.rsplit('+', 1)[1])
+        if k >= 2: plain.append(d)
+print('plain iterations: median %.3f ms, min %.3f, n %d' % (statistics.median(plain), min(plain), len(plain)))
+"
+done; done > gpurun_out/r02d/pass_prefetch2.txt 2>&1
