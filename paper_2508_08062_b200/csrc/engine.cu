@@ -552,7 +552,9 @@ void Problem::init_device(int device) {
   AAPDHG_CUDA(cudaEventCreateWithFlags(&ev_out_done_, cudaEventDisableTiming));
   for (auto& e : ev_blk_) AAPDHG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   pdl_ = env_int("AAPDHG_PDL", 1) != 0;
-  pass_prefetch_ = env_int("AAPDHG_PASS_PREFETCH", 0);  // 0, 2 (L2 prefetch) or 3 (register)
+  // later column passes fetch their row partial with the metadata: 3 = into a
+  // register (default), 2 = an L2 prefetch, 0 = after the gather chain
+  pass_prefetch_ = env_int("AAPDHG_PASS_PREFETCH", 3);
   if (pass_prefetch_ != 2 && pass_prefetch_ != 3) pass_prefetch_ = 0;
 }
 

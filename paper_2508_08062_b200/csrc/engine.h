@@ -267,7 +267,7 @@ class Problem {
   int device_;
   int num_sms_ = 148;
   bool pdl_ = true;  // AAPDHG_PDL=0 disables programmatic dependent launch
-  int pass_prefetch_ = 0;  // AAPDHG_PASS_PREFETCH: later column passes fetch their partial early (2: L2, 3: register)
+  int pass_prefetch_ = 3;  // AAPDHG_PASS_PREFETCH: later column passes fetch their partial early (3: register, 2: L2, 0: off)
   cudaStream_t stream_ = nullptr;
   cudaStream_t own_stream_ = nullptr;
   cudaStream_t side_ = nullptr;  // SERIAL: x-side chains beside K2 (fork/join)

@@ -883,9 +883,11 @@ __device__ __forceinline__ void fused_control_tail(const IterBufs& B, DevState* 
 
 // One column pass of an L2-blocked SpMV: part[row] (+)= the row's products
 // with the columns of this block (passes in block order: deterministic).
-__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
-    k_spmv_pass(CsrDev A, VecRef xr, double* __restrict__ part, int first, const DevState* S,
-                int pred_aa, const int32_t* stop) {
+template <int U>
+__device__ __forceinline__ void spmv_pass_body(const CsrDev& A, const VecRef& xr,
+                                               double* __restrict__ part, int first,
+                                               const DevState* S, int pred_aa,
+                                               const int32_t* stop) {
   TL_MARK(20);
   if (skip_launch(S, 0, stop)) return;
   if (S && pred_aa == 1 && (!S->aa_attempt || !S->aa_ok)) return;  // (AA recache passes)
@@ -900,11 +902,18 @@ __global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
       if (first == 2) l2_prefetch(part + r);
       else if (first == 3) prev = __ldcs(part + r);
     };
-    const int row = row_sum<false, kUnroll, false, false, decltype(pre), true>(A, x, s, pre, -1, rep);
+    const int row = row_sum<false, U, false, false, decltype(pre), true>(A, x, s, pre, -1, rep);
     if (row == -2) break;
     if (row >= 0)
       __stcs(part + row, first == 1 ? s : __dadd_rn(first == 3 ? prev : __ldcs(part + row), s));
   }
+}
+
+
+__global__ void __launch_bounds__(kThreads, kSpmvBlocksPerSM)
+    k_spmv_pass(CsrDev A, VecRef xr, double* __restrict__ part, int first, const DevState* S,
+                int pred_aa, const int32_t* stop) {
+  spmv_pass_body<kUnroll>(A, xr, part, first, S, pred_aa, stop);
 }
 
 // ---------------------------------------------------------------------------
