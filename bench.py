@@ -569,8 +569,9 @@ def config1_leg(args, torch, dev, stream):
     # warm-up: graph instantiation and the persistent grid's first partition
     # calibration (engine.cu rebalance: a solve of >= 16 iterations)
     s.solve(solver_config(tau=tau, max_iters=max(args.warmup, 64)))
+    steps1 = getattr(args, "steps_cfg1", args.steps)
     hp, hout = pinned_problem(torch, p)
-    cfg = solver_config(tau=tau, max_iters=args.steps)
+    cfg = solver_config(tau=tau, max_iters=steps1)
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
@@ -605,7 +606,7 @@ def config1_leg(args, torch, dev, stream):
     ttt = None if args.no_ttt else time_to_tol(args, p, s)
     s.close()
     e2e_s, e2e_runs, out2 = time_e2e(lambda: Solver(hp, device=dev),
-                                     solver_config(tau=tau, max_iters=args.steps), hout, torch, dev)
+                                     solver_config(tau=tau, max_iters=steps1), hout, torch, dev)
     h2d = sum(a.nbytes for a in (p.k.row_ptr, p.k.col_idx, p.k.vals, p.c, p.q, p.l, p.u))
     d2h = (p.n() * 16 + p.k.nrows * 8) + out2.trajectory.nbytes
     cpu = None
@@ -735,7 +736,8 @@ def time_to_tol(args, p, s):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20000)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed iterations (default: 200 for configs[4], 20,000 for configs[1])")
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-iters", type=int, default=20)
@@ -759,12 +761,17 @@ def main():
         # bounded CPU sample: <= 500 iterations (~20 s of reference work at
         # ~40 ms per iteration); the driver's --steps 20 --warmup 5 run as given
         args.warmup = max(args.warmup, 0)
-        args.steps = min(args.steps, 500)
+        args.steps = min(args.steps if args.steps is not None else 500, 500)
         args.warmup = min(args.warmup, 50)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     select_workload(args, world)
+    # no --steps: a run that ends within minutes — configs[4] 200 iterations
+    # (~1.5 s timed, the e2e leg as many), the configs[1] leg its 20,000
+    args.steps_cfg1 = args.steps if args.steps is not None else 20000
+    if args.steps is None:
+        args.steps = 200 if CONFIG_ID == 4 else 20000
     if world > 1 and args.impl == "ours":
         import torch
         import torch.distributed as tdist
